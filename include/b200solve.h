@@ -1,0 +1,174 @@
+/*
+ * b200solve.h -- C ABI of libb200solve.so, the sm_100a kernels behind the
+ * drop-in replacement for the reference `blocksolve` ILU0-BiCGStab path.
+ *
+ * The reference (/root/reference/pkg/src/blocksolve, "bs/") is pure Python
+ * and has no FFI of its own; each entry point below replaces the body of the
+ * reference function cited beside it, and the Python layer
+ * (paper_2309_11488_b200/) keeps the reference's names, argument meaning and
+ * exceptions on top (binding: paper_2309_11488_b200/_lib.py, ctypes).
+ *
+ * Conventions
+ *   - every pointer is DEVICE memory unless its name ends in `_host`;
+ *   - indices are int32 (the reference uses int64, bs/blockcore.py:83-84),
+ *     values fp64, block vectors interleaved [row][b], blocks row-major;
+ *   - all work is ordered on the caller's `stream`; functions that must
+ *     report a data-dependent result (missing diagonal, singular pivot,
+ *     sizes) synchronise that stream before returning;
+ *   - the library keeps no global mutable state: independent solves may run
+ *     concurrently on different streams;
+ *   - return value: B2S_OK or one of the error codes below, which the Python
+ *     layer maps onto the reference's exceptions (bs/errors.py).
+ */
+#ifndef B200SOLVE_H
+#define B200SOLVE_H
+
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2S_OK 0
+#define B2S_SHAPE 1            /* -> ShapeError            (bs/errors.py:8-9)   */
+#define B2S_MISSING_DIAGONAL 2 /* -> MissingDiagonal(row)  (bs/errors.py:20-25) */
+#define B2S_SINGULAR_PIVOT 3   /* -> SingularPivot(row)    (bs/errors.py:28-33) */
+#define B2S_CUDA_ERROR 4       /* -> RuntimeError                              */
+#define B2S_UNSUPPORTED 5      /* block size outside 1..4                      */
+
+/* ---- analysis (bs/analysis.py) ------------------------------------------ */
+
+/* diagonal slot per row (-1 if absent); replaces SparsityPattern.
+ * diagonal_positions (bs/blockcore.py:127-134) and the missing-diagonal scans
+ * (bs/analysis.py:79-82, bs/ilu0.py:159-161): B2S_MISSING_DIAGONAL with the
+ * first such row in *first_missing_host. */
+int b2s_find_diagonal(int n, const int32_t* rp, const int32_t* ci, int32_t* diag_pos,
+                      int32_t* first_missing_host, cudaStream_t stream);
+
+/* level_schedule (bs/analysis.py:85-100): row_group[i] = level, bit-exact. */
+int b2s_level_schedule(int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,
+                       int32_t* ngroups_host, cudaStream_t stream);
+
+/* graph_color (bs/analysis.py:103-145): greedy first-fit colours, bit-exact. */
+int b2s_graph_color(int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,
+                    int32_t* ngroups_host, cudaStream_t stream);
+
+/* _plan_from_groups (bs/analysis.py:61-71): perm (old->new), iperm (new->old,
+ * stable), offsets (ngroups+1). */
+int b2s_plan_from_groups(int n, const int32_t* row_group, int ngroups, int32_t* perm,
+                         int32_t* iperm, int32_t* offsets, cudaStream_t stream);
+
+/* apply_permutation (bs/analysis.py:162-197): new row k = old row take[k],
+ * columns through cmap, re-sorted.  Forward: cmap = perm, take = iperm.
+ * out_src (optional) receives the source slot of every output block. */
+int b2s_permute_bsr(int n, int b, const int32_t* rp, const int32_t* ci, const double* vals,
+                    const int32_t* cmap, const int32_t* take, int32_t* out_rp, int32_t* out_ci,
+                    double* out_vals, int32_t* out_src, cudaStream_t stream);
+
+/* apply_permutation_vec (bs/analysis.py:153-159): out[i] = in[src[i]]. */
+int b2s_gather_rows(int n, int b, const int32_t* src, const double* in, double* out,
+                    cudaStream_t stream);
+
+/* block gather out[q] = in[src[q]] (refresh_values, bs/jacobi.py:139-147). */
+int b2s_gather_blocks(long long nblk, int b, const int32_t* src, const double* in, double* out,
+                      cudaStream_t stream);
+
+/* ---- SELL-32 device layouts (no reference counterpart: the device form of
+ *      the BLOCK_ROW_MAJOR values, bs/blockcore.py:26-44, and of the
+ *      per-sweep _Phase packing, bs/ilu0.py:204-236) ----------------------- */
+
+int b2s_slices_plain(int n, int32_t* row0, int32_t* nrows, cudaStream_t stream);
+int b2s_slices_grouped_count(int ngroups, const int32_t* offsets, int32_t* base,
+                             int32_t* nslices_host, cudaStream_t stream);
+int b2s_slices_grouped_fill(int ngroups, int nslices, const int32_t* offsets,
+                            const int32_t* base, int32_t* row0, int32_t* nrows,
+                            cudaStream_t stream);
+/* sel: 0 = all blocks, 1 = strict lower, 2 = strict upper */
+int b2s_sell_offsets(int nslices, const int32_t* row0, const int32_t* nrows, const int32_t* rp,
+                     const int32_t* ci, int sel, int32_t* sp, long long* slots_host,
+                     cudaStream_t stream);
+int b2s_sell_fill(int nslices, int b, const int32_t* row0, const int32_t* nrows,
+                  const int32_t* rp, const int32_t* ci, const double* vals, int sel,
+                  const int32_t* sp, int32_t* cols, double* svals, cudaStream_t stream);
+int b2s_diag_tiles(int nslices, int b, const int32_t* row0, const int32_t* nrows,
+                   const double* inv, double* tiles, cudaStream_t stream);
+int b2s_slice_conflicts(int nslices, const int32_t* row0, const int32_t* nrows,
+                        const int32_t* rp, const int32_t* ci, int* conflict_host,
+                        cudaStream_t stream);
+
+/* ---- SpMV (bs/blockcore.py:342-376 spmv_array / residual) --------------- */
+
+/* mode 0: y = A x; 1: + partials w.y; 2: + partials y.y and y.w;
+ * 3: y = w - A x (residual) + partials y.y.  One partial per CTA (nparts). */
+int b2s_spmv(int b, int mode, int nparts, int nslices, const int32_t* row0,
+             const int32_t* nrows, const int32_t* sp, const int32_t* cols, const double* vals,
+             const double* x, double* y, const double* w, double* part0, double* part1,
+             const int* done, cudaStream_t stream);
+
+/* ---- ILU0 (bs/ilu0.py) --------------------------------------------------- */
+
+/* decompose (bs/ilu0.py:145-201) on an already permuted matrix, in place;
+ * B2S_SINGULAR_PIVOT with the smallest failing permuted row. */
+int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_t* nrows,
+                    const int32_t* rp, const int32_t* ci, const int32_t* diag, double* vals,
+                    double* inv_diag, int32_t* bad_row_host, cudaStream_t stream);
+
+/* Ilu0Factorization.apply_permuted_array (bs/ilu0.py:105-142). */
+int b2s_ilu0_apply(int n, int b, int kc, int nslices, const int32_t* row0, const int32_t* nrows,
+                   const int32_t* l_sp, const int32_t* l_cols, const double* l_vals,
+                   const int32_t* u_sp, const int32_t* u_cols, const double* u_vals,
+                   const double* dinv_tiles, const double* r, double* y, double* z, int reset_y,
+                   void* tickets, cudaStream_t stream);
+int b2s_fill_sentinel(long long m, double* v, cudaStream_t stream);
+
+/* ---- reductions (bs/krylov.py:30-60) ------------------------------------ */
+
+int b2s_dot(long long m, const double* a, const double* b, int nparts, double* parts,
+            double* out, cudaStream_t stream);
+int b2s_all_finite(long long m, const double* a, int* bad, cudaStream_t stream);
+
+/* ---- BiCGStab (bs/krylov.py:140-244) ------------------------------------ */
+
+typedef struct {
+  int n, b, nparts, precond /* 0 none, 1 ilu0 */, kc, maxit, check_lag;
+  double tol;
+  int nslices;
+  const int32_t *row0, *nrows;
+  const int32_t *a_sp, *a_cols;
+  const double* a_vals;
+  const int32_t *l_sp, *l_cols;
+  const double* l_vals;
+  const int32_t *u_sp, *u_cols;
+  const double* u_vals;
+  const double* dinv_tiles;
+  const double* rhs;
+  double* x;    /* x0 on entry, solution on exit */
+  double* work; /* b2s_bicgstab_workspace_bytes() */
+  cudaStream_t stream;
+} b2s_bicg_args;
+
+typedef struct {
+  int converged, reason /* 1 converged 2 breakdown 3 numerical 4 budget */;
+  int graph_launches, kernels_per_iteration;
+  double iterations, initial_norm, final_norm;
+} b2s_bicg_result;
+
+long long b2s_bicgstab_workspace_bytes(int n, int b, int nparts);
+int b2s_bicgstab(const b2s_bicg_args* args, b2s_bicg_result* result);
+
+/* ---- Block-Jacobi copy plan (bs/jacobi.py:111-147) ---------------------- */
+
+int b2s_jacobi_pattern(int n, const int32_t* rp, const int32_t* ci, const int32_t* part,
+                       int32_t* new_rp, int32_t* kept_host, cudaStream_t stream);
+int b2s_jacobi_fill(int n, const int32_t* rp, const int32_t* ci, const int32_t* part,
+                    const int32_t* new_rp, int32_t* new_ci, int32_t* indices,
+                    cudaStream_t stream);
+
+/* ---- library identity --------------------------------------------------- */
+const char* b2s_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200SOLVE_H */

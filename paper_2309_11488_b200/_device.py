@@ -1,0 +1,251 @@
+"""Device mirrors of the reference's data types and the thin engine layer.
+
+Host objects (``BlockMatrix``/``BlockVector``/``ParallelPlan``) keep the
+reference's numpy-facing API; everything numeric happens on the GPU through
+libb200solve.so.  Device buffers are torch CUDA tensors owned by Python (the
+C side only receives pointers, sizes and the current stream).
+
+Layout in HBM:
+  * pattern: int32 row pointers (n+1) and column indices (nnzb);
+  * values: fp64 canonical block-row-major (nnzb*b*b);
+  * block vectors: fp64 interleaved [row][b];
+  * SELL-32 tiles built once per matrix for the bandwidth-bound kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+
+NPARTS = 148 * 4   # CTAs of every reducing kernel: fixed => deterministic sums
+
+_I32_MAX = 2 ** 31 - 1
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2309_11488_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def lib():
+    return _lib.load()
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def i32(a: np.ndarray, dev) -> torch.Tensor:
+    a = np.asarray(a)
+    if a.size and (a.max() > _I32_MAX or a.min() < -_I32_MAX):
+        raise ValueError("index does not fit the device's int32 indices")
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev, non_blocking=False)
+
+
+def f64(a: np.ndarray, dev) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+
+def empty_i32(n, dev):
+    return torch.empty(max(int(n), 1), dtype=torch.int32, device=dev)
+
+
+def empty_f64(n, dev):
+    return torch.empty(max(int(n), 1), dtype=torch.float64, device=dev)
+
+
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DevPattern:
+    n: int
+    nnz: int
+    rp: torch.Tensor
+    ci: torch.Tensor
+
+    @classmethod
+    def upload(cls, pattern) -> "DevPattern":
+        dev = require_cuda()
+        n = int(pattern.num_block_rows)
+        rp = np.asarray(pattern.row_pointers)
+        ci = np.asarray(pattern.column_indices)
+        return cls(n, int(rp[-1]) if n else 0, i32(rp, dev), i32(ci, dev) if ci.size
+                   else empty_i32(1, dev))
+
+    def host(self):
+        rp = self.rp[: self.n + 1].cpu().numpy().astype(np.int64)
+        ci = self.ci[: self.nnz].cpu().numpy().astype(np.int64)
+        return rp, ci
+
+
+@dataclass
+class DevBSR:
+    pat: DevPattern
+    b: int
+    vals: torch.Tensor
+
+    @classmethod
+    def upload(cls, m) -> "DevBSR":
+        m = m.as_block_row_major()
+        pat = DevPattern.upload(m.pattern)
+        vals = f64(m.values, pat.rp.device) if m.values.size else empty_f64(1, pat.rp.device)
+        return cls(pat, int(m.block_size), vals)
+
+
+def find_diagonal(p: DevPattern) -> torch.Tensor:
+    diag = empty_i32(p.n, p.rp.device)
+    bad = C.c_int32(-1)
+    rc = lib().b2s_find_diagonal(p.n, ptr(p.rp), ptr(p.ci), ptr(diag), C.byref(bad), stream())
+    check(rc, "find_diagonal", bad.value)
+    return diag
+
+
+def groups(p: DevPattern, kind: str):
+    """Device level schedule / colouring; returns (row_group int32, ngroups)."""
+    g = empty_i32(p.n, p.rp.device)
+    ng = C.c_int32(0)
+    fn = lib().b2s_level_schedule if kind == "level" else lib().b2s_graph_color
+    # MissingDiagonal first, exactly like bs/analysis.py:79-82
+    find_diagonal(p)
+    check(fn(p.n, ptr(p.rp), ptr(p.ci), ptr(g), C.byref(ng), stream()), kind)
+    return g, int(ng.value)
+
+
+def plan_arrays(row_group: torch.Tensor, n: int, ngroups: int):
+    dev = row_group.device
+    perm = empty_i32(n, dev)
+    iperm = empty_i32(n, dev)
+    off = empty_i32(ngroups + 1, dev)
+    check(lib().b2s_plan_from_groups(n, ptr(row_group), ngroups, ptr(perm), ptr(iperm),
+                                     ptr(off), stream()), "plan_from_groups")
+    return perm, iperm, off
+
+
+def permute(m: DevBSR, cmap: torch.Tensor, take: torch.Tensor, want_src=False):
+    p = m.pat
+    dev = p.rp.device
+    rp = empty_i32(p.n + 1, dev)
+    ci = empty_i32(p.nnz, dev)
+    bb = m.b * m.b
+    vals = empty_f64(p.nnz * bb, dev)
+    src = empty_i32(p.nnz, dev) if want_src else None
+    check(lib().b2s_permute_bsr(p.n, m.b, ptr(p.rp), ptr(p.ci), ptr(m.vals), ptr(cmap),
+                                ptr(take), ptr(rp), ptr(ci), ptr(vals), ptr(src), stream()),
+          "permute_bsr")
+    out = DevBSR(DevPattern(p.n, p.nnz, rp, ci), m.b, vals)
+    return (out, src) if want_src else out
+
+
+def gather_rows(v: torch.Tensor, src: torch.Tensor, n: int, b: int) -> torch.Tensor:
+    out = torch.empty(n * b, dtype=torch.float64, device=v.device)
+    check(lib().b2s_gather_rows(n, b, ptr(src), ptr(v), ptr(out), stream()), "gather_rows")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# slice maps and SELL-32 layouts
+
+@dataclass
+class SliceMap:
+    nslices: int
+    row0: torch.Tensor
+    nrows: torch.Tensor
+
+    @classmethod
+    def plain(cls, n: int, dev) -> "SliceMap":
+        ns = (n + 31) // 32
+        row0, nrows = empty_i32(ns, dev), empty_i32(ns, dev)
+        check(lib().b2s_slices_plain(n, ptr(row0), ptr(nrows), stream()), "slices_plain")
+        return cls(ns, row0, nrows)
+
+    @classmethod
+    def grouped(cls, offsets: torch.Tensor, ngroups: int) -> "SliceMap":
+        dev = offsets.device
+        base = empty_i32(ngroups + 1, dev)
+        ns = C.c_int32(0)
+        check(lib().b2s_slices_grouped_count(ngroups, ptr(offsets), ptr(base), C.byref(ns),
+                                             stream()), "slices_grouped")
+        row0, nrows = empty_i32(ns.value, dev), empty_i32(ns.value, dev)
+        check(lib().b2s_slices_grouped_fill(ngroups, ns.value, ptr(offsets), ptr(base),
+                                            ptr(row0), ptr(nrows), stream()), "slices_grouped")
+        return cls(int(ns.value), row0, nrows)
+
+    @classmethod
+    def singles(cls, n: int, dev) -> "SliceMap":
+        """One row per slice: always safe for the triangular sweeps."""
+        row0 = torch.arange(max(n, 1), dtype=torch.int32, device=dev)
+        nrows = torch.ones(max(n, 1), dtype=torch.int32, device=dev)
+        return cls(n, row0, nrows)
+
+    def conflicts(self, p: DevPattern) -> bool:
+        c = C.c_int(0)
+        check(lib().b2s_slice_conflicts(self.nslices, ptr(self.row0), ptr(self.nrows),
+                                        ptr(p.rp), ptr(p.ci), C.byref(c), stream()),
+              "slice_conflicts")
+        return bool(c.value)
+
+
+@dataclass
+class Sell:
+    sp: torch.Tensor
+    cols: torch.Tensor
+    vals: torch.Tensor
+    slots: int
+    width: int   # widest slice (entries)
+
+    @classmethod
+    def build(cls, smap: SliceMap, m: DevBSR, sel: int) -> "Sell":
+        dev = m.pat.rp.device
+        sp = empty_i32(smap.nslices + 1, dev)
+        slots = C.c_longlong(0)
+        check(lib().b2s_sell_offsets(smap.nslices, ptr(smap.row0), ptr(smap.nrows),
+                                     ptr(m.pat.rp), ptr(m.pat.ci), sel, ptr(sp),
+                                     C.byref(slots), stream()), "sell_offsets")
+        ns = int(slots.value)
+        if ns * m.b * m.b > _I32_MAX * 8:
+            raise ValueError("matrix too large for one device layout")
+        cols = empty_i32(ns, dev)
+        vals = empty_f64(ns * m.b * m.b, dev)
+        check(lib().b2s_sell_fill(smap.nslices, m.b, ptr(smap.row0), ptr(smap.nrows),
+                                  ptr(m.pat.rp), ptr(m.pat.ci), ptr(m.vals), sel, ptr(sp),
+                                  ptr(cols), ptr(vals), stream()), "sell_fill")
+        width = 0
+        if smap.nslices:
+            width = int(((sp[1:smap.nslices + 1] - sp[:smap.nslices]).max().item()) // 32)
+        return cls(sp, cols, vals, ns, width)
+
+
+def spmv(smap: SliceMap, a: Sell, b: int, x: torch.Tensor, y: torch.Tensor, mode: int = 0,
+         w: torch.Tensor | None = None, parts0=None, parts1=None):
+    check(lib().b2s_spmv(b, mode, NPARTS, smap.nslices, ptr(smap.row0), ptr(smap.nrows),
+                         ptr(a.sp), ptr(a.cols), ptr(a.vals), ptr(x), ptr(y), ptr(w),
+                         ptr(parts0), ptr(parts1), None, stream()), "spmv")
+
+
+def dot(a: torch.Tensor, b: torch.Tensor, m: int) -> float:
+    dev = a.device
+    parts = torch.empty(NPARTS, dtype=torch.float64, device=dev)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    check(lib().b2s_dot(m, ptr(a), ptr(b), NPARTS, ptr(parts), ptr(out), stream()), "dot")
+    return float(out.item())
+
+
+def fill_sentinel(v: torch.Tensor, m: int):
+    check(lib().b2s_fill_sentinel(m, ptr(v), stream()), "fill_sentinel")
+
+
+def all_finite(v: torch.Tensor, m: int) -> bool:
+    bad = torch.zeros(1, dtype=torch.int32, device=v.device)
+    check(lib().b2s_all_finite(m, ptr(v), ptr(bad), stream()), "all_finite")
+    return not bool(bad.item())

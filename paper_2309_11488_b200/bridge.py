@@ -1,0 +1,213 @@
+"""Backend registry, solve orchestration and the sequential fallback
+(drop-in for bs/bridge.py).
+
+``solve_with_fallback`` keeps the reference's contract: build the operator,
+optionally Jacobi-relax the preconditioner matrix, extract parallelism per
+backend, factor, run BiCGStab, and on failure (not converged or singular
+pivot) rerun with the sequential ILU0 of the full matrix and at least the
+default budget; raise ``SolveFailed`` when that fails too.
+
+B200 specifics: the matrix crosses to the GPU once per call; analysis,
+permutation, factorisation, the Krylov loop and the fallback all run on it,
+and only the solution vector comes back.  :class:`DeviceSolver` exposes the
+same pipeline for device-resident inputs (benchmarks, repeated solves).
+"""
+
+from __future__ import annotations
+
+import enum
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as D
+from .analysis import (ParallelPlan, Strategy, _device_plan, sequential_plan)
+from .blockcore import BlockMatrix, BlockVector
+from .errors import SingularPivot, SolveFailed
+from .ilu0 import Ilu0Factorization, factor_device
+from .krylov import (DEFAULT_MAX_ITERATIONS, DeviceKrylov, SolveReport, StoppingCriteria,
+                     _REASONS)
+
+
+class Backend(enum.Enum):
+    """Same members as bs/bridge.py:26-37 (tests iterate over the enum and
+    reject unknown names such as "gpu"); every member runs on the B200."""
+
+    REFERENCE_SEQUENTIAL = "reference"
+    LEVEL_SCHEDULED = "level"
+    GRAPH_COLORED = "color"
+
+    @classmethod
+    def from_name(cls, name: str) -> "Backend":
+        for member in cls:
+            if member.value == name:
+                return member
+        raise ValueError(f"unknown backend {name!r}; choose from {[m.value for m in cls]}")
+
+
+class WellMode(enum.Enum):
+    COUPLED = "coupled"
+    SEPARATE = "separate"
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """bs/bridge.py:40-55."""
+
+    backend: Backend = Backend.LEVEL_SCHEDULED
+    jacobi_partitions: int = 0
+    well_mode: WellMode = WellMode.SEPARATE
+    stop: StoppingCriteria = field(default_factory=StoppingCriteria)
+
+    def __post_init__(self):
+        if self.jacobi_partitions < 0:
+            raise ValueError("jacobi_partitions must be >= 0")
+
+
+def plan_device(backend: Backend, pat: "D.DevPattern") -> ParallelPlan:
+    """_plan_for (bs/bridge.py:58-63) on an uploaded pattern."""
+    if backend is Backend.LEVEL_SCHEDULED:
+        g, ng = D.groups(pat, "level")
+        return _device_plan(Strategy.LEVEL_SCHEDULING, g, pat.n, ng)
+    if backend is Backend.GRAPH_COLORED:
+        g, ng = D.groups(pat, "color")
+        return _device_plan(Strategy.GRAPH_COLORING, g, pat.n, ng)
+    return sequential_plan(pat.n)
+
+
+def _failed_report(reason: str) -> SolveReport:
+    return SolveReport(False, 0.0, float("nan"), float("nan"), 0.0, 0, failure_reason=reason)
+
+
+class DeviceSolver:
+    """The whole reference pipeline on device-resident data.
+
+    ``setup()`` = analysis + permutation + factorisation + operator layout;
+    ``solve(rhs, x)`` = BiCGStab on plan-ordered device vectors.  Inputs and
+    outputs are torch CUDA tensors in the matrix's own row order.
+    """
+
+    def __init__(self, a: BlockMatrix, bsr: "D.DevBSR", cfg: SolverConfig,
+                 precond_bsr: "D.DevBSR" = None, precond_matrix: BlockMatrix = None):
+        self.a = a
+        self.bsr = bsr
+        self.cfg = cfg
+        self.pre_bsr = precond_bsr or bsr
+        self.pre_matrix = precond_matrix or a
+        self.fact: Ilu0Factorization | None = None
+        self.krylov: DeviceKrylov | None = None
+        self.plan: ParallelPlan | None = None
+
+    def setup(self, backend: Backend | None = None):
+        backend = backend or self.cfg.backend
+        self.plan = plan_device(backend, self.pre_bsr.pat)
+        self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr)
+        a_perm = self.fact._a_perm if self.pre_bsr is self.bsr else None
+        if a_perm is None:
+            from .analysis import permute_device
+            a_perm = (self.bsr if self.fact._identity_perm
+                      else permute_device(self.bsr, self.plan))
+        self.krylov = DeviceKrylov.build(self.a, self.fact, a_perm)
+        return self
+
+    def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria):
+        """x (input order) holds x0 on entry and the solution on exit."""
+        n, b = self.krylov.n, self.krylov.b
+        f = self.fact
+        if f._identity_perm:
+            return self.krylov.solve(rhs, x, stop)
+        iperm = f.plan.device("inverse_permutation")
+        bp = D.gather_rows(rhs, iperm, n, b)
+        xp = D.gather_rows(x, iperm, n, b)
+        res = self.krylov.solve(bp, xp, stop)
+        x.copy_(D.gather_rows(xp, f.plan.device("permutation"), n, b)[: n * b])
+        return res
+
+
+def _report(res, elapsed, groups) -> SolveReport:
+    return SolveReport(bool(res.converged), float(res.iterations), float(res.initial_norm),
+                       float(res.final_norm), elapsed, groups,
+                       failure_reason=None if res.converged else _REASONS.get(res.reason, "budget"),
+                       gpu_launches=int(res.graph_launches) * int(res.kernels_per_iteration))
+
+
+def _sync():
+    torch.cuda.current_stream().synchronize()
+
+
+def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells=None,
+                        x0: BlockVector | None = None) -> tuple[BlockVector, SolveReport]:
+    """Configured backend first, sequential ILU0 fallback second
+    (bs/bridge.py:71-136)."""
+    from .errors import ShapeError
+    if wells is not None and not getattr(wells, "is_empty", True):
+        raise NotImplementedError("wells are not on this build's device path (SURVEY §8(f))")
+    t0 = time.perf_counter()
+    a_sys = a.as_block_row_major()
+    n, bs = a_sys.num_block_rows, a_sys.block_size
+    if b.block_size != bs or b.num_blocks != n:
+        raise ShapeError("right-hand side does not match the operator")
+    if x0 is None:
+        x0 = BlockVector.zeros(n, bs)
+    elif x0.block_size != bs or x0.num_blocks != n:
+        raise ShapeError("initial guess does not match the right-hand side")
+    if n == 0:
+        rep = SolveReport(True, 0.0, 0.0, 0.0, 0.0, 0)
+        return BlockVector(x0.data.copy(), bs), rep
+    dev = D.require_cuda()
+    bsr = D.DevBSR.upload(a_sys)
+    rhs = D.f64(b.data, dev)
+    x0d = D.f64(x0.data, dev)
+
+    pre_bsr, pre_mat = bsr, a_sys
+    primary = None
+    x = None
+    try:
+        if cfg.jacobi_partitions > 0:
+            from .jacobi import drop_cross_blocks, partition, transmissibility_weights
+            parts = partition(a_sys.pattern, transmissibility_weights(a_sys),
+                              cfg.jacobi_partitions)
+            pre_mat, _ = drop_cross_blocks(a_sys, parts)
+            pre_bsr = D.DevBSR.upload(pre_mat)
+        solver = DeviceSolver(a_sys, bsr, cfg, pre_bsr, pre_mat).setup()
+        _sync()
+        setup = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        xd = x0d.clone()
+        res = solver.solve(rhs, xd, cfg.stop)
+        _sync()
+        primary = _report(res, time.perf_counter() - t1, solver.plan.group_count)
+        primary.setup_elapsed = setup
+        x = xd
+    except SingularPivot as exc:
+        primary = _failed_report(f"singular pivot in row {exc.row}")
+        primary.setup_elapsed = time.perf_counter() - t0
+
+    if primary.converged:
+        return BlockVector(x[: n * bs].cpu().numpy(), bs), primary
+
+    fb_t0 = time.perf_counter()
+    fb_stop = StoppingCriteria(cfg.stop.relative_reduction,
+                               max(cfg.stop.max_iterations, DEFAULT_MAX_ITERATIONS))
+    fcfg = SolverConfig(Backend.REFERENCE_SEQUENTIAL, 0, cfg.well_mode, fb_stop)
+    try:
+        fb = DeviceSolver(a_sys, bsr, fcfg).setup()
+    except SingularPivot as exc:
+        fb_report = _failed_report(f"singular pivot in row {exc.row}")
+        fb_report.fallback_used = True
+        raise SolveFailed(primary, fb_report)
+    _sync()
+    fb_setup = time.perf_counter() - fb_t0
+    t2 = time.perf_counter()
+    xd = x0d.clone()
+    res = fb.solve(rhs, xd, fb_stop)
+    _sync()
+    report = _report(res, time.perf_counter() - t2, n)
+    report.fallback_used = True
+    report.setup_elapsed = primary.setup_elapsed + fb_setup
+    report.elapsed += primary.elapsed
+    if not report.converged:
+        raise SolveFailed(primary, report)
+    return BlockVector(xd[: n * bs].cpu().numpy(), bs), report

@@ -1,0 +1,440 @@
+// Device-side parallelism extraction: diagonal lookup, level schedule, greedy
+// colouring, plan construction (stable counting order) and the symmetric
+// block-CSR permutation.  Integer results are bit-exact against the
+// reference (bs/analysis.py); see DESIGN.md §3.
+//
+// Level schedule and colouring are both "sync-free wavefronts": rows are
+// handed out to warps in ascending index order through an atomic ticket, and
+// each row spins until the rows it depends on (all with smaller index) have
+// published their value.  Because tickets are issued in order to resident
+// warps, the smallest unfinished row always has all its inputs: no deadlock,
+// no grid barrier, and the critical path is the DAG depth (one L2 round
+// trip per level) instead of one kernel launch per level.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace b2s {
+
+// ---------------------------------------------------------------------------
+// diagonal positions (bs/blockcore.py:127-134) + first missing row
+// (bs/analysis.py:79-82, bs/ilu0.py:159-161)
+__global__ void k_find_diag(int n, const int32_t* __restrict__ rp,
+                            const int32_t* __restrict__ ci, int32_t* __restrict__ diag,
+                            int32_t* __restrict__ first_missing) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int lo = rp[i], hi = rp[i + 1] - 1, pos = -1;
+    while (lo <= hi) {  // columns are strictly increasing per row
+      int mid = (lo + hi) >> 1;
+      int c = ci[mid];
+      if (c == i) { pos = mid; break; }
+      if (c < i) lo = mid + 1; else hi = mid - 1;
+    }
+    diag[i] = pos;
+    if (pos < 0) atomicMin(first_missing, i);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// level(i) = 1 + max level(j) over strict-lower j, 0 without lower
+// neighbours (bs/analysis.py:85-100).  level[] must be -1 on entry.
+__global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
+                                  const int32_t* __restrict__ ci, int32_t* level,
+                                  unsigned int* ticket) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned int s = 0;
+    if (lane == 0) s = atomicAdd(ticket, 1u);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    const long long row0 = (long long)s * kSlice;
+    if (row0 >= n) break;
+    const int i = (int)row0 + lane;
+    bool done = i >= n;
+    int k = done ? 0 : rp[i];
+    const int end = done ? 0 : rp[i + 1];
+    int best = -1;
+    for (;;) {
+      if (!done) {
+        while (k < end) {
+          const int j = ci[k];
+          if (j >= i) { k = end; break; }
+          const int lj = ld_volatile(level + j);
+          if (lj < 0) break;  // not yet published
+          best = max(best, lj);
+          ++k;
+        }
+        if (k >= end) {
+          st_volatile(level + i, best + 1);
+          done = true;
+        }
+      }
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Greedy first-fit colouring in ascending row order over the symmetrised
+// adjacency (bs/analysis.py:103-145): colour(i) = mex of the colours of the
+// neighbours j < i, where j is a neighbour if (i,j) or (j,i) is stored.
+// The (j,i) half comes from `ut_ptr/ut_idx`: for every column c, the rows
+// j < c that store (j, c).  colour[] must be -1 on entry.
+__global__ void k_color_sync_free(int n, const int32_t* __restrict__ rp,
+                                  const int32_t* __restrict__ ci,
+                                  const int32_t* __restrict__ ut_ptr,
+                                  const int32_t* __restrict__ ut_idx, int32_t* color,
+                                  unsigned int* ticket) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned int s = 0;
+    if (lane == 0) s = atomicAdd(ticket, 1u);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    const long long row0 = (long long)s * kSlice;
+    if (row0 >= n) break;
+    const int i = (int)row0 + lane;
+    bool done = i >= n;
+    // phase 0 walks the row's own strict-lower columns, phase 1 the
+    // transposed list; both only ever wait on rows j < i
+    int k = done ? 0 : rp[i];
+    int end = done ? 0 : rp[i + 1];
+    int phase = 0;
+    unsigned long long used = 0ull;  // colours 0..63 seen
+    bool big = false;                 // some neighbour has colour >= 64
+    for (;;) {
+      if (!done) {
+        for (;;) {
+          if (k >= end) {
+            if (phase == 0) { phase = 1; k = ut_ptr[i]; end = ut_ptr[i + 1]; continue; }
+            break;
+          }
+          const int j = (phase == 0) ? ci[k] : ut_idx[k];
+          if (phase == 0 && j >= i) { k = end; continue; }
+          const int cj = ld_volatile(color + j);
+          if (cj < 0) break;
+          if (cj < 64) used |= 1ull << cj; else big = true;
+          ++k;
+        }
+        if (phase == 1 && k >= end) {
+          int c = __ffsll((long long)~used) - 1;  // mex below 64
+          if (used == ~0ull) c = 64;
+          if (big && c >= 64) {
+            // rare: >= 64 distinct neighbour colours; walk the set directly
+            for (bool hit = true; hit;) {
+              hit = false;
+              for (int q = rp[i]; q < rp[i + 1] && !hit; ++q) {
+                const int j = ci[q];
+                if (j < i && ld_volatile(color + j) == c) hit = true;
+              }
+              for (int q = ut_ptr[i]; q < ut_ptr[i + 1] && !hit; ++q)
+                if (ld_volatile(color + ut_idx[q]) == c) hit = true;
+              if (hit) ++c;
+            }
+          }
+          st_volatile(color + i, c);
+          done = true;
+        }
+      }
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+  }
+}
+
+// transpose of the strict-upper part: for every stored (j, c) with c > j,
+// record j in the list of c.  Order inside a list is irrelevant (mex).
+__global__ void k_upper_count(int n, const int32_t* __restrict__ rp,
+                              const int32_t* __restrict__ ci, int32_t* cnt) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    for (int q = rp[j]; q < rp[j + 1]; ++q) {
+      const int c = ci[q];
+      if (c > j) atomicAdd(cnt + c, 1);
+    }
+}
+__global__ void k_upper_fill(int n, const int32_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, const int32_t* __restrict__ ptr,
+                             int32_t* fillpos, int32_t* idx) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    for (int q = rp[j]; q < rp[j + 1]; ++q) {
+      const int c = ci[q];
+      if (c > j) idx[ptr[c] + atomicAdd(fillpos + c, 1)] = j;
+    }
+}
+
+__global__ void k_fill_int(int n, int32_t* p, int v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
+__global__ void k_iota(int n, int32_t* p) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+__global__ void k_max_reduce(int n, const int32_t* __restrict__ v, int32_t* out) {
+  int m = -1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    m = max(m, v[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+__global__ void k_histogram(int n, const int32_t* __restrict__ g, int32_t* cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(cnt + g[i], 1);
+}
+// perm[iperm[k]] = k  (bs/analysis.py:64-65)
+__global__ void k_invert_perm(int n, const int32_t* __restrict__ iperm, int32_t* perm) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    perm[iperm[k]] = k;
+}
+
+// ---------------------------------------------------------------------------
+// symmetric permutation (bs/analysis.py:162-197): new row k is old row
+// take[k]; columns are mapped through cmap and re-sorted ascending.  The
+// per-row sort is an insertion sort on (new column, source slot) pairs held
+// in the output arrays (rows are short: 7 for the stencil).
+__global__ void k_permute_count(int n, const int32_t* __restrict__ rp,
+                                const int32_t* __restrict__ take, int32_t* cnt) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int o = take[k];
+    cnt[k] = rp[o + 1] - rp[o];
+  }
+}
+__global__ void k_permute_cols(int n, const int32_t* __restrict__ rp,
+                               const int32_t* __restrict__ ci,
+                               const int32_t* __restrict__ take,
+                               const int32_t* __restrict__ cmap,
+                               const int32_t* __restrict__ nrp, int32_t* nci, int32_t* src) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int o = take[k];
+    const int s = rp[o], len = rp[o + 1] - s, d = nrp[k];
+    for (int t = 0; t < len; ++t) {
+      const int c = cmap[ci[s + t]];
+      int u = t;
+      while (u > 0 && nci[d + u - 1] > c) {
+        nci[d + u] = nci[d + u - 1];
+        src[d + u] = src[d + u - 1];
+        --u;
+      }
+      nci[d + u] = c;
+      src[d + u] = s + t;
+    }
+  }
+}
+// out block q = in block src[q]  (bb doubles per block)
+__global__ void k_gather_blocks(long long nblk, int bb, const int32_t* __restrict__ src,
+                                const double* __restrict__ in, double* __restrict__ out) {
+  const long long total = nblk * bb;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long q = t / bb;
+    const int e = (int)(t - q * bb);
+    out[t] = in[(long long)src[q] * bb + e];
+  }
+}
+// vector rows: out[i] = in[src[i]]  (bs/analysis.py:153-159)
+__global__ void k_gather_rows(int n, int b, const int32_t* __restrict__ src,
+                              const double* __restrict__ in, double* __restrict__ out) {
+  const long long total = (long long)n * b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / b;
+    const int c = (int)(t - i * b);
+    out[t] = in[(long long)src[i] * b + c];
+  }
+}
+
+inline int grid_for(long long work, int threads = 256) {
+  long long g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > kSms * 32) g = kSms * 32;
+  return (int)g;
+}
+
+// persistent sync-free grids: enough resident warps to cover many levels
+inline int sync_free_grid(int n) {
+  long long slices = ((long long)n + kSlice - 1) / kSlice;
+  long long ctas = (slices + 7) / 8;  // 8 warps per CTA
+  long long cap = (long long)kSms * 8;
+  return (int)(ctas < 1 ? 1 : (ctas > cap ? cap : ctas));
+}
+
+}  // namespace b2s
+
+using namespace b2s;
+
+extern "C" {
+
+int b2s_find_diagonal(int n, const int32_t* rp, const int32_t* ci, int32_t* diag_pos,
+                      int32_t* first_missing_host, cudaStream_t st) {
+  if (n < 0) return B2S_SHAPE;
+  *first_missing_host = -1;
+  if (n == 0) return B2S_OK;
+  int32_t* d_first = nullptr;
+  B2S_CHECK(cudaMallocAsync(&d_first, sizeof(int32_t), st));
+  const int32_t big = 0x7fffffff;
+  B2S_CHECK(cudaMemcpyAsync(d_first, &big, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  k_find_diag<<<grid_for(n), 256, 0, st>>>(n, rp, ci, diag_pos, d_first);
+  B2S_LAUNCH_CHECK();
+  int32_t h = big;
+  B2S_CHECK(cudaMemcpyAsync(&h, d_first, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(d_first, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  if (h != big) { *first_missing_host = h; return B2S_MISSING_DIAGONAL; }
+  return B2S_OK;
+}
+
+// Shared tail of level_schedule / graph_color: number of groups.
+static int finish_groups(int n, const int32_t* groups, int32_t* ngroups_host, cudaStream_t st) {
+  int32_t* d_max = nullptr;
+  B2S_CHECK(cudaMallocAsync(&d_max, sizeof(int32_t), st));
+  B2S_CHECK(cudaMemsetAsync(d_max, 0xff, sizeof(int32_t), st));  // -1
+  k_max_reduce<<<grid_for(n), 256, 0, st>>>(n, groups, d_max);
+  B2S_LAUNCH_CHECK();
+  int32_t h = -1;
+  B2S_CHECK(cudaMemcpyAsync(&h, d_max, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(d_max, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  *ngroups_host = h + 1;
+  return B2S_OK;
+}
+
+int b2s_level_schedule(int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,
+                       int32_t* ngroups_host, cudaStream_t st) {
+  *ngroups_host = 0;
+  if (n <= 0) return n < 0 ? B2S_SHAPE : B2S_OK;
+  unsigned int* ticket = nullptr;
+  B2S_CHECK(cudaMallocAsync(&ticket, sizeof(unsigned int), st));
+  B2S_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+  k_fill_int<<<grid_for(n), 256, 0, st>>>(n, row_group, -1);
+  k_level_sync_free<<<sync_free_grid(n), 256, 0, st>>>(n, rp, ci, row_group, ticket);
+  B2S_LAUNCH_CHECK();
+  B2S_CHECK(cudaFreeAsync(ticket, st));
+  return finish_groups(n, row_group, ngroups_host, st);
+}
+
+int b2s_graph_color(int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,
+                    int32_t* ngroups_host, cudaStream_t st) {
+  *ngroups_host = 0;
+  if (n <= 0) return n < 0 ? B2S_SHAPE : B2S_OK;
+  int32_t *cnt = nullptr, *ptr = nullptr, *fill = nullptr, *idx = nullptr;
+  unsigned int* ticket = nullptr;
+  int32_t nnz = 0;
+  B2S_CHECK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (n + 1), st));
+  B2S_CHECK(cudaMallocAsync(&ptr, sizeof(int32_t) * (n + 1), st));
+  B2S_CHECK(cudaMallocAsync(&fill, sizeof(int32_t) * n, st));
+  B2S_CHECK(cudaMallocAsync(&idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1), st));
+  B2S_CHECK(cudaMallocAsync(&ticket, sizeof(unsigned int), st));
+  B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n + 1), st));
+  B2S_CHECK(cudaMemsetAsync(fill, 0, sizeof(int32_t) * n, st));
+  B2S_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+  k_upper_count<<<grid_for(n), 256, 0, st>>>(n, rp, ci, cnt);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, ptr, n + 1, st);
+  void* tmp = nullptr;
+  B2S_CHECK(cudaMallocAsync(&tmp, tmp_bytes, st));
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, ptr, n + 1, st);
+  k_upper_fill<<<grid_for(n), 256, 0, st>>>(n, rp, ci, ptr, fill, idx);
+  k_fill_int<<<grid_for(n), 256, 0, st>>>(n, row_group, -1);
+  k_color_sync_free<<<sync_free_grid(n), 256, 0, st>>>(n, rp, ci, ptr, idx, row_group, ticket);
+  B2S_LAUNCH_CHECK();
+  B2S_CHECK(cudaFreeAsync(tmp, st));
+  B2S_CHECK(cudaFreeAsync(cnt, st));
+  B2S_CHECK(cudaFreeAsync(ptr, st));
+  B2S_CHECK(cudaFreeAsync(fill, st));
+  B2S_CHECK(cudaFreeAsync(idx, st));
+  B2S_CHECK(cudaFreeAsync(ticket, st));
+  return finish_groups(n, row_group, ngroups_host, st);
+}
+
+// bs/analysis.py:61-71: iperm = stable argsort(row_group), perm = its
+// inverse, offsets = exclusive scan of the group histogram.
+int b2s_plan_from_groups(int n, const int32_t* row_group, int ngroups, int32_t* perm,
+                         int32_t* iperm, int32_t* offsets, cudaStream_t st) {
+  if (n < 0 || ngroups < 0 || (n > 0 && ngroups < 1)) return B2S_SHAPE;
+  if (n == 0) {
+    B2S_CHECK(cudaMemsetAsync(offsets, 0, sizeof(int32_t), st));
+    return B2S_OK;
+  }
+  int32_t *cnt = nullptr, *vals_in = nullptr, *keys_out = nullptr;
+  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (ngroups + 1), st));
+  B2S_CHECK(cudaMallocAsync(&vals_in, sizeof(int32_t) * n, st));
+  B2S_CHECK(cudaMallocAsync(&keys_out, sizeof(int32_t) * n, st));
+  B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (ngroups + 1), st));
+  k_histogram<<<grid_for(n), 256, 0, st>>>(n, row_group, cnt);
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t1, cnt, offsets, ngroups + 1, st);
+  int end_bit = 1;
+  while (end_bit < 31 && (1ll << end_bit) < (long long)ngroups) ++end_bit;
+  cub::DeviceRadixSort::SortPairs(nullptr, t2, row_group, keys_out, vals_in, iperm, n, 0,
+                                  end_bit, st);
+  void* tmp = nullptr;
+  size_t tb = t1 > t2 ? t1 : t2;
+  B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
+  cub::DeviceScan::ExclusiveSum(tmp, t1, cnt, offsets, ngroups + 1, st);
+  k_iota<<<grid_for(n), 256, 0, st>>>(n, vals_in);
+  // LSD radix sort is stable: equal groups keep ascending row order
+  cub::DeviceRadixSort::SortPairs(tmp, t2, row_group, keys_out, vals_in, iperm, n, 0, end_bit,
+                                  st);
+  k_invert_perm<<<grid_for(n), 256, 0, st>>>(n, iperm, perm);
+  B2S_LAUNCH_CHECK();
+  B2S_CHECK(cudaFreeAsync(tmp, st));
+  B2S_CHECK(cudaFreeAsync(cnt, st));
+  B2S_CHECK(cudaFreeAsync(vals_in, st));
+  B2S_CHECK(cudaFreeAsync(keys_out, st));
+  return B2S_OK;
+}
+
+// Symmetric reorder of a block-CSR matrix.  take = iperm, cmap = perm for the
+// forward direction (inverse=False in the reference); swap them for inverse.
+// out_src (nnzb int32, may be null) receives, per output slot, the input slot
+// it came from (the reference's `order` composition; used to build CopyPlans).
+int b2s_permute_bsr(int n, int b, const int32_t* rp, const int32_t* ci, const double* vals,
+                    const int32_t* cmap, const int32_t* take, int32_t* out_rp, int32_t* out_ci,
+                    double* out_vals, int32_t* out_src, cudaStream_t st) {
+  if (n < 0 || b < 1) return B2S_SHAPE;
+  if (n == 0) {
+    B2S_CHECK(cudaMemsetAsync(out_rp, 0, sizeof(int32_t), st));
+    return B2S_OK;
+  }
+  int32_t* cnt = nullptr;
+  int32_t* src = out_src;
+  int32_t nnz = 0;
+  B2S_CHECK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (n + 1), st));
+  if (!src) B2S_CHECK(cudaMallocAsync(&src, sizeof(int32_t) * (nnz > 0 ? nnz : 1), st));
+  B2S_CHECK(cudaMemsetAsync(cnt + n, 0, sizeof(int32_t), st));
+  k_permute_count<<<grid_for(n), 256, 0, st>>>(n, rp, take, cnt);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, out_rp, n + 1, st);
+  void* tmp = nullptr;
+  B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, out_rp, n + 1, st);
+  k_permute_cols<<<grid_for(n), 256, 0, st>>>(n, rp, ci, take, cmap, out_rp, out_ci, src);
+  if (nnz > 0 && vals && out_vals)
+    k_gather_blocks<<<grid_for((long long)nnz * b * b), 256, 0, st>>>(nnz, b * b, src, vals,
+                                                                      out_vals);
+  B2S_LAUNCH_CHECK();
+  B2S_CHECK(cudaFreeAsync(tmp, st));
+  B2S_CHECK(cudaFreeAsync(cnt, st));
+  if (!out_src) B2S_CHECK(cudaFreeAsync(src, st));
+  return B2S_OK;
+}
+
+int b2s_gather_rows(int n, int b, const int32_t* src, const double* in, double* out,
+                    cudaStream_t st) {
+  if (n < 0 || b < 1) return B2S_SHAPE;
+  if (n == 0) return B2S_OK;
+  k_gather_rows<<<grid_for((long long)n * b), 256, 0, st>>>(n, b, src, in, out);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+int b2s_gather_blocks(long long nblk, int b, const int32_t* src, const double* in, double* out,
+                      cudaStream_t st) {
+  if (nblk < 0 || b < 1) return B2S_SHAPE;
+  if (nblk == 0) return B2S_OK;
+  k_gather_blocks<<<grid_for(nblk * b * b), 256, 0, st>>>(nblk, b * b, src, in, out);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,423 @@
+// Zero-fill block ILU0: factorisation (bs/ilu0.py:145-201) and its
+// two-phase application (bs/ilu0.py:93-142), both as sync-free wavefronts.
+//
+// Rows are processed in plan (permuted) order.  A warp claims the next
+// group-aligned slice of <= 32 rows through an atomic ticket (ascending for
+// the factorisation and the forward sweep, descending for the backward
+// sweep); because tickets go only to resident warps and every dependency of
+// a row lies in an earlier ticket, the oldest unfinished slice can always
+// proceed.  There is no per-level launch and no grid barrier: a row waits
+// only for the rows it actually reads, so independent parts of consecutive
+// levels overlap, and the critical path costs one L2 round trip per level.
+//
+//  * factorisation: per-row "finished" flags (acquire/release), general
+//    IKJ elimination exactly as the reference orders it;
+//  * sweeps: the dependency vector itself is the flag -- it is pre-filled
+//    with a NaN sentinel and a consumer spins until the producer's value
+//    replaces it (one round trip, no separate flag + fence).  The backward
+//    sweep restores the forward scratch vector to the sentinel as it
+//    consumes it, and the Krylov kernels restore the backward output after
+//    its last use, so no extra fill pass is needed per application.
+#include "sell.cuh"
+
+namespace b2s {
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct Tickets {
+  unsigned int next;      // next slice ticket
+  unsigned int finished;  // warps that ran out of work (self-reset)
+};
+
+// Claim the next ticket for the calling warp; returns -1 once exhausted
+// (after registering the warp's exit; the last warp out resets the pair so
+// the kernel can be relaunched or graph-replayed without a memset).
+__device__ __forceinline__ long long claim(Tickets* tk, int nslices) {
+  const int lane = threadIdx.x & 31;
+  unsigned int t = 0;
+  if (lane == 0) t = atomicAdd(&tk->next, 1u);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t < (unsigned)nslices) return t;
+  if (lane == 0) {
+    const unsigned int total = gridDim.x * (blockDim.x >> 5);
+    const unsigned int f = atomicAdd(&tk->finished, 1u);
+    if (f == total - 1) {
+      tk->next = 0;
+      tk->finished = 0;
+      __threadfence();
+    }
+  }
+  return -1;
+}
+
+// ---------------------------------------------------------------------------
+// factorisation, in place on the permuted block-CSR values
+template <int B>
+__global__ void __launch_bounds__(256) k_ilu0_factor(SliceMap map, const int32_t* __restrict__ rp,
+                                                     const int32_t* __restrict__ ci,
+                                                     const int32_t* __restrict__ diag, double* w,
+                                                     double* invd, int* flag, int* bad,
+                                                     Tickets* tk) {
+  constexpr int BB = B * B;
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const long long s = claim(tk, map.nslices);
+    if (s < 0) break;
+    const int i = map.row0[s] + lane;
+    bool done = lane >= map.nrows[s];
+    int k = 0, dpos = 0, end = 0;
+    if (!done) { k = rp[i]; dpos = diag[i]; end = rp[i + 1]; }
+    for (;;) {
+      if (!done) {
+        while (k < dpos) {
+          const int r = ci[k];
+          if (ld_acquire(flag + r) == 0) break;
+          double inv_r[BB], wik[BB], l[BB];
+#pragma unroll
+          for (int e = 0; e < BB; ++e) {
+            inv_r[e] = __ldcg(invd + (long long)r * BB + e);
+            wik[e] = w[(long long)k * BB + e];
+          }
+          matmul<B>(wik, inv_r, l);  // L_ir = A_ir inv(U_rr)
+#pragma unroll
+          for (int e = 0; e < BB; ++e) w[(long long)k * BB + e] = l[e];
+          // A_ij -= L_ir U_rj for every j > r stored in both rows
+          int p = k + 1;
+          const int rend = rp[r + 1];
+          for (int q = diag[r] + 1; q < rend && p < end; ++q) {
+            const int j = ci[q];
+            while (p < end && ci[p] < j) ++p;
+            if (p < end && ci[p] == j) {
+              double urj[BB], prod[BB];
+#pragma unroll
+              for (int e = 0; e < BB; ++e) urj[e] = __ldcg(w + (long long)q * BB + e);
+              matmul<B>(l, urj, prod);
+#pragma unroll
+              for (int e = 0; e < BB; ++e) w[(long long)p * BB + e] -= prod[e];
+            }
+          }
+          ++k;
+        }
+        if (k >= dpos) {
+          double dblk[BB], inv[BB];
+#pragma unroll
+          for (int e = 0; e < BB; ++e) dblk[e] = w[(long long)dpos * BB + e];
+          if (!invert_block<B>(dblk, inv)) atomicMin(bad, i);
+#pragma unroll
+          for (int e = 0; e < BB; ++e) invd[(long long)i * BB + e] = inv[e];
+          st_release(flag + i, 1);  // orders this row's stores before the flag
+          done = true;
+        }
+      }
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sweeps.  KC = entries prefetched into registers per chunk (compile-time).
+template <int B>
+__device__ __forceinline__ void wait_row(const double* v, int c, double* out) {
+  const double* p = v + (long long)c * B;
+  bool pending;
+  do {
+    pending = false;
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      out[q] = ld_volatile(p + q);
+      pending |= is_sentinel(out[q]);
+    }
+  } while (pending);
+}
+
+// forward: y_i = r_i - sum_k L_ik y_k   (unit lower, ascending columns)
+template <int B, int KC>
+__global__ void __launch_bounds__(256) k_ilu0_forward(SliceMap map, Sell lo,
+                                                      const double* __restrict__ r, double* y,
+                                                      Tickets* tk, const int* done) {
+  constexpr int BB = B * B;
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const long long s = claim(tk, map.nslices);
+    if (s < 0) break;
+    const bool ok = lane < map.nrows[s];
+    const long long i = (long long)map.row0[s] + lane;
+    const int slot0 = lo.sp[s];
+    const int width = (lo.sp[s + 1] - slot0) >> 5;
+    double rv[B], acc[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      rv[c] = ok ? r[i * B + c] : 0.0;
+      acc[c] = 0.0;
+    }
+    for (int k0 = 0; k0 < width; k0 += KC) {
+      int col[KC];
+      double blk[KC][BB];
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const bool in = k0 + kk < width;
+        col[kk] = in ? __ldcs(lo.cols + slot0 + 32 * (k0 + kk) + lane) : -1;
+#pragma unroll
+        for (int e = 0; e < BB; ++e)
+          blk[kk][e] = in ? __ldcs(lo.vals + vidx(slot0, k0 + kk, e, lane, BB)) : 0.0;
+      }
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        if (col[kk] >= 0) {
+          double dep[B], pr[B];
+          wait_row<B>(y, col[kk], dep);
+          matvec<B>(blk[kk], dep, pr);
+#pragma unroll
+          for (int c = 0; c < B; ++c) acc[c] += pr[c];
+        }
+      }
+    }
+    if (ok) {
+#pragma unroll
+      for (int c = 0; c < B; ++c) st_volatile(y + i * B + c, canon(rv[c] - acc[c]));
+    }
+  }
+}
+
+// backward: z_i = inv(U_ii) (y_i - sum_k U_ik z_k)   (descending slices)
+template <int B, int KC>
+__global__ void __launch_bounds__(256) k_ilu0_backward(SliceMap map, Sell up,
+                                                       const double* __restrict__ dtiles,
+                                                       double* y, double* z, int reset_y,
+                                                       Tickets* tk, const int* done) {
+  constexpr int BB = B * B;
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const long long t = claim(tk, map.nslices);
+    if (t < 0) break;
+    const long long s = map.nslices - 1 - t;
+    const bool ok = lane < map.nrows[s];
+    const long long i = (long long)map.row0[s] + lane;
+    const int slot0 = up.sp[s];
+    const int width = (up.sp[s + 1] - slot0) >> 5;
+    double yv[B], acc[B], dinv[BB];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      yv[c] = ok ? y[i * B + c] : 0.0;
+      acc[c] = 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < BB; ++e) dinv[e] = __ldcs(dtiles + (s * BB + e) * 32 + lane);
+    for (int k0 = 0; k0 < width; k0 += KC) {
+      int col[KC];
+      double blk[KC][BB];
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const bool in = k0 + kk < width;
+        col[kk] = in ? __ldcs(up.cols + slot0 + 32 * (k0 + kk) + lane) : -1;
+#pragma unroll
+        for (int e = 0; e < BB; ++e)
+          blk[kk][e] = in ? __ldcs(up.vals + vidx(slot0, k0 + kk, e, lane, BB)) : 0.0;
+      }
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        if (col[kk] >= 0) {
+          double dep[B], pr[B];
+          wait_row<B>(z, col[kk], dep);
+          matvec<B>(blk[kk], dep, pr);
+#pragma unroll
+          for (int c = 0; c < B; ++c) acc[c] += pr[c];
+        }
+      }
+    }
+    if (ok) {
+      double tv[B], out[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) tv[c] = yv[c] - acc[c];
+      matvec<B>(dinv, tv, out);
+#pragma unroll
+      for (int c = 0; c < B; ++c) st_volatile(z + i * B + c, canon(out[c]));
+      if (reset_y) {
+#pragma unroll
+        for (int c = 0; c < B; ++c) y[i * B + c] = sentinel();
+      }
+    }
+  }
+}
+
+__global__ void k_fill_sentinel(long long m, double* v) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m;
+       t += (long long)gridDim.x * blockDim.x)
+    v[t] = sentinel();
+}
+
+// rows whose lower entries reach into their own slice (possible only for a
+// user-built plan whose groups are not independent sets)
+__global__ void k_slice_conflicts(SliceMap map, const int32_t* __restrict__ rp,
+                                  const int32_t* __restrict__ ci, int* conflict) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = gw; s < map.nslices; s += nw) {
+    if (lane >= map.nrows[s]) continue;
+    const int r0 = map.row0[s], i = r0 + lane;
+    for (int q = rp[i]; q < rp[i + 1]; ++q) {
+      const int c = ci[q];
+      if (c >= r0 && c != i && c < r0 + map.nrows[s]) atomicExch(conflict, 1);
+    }
+  }
+}
+
+template <int B>
+int occupancy_grid(const void* fn) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int dev = 0, sms = kSms;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms;
+}
+
+template <int B>
+int launch_factor_b(SliceMap map, const int32_t* rp, const int32_t* ci, const int32_t* diag,
+                    double* w, double* invd, int* flag, int* bad, Tickets* tk, cudaStream_t st) {
+  const int g = occupancy_grid<B>((const void*)k_ilu0_factor<B>);
+  k_ilu0_factor<B><<<g, 256, 0, st>>>(map, rp, ci, diag, w, invd, flag, bad, tk);
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
+template <int B, int KC>
+int launch_sweeps_bk(SliceMap map, Sell lo, Sell up, const double* dt, const double* r,
+                     double* y, double* z, int reset_y, Tickets* tk, const int* done,
+                     cudaStream_t st) {
+  const int gf = occupancy_grid<B>((const void*)k_ilu0_forward<B, KC>);
+  k_ilu0_forward<B, KC><<<gf, 256, 0, st>>>(map, lo, r, y, tk, done);
+  const int gb = occupancy_grid<B>((const void*)k_ilu0_backward<B, KC>);
+  k_ilu0_backward<B, KC><<<gb, 256, 0, st>>>(map, up, dt, y, z, reset_y, tk + 1, done);
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
+template <int B>
+int launch_sweeps_b(int kc, SliceMap map, Sell lo, Sell up, const double* dt, const double* r,
+                    double* y, double* z, int reset_y, Tickets* tk, const int* done,
+                    cudaStream_t st) {
+  if (kc <= 2) return launch_sweeps_bk<B, 2>(map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+  if (kc <= 4) return launch_sweeps_bk<B, 4>(map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+  return launch_sweeps_bk<B, 8>(map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+}
+
+int launch_sweeps(int b, int kc, SliceMap map, Sell lo, Sell up, const double* dt,
+                  const double* r, double* y, double* z, int reset_y, void* tickets,
+                  const int* done, cudaStream_t st) {
+  Tickets* tk = reinterpret_cast<Tickets*>(tickets);
+  switch (b) {
+    case 1: return launch_sweeps_b<1>(kc, map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+    case 2: return launch_sweeps_b<2>(kc, map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+    case 3: return launch_sweeps_b<3>(kc, map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+    case 4: return launch_sweeps_b<4>(kc, map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+    default: return B2S_UNSUPPORTED;
+  }
+}
+
+int fill_sentinel(long long m, double* v, cudaStream_t st) {
+  if (m <= 0) return B2S_OK;
+  long long g = (m + 255) / 256;
+  if (g > kSms * 32) g = kSms * 32;
+  k_fill_sentinel<<<(int)g, 256, 0, st>>>(m, v);
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
+}  // namespace b2s
+
+using namespace b2s;
+
+extern "C" {
+
+// Factor the permuted block-CSR matrix in place (values become combined
+// L\U) and write the inverse diagonal blocks (row-major, n*b*b).  The slice
+// map must follow the plan's groups (rows of one slice independent).  On a
+// singular pivot the smallest failing *permuted* row goes to bad_row_host.
+int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_t* nrows,
+                    const int32_t* rp, const int32_t* ci, const int32_t* diag, double* vals,
+                    double* inv_diag, int32_t* bad_row_host, cudaStream_t st) {
+  *bad_row_host = -1;
+  if (n < 0 || b < 1) return B2S_SHAPE;
+  if (n == 0) return B2S_OK;
+  if (b > 4) return B2S_UNSUPPORTED;
+  int* flag = nullptr;
+  int* bad = nullptr;
+  Tickets* tk = nullptr;
+  B2S_CHECK(cudaMallocAsync(&flag, sizeof(int) * n, st));
+  B2S_CHECK(cudaMallocAsync(&bad, sizeof(int), st));
+  B2S_CHECK(cudaMallocAsync(&tk, sizeof(Tickets), st));
+  B2S_CHECK(cudaMemsetAsync(flag, 0, sizeof(int) * n, st));
+  B2S_CHECK(cudaMemsetAsync(tk, 0, sizeof(Tickets), st));
+  const int big = 0x7fffffff;
+  B2S_CHECK(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  SliceMap map{nslices, row0, nrows};
+  int rc;
+  switch (b) {
+    case 1: rc = launch_factor_b<1>(map, rp, ci, diag, vals, inv_diag, flag, bad, tk, st); break;
+    case 2: rc = launch_factor_b<2>(map, rp, ci, diag, vals, inv_diag, flag, bad, tk, st); break;
+    case 3: rc = launch_factor_b<3>(map, rp, ci, diag, vals, inv_diag, flag, bad, tk, st); break;
+    default: rc = launch_factor_b<4>(map, rp, ci, diag, vals, inv_diag, flag, bad, tk, st); break;
+  }
+  if (rc != B2S_OK) return rc;
+  int h = big;
+  B2S_CHECK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(flag, st));
+  B2S_CHECK(cudaFreeAsync(bad, st));
+  B2S_CHECK(cudaFreeAsync(tk, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  if (h != big) { *bad_row_host = h; return B2S_SINGULAR_PIVOT; }
+  return B2S_OK;
+}
+
+// 1 in *conflict_host if some row of the slice map reads a row of its own
+// slice through its strict-lower part (the plan's groups are not
+// independent); such maps must fall back to one row per slice.
+int b2s_slice_conflicts(int nslices, const int32_t* row0, const int32_t* nrows,
+                        const int32_t* rp, const int32_t* ci, int* conflict_host,
+                        cudaStream_t st) {
+  *conflict_host = 0;
+  if (nslices <= 0) return B2S_OK;
+  int* d = nullptr;
+  B2S_CHECK(cudaMallocAsync(&d, sizeof(int), st));
+  B2S_CHECK(cudaMemsetAsync(d, 0, sizeof(int), st));
+  SliceMap map{nslices, row0, nrows};
+  long long g = ((long long)nslices * 32 + 255) / 256;
+  if (g > kSms * 32) g = kSms * 32;
+  k_slice_conflicts<<<(int)g, 256, 0, st>>>(map, rp, ci, d);
+  B2S_LAUNCH_CHECK();
+  B2S_CHECK(cudaMemcpyAsync(conflict_host, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(d, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  return B2S_OK;
+}
+
+int b2s_fill_sentinel(long long m, double* v, cudaStream_t st) { return fill_sentinel(m, v, st); }
+
+// z = U^-1 L^-1 r in plan order.  Preconditions: y and z hold the sentinel
+// everywhere (b2s_fill_sentinel); tickets points at 16 zeroed bytes that the
+// kernels keep reset between calls.  On return z holds the result and, when
+// reset_y != 0, y holds the sentinel again.  kc = max entries per row of L
+// and U (selects the register prefetch depth).
+int b2s_ilu0_apply(int n, int b, int kc, int nslices, const int32_t* row0, const int32_t* nrows,
+                   const int32_t* l_sp, const int32_t* l_cols, const double* l_vals,
+                   const int32_t* u_sp, const int32_t* u_cols, const double* u_vals,
+                   const double* dinv_tiles, const double* r, double* y, double* z, int reset_y,
+                   void* tickets, cudaStream_t st) {
+  if (n < 0 || b < 1) return B2S_SHAPE;
+  if (n == 0) return B2S_OK;
+  SliceMap map{nslices, row0, nrows};
+  Sell lo{l_sp, l_cols, l_vals}, up{u_sp, u_cols, u_vals};
+  return launch_sweeps(b, kc, map, lo, up, dinv_tiles, r, y, z, reset_y, tickets, nullptr, st);
+}
+
+}  // extern "C"

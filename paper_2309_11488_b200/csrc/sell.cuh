@@ -1,0 +1,30 @@
+// SELL-32 device layout descriptors shared by SpMV, ILU0 and the Krylov loop.
+#pragma once
+#include "common.cuh"
+
+namespace b2s {
+
+// A "slice map" assigns each SELL slice a contiguous run of at most 32 rows.
+// Plain maps cover rows [32s, 32s+32); group-aligned maps (used for the
+// level / colour plans) never let a slice cross a group boundary, so the
+// rows of one slice never depend on each other in a triangular sweep.
+struct SliceMap {
+  int nslices;
+  const int32_t* row0;   // first row of slice s
+  const int32_t* nrows;  // rows in slice s (1..32)
+};
+
+// One SELL-32 matrix on a slice map.  Slot (s, k, lane) lives at
+// sp[s] + 32k + lane; its b*b values at (sp[s] + 32k)*b*b + 32e + lane.
+struct Sell {
+  const int32_t* sp;    // [nslices+1] slot offsets (multiples of 32)
+  const int32_t* cols;  // [slots], -1 = padding (always at the end of a row)
+  const double* vals;   // [slots*b*b]
+};
+
+__device__ __forceinline__ long long vidx(long long slot0, int k, int e, int lane, int bb) {
+  // value index of entry (k, e) of the lane in the slice starting at slot0
+  return (slot0 + 32ll * k) * bb + 32ll * e + lane;
+}
+
+}  // namespace b2s

@@ -1,0 +1,325 @@
+// SELL-32 construction and the BSR SpMV (bs/blockcore.py:342-376).
+//
+// SpMV is HBM-bound (0.2 flop/B): per block row it streams the row's blocks
+// (72 B each for b = 3) and column indices once, gathers x (L2-resident: the
+// whole x of a 1M-cell system is 24 MB against a 126 MB L2) and writes y.
+// One thread owns one block row; a warp owns one 32-row slice, so every
+// value/column load instruction of the warp reads 32 consecutive 8-byte
+// words.  Values and columns are loaded with the streaming (evict-first)
+// hint so the matrix does not push the vectors out of L2.  Each row sums
+// its block products in ascending column order, like np.add.reduceat.
+//
+// Optional fused epilogues produce the per-CTA partial sums of the dot
+// products BiCGStab needs right after an operator application, so those
+// vectors are never re-read: gamma = rhat.v, (t.t, t.s), and the residual
+// norm.  Partials are reduced in a fixed order (no atomics): deterministic.
+#include <cub/cub.cuh>
+
+#include "sell.cuh"
+
+namespace b2s {
+
+__device__ __forceinline__ bool row_selected(int sel, int row, int c) {
+  return sel == 0 || (sel == 1 && c < row) || (sel == 2 && c > row);
+}
+
+__global__ void k_plain_slices(int n, int nslices, int32_t* row0, int32_t* nrows) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nslices; s += gridDim.x * blockDim.x) {
+    row0[s] = s * kSlice;
+    nrows[s] = min(kSlice, n - s * kSlice);
+  }
+}
+
+__global__ void k_group_slice_counts(int ngroups, const int32_t* __restrict__ off, int32_t* cnt) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x)
+    cnt[g] = (off[g + 1] - off[g] + kSlice - 1) / kSlice;
+}
+
+__global__ void k_group_slices(int ngroups, int nslices, const int32_t* __restrict__ off,
+                               const int32_t* __restrict__ base, int32_t* row0,
+                               int32_t* nrows) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nslices; s += gridDim.x * blockDim.x) {
+    int lo = 0, hi = ngroups - 1;  // last g with base[g] <= s
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (base[mid] <= s) lo = mid; else hi = mid - 1;
+    }
+    const int r0 = off[lo] + (s - base[lo]) * kSlice;
+    row0[s] = r0;
+    nrows[s] = min(kSlice, off[lo + 1] - r0);
+  }
+}
+
+// slots of slice s = 32 * longest selected row of the slice
+__global__ void k_sell_width(int nslices, const int32_t* __restrict__ row0,
+                             const int32_t* __restrict__ nrows, const int32_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, int sel, int32_t* slots) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = gw; s < nslices; s += nw) {
+    int cnt = 0;
+    if (lane < nrows[s]) {
+      const int row = row0[s] + lane;
+      if (sel == 0) {
+        cnt = rp[row + 1] - rp[row];
+      } else {
+        for (int q = rp[row]; q < rp[row + 1]; ++q) cnt += row_selected(sel, row, ci[q]) ? 1 : 0;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, o));
+    if (lane == 0) slots[s] = cnt * kSlice;
+  }
+}
+
+__global__ void k_sell_fill(int nslices, int bb, const int32_t* __restrict__ row0,
+                            const int32_t* __restrict__ nrows, const int32_t* __restrict__ rp,
+                            const int32_t* __restrict__ ci, const double* __restrict__ vals,
+                            int sel, const int32_t* __restrict__ sp, int32_t* __restrict__ ocols,
+                            double* __restrict__ ovals) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = gw; s < nslices; s += nw) {
+    const long long slot0 = sp[s];
+    const int width = (sp[s + 1] - sp[s]) / kSlice;
+    int k = 0;
+    if (lane < nrows[s]) {
+      const int row = row0[s] + lane;
+      for (int q = rp[row]; q < rp[row + 1]; ++q) {
+        const int c = ci[q];
+        if (!row_selected(sel, row, c)) continue;
+        ocols[slot0 + 32ll * k + lane] = c;
+        for (int e = 0; e < bb; ++e) ovals[vidx(slot0, k, e, lane, bb)] = vals[(long long)q * bb + e];
+        ++k;
+      }
+    }
+    for (; k < width; ++k) {
+      ocols[slot0 + 32ll * k + lane] = -1;
+      for (int e = 0; e < bb; ++e) ovals[vidx(slot0, k, e, lane, bb)] = 0.0;
+    }
+  }
+}
+
+// per-slice b*b x 32 tiles of the inverse diagonal (row order of the map)
+__global__ void k_diag_tiles(int nslices, int bb, const int32_t* __restrict__ row0,
+                             const int32_t* __restrict__ nrows, const double* __restrict__ inv,
+                             double* __restrict__ tiles) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = gw; s < nslices; s += nw) {
+    const bool ok = lane < nrows[s];
+    const long long row = (long long)row0[s] + lane;
+    for (int e = 0; e < bb; ++e)
+      tiles[((long long)s * bb + e) * 32 + lane] = ok ? inv[row * bb + e] : 0.0;
+  }
+}
+
+enum SpmvMode { kPlain = 0, kDotW = 1, kSelfAndW = 2, kResidual = 3 };
+
+template <int B, int MODE>
+__global__ void __launch_bounds__(256) k_spmv(SliceMap map, Sell a, const double* __restrict__ x,
+                                              double* __restrict__ y,
+                                              const double* __restrict__ w,
+                                              double* __restrict__ part0,
+                                              double* __restrict__ part1, const int* done) {
+  constexpr int BB = B * B;
+  __shared__ double red[8];
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  double p0 = 0.0, p1 = 0.0;
+  for (int s = gw; s < map.nslices; s += nw) {
+    const int slot0 = a.sp[s];
+    const int width = (a.sp[s + 1] - slot0) >> 5;
+    const bool ok = lane < map.nrows[s];
+    const long long row = (long long)map.row0[s] + lane;
+    double acc[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] = 0.0;
+    for (int k = 0; k < width; ++k) {
+      const int col = __ldcs(a.cols + slot0 + 32 * k + lane);
+      if (col < 0) continue;
+      double blk[BB], xv[B], pr[B];
+#pragma unroll
+      for (int e = 0; e < BB; ++e) blk[e] = __ldcs(a.vals + vidx(slot0, k, e, lane, BB));
+#pragma unroll
+      for (int c = 0; c < B; ++c) xv[c] = __ldg(x + (long long)col * B + c);
+      matvec<B>(blk, xv, pr);
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] += pr[c];
+    }
+    if (ok) {
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        double v = acc[c];
+        if (MODE == kResidual) v = w[row * B + c] - v;
+        y[row * B + c] = v;
+        if (MODE == kDotW) p0 = fma(w[row * B + c], v, p0);
+        if (MODE == kSelfAndW) { p0 = fma(v, v, p0); p1 = fma(v, w[row * B + c], p1); }
+        if (MODE == kResidual) p0 = fma(v, v, p0);
+      }
+    }
+  }
+  if (MODE != kPlain) {
+    double t0 = block_sum(p0, red);
+    if (threadIdx.x == 0) part0[blockIdx.x] = t0;
+    if (MODE == kSelfAndW) {
+      double t1 = block_sum(p1, red);
+      if (threadIdx.x == 0) part1[blockIdx.x] = t1;
+    }
+  }
+}
+
+inline int grid_for(long long work, int threads = 256) {
+  long long g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > kSms * 32) g = kSms * 32;
+  return (int)g;
+}
+
+template <int B>
+int launch_spmv_b(int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
+                  const double* w, double* p0, double* p1, const int* done, cudaStream_t st) {
+  dim3 g(nparts), t(256);
+  switch (mode) {
+    case kPlain: k_spmv<B, kPlain><<<g, t, 0, st>>>(map, a, x, y, w, p0, p1, done); break;
+    case kDotW: k_spmv<B, kDotW><<<g, t, 0, st>>>(map, a, x, y, w, p0, p1, done); break;
+    case kSelfAndW: k_spmv<B, kSelfAndW><<<g, t, 0, st>>>(map, a, x, y, w, p0, p1, done); break;
+    case kResidual: k_spmv<B, kResidual><<<g, t, 0, st>>>(map, a, x, y, w, p0, p1, done); break;
+    default: return B2S_SHAPE;
+  }
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
+int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
+                const double* w, double* p0, double* p1, const int* done, cudaStream_t st) {
+  switch (b) {
+    case 1: return launch_spmv_b<1>(mode, nparts, map, a, x, y, w, p0, p1, done, st);
+    case 2: return launch_spmv_b<2>(mode, nparts, map, a, x, y, w, p0, p1, done, st);
+    case 3: return launch_spmv_b<3>(mode, nparts, map, a, x, y, w, p0, p1, done, st);
+    case 4: return launch_spmv_b<4>(mode, nparts, map, a, x, y, w, p0, p1, done, st);
+    default: return B2S_UNSUPPORTED;
+  }
+}
+
+}  // namespace b2s
+
+using namespace b2s;
+
+extern "C" {
+
+// Plain slice map: slice s covers rows [32s, min(32s+32, n)).
+int b2s_slices_plain(int n, int32_t* row0, int32_t* nrows, cudaStream_t st) {
+  if (n < 0) return B2S_SHAPE;
+  const int ns = (n + kSlice - 1) / kSlice;
+  if (ns == 0) return B2S_OK;
+  k_plain_slices<<<grid_for(ns), 256, 0, st>>>(n, ns, row0, nrows);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+// Number of group-aligned slices for group offsets off[0..ngroups].
+// base (ngroups+1 int32, device) receives the first slice of every group.
+int b2s_slices_grouped_count(int ngroups, const int32_t* off, int32_t* base,
+                             int32_t* nslices_host, cudaStream_t st) {
+  if (ngroups < 0) return B2S_SHAPE;
+  *nslices_host = 0;
+  if (ngroups == 0) return B2S_OK;
+  int32_t* cnt = nullptr;
+  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (ngroups + 1), st));
+  B2S_CHECK(cudaMemsetAsync(cnt + ngroups, 0, sizeof(int32_t), st));
+  k_group_slice_counts<<<grid_for(ngroups), 256, 0, st>>>(ngroups, off, cnt);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, base, ngroups + 1, st);
+  void* tmp = nullptr;
+  B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, base, ngroups + 1, st);
+  B2S_LAUNCH_CHECK();
+  int32_t h = 0;
+  B2S_CHECK(cudaMemcpyAsync(&h, base + ngroups, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(tmp, st));
+  B2S_CHECK(cudaFreeAsync(cnt, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  *nslices_host = h;
+  return B2S_OK;
+}
+
+int b2s_slices_grouped_fill(int ngroups, int nslices, const int32_t* off, const int32_t* base,
+                            int32_t* row0, int32_t* nrows, cudaStream_t st) {
+  if (ngroups < 0 || nslices < 0) return B2S_SHAPE;
+  if (nslices == 0) return B2S_OK;
+  k_group_slices<<<grid_for(nslices), 256, 0, st>>>(ngroups, nslices, off, base, row0, nrows);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+// Slot offsets of a SELL-32 layout: sp[0..nslices], total slots to host.
+// sel: 0 = every block, 1 = strict lower, 2 = strict upper.
+int b2s_sell_offsets(int nslices, const int32_t* row0, const int32_t* nrows, const int32_t* rp,
+                     const int32_t* ci, int sel, int32_t* sp, long long* slots_host,
+                     cudaStream_t st) {
+  if (nslices < 0 || sel < 0 || sel > 2) return B2S_SHAPE;
+  *slots_host = 0;
+  if (nslices == 0) {
+    B2S_CHECK(cudaMemsetAsync(sp, 0, sizeof(int32_t), st));
+    return B2S_OK;
+  }
+  int32_t* cnt = nullptr;
+  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (nslices + 1), st));
+  B2S_CHECK(cudaMemsetAsync(cnt + nslices, 0, sizeof(int32_t), st));
+  k_sell_width<<<grid_for((long long)nslices * 32), 256, 0, st>>>(nslices, row0, nrows, rp, ci,
+                                                                   sel, cnt);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, sp, nslices + 1, st);
+  void* tmp = nullptr;
+  B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, sp, nslices + 1, st);
+  B2S_LAUNCH_CHECK();
+  int32_t h = 0;
+  B2S_CHECK(cudaMemcpyAsync(&h, sp + nslices, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(tmp, st));
+  B2S_CHECK(cudaFreeAsync(cnt, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  *slots_host = h;
+  return B2S_OK;
+}
+
+int b2s_sell_fill(int nslices, int b, const int32_t* row0, const int32_t* nrows,
+                  const int32_t* rp, const int32_t* ci, const double* vals, int sel,
+                  const int32_t* sp, int32_t* cols, double* svals, cudaStream_t st) {
+  if (nslices < 0 || b < 1 || sel < 0 || sel > 2) return B2S_SHAPE;
+  if (nslices == 0) return B2S_OK;
+  k_sell_fill<<<grid_for((long long)nslices * 32), 256, 0, st>>>(nslices, b * b, row0, nrows, rp,
+                                                                  ci, vals, sel, sp, cols, svals);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+int b2s_diag_tiles(int nslices, int b, const int32_t* row0, const int32_t* nrows,
+                   const double* inv, double* tiles, cudaStream_t st) {
+  if (nslices < 0 || b < 1) return B2S_SHAPE;
+  if (nslices == 0) return B2S_OK;
+  k_diag_tiles<<<grid_for((long long)nslices * 32), 256, 0, st>>>(nslices, b * b, row0, nrows,
+                                                                   inv, tiles);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+// y = A x (mode 0), with gamma partials w.y (mode 1), with (y.y, y.w)
+// partials (mode 2), or the residual y = w - A x with y.y partials (mode 3).
+// `nparts` CTAs are launched; part0/part1 receive one partial per CTA.
+int b2s_spmv(int b, int mode, int nparts, int nslices, const int32_t* row0,
+             const int32_t* nrows, const int32_t* sp, const int32_t* cols, const double* vals,
+             const double* x, double* y, const double* w, double* part0, double* part1,
+             const int* done, cudaStream_t st) {
+  if (nslices < 0 || nparts < 1) return B2S_SHAPE;
+  SliceMap map{nslices, row0, nrows};
+  Sell a{sp, cols, vals};
+  return launch_spmv(b, mode, nparts, map, a, x, y, w, part0, part1, done, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+"""Zero-fill block ILU0 on the GPU: ``decompose`` and ``Ilu0Factorization``.
+
+Same contract as ``bs/ilu0.py``: the factorisation runs on the plan-permuted
+copy of the matrix in ascending permuted order (IKJ), keeps combined L\\U in
+the input pattern (permuted), raises ``MissingDiagonal`` / ``SingularPivot``
+with input row numbers, and ``apply`` solves L y = r, U z = y with the
+permutation handled internally.
+
+Device work (csrc/analysis.cu, csrc/ilu0.cu): permutation, sync-free
+factorisation, then SELL-32 tiles of the strict-lower and strict-upper
+blocks plus the inverse-diagonal tiles that the sweeps stream.  Host
+attributes (``combined``, ``inverted_diagonals``) are materialised lazily.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import SINGULAR_PIVOT, check
+from .analysis import ParallelPlan, apply_permutation, dev_to_matrix, permute_device
+from .blockcore import BlockMatrix, BlockVector
+from .errors import MissingDiagonal, ShapeError, SingularPivot
+
+
+def _kc(width: int) -> int:
+    return 2 if width <= 2 else (4 if width <= 4 else 8)
+
+
+class Ilu0Factorization:
+    """Combined L/U factors (plan order), inverse diagonals and the plan,
+    resident on the GPU (bs/ilu0.py:59-142)."""
+
+    def __init__(self, plan: ParallelPlan, b: int, n: int, lu: "D.DevBSR", invd: torch.Tensor,
+                 smap: "D.SliceMap", lower: "D.Sell", upper: "D.Sell", dtiles: torch.Tensor,
+                 identity: bool, source: BlockMatrix, a_perm: "D.DevBSR"):
+        self.plan = plan
+        self._b = b
+        self._n = n
+        self._lu = lu
+        self._invd = invd
+        self.smap = smap
+        self.lower = lower
+        self.upper = upper
+        self.dtiles = dtiles
+        self._identity_perm = identity
+        self._source = source        # the (block-row-major) matrix that was factored
+        self._a_perm = a_perm        # its unfactored plan-order copy (reused as operator)
+        self.kc = _kc(max(lower.width, upper.width))
+        self._combined = None
+        self._inv_host = None
+        self._tickets = torch.zeros(8, dtype=torch.int32, device=invd.device)
+
+    # -- reference attributes --------------------------------------------------
+    @property
+    def block_size(self) -> int:
+        return self._b
+
+    @property
+    def num_block_rows(self) -> int:
+        return self._n
+
+    @property
+    def combined(self) -> BlockMatrix:
+        if self._combined is None:
+            if self._identity_perm:
+                bb = self._b * self._b
+                vals = self._lu.vals[: self._lu.pat.nnz * bb].cpu().numpy()
+                self._combined = BlockMatrix(self._source.pattern, self._b, vals)
+            else:
+                self._combined = dev_to_matrix(self._lu)
+        return self._combined
+
+    @property
+    def inverted_diagonals(self) -> np.ndarray:
+        if self._inv_host is None:
+            bb = self._b * self._b
+            self._inv_host = self._invd[: self._n * bb].cpu().numpy().reshape(self._n, self._b,
+                                                                             self._b)
+        return self._inv_host
+
+    def factors_in_input_order(self) -> BlockMatrix:
+        """The combined factors carried back to input numbering (bs/ilu0.py:79-83)."""
+        if self._identity_perm:
+            return self.combined.copy()
+        return dev_to_matrix(permute_device(self._lu, self.plan, inverse=True))
+
+    # -- application -------------------------------------------------------------
+    def apply_device(self, r_perm: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """z = U^-1 L^-1 r for a plan-order device vector."""
+        m = self._n * self._b
+        dev = r_perm.device
+        y = D.empty_f64(m, dev)
+        z = out if out is not None else D.empty_f64(m, dev)
+        if m == 0:
+            return z
+        D.fill_sentinel(y, m)
+        D.fill_sentinel(z, m)
+        s = self.smap
+        lo, up = self.lower, self.upper
+        check(D.lib().b2s_ilu0_apply(self._n, self._b, self.kc, s.nslices, D.ptr(s.row0),
+                                     D.ptr(s.nrows), D.ptr(lo.sp), D.ptr(lo.cols),
+                                     D.ptr(lo.vals), D.ptr(up.sp), D.ptr(up.cols),
+                                     D.ptr(up.vals), D.ptr(self.dtiles), D.ptr(r_perm),
+                                     D.ptr(y), D.ptr(z), 1, D.ptr(self._tickets), D.stream()),
+              "ilu0_apply")
+        return z
+
+    def apply(self, r: BlockVector) -> BlockVector:
+        if r.block_size != self._b:
+            raise ShapeError("vector block size does not match factorization")
+        if r.num_blocks != self._n:
+            raise ShapeError("vector length does not match factorization")
+        return BlockVector(self.apply_array(r.data), self._b)
+
+    def apply_array(self, r: np.ndarray) -> np.ndarray:
+        """Input order in, input order out (bs/ilu0.py:93-103)."""
+        if self._n == 0:
+            return np.asarray(r, dtype=np.float64).copy()
+        dev = self._invd.device
+        rd = D.f64(np.asarray(r).reshape(-1), dev)
+        if self._identity_perm:
+            return self.apply_device(rd)[: self._n * self._b].cpu().numpy()
+        rp = D.gather_rows(rd, self.plan.device("inverse_permutation"), self._n, self._b)
+        z = self.apply_device(rp)
+        return D.gather_rows(z, self.plan.device("permutation"), self._n,
+                             self._b).cpu().numpy()
+
+    def apply_permuted_array(self, r: np.ndarray) -> np.ndarray:
+        if self._n == 0:
+            return np.asarray(r, dtype=np.float64).copy()
+        rd = D.f64(np.asarray(r).reshape(-1), self._invd.device)
+        return self.apply_device(rd)[: self._n * self._b].cpu().numpy()
+
+    def __call__(self, r: np.ndarray) -> np.ndarray:
+        return self.apply_array(r)
+
+
+def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) -> Ilu0Factorization:
+    """``decompose`` on an (optionally pre-uploaded) matrix."""
+    a = a.as_block_row_major()
+    n = a.num_block_rows
+    if plan.num_rows != n:
+        raise ShapeError("plan does not match the matrix")
+    b = a.block_size
+    bsr = bsr or D.DevBSR.upload(a)
+    dev = bsr.pat.rp.device
+    D.find_diagonal(bsr.pat)                       # MissingDiagonal(first row)
+    identity = plan.is_identity
+    a_perm = bsr if identity else permute_device(bsr, plan)
+    lu = D.DevBSR(a_perm.pat, b, a_perm.vals.clone())
+    diag = D.find_diagonal(lu.pat)
+    smap = plan.slice_map()
+    if not plan.independent_groups and smap.conflicts(lu.pat):
+        # a user-built plan whose groups are not independent sets: fall back
+        # to one row per slice, which is always safe for the wavefronts
+        smap = D.SliceMap.singles(n, dev)
+    inv = D.empty_f64(n * b * b, dev)
+    bad = C.c_int32(-1)
+    rc = D.lib().b2s_ilu0_factor(n, b, smap.nslices, D.ptr(smap.row0), D.ptr(smap.nrows),
+                                 D.ptr(lu.pat.rp), D.ptr(lu.pat.ci), D.ptr(diag),
+                                 D.ptr(lu.vals), D.ptr(inv), C.byref(bad), D.stream())
+    if rc == SINGULAR_PIVOT:
+        row = int(bad.value)
+        if not identity:
+            row = int(plan.device("inverse_permutation")[row].item())
+        raise SingularPivot(row)
+    check(rc, "ilu0_factor")
+    lower = D.Sell.build(smap, lu, 1)
+    upper = D.Sell.build(smap, lu, 2)
+    dtiles = D.empty_f64(smap.nslices * b * b * 32, dev)
+    check(D.lib().b2s_diag_tiles(smap.nslices, b, D.ptr(smap.row0), D.ptr(smap.nrows),
+                                 D.ptr(inv), D.ptr(dtiles), D.stream()), "diag_tiles")
+    return Ilu0Factorization(plan, b, n, lu, inv, smap, lower, upper, dtiles, identity, a,
+                             a_perm)
+
+
+def decompose(a: BlockMatrix, plan: ParallelPlan) -> Ilu0Factorization:
+    """Blocked zero-fill LU of ``a`` in plan order (bs/ilu0.py:145-201)."""
+    a = a.as_block_row_major()
+    if plan.num_rows != a.num_block_rows:
+        raise ShapeError("plan does not match the matrix")
+    return factor_device(a, plan)
+
+
+__all__ = ["Ilu0Factorization", "decompose", "apply_permutation"]

@@ -1,0 +1,362 @@
+"""Right-preconditioned BiCGStab on the GPU (drop-in for bs/krylov.py).
+
+``bicgstab(MatrixOperator(A), decompose(A, plan), b)`` runs entirely on the
+device through the native driver ``b2s_bicgstab`` (csrc/krylov.cu): the
+Krylov vectors live in plan order next to the plan-ordered operator and the
+ILU factors, one iteration is one CUDA-graph replay, and the host only reads
+a pinned completion word.  The reference's semantics are kept exactly:
+half-step counting, the 1e-60 breakdown floor, the order of the exit tests,
+the true-residual ``final_norm`` and the x0 return on non-finite x.
+
+Other operator / preconditioner combinations the reference accepts (any
+callable preconditioner, duck-typed operators) run a host-driven loop over
+device vectors with the same control flow.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import BicgArgs, BicgResult, check
+from .blockcore import BlockMatrix, BlockVector, DeviceOperator
+from .errors import ShapeError
+from .ilu0 import Ilu0Factorization
+
+REDUCTION_CHUNK = 64          # bs/krylov.py:24
+DEFAULT_REDUCTION = 0.01
+DEFAULT_MAX_ITERATIONS = 200
+_BREAKDOWN_FLOOR = 1e-60
+_REASONS = {2: "breakdown", 3: "numerical", 4: "budget"}
+
+
+# ---------------------------------------------------------------------------
+# reductions
+
+def dot_partials(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Per-chunk partial sums of a*b over consecutive 64-element chunks
+    (bs/krylov.py:30-36), computed on the device."""
+    a = np.asarray(a, dtype=np.float64).reshape(-1)
+    b = np.asarray(b, dtype=np.float64).reshape(-1)
+    if a.size == 0:
+        return np.zeros(0)
+    dev = D.require_cuda()
+    prod = D.f64(a, dev) * D.f64(b, dev)
+    pad = (-prod.numel()) % REDUCTION_CHUNK
+    if pad:
+        prod = torch.cat([prod, prod.new_zeros(pad)])
+    return prod.view(-1, REDUCTION_CHUNK).sum(dim=1).cpu().numpy()
+
+
+def dot_arrays(a: np.ndarray, b: np.ndarray) -> float:
+    a = np.asarray(a, dtype=np.float64).reshape(-1)
+    b = np.asarray(b, dtype=np.float64).reshape(-1)
+    if a.size == 0:
+        return 0.0
+    dev = D.require_cuda()
+    return D.dot(D.f64(a, dev), D.f64(b, dev), a.size)
+
+
+def norm_array(a: np.ndarray) -> float:
+    return float(np.sqrt(dot_arrays(a, a)))
+
+
+def dot(a: BlockVector, b: BlockVector) -> float:
+    """Deterministic inner product of two block vectors (fixed-order device
+    reduction: identical results on every run)."""
+    if a.data.size != b.data.size:
+        raise ShapeError("vectors have different lengths")
+    return dot_arrays(a.data, b.data)
+
+
+def norm(a: BlockVector) -> float:
+    return float(np.sqrt(dot(a, a)))
+
+
+# ---------------------------------------------------------------------------
+# operators and reports
+
+class MatrixOperator:
+    """Plain blocked SpMV operator (bs/krylov.py:63-81)."""
+
+    def __init__(self, a: BlockMatrix):
+        self.matrix = a.as_block_row_major()
+        self._dev = None
+
+    @property
+    def block_size(self) -> int:
+        return self.matrix.block_size
+
+    @property
+    def num_blocks(self) -> int:
+        return self.matrix.num_block_rows
+
+    def device(self) -> DeviceOperator:
+        if self._dev is None:
+            self._dev = DeviceOperator(self.matrix)
+        return self._dev
+
+    def apply_device(self, x: torch.Tensor, y: torch.Tensor):
+        self.device().apply(x, y)
+
+    def apply_array(self, x: np.ndarray) -> np.ndarray:
+        op = self.device()
+        dev = op.bsr.pat.rp.device
+        y = D.empty_f64(op.n * op.b, dev)
+        op.apply(D.f64(x, dev), y)
+        return y[: op.n * op.b].cpu().numpy()
+
+    def apply(self, x: BlockVector) -> BlockVector:
+        return BlockVector(self.apply_array(x.data), self.block_size)
+
+
+class WellAugmentedOperator(MatrixOperator):
+    """Well-augmented operator (bs/krylov.py:84-94): next on the roadmap
+    (SURVEY.md §8(f) row 1), not part of this build's hot path."""
+
+    def __init__(self, a: BlockMatrix, wells):
+        super().__init__(a)
+        self.wells = wells
+        if not getattr(wells, "is_empty", True):
+            raise NotImplementedError("separate well application is not on the device path yet")
+
+
+@dataclass(frozen=True)
+class StoppingCriteria:
+    """Relative residual reduction and iteration budget (bs/krylov.py:97-108)."""
+
+    relative_reduction: float = DEFAULT_REDUCTION
+    max_iterations: int = DEFAULT_MAX_ITERATIONS
+
+    def __post_init__(self):
+        if not 0.0 < self.relative_reduction < 1.0:
+            raise ValueError("relative_reduction must lie in (0, 1)")
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be >= 1")
+
+
+@dataclass
+class SolveReport:
+    """Outcome of one solve (bs/krylov.py:111-129); iterations in half steps."""
+
+    converged: bool
+    iterations: float
+    initial_norm: float
+    final_norm: float
+    elapsed: float
+    group_count: int
+    fallback_used: bool = False
+    failure_reason: str | None = None
+    setup_elapsed: float = 0.0
+    # device-side accounting (not in the reference): graph replays and kernels
+    gpu_launches: int = 0
+
+
+# ---------------------------------------------------------------------------
+# the native driver
+
+@dataclass
+class DeviceKrylov:
+    """Everything ``b2s_bicgstab`` needs, resident in plan order."""
+
+    n: int
+    b: int
+    smap: "D.SliceMap"
+    a: "D.Sell"
+    fact: Ilu0Factorization | None
+    work: torch.Tensor
+
+    @classmethod
+    def build(cls, matrix: BlockMatrix, fact: Ilu0Factorization | None,
+              a_bsr: "D.DevBSR" = None) -> "DeviceKrylov":
+        n, b = matrix.num_block_rows, matrix.block_size
+        if fact is not None:
+            smap = fact.smap
+            if a_bsr is None:
+                a_bsr = (fact._a_perm if fact._source is matrix
+                         else _plan_order(D.DevBSR.upload(matrix), fact))
+            dev = a_bsr.pat.rp.device
+        else:
+            a_bsr = a_bsr or D.DevBSR.upload(matrix)
+            dev = a_bsr.pat.rp.device
+            smap = D.SliceMap.plain(n, dev)
+        sell = D.Sell.build(smap, a_bsr, 0)
+        nbytes = int(D.lib().b2s_bicgstab_workspace_bytes(n, b, D.NPARTS))
+        work = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=dev)
+        return cls(n, b, smap, sell, fact, work)
+
+    def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
+              check_lag: int = 2) -> BicgResult:
+        """Solve in place on plan-order device vectors (x: x0 in, x out)."""
+        f = self.fact
+        args = BicgArgs()
+        args.n, args.b, args.nparts = self.n, self.b, D.NPARTS
+        args.precond = 1 if f is not None else 0
+        args.kc = f.kc if f is not None else 2
+        args.maxit = stop.max_iterations
+        args.check_lag = check_lag
+        args.tol = stop.relative_reduction
+        s = self.smap
+        args.nslices, args.row0, args.nrows = s.nslices, D.ptr(s.row0), D.ptr(s.nrows)
+        args.a_sp, args.a_cols, args.a_vals = D.ptr(self.a.sp), D.ptr(self.a.cols), D.ptr(self.a.vals)
+        if f is not None:
+            args.l_sp, args.l_cols, args.l_vals = (D.ptr(f.lower.sp), D.ptr(f.lower.cols),
+                                                   D.ptr(f.lower.vals))
+            args.u_sp, args.u_cols, args.u_vals = (D.ptr(f.upper.sp), D.ptr(f.upper.cols),
+                                                   D.ptr(f.upper.vals))
+            args.dinv_tiles = D.ptr(f.dtiles)
+        args.rhs, args.x, args.work = D.ptr(rhs), D.ptr(x), D.ptr(self.work)
+        args.stream = D.stream()
+        res = BicgResult()
+        check(D.lib().b2s_bicgstab(C.byref(args), C.byref(res)), "bicgstab")
+        return res
+
+
+def _plan_order(bsr: "D.DevBSR", fact: Ilu0Factorization) -> "D.DevBSR":
+    from .analysis import permute_device
+    return bsr if fact._identity_perm else permute_device(bsr, fact.plan)
+
+
+def _as_precond(precond) -> Callable[[np.ndarray], np.ndarray]:
+    if precond is None:
+        return lambda r: r
+    if isinstance(precond, Ilu0Factorization):
+        return precond.apply_array
+    return precond
+
+
+def bicgstab(op, precond, b: BlockVector, x0: BlockVector | None = None,
+             stop: StoppingCriteria | None = None) -> tuple[BlockVector, SolveReport]:
+    """Solve op(x) = b with right-preconditioned BiCGStab (bs/krylov.py:140-244)."""
+    if stop is None:
+        stop = StoppingCriteria()
+    if b.block_size != op.block_size or b.num_blocks != op.num_blocks:
+        raise ShapeError("right-hand side does not match the operator")
+    if x0 is None:
+        x0 = BlockVector.zeros(op.num_blocks, op.block_size)
+    elif x0.block_size != b.block_size or x0.num_blocks != b.num_blocks:
+        raise ShapeError("initial guess does not match the right-hand side")
+    native = (type(op) is MatrixOperator and
+              (precond is None or isinstance(precond, Ilu0Factorization)) and
+              op.num_blocks > 0)
+    if native:
+        return _bicgstab_native(op, precond, b, x0, stop)
+    return _bicgstab_generic(op, precond, b, x0, stop)
+
+
+def _bicgstab_native(op: MatrixOperator, fact, b: BlockVector, x0: BlockVector,
+                     stop: StoppingCriteria, krylov: DeviceKrylov | None = None):
+    t0 = time.perf_counter()
+    kr = krylov or DeviceKrylov.build(op.matrix, fact)
+    n, bs = kr.n, kr.b
+    dev = kr.work.device
+    bd, xd = D.f64(b.data, dev), D.f64(x0.data, dev)
+    perm = fact is not None and not fact._identity_perm
+    if perm:
+        iperm = fact.plan.device("inverse_permutation")
+        bd, xd = D.gather_rows(bd, iperm, n, bs), D.gather_rows(xd, iperm, n, bs)
+    res = kr.solve(bd, xd, stop)
+    if perm:
+        xd = D.gather_rows(xd, fact.plan.device("permutation"), n, bs)
+    x = xd[: n * bs].cpu().numpy()
+    groups = fact.plan.group_count if fact is not None else 0
+    rep = SolveReport(bool(res.converged), float(res.iterations), float(res.initial_norm),
+                      float(res.final_norm), time.perf_counter() - t0, groups,
+                      failure_reason=None if res.converged else _REASONS.get(res.reason, "budget"),
+                      gpu_launches=int(res.graph_launches) * int(res.kernels_per_iteration))
+    if not res.converged and res.reason == 3 and res.iterations == 0.0 and \
+            not np.isfinite(res.initial_norm):
+        x = x0.data.copy()
+    return BlockVector(x, bs), rep
+
+
+def _bicgstab_generic(op, precond, b: BlockVector, x0: BlockVector, stop: StoppingCriteria):
+    """Host-driven loop for duck-typed operators / callable preconditioners;
+    vectors stay on the device, reductions use the device dot kernel."""
+    apply_m = _as_precond(precond)
+    groups = precond.plan.group_count if isinstance(precond, Ilu0Factorization) else 0
+    t0 = time.perf_counter()
+    dev = D.require_cuda()
+    m = b.data.size
+
+    def A(v):   # device -> device through the operator's array API
+        return D.f64(op.apply_array(v.cpu().numpy()), dev)
+
+    def M(v):
+        return D.f64(apply_m(v.cpu().numpy()), dev)
+
+    def nrm(v):
+        return float(np.sqrt(D.dot(v, v, m))) if m else 0.0
+
+    x = D.f64(x0.data, dev) if m else torch.zeros(0, dtype=torch.float64, device=dev)
+    bd = D.f64(b.data, dev) if m else x.clone()
+    r = bd - A(x) if m else x.clone()
+    norm0 = nrm(r)
+    target = stop.relative_reduction * norm0
+
+    def report(conv, its, final, reason=None):
+        return SolveReport(conv, its, norm0, final, time.perf_counter() - t0, groups,
+                           failure_reason=reason)
+
+    if not np.isfinite(norm0):
+        return BlockVector(x0.data.copy(), b.block_size), report(False, 0.0, norm0, "numerical")
+    if norm0 <= target or norm0 == 0.0:
+        return BlockVector(x.cpu().numpy(), b.block_size), report(True, 0.0, norm0)
+    rhat = r.clone()
+    rho_prev = alpha = omega = 1.0
+    v = torch.zeros_like(r)
+    p = torch.zeros_like(r)
+    its = 0.0
+    reason = "budget"
+    for k in range(stop.max_iterations):
+        rho = D.dot(rhat, r, m)
+        if abs(rho) < _BREAKDOWN_FLOOR:
+            reason = "breakdown"
+            break
+        p = r.clone() if k == 0 else r + ((rho / rho_prev) * (alpha / omega)) * (p - omega * v)
+        phat = M(p)
+        v = A(phat)
+        gamma = D.dot(rhat, v, m)
+        if abs(gamma) < _BREAKDOWN_FLOOR:
+            reason = "breakdown"
+            break
+        alpha = rho / gamma
+        s = r - alpha * v
+        x = x + alpha * phat
+        its += 0.5
+        ns = nrm(s)
+        if not np.isfinite(ns):
+            reason = "numerical"
+            break
+        if ns <= target:
+            return BlockVector(x.cpu().numpy(), b.block_size), report(True, its, ns)
+        shat = M(s)
+        t = A(shat)
+        tt = D.dot(t, t, m)
+        if tt < _BREAKDOWN_FLOOR:
+            reason = "breakdown"
+            break
+        omega = D.dot(t, s, m) / tt
+        if abs(omega) < _BREAKDOWN_FLOOR:
+            reason = "breakdown"
+            break
+        x = x + omega * shat
+        r = s - omega * t
+        its += 0.5
+        nr = nrm(r)
+        if not np.isfinite(nr):
+            reason = "numerical"
+            break
+        if nr <= target:
+            return BlockVector(x.cpu().numpy(), b.block_size), report(True, its, nr)
+        rho_prev = rho
+    final = nrm(bd - A(x))
+    xh = x.cpu().numpy()
+    out = xh if np.all(np.isfinite(xh)) else x0.data.copy()
+    return BlockVector(out, b.block_size), report(False, its, final, reason)

@@ -1,0 +1,136 @@
+"""The oracle port (oracle/port.py) against the reference-generated golden
+fixtures: pins the checker before the CUDA path is judged by it.  CPU only."""
+
+import numpy as np
+import pytest
+from numpy.testing import assert_allclose, assert_array_equal
+
+from oracle import port as O
+
+
+def _sys(g):
+    b = int(g["b"])
+    rp, ci = g["rp"], g["ci"]
+    return rp, ci, g["vals"].reshape(-1, b, b), b
+
+
+@pytest.mark.parametrize("name", ["c1_20x20x10", "gen_6x5x4_b2", "gen_7x3x5_b1"])
+def test_plans_bit_exact(golden, name):
+    g = golden(name)
+    rp, ci, _, _ = _sys(g)
+    lev = O.plan_from_groups(O.level_groups(rp, ci))
+    col = O.plan_from_groups(O.color_groups(rp, ci))
+    for tag, plan in (("level", lev), ("color", col)):
+        assert_array_equal(plan.row_group, g[f"{tag}_row_group"])
+        assert_array_equal(plan.permutation, g[f"{tag}_perm"])
+        assert_array_equal(plan.inverse_permutation, g[f"{tag}_iperm"])
+        assert_array_equal(plan.group_offsets, g[f"{tag}_offsets"])
+
+
+@pytest.mark.parametrize("name", ["c1_20x20x10", "gen_6x5x4_b2", "gen_7x3x5_b1"])
+@pytest.mark.parametrize("strategy", ["level", "color", "sequential"])
+def test_factor_apply_solve(golden, name, strategy):
+    g = golden(name)
+    rp, ci, v3, b = _sys(g)
+    plan = {"level": lambda: O.plan_from_groups(O.level_groups(rp, ci)),
+            "color": lambda: O.plan_from_groups(O.color_groups(rp, ci)),
+            "sequential": lambda: O.sequential(len(rp) - 1)}[strategy]()
+    f = O.ilu0(rp, ci, v3, plan)
+    assert_array_equal(f.rp, g[f"{strategy}_lu_perm_rp"])
+    assert_array_equal(f.ci, g[f"{strategy}_lu_perm_ci"])
+    ref = g[f"{strategy}_lu"]
+    assert_allclose(f.lu.reshape(-1), ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+    ref = g[f"{strategy}_invd"]
+    assert_allclose(f.inv_diag.reshape(-1), ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+    z = O.ilu0_apply(f, g["x"])
+    ref = g[f"{strategy}_apply"]
+    assert np.linalg.norm(z - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert_allclose(O.spmv(rp, ci, v3, g["x"]), g["spmv"], rtol=1e-13, atol=1e-13)
+    for tol in (0.01, 1e-8):
+        x, rep = O.bicgstab(lambda v: O.spmv(rp, ci, v3, v), lambda r: O.ilu0_apply(f, r),
+                            g["rhs"], tol=tol)
+        conv, its, n0, fin = g[f"{strategy}_tol{tol:g}_report"]
+        assert rep.converged == bool(conv)
+        assert rep.iterations == its
+        assert_allclose(rep.initial_norm, n0, rtol=1e-13)
+        assert_allclose(rep.final_norm, fin, rtol=1e-6)
+        ref = g[f"{strategy}_tol{tol:g}_x"]
+        assert np.linalg.norm(x - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+def test_random_patterns(golden):
+    g = golden("random_patterns")
+    for t in range(12):
+        e = {k[len(f"r{t}_"):]: v for k, v in g.items() if k.startswith(f"r{t}_")}
+        b = int(e["b"])
+        rp, ci, v3 = e["rp"], e["ci"], e["vals"].reshape(-1, b, b)
+        assert_allclose(O.spmv(rp, ci, v3, e["x"]), e["spmv"], rtol=1e-13, atol=1e-13)
+        for tag, groups in (("level", O.level_groups(rp, ci)), ("color", O.color_groups(rp, ci))):
+            assert_array_equal(groups, e[f"{tag}_row_group"])
+            plan = O.plan_from_groups(groups)
+            assert_array_equal(plan.inverse_permutation, e[f"{tag}_iperm"])
+            f = O.ilu0(rp, ci, v3, plan)
+            assert_array_equal(f.ci, e[f"{tag}_lu_perm_ci"])
+            assert_allclose(f.lu.reshape(-1), e[f"{tag}_lu"], atol=1e-12 * np.abs(e[f"{tag}_lu"]).max())
+            _, _, back = O.factors_input_order(f)
+            assert_allclose(back.reshape(-1), e[f"{tag}_inorder"],
+                            atol=1e-12 * np.abs(e[f"{tag}_inorder"]).max())
+            z = O.ilu0_apply(f, e["x"])
+            assert np.linalg.norm(z - e[f"{tag}_apply"]) <= 1e-11 * np.linalg.norm(e[f"{tag}_apply"])
+
+
+def test_hand_cases(golden):
+    h = golden("hand_cases")
+    rp = np.array([0, 2, 4]); ci = np.array([0, 1, 0, 1])
+    v3 = np.array([4.0, 2.0, 1.0, 3.0]).reshape(4, 1, 1)
+    f = O.ilu0(rp, ci, v3, O.sequential(2))
+    assert_array_equal(f.lu.reshape(-1), h["scalar_lu"])
+    assert_array_equal(h["scalar_lu"], [4.0, 2.0, 0.25, 2.5])
+    chain_rp, chain_ci = np.array([0, 1, 3, 5]), np.array([0, 0, 1, 1, 2])
+    assert_array_equal(O.level_groups(chain_rp, chain_ci), h["chain_levels"])
+    assert_array_equal(O.color_groups(chain_rp, chain_ci), h["chain_colors"])
+    assert_array_equal(O.dot_partials(np.ones(130), np.ones(130)), h["partials_130"])
+    v = h["dot_v"]
+    assert O.dot(v, v) == float(h["dot_vv"])
+
+
+def test_jacobi_golden(golden):
+    h = golden("hand_cases")
+    from paper_2309_11488_b200.synthetic import GeneratorSpec, generate
+    g = generate(GeneratorSpec(12, 12, 8, seed=3))
+    a = g.a
+    rp, ci = a.pattern.row_pointers, a.pattern.column_indices
+    nrp, nci, nv, idx = O.drop_cross(rp, ci, a.values3d, h["jac_part"])
+    assert_array_equal(nrp, h["jac_rp"])
+    assert_array_equal(nci, h["jac_ci"])
+    assert_array_equal(idx, h["jac_idx"])
+    f = O.ilu0(nrp, nci, nv, O.plan_from_groups(O.level_groups(nrp, nci)))
+    x, rep = O.bicgstab(lambda v: O.spmv(rp, ci, a.values3d, v), lambda r: O.ilu0_apply(f, r),
+                        g.rhs.data, tol=1e-8)
+    conv, its, n0, fin = h["jac_report"]
+    assert rep.converged and rep.iterations == its
+
+
+@pytest.mark.parametrize("name", ["c1_20x20x10", "gen_6x5x4_b2", "gen_7x3x5_b1"])
+def test_generator_draw_for_draw(golden, name):
+    """paper_2309_11488_b200.synthetic.generate == bs/io.py generate, bit for bit."""
+    from paper_2309_11488_b200.synthetic import GeneratorSpec, generate
+    spec = {"c1_20x20x10": GeneratorSpec(20, 20, 10, seed=0),
+            "gen_6x5x4_b2": GeneratorSpec(6, 5, 4, block_size=2, tz=0.1, diagonal_boost=0.05, seed=31),
+            "gen_7x3x5_b1": GeneratorSpec(7, 3, 5, block_size=1, seed=5)}[name]
+    g = golden(name)
+    s = generate(spec)
+    assert_array_equal(s.a.pattern.row_pointers, g["rp"])
+    assert_array_equal(s.a.pattern.column_indices, g["ci"])
+    assert_array_equal(s.a.values, g["vals"])
+    assert_array_equal(s.rhs.data, g["rhs"])
+
+
+def test_generator_digests(golden):
+    from paper_2309_11488_b200.synthetic import GeneratorSpec, generate
+    h = golden("hand_cases")
+    for dims in ((20, 20, 10), (30, 17, 9)):
+        gg = generate(GeneratorSpec(*dims, seed=0))
+        got = np.array([gg.a.values.sum(), np.abs(gg.a.values).sum(), gg.rhs.data.sum(),
+                        float(gg.a.pattern.column_indices.sum())])
+        assert_array_equal(got, h[f"gen_{'x'.join(map(str, dims))}_sum"])
