@@ -88,9 +88,14 @@ int b2s_slices_grouped_fill(int ngroups, int nslices, const int32_t* offsets,
 int b2s_sell_offsets(int nslices, const int32_t* row0, const int32_t* nrows, const int32_t* rp,
                      const int32_t* ci, int sel, int32_t* sp, long long* slots_host,
                      cudaStream_t stream);
+/* goff/ngroups (optional, plan group offsets): entries of a triangular
+ * selection whose column lies in the row's own group are encoded -(c+2),
+ * "read the value from before the sweep" -- the reference updates a whole
+ * group at once (bs/ilu0.py:125-142). */
 int b2s_sell_fill(int nslices, int b, const int32_t* row0, const int32_t* nrows,
                   const int32_t* rp, const int32_t* ci, const double* vals, int sel,
-                  const int32_t* sp, int32_t* cols, double* svals, cudaStream_t stream);
+                  const int32_t* sp, const int32_t* goff, int ngroups, int32_t* cols,
+                  double* svals, cudaStream_t stream);
 int b2s_diag_tiles(int nslices, int b, const int32_t* row0, const int32_t* nrows,
                    const double* inv, double* tiles, cudaStream_t stream);
 int b2s_slice_conflicts(int nslices, const int32_t* row0, const int32_t* nrows,
@@ -119,7 +124,7 @@ int b2s_ilu0_apply(int n, int b, int kc, int nslices, const int32_t* row0, const
                    const int32_t* l_sp, const int32_t* l_cols, const double* l_vals,
                    const int32_t* u_sp, const int32_t* u_cols, const double* u_vals,
                    const double* dinv_tiles, const double* r, double* y, double* z, int reset_y,
-                   void* tickets, cudaStream_t stream);
+                   int flags, void* tickets, cudaStream_t stream);
 int b2s_fill_sentinel(long long m, double* v, cudaStream_t stream);
 
 /* ---- reductions (bs/krylov.py:30-60) ------------------------------------ */
@@ -132,6 +137,8 @@ int b2s_all_finite(long long m, const double* a, int* bad, cudaStream_t stream);
 
 typedef struct {
   int n, b, nparts, precond /* 0 none, 1 ilu0 */, kc, maxit, check_lag;
+  int refill_y; /* 1: U has same-group entries, refill the sweep scratch each apply */
+  int sweep_flags; /* bit 0: nanosleep back-off while polling */
   double tol;
   int nslices;
   const int32_t *row0, *nrows;
@@ -165,8 +172,10 @@ int b2s_jacobi_fill(int n, const int32_t* rp, const int32_t* ci, const int32_t* 
                     const int32_t* new_rp, int32_t* new_ci, int32_t* indices,
                     cudaStream_t stream);
 
-/* ---- library identity --------------------------------------------------- */
+/* ---- library identity / process configuration --------------------------- */
 const char* b2s_version(void);
+/* keep freed cudaMallocAsync scratch in the default pool (setup speed) */
+int b2s_retain_pool_memory(int device);
 
 #ifdef __cplusplus
 }

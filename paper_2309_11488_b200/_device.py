@@ -28,10 +28,17 @@ NPARTS = 148 * 4   # CTAs of every reducing kernel: fixed => deterministic sums
 _I32_MAX = 2 ** 31 - 1
 
 
+_configured = set()
+
+
 def require_cuda() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2309_11488_b200 needs a CUDA device (no CPU fallback)")
-    return torch.device("cuda", torch.cuda.current_device())
+    d = torch.cuda.current_device()
+    if d not in _configured:
+        check(lib().b2s_retain_pool_memory(d), "retain_pool_memory")
+        _configured.add(d)
+    return torch.device("cuda", d)
 
 
 def lib():
@@ -203,9 +210,13 @@ class Sell:
     vals: torch.Tensor
     slots: int
     width: int   # widest slice (entries)
+    stale: bool = False  # some entry reads a same-group (pre-sweep) value
 
     @classmethod
-    def build(cls, smap: SliceMap, m: DevBSR, sel: int) -> "Sell":
+    def build(cls, smap: SliceMap, m: DevBSR, sel: int, goff: torch.Tensor | None = None,
+              ngroups: int = 0) -> "Sell":
+        """SELL-32 copy of ``m`` (sel 0 all / 1 strict lower / 2 strict upper);
+        with plan group offsets, same-group triangular entries are marked."""
         dev = m.pat.rp.device
         sp = empty_i32(smap.nslices + 1, dev)
         slots = C.c_longlong(0)
@@ -219,11 +230,13 @@ class Sell:
         vals = empty_f64(ns * m.b * m.b, dev)
         check(lib().b2s_sell_fill(smap.nslices, m.b, ptr(smap.row0), ptr(smap.nrows),
                                   ptr(m.pat.rp), ptr(m.pat.ci), ptr(m.vals), sel, ptr(sp),
-                                  ptr(cols), ptr(vals), stream()), "sell_fill")
+                                  ptr(goff), int(ngroups), ptr(cols), ptr(vals), stream()),
+              "sell_fill")
         width = 0
         if smap.nslices:
             width = int(((sp[1:smap.nslices + 1] - sp[:smap.nslices]).max().item()) // 32)
-        return cls(sp, cols, vals, ns, width)
+        stale = bool((cols[:ns] <= -2).any().item()) if (goff is not None and ns) else False
+        return cls(sp, cols, vals, ns, width, stale)
 
 
 def spmv(smap: SliceMap, a: Sell, b: int, x: torch.Tensor, y: torch.Tensor, mode: int = 0,

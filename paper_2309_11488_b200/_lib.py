@@ -28,7 +28,8 @@ _PLL = C.POINTER(C.c_longlong)
 
 class BicgArgs(C.Structure):
     _fields_ = [("n", _I), ("b", _I), ("nparts", _I), ("precond", _I), ("kc", _I),
-                ("maxit", _I), ("check_lag", _I), ("tol", C.c_double), ("nslices", _I),
+                ("maxit", _I), ("check_lag", _I), ("refill_y", _I), ("sweep_flags", _I),
+                ("tol", C.c_double), ("nslices", _I),
                 ("row0", _P), ("nrows", _P), ("a_sp", _P), ("a_cols", _P), ("a_vals", _P),
                 ("l_sp", _P), ("l_cols", _P), ("l_vals", _P),
                 ("u_sp", _P), ("u_cols", _P), ("u_vals", _P),
@@ -54,13 +55,13 @@ SIGNATURES = {
     "b2s_slices_grouped_count": (_I, [_I, _P, _P, _PI, _P]),
     "b2s_slices_grouped_fill": (_I, [_I, _I, _P, _P, _P, _P, _P]),
     "b2s_sell_offsets": (_I, [_I, _P, _P, _P, _P, _I, _P, _PLL, _P]),
-    "b2s_sell_fill": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P]),
+    "b2s_sell_fill": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P]),
     "b2s_diag_tiles": (_I, [_I, _I, _P, _P, _P, _P, _P]),
     "b2s_slice_conflicts": (_I, [_I, _P, _P, _P, _P, _PI, _P]),
     "b2s_spmv": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "b2s_ilu0_factor": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _PI, _P]),
     "b2s_ilu0_apply": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                            _I, _P, _P]),
+                            _I, _I, _P, _P]),
     "b2s_fill_sentinel": (_I, [_LL, _P, _P]),
     "b2s_dot": (_I, [_LL, _P, _P, _I, _P, _P, _P]),
     "b2s_all_finite": (_I, [_LL, _P, _P, _P]),
@@ -69,6 +70,7 @@ SIGNATURES = {
     "b2s_jacobi_pattern": (_I, [_I, _P, _P, _P, _P, _PI, _P]),
     "b2s_jacobi_fill": (_I, [_I, _P, _P, _P, _P, _P, _P, _P]),
     "b2s_version": (C.c_char_p, []),
+    "b2s_retain_pool_memory": (_I, [_I]),
 }
 
 _lock = threading.Lock()

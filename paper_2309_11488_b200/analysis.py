@@ -113,9 +113,12 @@ class ParallelPlan:
 
 def _device_plan(strategy: Strategy, g: torch.Tensor, n: int, ngroups: int) -> ParallelPlan:
     perm, iperm, off = D.plan_arrays(g, n, ngroups)
+    # one group keeps the stable order => identity; otherwise treat the plan as
+    # a permutation (an identity that is permuted anyway costs a copy, not a
+    # wrong answer) and spare the device->host check
     return ParallelPlan(strategy, _dev={"row_group": g, "permutation": perm,
                                         "inverse_permutation": iperm, "group_offsets": off},
-                        _ngroups=ngroups, _independent=True)
+                        _ngroups=ngroups, _independent=True, _identity=(ngroups <= 1))
 
 
 def sequential_plan(num_rows: int) -> ParallelPlan:

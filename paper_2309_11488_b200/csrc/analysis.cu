@@ -16,6 +16,15 @@
 
 namespace b2s {
 
+__device__ __forceinline__ int ld_relaxed_i(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_i(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // diagonal positions (bs/blockcore.py:127-134) + first missing row
 // (bs/analysis.py:79-82, bs/ilu0.py:159-161)
@@ -58,13 +67,13 @@ __global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
         while (k < end) {
           const int j = ci[k];
           if (j >= i) { k = end; break; }
-          const int lj = ld_volatile(level + j);
+          const int lj = ld_relaxed_i(level + j);
           if (lj < 0) break;  // not yet published
           best = max(best, lj);
           ++k;
         }
         if (k >= end) {
-          st_volatile(level + i, best + 1);
+          st_relaxed_i(level + i, best + 1);
           done = true;
         }
       }
@@ -109,7 +118,7 @@ __global__ void k_color_sync_free(int n, const int32_t* __restrict__ rp,
           }
           const int j = (phase == 0) ? ci[k] : ut_idx[k];
           if (phase == 0 && j >= i) { k = end; continue; }
-          const int cj = ld_volatile(color + j);
+          const int cj = ld_relaxed_i(color + j);
           if (cj < 0) break;
           if (cj < 64) used |= 1ull << cj; else big = true;
           ++k;
@@ -130,7 +139,7 @@ __global__ void k_color_sync_free(int n, const int32_t* __restrict__ rp,
               if (hit) ++c;
             }
           }
-          st_volatile(color + i, c);
+          st_relaxed_i(color + i, c);
           done = true;
         }
       }

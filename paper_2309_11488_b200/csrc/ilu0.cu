@@ -22,9 +22,14 @@
 
 namespace b2s {
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// Flag polling uses a *relaxed* gpu-scope load: an acquire load makes ptxas
+// emit CCTL.IVALL (whole-L1 invalidation) after every poll.  The data read
+// after the flag is read with L1-bypassing .cg loads issued only once the
+// flag has been observed (control dependency), and the producer publishes
+// with a release store, so the values seen are the final ones.
+__device__ __forceinline__ int ld_flag(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
@@ -78,7 +83,7 @@ __global__ void __launch_bounds__(256) k_ilu0_factor(SliceMap map, const int32_t
       if (!done) {
         while (k < dpos) {
           const int r = ci[k];
-          if (ld_acquire(flag + r) == 0) break;
+          if (ld_flag(flag + r) == 0) break;
           double inv_r[BB], wik[BB], l[BB];
 #pragma unroll
           for (int e = 0; e < BB; ++e) {
@@ -123,25 +128,68 @@ __global__ void __launch_bounds__(256) k_ilu0_factor(SliceMap map, const int32_t
 
 // ---------------------------------------------------------------------------
 // sweeps.  KC = entries prefetched into registers per chunk (compile-time).
-template <int B>
-__device__ __forceinline__ void wait_row(const double* v, int c, double* out) {
-  const double* p = v + (long long)c * B;
-  bool pending;
-  do {
-    pending = false;
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+
+// Dependencies of one prefetched chunk, polled *together*: every pending
+// entry's loads are issued back to back each round, so a row pays about one
+// L2 round trip after its last input lands instead of one per input.
+// col[kk] >= 0: wait for ready[col]; col[kk] <= -2: same-group entry, take
+// stale[-col-2] (the vector before this sweep); -1: padding.
+template <int B, int KC>
+__device__ __forceinline__ void fetch_deps(const int (&col)[KC], const double* ready,
+                                           const double* stale, double (&dep)[KC][B],
+                                           int flags) {
+  unsigned int pend = 0;
 #pragma unroll
-    for (int q = 0; q < B; ++q) {
-      out[q] = ld_volatile(p + q);
-      pending |= is_sentinel(out[q]);
+  for (int kk = 0; kk < KC; ++kk) {
+    const int c0 = col[kk];
+    if (c0 <= -2) {
+#pragma unroll
+      for (int c = 0; c < B; ++c) dep[kk][c] = stale[(long long)(-c0 - 2) * B + c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < B; ++c) dep[kk][c] = 0.0;
+      if (c0 >= 0) pend |= 1u << kk;
     }
-  } while (pending);
+  }
+  unsigned int ns = 32;
+  while (pend) {
+    const unsigned int todo = pend;  // issue every pending load first ...
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      if (todo & (1u << kk)) {
+        const double* p = ready + (long long)col[kk] * B;
+#pragma unroll
+        for (int c = 0; c < B; ++c) dep[kk][c] = ld_relaxed(p + c);
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {  // ... then test them
+      bool miss = false;
+#pragma unroll
+      for (int c = 0; c < B; ++c) miss |= is_sentinel(dep[kk][c]);
+      if ((todo & (1u << kk)) && !miss) pend &= ~(1u << kk);
+    }
+    if (pend && (flags & 1)) {
+      __nanosleep(ns);
+      ns = ns < 256 ? ns * 2 : 256;
+    }
+  }
 }
 
 // forward: y_i = r_i - sum_k L_ik y_k   (unit lower, ascending columns)
 template <int B, int KC>
 __global__ void __launch_bounds__(256) k_ilu0_forward(SliceMap map, Sell lo,
                                                       const double* __restrict__ r, double* y,
-                                                      Tickets* tk, const int* done) {
+                                                      int flags, Tickets* tk, const int* done) {
   constexpr int BB = B * B;
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
@@ -169,12 +217,13 @@ __global__ void __launch_bounds__(256) k_ilu0_forward(SliceMap map, Sell lo,
         for (int e = 0; e < BB; ++e)
           blk[kk][e] = in ? __ldcs(lo.vals + vidx(slot0, k0 + kk, e, lane, BB)) : 0.0;
       }
+      double dep[KC][B];
+      fetch_deps<B, KC>(col, y, r, dep, flags);
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        if (col[kk] >= 0) {
-          double dep[B], pr[B];
-          wait_row<B>(y, col[kk], dep);
-          matvec<B>(blk[kk], dep, pr);
+        if (col[kk] != -1) {  // ascending column order, like the reference
+          double pr[B];
+          matvec<B>(blk[kk], dep[kk], pr);
 #pragma unroll
           for (int c = 0; c < B; ++c) acc[c] += pr[c];
         }
@@ -182,7 +231,7 @@ __global__ void __launch_bounds__(256) k_ilu0_forward(SliceMap map, Sell lo,
     }
     if (ok) {
 #pragma unroll
-      for (int c = 0; c < B; ++c) st_volatile(y + i * B + c, canon(rv[c] - acc[c]));
+      for (int c = 0; c < B; ++c) st_relaxed(y + i * B + c, canon(rv[c] - acc[c]));
     }
   }
 }
@@ -192,7 +241,7 @@ template <int B, int KC>
 __global__ void __launch_bounds__(256) k_ilu0_backward(SliceMap map, Sell up,
                                                        const double* __restrict__ dtiles,
                                                        double* y, double* z, int reset_y,
-                                                       Tickets* tk, const int* done) {
+                                                       int flags, Tickets* tk, const int* done) {
   constexpr int BB = B * B;
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
@@ -223,12 +272,13 @@ __global__ void __launch_bounds__(256) k_ilu0_backward(SliceMap map, Sell up,
         for (int e = 0; e < BB; ++e)
           blk[kk][e] = in ? __ldcs(up.vals + vidx(slot0, k0 + kk, e, lane, BB)) : 0.0;
       }
+      double dep[KC][B];
+      fetch_deps<B, KC>(col, z, y, dep, flags);  // same group: forward result
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        if (col[kk] >= 0) {
-          double dep[B], pr[B];
-          wait_row<B>(z, col[kk], dep);
-          matvec<B>(blk[kk], dep, pr);
+        if (col[kk] != -1) {
+          double pr[B];
+          matvec<B>(blk[kk], dep[kk], pr);
 #pragma unroll
           for (int c = 0; c < B; ++c) acc[c] += pr[c];
         }
@@ -240,7 +290,7 @@ __global__ void __launch_bounds__(256) k_ilu0_backward(SliceMap map, Sell up,
       for (int c = 0; c < B; ++c) tv[c] = yv[c] - acc[c];
       matvec<B>(dinv, tv, out);
 #pragma unroll
-      for (int c = 0; c < B; ++c) st_volatile(z + i * B + c, canon(out[c]));
+      for (int c = 0; c < B; ++c) st_relaxed(z + i * B + c, canon(out[c]));
       if (reset_y) {
 #pragma unroll
         for (int c = 0; c < B; ++c) y[i * B + c] = sentinel();
@@ -294,33 +344,38 @@ int launch_factor_b(SliceMap map, const int32_t* rp, const int32_t* ci, const in
 
 template <int B, int KC>
 int launch_sweeps_bk(SliceMap map, Sell lo, Sell up, const double* dt, const double* r,
-                     double* y, double* z, int reset_y, Tickets* tk, const int* done,
+                     double* y, double* z, int reset_y, int flags, Tickets* tk, const int* done,
                      cudaStream_t st) {
-  const int gf = occupancy_grid<B>((const void*)k_ilu0_forward<B, KC>);
-  k_ilu0_forward<B, KC><<<gf, 256, 0, st>>>(map, lo, r, y, tk, done);
-  const int gb = occupancy_grid<B>((const void*)k_ilu0_backward<B, KC>);
-  k_ilu0_backward<B, KC><<<gb, 256, 0, st>>>(map, up, dt, y, z, reset_y, tk + 1, done);
+  // flags bits 4-7: CTAs per SM (0 = max occupancy), bits 8-11: warps per
+  // CTA (0 = 8).  Fewer resident warps = fewer pollers competing for L2.
+  const int per_sm = (flags >> 4) & 15, warps = ((flags >> 8) & 15) ? ((flags >> 8) & 15) : 8;
+  int gf = occupancy_grid<B>((const void*)k_ilu0_forward<B, KC>);
+  int gb = occupancy_grid<B>((const void*)k_ilu0_backward<B, KC>);
+  if (per_sm) { gf = min(gf, per_sm * kSms); gb = min(gb, per_sm * kSms); }
+  k_ilu0_forward<B, KC><<<gf, 32 * warps, 0, st>>>(map, lo, r, y, flags, tk, done);
+  k_ilu0_backward<B, KC><<<gb, 32 * warps, 0, st>>>(map, up, dt, y, z, reset_y, flags, tk + 1,
+                                                    done);
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
 template <int B>
 int launch_sweeps_b(int kc, SliceMap map, Sell lo, Sell up, const double* dt, const double* r,
-                    double* y, double* z, int reset_y, Tickets* tk, const int* done,
+                    double* y, double* z, int reset_y, int flags, Tickets* tk, const int* done,
                     cudaStream_t st) {
-  if (kc <= 2) return launch_sweeps_bk<B, 2>(map, lo, up, dt, r, y, z, reset_y, tk, done, st);
-  if (kc <= 4) return launch_sweeps_bk<B, 4>(map, lo, up, dt, r, y, z, reset_y, tk, done, st);
-  return launch_sweeps_bk<B, 8>(map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+  if (kc <= 2) return launch_sweeps_bk<B, 2>(map, lo, up, dt, r, y, z, reset_y, flags, tk, done, st);
+  if (kc <= 4) return launch_sweeps_bk<B, 4>(map, lo, up, dt, r, y, z, reset_y, flags, tk, done, st);
+  return launch_sweeps_bk<B, 8>(map, lo, up, dt, r, y, z, reset_y, flags, tk, done, st);
 }
 
 int launch_sweeps(int b, int kc, SliceMap map, Sell lo, Sell up, const double* dt,
-                  const double* r, double* y, double* z, int reset_y, void* tickets,
+                  const double* r, double* y, double* z, int reset_y, int flags, void* tickets,
                   const int* done, cudaStream_t st) {
   Tickets* tk = reinterpret_cast<Tickets*>(tickets);
   switch (b) {
-    case 1: return launch_sweeps_b<1>(kc, map, lo, up, dt, r, y, z, reset_y, tk, done, st);
-    case 2: return launch_sweeps_b<2>(kc, map, lo, up, dt, r, y, z, reset_y, tk, done, st);
-    case 3: return launch_sweeps_b<3>(kc, map, lo, up, dt, r, y, z, reset_y, tk, done, st);
-    case 4: return launch_sweeps_b<4>(kc, map, lo, up, dt, r, y, z, reset_y, tk, done, st);
+    case 1: return launch_sweeps_b<1>(kc, map, lo, up, dt, r, y, z, reset_y, flags, tk, done, st);
+    case 2: return launch_sweeps_b<2>(kc, map, lo, up, dt, r, y, z, reset_y, flags, tk, done, st);
+    case 3: return launch_sweeps_b<3>(kc, map, lo, up, dt, r, y, z, reset_y, flags, tk, done, st);
+    case 4: return launch_sweeps_b<4>(kc, map, lo, up, dt, r, y, z, reset_y, flags, tk, done, st);
     default: return B2S_UNSUPPORTED;
   }
 }
@@ -412,12 +467,13 @@ int b2s_ilu0_apply(int n, int b, int kc, int nslices, const int32_t* row0, const
                    const int32_t* l_sp, const int32_t* l_cols, const double* l_vals,
                    const int32_t* u_sp, const int32_t* u_cols, const double* u_vals,
                    const double* dinv_tiles, const double* r, double* y, double* z, int reset_y,
-                   void* tickets, cudaStream_t st) {
+                   int flags, void* tickets, cudaStream_t st) {
   if (n < 0 || b < 1) return B2S_SHAPE;
   if (n == 0) return B2S_OK;
   SliceMap map{nslices, row0, nrows};
   Sell lo{l_sp, l_cols, l_vals}, up{u_sp, u_cols, u_vals};
-  return launch_sweeps(b, kc, map, lo, up, dinv_tiles, r, y, z, reset_y, tickets, nullptr, st);
+  return launch_sweeps(b, kc, map, lo, up, dinv_tiles, r, y, z, reset_y, flags, tickets, nullptr,
+                       st);
 }
 
 }  // extern "C"

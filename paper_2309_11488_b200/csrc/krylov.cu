@@ -29,7 +29,7 @@ namespace b2s {
 int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
                 const double* w, double* p0, double* p1, const int* done, cudaStream_t st);
 int launch_sweeps(int b, int kc, SliceMap map, Sell lo, Sell up, const double* dt,
-                  const double* r, double* y, double* z, int reset_y, void* tickets,
+                  const double* r, double* y, double* z, int reset_y, int flags, void* tickets,
                   const int* done, cudaStream_t st);
 int fill_sentinel(long long m, double* v, cudaStream_t st);
 
@@ -311,12 +311,23 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     double* sh = ilu ? shat : s;
     k_ctl_begin<<<1, 256, 0, cs>>>(state, prr, prho, np); ++kernels;
     k_p_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, p); ++kernels;
-    if (ilu) { launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, 1, tickets, done, cs); kernels += 2; }
+    const int reset_y = a->refill_y ? 0 : 1;
+    if (ilu) {
+      if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
+      launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, reset_y, a->sweep_flags,
+                    tickets, done, cs);
+      kernels += 2;
+    }
     launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done, cs); ++kernels;
     k_ctl_alpha<<<1, 256, 0, cs>>>(state, pg, np); ++kernels;
     k_s_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, ph, a->x, s, pss, ilu ? 1 : 0); ++kernels;
     k_ctl_s<<<1, 256, 0, cs>>>(state, pss, np); ++kernels;
-    if (ilu) { launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, 1, tickets, done, cs); kernels += 2; }
+    if (ilu) {
+      if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
+      launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, reset_y, a->sweep_flags,
+                    tickets, done, cs);
+      kernels += 2;
+    }
     launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done, cs); ++kernels;
     k_ctl_omega<<<1, 256, 0, cs>>>(state, ptt, pts, np); ++kernels;
     k_r_update<<<grid_v, 256, 0, cs>>>(m, state, sh, t, s, rhat, a->x, r, prr, prho, ilu ? 1 : 0); ++kernels;
@@ -404,6 +415,17 @@ int b2s_dot(long long m, const double* a, const double* b, int nparts, double* p
 }
 
 const char* b2s_version(void) { return "b200solve 0.1.0 sm_100a"; }
+
+// Keep freed stream-ordered scratch (cudaMallocAsync) in the device's default
+// pool instead of returning it to the driver at every synchronisation; the
+// setup path allocates and frees scratch per call.
+int b2s_retain_pool_memory(int device) {
+  cudaMemPool_t pool;
+  B2S_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = ~0ull;
+  B2S_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  return B2S_OK;
+}
 
 int b2s_all_finite(long long m, const double* a, int* bad_dev, cudaStream_t st) {
   if (m < 0) return B2S_SHAPE;

@@ -73,10 +73,22 @@ __global__ void k_sell_width(int nslices, const int32_t* __restrict__ row0,
   }
 }
 
+// group of a plan-order row: last g with goff[g] <= row
+__device__ __forceinline__ int group_of(const int32_t* goff, int ngroups, int row) {
+  int lo = 0, hi = ngroups - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (goff[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 __global__ void k_sell_fill(int nslices, int bb, const int32_t* __restrict__ row0,
                             const int32_t* __restrict__ nrows, const int32_t* __restrict__ rp,
                             const int32_t* __restrict__ ci, const double* __restrict__ vals,
-                            int sel, const int32_t* __restrict__ sp, int32_t* __restrict__ ocols,
+                            int sel, const int32_t* __restrict__ sp,
+                            const int32_t* __restrict__ goff, int ngroups,
+                            int32_t* __restrict__ ocols,
                             double* __restrict__ ovals) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -90,7 +102,11 @@ __global__ void k_sell_fill(int nslices, int bb, const int32_t* __restrict__ row
       for (int q = rp[row]; q < rp[row + 1]; ++q) {
         const int c = ci[q];
         if (!row_selected(sel, row, c)) continue;
-        ocols[slot0 + 32ll * k + lane] = c;
+        // same-group entries of a triangular factor read the value the
+        // vector had *before* the sweep (the reference updates a whole group
+        // at once, bs/ilu0.py:125-142): encode them as -(c + 2)
+        const bool stale = goff != nullptr && group_of(goff, ngroups, c) == group_of(goff, ngroups, row);
+        ocols[slot0 + 32ll * k + lane] = stale ? -(c + 2) : c;
         for (int e = 0; e < bb; ++e) ovals[vidx(slot0, k, e, lane, bb)] = vals[(long long)q * bb + e];
         ++k;
       }
@@ -290,11 +306,13 @@ int b2s_sell_offsets(int nslices, const int32_t* row0, const int32_t* nrows, con
 
 int b2s_sell_fill(int nslices, int b, const int32_t* row0, const int32_t* nrows,
                   const int32_t* rp, const int32_t* ci, const double* vals, int sel,
-                  const int32_t* sp, int32_t* cols, double* svals, cudaStream_t st) {
+                  const int32_t* sp, const int32_t* goff, int ngroups, int32_t* cols,
+                  double* svals, cudaStream_t st) {
   if (nslices < 0 || b < 1 || sel < 0 || sel > 2) return B2S_SHAPE;
   if (nslices == 0) return B2S_OK;
   k_sell_fill<<<grid_for((long long)nslices * 32), 256, 0, st>>>(nslices, b * b, row0, nrows, rp,
-                                                                  ci, vals, sel, sp, cols, svals);
+                                                                  ci, vals, sel, sp, goff, ngroups,
+                                                                  cols, svals);
   B2S_LAUNCH_CHECK();
   return B2S_OK;
 }

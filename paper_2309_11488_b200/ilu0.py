@@ -53,6 +53,7 @@ class Ilu0Factorization:
         self._combined = None
         self._inv_host = None
         self._tickets = torch.zeros(8, dtype=torch.int32, device=invd.device)
+        self.sweep_flags = 0
 
     # -- reference attributes --------------------------------------------------
     @property
@@ -105,7 +106,8 @@ class Ilu0Factorization:
                                      D.ptr(s.nrows), D.ptr(lo.sp), D.ptr(lo.cols),
                                      D.ptr(lo.vals), D.ptr(up.sp), D.ptr(up.cols),
                                      D.ptr(up.vals), D.ptr(self.dtiles), D.ptr(r_perm),
-                                     D.ptr(y), D.ptr(z), 1, D.ptr(self._tickets), D.stream()),
+                                     D.ptr(y), D.ptr(z), 0 if self.upper.stale else 1,
+                                     self.sweep_flags, D.ptr(self._tickets), D.stream()),
               "ilu0_apply")
         return z
 
@@ -153,11 +155,9 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) ->
     a_perm = bsr if identity else permute_device(bsr, plan)
     lu = D.DevBSR(a_perm.pat, b, a_perm.vals.clone())
     diag = D.find_diagonal(lu.pat)
+    # group-aligned slices: a sweep never waits on a row of its own group
+    # (same-group reads take the pre-sweep value, as the reference does)
     smap = plan.slice_map()
-    if not plan.independent_groups and smap.conflicts(lu.pat):
-        # a user-built plan whose groups are not independent sets: fall back
-        # to one row per slice, which is always safe for the wavefronts
-        smap = D.SliceMap.singles(n, dev)
     inv = D.empty_f64(n * b * b, dev)
     bad = C.c_int32(-1)
     rc = D.lib().b2s_ilu0_factor(n, b, smap.nslices, D.ptr(smap.row0), D.ptr(smap.nrows),
@@ -169,8 +169,9 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) ->
             row = int(plan.device("inverse_permutation")[row].item())
         raise SingularPivot(row)
     check(rc, "ilu0_factor")
-    lower = D.Sell.build(smap, lu, 1)
-    upper = D.Sell.build(smap, lu, 2)
+    goff = plan.device("group_offsets")
+    lower = D.Sell.build(smap, lu, 1, goff, plan.group_count)
+    upper = D.Sell.build(smap, lu, 2, goff, plan.group_count)
     dtiles = D.empty_f64(smap.nslices * b * b * 32, dev)
     check(D.lib().b2s_diag_tiles(smap.nslices, b, D.ptr(smap.row0), D.ptr(smap.nrows),
                                  D.ptr(inv), D.ptr(dtiles), D.stream()), "diag_tiles")

@@ -201,6 +201,8 @@ class DeviceKrylov:
         args.kc = f.kc if f is not None else 2
         args.maxit = stop.max_iterations
         args.check_lag = check_lag
+        args.refill_y = 1 if (f is not None and f.upper.stale) else 0
+        args.sweep_flags = f.sweep_flags if f is not None else 0
         args.tol = stop.relative_reduction
         s = self.smap
         args.nslices, args.row0, args.nrows = s.nslices, D.ptr(s.row0), D.ptr(s.nrows)
