@@ -33,7 +33,8 @@ class BicgArgs(C.Structure):
                 ("row0", _P), ("nrows", _P), ("a_sp", _P), ("a_cols", _P), ("a_vals", _P),
                 ("l_sp", _P), ("l_cols", _P), ("l_vals", _P),
                 ("u_sp", _P), ("u_cols", _P), ("u_vals", _P),
-                ("dinv_tiles", _P), ("rhs", _P), ("x", _P), ("work", _P), ("stream", _P)]
+                ("dinv_tiles", _P), ("tiles", _P), ("rhs", _P), ("x", _P), ("work", _P),
+                ("stream", _P)]
 
 
 class BicgResult(C.Structure):
@@ -63,6 +64,11 @@ SIGNATURES = {
     "b2s_ilu0_apply": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                             _I, _I, _P, _P]),
     "b2s_fill_sentinel": (_I, [_LL, _P, _P]),
+    "b2s_tiles_smem_bytes": (_LL, [_I, _I]),
+    "b2s_tiles_create": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, C.POINTER(C.c_void_p),
+                              _P]),
+    "b2s_tiles_destroy": (_I, [_P]),
+    "b2s_tiles_apply": (_I, [_I, _P, _P, _P, _P, _I, _P]),
     "b2s_dot": (_I, [_LL, _P, _P, _I, _P, _P, _P]),
     "b2s_all_finite": (_I, [_LL, _P, _P, _P]),
     "b2s_bicgstab_workspace_bytes": (_LL, [_I, _I, _I]),

@@ -1,0 +1,250 @@
+// Block ILU0 factorisation (bs/ilu0.py:145-201) as a sync-free wavefront.
+//
+// Phase 1, symbolic (value independent): for every strict-lower slot k of
+// permuted row i (column r) list the update pairs (p, q) -- slot p of row i
+// and slot q of row r with equal columns j > r.  These are exactly the
+// targets of the reference's `A_ij -= L_ir A_rj` (the searchsorted merge of
+// bs/ilu0.py:183-195), precomputed so that the numeric phase has nothing
+// but value loads left on its critical path.  On a 7-point stencil every
+// list holds one pair (the diagonal).
+//
+// Phase 2, numeric: rows are claimed slice by slice in plan order through an
+// atomic ticket; a row processes its lower slots in ascending column order
+// (the reference's order), waiting on a per-row "finished" flag for each
+// pivot row r, then L_ir = A_ir inv(U_rr), A_ip -= L_ir A_rq over its pairs,
+// and finally inv(A_ii) with the reference's singularity rule.  A warp keeps
+// polling while any of its lanes still waits, so lanes of one slice may even
+// depend on each other (user-built plans) without deadlock.
+#include <cub/cub.cuh>
+
+#include "sell.cuh"
+
+namespace b2s {
+
+struct Tickets2 {
+  unsigned int next, finished;
+};
+
+__device__ __forceinline__ long long claim_slice(Tickets2* tk, int nslices) {
+  const int lane = threadIdx.x & 31;
+  unsigned int t = 0;
+  if (lane == 0) t = atomicAdd(&tk->next, 1u);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t < (unsigned)nslices) return t;
+  if (lane == 0) {
+    const unsigned int total = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(&tk->finished, 1u) == total - 1) {
+      tk->next = 0;
+      tk->finished = 0;
+      __threadfence();
+    }
+  }
+  return -1;
+}
+
+__device__ __forceinline__ int ld_flag_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_flag_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---- symbolic phase: count (pairs == nullptr) or fill the update pairs
+__global__ void k_factor_pairs(int n, const int32_t* __restrict__ rp,
+                               const int32_t* __restrict__ ci, const int32_t* __restrict__ diag,
+                               int32_t* __restrict__ cnt, const int32_t* __restrict__ ptr,
+                               int2* __restrict__ pairs) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int end = rp[i + 1];
+    for (int k = rp[i]; k < diag[i]; ++k) {
+      const int r = ci[k];
+      int m = 0, p = k + 1;
+      const int out = pairs ? ptr[k] : 0;
+      const int rend = rp[r + 1];
+      for (int q = diag[r] + 1; q < rend && p < end; ++q) {
+        const int j = ci[q];
+        while (p < end && ci[p] < j) ++p;
+        if (p < end && ci[p] == j) {
+          if (pairs) pairs[out + m] = make_int2(p, q);
+          ++m;
+        }
+      }
+      if (!pairs) cnt[k] = m;
+    }
+  }
+}
+
+// ---- numeric phase
+template <int B>
+__global__ void __launch_bounds__(256) k_factor_numeric(
+    SliceMap map, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+    const int32_t* __restrict__ diag, const int32_t* __restrict__ pptr,
+    const int2* __restrict__ pairs, double* w, double* invd, int* flag, int* bad, Tickets2* tk) {
+  constexpr int BB = B * B;
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const long long s = claim_slice(tk, map.nslices);
+    if (s < 0) break;
+    const int i = map.row0[s] + lane;
+    bool done = lane >= map.nrows[s];
+    int k = 0, dpos = 0;
+    int r = -1, pb = 0, pe = 0;
+    int2 pq0 = make_int2(0, 0);
+    if (!done) {
+      k = rp[i];
+      dpos = diag[i];
+      if (k < dpos) {  // static data of the first pivot: off the critical path
+        r = ci[k]; pb = pptr[k]; pe = pptr[k + 1];
+        if (pb < pe) pq0 = pairs[pb];
+      }
+    }
+    for (;;) {
+      if (!done) {
+        while (k < dpos) {
+          if (ld_flag_relaxed(flag + r) == 0) break;
+          // every value load of this pivot step is independent: one round trip
+          double inv_r[BB], wik[BB], urq[BB], wip[BB], l[BB], prod[BB];
+#pragma unroll
+          for (int e = 0; e < BB; ++e) {
+            inv_r[e] = __ldcg(invd + (long long)r * BB + e);
+            wik[e] = w[(long long)k * BB + e];
+          }
+          if (pb < pe) {
+#pragma unroll
+            for (int e = 0; e < BB; ++e) {
+              urq[e] = __ldcg(w + (long long)pq0.y * BB + e);
+              wip[e] = w[(long long)pq0.x * BB + e];
+            }
+          }
+          matmul<B>(wik, inv_r, l);  // L_ir = A_ir inv(U_rr)
+#pragma unroll
+          for (int e = 0; e < BB; ++e) w[(long long)k * BB + e] = l[e];
+          if (pb < pe) {
+            matmul<B>(l, urq, prod);  // A_ip -= L_ir U_rq
+#pragma unroll
+            for (int e = 0; e < BB; ++e) w[(long long)pq0.x * BB + e] = wip[e] - prod[e];
+            for (int t = pb + 1; t < pe; ++t) {  // further pairs (not on stencils)
+              const int2 pq = pairs[t];
+#pragma unroll
+              for (int e = 0; e < BB; ++e) urq[e] = __ldcg(w + (long long)pq.y * BB + e);
+              matmul<B>(l, urq, prod);
+#pragma unroll
+              for (int e = 0; e < BB; ++e) w[(long long)pq.x * BB + e] -= prod[e];
+            }
+          }
+          ++k;
+          if (k < dpos) {
+            r = ci[k]; pb = pptr[k]; pe = pptr[k + 1];
+            if (pb < pe) pq0 = pairs[pb];
+          }
+        }
+        if (k >= dpos) {
+          double dblk[BB], inv[BB];
+#pragma unroll
+          for (int e = 0; e < BB; ++e) dblk[e] = w[(long long)dpos * BB + e];
+          if (!invert_block<B>(dblk, inv)) atomicMin(bad, i);
+#pragma unroll
+          for (int e = 0; e < BB; ++e) invd[(long long)i * BB + e] = inv[e];
+          st_flag_release(flag + i, 1);  // publishes this row's L, U and inverse
+          done = true;
+        }
+      }
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+  }
+}
+
+template <int B>
+int launch_numeric(SliceMap map, const int32_t* rp, const int32_t* ci, const int32_t* diag,
+                   const int32_t* pptr, const int2* pairs, double* w, double* invd, int* flag,
+                   int* bad, Tickets2* tk, cudaStream_t st) {
+  int per_sm = 0, dev = 0, sms = kSms;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_factor_numeric<B>, 256, 0);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int g = (per_sm < 1 ? 1 : per_sm) * sms;
+  k_factor_numeric<B><<<g, 256, 0, st>>>(map, rp, ci, diag, pptr, pairs, w, invd, flag, bad, tk);
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
+inline int grid_rows(long long work) {
+  long long g = (work + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > kSms * 16) g = kSms * 16;
+  return (int)g;
+}
+
+}  // namespace b2s
+
+using namespace b2s;
+
+extern "C" {
+
+// Factor the permuted block-CSR matrix in place (values become combined
+// L\U) and write the inverse diagonal blocks (row-major, n*b*b).  The slice
+// map gives the claim order (plan order); on a singular pivot the smallest
+// failing *permuted* row goes to bad_row_host (B2S_SINGULAR_PIVOT).
+int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_t* nrows,
+                    const int32_t* rp, const int32_t* ci, const int32_t* diag, double* vals,
+                    double* inv_diag, int32_t* bad_row_host, cudaStream_t st) {
+  *bad_row_host = -1;
+  if (n < 0 || b < 1) return B2S_SHAPE;
+  if (n == 0) return B2S_OK;
+  if (b > 4) return B2S_UNSUPPORTED;
+  int32_t nnz = 0;
+  B2S_CHECK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  int32_t *cnt = nullptr, *pptr = nullptr;
+  int* flag = nullptr;
+  int* bad = nullptr;
+  Tickets2* tk = nullptr;
+  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (nnz + 1), st));
+  B2S_CHECK(cudaMallocAsync(&pptr, sizeof(int32_t) * (nnz + 1), st));
+  B2S_CHECK(cudaMallocAsync(&flag, sizeof(int) * n, st));
+  B2S_CHECK(cudaMallocAsync(&bad, sizeof(int), st));
+  B2S_CHECK(cudaMallocAsync(&tk, sizeof(Tickets2), st));
+  B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nnz + 1), st));
+  B2S_CHECK(cudaMemsetAsync(flag, 0, sizeof(int) * n, st));
+  B2S_CHECK(cudaMemsetAsync(tk, 0, sizeof(Tickets2), st));
+  const int big = 0x7fffffff;
+  B2S_CHECK(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  // symbolic: count, scan, fill
+  k_factor_pairs<<<grid_rows(n), 256, 0, st>>>(n, rp, ci, diag, cnt, nullptr, nullptr);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, pptr, nnz + 1, st);
+  void* tmp = nullptr;
+  B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pptr, nnz + 1, st);
+  int32_t npairs = 0;
+  B2S_CHECK(cudaMemcpyAsync(&npairs, pptr + nnz, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  int2* pairs = nullptr;
+  B2S_CHECK(cudaMallocAsync(&pairs, sizeof(int2) * (npairs > 0 ? npairs : 1), st));
+  k_factor_pairs<<<grid_rows(n), 256, 0, st>>>(n, rp, ci, diag, nullptr, pptr, pairs);
+  B2S_LAUNCH_CHECK();
+  SliceMap map{nslices, row0, nrows};
+  int rc;
+  switch (b) {
+    case 1: rc = launch_numeric<1>(map, rp, ci, diag, pptr, pairs, vals, inv_diag, flag, bad, tk, st); break;
+    case 2: rc = launch_numeric<2>(map, rp, ci, diag, pptr, pairs, vals, inv_diag, flag, bad, tk, st); break;
+    case 3: rc = launch_numeric<3>(map, rp, ci, diag, pptr, pairs, vals, inv_diag, flag, bad, tk, st); break;
+    default: rc = launch_numeric<4>(map, rp, ci, diag, pptr, pairs, vals, inv_diag, flag, bad, tk, st); break;
+  }
+  if (rc != B2S_OK) return rc;
+  int h = big;
+  B2S_CHECK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(tmp, st));
+  B2S_CHECK(cudaFreeAsync(pairs, st));
+  B2S_CHECK(cudaFreeAsync(cnt, st));
+  B2S_CHECK(cudaFreeAsync(pptr, st));
+  B2S_CHECK(cudaFreeAsync(flag, st));
+  B2S_CHECK(cudaFreeAsync(bad, st));
+  B2S_CHECK(cudaFreeAsync(tk, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  if (h != big) { *bad_row_host = h; return B2S_SINGULAR_PIVOT; }
+  return B2S_OK;
+}
+
+}  // extern "C"

@@ -1,5 +1,5 @@
-// Zero-fill block ILU0: factorisation (bs/ilu0.py:145-201) and its
-// two-phase application (bs/ilu0.py:93-142), both as sync-free wavefronts.
+// Zero-fill block ILU0 application (bs/ilu0.py:93-142): the forward and
+// backward block-triangular sweeps as sync-free wavefronts.
 //
 // Rows are processed in plan (permuted) order.  A warp claims the next
 // group-aligned slice of <= 32 rows through an atomic ticket (ascending for
@@ -10,8 +10,7 @@
 // only for the rows it actually reads, so independent parts of consecutive
 // levels overlap, and the critical path costs one L2 round trip per level.
 //
-//  * factorisation: per-row "finished" flags (acquire/release), general
-//    IKJ elimination exactly as the reference orders it;
+//  * factorisation: see factor.cu;
 //  * sweeps: the dependency vector itself is the flag -- it is pre-filled
 //    with a NaN sentinel and a consumer spins until the producer's value
 //    replaces it (one round trip, no separate flag + fence).  The backward
@@ -21,20 +20,6 @@
 #include "sell.cuh"
 
 namespace b2s {
-
-// Flag polling uses a *relaxed* gpu-scope load: an acquire load makes ptxas
-// emit CCTL.IVALL (whole-L1 invalidation) after every poll.  The data read
-// after the flag is read with L1-bypassing .cg loads issued only once the
-// flag has been observed (control dependency), and the producer publishes
-// with a release store, so the values seen are the final ones.
-__device__ __forceinline__ int ld_flag(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 struct Tickets {
   unsigned int next;      // next slice ticket
@@ -60,70 +45,6 @@ __device__ __forceinline__ long long claim(Tickets* tk, int nslices) {
     }
   }
   return -1;
-}
-
-// ---------------------------------------------------------------------------
-// factorisation, in place on the permuted block-CSR values
-template <int B>
-__global__ void __launch_bounds__(256) k_ilu0_factor(SliceMap map, const int32_t* __restrict__ rp,
-                                                     const int32_t* __restrict__ ci,
-                                                     const int32_t* __restrict__ diag, double* w,
-                                                     double* invd, int* flag, int* bad,
-                                                     Tickets* tk) {
-  constexpr int BB = B * B;
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    const long long s = claim(tk, map.nslices);
-    if (s < 0) break;
-    const int i = map.row0[s] + lane;
-    bool done = lane >= map.nrows[s];
-    int k = 0, dpos = 0, end = 0;
-    if (!done) { k = rp[i]; dpos = diag[i]; end = rp[i + 1]; }
-    for (;;) {
-      if (!done) {
-        while (k < dpos) {
-          const int r = ci[k];
-          if (ld_flag(flag + r) == 0) break;
-          double inv_r[BB], wik[BB], l[BB];
-#pragma unroll
-          for (int e = 0; e < BB; ++e) {
-            inv_r[e] = __ldcg(invd + (long long)r * BB + e);
-            wik[e] = w[(long long)k * BB + e];
-          }
-          matmul<B>(wik, inv_r, l);  // L_ir = A_ir inv(U_rr)
-#pragma unroll
-          for (int e = 0; e < BB; ++e) w[(long long)k * BB + e] = l[e];
-          // A_ij -= L_ir U_rj for every j > r stored in both rows
-          int p = k + 1;
-          const int rend = rp[r + 1];
-          for (int q = diag[r] + 1; q < rend && p < end; ++q) {
-            const int j = ci[q];
-            while (p < end && ci[p] < j) ++p;
-            if (p < end && ci[p] == j) {
-              double urj[BB], prod[BB];
-#pragma unroll
-              for (int e = 0; e < BB; ++e) urj[e] = __ldcg(w + (long long)q * BB + e);
-              matmul<B>(l, urj, prod);
-#pragma unroll
-              for (int e = 0; e < BB; ++e) w[(long long)p * BB + e] -= prod[e];
-            }
-          }
-          ++k;
-        }
-        if (k >= dpos) {
-          double dblk[BB], inv[BB];
-#pragma unroll
-          for (int e = 0; e < BB; ++e) dblk[e] = w[(long long)dpos * BB + e];
-          if (!invert_block<B>(dblk, inv)) atomicMin(bad, i);
-#pragma unroll
-          for (int e = 0; e < BB; ++e) invd[(long long)i * BB + e] = inv[e];
-          st_release(flag + i, 1);  // orders this row's stores before the flag
-          done = true;
-        }
-      }
-      if (__all_sync(0xffffffffu, done)) break;
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -334,14 +255,6 @@ int occupancy_grid(const void* fn) {
   return per_sm * sms;
 }
 
-template <int B>
-int launch_factor_b(SliceMap map, const int32_t* rp, const int32_t* ci, const int32_t* diag,
-                    double* w, double* invd, int* flag, int* bad, Tickets* tk, cudaStream_t st) {
-  const int g = occupancy_grid<B>((const void*)k_ilu0_factor<B>);
-  k_ilu0_factor<B><<<g, 256, 0, st>>>(map, rp, ci, diag, w, invd, flag, bad, tk);
-  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
-}
-
 template <int B, int KC>
 int launch_sweeps_bk(SliceMap map, Sell lo, Sell up, const double* dt, const double* r,
                      double* y, double* z, int reset_y, int flags, Tickets* tk, const int* done,
@@ -393,46 +306,6 @@ int fill_sentinel(long long m, double* v, cudaStream_t st) {
 using namespace b2s;
 
 extern "C" {
-
-// Factor the permuted block-CSR matrix in place (values become combined
-// L\U) and write the inverse diagonal blocks (row-major, n*b*b).  The slice
-// map must follow the plan's groups (rows of one slice independent).  On a
-// singular pivot the smallest failing *permuted* row goes to bad_row_host.
-int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_t* nrows,
-                    const int32_t* rp, const int32_t* ci, const int32_t* diag, double* vals,
-                    double* inv_diag, int32_t* bad_row_host, cudaStream_t st) {
-  *bad_row_host = -1;
-  if (n < 0 || b < 1) return B2S_SHAPE;
-  if (n == 0) return B2S_OK;
-  if (b > 4) return B2S_UNSUPPORTED;
-  int* flag = nullptr;
-  int* bad = nullptr;
-  Tickets* tk = nullptr;
-  B2S_CHECK(cudaMallocAsync(&flag, sizeof(int) * n, st));
-  B2S_CHECK(cudaMallocAsync(&bad, sizeof(int), st));
-  B2S_CHECK(cudaMallocAsync(&tk, sizeof(Tickets), st));
-  B2S_CHECK(cudaMemsetAsync(flag, 0, sizeof(int) * n, st));
-  B2S_CHECK(cudaMemsetAsync(tk, 0, sizeof(Tickets), st));
-  const int big = 0x7fffffff;
-  B2S_CHECK(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-  SliceMap map{nslices, row0, nrows};
-  int rc;
-  switch (b) {
-    case 1: rc = launch_factor_b<1>(map, rp, ci, diag, vals, inv_diag, flag, bad, tk, st); break;
-    case 2: rc = launch_factor_b<2>(map, rp, ci, diag, vals, inv_diag, flag, bad, tk, st); break;
-    case 3: rc = launch_factor_b<3>(map, rp, ci, diag, vals, inv_diag, flag, bad, tk, st); break;
-    default: rc = launch_factor_b<4>(map, rp, ci, diag, vals, inv_diag, flag, bad, tk, st); break;
-  }
-  if (rc != B2S_OK) return rc;
-  int h = big;
-  B2S_CHECK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-  B2S_CHECK(cudaFreeAsync(flag, st));
-  B2S_CHECK(cudaFreeAsync(bad, st));
-  B2S_CHECK(cudaFreeAsync(tk, st));
-  B2S_CHECK(cudaStreamSynchronize(st));
-  if (h != big) { *bad_row_host = h; return B2S_SINGULAR_PIVOT; }
-  return B2S_OK;
-}
 
 // 1 in *conflict_host if some row of the slice map reads a row of its own
 // slice through its strict-lower part (the plan's groups are not

@@ -32,6 +32,8 @@ int launch_sweeps(int b, int kc, SliceMap map, Sell lo, Sell up, const double* d
                   const double* r, double* y, double* z, int reset_y, int flags, void* tickets,
                   const int* done, cudaStream_t st);
 int fill_sentinel(long long m, double* v, cudaStream_t st);
+int launch_tiled(int b, const void* handle, const double* r, double* y, double* z, int reset_y,
+                 const int* done, cudaStream_t st);
 
 constexpr double kBreakdown = 1e-60;  // bs/krylov.py:27
 
@@ -314,8 +316,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     const int reset_y = a->refill_y ? 0 : 1;
     if (ilu) {
       if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
-      launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, reset_y, a->sweep_flags,
-                    tickets, done, cs);
+      if (a->tiles) launch_tiled(a->b, a->tiles, p, y, phat, reset_y, done, cs);
+      else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, reset_y, a->sweep_flags,
+                         tickets, done, cs);
       kernels += 2;
     }
     launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done, cs); ++kernels;
@@ -324,8 +327,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     k_ctl_s<<<1, 256, 0, cs>>>(state, pss, np); ++kernels;
     if (ilu) {
       if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
-      launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, reset_y, a->sweep_flags,
-                    tickets, done, cs);
+      if (a->tiles) launch_tiled(a->b, a->tiles, s, y, shat, reset_y, done, cs);
+      else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, reset_y, a->sweep_flags,
+                         tickets, done, cs);
       kernels += 2;
     }
     launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done, cs); ++kernels;

@@ -15,6 +15,7 @@ attributes (``combined``, ``inverted_diagonals``) are materialised lazily.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -54,6 +55,7 @@ class Ilu0Factorization:
         self._inv_host = None
         self._tickets = torch.zeros(8, dtype=torch.int32, device=invd.device)
         self.sweep_flags = 0
+        self.tiles = None        # b2s_tiles_create handle (tiled level sweeps), or None
 
     # -- reference attributes --------------------------------------------------
     @property
@@ -100,6 +102,11 @@ class Ilu0Factorization:
             return z
         D.fill_sentinel(y, m)
         D.fill_sentinel(z, m)
+        if self.tiles:
+            check(D.lib().b2s_tiles_apply(self._b, self.tiles, D.ptr(r_perm), D.ptr(y), D.ptr(z),
+                                          0 if self.upper.stale else 1, D.stream()),
+                  "tiles_apply")
+            return z
         s = self.smap
         lo, up = self.lower, self.upper
         check(D.lib().b2s_ilu0_apply(self._n, self._b, self.kc, s.nslices, D.ptr(s.row0),
@@ -140,6 +147,14 @@ class Ilu0Factorization:
     def __call__(self, r: np.ndarray) -> np.ndarray:
         return self.apply_array(r)
 
+    def __del__(self):
+        if getattr(self, "tiles", None):
+            try:
+                D.lib().b2s_tiles_destroy(self.tiles)
+            except Exception:
+                pass
+            self.tiles = None
+
 
 def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) -> Ilu0Factorization:
     """``decompose`` on an (optionally pre-uploaded) matrix."""
@@ -175,8 +190,33 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) ->
     dtiles = D.empty_f64(smap.nslices * b * b * 32, dev)
     check(D.lib().b2s_diag_tiles(smap.nslices, b, D.ptr(smap.row0), D.ptr(smap.nrows),
                                  D.ptr(inv), D.ptr(dtiles), D.stream()), "diag_tiles")
-    return Ilu0Factorization(plan, b, n, lu, inv, smap, lower, upper, dtiles, identity, a,
-                             a_perm)
+    f = Ilu0Factorization(plan, b, n, lu, inv, smap, lower, upper, dtiles, identity, a, a_perm)
+    _maybe_tiles(f, plan, diag)
+    return f
+
+
+def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
+    """Deep level schedules are latency-bound in the sync-free sweeps; give
+    them the tiled kernels (csrc/tiles.cu) when a tile fits in an SM.
+    B2S_TILES=0 disables, B2S_TILES_T sets the tile count."""
+    if os.environ.get("B2S_TILES", "1") == "0":
+        return
+    n = f.num_block_rows
+    sms = torch.cuda.get_device_properties(diag.device).multi_processor_count
+    T = int(os.environ.get("B2S_TILES_T", sms))
+    min_rows = int(os.environ.get("B2S_TILES_MIN_ROWS", 64))     # per tile
+    if plan.group_count < int(os.environ.get("B2S_TILES_MIN_GROUPS", 32)) or n < min_rows * T:
+        return
+    h = C.c_void_p(None)
+    rc = D.lib().b2s_tiles_create(n, f._b, T, D.ptr(plan.device("inverse_permutation")),
+                                  D.ptr(f._lu.pat.rp), D.ptr(f._lu.pat.ci), D.ptr(diag),
+                                  D.ptr(f._lu.vals), D.ptr(f._invd),
+                                  D.ptr(plan.device("group_offsets")), plan.group_count,
+                                  C.byref(h), D.stream())
+    if rc == 5:   # B2S_UNSUPPORTED: a tile does not fit, keep the sync-free sweeps
+        return
+    check(rc, "tiles_create")
+    f.tiles = h.value
 
 
 def decompose(a: BlockMatrix, plan: ParallelPlan) -> Ilu0Factorization:

@@ -213,6 +213,7 @@ class DeviceKrylov:
             args.u_sp, args.u_cols, args.u_vals = (D.ptr(f.upper.sp), D.ptr(f.upper.cols),
                                                    D.ptr(f.upper.vals))
             args.dinv_tiles = D.ptr(f.dtiles)
+            args.tiles = f.tiles
         args.rhs, args.x, args.work = D.ptr(rhs), D.ptr(x), D.ptr(self.work)
         args.stream = D.stream()
         res = BicgResult()

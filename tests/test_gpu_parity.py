@@ -296,3 +296,43 @@ def test_block_jacobi_copy_plan(golden):
     x, rep = P.bicgstab(P.MatrixOperator(g.a), f, g.rhs, stop=P.StoppingCriteria(1e-8, 200))
     conv, its, n0, fin = h["jac_report"]
     assert rep.converged and rep.iterations == its
+
+
+@pytest.mark.parametrize("T", [4, 8, 13])
+def test_tiled_sweeps_bit_equal_to_sync_free(monkeypatch, golden, T):
+    """The tiled level sweeps (csrc/tiles.cu) give bit-identical results to the
+    sync-free sweeps and the same solve."""
+    g = golden("c1_20x20x10")
+    a = matrix(g)
+    plan = P.level_schedule(a.pattern)
+    monkeypatch.setenv("B2S_TILES", "0")
+    f0 = P.decompose(a, plan)
+    monkeypatch.setenv("B2S_TILES", "1")
+    monkeypatch.setenv("B2S_TILES_T", str(T))
+    f1 = P.decompose(a, plan)
+    assert f1.tiles and not f0.tiles
+    r = P.BlockVector(g["x"], 3)
+    assert_array_equal(f1.apply(r).data, f0.apply(r).data)
+    close(f1.apply(r).data, g["level_apply"], 1e-12)
+    x0, r0 = P.bicgstab(P.MatrixOperator(a), f0, P.BlockVector(g["rhs"], 3),
+                        stop=P.StoppingCriteria(1e-8, 200))
+    x1, r1 = P.bicgstab(P.MatrixOperator(a), f1, P.BlockVector(g["rhs"], 3),
+                        stop=P.StoppingCriteria(1e-8, 200))
+    assert r0.iterations == r1.iterations
+    assert_array_equal(x0.data, x1.data)
+
+
+def test_tiled_sweeps_nonsymmetric_same_group(monkeypatch, golden):
+    """Random non-symmetric patterns (same-group upper entries) through the tiles."""
+    g = golden("random_patterns")
+    monkeypatch.setenv("B2S_TILES_T", "3")
+    monkeypatch.setenv("B2S_TILES_MIN_GROUPS", "1")
+    monkeypatch.setenv("B2S_TILES_MIN_ROWS", "1")
+    for t in range(12):
+        e = {k[len(f"r{t}_"):]: v for k, v in g.items() if k.startswith(f"r{t}_")}
+        a = matrix(e)
+        f = P.decompose(a, P.level_schedule(a.pattern))
+        assert f.tiles
+        z = f.apply(P.BlockVector(e["x"], a.block_size)).data
+        ref = e["level_apply"]
+        assert np.linalg.norm(z - ref) <= 1e-11 * np.linalg.norm(ref)
