@@ -127,14 +127,15 @@ int b2s_ilu0_apply(int n, int b, int kc, int nslices, const int32_t* row0, const
                    int flags, void* tickets, cudaStream_t stream);
 int b2s_fill_sentinel(long long m, double* v, cudaStream_t stream);
 
-/* Tiled level-scheduled sweeps (csrc/tiles.cu): T tiles = contiguous input
- * row ranges, one co-resident CTA each, tile values in shared memory, TMA-
- * streamed records.  B2S_UNSUPPORTED when a tile does not fit on an SM. */
+/* Tiled level-scheduled sweeps (csrc/tiles.cu): px*py column patches of an
+ * nx x ny natural-order grid (px > 0) or T contiguous input-row ranges; one
+ * co-resident CTA per tile, tile values in shared memory.  kc = max entries
+ * per row of L/U.  B2S_UNSUPPORTED when a tile does not fit on an SM. */
 long long b2s_tiles_smem_bytes(int b, int rmax);
-int b2s_tiles_create(int n, int b, int T, const int32_t* iperm, const int32_t* rp,
-                     const int32_t* ci, const int32_t* diag, const double* lu,
-                     const double* inv, const int32_t* goff, int ngroups, void** handle_out,
-                     cudaStream_t stream);
+int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const int32_t* iperm,
+                     const int32_t* rp, const int32_t* ci, const int32_t* diag, const double* lu,
+                     const double* inv, const int32_t* goff, int ngroups, int kc,
+                     void** handle_out, cudaStream_t stream);
 int b2s_tiles_destroy(void* handle);
 int b2s_tiles_apply(int b, const void* handle, const double* r, double* y, double* z,
                     int reset_y, cudaStream_t stream);

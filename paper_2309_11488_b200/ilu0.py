@@ -195,6 +195,39 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) ->
     return f
 
 
+def grid_shape(a: BlockMatrix):
+    """(nx, ny, nz) if ``a`` looks like a natural-order 3D 7-point grid (all
+    off-diagonal couplings at offsets 1, nx, nx*ny), else None.  Only used to
+    shape the sweep tiles; results never depend on it."""
+    p = a.pattern
+    n = p.num_block_rows
+    m = min(n, 65536)
+    if m < 8:
+        return None
+    end = int(p.row_pointers[m])
+    rows = np.repeat(np.arange(m, dtype=np.int64), np.diff(p.row_pointers[: m + 1]))
+    off = np.abs(p.column_indices[:end] - rows)
+    u = np.unique(off[off > 0])
+    if len(u) != 3 or u[0] != 1 or u[2] % u[1] or n % u[2]:
+        return None
+    nx, nxy = int(u[1]), int(u[2])
+    return nx, nxy // nx, n // nxy
+
+
+def _patches(nx: int, ny: int, tiles: int):
+    """px x py <= tiles column patches, as square as the grid allows."""
+    cands = []
+    for px in range(1, min(nx, tiles) + 1):
+        py = min(ny, tiles // px)
+        if py >= 1:
+            cands.append((px * py, abs(nx / px - ny / py), px, py))
+    most = max(c[0] for c in cands)
+    # near-maximal tile count, then the squarest patches (fewest boundary rows)
+    ok = [c for c in cands if c[0] >= 0.9 * most]
+    _, _, px, py = min(ok, key=lambda c: (c[1], -c[0]))
+    return px, py
+
+
 def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
     """Deep level schedules are latency-bound in the sync-free sweeps; give
     them the tiled kernels (csrc/tiles.cu) when a tile fits in an SM.
@@ -207,16 +240,23 @@ def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
     min_rows = int(os.environ.get("B2S_TILES_MIN_ROWS", 64))     # per tile
     if plan.group_count < int(os.environ.get("B2S_TILES_MIN_GROUPS", 32)) or n < min_rows * T:
         return
+    nx = ny = px = py = 0
+    g = grid_shape(f._source) if os.environ.get("B2S_TILES_GRID", "1") == "1" else None
+    if g is not None and g[2] > 1:
+        nx, ny, _ = g
+        px, py = _patches(nx, ny, T)
     h = C.c_void_p(None)
-    rc = D.lib().b2s_tiles_create(n, f._b, T, D.ptr(plan.device("inverse_permutation")),
+    rc = D.lib().b2s_tiles_create(n, f._b, T, nx, ny, px, py,
+                                  D.ptr(plan.device("inverse_permutation")),
                                   D.ptr(f._lu.pat.rp), D.ptr(f._lu.pat.ci), D.ptr(diag),
                                   D.ptr(f._lu.vals), D.ptr(f._invd),
-                                  D.ptr(plan.device("group_offsets")), plan.group_count,
+                                  D.ptr(plan.device("group_offsets")), plan.group_count, f.kc,
                                   C.byref(h), D.stream())
     if rc == 5:   # B2S_UNSUPPORTED: a tile does not fit, keep the sync-free sweeps
         return
     check(rc, "tiles_create")
     f.tiles = h.value
+    f.tile_shape = (px, py) if px else (T,)
 
 
 def decompose(a: BlockMatrix, plan: ParallelPlan) -> Ilu0Factorization:

@@ -34,12 +34,11 @@ def main():
     apply_bytes = (nnz - n) * 76 + 72 * n + 8 * (n + 1) + 96 * n
     plan = plan_device(P.Backend.LEVEL_SCHEDULED, bsr.pat)
     ref = None
-    for cfg in ("0", "148", "74", "120"):
-        if cfg == "0":
-            os.environ["B2S_TILES"] = "0"
-        else:
-            os.environ["B2S_TILES"] = "1"
-            os.environ["B2S_TILES_T"] = cfg
+    for cfg in ("0", "grid148", "grid120", "range148"):
+        os.environ["B2S_TILES"] = "0" if cfg == "0" else "1"
+        os.environ["B2S_TILES_GRID"] = "1" if cfg.startswith("grid") else "0"
+        if cfg != "0":
+            os.environ["B2S_TILES_T"] = cfg[-3:]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         f = factor_device(a, plan, bsr)
@@ -63,7 +62,8 @@ def main():
         res = kr.solve(rhs, x0.clone(), stop)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) * 1e3
-        print(json.dumps({"tiles": cfg, "tiled": bool(f.tiles), "factor_ms": tf,
+        print(json.dumps({"tiles": cfg, "tiled": bool(f.tiles),
+                          "shape": getattr(f, "tile_shape", None), "factor_ms": tf,
                           "ilu_apply_us": us, "gbs": apply_bytes / (us * 1e-6) / 1e9,
                           "bit_equal_to_sync_free": same, "krylov_ms": dt,
                           "its": res.iterations}), flush=True)
