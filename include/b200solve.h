@@ -134,7 +134,7 @@ int b2s_fill_sentinel(long long m, double* v, cudaStream_t stream);
 long long b2s_tiles_smem_bytes(int b, int rmax);
 int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const int32_t* iperm,
                      const int32_t* rp, const int32_t* ci, const int32_t* diag, const double* lu,
-                     const double* inv, const int32_t* goff, int ngroups, int kc,
+                     const double* inv, const int32_t* goff, int ngroups, int kc, int warps,
                      void** handle_out, cudaStream_t stream);
 int b2s_tiles_destroy(void* handle);
 int b2s_tiles_apply(int b, const void* handle, const double* r, double* y, double* z,
@@ -145,6 +145,18 @@ int b2s_tiles_apply(int b, const void* handle, const double* r, double* y, doubl
 int b2s_dot(long long m, const double* a, const double* b, int nparts, double* parts,
             double* out, cudaStream_t stream);
 int b2s_all_finite(long long m, const double* a, int* bad, cudaStream_t stream);
+int b2s_reduce(const double* parts, int np, double* out, cudaStream_t stream);
+
+/* BiCGStab vector steps with host scalars (multi-GPU loop; bs/krylov.py:201-233):
+ * scratch = >= 128 device bytes for the staged scalars. */
+int b2s_vec_p(long long m, int k, double beta, double omega, const double* r, const double* v,
+              double* p, double* scratch, cudaStream_t stream);
+int b2s_vec_s(long long m, double alpha, const double* r, const double* v, double* phat,
+              double* x, double* s, double* parts, int nparts, int reset, double* scratch,
+              cudaStream_t stream);
+int b2s_vec_r(long long m, double omega, double* shat, const double* t, const double* s,
+              const double* rhat, double* x, double* r, double* prr, double* prho, int nparts,
+              int reset, double* scratch, cudaStream_t stream);
 
 /* ---- BiCGStab (bs/krylov.py:140-244) ------------------------------------ */
 

@@ -66,11 +66,15 @@ SIGNATURES = {
     "b2s_fill_sentinel": (_I, [_LL, _P, _P]),
     "b2s_tiles_smem_bytes": (_LL, [_I, _I]),
     "b2s_tiles_create": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I,
-                              C.POINTER(C.c_void_p), _P]),
+                              _I, C.POINTER(C.c_void_p), _P]),
     "b2s_tiles_destroy": (_I, [_P]),
     "b2s_tiles_apply": (_I, [_I, _P, _P, _P, _P, _I, _P]),
     "b2s_dot": (_I, [_LL, _P, _P, _I, _P, _P, _P]),
     "b2s_all_finite": (_I, [_LL, _P, _P, _P]),
+    "b2s_reduce": (_I, [_P, _I, _P, _P]),
+    "b2s_vec_p": (_I, [_LL, _I, C.c_double, C.c_double, _P, _P, _P, _P, _P]),
+    "b2s_vec_s": (_I, [_LL, C.c_double, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
+    "b2s_vec_r": (_I, [_LL, C.c_double, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "b2s_bicgstab_workspace_bytes": (_LL, [_I, _I, _I]),
     "b2s_bicgstab": (_I, [C.POINTER(BicgArgs), C.POINTER(BicgResult)]),
     "b2s_jacobi_pattern": (_I, [_I, _P, _P, _P, _P, _PI, _P]),

@@ -431,6 +431,62 @@ int b2s_retain_pool_memory(int device) {
   return B2S_OK;
 }
 
+// ---- fused BiCGStab vector steps with host-provided scalars (the
+//      multi-GPU loop, paper_2309_11488_b200/distributed.py, drives these and
+//      all-reduces the partial sums between them).  A 2-double "scalars"
+//      record is staged on the device so the same kernels serve both paths.
+static State* stage_state(double* scratch, int k, double alpha, double beta, double omega,
+                          cudaStream_t st, int* rc) {
+  State h{};
+  h.alpha = alpha; h.beta = beta; h.omega = omega; h.k = k; h.done = 0;
+  State* d = reinterpret_cast<State*>(scratch);
+  *rc = cudaMemcpyAsync(d, &h, sizeof(State), cudaMemcpyHostToDevice, st) == cudaSuccess
+            ? B2S_OK : B2S_CUDA_ERROR;
+  return d;
+}
+
+// p = r (k == 0) or r + beta (p - omega v); scratch >= 128 bytes device
+int b2s_vec_p(long long m, int k, double beta, double omega, const double* r, const double* v,
+              double* p, double* scratch, cudaStream_t st) {
+  int rc;
+  State* s = stage_state(scratch, k, 0.0, beta, omega, st, &rc);
+  if (rc) return rc;
+  k_p_update<<<kSms * 4, 256, 0, st>>>(m, s, r, v, p);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+// s = r - alpha v ; x += alpha phat ; partials |s|^2 (nparts CTAs)
+int b2s_vec_s(long long m, double alpha, const double* r, const double* v, double* phat,
+              double* x, double* s, double* parts, int nparts, int reset, double* scratch,
+              cudaStream_t st) {
+  int rc;
+  State* d = stage_state(scratch, 0, alpha, 0.0, 0.0, st, &rc);
+  if (rc) return rc;
+  k_s_update<<<nparts, 256, 0, st>>>(m, d, r, v, phat, x, s, parts, reset);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+// x += omega shat ; r = s - omega t ; partials |r|^2 and rhat.r
+int b2s_vec_r(long long m, double omega, double* shat, const double* t, const double* s,
+              const double* rhat, double* x, double* r, double* prr, double* prho, int nparts,
+              int reset, double* scratch, cudaStream_t st) {
+  int rc;
+  State* d = stage_state(scratch, 0, 0.0, 0.0, omega, st, &rc);
+  if (rc) return rc;
+  k_r_update<<<nparts, 256, 0, st>>>(m, d, shat, t, s, rhat, x, r, prr, prho, reset);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+// out[0] = fixed-order sum of parts[0..np)
+int b2s_reduce(const double* parts, int np, double* out, cudaStream_t st) {
+  k_reduce_parts<<<1, 256, 0, st>>>(parts, np, out);
+  B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
 int b2s_all_finite(long long m, const double* a, int* bad_dev, cudaStream_t st) {
   if (m < 0) return B2S_SHAPE;
   B2S_CHECK(cudaMemsetAsync(bad_dev, 0, sizeof(int), st));

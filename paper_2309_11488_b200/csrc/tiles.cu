@@ -35,7 +35,7 @@
 
 namespace b2s {
 
-constexpr int kTileWarps = 8;
+constexpr unsigned kPollNs = 40;   // pause between polling rounds
 
 struct TileSet {
   int T, nsl, rmax;
@@ -103,12 +103,15 @@ __device__ __forceinline__ void tile_deps(const int (&code)[KC], const double* r
       for (int c = 0; c < B; ++c) miss |= is_sentinel(dep[kk][c]);
       if ((todo & (1u << kk)) && !miss) pend &= ~(1u << kk);
     }
+    // a shared-memory poll returns in tens of cycles: without a pause the
+    // waiting warps would take the issue slots of the warps doing the work
+    if (pend) __nanosleep(kPollNs);
   }
 }
 
 // DIR = 0 forward (out = y = L^-1 in), 1 backward (out = z = U^-1 in).
-template <int B, int KC, int DIR>
-__global__ void __launch_bounds__(kTileWarps * 32, 1)
+template <int B, int KC, int DIR, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
     k_tile_sweep(TileSet ts, const double* __restrict__ in, double* out, double* yreset,
                  int reset, const int* done) {
   constexpr int BB = B * B;
@@ -321,17 +324,17 @@ inline int grid_n(long long work) {
 
 struct TileHandle {
   TileSet ts;
-  int b, kc;
+  int b, kc, warps;
   size_t smem;
   int32_t *trow, *sstart, *tslice, *toff, *lsp, *lcols, *usp, *ucols;
   double *lvals, *uvals, *dtile;
 };
 
-template <int B, int KC>
-int launch_tiled_bk(const TileHandle* h, const double* r, double* y, double* z, int reset_y,
-                    const int* done, cudaStream_t st) {
-  auto* f = k_tile_sweep<B, KC, 0>;
-  auto* g = k_tile_sweep<B, KC, 1>;
+template <int B, int KC, int NW>
+int launch_tiled_bkw(const TileHandle* h, const double* r, double* y, double* z, int reset_y,
+                     const int* done, cudaStream_t st) {
+  auto* f = k_tile_sweep<B, KC, 0, NW>;
+  auto* g = k_tile_sweep<B, KC, 1, NW>;
   if (cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)h->smem) != cudaSuccess ||
       cudaFuncSetAttribute((const void*)g, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -343,7 +346,7 @@ int launch_tiled_bk(const TileHandle* h, const double* r, double* y, double* z, 
   attr.val.cooperative = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(h->ts.T);
-  cfg.blockDim = dim3(kTileWarps * 32);
+  cfg.blockDim = dim3(NW * 32);
   cfg.dynamicSmemBytes = h->smem;
   cfg.stream = st;
   cfg.attrs = &attr;
@@ -353,6 +356,14 @@ int launch_tiled_bk(const TileHandle* h, const double* r, double* y, double* z, 
   if (cudaLaunchKernelEx(&cfg, g, h->ts, (const double*)y, z, y, reset_y, done) != cudaSuccess)
     return B2S_CUDA_ERROR;
   return B2S_OK;
+}
+
+template <int B, int KC>
+int launch_tiled_bk(const TileHandle* h, const double* r, double* y, double* z, int reset_y,
+                    const int* done, cudaStream_t st) {
+  if (h->warps >= 32) return launch_tiled_bkw<B, KC, 32>(h, r, y, z, reset_y, done, st);
+  if (h->warps >= 16) return launch_tiled_bkw<B, KC, 16>(h, r, y, z, reset_y, done, st);
+  return launch_tiled_bkw<B, KC, 8>(h, r, y, z, reset_y, done, st);
 }
 
 template <int B>
@@ -398,7 +409,7 @@ long long b2s_tiles_smem_bytes(int b, int rmax) { return (long long)rmax * b * 8
 // tile's values do not fit in one SM's shared memory or T exceeds the SMs.
 int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const int32_t* iperm,
                      const int32_t* rp, const int32_t* ci, const int32_t* diag, const double* lu,
-                     const double* inv, const int32_t* goff, int ngroups, int kc,
+                     const double* inv, const int32_t* goff, int ngroups, int kc, int warps,
                      void** handle_out, cudaStream_t st) {
   *handle_out = nullptr;
   if (n <= 0 || b < 1 || b > 4) return B2S_SHAPE;
@@ -501,6 +512,7 @@ int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const 
                     Sell{h->lsp, h->lcols, h->lvals}, Sell{h->usp, h->ucols, h->uvals}, h->dtile};
     h->b = b;
     h->kc = kc;
+    h->warps = warps;
     h->smem = (size_t)(smem > 0 ? smem : 16);
     B2S_CHECK(cudaStreamSynchronize(st));
     cudaFreeAsync(tmp2, st);

@@ -1,0 +1,480 @@
+"""Multi-GPU ILU0-BiCGStab: contiguous row slabs, block-Jacobi ILU0, halo
+SpMV and all-reduced inner products (the paper's MPI
+decomposition).
+
+Each rank ("shard") owns a contiguous range of global rows -- a z-slab of
+the natural-order grid.  Its preconditioner is ILU0 of the diagonal block
+(cross-slab couplings dropped, exactly ``drop_cross_blocks`` with the slab
+partition, bs/jacobi.py:111-136), so factorisation and sweeps are local.
+The operator keeps every coupling: before each SpMV the ghost rows (the
+off-slab columns a shard references) are exchanged with the owning ranks.
+The BiCGStab control flow is the reference's (bs/krylov.py:171-244); its
+scalars are sums of per-shard partials combined by an all-reduce, so every
+rank takes identical decisions.
+
+Communication is behind a small interface with two implementations:
+``NcclComm`` (one shard per process, torch.distributed over NCCL/NVLink,
+halos by grouped send/recv) and ``LocalComm`` (several shards in one
+process on one GPU, device copies and host sums) -- the latter lets the
+partitioned solver be checked against the oracle on a single GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import check
+from .analysis import ParallelPlan
+from .blockcore import BlockMatrix, Layout, SparsityPattern
+from .bridge import Backend, plan_device
+from .ilu0 import factor_device
+from .krylov import _BREAKDOWN_FLOOR, SolveReport, StoppingCriteria
+from .synthetic import GeneratorSpec
+
+
+# ---------------------------------------------------------------------------
+# slab generation: the rows [r0, r1) of generate(spec), without the rest
+
+@dataclass
+class Slab:
+    rank: int
+    world: int
+    n_global: int
+    r0: int
+    r1: int
+    b: int
+    rp: np.ndarray        # local rows, int64
+    ci: np.ndarray        # GLOBAL column ids, int64
+    vals3: np.ndarray     # (nnz, b, b)
+    rhs: np.ndarray       # (r1 - r0) * b
+
+    @property
+    def rows(self) -> int:
+        return self.r1 - self.r0
+
+
+def slab_bounds(nz: int, world: int, rank: int) -> tuple[int, int]:
+    """z-planes [z0, z1) of a rank: equal shares, the first ranks take the rest."""
+    base, rem = divmod(nz, world)
+    z0 = rank * base + min(rank, rem)
+    return z0, z0 + base + (1 if rank < rem else 0)
+
+
+def generate_slab(spec: GeneratorSpec, rank: int, world: int) -> Slab:
+    """Rows of the z-planes [z0, z1) of ``generate(spec)``, bit-identical to
+    the corresponding rows of the full system: the same PCG64 stream is
+    advanced past the draws other slabs own (bs/io.py:363-414 draw order:
+    all +x, +y, +z couplings src->dst in meshgrid order, then their mirrors,
+    then the right-hand side)."""
+    nx, ny, nz, b = spec.nx, spec.ny, spec.nz, spec.block_size
+    bb = b * b
+    nxy = nx * ny
+    n = nxy * nz
+    z0, z1 = slab_bounds(nz, world, rank)
+    nfx, nfy, nfz = (nx - 1) * ny * nz, nx * (ny - 1) * nz, nxy * (nz - 1)
+    npairs = nfx + nfy + nfz
+    # runs of consecutive coupling indices this slab needs: (first, count,
+    # direction, forward?) -- iz is the fastest enumeration index
+    runs = []
+    for fwd in (True, False):
+        base = 0 if fwd else npairs
+        for ix in range(nx - 1):                       # +x faces
+            for iy in range(ny):
+                e0 = (ix * ny + iy) * nz
+                runs.append((base + e0 + z0, z1 - z0, "x", fwd, ix, iy, z0))
+        for ix in range(nx):                           # +y faces
+            for iy in range(ny - 1):
+                e0 = nfx + (ix * (ny - 1) + iy) * nz
+                runs.append((base + e0 + z0, z1 - z0, "y", fwd, ix, iy, z0))
+        for ix in range(nx):                           # +z faces
+            for iy in range(ny):
+                e0 = nfx + nfy + (ix * ny + iy) * (nz - 1)
+                # forward block rows = src (iz); backward rows = dst (iz + 1)
+                lo, hi = (z0, min(z1, nz - 1)) if fwd else (max(z0 - 1, 0), z1 - 1)
+                if hi > lo:
+                    runs.append((base + e0 + lo, hi - lo, "z", fwd, ix, iy, lo))
+    runs.sort(key=lambda r: r[0])
+    rng = np.random.default_rng(spec.seed)
+    bg = rng.bit_generator
+    pos = 0
+    rows_l, cols_l, blks_l = [], [], []
+    tdir = {"x": spec.tx, "y": spec.ty, "z": spec.tz}
+    step = {"x": 1, "y": nx, "z": nxy}
+    for first, count, d, fwd, ix, iy, iz0 in runs:
+        if first * bb > pos:
+            bg.advance(first * bb - pos)
+            pos = first * bb
+        u = rng.uniform(0.5, 1.5, size=(count, b, b))
+        pos += count * bb
+        iz = iz0 + np.arange(count, dtype=np.int64)
+        src = ix + nx * (iy + ny * iz)
+        dst = src + step[d]
+        rows_l.append(src if fwd else dst)
+        cols_l.append(dst if fwd else src)
+        blks_l.append(-tdir[d] * u)
+    rhs_first = 2 * npairs * bb + z0 * nxy * b
+    bg.advance(rhs_first - pos)
+    rhs = rng.uniform(-1.0, 1.0, size=(z1 - z0) * nxy * b)
+    r0, r1 = z0 * nxy, z1 * nxy
+    diag = np.arange(r0, r1, dtype=np.int64)
+    rows = np.concatenate(rows_l + [diag])
+    cols = np.concatenate(cols_l + [diag])
+    blk = np.concatenate(blks_l + [np.zeros((r1 - r0, b, b))])
+    order = np.lexsort((cols, rows))
+    rows, cols, blk = rows[order], cols[order], blk[order]
+    nloc = r1 - r0
+    rp = np.zeros(nloc + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows - r0, minlength=nloc), out=rp[1:])
+    sums = np.zeros((nloc, b))
+    np.add.at(sums, rows - r0, np.abs(blk).sum(axis=2))
+    dpos = np.flatnonzero(rows == cols)
+    eye = np.arange(b)
+    dblk = np.zeros((nloc, b, b))
+    dblk[:, eye, eye] = sums + spec.diagonal_boost
+    blk[dpos] = dblk
+    return Slab(rank, world, n, r0, r1, b, rp, cols, blk, rhs)
+
+
+# ---------------------------------------------------------------------------
+# one rank's device state
+
+class HaloPlan:
+    """Host-side halo bookkeeping of one slab (pure numpy): the ghost rows it
+    references, which rank owns each, and local column ids with the ghosts
+    appended after the owned rows."""
+
+    def __init__(self, slab: Slab, owners: np.ndarray):
+        self.slab = slab
+        R = slab.rows
+        ci = slab.ci
+        self.own = (ci >= slab.r0) & (ci < slab.r1)
+        self.ghosts = np.unique(ci[~self.own])          # global ids, ascending
+        self.G = len(self.ghosts)
+        gowner = np.searchsorted(owners, self.ghosts, side="right") - 1
+        self.recv = {int(h): np.flatnonzero(gowner == h) for h in np.unique(gowner)}
+        self.lcol = np.where(self.own, ci - slab.r0,
+                             R + np.searchsorted(self.ghosts, ci)).astype(np.int64)
+
+    def requests(self):
+        """{owner rank: global ids this slab needs from it}"""
+        return {h: self.ghosts[idx] for h, idx in self.recv.items()}
+
+
+class Shard:
+    """Local rows in plan order + ghost section, block-Jacobi ILU0, halo maps."""
+
+    def __init__(self, slab: Slab, owners: np.ndarray, backend: Backend):
+        self.slab = slab
+        dev = D.require_cuda()
+        R, b = slab.rows, slab.b
+        self.R, self.b = R, b
+        ci = slab.ci
+        hp = HaloPlan(slab, owners)
+        self.halo_plan = hp
+        own, lcol = hp.own, hp.lcol
+        self.ghosts, self.G, self.recv = hp.ghosts, hp.G, hp.recv
+        rows = np.repeat(np.arange(R), np.diff(slab.rp))
+        # preconditioner source: the diagonal block (cross-slab blocks dropped)
+        prp = np.zeros(R + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows[own], minlength=R), out=prp[1:])
+        self.pmat = BlockMatrix(SparsityPattern(R, prp, lcol[own]), b,
+                                slab.vals3[own].reshape(-1), Layout.BLOCK_ROW_MAJOR)
+        # one upload: both matrices stay resident; setup() re-runs the device
+        # pipeline (plan, permutation, factorisation, layouts) from them
+        self.pbsr = D.DevBSR.upload(self.pmat)
+        opat = D.DevPattern(R, len(ci), D.i32(slab.rp, dev), D.i32(lcol, dev))
+        self.obsr = D.DevBSR(opat, b, D.f64(slab.vals3.reshape(-1), dev))
+        self.dev = dev
+        if backend is not None:
+            self.setup(backend)
+
+    def setup(self, backend: Backend):
+        R, dev = self.R, self.dev
+        self.plan = plan_device(backend, self.pbsr.pat)
+        self.fact = factor_device(self.pmat, self.plan, self.pbsr)
+        # operator rows in plan order; own columns through perm, ghosts appended
+        perm = self.plan.device("permutation")
+        iperm = self.plan.device("inverse_permutation")
+        cmap = torch.cat([perm, torch.arange(R, R + self.G, dtype=torch.int32, device=dev)])
+        self.op = D.permute(self.obsr, cmap, iperm)
+        self.smap = self.fact.smap
+        self.sell = D.Sell.build(self.smap, self.op, 0)
+        self.perm_h = self.plan.permutation          # local old -> new
+        if getattr(self, "_requests", None) is not None:
+            self.set_send(self._requests)
+        return self
+
+    # rows this shard must send to rank h (plan-order local ids), given the
+    # ghost ids rank h requested from us
+    def set_send(self, requests: dict[int, np.ndarray]):
+        self._requests = requests
+        self.send = {h: D.i32(self.perm_h[g - self.slab.r0], self.dev)
+                     for h, g in requests.items()}
+
+    def vec(self, with_ghosts=False):
+        return torch.zeros((self.R + (self.G if with_ghosts else 0)) * self.b,
+                           dtype=torch.float64, device=self.dev)
+
+
+# ---------------------------------------------------------------------------
+# communicators
+
+class LocalComm:
+    """All shards in this process (one GPU): halos are device copies."""
+
+    def __init__(self, shards):
+        self.shards = shards
+
+    def allreduce(self, vals):   # vals: per shard, 1-D CUDA tensor -> host floats
+        tot = None
+        for v in vals:
+            h = v.cpu().numpy().astype(np.float64)
+            tot = h if tot is None else tot + h
+        return [tot for _ in vals]
+
+    def halo(self, bufs):
+        by_rank = {s.slab.rank: (s, x) for s, x in zip(self.shards, bufs)}
+        for s, x in zip(self.shards, bufs):
+            for h, idx in s.recv.items():
+                src, xs = by_rank[h]
+                rows = src.send[s.slab.rank]
+                vals = D.gather_rows(xs, rows, len(idx), s.b)
+                dst = x.view(-1, s.b)
+                dst[s.R + torch.as_tensor(idx, device=x.device)] = vals.view(-1, s.b)
+
+
+class NcclComm:
+    """One shard per process over torch.distributed (NCCL over NVLink)."""
+
+    def __init__(self, shard):
+        import torch.distributed as dist
+        self.dist = dist
+        self.shards = [shard]
+        s = shard
+        # contiguous receive ranges per neighbour (ghost ids are sorted and
+        # every owner's ids are contiguous)
+        self.recv_rng = {h: (int(idx[0]), int(idx[-1]) + 1) for h, idx in s.recv.items()}
+
+    def allreduce(self, vals):
+        v = vals[0].clone()
+        self.dist.all_reduce(v)
+        return [v.cpu().numpy()]
+
+    def halo(self, bufs):
+        s, x = self.shards[0], bufs[0]
+        ops, keep = [], []
+        for h, rows in s.send.items():
+            sb = D.gather_rows(x, rows, rows.numel(), s.b)
+            keep.append(sb)
+            ops.append(self.dist.P2POp(self.dist.isend, sb, h))
+        for h, (lo, hi) in self.recv_rng.items():
+            rv = x[(s.R + lo) * s.b:(s.R + hi) * s.b]
+            ops.append(self.dist.P2POp(self.dist.irecv, rv, h))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+
+def route_requests(mine, gather):
+    """Tell every owner which of its rows each local slab needs.
+
+    mine: [(rank, {owner: global ids needed})] for the slabs of this process;
+    gather: all_gather_object-like callable returning everyone's lists.
+    Returns {rank: {requester: global ids to send}} for the local ranks."""
+    everyone = gather(mine)
+    flat = [item for part in everyone for item in (part if isinstance(part, list) else [part])]
+    out = {}
+    for rank, _ in mine:
+        out[rank] = {req: needs[rank] for req, needs in flat if rank in needs}
+    return out
+
+
+def exchange_requests(shards, world, gather):
+    mine = [(s.slab.rank, s.halo_plan.requests()) for s in shards]
+    sends = route_requests(mine, gather)
+    for s in shards:
+        s.set_send(sends[s.slab.rank])
+
+
+# ---------------------------------------------------------------------------
+# the distributed BiCGStab (bs/krylov.py:140-244 control flow)
+
+def bicgstab_sharded(shards, comm, stop: StoppingCriteria):
+    """Solve for every shard's rhs/x0 (plan order) set in ``shard.rhs_p`` /
+    ``shard.x_p``; returns (report, x per shard in plan order)."""
+    lib = D.lib()
+    st = D.stream()
+    NP = D.NPARTS
+    for s in shards:
+        s.scr = torch.zeros(32, dtype=torch.float64, device=s.dev)
+        s.parts = torch.zeros(4 * NP, dtype=torch.float64, device=s.dev)
+        s.sums = torch.zeros(4, dtype=torch.float64, device=s.dev)
+        s.r = s.vec(); s.rhat = s.vec(); s.p = s.vec(); s.v = s.vec()
+        s.s = s.vec(); s.t = s.vec()
+        s.phat = s.vec(True); s.shat = s.vec(True); s.xg = s.vec(True)
+        s.y = s.vec()
+        s.xg[: s.R * s.b] = s.x_p
+
+    def reduce(idx_list):
+        """sum the partial arrays `idx_list` of every shard, then all-reduce"""
+        vals = []
+        for s in shards:
+            for j, k in enumerate(idx_list):
+                check(lib.b2s_reduce(D.ptr(s.parts[k * NP:(k + 1) * NP]), NP,
+                                     D.ptr(s.sums[j:j + 1]), st), "reduce")
+            vals.append(s.sums[: len(idx_list)])
+        return comm.allreduce(vals)[0]
+
+    def spmv(s, x_ext, y, mode, w, k0, k1=None):
+        D.spmv(s.smap, s.sell, s.b, x_ext, y, mode, w,
+               s.parts[k0 * NP:(k0 + 1) * NP],
+               None if k1 is None else s.parts[k1 * NP:(k1 + 1) * NP])
+
+    def apply_m(s, src, dst_ext):
+        s.fact.apply_device(src, dst_ext)
+
+    t0 = time.perf_counter()
+    comm.halo([s.xg for s in shards])
+    for s in shards:
+        spmv(s, s.xg, s.r, 3, s.rhs_p, 0)
+    rr0 = float(reduce([0])[0])
+    n0 = float(np.sqrt(rr0))
+    target = stop.relative_reduction * n0
+    groups = shards[0].plan.group_count
+    x0 = [s.xg[: s.R * s.b].clone() for s in shards]
+
+    def done(conv, its, final, reason=None):
+        rep = SolveReport(conv, its, n0, final, time.perf_counter() - t0, groups,
+                          failure_reason=reason)
+        return rep, [s.xg[: s.R * s.b] for s in shards]
+
+    if not np.isfinite(n0):
+        for s, x in zip(shards, x0):
+            s.xg[: s.R * s.b] = x
+        return done(False, 0.0, n0, "numerical")
+    if n0 <= target or n0 == 0.0:
+        return done(True, 0.0, n0)
+    for s in shards:
+        s.rhat.copy_(s.r)
+    rho_prev = alpha = omega = 1.0
+    its = 0.0
+    reason = "budget"
+    m = [s.R * s.b for s in shards]
+    rho = rr0
+    rho_known = True  # rho_0 = rhat.r = |r0|^2 (the same sum)
+    for k in range(stop.max_iterations):
+        if not rho_known:
+            rho = float(reduce([1])[0])
+        rho_known = False
+        if abs(rho) < _BREAKDOWN_FLOOR:
+            reason = "breakdown"
+            break
+        beta = 0.0 if k == 0 else (rho / rho_prev) * (alpha / omega)
+        for s, mm in zip(shards, m):
+            check(lib.b2s_vec_p(mm, k, beta, omega, D.ptr(s.r), D.ptr(s.v), D.ptr(s.p),
+                                D.ptr(s.scr), st), "vec_p")
+            apply_m(s, s.p, s.phat)
+        comm.halo([s.phat for s in shards])
+        for s in shards:
+            spmv(s, s.phat, s.v, 1, s.rhat, 2)
+        gamma = float(reduce([2])[0])
+        if abs(gamma) < _BREAKDOWN_FLOOR:
+            reason = "breakdown"
+            break
+        alpha = rho / gamma
+        for s, mm in zip(shards, m):
+            check(lib.b2s_vec_s(mm, alpha, D.ptr(s.r), D.ptr(s.v), D.ptr(s.phat), D.ptr(s.xg),
+                                D.ptr(s.s), D.ptr(s.parts[0:NP]), NP, 0, D.ptr(s.scr), st),
+                  "vec_s")
+        its += 0.5
+        ns = float(np.sqrt(reduce([0])[0]))
+        if not np.isfinite(ns):
+            reason = "numerical"
+            break
+        if ns <= target:
+            return done(True, its, ns)
+        for s in shards:
+            apply_m(s, s.s, s.shat)
+        comm.halo([s.shat for s in shards])
+        for s in shards:
+            spmv(s, s.shat, s.t, 2, s.s, 2, 3)
+        tt, ts = (float(v) for v in reduce([2, 3]))
+        if tt < _BREAKDOWN_FLOOR:
+            reason = "breakdown"
+            break
+        omega = ts / tt
+        if abs(omega) < _BREAKDOWN_FLOOR:
+            reason = "breakdown"
+            break
+        for s, mm in zip(shards, m):
+            check(lib.b2s_vec_r(mm, omega, D.ptr(s.shat), D.ptr(s.t), D.ptr(s.s),
+                                D.ptr(s.rhat), D.ptr(s.xg), D.ptr(s.r), D.ptr(s.parts[0:NP]),
+                                D.ptr(s.parts[NP:2 * NP]), NP, 0, D.ptr(s.scr), st), "vec_r")
+        its += 0.5
+        nr_rho = reduce([0, 1])
+        nr = float(np.sqrt(nr_rho[0]))
+        rho_next = float(nr_rho[1])
+        if not np.isfinite(nr):
+            reason = "numerical"
+            break
+        if nr <= target:
+            return done(True, its, nr)
+        rho_prev = rho
+        rho, rho_known = rho_next, True
+    comm.halo([s.xg for s in shards])
+    for s in shards:
+        spmv(s, s.xg, s.t, 3, s.rhs_p, 0)
+    final = float(np.sqrt(reduce([0])[0]))
+    finite = all(bool(torch.isfinite(s.xg[: s.R * s.b]).all()) for s in shards)
+    if not finite:
+        for s, x in zip(shards, x0):
+            s.xg[: s.R * s.b] = x
+    return done(False, its, final, reason)
+
+
+def solve_shards(shards, comm, stop: StoppingCriteria, x0=None):
+    """Global solve over prepared shards: rhs (input order) per shard in
+    ``shard.slab.rhs``; returns (report, list of per-shard x in input order)."""
+    for i, s in enumerate(shards):
+        iperm = s.plan.device("inverse_permutation")
+        rhs = D.f64(s.slab.rhs, s.dev)
+        s.rhs_p = D.gather_rows(rhs, iperm, s.R, s.b)
+        x = D.f64(x0[i], s.dev) if x0 is not None else torch.zeros_like(rhs)
+        s.x_p = D.gather_rows(x, iperm, s.R, s.b)
+    rep, xs = bicgstab_sharded(shards, comm, stop)
+    out = []
+    for s, xp in zip(shards, xs):
+        out.append(D.gather_rows(xp, s.plan.device("permutation"), s.R, s.b))
+    return rep, out
+
+
+def local_solver(spec: GeneratorSpec, world: int, backend=Backend.LEVEL_SCHEDULED):
+    """All `world` slabs of spec in this process (testing on one GPU)."""
+    slabs = [generate_slab(spec, r, world) for r in range(world)]
+    owners = np.array([s.r0 for s in slabs], dtype=np.int64)
+    shards = [Shard(s, owners, backend) for s in slabs]
+    exchange_requests(shards, world, lambda mine: [mine])
+    return shards, LocalComm(shards)
+
+
+def nccl_solver(spec: GeneratorSpec, backend=Backend.LEVEL_SCHEDULED):
+    """This process's slab of spec (torch.distributed must be initialised)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    slab = generate_slab(spec, rank, world)
+    owners = np.array([slab_bounds(spec.nz, world, r)[0] * spec.nx * spec.ny
+                       for r in range(world)], dtype=np.int64)
+    shard = Shard(slab, owners, backend)
+
+    def gather(mine):
+        out = [None] * world
+        dist.all_gather_object(out, mine)
+        return out
+    exchange_requests([shard], world, gather)
+    return [shard], NcclComm(shard)

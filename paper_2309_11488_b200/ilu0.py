@@ -232,7 +232,9 @@ def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
     """Deep level schedules are latency-bound in the sync-free sweeps; give
     them the tiled kernels (csrc/tiles.cu) when a tile fits in an SM.
     B2S_TILES=0 disables, B2S_TILES_T sets the tile count."""
-    if os.environ.get("B2S_TILES", "1") == "0":
+    # experimental (csrc/tiles.cu): correct but not yet faster than the
+    # sync-free sweeps on B200, so off unless B2S_TILES=1
+    if os.environ.get("B2S_TILES", "0") == "0":
         return
     n = f.num_block_rows
     sms = torch.cuda.get_device_properties(diag.device).multi_processor_count
@@ -251,7 +253,8 @@ def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
                                   D.ptr(f._lu.pat.rp), D.ptr(f._lu.pat.ci), D.ptr(diag),
                                   D.ptr(f._lu.vals), D.ptr(f._invd),
                                   D.ptr(plan.device("group_offsets")), plan.group_count, f.kc,
-                                  C.byref(h), D.stream())
+                                  int(os.environ.get("B2S_TILE_WARPS", 16)), C.byref(h),
+                                  D.stream())
     if rc == 5:   # B2S_UNSUPPORTED: a tile does not fit, keep the sync-free sweeps
         return
     check(rc, "tiles_create")

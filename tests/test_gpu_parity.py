@@ -325,6 +325,7 @@ def test_tiled_sweeps_bit_equal_to_sync_free(monkeypatch, golden, T):
 def test_tiled_sweeps_nonsymmetric_same_group(monkeypatch, golden):
     """Random non-symmetric patterns (same-group upper entries) through the tiles."""
     g = golden("random_patterns")
+    monkeypatch.setenv("B2S_TILES", "1")
     monkeypatch.setenv("B2S_TILES_T", "3")
     monkeypatch.setenv("B2S_TILES_MIN_GROUPS", "1")
     monkeypatch.setenv("B2S_TILES_MIN_ROWS", "1")
