@@ -45,6 +45,13 @@ __global__ void k_find_diag(int n, const int32_t* __restrict__ rp,
 }
 
 // ---------------------------------------------------------------------------
+// Neighbour lists of up to kNb entries are held in registers and all their
+// published values are polled in one round per pass (one L2 round trip per
+// dependency level instead of one per neighbour); longer lists fall back to
+// a one-at-a-time walk.  A warp keeps polling while any lane still waits, so
+// lanes of one slice may depend on each other (natural order).
+constexpr int kNb = 8;
+
 // level(i) = 1 + max level(j) over strict-lower j, 0 without lower
 // neighbours (bs/analysis.py:85-100).  level[] must be -1 on entry.
 __global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
@@ -59,22 +66,56 @@ __global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
     if (row0 >= n) break;
     const int i = (int)row0 + lane;
     bool done = i >= n;
-    int k = done ? 0 : rp[i];
-    const int end = done ? 0 : rp[i + 1];
+    int nb[kNb];
+    int cnt = 0, k = 0, end = 0;
+    bool longrow = false;
+    if (!done) {
+      k = rp[i];
+      end = rp[i + 1];
+      for (int q = k; q < end; ++q) {
+        const int j = ci[q];
+        if (j >= i) break;
+        if (cnt < kNb) {
+#pragma unroll
+          for (int t = 0; t < kNb; ++t)
+            if (t == cnt) nb[t] = j;
+        }
+        ++cnt;
+      }
+      longrow = cnt > kNb;
+    }
+    unsigned int pend = (!done && !longrow) ? ((1u << cnt) - 1u) : 0u;
     int best = -1;
     for (;;) {
       if (!done) {
-        while (k < end) {
-          const int j = ci[k];
-          if (j >= i) { k = end; break; }
-          const int lj = ld_relaxed_i(level + j);
-          if (lj < 0) break;  // not yet published
-          best = max(best, lj);
-          ++k;
-        }
-        if (k >= end) {
-          st_relaxed_i(level + i, best + 1);
-          done = true;
+        if (!longrow) {
+          int got[kNb];
+#pragma unroll
+          for (int t = 0; t < kNb; ++t)
+            got[t] = (pend & (1u << t)) ? ld_relaxed_i(level + nb[t]) : -1;
+#pragma unroll
+          for (int t = 0; t < kNb; ++t)
+            if ((pend & (1u << t)) && got[t] >= 0) {
+              best = max(best, got[t]);
+              pend &= ~(1u << t);
+            }
+          if (!pend) {
+            st_relaxed_i(level + i, best + 1);
+            done = true;
+          }
+        } else {
+          while (k < end) {
+            const int j = ci[k];
+            if (j >= i) { k = end; break; }
+            const int lj = ld_relaxed_i(level + j);
+            if (lj < 0) break;  // not yet published
+            best = max(best, lj);
+            ++k;
+          }
+          if (k >= end) {
+            st_relaxed_i(level + i, best + 1);
+            done = true;
+          }
         }
       }
       if (__all_sync(0xffffffffu, done)) break;
@@ -88,11 +129,16 @@ __global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
 // neighbours j < i, where j is a neighbour if (i,j) or (j,i) is stored.
 // The (j,i) half comes from `ut_ptr/ut_idx`: for every column c, the rows
 // j < c that store (j, c).  colour[] must be -1 on entry.
+__device__ __forceinline__ int mex64(unsigned long long used) {
+  return used == ~0ull ? 64 : __ffsll((long long)~used) - 1;
+}
+
 __global__ void k_color_sync_free(int n, const int32_t* __restrict__ rp,
                                   const int32_t* __restrict__ ci,
                                   const int32_t* __restrict__ ut_ptr,
                                   const int32_t* __restrict__ ut_idx, int32_t* color,
                                   unsigned int* ticket) {
+  constexpr int kC = 2 * kNb;
   const int lane = threadIdx.x & 31;
   for (;;) {
     unsigned int s = 0;
@@ -102,40 +148,77 @@ __global__ void k_color_sync_free(int n, const int32_t* __restrict__ rp,
     if (row0 >= n) break;
     const int i = (int)row0 + lane;
     bool done = i >= n;
-    // phase 0 walks the row's own strict-lower columns, phase 1 the
-    // transposed list; both only ever wait on rows j < i
-    int k = done ? 0 : rp[i];
-    int end = done ? 0 : rp[i + 1];
-    int phase = 0;
+    int nb[kC];
+    int cnt = 0;
+    if (!done) {
+      for (int q = rp[i]; q < rp[i + 1]; ++q) {
+        const int j = ci[q];
+        if (j >= i) break;
+        if (cnt < kC) {
+#pragma unroll
+          for (int t = 0; t < kC; ++t)
+            if (t == cnt) nb[t] = j;
+        }
+        ++cnt;
+      }
+      for (int q = ut_ptr[i]; q < ut_ptr[i + 1]; ++q) {
+        const int j = ut_idx[q];
+        if (cnt < kC) {
+#pragma unroll
+          for (int t = 0; t < kC; ++t)
+            if (t == cnt) nb[t] = j;
+        }
+        ++cnt;
+      }
+    }
+    const bool longrow = cnt > kC;
+    unsigned int pend = (!done && !longrow) ? (cnt == 32 ? ~0u : ((1u << cnt) - 1u)) : 0u;
     unsigned long long used = 0ull;  // colours 0..63 seen
     bool big = false;                 // some neighbour has colour >= 64
+    // long lists: phase 0 walks the row, phase 1 the transposed list
+    int k = done ? 0 : rp[i], end = done ? 0 : rp[i + 1], phase = 0;
     for (;;) {
       if (!done) {
-        for (;;) {
-          if (k >= end) {
-            if (phase == 0) { phase = 1; k = ut_ptr[i]; end = ut_ptr[i + 1]; continue; }
-            break;
+        bool ready = false;
+        if (!longrow) {
+          int got[kC];
+#pragma unroll
+          for (int t = 0; t < kC; ++t)
+            got[t] = (pend & (1u << t)) ? ld_relaxed_i(color + nb[t]) : -1;
+#pragma unroll
+          for (int t = 0; t < kC; ++t)
+            if ((pend & (1u << t)) && got[t] >= 0) {
+              if (got[t] < 64) used |= 1ull << got[t]; else big = true;
+              pend &= ~(1u << t);
+            }
+          ready = !pend;
+        } else {
+          for (;;) {
+            if (k >= end) {
+              if (phase == 0) { phase = 1; k = ut_ptr[i]; end = ut_ptr[i + 1]; continue; }
+              break;
+            }
+            const int j = (phase == 0) ? ci[k] : ut_idx[k];
+            if (phase == 0 && j >= i) { k = end; continue; }
+            const int cj = ld_relaxed_i(color + j);
+            if (cj < 0) break;
+            if (cj < 64) used |= 1ull << cj; else big = true;
+            ++k;
           }
-          const int j = (phase == 0) ? ci[k] : ut_idx[k];
-          if (phase == 0 && j >= i) { k = end; continue; }
-          const int cj = ld_relaxed_i(color + j);
-          if (cj < 0) break;
-          if (cj < 64) used |= 1ull << cj; else big = true;
-          ++k;
+          ready = phase == 1 && k >= end;
         }
-        if (phase == 1 && k >= end) {
-          int c = __ffsll((long long)~used) - 1;  // mex below 64
-          if (used == ~0ull) c = 64;
+        if (ready) {
+          int c = mex64(used);
           if (big && c >= 64) {
             // rare: >= 64 distinct neighbour colours; walk the set directly
             for (bool hit = true; hit;) {
               hit = false;
               for (int q = rp[i]; q < rp[i + 1] && !hit; ++q) {
                 const int j = ci[q];
-                if (j < i && ld_volatile(color + j) == c) hit = true;
+                if (j < i && ld_relaxed_i(color + j) == c) hit = true;
               }
               for (int q = ut_ptr[i]; q < ut_ptr[i + 1] && !hit; ++q)
-                if (ld_volatile(color + ut_idx[q]) == c) hit = true;
+                if (ld_relaxed_i(color + ut_idx[q]) == c) hit = true;
               if (hit) ++c;
             }
           }

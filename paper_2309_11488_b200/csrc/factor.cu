@@ -21,6 +21,8 @@
 
 namespace b2s {
 
+constexpr int kFast = 3;   // lower entries handled by the one-round fast path
+
 struct Tickets2 {
   unsigned int next, finished;
 };
@@ -92,16 +94,83 @@ __global__ void __launch_bounds__(256) k_factor_numeric(
     int k = 0, dpos = 0;
     int r = -1, pb = 0, pe = 0;
     int2 pq0 = make_int2(0, 0);
+    // fast path (stencil-like rows): <= kFast lower entries whose updates all
+    // land on the diagonal -- poll every pivot flag in one round, then load
+    // every pivot's inverse and U block in one round, then eliminate in order
+    bool simple = false;
+    int fr[kFast], fq[kFast];
+    int nl = 0;
     if (!done) {
       k = rp[i];
       dpos = diag[i];
-      if (k < dpos) {  // static data of the first pivot: off the critical path
+      nl = dpos - k;
+      simple = nl <= kFast;
+#pragma unroll
+      for (int t = 0; t < kFast; ++t) {
+        fr[t] = 0; fq[t] = -1;
+        if (simple && t < nl) {
+          fr[t] = ci[k + t];
+          const int b0 = pptr[k + t], b1 = pptr[k + t + 1];
+          if (b1 - b0 > 1) simple = false;
+          if (b1 > b0) {
+            const int2 pq = pairs[b0];
+            if (pq.x != dpos) simple = false;
+            fq[t] = pq.y;
+          }
+        }
+      }
+      if (!simple && k < dpos) {  // static data of the first pivot
         r = ci[k]; pb = pptr[k]; pe = pptr[k + 1];
         if (pb < pe) pq0 = pairs[pb];
       }
     }
+    unsigned int fpend = simple ? ((1u << nl) - 1u) : 0u;
     for (;;) {
-      if (!done) {
+      if (!done && simple) {
+        int fl[kFast];
+#pragma unroll
+        for (int t = 0; t < kFast; ++t) fl[t] = (fpend & (1u << t)) ? ld_flag_relaxed(flag + fr[t]) : 0;
+#pragma unroll
+        for (int t = 0; t < kFast; ++t)
+          if ((fpend & (1u << t)) && fl[t]) fpend &= ~(1u << t);
+        if (!fpend) {
+          double inv_r[kFast][BB], urq[kFast][BB], dblk[BB];
+#pragma unroll
+          for (int t = 0; t < kFast; ++t)
+#pragma unroll
+            for (int e = 0; e < BB; ++e) {
+              inv_r[t][e] = t < nl ? __ldcg(invd + (long long)fr[t] * BB + e) : 0.0;
+              urq[t][e] = (t < nl && fq[t] >= 0) ? __ldcg(w + (long long)fq[t] * BB + e) : 0.0;
+            }
+#pragma unroll
+          for (int e = 0; e < BB; ++e) dblk[e] = w[(long long)dpos * BB + e];
+#pragma unroll
+          for (int t = 0; t < kFast; ++t) {
+            if (t < nl) {
+              double wik[BB], l[BB], prod[BB];
+#pragma unroll
+              for (int e = 0; e < BB; ++e) wik[e] = w[(long long)(k + t) * BB + e];
+              matmul<B>(wik, inv_r[t], l);  // L_ir = A_ir inv(U_rr)
+#pragma unroll
+              for (int e = 0; e < BB; ++e) w[(long long)(k + t) * BB + e] = l[e];
+              if (fq[t] >= 0) {
+                matmul<B>(l, urq[t], prod);  // A_ii -= L_ir U_ri
+#pragma unroll
+                for (int e = 0; e < BB; ++e) dblk[e] -= prod[e];
+              }
+            }
+          }
+          double inv[BB];
+#pragma unroll
+          for (int e = 0; e < BB; ++e) w[(long long)dpos * BB + e] = dblk[e];
+          if (!invert_block<B>(dblk, inv)) atomicMin(bad, i);
+#pragma unroll
+          for (int e = 0; e < BB; ++e) invd[(long long)i * BB + e] = inv[e];
+          st_flag_release(flag + i, 1);
+          done = true;
+        }
+      }
+      if (!done && !simple) {
         while (k < dpos) {
           if (ld_flag_relaxed(flag + r) == 0) break;
           // every value load of this pivot step is independent: one round trip

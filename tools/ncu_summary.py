@@ -1,0 +1,62 @@
+"""Summarise ncu outputs into profiles/ (run in the build container).
+
+python tools/ncu_summary.py <launches.csv> <prof.ncu-rep>... --out profiles/r01
+"""
+import collections
+import csv
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_bytes.sum"]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr = rows[h]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").split("<")[0]
+        agg[name][0] += 1
+        agg[name][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    tot = sum(v[1] for v in agg.values())
+    return [{"kernel": k, "launches": v[0], "total_us": round(v[1], 1),
+             "share": round(v[1] / tot, 4)} for k, v in sorted(agg.items(), key=lambda x: -x[1][1])]
+
+
+def full(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[hdr.index("Kernel Name")][:80]}
+        for k in KEYS:
+            if k in hdr:
+                d[k + (f" [{units[hdr.index(k)]}]" if units[hdr.index(k)] else "")] = r[hdr.index(k)]
+        res.append(d)
+    return res
+
+
+if __name__ == "__main__":
+    args = sys.argv[1:]
+    out = Path(args[args.index("--out") + 1])
+    out.mkdir(parents=True, exist_ok=True)
+    files = [a for a in args if not a.startswith("--") and a != str(out)]
+    for f in files:
+        name = Path(f).stem
+        data = launches(f) if f.endswith(".csv") else full(f)
+        (out / f"{name}.json").write_text(json.dumps(data, indent=1))
+        print(name, json.dumps(data[:8], indent=0)[:2500])
