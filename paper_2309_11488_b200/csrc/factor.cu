@@ -49,6 +49,14 @@ __device__ __forceinline__ int ld_flag_relaxed(const int* p) {
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 __device__ __forceinline__ void st_flag_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -78,12 +86,32 @@ __global__ void k_factor_pairs(int n, const int32_t* __restrict__ rp,
   }
 }
 
+// ---- per-row "simple" mark: <= kFast lower entries, each with at most one
+// update pair, every pair landing on the row's own diagonal.  The upper
+// blocks of a simple row are never modified by the factorisation, so its
+// consumers may read them before the row is finished.
+__global__ void k_factor_simple(int n, const int32_t* __restrict__ rp,
+                                const int32_t* __restrict__ diag,
+                                const int32_t* __restrict__ pptr,
+                                const int2* __restrict__ pairs, int8_t* simple) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int k0 = rp[i], d = diag[i];
+    bool ok = d - k0 <= kFast;
+    for (int k = k0; ok && k < d; ++k) {
+      const int b0 = pptr[k], b1 = pptr[k + 1];
+      if (b1 - b0 > 1 || (b1 > b0 && pairs[b0].x != d)) ok = false;
+    }
+    simple[i] = ok ? 1 : 0;
+  }
+}
+
 // ---- numeric phase
 template <int B>
 __global__ void __launch_bounds__(256) k_factor_numeric(
     SliceMap map, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
     const int32_t* __restrict__ diag, const int32_t* __restrict__ pptr,
-    const int2* __restrict__ pairs, double* w, double* invd, int* flag, int* bad, Tickets2* tk) {
+    const int2* __restrict__ pairs, const int8_t* __restrict__ simple_row, double* w,
+    double* invd, int* flag, int* bad, Tickets2* tk) {
   constexpr int BB = B * B;
   const int lane = threadIdx.x & 31;
   for (;;) {
@@ -94,32 +122,42 @@ __global__ void __launch_bounds__(256) k_factor_numeric(
     int k = 0, dpos = 0;
     int r = -1, pb = 0, pe = 0;
     int2 pq0 = make_int2(0, 0);
-    // fast path (stencil-like rows): <= kFast lower entries whose updates all
-    // land on the diagonal -- poll every pivot flag in one round, then load
-    // every pivot's inverse and U block in one round, then eliminate in order
+    // fast path: the row and all its pivots are "simple" (see k_factor_simple).
+    // Everything static (own blocks, the pivots' upper blocks) is prefetched
+    // at claim time; the only thing waited for is the pivots' inverse
+    // diagonals, polled directly (sentinel-initialised) -- one L2 round trip
+    // per dependency level, no flag, no fence on the consumer side.
     bool simple = false;
-    int fr[kFast], fq[kFast];
-    int nl = 0;
+    int fr[kFast], nl = 0;
+    double wik[kFast][BB], urq[kFast][BB], inv_r[kFast][BB], dblk[BB];
     if (!done) {
       k = rp[i];
       dpos = diag[i];
       nl = dpos - k;
-      simple = nl <= kFast;
+      simple = simple_row[i] != 0;
 #pragma unroll
       for (int t = 0; t < kFast; ++t) {
-        fr[t] = 0; fq[t] = -1;
+        fr[t] = 0;
         if (simple && t < nl) {
           fr[t] = ci[k + t];
-          const int b0 = pptr[k + t], b1 = pptr[k + t + 1];
-          if (b1 - b0 > 1) simple = false;
-          if (b1 > b0) {
-            const int2 pq = pairs[b0];
-            if (pq.x != dpos) simple = false;
-            fq[t] = pq.y;
-          }
+          if (!simple_row[fr[t]]) simple = false;
         }
       }
-      if (!simple && k < dpos) {  // static data of the first pivot
+      if (simple) {
+#pragma unroll
+        for (int t = 0; t < kFast; ++t) {
+          const int b0 = t < nl ? pptr[k + t] : 0, b1 = t < nl ? pptr[k + t + 1] : 0;
+          const int q = b1 > b0 ? pairs[b0].y : -1;
+#pragma unroll
+          for (int e = 0; e < BB; ++e) {
+            wik[t][e] = t < nl ? w[(long long)(k + t) * BB + e] : 0.0;
+            urq[t][e] = q >= 0 ? __ldcg(w + (long long)q * BB + e) : 0.0;
+            inv_r[t][e] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < BB; ++e) dblk[e] = w[(long long)dpos * BB + e];
+      } else if (k < dpos) {  // static data of the first pivot (general path)
         r = ci[k]; pb = pptr[k]; pe = pptr[k + 1];
         if (pb < pe) pq0 = pairs[pb];
       }
@@ -127,37 +165,31 @@ __global__ void __launch_bounds__(256) k_factor_numeric(
     unsigned int fpend = simple ? ((1u << nl) - 1u) : 0u;
     for (;;) {
       if (!done && simple) {
-        int fl[kFast];
-#pragma unroll
-        for (int t = 0; t < kFast; ++t) fl[t] = (fpend & (1u << t)) ? ld_flag_relaxed(flag + fr[t]) : 0;
+        const unsigned int todo = fpend;
 #pragma unroll
         for (int t = 0; t < kFast; ++t)
-          if ((fpend & (1u << t)) && fl[t]) fpend &= ~(1u << t);
+          if (todo & (1u << t)) {
+#pragma unroll
+            for (int e = 0; e < BB; ++e) inv_r[t][e] = ld_relaxed_f64(invd + (long long)fr[t] * BB + e);
+          }
+#pragma unroll
+        for (int t = 0; t < kFast; ++t) {
+          bool miss = false;
+#pragma unroll
+          for (int e = 0; e < BB; ++e) miss |= is_sentinel(inv_r[t][e]);
+          if ((todo & (1u << t)) && !miss) fpend &= ~(1u << t);
+        }
         if (!fpend) {
-          double inv_r[kFast][BB], urq[kFast][BB], dblk[BB];
-#pragma unroll
-          for (int t = 0; t < kFast; ++t)
-#pragma unroll
-            for (int e = 0; e < BB; ++e) {
-              inv_r[t][e] = t < nl ? __ldcg(invd + (long long)fr[t] * BB + e) : 0.0;
-              urq[t][e] = (t < nl && fq[t] >= 0) ? __ldcg(w + (long long)fq[t] * BB + e) : 0.0;
-            }
-#pragma unroll
-          for (int e = 0; e < BB; ++e) dblk[e] = w[(long long)dpos * BB + e];
 #pragma unroll
           for (int t = 0; t < kFast; ++t) {
             if (t < nl) {
-              double wik[BB], l[BB], prod[BB];
-#pragma unroll
-              for (int e = 0; e < BB; ++e) wik[e] = w[(long long)(k + t) * BB + e];
-              matmul<B>(wik, inv_r[t], l);  // L_ir = A_ir inv(U_rr)
+              double l[BB], prod[BB];
+              matmul<B>(wik[t], inv_r[t], l);  // L_ir = A_ir inv(U_rr)
 #pragma unroll
               for (int e = 0; e < BB; ++e) w[(long long)(k + t) * BB + e] = l[e];
-              if (fq[t] >= 0) {
-                matmul<B>(l, urq[t], prod);  // A_ii -= L_ir U_ri
+              matmul<B>(l, urq[t], prod);      // A_ii -= L_ir U_ri (zero block: no pair)
 #pragma unroll
-                for (int e = 0; e < BB; ++e) dblk[e] -= prod[e];
-              }
+              for (int e = 0; e < BB; ++e) dblk[e] -= prod[e];
             }
           }
           double inv[BB];
@@ -165,8 +197,8 @@ __global__ void __launch_bounds__(256) k_factor_numeric(
           for (int e = 0; e < BB; ++e) w[(long long)dpos * BB + e] = dblk[e];
           if (!invert_block<B>(dblk, inv)) atomicMin(bad, i);
 #pragma unroll
-          for (int e = 0; e < BB; ++e) invd[(long long)i * BB + e] = inv[e];
-          st_flag_release(flag + i, 1);
+          for (int e = 0; e < BB; ++e) st_relaxed_f64(invd + (long long)i * BB + e, canon(inv[e]));
+          st_flag_release(flag + i, 1);  // for general-path consumers
           done = true;
         }
       }
@@ -215,7 +247,7 @@ __global__ void __launch_bounds__(256) k_factor_numeric(
           for (int e = 0; e < BB; ++e) dblk[e] = w[(long long)dpos * BB + e];
           if (!invert_block<B>(dblk, inv)) atomicMin(bad, i);
 #pragma unroll
-          for (int e = 0; e < BB; ++e) invd[(long long)i * BB + e] = inv[e];
+          for (int e = 0; e < BB; ++e) st_relaxed_f64(invd + (long long)i * BB + e, canon(inv[e]));
           st_flag_release(flag + i, 1);  // publishes this row's L, U and inverse
           done = true;
         }
@@ -227,16 +259,20 @@ __global__ void __launch_bounds__(256) k_factor_numeric(
 
 template <int B>
 int launch_numeric(SliceMap map, const int32_t* rp, const int32_t* ci, const int32_t* diag,
-                   const int32_t* pptr, const int2* pairs, double* w, double* invd, int* flag,
+                   const int32_t* pptr, const int2* pairs, const int8_t* simple, double* w,
+                   double* invd, int* flag,
                    int* bad, Tickets2* tk, cudaStream_t st) {
   int per_sm = 0, dev = 0, sms = kSms;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_factor_numeric<B>, 256, 0);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int g = (per_sm < 1 ? 1 : per_sm) * sms;
-  k_factor_numeric<B><<<g, 256, 0, st>>>(map, rp, ci, diag, pptr, pairs, w, invd, flag, bad, tk);
+  k_factor_numeric<B><<<g, 256, 0, st>>>(map, rp, ci, diag, pptr, pairs, simple, w, invd, flag,
+                                         bad, tk);
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
+
+int fill_sentinel(long long m, double* v, cudaStream_t st);  // ilu0.cu
 
 inline int grid_rows(long long work) {
   long long g = (work + 255) / 256;
@@ -292,20 +328,26 @@ int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_
   int2* pairs = nullptr;
   B2S_CHECK(cudaMallocAsync(&pairs, sizeof(int2) * (npairs > 0 ? npairs : 1), st));
   k_factor_pairs<<<grid_rows(n), 256, 0, st>>>(n, rp, ci, diag, nullptr, pptr, pairs);
+  int8_t* simple = nullptr;
+  B2S_CHECK(cudaMallocAsync(&simple, n, st));
+  k_factor_simple<<<grid_rows(n), 256, 0, st>>>(n, rp, diag, pptr, pairs, simple);
+  // the inverse diagonals double as the fast path's "ready" marks
+  if (int rcf = fill_sentinel((long long)n * b * b, inv_diag, st)) return rcf;
   B2S_LAUNCH_CHECK();
   SliceMap map{nslices, row0, nrows};
   int rc;
   switch (b) {
-    case 1: rc = launch_numeric<1>(map, rp, ci, diag, pptr, pairs, vals, inv_diag, flag, bad, tk, st); break;
-    case 2: rc = launch_numeric<2>(map, rp, ci, diag, pptr, pairs, vals, inv_diag, flag, bad, tk, st); break;
-    case 3: rc = launch_numeric<3>(map, rp, ci, diag, pptr, pairs, vals, inv_diag, flag, bad, tk, st); break;
-    default: rc = launch_numeric<4>(map, rp, ci, diag, pptr, pairs, vals, inv_diag, flag, bad, tk, st); break;
+    case 1: rc = launch_numeric<1>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, st); break;
+    case 2: rc = launch_numeric<2>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, st); break;
+    case 3: rc = launch_numeric<3>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, st); break;
+    default: rc = launch_numeric<4>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, st); break;
   }
   if (rc != B2S_OK) return rc;
   int h = big;
   B2S_CHECK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   B2S_CHECK(cudaFreeAsync(tmp, st));
   B2S_CHECK(cudaFreeAsync(pairs, st));
+  B2S_CHECK(cudaFreeAsync(simple, st));
   B2S_CHECK(cudaFreeAsync(cnt, st));
   B2S_CHECK(cudaFreeAsync(pptr, st));
   B2S_CHECK(cudaFreeAsync(flag, st));

@@ -43,10 +43,12 @@ def main():
                 print(json.dumps({"backend": name, **t}), flush=True)
     # fine-grained: profile one level setup with torch profiler (kernel times)
     from torch.profiler import ProfilerActivity, profile
-    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        DeviceSolver(a, bsr, P.SolverConfig()).setup()
-        torch.cuda.synchronize()
-    print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25))
+    for be in (P.Backend.GRAPH_COLORED, P.Backend.LEVEL_SCHEDULED):
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            DeviceSolver(a, bsr, P.SolverConfig(backend=be)).setup()
+            torch.cuda.synchronize()
+        print(be, prof.key_averages().table(sort_by="cuda_time_total", row_limit=14,
+                                            max_name_column_width=40))
 
 
 if __name__ == "__main__":
