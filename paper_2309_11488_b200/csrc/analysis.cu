@@ -54,9 +54,6 @@ constexpr int kNb = 8;
 
 // level(i) = 1 + max level(j) over strict-lower j, 0 without lower
 // neighbours (bs/analysis.py:85-100).  level[] must be -1 on entry.
-// Neighbours inside the warp's own slice (in natural order row i-1 is
-// usually one) are read from the producing lane with a shuffle, so a chain
-// inside a slice costs shuffle rounds, not L2 round trips.
 __global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
                                   const int32_t* __restrict__ ci, int32_t* level,
                                   unsigned int* ticket) {
@@ -71,7 +68,7 @@ __global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
     bool done = i >= n;
     int nb[kNb];
     int cnt = 0, k = 0, end = 0;
-    unsigned int pin = 0, pout = 0;
+    bool longrow = false;
     if (!done) {
       k = rp[i];
       end = rp[i + 1];
@@ -82,51 +79,44 @@ __global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
 #pragma unroll
           for (int t = 0; t < kNb; ++t)
             if (t == cnt) nb[t] = j;
-          if (j >= row0) pin |= 1u << cnt; else pout |= 1u << cnt;
         }
         ++cnt;
       }
+      longrow = cnt > kNb;
     }
-    const bool longrow = cnt > kNb;
-    if (longrow) pin = pout = 0;
-    int best = -1, mine = -1;
+    unsigned int pend = (!done && !longrow) ? ((1u << cnt) - 1u) : 0u;
+    int best = -1;
     for (;;) {
-      // one round of global polls for neighbours outside the slice
-      if (!done && !longrow && pout) {
-        int got[kNb];
+      if (!done) {
+        if (!longrow) {
+          int got[kNb];
 #pragma unroll
-        for (int t = 0; t < kNb; ++t) got[t] = (pout & (1u << t)) ? ld_relaxed_i(level + nb[t]) : -1;
+          for (int t = 0; t < kNb; ++t)
+            got[t] = (pend & (1u << t)) ? ld_relaxed_i(level + nb[t]) : -1;
 #pragma unroll
-        for (int t = 0; t < kNb; ++t)
-          if ((pout & (1u << t)) && got[t] >= 0) { best = max(best, got[t]); pout &= ~(1u << t); }
-      }
-      if (!done && longrow) {
-        while (k < end) {
-          const int j = ci[k];
-          if (j >= i) { k = end; break; }
-          const int lj = ld_relaxed_i(level + j);
-          if (lj < 0) break;
-          best = max(best, lj);
-          ++k;
+          for (int t = 0; t < kNb; ++t)
+            if ((pend & (1u << t)) && got[t] >= 0) {
+              best = max(best, got[t]);
+              pend &= ~(1u << t);
+            }
+          if (!pend) {
+            st_relaxed_i(level + i, best + 1);
+            done = true;
+          }
+        } else {
+          while (k < end) {
+            const int j = ci[k];
+            if (j >= i) { k = end; break; }
+            const int lj = ld_relaxed_i(level + j);
+            if (lj < 0) break;  // not yet published
+            best = max(best, lj);
+            ++k;
+          }
+          if (k >= end) {
+            st_relaxed_i(level + i, best + 1);
+            done = true;
+          }
         }
-        if (k >= end) { mine = best + 1; st_relaxed_i(level + i, mine); done = true; }
-      }
-      // shuffle rounds for neighbours inside the slice, until no lane moves
-      for (;;) {
-        bool moved = false;
-#pragma unroll
-        for (int t = 0; t < kNb; ++t) {
-          const bool in = (pin >> t) & 1u;
-          const int v = __shfl_sync(0xffffffffu, mine, in ? nb[t] - (int)row0 : lane);
-          if (in && v >= 0) { best = max(best, v); pin &= ~(1u << t); }
-        }
-        if (!done && !longrow && !pin && !pout) {
-          mine = best + 1;
-          st_relaxed_i(level + i, mine);
-          done = true;
-          moved = true;
-        }
-        if (!__any_sync(0xffffffffu, moved)) break;
       }
       if (__all_sync(0xffffffffu, done)) break;
     }
@@ -138,8 +128,7 @@ __global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
 // adjacency (bs/analysis.py:103-145): colour(i) = mex of the colours of the
 // neighbours j < i, where j is a neighbour if (i,j) or (j,i) is stored.
 // The (j,i) half comes from `ut_ptr/ut_idx`: for every column c, the rows
-// j < c that store (j, c).  colour[] must be -1 on entry.  Same polling
-// scheme as the level schedule (global round + in-slice shuffle rounds).
+// j < c that store (j, c).  colour[] must be -1 on entry.
 __device__ __forceinline__ int mex64(unsigned long long used) {
   return used == ~0ull ? 64 : __ffsll((long long)~used) - 1;
 }
@@ -161,70 +150,70 @@ __global__ void k_color_sync_free(int n, const int32_t* __restrict__ rp,
     bool done = i >= n;
     int nb[kC];
     int cnt = 0;
-    unsigned int pin = 0, pout = 0;
     if (!done) {
-      for (int pass = 0; pass < 2; ++pass) {
-        const int q0 = pass == 0 ? rp[i] : ut_ptr[i];
-        const int q1 = pass == 0 ? rp[i + 1] : ut_ptr[i + 1];
-        for (int q = q0; q < q1; ++q) {
-          const int j = pass == 0 ? ci[q] : ut_idx[q];
-          if (pass == 0 && j >= i) break;
-          if (cnt < kC) {
+      for (int q = rp[i]; q < rp[i + 1]; ++q) {
+        const int j = ci[q];
+        if (j >= i) break;
+        if (cnt < kC) {
 #pragma unroll
-            for (int t = 0; t < kC; ++t)
-              if (t == cnt) nb[t] = j;
-            if (j >= row0) pin |= 1u << cnt; else pout |= 1u << cnt;
-          }
-          ++cnt;
+          for (int t = 0; t < kC; ++t)
+            if (t == cnt) nb[t] = j;
         }
+        ++cnt;
+      }
+      const int nrow = cnt;  // the row's own lower neighbours come first
+      for (int q = ut_ptr[i]; q < ut_ptr[i + 1]; ++q) {
+        const int j = ut_idx[q];
+        bool dup = false;  // (j,i) and (i,j) both stored: one neighbour
+#pragma unroll
+        for (int t = 0; t < kC; ++t)
+          if (t < nrow && t < kC && nb[t] == j) dup = true;
+        if (dup) continue;
+        if (cnt < kC) {
+#pragma unroll
+          for (int t = 0; t < kC; ++t)
+            if (t == cnt) nb[t] = j;
+        }
+        ++cnt;
       }
     }
     const bool longrow = cnt > kC;
-    if (longrow) pin = pout = 0;
+    unsigned int pend = (!done && !longrow) ? (cnt == 32 ? ~0u : ((1u << cnt) - 1u)) : 0u;
     unsigned long long used = 0ull;  // colours 0..63 seen
     bool big = false;                 // some neighbour has colour >= 64
-    int mine = -1;
+    // long lists: phase 0 walks the row, phase 1 the transposed list
     int k = done ? 0 : rp[i], end = done ? 0 : rp[i + 1], phase = 0;
     for (;;) {
-      bool ready = false;
-      if (!done && !longrow && pout) {
-        int got[kC];
+      if (!done) {
+        bool ready = false;
+        if (!longrow) {
+          int got[kC];
 #pragma unroll
-        for (int t = 0; t < kC; ++t) got[t] = (pout & (1u << t)) ? ld_relaxed_i(color + nb[t]) : -1;
+          for (int t = 0; t < kC; ++t)
+            got[t] = (pend & (1u << t)) ? ld_relaxed_i(color + nb[t]) : -1;
 #pragma unroll
-        for (int t = 0; t < kC; ++t)
-          if ((pout & (1u << t)) && got[t] >= 0) {
-            if (got[t] < 64) used |= 1ull << got[t]; else big = true;
-            pout &= ~(1u << t);
+          for (int t = 0; t < kC; ++t)
+            if ((pend & (1u << t)) && got[t] >= 0) {
+              if (got[t] < 64) used |= 1ull << got[t]; else big = true;
+              pend &= ~(1u << t);
+            }
+          ready = !pend;
+        } else {
+          for (;;) {
+            if (k >= end) {
+              if (phase == 0) { phase = 1; k = ut_ptr[i]; end = ut_ptr[i + 1]; continue; }
+              break;
+            }
+            const int j = (phase == 0) ? ci[k] : ut_idx[k];
+            if (phase == 0 && j >= i) { k = end; continue; }
+            const int cj = ld_relaxed_i(color + j);
+            if (cj < 0) break;
+            if (cj < 64) used |= 1ull << cj; else big = true;
+            ++k;
           }
-      }
-      if (!done && longrow) {
-        for (;;) {
-          if (k >= end) {
-            if (phase == 0) { phase = 1; k = ut_ptr[i]; end = ut_ptr[i + 1]; continue; }
-            break;
-          }
-          const int j = (phase == 0) ? ci[k] : ut_idx[k];
-          if (phase == 0 && j >= i) { k = end; continue; }
-          const int cj = ld_relaxed_i(color + j);
-          if (cj < 0) break;
-          if (cj < 64) used |= 1ull << cj; else big = true;
-          ++k;
+          ready = phase == 1 && k >= end;
         }
-        ready = phase == 1 && k >= end;
-      }
-      for (;;) {
-        bool moved = false;
-#pragma unroll
-        for (int t = 0; t < kC; ++t) {
-          const bool in = (pin >> t) & 1u;
-          const int v = __shfl_sync(0xffffffffu, mine, in ? nb[t] - (int)row0 : lane);
-          if (in && v >= 0) {
-            if (v < 64) used |= 1ull << v; else big = true;
-            pin &= ~(1u << t);
-          }
-        }
-        if (!done && (ready || (!longrow && !pin && !pout))) {
+        if (ready) {
           int c = mex64(used);
           if (big && c >= 64) {
             // rare: >= 64 distinct neighbour colours; walk the set directly
@@ -239,12 +228,9 @@ __global__ void k_color_sync_free(int n, const int32_t* __restrict__ rp,
               if (hit) ++c;
             }
           }
-          mine = c;
           st_relaxed_i(color + i, c);
           done = true;
-          moved = true;
         }
-        if (!__any_sync(0xffffffffu, moved)) break;
       }
       if (__all_sync(0xffffffffu, done)) break;
     }
