@@ -70,6 +70,11 @@ int b2s_permute_bsr(int n, int b, const int32_t* rp, const int32_t* ci, const do
 int b2s_gather_rows(int n, int b, const int32_t* src, const double* in, double* out,
                     cudaStream_t stream);
 
+/* int64 -> int32 index narrowing on the device; *overflow_host = 1 when a
+ * value does not fit (the host raises). */
+int b2s_narrow_index(long long m, const int64_t* in, int32_t* out, int* overflow_host,
+                     cudaStream_t stream);
+
 /* block gather out[q] = in[src[q]] (refresh_values, bs/jacobi.py:139-147). */
 int b2s_gather_blocks(long long nblk, int b, const int32_t* src, const double* in, double* out,
                       cudaStream_t stream);

@@ -54,7 +54,18 @@ def ptr(t: torch.Tensor | None) -> int | None:
 
 
 def i32(a: np.ndarray, dev) -> torch.Tensor:
+    """int32 device copy of an index array.  Large int64 arrays travel as they
+    are and are narrowed (and range-checked) by a device kernel."""
     a = np.asarray(a)
+    if a.dtype == np.int64 and a.size >= (1 << 16):
+        raw = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        out = torch.empty(a.size, dtype=torch.int32, device=dev)
+        bad = C.c_int(0)
+        check(lib().b2s_narrow_index(a.size, ptr(raw), ptr(out), C.byref(bad), stream()),
+              "narrow_index")
+        if bad.value:
+            raise ValueError("index does not fit the device's int32 indices")
+        return out
     if a.size and (a.max() > _I32_MAX or a.min() < -_I32_MAX):
         raise ValueError("index does not fit the device's int32 indices")
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev, non_blocking=False)
@@ -103,11 +114,43 @@ class DevBSR:
     vals: torch.Tensor
 
     @classmethod
-    def upload(cls, m) -> "DevBSR":
+    def upload(cls, m, overlap: bool = False) -> "DevBSR":
+        """Pattern first, then the values.  With ``overlap`` the value copy
+        (the bulk of the bytes) runs on a side stream from a helper thread
+        while the caller goes on with pattern-only work (the analysis);
+        ``wait_values()`` orders the current stream after it."""
         m = m.as_block_row_major()
         pat = DevPattern.upload(m.pattern)
-        vals = f64(m.values, pat.rp.device) if m.values.size else empty_f64(1, pat.rp.device)
-        return cls(pat, int(m.block_size), vals)
+        dev = pat.rp.device
+        if not m.values.size:
+            return cls(pat, int(m.block_size), empty_f64(1, dev))
+        out = cls(pat, int(m.block_size), torch.empty(m.values.size, dtype=torch.float64,
+                                                       device=dev))
+        if not overlap:
+            out.vals.copy_(torch.from_numpy(m.values))
+            return out
+        import threading
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        done = torch.cuda.Event()
+        src = torch.from_numpy(m.values)
+
+        def copy():
+            with torch.cuda.stream(side):
+                out.vals.copy_(src)
+                done.record(side)
+        th = threading.Thread(target=copy, daemon=True)
+        th.start()
+        out._pending = (th, done)
+        return out
+
+    def wait_values(self):
+        pending = getattr(self, "_pending", None)
+        if pending is not None:
+            th, ev = pending
+            th.join()
+            torch.cuda.current_stream().wait_event(ev)
+            self._pending = None
 
 
 def find_diagonal(p: DevPattern) -> torch.Tensor:

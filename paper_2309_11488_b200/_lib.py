@@ -51,6 +51,7 @@ SIGNATURES = {
     "b2s_plan_from_groups": (_I, [_I, _P, _I, _P, _P, _P, _P]),
     "b2s_permute_bsr": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "b2s_gather_rows": (_I, [_I, _I, _P, _P, _P, _P]),
+    "b2s_narrow_index": (_I, [_LL, _P, _P, C.POINTER(C.c_int), _P]),
     "b2s_gather_blocks": (_I, [_LL, _I, _P, _P, _P, _P]),
     "b2s_slices_plain": (_I, [_I, _P, _P, _P]),
     "b2s_slices_grouped_count": (_I, [_I, _P, _P, _PI, _P]),

@@ -103,6 +103,8 @@ class DeviceSolver:
     def setup(self, backend: Backend | None = None):
         backend = backend or self.cfg.backend
         self.plan = plan_device(backend, self.pre_bsr.pat)
+        self.pre_bsr.wait_values()   # values may still be in flight (overlapped upload)
+        self.bsr.wait_values()
         self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr)
         a_perm = self.fact._a_perm if self.pre_bsr is self.bsr else None
         if a_perm is None:
@@ -149,17 +151,18 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     n, bs = a_sys.num_block_rows, a_sys.block_size
     if b.block_size != bs or b.num_blocks != n:
         raise ShapeError("right-hand side does not match the operator")
-    if x0 is None:
-        x0 = BlockVector.zeros(n, bs)
-    elif x0.block_size != bs or x0.num_blocks != n:
+    if x0 is not None and (x0.block_size != bs or x0.num_blocks != n):
         raise ShapeError("initial guess does not match the right-hand side")
     if n == 0:
         rep = SolveReport(True, 0.0, 0.0, 0.0, 0.0, 0)
-        return BlockVector(x0.data.copy(), bs), rep
+        return BlockVector(np.zeros(0) if x0 is None else x0.data.copy(), bs), rep
     dev = D.require_cuda()
-    bsr = D.DevBSR.upload(a_sys)
+    # the 72 B/block values (the bulk of the upload) travel while the device
+    # analyses the pattern; the solve waits for them only at factorisation
+    bsr = D.DevBSR.upload(a_sys, overlap=cfg.jacobi_partitions == 0)
     rhs = D.f64(b.data, dev)
-    x0d = D.f64(x0.data, dev)
+    x0d = (torch.zeros(n * bs, dtype=torch.float64, device=dev) if x0 is None
+           else D.f64(x0.data, dev))
 
     pre_bsr, pre_mat = bsr, a_sys
     primary = None

@@ -351,6 +351,18 @@ __global__ void k_gather_rows(int n, int b, const int32_t* __restrict__ src,
   }
 }
 
+__global__ void k_narrow(long long m, const int64_t* __restrict__ in, int32_t* __restrict__ out,
+                         int* overflow) {
+  int bad = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int64_t v = in[t];
+    bad |= (v > 0x7fffffffll || v < -0x7fffffffll);
+    out[t] = (int32_t)v;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(overflow, 1);
+}
+
 inline int grid_for(long long work, int threads = 256) {
   long long g = (work + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -540,6 +552,25 @@ int b2s_gather_rows(int n, int b, const int32_t* src, const double* in, double* 
   if (n == 0) return B2S_OK;
   k_gather_rows<<<grid_for((long long)n * b), 256, 0, st>>>(n, b, src, in, out);
   B2S_LAUNCH_CHECK();
+  return B2S_OK;
+}
+
+// int64 -> int32 index narrowing on the device (the reference's patterns
+// are int64, bs/blockcore.py:83-84); *overflow_host = 1 if a value does not
+// fit.  Saves the host a conversion pass over the column indices.
+int b2s_narrow_index(long long m, const int64_t* in, int32_t* out, int* overflow_host,
+                     cudaStream_t st) {
+  *overflow_host = 0;
+  if (m < 0) return B2S_SHAPE;
+  if (m == 0) return B2S_OK;
+  int* d = nullptr;
+  B2S_CHECK(cudaMallocAsync(&d, sizeof(int), st));
+  B2S_CHECK(cudaMemsetAsync(d, 0, sizeof(int), st));
+  k_narrow<<<grid_for(m), 256, 0, st>>>(m, in, out, d);
+  B2S_LAUNCH_CHECK();
+  B2S_CHECK(cudaMemcpyAsync(overflow_host, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(d, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
   return B2S_OK;
 }
 
