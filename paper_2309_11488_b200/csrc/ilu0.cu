@@ -29,6 +29,24 @@ struct Tickets {
 // Claim the next ticket for the calling warp; returns -1 once exhausted
 // (after registering the warp's exit; the last warp out resets the pair so
 // the kernel can be relaunched or graph-replayed without a memset).
+__device__ __forceinline__ long long claim(Tickets* tk, int nslices);
+
+// Next slice ticket of the calling warp: dynamic (one atomic per slice) or,
+// with flags bit 2, static round-robin over the persistent grid's warps --
+// warp w takes tickets w, w+W, ... in order, which is deadlock-free for the
+// same reason (every warp's earlier tickets are lower, all warps resident)
+// and spares the single hot counter ~30k serialised atomics per sweep.
+__device__ __forceinline__ long long next_slice(Tickets* tk, int nslices, int flags,
+                                                long long& iter) {
+  if (flags & 4) {
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long t = gw + (iter++) * nw;
+    return t < nslices ? t : -1;
+  }
+  return claim(tk, nslices);
+}
+
 __device__ __forceinline__ long long claim(Tickets* tk, int nslices) {
   const int lane = threadIdx.x & 31;
   unsigned int t = 0;
@@ -114,8 +132,9 @@ __global__ void __launch_bounds__(256) k_ilu0_forward(SliceMap map, Sell lo,
   constexpr int BB = B * B;
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
+  long long iter = 0;
   for (;;) {
-    const long long s = claim(tk, map.nslices);
+    const long long s = next_slice(tk, map.nslices, flags, iter);
     if (s < 0) break;
     const bool ok = lane < map.nrows[s];
     const long long i = (long long)map.row0[s] + lane;
@@ -166,8 +185,9 @@ __global__ void __launch_bounds__(256) k_ilu0_backward(SliceMap map, Sell up,
   constexpr int BB = B * B;
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
+  long long iter = 0;
   for (;;) {
-    const long long t = claim(tk, map.nslices);
+    const long long t = next_slice(tk, map.nslices, flags, iter);
     if (t < 0) break;
     const long long s = map.nslices - 1 - t;
     const bool ok = lane < map.nrows[s];

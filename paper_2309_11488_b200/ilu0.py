@@ -56,7 +56,11 @@ class Ilu0Factorization:
         self._combined = None
         self._inv_host = None
         self._tickets = torch.zeros(8, dtype=torch.int32, device=invd.device)
-        self.sweep_flags = 0
+        # measured on B200 (tools/sweep_bench.py): few groups (colourings) are
+        # bandwidth-bound -> static slice order, no ticket atomics (0.77 of
+        # peak vs 0.68); deep level schedules are latency-bound -> dynamic
+        # tickets on one CTA per SM (1.10 vs 1.39 us per level)
+        self.sweep_flags = 0x4 if plan.group_count <= 16 else 0x10
         self.tiles = None        # b2s_tiles_create handle (tiled level sweeps), or None
 
     # -- reference attributes --------------------------------------------------

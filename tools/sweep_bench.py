@@ -66,7 +66,7 @@ def main():
         torch.cuda.synchronize()
         phases["operator_layout_ms"] = (time.perf_counter() - t) * 1e3
         print(json.dumps({"plan": name, "groups": plan.group_count, **phases}))
-        for flags in (0, 0x10, 0x410, 0x210, 0x20, 0x420, 0x810):
+        for flags in (0, 4, 0x14, 0x24, 0x414, 0x10):
             f.sweep_flags = flags
             us_apply = ev_time(lambda: f.apply_device(x, z))
             us_fill = ev_time(lambda: (D.fill_sentinel(y, m), D.fill_sentinel(z, m)))
