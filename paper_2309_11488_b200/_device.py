@@ -58,7 +58,8 @@ def i32(a: np.ndarray, dev) -> torch.Tensor:
     are and are narrowed (and range-checked) by a device kernel."""
     a = np.asarray(a)
     if a.dtype == np.int64 and a.size >= (1 << 16):
-        raw = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        src = torch.from_numpy(np.ascontiguousarray(a))
+        raw = src.to(dev, non_blocking=is_pinned(src))
         out = torch.empty(a.size, dtype=torch.int32, device=dev)
         bad = C.c_int(0)
         check(lib().b2s_narrow_index(a.size, ptr(raw), ptr(out), C.byref(bad), stream()),
@@ -72,7 +73,56 @@ def i32(a: np.ndarray, dev) -> torch.Tensor:
 
 
 def f64(a: np.ndarray, dev) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+    src = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    return src.to(dev, non_blocking=is_pinned(src))
+
+
+def is_pinned(t: torch.Tensor) -> bool:
+    """Page-locked host memory (cudaHostAlloc / torch pin_memory): copies from
+    it are plain DMA and can run asynchronously."""
+    try:
+        return bool(t.numel()) and t.is_pinned()
+    except RuntimeError:
+        return False
+
+
+def pinned_empty(n: int, dtype=np.float64) -> np.ndarray:
+    """A numpy array backed by page-locked host memory (torch's caching host
+    allocator: freed arrays go back to a pool, so repeated solves reuse them)."""
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64,
+           np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+    return torch.empty(int(n), dtype=tdt, pin_memory=True).numpy()
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    out = pinned_empty(np.asarray(a).size, np.asarray(a).dtype)
+    out[:] = np.asarray(a).reshape(-1)
+    return out.reshape(np.shape(a))
+
+
+def pin_host(obj):
+    """Copy of a BlockMatrix / BlockVector (or array) whose arrays live in
+    page-locked host memory -- what an assembler hands the solver when the
+    upload should run at DMA speed."""
+    from .blockcore import BlockMatrix, BlockVector, SparsityPattern
+    if isinstance(obj, BlockMatrix):
+        p = obj.pattern
+        pat = SparsityPattern(p.num_block_rows, pinned_copy(p.row_pointers),
+                              pinned_copy(p.column_indices))
+        return BlockMatrix(pat, obj.block_size, pinned_copy(obj.values), obj.layout)
+    if isinstance(obj, BlockVector):
+        return BlockVector(pinned_copy(obj.data), obj.block_size)
+    return pinned_copy(obj)
+
+
+def to_host(v: torch.Tensor, count: int) -> np.ndarray:
+    """D2H of the first ``count`` elements into page-locked memory (fast DMA;
+    the returned array owns a pinned block of the caching host allocator)."""
+    out = torch.empty(int(count), dtype=v.dtype, pin_memory=True)
+    if count:
+        out.copy_(v[: int(count)], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    return out.numpy()
 
 
 def empty_i32(n, dev):
@@ -126,14 +176,21 @@ class DevBSR:
             return cls(pat, int(m.block_size), empty_f64(1, dev))
         out = cls(pat, int(m.block_size), torch.empty(m.values.size, dtype=torch.float64,
                                                        device=dev))
+        src = torch.from_numpy(m.values)
+        pinned = is_pinned(src)
         if not overlap:
-            out.vals.copy_(torch.from_numpy(m.values))
+            out.vals.copy_(src, non_blocking=pinned)
             return out
-        import threading
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
         done = torch.cuda.Event()
-        src = torch.from_numpy(m.values)
+        if pinned:   # page-locked: the DMA is asynchronous, no helper thread needed
+            with torch.cuda.stream(side):
+                out.vals.copy_(src, non_blocking=True)
+                done.record(side)
+            out._pending = (None, done)
+            return out
+        import threading
 
         def copy():
             with torch.cuda.stream(side):
@@ -148,7 +205,8 @@ class DevBSR:
         pending = getattr(self, "_pending", None)
         if pending is not None:
             th, ev = pending
-            th.join()
+            if th is not None:
+                th.join()
             torch.cuda.current_stream().wait_event(ev)
             self._pending = None
 

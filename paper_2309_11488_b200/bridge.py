@@ -189,7 +189,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         primary.setup_elapsed = time.perf_counter() - t0
 
     if primary.converged:
-        return BlockVector(x[: n * bs].cpu().numpy(), bs), primary
+        return BlockVector(D.to_host(x, n * bs), bs), primary
 
     fb_t0 = time.perf_counter()
     fb_stop = StoppingCriteria(cfg.stop.relative_reduction,
@@ -213,4 +213,4 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     report.elapsed += primary.elapsed
     if not report.converged:
         raise SolveFailed(primary, report)
-    return BlockVector(xd[: n * bs].cpu().numpy(), bs), report
+    return BlockVector(D.to_host(xd, n * bs), bs), report

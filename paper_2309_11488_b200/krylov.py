@@ -267,7 +267,7 @@ def _bicgstab_native(op: MatrixOperator, fact, b: BlockVector, x0: BlockVector,
     res = kr.solve(bd, xd, stop)
     if perm:
         xd = D.gather_rows(xd, fact.plan.device("permutation"), n, bs)
-    x = xd[: n * bs].cpu().numpy()
+    x = D.to_host(xd, n * bs)
     groups = fact.plan.group_count if fact is not None else 0
     rep = SolveReport(bool(res.converged), float(res.iterations), float(res.initial_norm),
                       float(res.final_norm), time.perf_counter() - t0, groups,
