@@ -266,10 +266,18 @@ def run_single(args):
 
     t_spmv = timed(lambda: D.spmv(kr.smap, kr.a, b, xp, yp, 1, xp, parts))
     t_apply = timed(lambda: f.apply_device(xp, zp))
-    t_fill = timed(lambda: (D.fill_sentinel(yp, m), D.fill_sentinel(zp, m)))
-    t_sweeps = max(t_apply - t_fill, 1e-3)
     spmv_bytes = nnz * 76 + (n + 1) * 4 + 48 * n
-    apply_bytes = (nnz - n) * 76 + 72 * n + 8 * (n + 1) + 96 * n
+    if f.phased:
+        # phased sweeps (colourings): no sentinel fills; the intermediate y of
+        # a 2-group plan is never stored, so the kernel's own minimum is r in,
+        # z out (48 B/row) instead of SURVEY §8(d)'s r->y->z (96 B/row)
+        t_sweeps = t_apply
+        apply_bytes = (nnz - n) * 76 + 72 * n + 8 * (n + 1) + \
+            (48 if f.plan.group_count == 2 else 96) * n
+    else:
+        t_fill = timed(lambda: (D.fill_sentinel(yp, m), D.fill_sentinel(zp, m)))
+        t_sweeps = max(t_apply - t_fill, 1e-3)
+        apply_bytes = (nnz - n) * 76 + 72 * n + 8 * (n + 1) + 96 * n
     hbm, peak_kind = peaks()
     spmv_gbs = spmv_bytes / (t_spmv * 1e-6) / 1e9
     apply_gbs = apply_bytes / (t_sweeps * 1e-6) / 1e9

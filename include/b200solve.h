@@ -132,6 +132,18 @@ int b2s_ilu0_apply(int n, int b, int kc, int nslices, const int32_t* row0, const
                    int flags, void* tickets, cudaStream_t stream);
 int b2s_fill_sentinel(long long m, double* v, cudaStream_t stream);
 
+/* Phased application (same result as b2s_ilu0_apply, bit for bit) for plans
+ * of 2..32 independent groups with no same-group entries -- every colouring:
+ * 2(G-1) data-parallel passes, no polling, no sentinel preconditions.
+ * gslice_host[0..G]: first slice of each group of the group-aligned slice
+ * map (HOST memory); goff1: first plan row of group 1. */
+int b2s_ilu0_apply_phased(int n, int b, int kc, int ngroups, const int32_t* gslice_host,
+                          int goff1, const int32_t* row0, const int32_t* nrows,
+                          const int32_t* l_sp, const int32_t* l_cols, const double* l_vals,
+                          const int32_t* u_sp, const int32_t* u_cols, const double* u_vals,
+                          const double* dinv_tiles, const double* r, double* y, double* z,
+                          cudaStream_t stream);
+
 /* Tiled level-scheduled sweeps (csrc/tiles.cu): px*py column patches of an
  * nx x ny natural-order grid (px > 0) or T contiguous input-row ranges; one
  * co-resident CTA per tile, tile values in shared memory.  kc = max entries
@@ -184,6 +196,9 @@ typedef struct {
   double* x;    /* x0 on entry, solution on exit */
   double* work; /* b2s_bicgstab_workspace_bytes() */
   cudaStream_t stream;
+  /* phased sweeps (b2s_ilu0_apply_phased) when ngroups >= 2 */
+  int ngroups, goff1;
+  const int32_t* gslice_host;
 } b2s_bicg_args;
 
 typedef struct {

@@ -264,11 +264,16 @@ def gather_rows(v: torch.Tensor, src: torch.Tensor, n: int, b: int) -> torch.Ten
 # ---------------------------------------------------------------------------
 # slice maps and SELL-32 layouts
 
+PHASED_MAX_GROUPS = 32   # plans with at most this many groups may use phased sweeps
+
+
 @dataclass
 class SliceMap:
     nslices: int
     row0: torch.Tensor
     nrows: torch.Tensor
+    gslice_host: np.ndarray | None = None   # group g -> first slice (few-group plans)
+    goff1: int = 0                          # first row of group 1
 
     @classmethod
     def plain(cls, n: int, dev) -> "SliceMap":
@@ -287,7 +292,14 @@ class SliceMap:
         row0, nrows = empty_i32(ns.value, dev), empty_i32(ns.value, dev)
         check(lib().b2s_slices_grouped_fill(ngroups, ns.value, ptr(offsets), ptr(base),
                                             ptr(row0), ptr(nrows), stream()), "slices_grouped")
-        return cls(int(ns.value), row0, nrows)
+        out = cls(int(ns.value), row0, nrows)
+        if 2 <= ngroups <= PHASED_MAX_GROUPS:
+            # host copy of the group -> slice table: the phased sweeps launch
+            # one pass per group (the table is baked into the captured graph)
+            out.gslice_host = np.ascontiguousarray(base[: ngroups + 1].cpu().numpy(),
+                                                   dtype=np.int32)
+            out.goff1 = int(offsets[1].item())
+        return out
 
     @classmethod
     def singles(cls, n: int, dev) -> "SliceMap":

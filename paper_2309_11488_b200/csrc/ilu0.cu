@@ -240,6 +240,190 @@ __global__ void __launch_bounds__(256) k_ilu0_backward(SliceMap map, Sell up,
   }
 }
 
+template <int B>
+int occupancy_grid(const void* fn) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int dev = 0, sms = kSms;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms;
+}
+
+// ---------------------------------------------------------------------------
+// Phased sweeps for plans with few groups whose rows are independent sets
+// (every colouring; no same-group entries).  In plan order group 0 has no
+// strict-lower entries (y = r there) and the last group no strict-upper ones
+// (z = inv(U_ii) y there), so an application is 2(G-1) data-parallel passes
+// with no polling at all:
+//   forward  g = 1..G-1 : y_i = r_i - sum_k L_ik y_k   (y_k = r_k in group 0);
+//                         for the last group z_i = inv(U_ii) y_i directly;
+//   backward g = G-2..0 : z_i = inv(U_ii) (y_i - sum_k U_ik z_k)  (y_i = r_i in group 0).
+// For two colours that is two passes and the intermediate y is never stored.
+// Each row's arithmetic (ascending columns, acc then subtract, matvec with
+// the inverse diagonal) is exactly the sync-free sweeps' -- results are
+// bit-identical.  Dependencies come from earlier launches, so they are plain
+// read-only-path loads.
+// One entry at a time, like the SpMV: few registers, many resident warps
+// (the latency hiding comes from occupancy, not from register prefetch).
+template <int B>
+__device__ __forceinline__ void phase_row_sum(const Sell& m, int slot0, int width, int lane,
+                                              int goff1, const double* __restrict__ r,
+                                              const double* __restrict__ v, double (&acc)[B]) {
+  constexpr int BB = B * B;
+  for (int k = 0; k < width; ++k) {
+    const int col = __ldcs(m.cols + slot0 + 32 * k + lane);
+    if (col < 0) continue;   // padding (phased plans have no same-group entries)
+    double blk[BB], dep[B], pr[B];
+#pragma unroll
+    for (int e = 0; e < BB; ++e) blk[e] = __ldcs(m.vals + vidx(slot0, k, e, lane, BB));
+    const double* src = col < goff1 ? r : v;
+#pragma unroll
+    for (int c = 0; c < B; ++c) dep[c] = __ldg(src + (long long)col * B + c);
+    matvec<B>(blk, dep, pr);
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] += pr[c];
+  }
+}
+
+template <int B, int KC, bool LAST>
+__global__ void __launch_bounds__(256) k_phase_forward(int s0, int s1, int goff1, SliceMap map,
+                                                       Sell lo, const double* __restrict__ dtiles,
+                                                       const double* __restrict__ r,
+                                                       double* __restrict__ y,
+                                                       double* __restrict__ z, const int* done) {
+  constexpr int BB = B * B;
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long s = s0 + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < s1;
+       s += nw) {
+    const bool ok = lane < map.nrows[s];
+    const long long i = (long long)map.row0[s] + lane;
+    const int slot0 = lo.sp[s];
+    const int width = (lo.sp[s + 1] - slot0) >> 5;
+    double rv[B], acc[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      rv[c] = ok ? __ldcs(r + i * B + c) : 0.0;
+      acc[c] = 0.0;
+    }
+    double dinv[LAST ? BB : 1];
+    if (LAST) {
+#pragma unroll
+      for (int e = 0; e < BB; ++e) dinv[e] = __ldcs(dtiles + (s * BB + e) * 32 + lane);
+    }
+    phase_row_sum<B>(lo, slot0, width, lane, goff1, r, y, acc);
+    if (!ok) continue;
+    double tv[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) tv[c] = canon(rv[c] - acc[c]);
+    if (LAST) {
+      // backward row of the last group: no upper entries, acc = 0
+      double t2[B], out[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) t2[c] = tv[c] - 0.0;
+      matvec<B>(dinv, t2, out);
+#pragma unroll
+      for (int c = 0; c < B; ++c) z[i * B + c] = canon(out[c]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < B; ++c) y[i * B + c] = tv[c];
+    }
+  }
+}
+
+template <int B, int KC>
+__global__ void __launch_bounds__(256) k_phase_backward(int s0, int s1, int goff1, SliceMap map,
+                                                        Sell up, const double* __restrict__ dtiles,
+                                                        const double* __restrict__ r,
+                                                        const double* __restrict__ y,
+                                                        double* __restrict__ z, const int* done) {
+  constexpr int BB = B * B;
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long s = s0 + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < s1;
+       s += nw) {
+    const bool ok = lane < map.nrows[s];
+    const long long i = (long long)map.row0[s] + lane;
+    const int slot0 = up.sp[s];
+    const int width = (up.sp[s + 1] - slot0) >> 5;
+    const double* yin = (i < goff1) ? r : y;   // a slice lies in one group
+    double yv[B], acc[B], dinv[BB];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      yv[c] = ok ? __ldcs(yin + i * B + c) : 0.0;
+      acc[c] = 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < BB; ++e) dinv[e] = __ldcs(dtiles + (s * BB + e) * 32 + lane);
+    // upper entries point into later groups (never group 0): z only
+    phase_row_sum<B>(up, slot0, width, lane, 0, r, z, acc);
+    if (!ok) continue;
+    double tv[B], out[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) tv[c] = yv[c] - acc[c];
+    matvec<B>(dinv, tv, out);
+#pragma unroll
+    for (int c = 0; c < B; ++c) z[i * B + c] = canon(out[c]);
+  }
+}
+
+template <int B, int KC>
+int launch_phased_bk(int ngroups, const int32_t* gs, int goff1, SliceMap map, Sell lo, Sell up,
+                     const double* dt, const double* r, double* y, double* z, const int* done,
+                     cudaStream_t st) {
+  static int cap = 0;
+  if (!cap) cap = occupancy_grid<B>((const void*)k_phase_forward<B, KC, true>);
+  auto grid = [&](int ns) {
+    long long g = ((long long)ns + 7) / 8;  // 8 warps per CTA, one slice each
+    return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+  };
+  for (int g = 1; g < ngroups; ++g) {
+    const int s0 = gs[g], s1 = gs[g + 1];
+    if (s1 <= s0) continue;
+    if (g == ngroups - 1)
+      k_phase_forward<B, KC, true><<<grid(s1 - s0), 256, 0, st>>>(s0, s1, goff1, map, lo, dt, r,
+                                                                 y, z, done);
+    else
+      k_phase_forward<B, KC, false><<<grid(s1 - s0), 256, 0, st>>>(s0, s1, goff1, map, lo, dt, r,
+                                                                  y, z, done);
+  }
+  for (int g = ngroups - 2; g >= 0; --g) {
+    const int s0 = gs[g], s1 = gs[g + 1];
+    if (s1 <= s0) continue;
+    k_phase_backward<B, KC><<<grid(s1 - s0), 256, 0, st>>>(s0, s1, goff1, map, up, dt, r, y, z,
+                                                           done);
+  }
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
+template <int B>
+int launch_phased_b(int kc, int ngroups, const int32_t* gs, int goff1, SliceMap map, Sell lo,
+                    Sell up, const double* dt, const double* r, double* y, double* z,
+                    const int* done, cudaStream_t st) {
+  if (kc <= 2)
+    return launch_phased_bk<B, 2>(ngroups, gs, goff1, map, lo, up, dt, r, y, z, done, st);
+  return launch_phased_bk<B, 4>(ngroups, gs, goff1, map, lo, up, dt, r, y, z, done, st);
+}
+
+// ngroups >= 2; gslice_host[g] = first slice of group g (group-aligned map)
+int launch_phased(int b, int kc, int ngroups, const int32_t* gslice_host, int goff1, SliceMap map,
+                  Sell lo, Sell up, const double* dt, const double* r, double* y, double* z,
+                  const int* done, cudaStream_t st) {
+  if (ngroups < 2) return B2S_SHAPE;
+  switch (b) {
+    case 1: return launch_phased_b<1>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, st);
+    case 2: return launch_phased_b<2>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, st);
+    case 3: return launch_phased_b<3>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, st);
+    case 4: return launch_phased_b<4>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, st);
+    default: return B2S_UNSUPPORTED;
+  }
+}
+
 __global__ void k_fill_sentinel(long long m, double* v) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m;
        t += (long long)gridDim.x * blockDim.x)
@@ -263,17 +447,6 @@ __global__ void k_slice_conflicts(SliceMap map, const int32_t* __restrict__ rp,
   }
 }
 
-template <int B>
-int occupancy_grid(const void* fn) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  int dev = 0, sms = kSms;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return per_sm * sms;
-}
 
 template <int B, int KC>
 int launch_sweeps_bk(SliceMap map, Sell lo, Sell up, const double* dt, const double* r,
@@ -350,6 +523,22 @@ int b2s_slice_conflicts(int nslices, const int32_t* row0, const int32_t* nrows,
 }
 
 int b2s_fill_sentinel(long long m, double* v, cudaStream_t st) { return fill_sentinel(m, v, st); }
+
+// Phased application for plans of 2..32 independent groups without
+// same-group entries (colourings): no sentinel preconditions, y is scratch.
+int b2s_ilu0_apply_phased(int n, int b, int kc, int ngroups, const int32_t* gslice_host,
+                          int goff1, const int32_t* row0, const int32_t* nrows,
+                          const int32_t* l_sp, const int32_t* l_cols, const double* l_vals,
+                          const int32_t* u_sp, const int32_t* u_cols, const double* u_vals,
+                          const double* dinv_tiles, const double* r, double* y, double* z,
+                          cudaStream_t st) {
+  if (n < 0 || b < 1 || ngroups < 2 || !gslice_host) return B2S_SHAPE;
+  if (n == 0) return B2S_OK;
+  SliceMap map{gslice_host[ngroups], row0, nrows};
+  Sell lo{l_sp, l_cols, l_vals}, up{u_sp, u_cols, u_vals};
+  return launch_phased(b, kc, ngroups, gslice_host, goff1, map, lo, up, dinv_tiles, r, y, z,
+                       nullptr, st);
+}
 
 // z = U^-1 L^-1 r in plan order.  Preconditions: y and z hold the sentinel
 // everywhere (b2s_fill_sentinel); tickets points at 16 zeroed bytes that the

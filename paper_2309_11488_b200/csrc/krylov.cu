@@ -32,6 +32,9 @@ int launch_sweeps(int b, int kc, SliceMap map, Sell lo, Sell up, const double* d
                   const double* r, double* y, double* z, int reset_y, int flags, void* tickets,
                   const int* done, cudaStream_t st);
 int fill_sentinel(long long m, double* v, cudaStream_t st);
+int launch_phased(int b, int kc, int ngroups, const int32_t* gslice_host, int goff1, SliceMap map,
+                  Sell lo, Sell up, const double* dt, const double* r, double* y, double* z,
+                  const int* done, cudaStream_t st);
 int launch_tiled(int b, const void* handle, const double* r, double* y, double* z, int reset_y,
                  const int* done, cudaStream_t st);
 
@@ -255,6 +258,8 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   State* state = reinterpret_cast<State*>(parts + 6 * npv);
   void* tickets = reinterpret_cast<char*>(state) + 256;
   const bool ilu = a->precond == 1;
+  const bool phased = ilu && !a->tiles && a->ngroups >= 2 && a->gslice_host;
+  const int reset = (ilu && !phased) ? 1 : 0;  // sync-free sweeps need sentinel-filled outputs
   const int np = a->nparts;
   SliceMap map{a->nslices, a->row0, a->nrows};
   Sell A{a->a_sp, a->a_cols, a->a_vals};
@@ -272,7 +277,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
   k_copy<<<grid_v, 256, 0, user>>>(m, r, v);  // v is only read for k > 0
   B2S_CHECK(cudaMemcpyAsync(prho, prr, sizeof(double) * np, cudaMemcpyDeviceToDevice, user));
-  if (ilu) {
+  if (ilu && !phased) {
     if ((rc = fill_sentinel(m, y, user))) return rc;
     if ((rc = fill_sentinel(m, phat, user))) return rc;
     if ((rc = fill_sentinel(m, shat, user))) return rc;
@@ -314,7 +319,11 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     k_ctl_begin<<<1, 256, 0, cs>>>(state, prr, prho, np); ++kernels;
     k_p_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, p); ++kernels;
     const int reset_y = a->refill_y ? 0 : 1;
-    if (ilu) {
+    if (phased) {
+      launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
+                    p, y, phat, done, cs);
+      kernels += 2 * (a->ngroups - 1);
+    } else if (ilu) {
       if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
       if (a->tiles) launch_tiled(a->b, a->tiles, p, y, phat, reset_y, done, cs);
       else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, reset_y, a->sweep_flags,
@@ -323,9 +332,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     }
     launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done, cs); ++kernels;
     k_ctl_alpha<<<1, 256, 0, cs>>>(state, pg, np); ++kernels;
-    k_s_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, ph, a->x, s, pss, ilu ? 1 : 0); ++kernels;
+    k_s_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, ph, a->x, s, pss, reset); ++kernels;
     k_ctl_s<<<1, 256, 0, cs>>>(state, pss, np); ++kernels;
-    if (ilu) {
+    if (phased) {
+      launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
+                    s, y, shat, done, cs);
+      kernels += 2 * (a->ngroups - 1);
+    } else if (ilu) {
       if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
       if (a->tiles) launch_tiled(a->b, a->tiles, s, y, shat, reset_y, done, cs);
       else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, reset_y, a->sweep_flags,
@@ -334,7 +347,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     }
     launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done, cs); ++kernels;
     k_ctl_omega<<<1, 256, 0, cs>>>(state, ptt, pts, np); ++kernels;
-    k_r_update<<<grid_v, 256, 0, cs>>>(m, state, sh, t, s, rhat, a->x, r, prr, prho, ilu ? 1 : 0); ++kernels;
+    k_r_update<<<grid_v, 256, 0, cs>>>(m, state, sh, t, s, rhat, a->x, r, prr, prho, reset); ++kernels;
     k_ctl_end<<<1, 1, 0, cs>>>(state); ++kernels;
     k_copy_done<<<1, 1, 0, cs>>>(state, dev_done); ++kernels;
     if (cudaStreamEndCapture(cs, &graph) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }

@@ -62,6 +62,10 @@ class Ilu0Factorization:
         # tickets on one CTA per SM (1.10 vs 1.39 us per level)
         self.sweep_flags = 0x4 if plan.group_count <= 16 else 0x10
         self.tiles = None        # b2s_tiles_create handle (tiled level sweeps), or None
+        # few independent groups (colourings) and no same-group entries: the
+        # phased sweeps, 2(G-1) plain passes, no polling (bit-identical)
+        self.phased = (smap.gslice_host is not None and not lower.stale and not upper.stale
+                       and os.environ.get("B2S_PHASED", "1") != "0")
 
     # -- reference attributes --------------------------------------------------
     @property
@@ -105,6 +109,15 @@ class Ilu0Factorization:
         y = D.empty_f64(m, dev)
         z = out if out is not None else D.empty_f64(m, dev)
         if m == 0:
+            return z
+        s, lo, up = self.smap, self.lower, self.upper
+        if self.phased and not self.tiles:
+            check(D.lib().b2s_ilu0_apply_phased(
+                self._n, self._b, self.kc, len(s.gslice_host) - 1,
+                s.gslice_host.ctypes.data, s.goff1, D.ptr(s.row0), D.ptr(s.nrows),
+                D.ptr(lo.sp), D.ptr(lo.cols), D.ptr(lo.vals), D.ptr(up.sp), D.ptr(up.cols),
+                D.ptr(up.vals), D.ptr(self.dtiles), D.ptr(r_perm), D.ptr(y), D.ptr(z),
+                D.stream()), "ilu0_apply_phased")
             return z
         D.fill_sentinel(y, m)
         D.fill_sentinel(z, m)

@@ -214,6 +214,10 @@ class DeviceKrylov:
                                                    D.ptr(f.upper.vals))
             args.dinv_tiles = D.ptr(f.dtiles)
             args.tiles = f.tiles
+            if f.phased and not f.tiles:
+                args.ngroups = len(s.gslice_host) - 1
+                args.goff1 = s.goff1
+                args.gslice_host = s.gslice_host.ctypes.data
         args.rhs, args.x, args.work = D.ptr(rhs), D.ptr(x), D.ptr(self.work)
         args.stream = D.stream()
         res = BicgResult()

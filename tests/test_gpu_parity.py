@@ -337,3 +337,23 @@ def test_tiled_sweeps_nonsymmetric_same_group(monkeypatch, golden):
         z = f.apply(P.BlockVector(e["x"], a.block_size)).data
         ref = e["level_apply"]
         assert np.linalg.norm(z - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("name", SYSTEMS)
+def test_phased_sweeps_bit_equal_to_sync_free(monkeypatch, golden, name):
+    """Colour plans take the phased sweeps (csrc/ilu0.cu k_phase_*): same
+    bits as the sync-free wavefront sweeps, same solve."""
+    g = golden(name)
+    a = matrix(g)
+    plan = P.graph_color(a.pattern)
+    f1 = P.decompose(a, plan)
+    monkeypatch.setenv("B2S_PHASED", "0")
+    f0 = P.decompose(a, plan)
+    assert f1.phased and not f0.phased
+    r = P.BlockVector(g["x"], a.block_size)
+    assert_array_equal(f1.apply(r).data, f0.apply(r).data)
+    rhs = P.BlockVector(g["rhs"], a.block_size)
+    x0, r0 = P.bicgstab(P.MatrixOperator(a), f0, rhs, stop=P.StoppingCriteria(1e-8, 200))
+    x1, r1 = P.bicgstab(P.MatrixOperator(a), f1, rhs, stop=P.StoppingCriteria(1e-8, 200))
+    assert r0.iterations == r1.iterations and r0.final_norm == r1.final_norm
+    assert_array_equal(x0.data, x1.data)
