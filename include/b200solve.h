@@ -177,6 +177,16 @@ int b2s_vec_r(long long m, double omega, double* shat, const double* t, const do
 
 /* ---- BiCGStab (bs/krylov.py:140-244) ------------------------------------ */
 
+/* 2-colour plans: *ok_host = 1 when every colour-0 row of the operator
+ * (slices [0, s1) of the group-aligned map) is its diagonal block followed
+ * by exactly the factor's U row (same columns, bitwise-equal blocks) -- then
+ * the backward sweep of colour 0 and the SpMV of colour 0 share one read of
+ * those blocks (csrc/fused.cu). */
+int b2s_fuse_check(int s1, int b, const int32_t* row0, const int32_t* nrows, const int32_t* a_sp,
+                   const int32_t* a_cols, const double* a_vals, const int32_t* u_sp,
+                   const int32_t* u_cols, const double* u_vals, int* ok_host,
+                   cudaStream_t stream);
+
 typedef struct {
   int n, b, nparts, precond /* 0 none, 1 ilu0 */, kc, maxit, check_lag;
   int refill_y; /* 1: U has same-group entries, refill the sweep scratch each apply */
@@ -199,6 +209,8 @@ typedef struct {
   /* phased sweeps (b2s_ilu0_apply_phased) when ngroups >= 2 */
   int ngroups, goff1;
   const int32_t* gslice_host;
+  /* 2 colours and b2s_fuse_check() passed: fused colour-0 backward + SpMV */
+  int fuse;
 } b2s_bicg_args;
 
 typedef struct {

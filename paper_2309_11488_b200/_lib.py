@@ -34,7 +34,8 @@ class BicgArgs(C.Structure):
                 ("l_sp", _P), ("l_cols", _P), ("l_vals", _P),
                 ("u_sp", _P), ("u_cols", _P), ("u_vals", _P),
                 ("dinv_tiles", _P), ("tiles", _P), ("rhs", _P), ("x", _P), ("work", _P),
-                ("stream", _P), ("ngroups", _I), ("goff1", _I), ("gslice_host", _P)]
+                ("stream", _P), ("ngroups", _I), ("goff1", _I), ("gslice_host", _P),
+                ("fuse", _I)]
 
 
 class BicgResult(C.Structure):
@@ -65,6 +66,7 @@ SIGNATURES = {
     "b2s_ilu0_apply": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                             _I, _I, _P, _P]),
     "b2s_fill_sentinel": (_I, [_LL, _P, _P]),
+    "b2s_fuse_check": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _PI, _P]),
     "b2s_ilu0_apply_phased": (_I, [_I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                    _P, _P, _P, _P]),
     "b2s_tiles_smem_bytes": (_LL, [_I, _I]),

@@ -18,7 +18,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libb200solve.so"
-SOURCES = ["analysis.cu", "spmv.cu", "factor.cu", "ilu0.cu", "tiles.cu", "krylov.cu", "jacobi.cu"]
+SOURCES = ["analysis.cu", "spmv.cu", "factor.cu", "ilu0.cu", "fused.cu", "tiles.cu", "krylov.cu",
+           "jacobi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

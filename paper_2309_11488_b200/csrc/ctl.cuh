@@ -1,0 +1,107 @@
+// BiCGStab control state and the "last CTA" control steps (bs/krylov.py:
+// 171-244 semantics).  The kernel that produces a set of per-CTA partial
+// sums also finishes the reduction: every CTA publishes its partial, takes a
+// ticket, and the CTA that arrives last reduces all partials in a fixed
+// order (deterministic, no fp64 atomics) and runs the scalar logic of that
+// point of the iteration.  So no 1-CTA control kernel sits between the
+// bandwidth kernels of an iteration.
+#pragma once
+#include "common.cuh"
+
+namespace b2s {
+
+constexpr double kBreakdown = 1e-60;  // bs/krylov.py:27
+
+enum Reason { kRunning = 0, kConverged = 1, kBreakdownR = 2, kNumerical = 3, kBudget = 4 };
+
+struct State {
+  double rho, rho_prev, alpha, omega, beta;
+  double norm0, target, final_norm, its;
+  int k, maxit, done, reason;
+};
+
+enum CtlStep { kCtlNone = 0, kCtlAlpha = 1, kCtlS = 2, kCtlOmega = 3, kCtlEndBegin = 4 };
+
+struct Ctl {
+  State* st;            // solver state (nullptr: no control step)
+  unsigned* counter;    // arrival ticket of this call site (self-resetting)
+  int* host_done;       // mapped pinned word the host polls (may be nullptr)
+  int step;             // CtlStep
+};
+
+// deterministic sum of np partials by one CTA (L2 loads: written by other SMs)
+__device__ __forceinline__ double reduce_parts_cg(const double* parts, int np, double* red) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) v += __ldcg(parts + i);
+  return block_sum(v, red);  // valid in thread 0
+}
+
+// true in every thread of the CTA that arrived last; call after thread 0
+// stored this CTA's partials.  Resets the ticket for the next launch.
+__device__ __forceinline__ bool last_cta(unsigned* counter) {
+  __shared__ int am_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(counter, 1u);
+    am_last = (t == gridDim.x - 1);
+    if (am_last) *counter = 0u;
+  }
+  __syncthreads();
+  if (am_last) __threadfence();
+  return am_last;
+}
+
+__device__ __forceinline__ void ctl_finish(State* st, int* host_done, int reason) {
+  st->done = 1;
+  st->reason = reason;
+  if (host_done) *reinterpret_cast<volatile int*>(host_done) = 1;
+}
+
+// The scalar logic after each reduction point; whole CTA calls, thread 0 writes.
+__device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const double* p1, int np,
+                                        double* red) {
+  State* st = c.st;
+  const double a = reduce_parts_cg(p0, np, red);
+  double b = 0.0;
+  if (c.step == kCtlOmega || c.step == kCtlEndBegin) b = reduce_parts_cg(p1, np, red);
+  if (threadIdx.x != 0) return;
+  switch (c.step) {
+    case kCtlAlpha: {  // gamma = rhat.v  (bs/krylov.py:206-210)
+      if (fabs(a) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
+      st->alpha = st->rho / a;
+      return;
+    }
+    case kCtlS: {  // x has been advanced by alpha p^; test |s|  (bs/krylov.py:211-220)
+      st->its += 0.5;
+      const double ns = sqrt(a);
+      if (!isfinite(ns)) { ctl_finish(st, c.host_done, kNumerical); return; }
+      if (ns <= st->target) { st->final_norm = ns; ctl_finish(st, c.host_done, kConverged); }
+      return;
+    }
+    case kCtlOmega: {  // tt, ts  (bs/krylov.py:223-229)
+      if (a < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
+      const double om = b / a;
+      if (fabs(om) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
+      st->omega = om;
+      return;
+    }
+    case kCtlEndBegin: {  // end of iteration k, then the top of k+1 (bs/krylov.py:195-200,230-240)
+      st->its += 0.5;
+      const double nr = sqrt(a);
+      if (!isfinite(nr)) { ctl_finish(st, c.host_done, kNumerical); return; }
+      if (nr <= st->target) { st->final_norm = nr; ctl_finish(st, c.host_done, kConverged); return; }
+      st->rho_prev = st->rho;
+      st->k += 1;
+      if (st->k >= st->maxit) { ctl_finish(st, c.host_done, kBudget); return; }
+      if (fabs(b) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
+      st->rho = b;
+      st->beta = (b / st->rho_prev) * (st->alpha / st->omega);
+      return;
+    }
+    default:
+      return;
+  }
+}
+
+}  // namespace b2s

@@ -4,11 +4,13 @@
 // into a CUDA graph and replayed; the host only polls a pinned "done" word a
 // couple of iterations behind the GPU, so the device never idles on the
 // host.  Control decisions (breakdown floors, convergence tests, half-step
-// counting, the order of the reference's exits) run in four 1-CTA control
-// kernels that are the only writers of the solver state; every other kernel
-// reads `state->done` first and becomes a no-op once the solve has ended,
-// which reproduces the reference's early exits exactly even though later
-// kernels of the iteration are already queued.
+// counting, the order of the reference's exits) run in the last CTA of the
+// kernel that produces the partial sums they need (ctl.cuh): that CTA is the
+// only writer of the solver state; every kernel reads `state->done` first
+// and becomes a no-op once the solve has ended, which reproduces the
+// reference's early exits exactly even though later kernels of the
+// iteration are already queued.  Nine kernels per iteration, no 1-CTA
+// control kernels in between.
 //
 // Vector passes per iteration (fused so each vector is touched as few times
 // as possible; partial sums go to fixed per-CTA slots and are reduced in a
@@ -22,31 +24,29 @@
 //   x += omega s^, r = s - omega t, |r|^2 and r^.r partials (1 kernel)
 #include <cmath>
 
+#include "ctl.cuh"
 #include "sell.cuh"
 
 namespace b2s {
 
 int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
-                const double* w, double* p0, double* p1, const int* done, cudaStream_t st);
+                const double* w, double* p0, double* p1, const int* done, Ctl ctl,
+                cudaStream_t st);
 int launch_sweeps(int b, int kc, SliceMap map, Sell lo, Sell up, const double* dt,
                   const double* r, double* y, double* z, int reset_y, int flags, void* tickets,
                   const int* done, cudaStream_t st);
 int fill_sentinel(long long m, double* v, cudaStream_t st);
 int launch_phased(int b, int kc, int ngroups, const int32_t* gslice_host, int goff1, SliceMap map,
                   Sell lo, Sell up, const double* dt, const double* r, double* y, double* z,
-                  const int* done, cudaStream_t st);
+                  const int* done, cudaStream_t st, bool skip_g0);
+int launch_spmv_range(int b, int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
+                      const double* x, double* y, const double* w, double* p0, double* p1,
+                      const int* done, Ctl ctl, cudaStream_t st);
+int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
+                    const double* yin, double* z, double* v, const double* w, double* p0,
+                    double* p1, const int* done, int* grid_out, cudaStream_t st);
 int launch_tiled(int b, const void* handle, const double* r, double* y, double* z, int reset_y,
                  const int* done, cudaStream_t st);
-
-constexpr double kBreakdown = 1e-60;  // bs/krylov.py:27
-
-enum Reason { kRunning = 0, kConverged = 1, kBreakdownR = 2, kNumerical = 3, kBudget = 4 };
-
-struct State {
-  double rho, rho_prev, alpha, omega, beta;
-  double norm0, target, final_norm, its;
-  int k, maxit, done, reason;
-};
 
 // deterministic sum of np partials by one CTA of 256 threads
 __device__ double reduce_parts(const double* parts, int np, double* red) {
@@ -66,71 +66,28 @@ __global__ void k_ctl_init(State* st, const double* prr, int np, double tol, int
     st->done = 0;
     if (!isfinite(n0)) { st->done = 1; st->reason = kNumerical; }
     else if (n0 <= st->target || n0 == 0.0) { st->done = 1; st->reason = kConverged; }
+    // top of iteration 0 (maxit >= 1): rho_0 = rhat.r0 = the same partials
+    else if (fabs(s) < kBreakdown) { st->done = 1; st->reason = kBreakdownR; }
+    else st->rho = s;
   }
-}
-
-// top of iteration k: previous |r| test (k > 0), budget, rho, beta
-__global__ void k_ctl_begin(State* st, const double* prr, const double* prho, int np) {
-  __shared__ double red[8];
-  if (st->done) return;
-  const double rr = reduce_parts(prr, np, red);
-  const double rho = reduce_parts(prho, np, red);
-  if (threadIdx.x != 0) return;
-  const int k = st->k;
-  if (k > 0) {
-    const double nr = sqrt(rr);
-    if (!isfinite(nr)) { st->done = 1; st->reason = kNumerical; return; }
-    if (nr <= st->target) { st->done = 1; st->reason = kConverged; st->final_norm = nr; return; }
-    st->rho_prev = st->rho;
-  }
-  if (k >= st->maxit) { st->done = 1; st->reason = kBudget; return; }
-  if (fabs(rho) < kBreakdown) { st->done = 1; st->reason = kBreakdownR; return; }
-  st->rho = rho;
-  if (k > 0) st->beta = (rho / st->rho_prev) * (st->alpha / st->omega);
-}
-
-__global__ void k_ctl_alpha(State* st, const double* pg, int np) {
-  __shared__ double red[8];
-  if (st->done) return;
-  const double gamma = reduce_parts(pg, np, red);
-  if (threadIdx.x != 0) return;
-  if (fabs(gamma) < kBreakdown) { st->done = 1; st->reason = kBreakdownR; return; }
-  st->alpha = st->rho / gamma;
-}
-
-__global__ void k_ctl_s(State* st, const double* pss, int np) {
-  __shared__ double red[8];
-  if (st->done) return;
-  const double ss = reduce_parts(pss, np, red);
-  if (threadIdx.x != 0) return;
-  st->its += 0.5;  // the x update of this half step has happened
-  const double ns = sqrt(ss);
-  if (!isfinite(ns)) { st->done = 1; st->reason = kNumerical; return; }
-  if (ns <= st->target) { st->done = 1; st->reason = kConverged; st->final_norm = ns; }
-}
-
-__global__ void k_ctl_omega(State* st, const double* ptt, const double* pts, int np) {
-  __shared__ double red[8];
-  if (st->done) return;
-  const double tt = reduce_parts(ptt, np, red);
-  const double ts = reduce_parts(pts, np, red);
-  if (threadIdx.x != 0) return;
-  if (tt < kBreakdown) { st->done = 1; st->reason = kBreakdownR; return; }
-  const double om = ts / tt;
-  if (fabs(om) < kBreakdown) { st->done = 1; st->reason = kBreakdownR; return; }
-  st->omega = om;
-}
-
-// after the second half step: its, k
-__global__ void k_ctl_end(State* st) {
-  if (st->done) return;
-  st->its += 0.5;
-  st->k += 1;
 }
 
 #define GRID_STRIDE(t, m) \
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (m); \
        t += (long long)gridDim.x * blockDim.x)
+
+// Vector passes: 16-byte loads (double2) and two pairs in flight per thread
+// per step (all loads of a step issued before its arithmetic); an odd tail
+// element goes to thread 0 of CTA 0.  Callers guarantee 16-byte aligned
+// vectors (workspace sub-buffers are 256-byte aligned; torch allocations
+// 512-byte).  The per-thread accumulation order is fixed by (m, grid), so
+// the partial sums are deterministic.
+__device__ __forceinline__ double2 ld2(const double* p, long long j) {
+  return __ldcs(reinterpret_cast<const double2*>(p) + j);
+}
+__device__ __forceinline__ void st2(double* p, long long j, double a, double b) {
+  reinterpret_cast<double2*>(p)[j] = make_double2(a, b);
+}
 
 __global__ void __launch_bounds__(256) k_p_update(long long m, const State* st,
                                                   const double* __restrict__ r,
@@ -138,61 +95,120 @@ __global__ void __launch_bounds__(256) k_p_update(long long m, const State* st,
   if (st->done) return;
   const int k = st->k;
   const double beta = st->beta, omega = st->omega;
+  const long long m2 = m >> 1, T = (long long)gridDim.x * blockDim.x;
+  long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (k == 0) {
-    GRID_STRIDE(t, m) p[t] = r[t];
-  } else {
-    GRID_STRIDE(t, m) p[t] = r[t] + beta * (p[t] - omega * v[t]);
+    for (; j < m2; j += T) {
+      const double2 a = ld2(r, j);
+      st2(p, j, a.x, a.y);
+    }
+    if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[m - 1] = r[m - 1];
+    return;
   }
+  for (; j + T < m2; j += 2 * T) {
+    const double2 r0 = ld2(r, j), r1 = ld2(r, j + T);
+    const double2 p0 = ld2(p, j), p1 = ld2(p, j + T);
+    const double2 v0 = ld2(v, j), v1 = ld2(v, j + T);
+    st2(p, j, r0.x + beta * (p0.x - omega * v0.x), r0.y + beta * (p0.y - omega * v0.y));
+    st2(p, j + T, r1.x + beta * (p1.x - omega * v1.x), r1.y + beta * (p1.y - omega * v1.y));
+  }
+  if (j < m2) {
+    const double2 r0 = ld2(r, j), p0 = ld2(p, j), v0 = ld2(v, j);
+    st2(p, j, r0.x + beta * (p0.x - omega * v0.x), r0.y + beta * (p0.y - omega * v0.y));
+  }
+  if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+    p[m - 1] = r[m - 1] + beta * (p[m - 1] - omega * v[m - 1]);
 }
 
 // s = r - alpha v ; x += alpha p^ ; |s|^2 partials ; optionally p^ <- sentinel
+__device__ __forceinline__ void s_elem(double rv, double vv, double ph, double& xo, double& so,
+                                       double alpha, double& acc) {
+  so = rv - alpha * vv;
+  xo += alpha * ph;
+  acc = fma(so, so, acc);
+}
+
 __global__ void __launch_bounds__(256) k_s_update(long long m, const State* st,
                                                   const double* __restrict__ r,
                                                   const double* __restrict__ v, double* phat,
                                                   double* __restrict__ x,
                                                   double* __restrict__ s, double* pss,
-                                                  int reset) {
+                                                  int reset, Ctl ctl) {
   __shared__ double red[8];
   if (st->done) return;
   const double alpha = st->alpha;
   double acc = 0.0;
-  GRID_STRIDE(t, m) {
-    const double sv = r[t] - alpha * v[t];
-    const double ph = phat[t];
-    s[t] = sv;
-    x[t] += alpha * ph;
-    acc = fma(sv, sv, acc);
-    if (reset) phat[t] = sentinel();
+  const long long m2 = m >> 1, T = (long long)gridDim.x * blockDim.x;
+  long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; j < m2; j += T) {
+    const double2 rv = ld2(r, j), vv = ld2(v, j), ph = ld2(phat, j);
+    double2 xv = reinterpret_cast<const double2*>(x)[j];
+    double s0, s1;
+    s_elem(rv.x, vv.x, ph.x, xv.x, s0, alpha, acc);
+    s_elem(rv.y, vv.y, ph.y, xv.y, s1, alpha, acc);
+    st2(s, j, s0, s1);
+    st2(x, j, xv.x, xv.y);
+    if (reset) st2(phat, j, sentinel(), sentinel());
+  }
+  if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    double s0;
+    s_elem(r[m - 1], v[m - 1], phat[m - 1], x[m - 1], s0, alpha, acc);
+    s[m - 1] = s0;
+    if (reset) phat[m - 1] = sentinel();
   }
   const double tot = block_sum(acc, red);
   if (threadIdx.x == 0) pss[blockIdx.x] = tot;
+  if (ctl.st && last_cta(ctl.counter)) ctl_run(ctl, pss, nullptr, gridDim.x, red);
 }
 
 // x += omega s^ ; r = s - omega t ; |r|^2 and r^.r partials ; s^ <- sentinel
+__device__ __forceinline__ void r_elem(double sh, double tv, double sv, double rh, double& xo,
+                                       double& ro, double omega, double& a0, double& a1) {
+  xo += omega * sh;
+  ro = sv - omega * tv;
+  a0 = fma(ro, ro, a0);
+  a1 = fma(rh, ro, a1);
+}
+
 __global__ void __launch_bounds__(256) k_r_update(long long m, const State* st, double* shat,
                                                   const double* __restrict__ tv,
                                                   const double* __restrict__ s,
                                                   const double* __restrict__ rhat,
                                                   double* __restrict__ x,
                                                   double* __restrict__ r, double* prr,
-                                                  double* prho, int reset) {
+                                                  double* prho, int reset, Ctl ctl) {
   __shared__ double red[8];
   if (st->done) return;
   const double omega = st->omega;
   double a0 = 0.0, a1 = 0.0;
-  GRID_STRIDE(t, m) {
-    const double sh = shat[t];
-    x[t] += omega * sh;
-    const double rv = s[t] - omega * tv[t];
-    r[t] = rv;
-    a0 = fma(rv, rv, a0);
-    a1 = fma(rhat[t], rv, a1);
-    if (reset) shat[t] = sentinel();
+  const long long m2 = m >> 1, T = (long long)gridDim.x * blockDim.x;
+  long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; j < m2; j += T) {
+    const double2 sh = ld2(shat, j), t2 = ld2(tv, j), sv = ld2(s, j), rh = ld2(rhat, j);
+    double2 xv = reinterpret_cast<const double2*>(x)[j];
+    double r0, r1;
+    r_elem(sh.x, t2.x, sv.x, rh.x, xv.x, r0, omega, a0, a1);
+    r_elem(sh.y, t2.y, sv.y, rh.y, xv.y, r1, omega, a0, a1);
+    st2(x, j, xv.x, xv.y);
+    st2(r, j, r0, r1);
+    if (reset) st2(shat, j, sentinel(), sentinel());
+  }
+  if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    double r0;
+    r_elem(shat[m - 1], tv[m - 1], s[m - 1], rhat[m - 1], x[m - 1], r0, omega, a0, a1);
+    r[m - 1] = r0;
+    if (reset) shat[m - 1] = sentinel();
   }
   const double t0 = block_sum(a0, red);
   if (threadIdx.x == 0) prr[blockIdx.x] = t0;
   const double t1 = block_sum(a1, red);
   if (threadIdx.x == 0) prho[blockIdx.x] = t1;
+  if (ctl.st && last_cta(ctl.counter)) ctl_run(ctl, prr, prho, gridDim.x, red);
+}
+
+template <class... P>
+inline bool misaligned16(const P*... p) {
+  return ((reinterpret_cast<uintptr_t>(p) | ...) & 15) != 0;
 }
 
 __global__ void k_copy(long long m, const double* __restrict__ a, double* __restrict__ b) {
@@ -221,7 +237,6 @@ __global__ void k_all_finite(long long m, const double* __restrict__ a, int* bad
   if (__any_sync(0xffffffffu, local) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
 }
 
-__global__ void k_copy_done(const State* st, int* host_done) { *host_done = st->done; }
 
 }  // namespace b2s
 
@@ -236,8 +251,9 @@ static long long vec_doubles(int n, int b) {
 
 long long b2s_bicgstab_workspace_bytes(int n, int b, int nparts) {
   const long long m = vec_doubles(n, b);
-  // r rhat p v phat s shat t y x0  + 6 partial arrays + state + tickets
-  return (10 * m + 6 * (long long)((nparts + 31) / 32 * 32)) * 8 + 256 + 64;
+  // r rhat p v phat s shat t y x0  + 6 partial arrays (2 x nparts: the fused
+  // 2-colour passes split a dot product over two kernels) + state + tickets
+  return (10 * m + 6 * 2 * (long long)((nparts + 31) / 32 * 32)) * 8 + 256 + 64;
 }
 
 int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
@@ -245,9 +261,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   res->iterations = 0.0; res->initial_norm = 0.0; res->final_norm = 0.0;
   if (a->n < 0 || a->b < 1 || a->nparts < 1 || a->maxit < 1) return B2S_SHAPE;
   if (a->b > 4) return B2S_UNSUPPORTED;
+  // the vector passes use 16-byte loads
+  if ((reinterpret_cast<uintptr_t>(a->x) | reinterpret_cast<uintptr_t>(a->rhs) |
+       reinterpret_cast<uintptr_t>(a->work)) & 15)
+    return B2S_SHAPE;
   const long long m = (long long)a->n * a->b;
   const long long mv = vec_doubles(a->n, a->b);
-  const long long npv = (a->nparts + 31) / 32 * 32;
+  const long long npv = 2 * ((a->nparts + 31) / 32 * 32);
   double* w = a->work;
   double *r = w, *rhat = w + mv, *p = w + 2 * mv, *v = w + 3 * mv, *phat = w + 4 * mv,
          *s = w + 5 * mv, *shat = w + 6 * mv, *t = w + 7 * mv, *y = w + 8 * mv,
@@ -256,9 +276,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   double *prr = parts, *prho = parts + npv, *pg = parts + 2 * npv, *pss = parts + 3 * npv,
          *ptt = parts + 4 * npv, *pts = parts + 5 * npv;
   State* state = reinterpret_cast<State*>(parts + 6 * npv);
-  void* tickets = reinterpret_cast<char*>(state) + 256;
+  void* tickets = reinterpret_cast<char*>(state) + 256;  // 2 sweep ticket pairs (16 B)
+  unsigned* counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(tickets) + 32);
   const bool ilu = a->precond == 1;
   const bool phased = ilu && !a->tiles && a->ngroups >= 2 && a->gslice_host;
+  // 2 colours + colour-0 rows of A == [diag, U row] (b2s_fuse_check): the
+  // backward pass of colour 0 and the SpMV rows of colour 0 share one read
+  const bool fused = phased && a->ngroups == 2 && a->fuse;
   const int reset = (ilu && !phased) ? 1 : 0;  // sync-free sweeps need sentinel-filled outputs
   const int np = a->nparts;
   SliceMap map{a->nslices, a->row0, a->nrows};
@@ -271,12 +295,11 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // ---- setup on the caller's stream: r0 = b - A x0, |r0|, r^ = r0, rho_0 partials
   B2S_CHECK(cudaMemsetAsync(tickets, 0, 64, user));
   k_copy<<<grid_v, 256, 0, user>>>(m, a->x, x0);
-  int rc = launch_spmv(a->b, 3, np, map, A, a->x, r, a->rhs, prr, nullptr, nullptr, user);
+  int rc = launch_spmv(a->b, 3, np, map, A, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{}, user);
   if (rc) return rc;
   k_ctl_init<<<1, 256, 0, user>>>(state, prr, np, a->tol, a->maxit);
   k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
   k_copy<<<grid_v, 256, 0, user>>>(m, r, v);  // v is only read for k > 0
-  B2S_CHECK(cudaMemcpyAsync(prho, prr, sizeof(double) * np, cudaMemcpyDeviceToDevice, user));
   if (ilu && !phased) {
     if ((rc = fill_sentinel(m, y, user))) return rc;
     if ((rc = fill_sentinel(m, phat, user))) return rc;
@@ -316,12 +339,21 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     }
     double* ph = ilu ? phat : p;
     double* sh = ilu ? shat : s;
-    k_ctl_begin<<<1, 256, 0, cs>>>(state, prr, prho, np); ++kernels;
     k_p_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, p); ++kernels;
     const int reset_y = a->refill_y ? 0 : 1;
-    if (phased) {
+    const int s1c = fused ? a->gslice_host[1] : 0;
+    if (fused) {
+      launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, p, y,
+                    phat, done, cs, true);
+      int g0 = np;
+      launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
+                      done, &g0, cs);
+      launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
+                        done, Ctl{state, counters + 0, dev_done, kCtlAlpha}, cs);
+      kernels += 3;
+    } else if (phased) {
       launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
-                    p, y, phat, done, cs);
+                    p, y, phat, done, cs, false);
       kernels += 2 * (a->ngroups - 1);
     } else if (ilu) {
       if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
@@ -330,13 +362,24 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                          tickets, done, cs);
       kernels += 2;
     }
-    launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done, cs); ++kernels;
-    k_ctl_alpha<<<1, 256, 0, cs>>>(state, pg, np); ++kernels;
-    k_s_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, ph, a->x, s, pss, reset); ++kernels;
-    k_ctl_s<<<1, 256, 0, cs>>>(state, pss, np); ++kernels;
-    if (phased) {
+    if (!fused) {
+      launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done,
+                  Ctl{state, counters + 0, dev_done, kCtlAlpha}, cs); ++kernels;
+    }
+    k_s_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, ph, a->x, s, pss, reset,
+                                       Ctl{state, counters + 1, dev_done, kCtlS}); ++kernels;
+    if (fused) {
+      launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, s, y,
+                    shat, done, cs, true);
+      int g0 = np;
+      launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, s, shat, t, s, ptt, pts, done,
+                      &g0, cs);
+      launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
+                        Ctl{state, counters + 2, dev_done, kCtlOmega}, cs);
+      kernels += 3;
+    } else if (phased) {
       launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
-                    s, y, shat, done, cs);
+                    s, y, shat, done, cs, false);
       kernels += 2 * (a->ngroups - 1);
     } else if (ilu) {
       if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
@@ -345,11 +388,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                          tickets, done, cs);
       kernels += 2;
     }
-    launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done, cs); ++kernels;
-    k_ctl_omega<<<1, 256, 0, cs>>>(state, ptt, pts, np); ++kernels;
-    k_r_update<<<grid_v, 256, 0, cs>>>(m, state, sh, t, s, rhat, a->x, r, prr, prho, reset); ++kernels;
-    k_ctl_end<<<1, 1, 0, cs>>>(state); ++kernels;
-    k_copy_done<<<1, 1, 0, cs>>>(state, dev_done); ++kernels;
+    if (!fused) {
+      launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done,
+                  Ctl{state, counters + 2, dev_done, kCtlOmega}, cs); ++kernels;
+    }
+    k_r_update<<<grid_v, 256, 0, cs>>>(m, state, sh, t, s, rhat, a->x, r, prr, prho, reset,
+                                       Ctl{state, counters + 3, dev_done, kCtlEndBegin});
+    ++kernels;
     if (cudaStreamEndCapture(cs, &graph) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
     if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
     // order the graph after the setup work on the caller's stream
@@ -360,7 +405,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     cudaEventDestroy(ev);
     // ---- replay: the host stays `lag` iterations behind the device
     const int lag = a->check_lag > 0 ? a->check_lag : 2;
-    const int total = a->maxit + 1;  // +1: the final k_ctl_begin does the last |r| / budget test
+    const int total = a->maxit + 1;  // every exit sets done; the spare replay only no-ops
     cudaEvent_t ring[8];
     for (int q = 0; q < 8; ++q) cudaEventCreateWithFlags(&ring[q], cudaEventDisableTiming);
     int launched = 0;
@@ -401,7 +446,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   }
   // not converged: true residual of the current x, then x0 if x is not finite
   // (bs/krylov.py:242-244)
-  rc = launch_spmv(a->b, 3, np, map, A, a->x, t, a->rhs, pg, nullptr, nullptr, user);
+  rc = launch_spmv(a->b, 3, np, map, A, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user);
   if (rc) return rc;
   k_reduce_parts<<<1, 256, 0, user>>>(pg, np, pss);
   int* bad = reinterpret_cast<int*>(ptt);
@@ -461,6 +506,7 @@ static State* stage_state(double* scratch, int k, double alpha, double beta, dou
 // p = r (k == 0) or r + beta (p - omega v); scratch >= 128 bytes device
 int b2s_vec_p(long long m, int k, double beta, double omega, const double* r, const double* v,
               double* p, double* scratch, cudaStream_t st) {
+  if (misaligned16(r, v, p)) return B2S_SHAPE;
   int rc;
   State* s = stage_state(scratch, k, 0.0, beta, omega, st, &rc);
   if (rc) return rc;
@@ -473,10 +519,11 @@ int b2s_vec_p(long long m, int k, double beta, double omega, const double* r, co
 int b2s_vec_s(long long m, double alpha, const double* r, const double* v, double* phat,
               double* x, double* s, double* parts, int nparts, int reset, double* scratch,
               cudaStream_t st) {
+  if (misaligned16(r, v, phat, x, s)) return B2S_SHAPE;
   int rc;
   State* d = stage_state(scratch, 0, alpha, 0.0, 0.0, st, &rc);
   if (rc) return rc;
-  k_s_update<<<nparts, 256, 0, st>>>(m, d, r, v, phat, x, s, parts, reset);
+  k_s_update<<<nparts, 256, 0, st>>>(m, d, r, v, phat, x, s, parts, reset, Ctl{});
   B2S_LAUNCH_CHECK();
   return B2S_OK;
 }
@@ -485,10 +532,11 @@ int b2s_vec_s(long long m, double alpha, const double* r, const double* v, doubl
 int b2s_vec_r(long long m, double omega, double* shat, const double* t, const double* s,
               const double* rhat, double* x, double* r, double* prr, double* prho, int nparts,
               int reset, double* scratch, cudaStream_t st) {
+  if (misaligned16(shat, t, s, rhat, x, r)) return B2S_SHAPE;
   int rc;
   State* d = stage_state(scratch, 0, 0.0, 0.0, omega, st, &rc);
   if (rc) return rc;
-  k_r_update<<<nparts, 256, 0, st>>>(m, d, shat, t, s, rhat, x, r, prr, prho, reset);
+  k_r_update<<<nparts, 256, 0, st>>>(m, d, shat, t, s, rhat, x, r, prr, prho, reset, Ctl{});
   B2S_LAUNCH_CHECK();
   return B2S_OK;
 }

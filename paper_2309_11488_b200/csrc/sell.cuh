@@ -22,6 +22,10 @@ struct Sell {
   const double* vals;   // [slots*b*b]
 };
 
+// SpMV epilogues: 0 y = A x; 1 + partials w.y; 2 + partials y.y and y.w;
+// 3 y = w - A x (residual) + partials y.y
+enum SpmvMode { kPlain = 0, kDotW = 1, kSelfAndW = 2, kResidual = 3 };
+
 __device__ __forceinline__ long long vidx(long long slot0, int k, int e, int lane, int bb) {
   // value index of entry (k, e) of the lane in the slice starting at slot0
   return (slot0 + 32ll * k) * bb + 32ll * e + lane;

@@ -15,6 +15,7 @@
 // norm.  Partials are reduced in a fixed order (no atomics): deterministic.
 #include <cub/cub.cuh>
 
+#include "ctl.cuh"
 #include "sell.cuh"
 
 namespace b2s {
@@ -133,14 +134,15 @@ __global__ void k_diag_tiles(int nslices, int bb, const int32_t* __restrict__ ro
   }
 }
 
-enum SpmvMode { kPlain = 0, kDotW = 1, kSelfAndW = 2, kResidual = 3 };
 
 template <int B, int MODE>
-__global__ void __launch_bounds__(256) k_spmv(SliceMap map, Sell a, const double* __restrict__ x,
+__global__ void __launch_bounds__(256) k_spmv(SliceMap map, int s0, int s1, int poff, Sell a,
+                                              const double* __restrict__ x,
                                               double* __restrict__ y,
                                               const double* __restrict__ w,
                                               double* __restrict__ part0,
-                                              double* __restrict__ part1, const int* done) {
+                                              double* __restrict__ part1, const int* done,
+                                              Ctl ctl) {
   constexpr int BB = B * B;
   __shared__ double red[8];
   if (done && *done) return;
@@ -148,7 +150,7 @@ __global__ void __launch_bounds__(256) k_spmv(SliceMap map, Sell a, const double
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   double p0 = 0.0, p1 = 0.0;
-  for (int s = gw; s < map.nslices; s += nw) {
+  for (int s = s0 + gw; s < s1; s += nw) {
     const int slot0 = a.sp[s];
     const int width = (a.sp[s + 1] - slot0) >> 5;
     const bool ok = lane < map.nrows[s];
@@ -156,17 +158,33 @@ __global__ void __launch_bounds__(256) k_spmv(SliceMap map, Sell a, const double
     double acc[B];
 #pragma unroll
     for (int c = 0; c < B; ++c) acc[c] = 0.0;
-    for (int k = 0; k < width; ++k) {
-      const int col = __ldcs(a.cols + slot0 + 32 * k + lane);
-      if (col < 0) continue;
-      double blk[BB], xv[B], pr[B];
+    // two entries per step, all loads of the pair issued before any math
+    for (int k = 0; k < width; k += 2) {
+      const bool two = k + 1 < width;
+      int col[2];
+      col[0] = __ldcs(a.cols + slot0 + 32 * k + lane);
+      col[1] = two ? __ldcs(a.cols + slot0 + 32 * (k + 1) + lane) : -1;
+      double blk[2][BB], xv[2][B];
 #pragma unroll
-      for (int e = 0; e < BB; ++e) blk[e] = __ldcs(a.vals + vidx(slot0, k, e, lane, BB));
+      for (int e = 0; e < BB; ++e) {
+        blk[0][e] = __ldcs(a.vals + vidx(slot0, k, e, lane, BB));
+        blk[1][e] = two ? __ldcs(a.vals + vidx(slot0, k + 1, e, lane, BB)) : 0.0;
+      }
 #pragma unroll
-      for (int c = 0; c < B; ++c) xv[c] = __ldg(x + (long long)col * B + c);
-      matvec<B>(blk, xv, pr);
+      for (int q = 0; q < 2; ++q) {
+        const long long cq = col[q] < 0 ? 0 : col[q];
 #pragma unroll
-      for (int c = 0; c < B; ++c) acc[c] += pr[c];
+        for (int c = 0; c < B; ++c) xv[q][c] = __ldg(x + cq * B + c);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (col[q] >= 0) {   // ascending columns, padding contributes nothing
+          double pr[B];
+          matvec<B>(blk[q], xv[q], pr);
+#pragma unroll
+          for (int c = 0; c < B; ++c) acc[c] += pr[c];
+        }
+      }
     }
     if (ok) {
 #pragma unroll
@@ -182,11 +200,15 @@ __global__ void __launch_bounds__(256) k_spmv(SliceMap map, Sell a, const double
   }
   if (MODE != kPlain) {
     double t0 = block_sum(p0, red);
-    if (threadIdx.x == 0) part0[blockIdx.x] = t0;
+    if (threadIdx.x == 0) part0[poff + blockIdx.x] = t0;
     if (MODE == kSelfAndW) {
       double t1 = block_sum(p1, red);
-      if (threadIdx.x == 0) part1[blockIdx.x] = t1;
+      if (threadIdx.x == 0) part1[poff + blockIdx.x] = t1;
     }
+    // the last CTA to finish reduces the partials (those of an earlier
+    // kernel first, when poff > 0) and runs the solver's scalar step
+    // (alpha after gamma, omega after tt/ts)
+    if (ctl.st && last_cta(ctl.counter)) ctl_run(ctl, part0, part1, poff + gridDim.x, red);
   }
 }
 
@@ -198,28 +220,38 @@ inline int grid_for(long long work, int threads = 256) {
 }
 
 template <int B>
-int launch_spmv_b(int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
-                  const double* w, double* p0, double* p1, const int* done, cudaStream_t st) {
+int launch_spmv_b(int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
+                  const double* x, double* y, const double* w, double* p0, double* p1,
+                  const int* done, Ctl ctl, cudaStream_t st) {
   dim3 g(nparts), t(256);
   switch (mode) {
-    case kPlain: k_spmv<B, kPlain><<<g, t, 0, st>>>(map, a, x, y, w, p0, p1, done); break;
-    case kDotW: k_spmv<B, kDotW><<<g, t, 0, st>>>(map, a, x, y, w, p0, p1, done); break;
-    case kSelfAndW: k_spmv<B, kSelfAndW><<<g, t, 0, st>>>(map, a, x, y, w, p0, p1, done); break;
-    case kResidual: k_spmv<B, kResidual><<<g, t, 0, st>>>(map, a, x, y, w, p0, p1, done); break;
+    case kPlain: k_spmv<B, kPlain><<<g, t, 0, st>>>(map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
+    case kDotW: k_spmv<B, kDotW><<<g, t, 0, st>>>(map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
+    case kSelfAndW: k_spmv<B, kSelfAndW><<<g, t, 0, st>>>(map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
+    case kResidual: k_spmv<B, kResidual><<<g, t, 0, st>>>(map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
     default: return B2S_SHAPE;
   }
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
-int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
-                const double* w, double* p0, double* p1, const int* done, cudaStream_t st) {
+// SpMV over slices [s0, s1) of the map; partials land at [poff, poff + nparts)
+int launch_spmv_range(int b, int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
+                      const double* x, double* y, const double* w, double* p0, double* p1,
+                      const int* done, Ctl ctl, cudaStream_t st) {
   switch (b) {
-    case 1: return launch_spmv_b<1>(mode, nparts, map, a, x, y, w, p0, p1, done, st);
-    case 2: return launch_spmv_b<2>(mode, nparts, map, a, x, y, w, p0, p1, done, st);
-    case 3: return launch_spmv_b<3>(mode, nparts, map, a, x, y, w, p0, p1, done, st);
-    case 4: return launch_spmv_b<4>(mode, nparts, map, a, x, y, w, p0, p1, done, st);
+    case 1: return launch_spmv_b<1>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st);
+    case 2: return launch_spmv_b<2>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st);
+    case 3: return launch_spmv_b<3>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st);
+    case 4: return launch_spmv_b<4>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st);
     default: return B2S_UNSUPPORTED;
   }
+}
+
+int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
+                const double* w, double* p0, double* p1, const int* done, Ctl ctl,
+                cudaStream_t st) {
+  return launch_spmv_range(b, mode, nparts, map, 0, map.nslices, 0, a, x, y, w, p0, p1, done, ctl,
+                           st);
 }
 
 }  // namespace b2s
@@ -337,7 +369,7 @@ int b2s_spmv(int b, int mode, int nparts, int nslices, const int32_t* row0,
   if (nslices < 0 || nparts < 1) return B2S_SHAPE;
   SliceMap map{nslices, row0, nrows};
   Sell a{sp, cols, vals};
-  return launch_spmv(b, mode, nparts, map, a, x, y, w, part0, part1, done, st);
+  return launch_spmv(b, mode, nparts, map, a, x, y, w, part0, part1, done, Ctl{}, st);
 }
 
 }  // extern "C"

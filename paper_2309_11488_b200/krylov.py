@@ -16,6 +16,7 @@ device vectors with the same control flow.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass
 from typing import Callable
@@ -171,6 +172,7 @@ class DeviceKrylov:
     a: "D.Sell"
     fact: Ilu0Factorization | None
     work: torch.Tensor
+    fuse: bool = False   # 2-colour fused backward + SpMV passes (csrc/fused.cu)
 
     @classmethod
     def build(cls, matrix: BlockMatrix, fact: Ilu0Factorization | None,
@@ -189,7 +191,17 @@ class DeviceKrylov:
         sell = D.Sell.build(smap, a_bsr, 0)
         nbytes = int(D.lib().b2s_bicgstab_workspace_bytes(n, b, D.NPARTS))
         work = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=dev)
-        return cls(n, b, smap, sell, fact, work)
+        fuse = False
+        if (fact is not None and fact.phased and not fact.tiles and
+                len(smap.gslice_host) == 3 and os.environ.get("B2S_FUSE", "1") != "0"):
+            ok = C.c_int32(0)
+            up = fact.upper
+            check(D.lib().b2s_fuse_check(int(smap.gslice_host[1]), b, D.ptr(smap.row0),
+                                         D.ptr(smap.nrows), D.ptr(sell.sp), D.ptr(sell.cols),
+                                         D.ptr(sell.vals), D.ptr(up.sp), D.ptr(up.cols),
+                                         D.ptr(up.vals), C.byref(ok), D.stream()), "fuse_check")
+            fuse = bool(ok.value)
+        return cls(n, b, smap, sell, fact, work, fuse)
 
     def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
               check_lag: int = 2) -> BicgResult:
@@ -218,6 +230,7 @@ class DeviceKrylov:
                 args.ngroups = len(s.gslice_host) - 1
                 args.goff1 = s.goff1
                 args.gslice_host = s.gslice_host.ctypes.data
+                args.fuse = 1 if self.fuse else 0
         args.rhs, args.x, args.work = D.ptr(rhs), D.ptr(x), D.ptr(self.work)
         args.stream = D.stream()
         res = BicgResult()

@@ -346,6 +346,7 @@ def test_phased_sweeps_bit_equal_to_sync_free(monkeypatch, golden, name):
     g = golden(name)
     a = matrix(g)
     plan = P.graph_color(a.pattern)
+    monkeypatch.setenv("B2S_FUSE", "0")   # the fused SpMV rounds colour-0 rows differently
     f1 = P.decompose(a, plan)
     monkeypatch.setenv("B2S_PHASED", "0")
     f0 = P.decompose(a, plan)
@@ -357,3 +358,30 @@ def test_phased_sweeps_bit_equal_to_sync_free(monkeypatch, golden, name):
     x1, r1 = P.bicgstab(P.MatrixOperator(a), f1, rhs, stop=P.StoppingCriteria(1e-8, 200))
     assert r0.iterations == r1.iterations and r0.final_norm == r1.final_norm
     assert_array_equal(x0.data, x1.data)
+
+
+@pytest.mark.parametrize("dims", [(20, 20, 10), (13, 7, 9)])
+def test_fused_colour_pass_matches_unfused(monkeypatch, dims):
+    """2-colour solves fuse colour 0's backward sweep with its SpMV rows
+    (csrc/fused.cu); same iterations, solution within round-off of the
+    unfused loop (only the SpMV's rounding order of colour-0 rows differs)."""
+    bundle = P.generate(P.GeneratorSpec(*dims, seed=11))
+    a, rhs = bundle.a, bundle.rhs
+    f = P.decompose(a, P.graph_color(a.pattern))
+    op = P.MatrixOperator(a)
+    stop = P.StoppingCriteria(1e-8, 200)
+    from paper_2309_11488_b200.krylov import DeviceKrylov
+    assert DeviceKrylov.build(a, f).fuse
+    x1, r1 = P.bicgstab(op, f, rhs, stop=stop)
+    monkeypatch.setenv("B2S_FUSE", "0")
+    assert not DeviceKrylov.build(a, f).fuse
+    x0, r0 = P.bicgstab(op, f, rhs, stop=stop)
+    assert r1.converged and r0.converged
+    assert abs(r1.iterations - r0.iterations) <= 0.5
+    assert np.linalg.norm(x1.data - x0.data) <= 1e-9 * np.linalg.norm(x0.data)
+    rp, ci, v3 = a.pattern.row_pointers, a.pattern.column_indices, a.values3d
+    fo = O.ilu0(rp, ci, v3, O.plan_from_groups(O.color_groups(rp, ci)))
+    xo, ro = O.bicgstab(lambda v: O.spmv(rp, ci, v3, v), lambda r: O.ilu0_apply(fo, r),
+                        rhs.data, tol=1e-8)
+    assert abs(r1.iterations - ro.iterations) <= 1.0
+    assert np.linalg.norm(x1.data - xo) <= 1e-8 * np.linalg.norm(xo)
