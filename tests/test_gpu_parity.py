@@ -17,7 +17,7 @@ import paper_2309_11488_b200 as P  # noqa: E402
 from oracle import port as O  # noqa: E402
 from tests.helpers import dominant_matrix, pattern_from_rows, stencil_pattern  # noqa: E402
 
-SYSTEMS = ["c1_20x20x10", "gen_6x5x4_b2", "gen_7x3x5_b1"]
+SYSTEMS = ["c1_20x20x10", "gen_6x5x4_b2", "gen_7x3x5_b1", "masked_14x16x8", "hetero_10x12x6"]
 PLANS = {"level": P.level_schedule, "color": P.graph_color,
          "sequential": lambda p: P.sequential_plan(p.num_block_rows)}
 
@@ -62,6 +62,8 @@ def test_spmv_and_dot(golden, name):
 @pytest.mark.parametrize("strategy", ["level", "color", "sequential"])
 def test_factor_apply_solve(golden, name, strategy):
     g = golden(name)
+    if f"{strategy}_lu" not in g:
+        pytest.skip("fixture built for level/colour only")
     a = matrix(g)
     plan = PLANS[strategy](a.pattern)
     f = P.decompose(a, plan)
@@ -83,8 +85,9 @@ def test_factor_apply_solve(golden, name, strategy):
         assert rep.group_count == plan.group_count
         ref = g[f"{strategy}_tol{tol:g}_x"]
         assert np.linalg.norm(x.data - ref) <= 1e-8 * np.linalg.norm(ref)
-        # the reported norm is the reference's: ||s|| or ||r|| at exit
-        assert_allclose(rep.final_norm, fin, rtol=1e-6)
+        # the reported norm is the reference's: ||s|| or ||r|| at exit (its
+        # rounding scales with ||r0||, which matters on ill-conditioned cases)
+        assert abs(rep.final_norm - fin) <= max(1e-6 * fin, 1e-10 * n0)
 
 
 def test_random_nonsymmetric_patterns(golden):
@@ -385,3 +388,57 @@ def test_fused_colour_pass_matches_unfused(monkeypatch, dims):
                         rhs.data, tol=1e-8)
     assert abs(r1.iterations - ro.iterations) <= 1.0
     assert np.linalg.norm(x1.data - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+
+@pytest.mark.parametrize("backend", ["level", "color"])
+def test_c2_masked_full_size(golden, backend):
+    """BASELINE config 1 (NORNE-scale masked, 47,605 cells, irregular): device
+    plans bit-exact against the reference's, the same iteration count, and
+    the solution within the tolerance of the reference's."""
+    from paper_2309_11488_b200 import synthetic as S
+    d = golden("c2_masked_digest")
+    bnd = S.generate_masked(46, 112, 22, seed=2309)
+    a = bnd.a
+    plan = (P.level_schedule if backend == "level" else P.graph_color)(a.pattern)
+    assert_array_equal(plan.row_group, d[f"{backend}_row_group"])
+    cfg = P.SolverConfig(backend=P.Backend.from_name(backend), stop=P.StoppingCriteria(1e-8, 200))
+    x, rep = P.solve_with_fallback(cfg, a, bnd.rhs)
+    conv, its, n0, fin = d[f"{backend}_report"]
+    assert rep.converged and not rep.fallback_used
+    assert abs(rep.iterations - its) <= 1.0, (rep.iterations, its)
+    assert_allclose(rep.initial_norm, n0, rtol=1e-12)
+    ref = d[f"{backend}_x"]
+    assert np.linalg.norm(x.data - ref) <= 1e-7 * np.linalg.norm(ref)
+    f = P.decompose(a, plan)
+    assert_allclose(np.linalg.norm(f.inverted_diagonals), float(d[f"{backend}_invd_norm"]),
+                    rtol=1e-12)
+    assert_allclose(np.linalg.norm(f.combined.values), float(d[f"{backend}_lu_norm"]),
+                    rtol=1e-12)
+
+
+@pytest.mark.parametrize("backend", ["level", "color"])
+def test_c4_full_size_properties(golden, backend):
+    """BASELINE config 3 (1M cells) at full size, by size-independent
+    properties: device plan == oracle plan bit for bit (298 levels / 2
+    colours), the solve converges, and the true residual of the returned x,
+    recomputed by the oracle's SpMV on the host, meets the tolerance."""
+    bnd = P.generate(P.GeneratorSpec(100, 100, 100, seed=0))
+    a = bnd.a
+    rp, ci, v3 = a.pattern.row_pointers, a.pattern.column_indices, a.values3d
+    plan = (P.level_schedule if backend == "level" else P.graph_color)(a.pattern)
+    ref = (O.level_groups if backend == "level" else O.color_groups)(rp, ci)
+    assert_array_equal(plan.row_group, ref)
+    assert plan.group_count == (298 if backend == "level" else 2)
+    tol = 1e-8
+    cfg = P.SolverConfig(backend=P.Backend.from_name(backend), stop=P.StoppingCriteria(tol, 200))
+    x, rep = P.solve_with_fallback(cfg, a, bnd.rhs)
+    assert rep.converged and not rep.fallback_used
+    d = golden("c4_digest")   # the reference's own run (tests/golden/make_configs.py --c4)
+    conv, its, n0, fin = d[f"{backend}_report"]
+    assert abs(rep.iterations - its) <= 1.0, (rep.iterations, its)
+    assert_allclose(rep.initial_norm, n0, rtol=1e-12)
+    assert_allclose(x.data[d["x_idx"]], d[f"{backend}_x_sample"], rtol=0,
+                    atol=1e-7 * np.abs(d[f"{backend}_x_sample"]).max())
+    r = bnd.rhs.data - O.spmv(rp, ci, v3, x.data)
+    assert np.linalg.norm(r) <= tol * np.linalg.norm(bnd.rhs.data) * 1.01
