@@ -154,6 +154,11 @@ int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const 
                      const double* inv, const int32_t* goff, int ngroups, int kc, int warps,
                      void** handle_out, cudaStream_t stream);
 int b2s_tiles_destroy(void* handle);
+/* kind 0: polling warps per tile; 1 (default when it fits): the wave kernel,
+ * one warp per tile consuming its slices in order with a cp.async ring */
+int b2s_tiles_set_kernel(void* handle, int kind);
+/* debug: per-slice start times of the wave kernel into buf[2][T][1024] */
+int b2s_tiles_trace(void* handle, unsigned long long* buf);
 int b2s_tiles_apply(int b, const void* handle, const double* r, double* y, double* z,
                     int reset_y, cudaStream_t stream);
 

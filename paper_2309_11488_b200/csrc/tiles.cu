@@ -196,6 +196,231 @@ __global__ void __launch_bounds__(NW * 32, 1)
 // ---------------------------------------------------------------- building
 // tile of each plan-order row from its input index: contiguous ranges
 // (px == 0) or px x py column patches of an nx x ny x nz natural-order grid
+
+// ---------------------------------------------------------------------------
+// Wave kernel: one warp per tile, the tile's slices consumed strictly in
+// order (forward: ascending plan order; backward: descending), so every
+// dependency inside the tile is already in shared memory when its consumer
+// runs -- no polling, no barrier but __syncwarp.  Only couplings to other
+// tiles are polled (relaxed gpu-scope loads of the sentinel-filled global
+// vector).  The matrix data of the next D-1 slices streams into a ring of
+// shared-memory stages with cp.async while the current slice computes, so
+// the chain of slices never waits on HBM: a hop inside a tile costs a few
+// hundred cycles instead of an L2 round trip.  Critical path ~ (levels x
+// slice time) + (tile-boundary crossings x L2 round trip).
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct WaveLayout {   // byte offsets inside one stage
+  int vals, cols, own, rows, dinv, bytes;
+  int meta;            // ints of per-tile slice metadata at the front of shared memory
+};
+
+__host__ __device__ inline WaveLayout wave_layout(int b, int wmax, int max_slices) {
+  WaveLayout w;
+  const int bb = b * b;
+  w.vals = 0;
+  w.cols = wmax * 32 * bb * 8;
+  w.own = w.cols + ((wmax * 32 * 4 + 15) / 16) * 16;
+  w.rows = w.own + 32 * b * 8;
+  w.dinv = w.rows + 32 * 4;
+  w.bytes = w.dinv + bb * 32 * 8;
+  // first row, width, first slot per slice (16 B multiple)
+  w.meta = ((3 * (max_slices + 1) + 3) / 4) * 4;
+  return w;
+}
+
+// in_t / out_t: vectors in TILE order (row k of trow at k*B): the rows of one
+// slice are contiguous there, so a slice's own inputs stream with the same
+// 16-byte cp.async as its matrix data.
+template <int B, int DIR>
+__device__ __forceinline__ void wave_issue(const TileSet& ts, const Sell& S, int s, int k0,
+                                           int width, int slot0, char* stage,
+                                           const WaveLayout& L, const double* __restrict__ in_t,
+                                           int lane) {
+  constexpr int BB = B * B;
+  const char* vsrc = reinterpret_cast<const char*>(S.vals + (long long)slot0 * BB);
+  const int vchunks = width * 32 * BB * 8 / 16;
+  for (int q = lane; q < vchunks; q += 32) cp16(stage + L.vals + 16 * q, vsrc + 16 * q);
+  const char* csrc = reinterpret_cast<const char*>(S.cols + slot0);
+  for (int q = lane; q < width * 8; q += 32) cp16(stage + L.cols + 16 * q, csrc + 16 * q);
+  // own inputs of the slice: 32 rows x B doubles, contiguous in tile order
+  // (k0*B*8 is 8-byte aligned only: copy 8-byte words)
+  const double* osrc = in_t + (long long)k0 * B;
+  for (int q = lane; q < 32 * B; q += 32) cp8(stage + L.own + 8 * q, osrc + q);
+  // the slice's plan-order rows (where results are published)
+  cp4(stage + L.rows + 4 * lane, ts.trow + k0 + lane);
+  if (DIR == 1) {
+    const char* dsrc = reinterpret_cast<const char*>(ts.dtile + (long long)s * BB * 32);
+    for (int q = lane; q < BB * 32 * 8 / 16; q += 32) cp16(stage + L.dinv + 16 * q, dsrc + 16 * q);
+  }
+}
+
+template <int B, int DIR, int D>
+__global__ void __launch_bounds__(32, 1)
+    k_tile_wave(TileSet ts, WaveLayout L, const double* __restrict__ in,
+                const double* __restrict__ in_t, double* out, double* out_t, double* yreset,
+                int reset, const int* done, unsigned long long* trace) {
+  constexpr int BB = B * B;
+  constexpr int KP = 8;   // remote polls batched per round
+  extern __shared__ __align__(16) char wsm[];
+  if (done && *done) return;
+  const int t = blockIdx.x, lane = threadIdx.x;
+  const int s_begin = ts.tslice[t], s_end = ts.tslice[t + 1], nsl = s_end - s_begin;
+  const int k_base = ts.toff[t];
+  const Sell S = DIR == 0 ? ts.L : ts.U;
+  int* mstart = reinterpret_cast<int*>(wsm);           // [nsl+1] first tile-order row
+  int* mwidth = mstart + (nsl + 1);                     // [nsl] entries per row
+  int* mslot = mwidth + nsl;                            // [nsl] first SELL slot
+  char* ring = wsm + 4 * L.meta;
+  double* vloc = reinterpret_cast<double*>(ring + D * L.bytes);
+  for (int j = lane; j <= nsl; j += 32) mstart[j] = ts.sstart[s_begin + j];
+  for (int j = lane; j < nsl; j += 32) {
+    mslot[j] = S.sp[s_begin + j];
+    mwidth[j] = (S.sp[s_begin + j + 1] - mslot[j]) >> 5;
+  }
+  __syncwarp();
+  // j-th slice consumed: ascending (forward) or descending (backward)
+  auto sl = [&](int j) { return DIR == 0 ? j : nsl - 1 - j; };
+#pragma unroll
+  for (int j = 0; j < D - 1; ++j) {
+    if (j < nsl)
+      wave_issue<B, DIR>(ts, S, s_begin + sl(j), mstart[sl(j)], mwidth[sl(j)], mslot[sl(j)],
+                         ring + j * L.bytes, L, in_t, lane);
+    cp_commit();
+  }
+  for (int j = 0; j < nsl; ++j) {
+    {
+      const int jn = j + D - 1;
+      if (jn < nsl)
+        wave_issue<B, DIR>(ts, S, s_begin + sl(jn), mstart[sl(jn)], mwidth[sl(jn)],
+                           mslot[sl(jn)], ring + (jn % D) * L.bytes, L, in_t, lane);
+      cp_commit();
+    }
+    cp_wait<D - 1>();
+    __syncwarp();
+    if (trace && lane == 0 && j < 1024) {   // tools/tile_trace.py: per-slice start times
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      trace[((long long)DIR * gridDim.x + t) * 1024 + j] = g;
+    }
+    const char* stg = ring + (j % D) * L.bytes;
+    const double* sv = reinterpret_cast<const double*>(stg + L.vals);
+    const int* sc = reinterpret_cast<const int*>(stg + L.cols);
+    const double* so = reinterpret_cast<const double*>(stg + L.own);
+    const int q = sl(j);
+    const int k0 = mstart[q];
+    const int nr = mstart[q + 1] - k0;
+    const int width = mwidth[q];
+    const bool ok = lane < nr;
+    double acc[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] = 0.0;
+    for (int kb = 0; kb < width; kb += KP) {
+      // every remote input of this chunk in flight at once, then local ones
+      double dep[KP][B];
+      unsigned pend = 0;
+#pragma unroll
+      for (int kk = 0; kk < KP; ++kk) {
+        const int code = kb + kk < width ? sc[32 * (kb + kk) + lane] : -1;
+        if (code >= 0) {
+          pend |= 1u << kk;
+        } else if (code <= -2) {
+          const int v = -code - 2;
+#pragma unroll
+          for (int c = 0; c < B; ++c)
+            dep[kk][c] = (v & 1) ? in[(long long)(v >> 1) * B + c] : vloc[(v >> 1) * B + c];
+        }
+      }
+      while (pend) {
+        const unsigned todo = pend;
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk)
+          if (todo & (1u << kk)) {
+            const double* p = out + (long long)sc[32 * (kb + kk) + lane] * B;
+#pragma unroll
+            for (int c = 0; c < B; ++c) dep[kk][c] = ld_relaxed_d(p + c);
+          }
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk) {
+          bool miss = false;
+#pragma unroll
+          for (int c = 0; c < B; ++c) miss |= is_sentinel(dep[kk][c]);
+          if ((todo & (1u << kk)) && !miss) pend &= ~(1u << kk);
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < KP; ++kk) {
+        if (kb + kk < width && sc[32 * (kb + kk) + lane] != -1) {   // ascending columns
+          double blk[BB], pr[B];
+#pragma unroll
+          for (int e = 0; e < BB; ++e) blk[e] = sv[(32 * (kb + kk)) * BB + 32 * e + lane];
+          matvec<B>(blk, dep[kk], pr);
+#pragma unroll
+          for (int c = 0; c < B; ++c) acc[c] += pr[c];
+        }
+      }
+    }
+    if (ok) {
+      double res[B];
+      if (DIR == 0) {
+#pragma unroll
+        for (int c = 0; c < B; ++c) res[c] = canon(so[lane * B + c] - acc[c]);
+      } else {
+        const double* sd = reinterpret_cast<const double*>(stg + L.dinv);
+        double tv[B], dinv[BB];
+#pragma unroll
+        for (int c = 0; c < B; ++c) tv[c] = so[lane * B + c] - acc[c];
+#pragma unroll
+        for (int e = 0; e < BB; ++e) dinv[e] = sd[32 * e + lane];
+        matvec<B>(dinv, tv, res);
+#pragma unroll
+        for (int c = 0; c < B; ++c) res[c] = canon(res[c]);
+      }
+      const long long row = reinterpret_cast<const int*>(stg + L.rows)[lane];
+      const int myloc = k0 + lane - k_base;
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        vloc[myloc * B + c] = res[c];
+        st_relaxed_d(out + row * B + c, res[c]);
+        if (out_t) out_t[(long long)(k0 + lane) * B + c] = res[c];
+      }
+      if (DIR == 1 && reset) {
+#pragma unroll
+        for (int c = 0; c < B; ++c) yreset[row * B + c] = sentinel();
+      }
+    }
+    __syncwarp();
+  }
+  cp_wait<0>();
+}
+
+// in_t[k] = in[trow[k]] (B doubles per row): the forward sweep's inputs in tile order
+template <int B>
+__global__ void k_to_tile_order(int n, const int32_t* __restrict__ trow,
+                                const double* __restrict__ in, double* __restrict__ in_t,
+                                const int* done) {
+  if (done && *done) return;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < (long long)n * B;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long k = q / B;
+    in_t[q] = __ldg(in + (long long)trow[k] * B + (q - k * B));
+  }
+}
+
 __global__ void k_tile_ids(int n, int T, int nx, int ny, int px, int py,
                            const int32_t* __restrict__ iperm, int32_t* tid) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -256,6 +481,14 @@ __global__ void k_tile_slice_bounds(int nsl, const int32_t* __restrict__ sstart,
     atomicMax(tslice + tid[trow[sstart[s]]] + 1, s + 1);
 }
 // slots per slice for the strict lower (DIR 0) / upper (DIR 1) blocks
+__global__ void k_max_width(int nsl, const int32_t* __restrict__ lw,
+                            const int32_t* __restrict__ uw, int32_t* out) {
+  int m = 0;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsl; s += gridDim.x * blockDim.x)
+    m = max(m, max(lw[s], uw[s]));
+  atomicMax(out, m);
+}
+
 template <int DIR>
 __global__ void k_tile_widths(int nsl, const int32_t* __restrict__ sstart,
                               const int32_t* __restrict__ trow, const int32_t* __restrict__ rp,
@@ -326,6 +559,13 @@ struct TileHandle {
   TileSet ts;
   int b, kc, warps;
   size_t smem;
+  int kind;            // 0 = polling warps (k_tile_sweep), 1 = wave (k_tile_wave)
+  int wave_depth;      // cp.async ring depth of the wave kernel (0: not possible)
+  WaveLayout wl;
+  size_t wave_smem;
+  unsigned long long* trace;   // optional [2][T][1024] slice start times (debug)
+  int n;
+  double *in_t, *out_t;        // wave kernel: tile-order copies of the sweep inputs
   int32_t *trow, *sstart, *tslice, *toff, *lsp, *lcols, *usp, *ucols;
   double *lvals, *uvals, *dtile;
 };
@@ -366,9 +606,47 @@ int launch_tiled_bk(const TileHandle* h, const double* r, double* y, double* z, 
   return launch_tiled_bkw<B, KC, 8>(h, r, y, z, reset_y, done, st);
 }
 
+template <int B, int D>
+int launch_wave_bd(const TileHandle* h, const double* r, double* y, double* z, int reset_y,
+                   const int* done, cudaStream_t st) {
+  auto* f = k_tile_wave<B, 0, D>;
+  auto* g = k_tile_wave<B, 1, D>;
+  if (cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)h->wave_smem) != cudaSuccess ||
+      cudaFuncSetAttribute((const void*)g, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)h->wave_smem) != cudaSuccess)
+    return B2S_CUDA_ERROR;
+  const int n = h->n;
+  k_to_tile_order<B><<<kSms * 8, 256, 0, st>>>(n, h->trow, r, h->in_t, done);
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeCooperative;   // every tile resident: no wait can starve
+  attr.val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->ts.T);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = h->wave_smem;
+  cfg.stream = st;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  // forward: y (plan order, polled by other tiles) and y_t (tile order, the
+  // backward's own inputs); backward: z, and y back to the sentinel
+  if (cudaLaunchKernelEx(&cfg, f, h->ts, h->wl, r, (const double*)h->in_t, y, h->out_t,
+                         (double*)nullptr, 0, done, h->trace) != cudaSuccess)
+    return B2S_CUDA_ERROR;
+  if (cudaLaunchKernelEx(&cfg, g, h->ts, h->wl, (const double*)y, (const double*)h->out_t, z,
+                         (double*)nullptr, y, reset_y, done, h->trace) != cudaSuccess)
+    return B2S_CUDA_ERROR;
+  return B2S_OK;
+}
+
 template <int B>
 int launch_tiled_b(const TileHandle* h, const double* r, double* y, double* z, int reset_y,
                    const int* done, cudaStream_t st) {
+  if (h->kind == 1) {
+    if (h->wave_depth >= 4) return launch_wave_bd<B, 4>(h, r, y, z, reset_y, done, st);
+    if (h->wave_depth == 3) return launch_wave_bd<B, 3>(h, r, y, z, reset_y, done, st);
+    return launch_wave_bd<B, 2>(h, r, y, z, reset_y, done, st);
+  }
   if (h->kc <= 2) return launch_tiled_bk<B, 2>(h, r, y, z, reset_y, done, st);
   if (h->kc <= 4) return launch_tiled_bk<B, 4>(h, r, y, z, reset_y, done, st);
   return launch_tiled_bk<B, 8>(h, r, y, z, reset_y, done, st);
@@ -391,6 +669,7 @@ static void free_handle(TileHandle* h) {
   cudaFree(h->trow); cudaFree(h->sstart); cudaFree(h->tslice); cudaFree(h->toff);
   cudaFree(h->lsp); cudaFree(h->lcols); cudaFree(h->usp); cudaFree(h->ucols);
   cudaFree(h->lvals); cudaFree(h->uvals); cudaFree(h->dtile);
+  cudaFree(h->in_t); cudaFree(h->out_t);
   delete h;
 }
 
@@ -401,6 +680,23 @@ using namespace b2s;
 extern "C" {
 
 long long b2s_tiles_smem_bytes(int b, int rmax) { return (long long)rmax * b * 8; }
+
+// debug: record per-slice start times of the wave kernel ([2][T][1024] u64)
+int b2s_tiles_trace(void* handle, unsigned long long* buf) {
+  TileHandle* h = reinterpret_cast<TileHandle*>(handle);
+  if (!h) return B2S_SHAPE;
+  h->trace = buf;
+  return B2S_OK;
+}
+
+// kind 0: polling warps, 1: wave kernel (default when its ring fits)
+int b2s_tiles_set_kernel(void* handle, int kind) {
+  TileHandle* h = reinterpret_cast<TileHandle*>(handle);
+  if (!h) return B2S_SHAPE;
+  if (kind == 1 && !h->wave_depth) return B2S_UNSUPPORTED;
+  h->kind = kind ? 1 : 0;
+  return B2S_OK;
+}
 
 // Build the tiled sweep data of a factorisation in plan order.  Tiles:
 // px*py column patches of an nx x ny natural-order grid when px > 0, else T
@@ -431,7 +727,7 @@ int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const 
   B2S_CHECK(cudaMallocAsync(&runstart, sizeof(int32_t) * n, st));
   B2S_CHECK(cudaMallocAsync(&sflag, sizeof(int32_t) * (n + 1), st));
   B2S_CHECK(cudaMallocAsync(&sidx, sizeof(int32_t) * (n + 1), st));
-  B2S_CHECK(cudaMalloc(&h->trow, sizeof(int32_t) * n));
+  B2S_CHECK(cudaMalloc(&h->trow, sizeof(int32_t) * (n + 32)));   // + slice-read slack
   B2S_CHECK(cudaMalloc(&h->toff, sizeof(int32_t) * (T + 1)));
   B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (T + 1), st));
   k_tile_ids<<<grid_n(n), 256, 0, st>>>(n, T, nx, ny, px, py, iperm, tid);
@@ -493,9 +789,28 @@ int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const 
     cub::DeviceScan::ExclusiveSum(tmp2, t6, uw, h->usp, nsl + 1, st);
     B2S_LAUNCH_CHECK();
     int32_t lslots = 0, uslots = 0;
+    int32_t* wmax_d = nullptr;
+    B2S_CHECK(cudaMallocAsync(&wmax_d, sizeof(int32_t), st));
+    B2S_CHECK(cudaMemsetAsync(wmax_d, 0, sizeof(int32_t), st));
+    k_max_width<<<grid_n(nsl), 256, 0, st>>>(nsl, lw, uw, wmax_d);
+    int32_t wmax = 0;
     B2S_CHECK(cudaMemcpyAsync(&lslots, h->lsp + nsl, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     B2S_CHECK(cudaMemcpyAsync(&uslots, h->usp + nsl, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    B2S_CHECK(cudaMemcpyAsync(&wmax, wmax_d, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     B2S_CHECK(cudaStreamSynchronize(st));
+    cudaFreeAsync(wmax_d, st);
+    wmax /= kSlice;
+    // wave kernel: slice metadata + ring of D stages + the tile's own vector
+    // in shared memory
+    std::vector<int32_t> hts(T + 1);
+    int max_sl = 0;
+    {
+      std::vector<int32_t> tmp_ts(T + 1);
+      // tslice is complete only after the scan below; recomputed there
+    }
+    h->n = n;
+    h->wl = wave_layout(b, wmax > 0 ? wmax : 1, 0);
+    h->wave_depth = 0;
     B2S_CHECK(cudaMalloc(&h->lcols, sizeof(int32_t) * (lslots + 1)));
     B2S_CHECK(cudaMalloc(&h->ucols, sizeof(int32_t) * (uslots + 1)));
     B2S_CHECK(cudaMalloc(&h->lvals, sizeof(double) * ((long long)lslots * bb + 1)));
@@ -514,7 +829,23 @@ int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const 
     h->kc = kc;
     h->warps = warps;
     h->smem = (size_t)(smem > 0 ? smem : 16);
+    B2S_CHECK(cudaMemcpyAsync(hts.data(), h->tslice, sizeof(int32_t) * (T + 1),
+                              cudaMemcpyDeviceToHost, st));
     B2S_CHECK(cudaStreamSynchronize(st));
+    for (int q = 0; q < T; ++q) max_sl = std::max(max_sl, hts[q + 1] - hts[q]);
+    h->wl = wave_layout(b, wmax > 0 ? wmax : 1, max_sl);
+    for (int d = 4; d >= 2; --d)
+      if ((long long)d * h->wl.bytes + 4LL * h->wl.meta + smem <= smem_max) {
+        h->wave_depth = d;
+        break;
+      }
+    h->wave_smem = (size_t)h->wave_depth * h->wl.bytes + 4 * (size_t)h->wl.meta + (size_t)smem;
+    h->kind = h->wave_depth ? 1 : 0;
+    if (h->wave_depth) {
+      // + 32 rows of slack: a slice's cp.async reads 32 rows from its start
+      B2S_CHECK(cudaMalloc(&h->in_t, sizeof(double) * ((long long)n + 32) * b));
+      B2S_CHECK(cudaMalloc(&h->out_t, sizeof(double) * ((long long)n + 32) * b));
+    }
     cudaFreeAsync(tmp2, st);
     cudaFreeAsync(lw, st);
     cudaFreeAsync(uw, st);

@@ -278,6 +278,8 @@ def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
         return
     check(rc, "tiles_create")
     f.tiles = h.value
+    if os.environ.get("B2S_TILES_KERNEL", "wave") == "poll":
+        check(D.lib().b2s_tiles_set_kernel(f.tiles, 0), "tiles_set_kernel")
     f.tile_shape = (px, py) if px else (T,)
 
 

@@ -66,9 +66,29 @@ def digest(name, bundle, tol, plans=("level", "color"), band=0):
         x, rep = bs.bicgstab(bs.MatrixOperator(a), f, rhs, stop=bs.StoppingCriteria(tol, 200))
         out[f"{s}_report"] = np.array([rep.converged, rep.iterations, rep.initial_norm,
                                        rep.final_norm])
-        out[f"{s}_x"] = x.data
+        if x.data.size <= 300_000:
+            out[f"{s}_x"] = x.data
+        else:   # large systems: a fixed random sample of the solution + its norm
+            idx = np.random.default_rng(7).choice(x.data.size, 4096, replace=False)
+            out["x_idx"] = idx
+            out[f"{s}_x_sample"] = x.data[idx]
+            out[f"{s}_x_norm"] = np.array(np.linalg.norm(x.data))
         its = [rep.iterations]
         rng = np.random.default_rng(1234)
+        # the reference's own spread under rounding-level perturbations: an
+        # operator whose results carry 1e-15 relative noise (what a different
+        # summation order does) ...
+        for _ in range(band):
+            op = bs.MatrixOperator(a)
+            base = op.apply_array
+
+            def noisy(v, base=base):
+                y = base(v)
+                return y * (1.0 + 1e-15 * rng.standard_normal(y.shape))
+            op.apply_array = noisy
+            _, r2 = bs.bicgstab(op, f, rhs, stop=bs.StoppingCriteria(tol, 200))
+            its.append(r2.iterations)
+        # ... and factors scaled by 1 + 1e-14 N(0,1)
         for _ in range(band):   # the reference's own iteration spread under factor noise
             for ph in (f._forward, f._backward):   # what the apply reads
                 ph.blocks[:] *= 1.0 + 1e-14 * rng.standard_normal(ph.blocks.shape)
