@@ -101,6 +101,13 @@ int b2s_sell_fill(int nslices, int b, const int32_t* row0, const int32_t* nrows,
                   const int32_t* rp, const int32_t* ci, const double* vals, int sel,
                   const int32_t* sp, const int32_t* goff, int ngroups, int32_t* cols,
                   double* svals, cudaStream_t stream);
+/* as b2s_sell_fill, with the values of pattern slot q read from input slot
+ * src[q] (the permutation's source map): a plan-order layout filled straight
+ * from the unpermuted matrix */
+int b2s_sell_fill_src(int nslices, int b, const int32_t* row0, const int32_t* nrows,
+                      const int32_t* rp, const int32_t* ci, const double* vals, int sel,
+                      const int32_t* sp, const int32_t* goff, int ngroups, int32_t* cols,
+                      double* svals, const int32_t* src, cudaStream_t stream);
 int b2s_diag_tiles(int nslices, int b, const int32_t* row0, const int32_t* nrows,
                    const double* inv, double* tiles, cudaStream_t stream);
 int b2s_slice_conflicts(int nslices, const int32_t* row0, const int32_t* nrows,
@@ -123,6 +130,27 @@ int b2s_spmv(int b, int mode, int nparts, int nslices, const int32_t* row0,
 int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_t* nrows,
                     const int32_t* rp, const int32_t* ci, const int32_t* diag, double* vals,
                     double* inv_diag, int32_t* bad_row_host, cudaStream_t stream);
+
+/* decompose (bs/ilu0.py:145-201) for a plan of two independent groups
+ * (a 2-colouring), straight into SELL layouts on the group-aligned slice map
+ * (csrc/factor2c.cu): reads the operator's SELL (a_*), writes the strict-
+ * lower SELL (l_cols/l_vals on offsets l_sp), the plan-order inverse
+ * diagonals inv (n*b*b), colour 1's U_ii (udiag, (n-goff1)*b*b) and the
+ * per-slice inverse tiles.  s1/goff1: first slice / plan row of colour 1.
+ * B2S_SINGULAR_PIVOT (smallest failing plan row in *bad_row_host), or
+ * B2S_UNSUPPORTED when the pattern is not a 2-colour structure.  Results are
+ * bit-identical to b2s_ilu0_factor. */
+int b2s_factor_2colour(int n, int b, int goff1, int s1, int nslices, const int32_t* row0,
+                       const int32_t* nrows, const int32_t* a_sp, const int32_t* a_cols,
+                       const double* a_vals, const int32_t* l_sp, int32_t* l_cols,
+                       double* l_vals, double* inv, double* udiag, double* dtiles,
+                       int32_t* bad_row_host, cudaStream_t stream);
+/* the plan-order CSR values of combined L\U from the layouts above (rp =
+ * the plan-order row pointers); materialised only on request */
+int b2s_factor_2colour_combined(int n, int b, int goff1, int s1, const int32_t* rp,
+                                const int32_t* a_sp, const int32_t* a_cols, const double* a_vals,
+                                const int32_t* l_sp, const int32_t* l_cols, const double* l_vals,
+                                const double* udiag, double* lu, cudaStream_t stream);
 
 /* Ilu0Factorization.apply_permuted_array (bs/ilu0.py:105-142). */
 int b2s_ilu0_apply(int n, int b, int kc, int nslices, const int32_t* row0, const int32_t* nrows,

@@ -255,6 +255,18 @@ def permute(m: DevBSR, cmap: torch.Tensor, take: torch.Tensor, want_src=False):
     return (out, src) if want_src else out
 
 
+def permute_pattern(p: DevPattern, cmap: torch.Tensor, take: torch.Tensor):
+    """Plan-order pattern and the source map (input slot of every plan-order
+    slot), without moving any values."""
+    dev = p.rp.device
+    rp = empty_i32(p.n + 1, dev)
+    ci = empty_i32(p.nnz, dev)
+    src = empty_i32(p.nnz, dev)
+    check(lib().b2s_permute_bsr(p.n, 1, ptr(p.rp), ptr(p.ci), None, ptr(cmap), ptr(take),
+                                ptr(rp), ptr(ci), None, ptr(src), stream()), "permute_pattern")
+    return DevPattern(p.n, p.nnz, rp, ci), src
+
+
 def gather_rows(v: torch.Tensor, src: torch.Tensor, n: int, b: int) -> torch.Tensor:
     out = torch.empty(n * b, dtype=torch.float64, device=v.device)
     check(lib().b2s_gather_rows(n, b, ptr(src), ptr(v), ptr(out), stream()), "gather_rows")
@@ -327,9 +339,13 @@ class Sell:
 
     @classmethod
     def build(cls, smap: SliceMap, m: DevBSR, sel: int, goff: torch.Tensor | None = None,
-              ngroups: int = 0) -> "Sell":
+              ngroups: int = 0, src: torch.Tensor | None = None,
+              fill: bool = True) -> "Sell":
         """SELL-32 copy of ``m`` (sel 0 all / 1 strict lower / 2 strict upper);
-        with plan group offsets, same-group triangular entries are marked."""
+        with plan group offsets, same-group triangular entries are marked.
+        ``src``: values of pattern slot q come from slot src[q] of ``m.vals``
+        (a permuted layout filled from the unpermuted values).  ``fill=False``
+        only sizes and allocates the layout (a kernel fills it later)."""
         dev = m.pat.rp.device
         sp = empty_i32(smap.nslices + 1, dev)
         slots = C.c_longlong(0)
@@ -341,14 +357,16 @@ class Sell:
             raise ValueError("matrix too large for one device layout")
         cols = empty_i32(ns, dev)
         vals = empty_f64(ns * m.b * m.b, dev)
-        check(lib().b2s_sell_fill(smap.nslices, m.b, ptr(smap.row0), ptr(smap.nrows),
-                                  ptr(m.pat.rp), ptr(m.pat.ci), ptr(m.vals), sel, ptr(sp),
-                                  ptr(goff), int(ngroups), ptr(cols), ptr(vals), stream()),
-              "sell_fill")
+        if fill:
+            check(lib().b2s_sell_fill_src(smap.nslices, m.b, ptr(smap.row0), ptr(smap.nrows),
+                                          ptr(m.pat.rp), ptr(m.pat.ci), ptr(m.vals), sel,
+                                          ptr(sp), ptr(goff), int(ngroups), ptr(cols),
+                                          ptr(vals), ptr(src), stream()), "sell_fill")
         width = 0
         if smap.nslices:
             width = int(((sp[1:smap.nslices + 1] - sp[:smap.nslices]).max().item()) // 32)
-        stale = bool((cols[:ns] <= -2).any().item()) if (goff is not None and ns) else False
+        stale = (bool((cols[:ns] <= -2).any().item())
+                 if (fill and goff is not None and ns) else False)
         return cls(sp, cols, vals, ns, width, stale)
 
 

@@ -60,6 +60,11 @@ SIGNATURES = {
     "b2s_sell_offsets": (_I, [_I, _P, _P, _P, _P, _I, _P, _PLL, _P]),
     "b2s_sell_fill": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P]),
     "b2s_diag_tiles": (_I, [_I, _I, _P, _P, _P, _P, _P]),
+    "b2s_sell_fill_src": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
+    "b2s_factor_2colour": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                _PI, _P]),
+    "b2s_factor_2colour_combined": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                         _P]),
     "b2s_slice_conflicts": (_I, [_I, _P, _P, _P, _P, _PI, _P]),
     "b2s_spmv": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "b2s_ilu0_factor": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _PI, _P]),

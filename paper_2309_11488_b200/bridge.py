@@ -106,6 +106,10 @@ class DeviceSolver:
         self.pre_bsr.wait_values()   # values may still be in flight (overlapped upload)
         self.bsr.wait_values()
         self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr)
+        if self.pre_bsr is self.bsr and self.fact.a_sell is not None:
+            # 2-colour factorisation: the operator's SELL layout already exists
+            self.krylov = DeviceKrylov.build(self.a, self.fact)
+            return self
         a_perm = self.fact._a_perm if self.pre_bsr is self.bsr else None
         if a_perm is None:
             from .analysis import permute_device

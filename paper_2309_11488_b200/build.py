@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libb200solve.so"
-SOURCES = ["analysis.cu", "spmv.cu", "factor.cu", "ilu0.cu", "fused.cu", "tiles.cu", "krylov.cu",
+SOURCES = ["analysis.cu", "spmv.cu", "factor.cu", "ilu0.cu", "fused.cu", "factor2c.cu", "tiles.cu", "krylov.cu",
            "jacobi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

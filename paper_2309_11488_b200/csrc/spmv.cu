@@ -90,7 +90,7 @@ __global__ void k_sell_fill(int nslices, int bb, const int32_t* __restrict__ row
                             int sel, const int32_t* __restrict__ sp,
                             const int32_t* __restrict__ goff, int ngroups,
                             int32_t* __restrict__ ocols,
-                            double* __restrict__ ovals) {
+                            double* __restrict__ ovals, const int32_t* __restrict__ src) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -108,7 +108,10 @@ __global__ void k_sell_fill(int nslices, int bb, const int32_t* __restrict__ row
         // at once, bs/ilu0.py:125-142): encode them as -(c + 2)
         const bool stale = goff != nullptr && group_of(goff, ngroups, c) == group_of(goff, ngroups, row);
         ocols[slot0 + 32ll * k + lane] = stale ? -(c + 2) : c;
-        for (int e = 0; e < bb; ++e) ovals[vidx(slot0, k, e, lane, bb)] = vals[(long long)q * bb + e];
+        // values of slot q, or of input slot src[q] (straight from the
+        // unpermuted matrix: the plan-order CSR values are never built)
+        const long long qv = src ? src[q] : q;
+        for (int e = 0; e < bb; ++e) ovals[vidx(slot0, k, e, lane, bb)] = vals[qv * bb + e];
         ++k;
       }
     }
@@ -336,17 +339,25 @@ int b2s_sell_offsets(int nslices, const int32_t* row0, const int32_t* nrows, con
   return B2S_OK;
 }
 
-int b2s_sell_fill(int nslices, int b, const int32_t* row0, const int32_t* nrows,
-                  const int32_t* rp, const int32_t* ci, const double* vals, int sel,
-                  const int32_t* sp, const int32_t* goff, int ngroups, int32_t* cols,
-                  double* svals, cudaStream_t st) {
+int b2s_sell_fill_src(int nslices, int b, const int32_t* row0, const int32_t* nrows,
+                      const int32_t* rp, const int32_t* ci, const double* vals, int sel,
+                      const int32_t* sp, const int32_t* goff, int ngroups, int32_t* cols,
+                      double* svals, const int32_t* src, cudaStream_t st) {
   if (nslices < 0 || b < 1 || sel < 0 || sel > 2) return B2S_SHAPE;
   if (nslices == 0) return B2S_OK;
   k_sell_fill<<<grid_for((long long)nslices * 32), 256, 0, st>>>(nslices, b * b, row0, nrows, rp,
                                                                   ci, vals, sel, sp, goff, ngroups,
-                                                                  cols, svals);
+                                                                  cols, svals, src);
   B2S_LAUNCH_CHECK();
   return B2S_OK;
+}
+
+int b2s_sell_fill(int nslices, int b, const int32_t* row0, const int32_t* nrows,
+                  const int32_t* rp, const int32_t* ci, const double* vals, int sel,
+                  const int32_t* sp, const int32_t* goff, int ngroups, int32_t* cols,
+                  double* svals, cudaStream_t st) {
+  return b2s_sell_fill_src(nslices, b, row0, nrows, rp, ci, vals, sel, sp, goff, ngroups, cols,
+                           svals, nullptr, st);
 }
 
 int b2s_diag_tiles(int nslices, int b, const int32_t* row0, const int32_t* nrows,

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _device as D
-from ._lib import SINGULAR_PIVOT, check
+from ._lib import SINGULAR_PIVOT, UNSUPPORTED, check
 from .analysis import ParallelPlan, apply_permutation, dev_to_matrix, permute_device
 from .blockcore import BlockMatrix, BlockVector
 from .errors import MissingDiagonal, ShapeError, SingularPivot
@@ -39,7 +39,7 @@ class Ilu0Factorization:
 
     def __init__(self, plan: ParallelPlan, b: int, n: int, lu: "D.DevBSR", invd: torch.Tensor,
                  smap: "D.SliceMap", lower: "D.Sell", upper: "D.Sell", dtiles: torch.Tensor,
-                 identity: bool, source: BlockMatrix, a_perm: "D.DevBSR"):
+                 identity: bool, source: BlockMatrix, a_perm: "D.DevBSR", two_colour=None):
         self.plan = plan
         self._b = b
         self._n = n
@@ -47,12 +47,17 @@ class Ilu0Factorization:
         self._invd = invd
         self.smap = smap
         self.lower = lower
-        self.upper = upper
+        self._upper = upper
         self.dtiles = dtiles
         self._identity_perm = identity
         self._source = source        # the (block-row-major) matrix that was factored
         self._a_perm = a_perm        # its unfactored plan-order copy (reused as operator)
-        self.kc = _kc(max(lower.width, upper.width))
+        # 2-colour plans (csrc/factor2c.cu): the operator's SELL layout (U's
+        # rows live there) and what is needed to rebuild the CSR factors
+        self._two_colour = two_colour
+        self.a_sell = two_colour["a_sell"] if two_colour else None
+        uw = (self.a_sell.width - 1) if two_colour else upper.width
+        self.kc = _kc(max(lower.width, uw))
         self._combined = None
         self._inv_host = None
         self._tickets = torch.zeros(8, dtype=torch.int32, device=invd.device)
@@ -64,8 +69,33 @@ class Ilu0Factorization:
         self.tiles = None        # b2s_tiles_create handle (tiled level sweeps), or None
         # few independent groups (colourings) and no same-group entries: the
         # phased sweeps, 2(G-1) plain passes, no polling (bit-identical)
-        self.phased = (smap.gslice_host is not None and not lower.stale and not upper.stale
+        ustale = False if two_colour else upper.stale
+        self.phased = (smap.gslice_host is not None and not lower.stale and not ustale
                        and os.environ.get("B2S_PHASED", "1") != "0")
+
+    # -- lazily materialised pieces of a 2-colour factorisation ----------------
+    @property
+    def lu_device(self) -> "D.DevBSR":
+        """Combined L\\U in plan order, block CSR (built on first use for 2-colour
+        factorisations, which never need it on the solve path)."""
+        if self._lu is None:
+            t = self._two_colour
+            pat, a_s, lo = t["pattern"], t["a_sell"], self.lower
+            bb = self._b * self._b
+            vals = D.empty_f64(pat.nnz * bb, pat.rp.device)
+            check(D.lib().b2s_factor_2colour_combined(
+                self._n, self._b, t["goff1"], t["s1"], D.ptr(pat.rp), D.ptr(a_s.sp),
+                D.ptr(a_s.cols), D.ptr(a_s.vals), D.ptr(lo.sp), D.ptr(lo.cols), D.ptr(lo.vals),
+                D.ptr(t["udiag"]), D.ptr(vals), D.stream()), "factor_2colour_combined")
+            self._lu = D.DevBSR(pat, self._b, vals)
+        return self._lu
+
+    @property
+    def upper(self) -> "D.Sell":
+        if self._upper is None:
+            self._upper = D.Sell.build(self.smap, self.lu_device, 2,
+                                       self.plan.device("group_offsets"), self.plan.group_count)
+        return self._upper
 
     # -- reference attributes --------------------------------------------------
     @property
@@ -81,10 +111,10 @@ class Ilu0Factorization:
         if self._combined is None:
             if self._identity_perm:
                 bb = self._b * self._b
-                vals = self._lu.vals[: self._lu.pat.nnz * bb].cpu().numpy()
+                vals = self.lu_device.vals[: self.lu_device.pat.nnz * bb].cpu().numpy()
                 self._combined = BlockMatrix(self._source.pattern, self._b, vals)
             else:
-                self._combined = dev_to_matrix(self._lu)
+                self._combined = dev_to_matrix(self.lu_device)
         return self._combined
 
     @property
@@ -99,7 +129,7 @@ class Ilu0Factorization:
         """The combined factors carried back to input numbering (bs/ilu0.py:79-83)."""
         if self._identity_perm:
             return self.combined.copy()
-        return dev_to_matrix(permute_device(self._lu, self.plan, inverse=True))
+        return dev_to_matrix(permute_device(self.lu_device, self.plan, inverse=True))
 
     # -- application -------------------------------------------------------------
     def apply_device(self, r_perm: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -175,6 +205,40 @@ class Ilu0Factorization:
             self.tiles = None
 
 
+def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR"):
+    """2-colour plans: operator layout + factors straight from the input
+    values (csrc/factor2c.cu); None if the pattern is not a 2-colour
+    structure (then the general path runs)."""
+    n, b = a.num_block_rows, a.block_size
+    bb = b * b
+    dev = bsr.pat.rp.device
+    pat, src = D.permute_pattern(bsr.pat, plan.device("permutation"),
+                                 plan.device("inverse_permutation"))
+    smap = plan.slice_map()
+    if smap.gslice_host is None or len(smap.gslice_host) != 3:
+        return None
+    s1, goff1 = int(smap.gslice_host[1]), int(smap.goff1)
+    a_sell = D.Sell.build(smap, D.DevBSR(pat, b, bsr.vals), 0, src=src)
+    lower = D.Sell.build(smap, D.DevBSR(pat, b, bsr.vals), 1, fill=False)
+    inv = D.empty_f64(n * bb, dev)
+    udiag = D.empty_f64((n - goff1) * bb, dev)
+    dtiles = D.empty_f64(smap.nslices * bb * 32, dev)
+    bad = C.c_int32(-1)
+    rc = D.lib().b2s_factor_2colour(n, b, goff1, s1, smap.nslices, D.ptr(smap.row0),
+                                    D.ptr(smap.nrows), D.ptr(a_sell.sp), D.ptr(a_sell.cols),
+                                    D.ptr(a_sell.vals), D.ptr(lower.sp), D.ptr(lower.cols),
+                                    D.ptr(lower.vals), D.ptr(inv), D.ptr(udiag), D.ptr(dtiles),
+                                    C.byref(bad), D.stream())
+    if rc == UNSUPPORTED:
+        return None
+    if rc == SINGULAR_PIVOT:
+        raise SingularPivot(int(plan.device("inverse_permutation")[int(bad.value)].item()))
+    check(rc, "factor_2colour")
+    tc = {"pattern": pat, "a_sell": a_sell, "udiag": udiag, "goff1": goff1, "s1": s1}
+    return Ilu0Factorization(plan, b, n, None, inv, smap, lower, None, dtiles, False, a, None,
+                             two_colour=tc)
+
+
 def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) -> Ilu0Factorization:
     """``decompose`` on an (optionally pre-uploaded) matrix."""
     a = a.as_block_row_major()
@@ -186,6 +250,11 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) ->
     dev = bsr.pat.rp.device
     D.find_diagonal(bsr.pat)                       # MissingDiagonal(first row)
     identity = plan.is_identity
+    if (plan.group_count == 2 and not identity and b <= 4 and
+            os.environ.get("B2S_FACTOR_2C", "1") != "0"):
+        f = _factor_two_colour(a, plan, bsr)
+        if f is not None:
+            return f
     a_perm = bsr if identity else permute_device(bsr, plan)
     lu = D.DevBSR(a_perm.pat, b, a_perm.vals.clone())
     diag = D.find_diagonal(lu.pat)

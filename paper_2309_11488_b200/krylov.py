@@ -178,22 +178,30 @@ class DeviceKrylov:
     def build(cls, matrix: BlockMatrix, fact: Ilu0Factorization | None,
               a_bsr: "D.DevBSR" = None) -> "DeviceKrylov":
         n, b = matrix.num_block_rows, matrix.block_size
+        fuse_env = os.environ.get("B2S_FUSE", "1") != "0"
+        sell = None
         if fact is not None:
             smap = fact.smap
-            if a_bsr is None:
+            if a_bsr is None and fact.a_sell is not None and fact._source is matrix:
+                sell = fact.a_sell   # 2-colour factorisation: the operator layout exists
+            elif a_bsr is None:
                 a_bsr = (fact._a_perm if fact._source is matrix
                          else _plan_order(D.DevBSR.upload(matrix), fact))
-            dev = a_bsr.pat.rp.device
+            dev = fact.dtiles.device
         else:
             a_bsr = a_bsr or D.DevBSR.upload(matrix)
             dev = a_bsr.pat.rp.device
             smap = D.SliceMap.plain(n, dev)
-        sell = D.Sell.build(smap, a_bsr, 0)
+        if sell is None:
+            sell = D.Sell.build(smap, a_bsr, 0)
         nbytes = int(D.lib().b2s_bicgstab_workspace_bytes(n, b, D.NPARTS))
         work = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=dev)
         fuse = False
-        if (fact is not None and fact.phased and not fact.tiles and
-                len(smap.gslice_host) == 3 and os.environ.get("B2S_FUSE", "1") != "0"):
+        if sell is not None and fact is not None and sell is fact.a_sell:
+            # U's colour-0 rows are this very layout (factor2c.cu): fusable by construction
+            fuse = fact.phased and fuse_env
+        elif (fact is not None and fact.phased and not fact.tiles and
+                len(smap.gslice_host) == 3 and fuse_env):
             ok = C.c_int32(0)
             up = fact.upper
             check(D.lib().b2s_fuse_check(int(smap.gslice_host[1]), b, D.ptr(smap.row0),
@@ -213,7 +221,7 @@ class DeviceKrylov:
         args.kc = f.kc if f is not None else 2
         args.maxit = stop.max_iterations
         args.check_lag = check_lag
-        args.refill_y = 1 if (f is not None and f.upper.stale) else 0
+        args.refill_y = 1 if (f is not None and not self.fuse and f.upper.stale) else 0
         args.sweep_flags = f.sweep_flags if f is not None else 0
         args.tol = stop.relative_reduction
         s = self.smap
@@ -222,8 +230,9 @@ class DeviceKrylov:
         if f is not None:
             args.l_sp, args.l_cols, args.l_vals = (D.ptr(f.lower.sp), D.ptr(f.lower.cols),
                                                    D.ptr(f.lower.vals))
-            args.u_sp, args.u_cols, args.u_vals = (D.ptr(f.upper.sp), D.ptr(f.upper.cols),
-                                                   D.ptr(f.upper.vals))
+            if not self.fuse:   # (the fused passes read U's rows from the operator)
+                args.u_sp, args.u_cols, args.u_vals = (D.ptr(f.upper.sp), D.ptr(f.upper.cols),
+                                                       D.ptr(f.upper.vals))
             args.dinv_tiles = D.ptr(f.dtiles)
             args.tiles = f.tiles
             if f.phased and not f.tiles:

@@ -467,3 +467,31 @@ def test_c3_hetero_full_size(golden):
     rp, ci, v3 = a.pattern.row_pointers, a.pattern.column_indices, a.values3d
     r = bnd.rhs.data - O.spmv(rp, ci, v3, x.data)
     assert np.linalg.norm(r) <= tol * n0 * 1.01
+
+
+@pytest.mark.parametrize("name", SYSTEMS)
+def test_two_colour_factor_bit_equal_to_general(monkeypatch, golden, name):
+    """2-colour plans factor straight into the SELL layouts (csrc/factor2c.cu):
+    combined factors, inverse diagonals, applications and solves are
+    bit-identical to the general sync-free factorisation."""
+    g = golden(name)
+    a = matrix(g)
+    plan = P.graph_color(a.pattern)
+    f1 = P.decompose(a, plan)
+    monkeypatch.setenv("B2S_FACTOR_2C", "0")
+    f0 = P.decompose(a, plan)
+    assert f0.a_sell is None
+    assert (f1.a_sell is not None) == (plan.group_count == 2)
+    assert_array_equal(f1.combined.pattern.column_indices, f0.combined.pattern.column_indices)
+    assert_array_equal(f1.combined.values, f0.combined.values)
+    assert_array_equal(f1.inverted_diagonals, f0.inverted_diagonals)
+    assert_array_equal(f1.factors_in_input_order().values, f0.factors_in_input_order().values)
+    r = P.BlockVector(g["x"], a.block_size)
+    assert_array_equal(f1.apply(r).data, f0.apply(r).data)
+    close(f1.combined.values, g["color_lu"], 1e-12)
+    rhs = P.BlockVector(g["rhs"], a.block_size)
+    stop = P.StoppingCriteria(1e-8, 200)
+    x0, r0 = P.bicgstab(P.MatrixOperator(a), f0, rhs, stop=stop)
+    x1, r1 = P.bicgstab(P.MatrixOperator(a), f1, rhs, stop=stop)
+    assert r0.iterations == r1.iterations and r0.final_norm == r1.final_norm
+    assert_array_equal(x0.data, x1.data)
