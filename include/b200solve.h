@@ -54,6 +54,11 @@ int b2s_level_schedule(int n, const int32_t* rp, const int32_t* ci, int32_t* row
 int b2s_graph_color(int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,
                     int32_t* ngroups_host, cudaStream_t stream);
 
+/* debug: rerun the level (kind 0) / colour (1) kernel recording each row's
+ * publication time (%globaltimer, ns) in trace[n] */
+int b2s_analysis_trace(int kind, int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,
+                       unsigned long long* trace, cudaStream_t stream);
+
 /* _plan_from_groups (bs/analysis.py:61-71): perm (old->new), iperm (new->old,
  * stable), offsets (ngroups+1). */
 int b2s_plan_from_groups(int n, const int32_t* row_group, int ngroups, int32_t* perm,

@@ -54,71 +54,102 @@ constexpr int kNb = 8;
 
 // level(i) = 1 + max level(j) over strict-lower j, 0 without lower
 // neighbours (bs/analysis.py:85-100).  level[] must be -1 on entry.
-__global__ void k_level_sync_free(int n, const int32_t* __restrict__ rp,
+__device__ __forceinline__ void trace_row(unsigned long long* trace, int i) {
+  if (trace) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    trace[i] = g;
+  }
+}
+
+// A warp claims R consecutive 32-row slices per ticket (lane l holds rows
+// l, l+32, ..., of the unit) and polls all of them each round.  The window of
+// rows in flight is what limits these wavefronts: rows are claimed in index
+// order but become ready along the (diagonal) level front, so a window
+// smaller than the front's index spread throttles it (measured on C4: 1-slice
+// units, ~11-23 z-planes in flight, ran at 1/4-1/7 of the hop speed).  Short
+// neighbour lists in registers keep R rows per lane affordable; longer rows
+// walk their list from memory.  Deadlock-free: units are claimed in order by
+// running warps, and the smallest unfinished row always has its inputs.
+constexpr int kLNb = 4;    // lower neighbours held in registers (level)
+constexpr int kLR = 6;     // slices per warp unit (level)
+
+__global__ void __launch_bounds__(256, 5) k_level_sync_free(int n, const int32_t* __restrict__ rp,
                                   const int32_t* __restrict__ ci, int32_t* level,
-                                  unsigned int* ticket) {
+                                  unsigned int* ticket, unsigned long long* trace = nullptr) {
   const int lane = threadIdx.x & 31;
+  // neighbour lists live in shared memory (registers would cap the rows in flight)
+  __shared__ int snb[8][kLR][kLNb][32];
+  auto nb = [&](int q, int w) -> int& { return snb[threadIdx.x >> 5][q][w][lane]; };
   for (;;) {
-    unsigned int s = 0;
-    if (lane == 0) s = atomicAdd(ticket, 1u);
-    s = __shfl_sync(0xffffffffu, s, 0);
-    const long long row0 = (long long)s * kSlice;
-    if (row0 >= n) break;
-    const int i = (int)row0 + lane;
-    bool done = i >= n;
-    int nb[kNb];
-    int cnt = 0, k = 0, end = 0;
-    bool longrow = false;
-    if (!done) {
-      k = rp[i];
-      end = rp[i + 1];
-      for (int q = k; q < end; ++q) {
-        const int j = ci[q];
-        if (j >= i) break;
-        if (cnt < kNb) {
+    unsigned int u = 0;
+    if (lane == 0) u = atomicAdd(ticket, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    const long long base = (long long)u * kLR * kSlice;
+    if (base >= n) break;
+    unsigned pend[kLR];
+    int best[kLR], k[kLR], end[kLR];
+    bool longrow[kLR], live[kLR];
+    // (row by row: measured faster here than issuing all rows' setup loads
+    // together -- unlike the colour kernel, whose setup is twice as long)
 #pragma unroll
-          for (int t = 0; t < kNb; ++t)
-            if (t == cnt) nb[t] = j;
+    for (int q = 0; q < kLR; ++q) {
+      const long long i = base + q * kSlice + lane;
+      live[q] = i < n;
+      pend[q] = 0; best[q] = -1; k[q] = 0; end[q] = 0; longrow[q] = false;
+      if (live[q]) {
+        k[q] = rp[i];
+        end[q] = rp[i + 1];
+        int cnt = 0;
+        for (int t = k[q]; t < end[q]; ++t) {
+          const int j = ci[t];
+          if (j >= i) break;
+          if (cnt < kLNb) nb(q, cnt) = j;
+          ++cnt;
         }
-        ++cnt;
+        longrow[q] = cnt > kLNb;
+        pend[q] = longrow[q] ? 0u : ((1u << cnt) - 1u);
       }
-      longrow = cnt > kNb;
     }
-    unsigned int pend = (!done && !longrow) ? ((1u << cnt) - 1u) : 0u;
-    int best = -1;
     for (;;) {
-      if (!done) {
-        if (!longrow) {
-          int got[kNb];
+      bool any = false;
 #pragma unroll
-          for (int t = 0; t < kNb; ++t)
-            got[t] = (pend & (1u << t)) ? ld_relaxed_i(level + nb[t]) : -1;
+      for (int q = 0; q < kLR; ++q) {
+        if (!live[q]) continue;
+        const int i = (int)(base + q * kSlice + lane);
+        bool fin;
+        if (!longrow[q]) {
+          int got[kLNb];
 #pragma unroll
-          for (int t = 0; t < kNb; ++t)
-            if ((pend & (1u << t)) && got[t] >= 0) {
-              best = max(best, got[t]);
-              pend &= ~(1u << t);
+          for (int w = 0; w < kLNb; ++w)
+            got[w] = (pend[q] & (1u << w)) ? ld_relaxed_i(level + nb(q, w)) : -1;
+#pragma unroll
+          for (int w = 0; w < kLNb; ++w)
+            if ((pend[q] & (1u << w)) && got[w] >= 0) {
+              best[q] = max(best[q], got[w]);
+              pend[q] &= ~(1u << w);
             }
-          if (!pend) {
-            st_relaxed_i(level + i, best + 1);
-            done = true;
-          }
+          fin = !pend[q];
         } else {
-          while (k < end) {
-            const int j = ci[k];
-            if (j >= i) { k = end; break; }
+          while (k[q] < end[q]) {
+            const int j = ci[k[q]];
+            if (j >= i) { k[q] = end[q]; break; }
             const int lj = ld_relaxed_i(level + j);
             if (lj < 0) break;  // not yet published
-            best = max(best, lj);
-            ++k;
+            best[q] = max(best[q], lj);
+            ++k[q];
           }
-          if (k >= end) {
-            st_relaxed_i(level + i, best + 1);
-            done = true;
-          }
+          fin = k[q] >= end[q];
+        }
+        if (fin) {
+          st_relaxed_i(level + i, best[q] + 1);
+          trace_row(trace, i);
+          live[q] = false;
+        } else {
+          any = true;
         }
       }
-      if (__all_sync(0xffffffffu, done)) break;
+      if (!__any_sync(0xffffffffu, any)) break;
     }
   }
 }
@@ -133,106 +164,183 @@ __device__ __forceinline__ int mex64(unsigned long long used) {
   return used == ~0ull ? 64 : __ffsll((long long)~used) - 1;
 }
 
-__global__ void k_color_sync_free(int n, const int32_t* __restrict__ rp,
+constexpr int kCNb = 6;    // symmetrised lower neighbours held in registers (colour)
+constexpr int kCR = 6;     // slices per warp unit (colour)
+
+// neighbours j < i of row i in the symmetrised graph, deduplicated: the
+// row's own lower entries, then the transposed upper entries (ut) not
+// already present; returns the count (entries beyond KC are not stored)
+template <int KC>
+__device__ __forceinline__ int color_nbrs(int i, const int32_t* __restrict__ rp,
+                                          const int32_t* __restrict__ ci,
+                                          const int32_t* __restrict__ ut_ptr,
+                                          const int32_t* __restrict__ ut_idx, int (&nb)[KC]) {
+  int cnt = 0;
+  for (int q = rp[i]; q < rp[i + 1]; ++q) {
+    const int j = ci[q];
+    if (j >= i) break;
+    if (cnt < KC) {
+#pragma unroll
+      for (int t = 0; t < KC; ++t)
+        if (t == cnt) nb[t] = j;
+    }
+    ++cnt;
+  }
+  const int nrow = cnt;
+  for (int q = ut_ptr[i]; q < ut_ptr[i + 1]; ++q) {
+    const int j = ut_idx[q];
+    bool dup = false;  // (j,i) and (i,j) both stored: one neighbour
+    if (nrow <= KC) {
+#pragma unroll
+      for (int t = 0; t < KC; ++t)
+        if (t < nrow && nb[t] == j) dup = true;
+    } else {
+      for (int t = rp[i]; t < rp[i] + nrow; ++t) dup |= ci[t] == j;
+    }
+    if (dup) continue;
+    if (cnt < KC) {
+#pragma unroll
+      for (int t = 0; t < KC; ++t)
+        if (t == cnt) nb[t] = j;
+    }
+    ++cnt;
+  }
+  return cnt;
+}
+
+// mex over the symmetrised lower neighbours, walked from memory (long rows);
+// returns -1 while some neighbour is unpublished
+__device__ int color_walk(int i, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const int32_t* __restrict__ ut_ptr, const int32_t* __restrict__ ut_idx,
+                          const int32_t* color) {
+  unsigned long long used = 0ull;
+  bool big = false;
+  for (int q = rp[i]; q < rp[i + 1]; ++q) {
+    const int j = ci[q];
+    if (j >= i) break;
+    const int cj = ld_relaxed_i(color + j);
+    if (cj < 0) return -1;
+    if (cj < 64) used |= 1ull << cj; else big = true;
+  }
+  for (int q = ut_ptr[i]; q < ut_ptr[i + 1]; ++q) {
+    const int cj = ld_relaxed_i(color + ut_idx[q]);
+    if (cj < 0) return -1;
+    if (cj < 64) used |= 1ull << cj; else big = true;
+  }
+  int c = mex64(used);
+  if (big && c >= 64) {   // rare: >= 64 distinct neighbour colours
+    for (bool hit = true; hit;) {
+      hit = false;
+      for (int q = rp[i]; q < rp[i + 1] && !hit; ++q) {
+        const int j = ci[q];
+        if (j < i && ld_relaxed_i(color + j) == c) hit = true;
+      }
+      for (int q = ut_ptr[i]; q < ut_ptr[i + 1] && !hit; ++q)
+        if (ld_relaxed_i(color + ut_idx[q]) == c) hit = true;
+      if (hit) ++c;
+    }
+  }
+  return c;
+}
+
+// (same R-slice units as k_level_sync_free)
+__global__ void __launch_bounds__(256, 5) k_color_sync_free(int n, const int32_t* __restrict__ rp,
                                   const int32_t* __restrict__ ci,
                                   const int32_t* __restrict__ ut_ptr,
                                   const int32_t* __restrict__ ut_idx, int32_t* color,
-                                  unsigned int* ticket) {
-  constexpr int kC = 2 * kNb;
+                                  unsigned int* ticket, unsigned long long* trace = nullptr) {
   const int lane = threadIdx.x & 31;
+  __shared__ int snb[8][kCR][kCNb][32];   // neighbour lists (see k_level_sync_free)
   for (;;) {
-    unsigned int s = 0;
-    if (lane == 0) s = atomicAdd(ticket, 1u);
-    s = __shfl_sync(0xffffffffu, s, 0);
-    const long long row0 = (long long)s * kSlice;
-    if (row0 >= n) break;
-    const int i = (int)row0 + lane;
-    bool done = i >= n;
-    int nb[kC];
-    int cnt = 0;
-    if (!done) {
-      for (int q = rp[i]; q < rp[i + 1]; ++q) {
-        const int j = ci[q];
-        if (j >= i) break;
-        if (cnt < kC) {
+    unsigned int u = 0;
+    if (lane == 0) u = atomicAdd(ticket, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    const long long base = (long long)u * kCR * kSlice;
+    if (base >= n) break;
+    unsigned pend[kCR];
+    unsigned used[kCR];   // colours 0..31 seen: a short row's mex is <= kCNb
+    bool longrow[kCR], live[kCR];
+    // row setup in two rounds for all R rows at once (row and transposed
+    // extents, then the first entries of both lists); rows whose neighbour
+    // set may exceed kCNb walk memory instead (color_walk)
+    int k0[kCR], k1[kCR], u0[kCR], u1[kCR];
 #pragma unroll
-          for (int t = 0; t < kC; ++t)
-            if (t == cnt) nb[t] = j;
-        }
-        ++cnt;
-      }
-      const int nrow = cnt;  // the row's own lower neighbours come first
-      for (int q = ut_ptr[i]; q < ut_ptr[i + 1]; ++q) {
-        const int j = ut_idx[q];
-        bool dup = false;  // (j,i) and (i,j) both stored: one neighbour
-#pragma unroll
-        for (int t = 0; t < kC; ++t)
-          if (t < nrow && t < kC && nb[t] == j) dup = true;
-        if (dup) continue;
-        if (cnt < kC) {
-#pragma unroll
-          for (int t = 0; t < kC; ++t)
-            if (t == cnt) nb[t] = j;
-        }
-        ++cnt;
-      }
+    for (int q = 0; q < kCR; ++q) {
+      const long long i = base + q * kSlice + lane;
+      live[q] = i < n;
+      pend[q] = 0; used[q] = 0u; longrow[q] = false;
+      k0[q] = live[q] ? rp[i] : 0;
+      k1[q] = live[q] ? rp[i + 1] : 0;
+      u0[q] = live[q] ? ut_ptr[i] : 0;
+      u1[q] = live[q] ? ut_ptr[i + 1] : 0;
     }
-    const bool longrow = cnt > kC;
-    unsigned int pend = (!done && !longrow) ? (cnt == 32 ? ~0u : ((1u << cnt) - 1u)) : 0u;
-    unsigned long long used = 0ull;  // colours 0..63 seen
-    bool big = false;                 // some neighbour has colour >= 64
-    // long lists: phase 0 walks the row, phase 1 the transposed list
-    int k = done ? 0 : rp[i], end = done ? 0 : rp[i + 1], phase = 0;
-    for (;;) {
-      if (!done) {
-        bool ready = false;
-        if (!longrow) {
-          int got[kC];
 #pragma unroll
-          for (int t = 0; t < kC; ++t)
-            got[t] = (pend & (1u << t)) ? ld_relaxed_i(color + nb[t]) : -1;
+    for (int q = 0; q < kCR; ++q) {
+      const long long i = base + q * kSlice + lane;
+      int c[kCNb + 1], t[kCNb + 1];
 #pragma unroll
-          for (int t = 0; t < kC; ++t)
-            if ((pend & (1u << t)) && got[t] >= 0) {
-              if (got[t] < 64) used |= 1ull << got[t]; else big = true;
-              pend &= ~(1u << t);
-            }
-          ready = !pend;
-        } else {
-          for (;;) {
-            if (k >= end) {
-              if (phase == 0) { phase = 1; k = ut_ptr[i]; end = ut_ptr[i + 1]; continue; }
-              break;
-            }
-            const int j = (phase == 0) ? ci[k] : ut_idx[k];
-            if (phase == 0 && j >= i) { k = end; continue; }
-            const int cj = ld_relaxed_i(color + j);
-            if (cj < 0) break;
-            if (cj < 64) used |= 1ull << cj; else big = true;
-            ++k;
-          }
-          ready = phase == 1 && k >= end;
+      for (int w = 0; w <= kCNb; ++w) {
+        c[w] = k0[q] + w < k1[q] ? ci[k0[q] + w] : n;
+        t[w] = u0[q] + w < u1[q] ? ut_idx[u0[q] + w] : -1;
+      }
+      int cnt = 0;
+      int nbq[kCNb];
+#pragma unroll
+      for (int w = 0; w <= kCNb; ++w)
+        if (c[w] < i) {
+          if (cnt < kCNb) nbq[cnt] = c[w];
+          ++cnt;
         }
-        if (ready) {
-          int c = mex64(used);
-          if (big && c >= 64) {
-            // rare: >= 64 distinct neighbour colours; walk the set directly
-            for (bool hit = true; hit;) {
-              hit = false;
-              for (int q = rp[i]; q < rp[i + 1] && !hit; ++q) {
-                const int j = ci[q];
-                if (j < i && ld_relaxed_i(color + j) == c) hit = true;
-              }
-              for (int q = ut_ptr[i]; q < ut_ptr[i + 1] && !hit; ++q)
-                if (ld_relaxed_i(color + ut_idx[q]) == c) hit = true;
-              if (hit) ++c;
+      const int nrow = cnt;
+      bool overflow = nrow > kCNb || u1[q] - u0[q] > kCNb;
+#pragma unroll
+      for (int w = 0; w < kCNb; ++w) {
+        if (t[w] < 0) continue;
+        bool dup = false;   // (j,i) and (i,j) both stored: one neighbour
+#pragma unroll
+        for (int v = 0; v < kCNb; ++v) dup |= v < nrow && nbq[v] == t[w];
+        if (dup) continue;
+        if (cnt < kCNb) nbq[cnt] = t[w];
+        ++cnt;
+      }
+      overflow |= cnt > kCNb;
+#pragma unroll
+      for (int w = 0; w < kCNb; ++w) snb[threadIdx.x >> 5][q][w][lane] = nbq[w];
+      longrow[q] = overflow;
+      pend[q] = (live[q] && !overflow) ? ((1u << cnt) - 1u) : 0u;
+    }
+    for (;;) {
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < kCR; ++q) {
+        if (!live[q]) continue;
+        const int i = (int)(base + q * kSlice + lane);
+        int c = -1;
+        if (!longrow[q]) {
+          int got[kCNb];
+#pragma unroll
+          for (int w = 0; w < kCNb; ++w)
+            got[w] = (pend[q] & (1u << w)) ? ld_relaxed_i(color + snb[threadIdx.x >> 5][q][w][lane])
+                                           : -1;
+#pragma unroll
+          for (int w = 0; w < kCNb; ++w)
+            if ((pend[q] & (1u << w)) && got[w] >= 0) {
+              if (got[w] < 32) used[q] |= 1u << got[w];   // larger ones cannot be the mex
+              pend[q] &= ~(1u << w);
             }
-          }
+          if (!pend[q]) c = __ffs(~used[q]) - 1;
+        } else {
+          c = color_walk(i, rp, ci, ut_ptr, ut_idx, color);
+        }
+        if (c >= 0) {
           st_relaxed_i(color + i, c);
-          done = true;
+          trace_row(trace, i);
+          live[q] = false;
+        } else {
+          any = true;
         }
       }
-      if (__all_sync(0xffffffffu, done)) break;
+      if (!__any_sync(0xffffffffu, any)) break;
     }
   }
 }
@@ -370,12 +478,18 @@ inline int grid_for(long long work, int threads = 256) {
   return (int)g;
 }
 
-// persistent sync-free grids: enough resident warps to cover many levels
-inline int sync_free_grid(int n) {
-  long long slices = ((long long)n + kSlice - 1) / kSlice;
-  long long ctas = (slices + 7) / 8;  // 8 warps per CTA
-  long long cap = (long long)kSms * 8;
-  return (int)(ctas < 1 ? 1 : (ctas > cap ? cap : ctas));
+// persistent sync-free grids: every thread resident (the strided dealing
+// relies on it), sized from the kernel's occupancy
+inline int sync_free_grid(int n, const void* fn) {
+  int per_sm = 0, dev = 0, sms = kSms;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long need = ((long long)n + 255) / 256;
+  const long long cap = (long long)per_sm * sms;
+  return (int)(need < 1 ? 1 : (need > cap ? cap : need));
 }
 
 }  // namespace b2s
@@ -426,7 +540,7 @@ int b2s_level_schedule(int n, const int32_t* rp, const int32_t* ci, int32_t* row
   B2S_CHECK(cudaMallocAsync(&ticket, sizeof(unsigned int), st));
   B2S_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
   k_fill_int<<<grid_for(n), 256, 0, st>>>(n, row_group, -1);
-  k_level_sync_free<<<sync_free_grid(n), 256, 0, st>>>(n, rp, ci, row_group, ticket);
+  k_level_sync_free<<<sync_free_grid(n, (const void*)k_level_sync_free), 256, 0, st>>>(n, rp, ci, row_group, ticket);
   B2S_LAUNCH_CHECK();
   B2S_CHECK(cudaFreeAsync(ticket, st));
   return finish_groups(n, row_group, ngroups_host, st);
@@ -457,7 +571,7 @@ int b2s_graph_color(int n, const int32_t* rp, const int32_t* ci, int32_t* row_gr
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, ptr, n + 1, st);
   k_upper_fill<<<grid_for(n), 256, 0, st>>>(n, rp, ci, ptr, fill, idx);
   k_fill_int<<<grid_for(n), 256, 0, st>>>(n, row_group, -1);
-  k_color_sync_free<<<sync_free_grid(n), 256, 0, st>>>(n, rp, ci, ptr, idx, row_group, ticket);
+  k_color_sync_free<<<sync_free_grid(n, (const void*)k_color_sync_free), 256, 0, st>>>(n, rp, ci, ptr, idx, row_group, ticket);
   B2S_LAUNCH_CHECK();
   B2S_CHECK(cudaFreeAsync(tmp, st));
   B2S_CHECK(cudaFreeAsync(cnt, st));
@@ -466,6 +580,45 @@ int b2s_graph_color(int n, const int32_t* rp, const int32_t* ci, int32_t* row_gr
   B2S_CHECK(cudaFreeAsync(idx, st));
   B2S_CHECK(cudaFreeAsync(ticket, st));
   return finish_groups(n, row_group, ngroups_host, st);
+}
+
+// debug (tools/analysis_trace.py): publication time of every row
+int b2s_analysis_trace(int kind, int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,
+                       unsigned long long* trace, cudaStream_t st) {
+  if (n <= 0) return B2S_SHAPE;
+  unsigned int* ticket = nullptr;
+  B2S_CHECK(cudaMallocAsync(&ticket, sizeof(unsigned int), st));
+  B2S_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+  k_fill_int<<<grid_for(n), 256, 0, st>>>(n, row_group, -1);
+  if (kind == 0) {
+    k_level_sync_free<<<sync_free_grid(n, (const void*)k_level_sync_free), 256, 0, st>>>(n, rp, ci, row_group, ticket, trace);
+  } else {
+    int32_t nnz = 0;
+    B2S_CHECK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    B2S_CHECK(cudaStreamSynchronize(st));
+    int32_t *cnt, *ptr, *fill, *idx;
+    B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (n + 1), st));
+    B2S_CHECK(cudaMallocAsync(&ptr, sizeof(int32_t) * (n + 1), st));
+    B2S_CHECK(cudaMallocAsync(&fill, sizeof(int32_t) * n, st));
+    B2S_CHECK(cudaMallocAsync(&idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1), st));
+    B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n + 1), st));
+    B2S_CHECK(cudaMemsetAsync(fill, 0, sizeof(int32_t) * n, st));
+    k_upper_count<<<grid_for(n), 256, 0, st>>>(n, rp, ci, cnt);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, ptr, n + 1, st);
+    void* tmp = nullptr;
+    B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, ptr, n + 1, st);
+    k_upper_fill<<<grid_for(n), 256, 0, st>>>(n, rp, ci, ptr, fill, idx);
+    k_color_sync_free<<<sync_free_grid(n, (const void*)k_color_sync_free), 256, 0, st>>>(n, rp, ci, ptr, idx, row_group, ticket,
+                                                         trace);
+    cudaFreeAsync(tmp, st); cudaFreeAsync(cnt, st); cudaFreeAsync(ptr, st);
+    cudaFreeAsync(fill, st); cudaFreeAsync(idx, st);
+  }
+  B2S_LAUNCH_CHECK();
+  B2S_CHECK(cudaFreeAsync(ticket, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  return B2S_OK;
 }
 
 // bs/analysis.py:61-71: iperm = stable argsort(row_group), perm = its
