@@ -189,6 +189,7 @@ class DevBSR:
                 out.vals.copy_(src, non_blocking=True)
                 done.record(side)
             out._pending = (None, done)
+            out._side = side
             return out
         import threading
 
@@ -199,6 +200,23 @@ class DevBSR:
         th = threading.Thread(target=copy, daemon=True)
         th.start()
         out._pending = (th, done)
+        return out
+
+    def upload_after(self, a: np.ndarray) -> torch.Tensor:
+        """fp64 device copy of ``a`` queued behind the (overlapped) value
+        upload, so the current stream's pattern analysis does not wait for
+        it on the copy engine; ordered by wait_values()."""
+        side = getattr(self, "_side", None)
+        pending = getattr(self, "_pending", None)
+        if side is None or pending is None or pending[0] is not None:
+            return f64(a, self.vals.device)
+        src = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        out = torch.empty(src.numel(), dtype=torch.float64, device=self.vals.device)
+        with torch.cuda.stream(side):
+            out.copy_(src, non_blocking=is_pinned(src))
+            done = torch.cuda.Event()
+            done.record(side)
+        self._pending = (None, done)
         return out
 
     def wait_values(self):

@@ -164,9 +164,11 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     # the 72 B/block values (the bulk of the upload) travel while the device
     # analyses the pattern; the solve waits for them only at factorisation
     bsr = D.DevBSR.upload(a_sys, overlap=cfg.jacobi_partitions == 0)
-    rhs = D.f64(b.data, dev)
+    # the vectors queue behind the values on the copy stream: the analysis
+    # (pattern only) must not wait for them
+    rhs = bsr.upload_after(b.data)
     x0d = (torch.zeros(n * bs, dtype=torch.float64, device=dev) if x0 is None
-           else D.f64(x0.data, dev))
+           else bsr.upload_after(x0.data))
 
     pre_bsr, pre_mat = bsr, a_sys
     primary = None

@@ -36,6 +36,34 @@
 
 namespace b2s {
 
+// Programmatic dependent launch (PDL): a kernel launched with
+// launch_k(..., pdl = true) may start while its predecessor's last CTAs
+// still run; griddep_wait() (first thing in every such kernel, before any
+// read of the predecessor's results) blocks until the predecessor finished
+// and its writes are visible; griddep_launch() lets the successor be
+// scheduled as soon as every CTA of this grid is running.  Both are no-ops
+// for kernels launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? &attr : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 constexpr int kSlice = 32;          // rows per SELL slice == warp width
 constexpr int kSms = 148;           // B200 SM count (grid sizing unit)
 

@@ -37,6 +37,8 @@ __global__ void __launch_bounds__(256) k_bwd_spmv(SliceMap map, int s0, int s1, 
                                                   double* __restrict__ part1, const int* done) {
   constexpr int BB = B * B;
   __shared__ double red[8];
+  griddep_wait();
+  griddep_launch();
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -157,15 +159,17 @@ inline int one_wave(const void* fn, int cap) {
 template <int B>
 int launch_bwd_spmv_b(int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                       const double* yin, double* z, double* v, const double* w, double* p0,
-                      double* p1, const int* done, int* grid_out, cudaStream_t st) {
+                      double* p1, const int* done, int* grid_out, cudaStream_t st, bool pdl) {
   if (mode == kDotW) {
     const int g = one_wave((const void*)k_bwd_spmv<B, kDotW>, nparts);
     *grid_out = g;
-    k_bwd_spmv<B, kDotW><<<g, 256, 0, st>>>(map, 0, s1, a, dt, yin, z, v, w, p0, p1, done);
+    launch_k(k_bwd_spmv<B, kDotW>, dim3(g), dim3(256), 0, st, pdl, map, 0, s1, a, dt, yin, z, v,
+             w, p0, p1, done);
   } else if (mode == kSelfAndW) {
     const int g = one_wave((const void*)k_bwd_spmv<B, kSelfAndW>, nparts);
     *grid_out = g;
-    k_bwd_spmv<B, kSelfAndW><<<g, 256, 0, st>>>(map, 0, s1, a, dt, yin, z, v, w, p0, p1, done);
+    launch_k(k_bwd_spmv<B, kSelfAndW>, dim3(g), dim3(256), 0, st, pdl, map, 0, s1, a, dt, yin, z,
+             v, w, p0, p1, done);
   } else {
     return B2S_SHAPE;
   }
@@ -176,12 +180,12 @@ int launch_bwd_spmv_b(int mode, int nparts, SliceMap map, int s1, Sell a, const 
 // [0, *grid_out) -- at most nparts CTAs, one resident wave
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
-                    double* p1, const int* done, int* grid_out, cudaStream_t st) {
+                    double* p1, const int* done, int* grid_out, cudaStream_t st, bool pdl) {
   switch (b) {
-    case 1: return launch_bwd_spmv_b<1>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st);
-    case 2: return launch_bwd_spmv_b<2>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st);
-    case 3: return launch_bwd_spmv_b<3>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st);
-    case 4: return launch_bwd_spmv_b<4>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st);
+    case 1: return launch_bwd_spmv_b<1>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl);
+    case 2: return launch_bwd_spmv_b<2>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl);
+    case 3: return launch_bwd_spmv_b<3>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl);
+    case 4: return launch_bwd_spmv_b<4>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl);
     default: return B2S_UNSUPPORTED;
   }
 }

@@ -295,6 +295,8 @@ __global__ void __launch_bounds__(256) k_phase_forward(int s0, int s1, int goff1
                                                        double* __restrict__ y,
                                                        double* __restrict__ z, const int* done) {
   constexpr int BB = B * B;
+  griddep_wait();
+  griddep_launch();
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
@@ -342,6 +344,8 @@ __global__ void __launch_bounds__(256) k_phase_backward(int s0, int s1, int goff
                                                         const double* __restrict__ y,
                                                         double* __restrict__ z, const int* done) {
   constexpr int BB = B * B;
+  griddep_wait();
+  griddep_launch();
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
@@ -375,7 +379,7 @@ __global__ void __launch_bounds__(256) k_phase_backward(int s0, int s1, int goff
 template <int B, int KC>
 int launch_phased_bk(int ngroups, const int32_t* gs, int goff1, SliceMap map, Sell lo, Sell up,
                      const double* dt, const double* r, double* y, double* z, const int* done,
-                     bool skip_g0, cudaStream_t st) {
+                     bool skip_g0, cudaStream_t st, bool pdl) {
   static int cap = 0;
   if (!cap) cap = occupancy_grid<B>((const void*)k_phase_forward<B, KC, true>);
   auto grid = [&](int ns) {
@@ -386,17 +390,17 @@ int launch_phased_bk(int ngroups, const int32_t* gs, int goff1, SliceMap map, Se
     const int s0 = gs[g], s1 = gs[g + 1];
     if (s1 <= s0) continue;
     if (g == ngroups - 1)
-      k_phase_forward<B, KC, true><<<grid(s1 - s0), 256, 0, st>>>(s0, s1, goff1, map, lo, dt, r,
-                                                                 y, z, done);
+      launch_k(k_phase_forward<B, KC, true>, dim3(grid(s1 - s0)), dim3(256), 0, st, pdl, s0, s1,
+               goff1, map, lo, dt, r, y, z, done);
     else
-      k_phase_forward<B, KC, false><<<grid(s1 - s0), 256, 0, st>>>(s0, s1, goff1, map, lo, dt, r,
-                                                                  y, z, done);
+      launch_k(k_phase_forward<B, KC, false>, dim3(grid(s1 - s0)), dim3(256), 0, st, pdl, s0, s1,
+               goff1, map, lo, dt, r, y, z, done);
   }
   for (int g = ngroups - 2; g >= (skip_g0 ? 1 : 0); --g) {
     const int s0 = gs[g], s1 = gs[g + 1];
     if (s1 <= s0) continue;
-    k_phase_backward<B, KC><<<grid(s1 - s0), 256, 0, st>>>(s0, s1, goff1, map, up, dt, r, y, z,
-                                                           done);
+    launch_k(k_phase_backward<B, KC>, dim3(grid(s1 - s0)), dim3(256), 0, st, pdl, s0, s1, goff1,
+             map, up, dt, (const double*)r, (const double*)y, z, done);
   }
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
@@ -404,10 +408,10 @@ int launch_phased_bk(int ngroups, const int32_t* gs, int goff1, SliceMap map, Se
 template <int B>
 int launch_phased_b(int kc, int ngroups, const int32_t* gs, int goff1, SliceMap map, Sell lo,
                     Sell up, const double* dt, const double* r, double* y, double* z,
-                    const int* done, bool skip_g0, cudaStream_t st) {
+                    const int* done, bool skip_g0, cudaStream_t st, bool pdl) {
   if (kc <= 2)
-    return launch_phased_bk<B, 2>(ngroups, gs, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st);
-  return launch_phased_bk<B, 4>(ngroups, gs, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st);
+    return launch_phased_bk<B, 2>(ngroups, gs, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st, pdl);
+  return launch_phased_bk<B, 4>(ngroups, gs, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st, pdl);
 }
 
 // ngroups >= 2; gslice_host[g] = first slice of group g (group-aligned map).
@@ -415,13 +419,13 @@ int launch_phased_b(int kc, int ngroups, const int32_t* gs, int goff1, SliceMap 
 // together with the SpMV rows of group 0).
 int launch_phased(int b, int kc, int ngroups, const int32_t* gslice_host, int goff1, SliceMap map,
                   Sell lo, Sell up, const double* dt, const double* r, double* y, double* z,
-                  const int* done, cudaStream_t st, bool skip_g0) {
+                  const int* done, cudaStream_t st, bool skip_g0, bool pdl) {
   if (ngroups < 2) return B2S_SHAPE;
   switch (b) {
-    case 1: return launch_phased_b<1>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st);
-    case 2: return launch_phased_b<2>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st);
-    case 3: return launch_phased_b<3>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st);
-    case 4: return launch_phased_b<4>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st);
+    case 1: return launch_phased_b<1>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st, pdl);
+    case 2: return launch_phased_b<2>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st, pdl);
+    case 3: return launch_phased_b<3>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st, pdl);
+    case 4: return launch_phased_b<4>(kc, ngroups, gslice_host, goff1, map, lo, up, dt, r, y, z, done, skip_g0, st, pdl);
     default: return B2S_UNSUPPORTED;
   }
 }
@@ -539,7 +543,7 @@ int b2s_ilu0_apply_phased(int n, int b, int kc, int ngroups, const int32_t* gsli
   SliceMap map{gslice_host[ngroups], row0, nrows};
   Sell lo{l_sp, l_cols, l_vals}, up{u_sp, u_cols, u_vals};
   return launch_phased(b, kc, ngroups, gslice_host, goff1, map, lo, up, dinv_tiles, r, y, z,
-                       nullptr, st, false);
+                       nullptr, st, false, false);
 }
 
 // z = U^-1 L^-1 r in plan order.  Preconditions: y and z hold the sentinel

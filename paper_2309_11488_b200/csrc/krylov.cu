@@ -23,6 +23,7 @@
 //   t  = A s^,  (t.t, t.s) partials                   (SpMV epilogue)
 //   x += omega s^, r = s - omega t, |r|^2 and r^.r partials (1 kernel)
 #include <cmath>
+#include <cstdlib>
 
 #include "ctl.cuh"
 #include "sell.cuh"
@@ -31,20 +32,21 @@ namespace b2s {
 
 int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
                 const double* w, double* p0, double* p1, const int* done, Ctl ctl,
-                cudaStream_t st);
+                cudaStream_t st, bool pdl = false);
 int launch_sweeps(int b, int kc, SliceMap map, Sell lo, Sell up, const double* dt,
                   const double* r, double* y, double* z, int reset_y, int flags, void* tickets,
                   const int* done, cudaStream_t st);
 int fill_sentinel(long long m, double* v, cudaStream_t st);
 int launch_phased(int b, int kc, int ngroups, const int32_t* gslice_host, int goff1, SliceMap map,
                   Sell lo, Sell up, const double* dt, const double* r, double* y, double* z,
-                  const int* done, cudaStream_t st, bool skip_g0);
+                  const int* done, cudaStream_t st, bool skip_g0, bool pdl = false);
 int launch_spmv_range(int b, int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
                       const double* x, double* y, const double* w, double* p0, double* p1,
-                      const int* done, Ctl ctl, cudaStream_t st);
+                      const int* done, Ctl ctl, cudaStream_t st, bool pdl = false);
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
-                    double* p1, const int* done, int* grid_out, cudaStream_t st);
+                    double* p1, const int* done, int* grid_out, cudaStream_t st,
+                    bool pdl = false);
 int launch_tiled(int b, const void* handle, const double* r, double* y, double* z, int reset_y,
                  const int* done, cudaStream_t st);
 
@@ -92,6 +94,8 @@ __device__ __forceinline__ void st2(double* p, long long j, double a, double b) 
 __global__ void __launch_bounds__(256) k_p_update(long long m, const State* st,
                                                   const double* __restrict__ r,
                                                   const double* __restrict__ v, double* p) {
+  griddep_wait();
+  griddep_launch();
   if (st->done) return;
   const int k = st->k;
   const double beta = st->beta, omega = st->omega;
@@ -135,6 +139,8 @@ __global__ void __launch_bounds__(256) k_s_update(long long m, const State* st,
                                                   double* __restrict__ s, double* pss,
                                                   int reset, Ctl ctl) {
   __shared__ double red[8];
+  griddep_wait();
+  griddep_launch();
   if (st->done) return;
   const double alpha = st->alpha;
   double acc = 0.0;
@@ -178,6 +184,8 @@ __global__ void __launch_bounds__(256) k_r_update(long long m, const State* st, 
                                                   double* __restrict__ r, double* prr,
                                                   double* prho, int reset, Ctl ctl) {
   __shared__ double red[8];
+  griddep_wait();
+  griddep_launch();
   if (st->done) return;
   const double omega = st->omega;
   double a0 = 0.0, a1 = 0.0;
@@ -337,23 +345,29 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       status = B2S_CUDA_ERROR; break;
     }
+    // programmatic dependent launch between the iteration's kernels
+    // (B2S_PDL=0 turns it off)
+    const char* pdl_env = getenv("B2S_PDL");
+    const bool pdl = !(pdl_env && pdl_env[0] == '0');
     double* ph = ilu ? phat : p;
     double* sh = ilu ? shat : s;
-    k_p_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, p); ++kernels;
+    launch_k(k_p_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
+             (const double*)r, (const double*)v, p);
+    ++kernels;
     const int reset_y = a->refill_y ? 0 : 1;
     const int s1c = fused ? a->gslice_host[1] : 0;
     if (fused) {
       launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, p, y,
-                    phat, done, cs, true);
+                    phat, done, cs, true, pdl);
       int g0 = np;
       launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
-                      done, &g0, cs);
+                      done, &g0, cs, pdl);
       launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
-                        done, Ctl{state, counters + 0, dev_done, kCtlAlpha}, cs);
+                        done, Ctl{state, counters + 0, dev_done, kCtlAlpha}, cs, pdl);
       kernels += 3;
     } else if (phased) {
       launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
-                    p, y, phat, done, cs, false);
+                    p, y, phat, done, cs, false, pdl);
       kernels += 2 * (a->ngroups - 1);
     } else if (ilu) {
       if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
@@ -364,22 +378,24 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     }
     if (!fused) {
       launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done,
-                  Ctl{state, counters + 0, dev_done, kCtlAlpha}, cs); ++kernels;
+                  Ctl{state, counters + 0, dev_done, kCtlAlpha}, cs, pdl); ++kernels;
     }
-    k_s_update<<<grid_v, 256, 0, cs>>>(m, state, r, v, ph, a->x, s, pss, reset,
-                                       Ctl{state, counters + 1, dev_done, kCtlS}); ++kernels;
+    launch_k(k_s_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
+             (const double*)r, (const double*)v, ph, a->x, s, pss, reset,
+             Ctl{state, counters + 1, dev_done, kCtlS});
+    ++kernels;
     if (fused) {
       launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, s, y,
-                    shat, done, cs, true);
+                    shat, done, cs, true, pdl);
       int g0 = np;
       launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, s, shat, t, s, ptt, pts, done,
-                      &g0, cs);
+                      &g0, cs, pdl);
       launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
-                        Ctl{state, counters + 2, dev_done, kCtlOmega}, cs);
+                        Ctl{state, counters + 2, dev_done, kCtlOmega}, cs, pdl);
       kernels += 3;
     } else if (phased) {
       launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
-                    s, y, shat, done, cs, false);
+                    s, y, shat, done, cs, false, pdl);
       kernels += 2 * (a->ngroups - 1);
     } else if (ilu) {
       if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
@@ -390,10 +406,11 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     }
     if (!fused) {
       launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done,
-                  Ctl{state, counters + 2, dev_done, kCtlOmega}, cs); ++kernels;
+                  Ctl{state, counters + 2, dev_done, kCtlOmega}, cs, pdl); ++kernels;
     }
-    k_r_update<<<grid_v, 256, 0, cs>>>(m, state, sh, t, s, rhat, a->x, r, prr, prho, reset,
-                                       Ctl{state, counters + 3, dev_done, kCtlEndBegin});
+    launch_k(k_r_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state, sh,
+             (const double*)t, (const double*)s, (const double*)rhat, a->x, r, prr, prho, reset,
+             Ctl{state, counters + 3, dev_done, kCtlEndBegin});
     ++kernels;
     if (cudaStreamEndCapture(cs, &graph) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
     if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }

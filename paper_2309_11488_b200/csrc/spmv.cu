@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(256) k_spmv(SliceMap map, int s0, int s1, int 
                                               Ctl ctl) {
   constexpr int BB = B * B;
   __shared__ double red[8];
+  griddep_wait();
+  griddep_launch();
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -225,13 +227,13 @@ inline int grid_for(long long work, int threads = 256) {
 template <int B>
 int launch_spmv_b(int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
                   const double* x, double* y, const double* w, double* p0, double* p1,
-                  const int* done, Ctl ctl, cudaStream_t st) {
+                  const int* done, Ctl ctl, cudaStream_t st, bool pdl) {
   dim3 g(nparts), t(256);
   switch (mode) {
-    case kPlain: k_spmv<B, kPlain><<<g, t, 0, st>>>(map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
-    case kDotW: k_spmv<B, kDotW><<<g, t, 0, st>>>(map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
-    case kSelfAndW: k_spmv<B, kSelfAndW><<<g, t, 0, st>>>(map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
-    case kResidual: k_spmv<B, kResidual><<<g, t, 0, st>>>(map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
+    case kPlain: launch_k(k_spmv<B, kPlain>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
+    case kDotW: launch_k(k_spmv<B, kDotW>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
+    case kSelfAndW: launch_k(k_spmv<B, kSelfAndW>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
+    case kResidual: launch_k(k_spmv<B, kResidual>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
     default: return B2S_SHAPE;
   }
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
@@ -240,21 +242,21 @@ int launch_spmv_b(int mode, int nparts, SliceMap map, int s0, int s1, int poff, 
 // SpMV over slices [s0, s1) of the map; partials land at [poff, poff + nparts)
 int launch_spmv_range(int b, int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
                       const double* x, double* y, const double* w, double* p0, double* p1,
-                      const int* done, Ctl ctl, cudaStream_t st) {
+                      const int* done, Ctl ctl, cudaStream_t st, bool pdl) {
   switch (b) {
-    case 1: return launch_spmv_b<1>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st);
-    case 2: return launch_spmv_b<2>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st);
-    case 3: return launch_spmv_b<3>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st);
-    case 4: return launch_spmv_b<4>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st);
+    case 1: return launch_spmv_b<1>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl);
+    case 2: return launch_spmv_b<2>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl);
+    case 3: return launch_spmv_b<3>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl);
+    case 4: return launch_spmv_b<4>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl);
     default: return B2S_UNSUPPORTED;
   }
 }
 
 int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
                 const double* w, double* p0, double* p1, const int* done, Ctl ctl,
-                cudaStream_t st) {
+                cudaStream_t st, bool pdl) {
   return launch_spmv_range(b, mode, nparts, map, 0, map.nslices, 0, a, x, y, w, p0, p1, done, ctl,
-                           st);
+                           st, pdl);
 }
 
 }  // namespace b2s
@@ -380,7 +382,7 @@ int b2s_spmv(int b, int mode, int nparts, int nslices, const int32_t* row0,
   if (nslices < 0 || nparts < 1) return B2S_SHAPE;
   SliceMap map{nslices, row0, nrows};
   Sell a{sp, cols, vals};
-  return launch_spmv(b, mode, nparts, map, a, x, y, w, part0, part1, done, Ctl{}, st);
+  return launch_spmv(b, mode, nparts, map, a, x, y, w, part0, part1, done, Ctl{}, st, false);
 }
 
 }  // extern "C"
