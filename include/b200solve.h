@@ -260,6 +260,33 @@ typedef struct {
 long long b2s_bicgstab_workspace_bytes(int n, int b, int nparts);
 int b2s_bicgstab(const b2s_bicg_args* args, b2s_bicg_result* result);
 
+/* ---- wells applied separately (bs/wells.py:125-162, bs/krylov.py:84-94) --- */
+
+/* Device description of a WellSet (standard wells first, then multi-segment
+ * ones, in list order); every pointer is device memory, offsets in doubles.
+ * Built by paper_2309_11488_b200/wells.py (DeviceWells). */
+typedef struct {
+  int nwells, nb;
+  const int32_t *kind, *M, *nseg, *bptr, *bcell, *bseg;
+  const int64_t* boff;
+  const double* bvals;
+  const int64_t* doff;
+  const double* dvals;
+  const int64_t* pivoff;
+  const int32_t* piv;
+  const int64_t* toff;
+  int ncells;
+  const int32_t *cells, *cptr;
+  const int64_t *ccoff, *ct2;
+  const int32_t* cM;
+  const double* cvals;
+} b2s_wells;
+
+/* y -= sum_w C_w^T D_w^-1 B_w x; scratch: sum over wells of nseg*M doubles.
+ * Replaces WellSet.apply_contributions_array (bs/wells.py:196-202). */
+int b2s_wells_apply(const b2s_wells* wells, const double* x, double* y, double* scratch,
+                    cudaStream_t stream);
+
 /* ---- Block-Jacobi copy plan (bs/jacobi.py:111-147) ---------------------- */
 
 int b2s_jacobi_pattern(int n, const int32_t* rp, const int32_t* ci, const int32_t* part,

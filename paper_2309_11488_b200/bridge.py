@@ -28,7 +28,8 @@ from .blockcore import BlockMatrix, BlockVector
 from .errors import SingularPivot, SolveFailed
 from .ilu0 import Ilu0Factorization, factor_device
 from .krylov import (DEFAULT_MAX_ITERATIONS, DeviceKrylov, SolveReport, StoppingCriteria,
-                     _REASONS)
+                     WellAugmentedOperator, _REASONS, bicgstab)
+from .wells import WellMode, WellSet, fold_into_matrix
 
 
 class Backend(enum.Enum):
@@ -45,11 +46,6 @@ class Backend(enum.Enum):
             if member.value == name:
                 return member
         raise ValueError(f"unknown backend {name!r}; choose from {[m.value for m in cls]}")
-
-
-class WellMode(enum.Enum):
-    COUPLED = "coupled"
-    SEPARATE = "separate"
 
 
 @dataclass(frozen=True)
@@ -148,10 +144,17 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     """Configured backend first, sequential ILU0 fallback second
     (bs/bridge.py:71-136)."""
     from .errors import ShapeError
-    if wells is not None and not getattr(wells, "is_empty", True):
-        raise NotImplementedError("wells are not on this build's device path (SURVEY §8(f))")
+    if wells is None:
+        wells = WellSet()
     t0 = time.perf_counter()
-    a_sys = a.as_block_row_major()
+    if cfg.well_mode is WellMode.COUPLED and not wells.is_empty:
+        a_sys = fold_into_matrix(a, wells)          # host assembly, as the reference
+    else:
+        a_sys = a.as_block_row_major()
+        if not wells.is_empty:
+            # the config governs the treatment, whatever the set was marked as
+            sep = WellSet(wells.standard, wells.multisegment, WellMode.SEPARATE)
+            return _solve_separate_wells(cfg, a_sys, sep, b, x0, t0)
     n, bs = a_sys.num_block_rows, a_sys.block_size
     if b.block_size != bs or b.num_blocks != n:
         raise ShapeError("right-hand side does not match the operator")
@@ -220,3 +223,52 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     if not report.converged:
         raise SolveFailed(primary, report)
     return BlockVector(D.to_host(xd, n * bs), bs), report
+
+
+def _solve_separate_wells(cfg: SolverConfig, a_sys: BlockMatrix, wells: WellSet,
+                          b: BlockVector, x0: BlockVector | None, t0: float):
+    """Wells applied after every SpMV (WellAugmentedOperator): device SpMV,
+    device well terms and device ILU0 inside the host-driven BiCGStab loop
+    (bs/bridge.py:92-98,108-136)."""
+    from .errors import ShapeError
+    from .ilu0 import decompose
+    n, bs = a_sys.num_block_rows, a_sys.block_size
+    if b.block_size != bs or b.num_blocks != n:
+        raise ShapeError("right-hand side does not match the operator")
+    op = WellAugmentedOperator(a_sys, wells)
+    primary = None
+    x = None
+    try:
+        pre = a_sys
+        if cfg.jacobi_partitions > 0:
+            from .jacobi import drop_cross_blocks, partition, transmissibility_weights
+            parts = partition(a_sys.pattern, transmissibility_weights(a_sys),
+                              cfg.jacobi_partitions)
+            pre, _ = drop_cross_blocks(a_sys, parts)
+        dev_pat = D.DevPattern.upload(pre.pattern)
+        fact = decompose(pre, plan_device(cfg.backend, dev_pat))
+        setup = time.perf_counter() - t0
+        x, primary = bicgstab(op, fact, b, x0=x0, stop=cfg.stop)
+        primary.setup_elapsed = setup
+    except SingularPivot as exc:
+        primary = _failed_report(f"singular pivot in row {exc.row}")
+        primary.setup_elapsed = time.perf_counter() - t0
+    if primary.converged:
+        return x, primary
+    fb_t0 = time.perf_counter()
+    fb_stop = StoppingCriteria(cfg.stop.relative_reduction,
+                               max(cfg.stop.max_iterations, DEFAULT_MAX_ITERATIONS))
+    try:
+        fb_fact = decompose(a_sys, sequential_plan(n))
+    except SingularPivot as exc:
+        fb_report = _failed_report(f"singular pivot in row {exc.row}")
+        fb_report.fallback_used = True
+        raise SolveFailed(primary, fb_report)
+    fb_setup = time.perf_counter() - fb_t0
+    x, report = bicgstab(op, fb_fact, b, x0=x0, stop=fb_stop)
+    report.fallback_used = True
+    report.setup_elapsed = primary.setup_elapsed + fb_setup
+    report.elapsed += primary.elapsed
+    if not report.converged:
+        raise SolveFailed(primary, report)
+    return x, report

@@ -118,14 +118,24 @@ class MatrixOperator:
 
 
 class WellAugmentedOperator(MatrixOperator):
-    """Well-augmented operator (bs/krylov.py:84-94): next on the roadmap
-    (SURVEY.md §8(f) row 1), not part of this build's hot path."""
+    """SpMV followed by every well's -C^T D^-1 B x (bs/krylov.py:84-94), both on
+    the device (csrc/spmv.cu, csrc/wells.cu)."""
 
     def __init__(self, a: BlockMatrix, wells):
         super().__init__(a)
         self.wells = wells
-        if not getattr(wells, "is_empty", True):
-            raise NotImplementedError("separate well application is not on the device path yet")
+
+    def apply_device(self, x: torch.Tensor, y: torch.Tensor):
+        self.device().apply(x, y)
+        self.wells.device(self.block_size, self.num_blocks).apply(x, y)
+
+    def apply_array(self, x: np.ndarray) -> np.ndarray:
+        op = self.device()
+        dev = op.bsr.pat.rp.device
+        xd = D.f64(x, dev)
+        y = D.empty_f64(op.n * op.b, dev)
+        self.apply_device(xd, y)
+        return y[: op.n * op.b].cpu().numpy()
 
 
 @dataclass(frozen=True)
@@ -274,6 +284,8 @@ def bicgstab(op, precond, b: BlockVector, x0: BlockVector | None = None,
     native = (type(op) is MatrixOperator and
               (precond is None or isinstance(precond, Ilu0Factorization)) and
               op.num_blocks > 0)
+    # WellAugmentedOperator and other operators/preconditioners: host-driven
+    # loop over device vectors (device operators stay on the device)
     if native:
         return _bicgstab_native(op, precond, b, x0, stop)
     return _bicgstab_generic(op, precond, b, x0, stop)
@@ -314,11 +326,29 @@ def _bicgstab_generic(op, precond, b: BlockVector, x0: BlockVector, stop: Stoppi
     dev = D.require_cuda()
     m = b.data.size
 
-    def A(v):   # device -> device through the operator's array API
-        return D.f64(op.apply_array(v.cpu().numpy()), dev)
+    if hasattr(op, "apply_device"):
+        def A(v):   # device operator (SpMV [+ wells]): no host round trip
+            y = torch.empty_like(v)
+            op.apply_device(v, y)
+            return y
+    else:
+        def A(v):   # duck-typed operator: through its array API
+            return D.f64(op.apply_array(v.cpu().numpy()), dev)
 
-    def M(v):
-        return D.f64(apply_m(v.cpu().numpy()), dev)
+    if isinstance(precond, Ilu0Factorization) and m:
+        f = precond
+
+        def M(v):   # device ILU0 application in plan order
+            if f._identity_perm:
+                return f.apply_device(v)[:m]
+            vp = D.gather_rows(v, f.plan.device("inverse_permutation"), f.num_block_rows,
+                               f.block_size)
+            z = f.apply_device(vp)
+            return D.gather_rows(z, f.plan.device("permutation"), f.num_block_rows,
+                                 f.block_size)[:m]
+    else:
+        def M(v):
+            return D.f64(apply_m(v.cpu().numpy()), dev)
 
     def nrm(v):
         return float(np.sqrt(D.dot(v, v, m))) if m else 0.0

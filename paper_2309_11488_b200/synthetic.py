@@ -6,8 +6,8 @@ the identical matrix and right-hand side: a 7-point stencil on an
 ``nx*ny*nz`` grid in natural order ``cell = ix + nx*(iy + ny*iz)``, every
 off-diagonal block ``-t * U(0.5, 1.5)`` with the per-direction
 transmissibility ``t``, each diagonal block ``diag(row abs sums) + boost*I``,
-and a ``U(-1, 1)`` right-hand side.  (Wells, ``bs/io.py:417-442``, are out of
-scope for this hot path: ``well_count`` must stay 0.)
+and a ``U(-1, 1)`` right-hand side, then the optional wells
+(``bs/io.py:417-442``, same draws).
 
 Two harness extensions build the BASELINE configs the reference generator
 cannot express:
@@ -60,8 +60,6 @@ class GeneratorSpec:
             raise ValueError("well_kind must be standard or multisegment")
         if self.well_count < 0 or (self.well_count and self.well_depth < 1):
             raise ValueError("wells need a non-negative count and depth >= 1")
-        if self.well_count:
-            raise NotImplementedError("wells are outside this build's hot path")
 
 
 @dataclass
@@ -70,6 +68,12 @@ class SystemBundle:
     rhs: BlockVector
     name: str
     grid_dims: tuple | None = None
+    wells: object = None     # WellSet (empty when the spec has no wells)
+
+    def __post_init__(self):
+        if self.wells is None:
+            from .wells import WellSet
+            self.wells = WellSet()
 
 
 def _faces(nx, ny, nz, active=None):
@@ -137,7 +141,36 @@ def generate(spec: GeneratorSpec) -> SystemBundle:
                         zip(faces, (spec.tx, spec.ty, spec.tz))])
     rp, ci, blk = _assemble(n, lo, hi, t, b, spec.diagonal_boost, rng)
     rhs = rng.uniform(-1.0, 1.0, size=n * b)
-    return _bundle(rp, ci, blk, rhs, b, f"synthetic-{nx}x{ny}x{nz}", (nx, ny, nz))
+    out = _bundle(rp, ci, blk, rhs, b, f"synthetic-{nx}x{ny}x{nz}", (nx, ny, nz))
+    out.wells = _generate_wells(spec, rng)
+    return out
+
+
+def _generate_wells(spec: GeneratorSpec, rng):
+    """Vertical wells in random columns, same draws as bs/io.py:417-442."""
+    from .wells import MultisegmentWell, StandardWell, WellSet
+    if spec.well_count == 0:
+        return WellSet()
+    nx, ny, nz, b = spec.nx, spec.ny, spec.nz, spec.block_size
+    depth = min(spec.well_depth, nz)
+    m = b + 1
+    columns = rng.choice(nx * ny, size=min(spec.well_count, nx * ny), replace=False)
+    standard, multisegment = [], []
+    for col in columns:
+        cx, cy = int(col) % nx, int(col) // nx
+        cells = np.array([cx + nx * (cy + ny * z) for z in range(depth)], dtype=np.int64)
+        bb = rng.uniform(-0.1, 0.1, size=(depth, m, b))
+        cc = rng.uniform(-0.1, 0.1, size=(depth, m, b))
+        if spec.well_kind == "standard":
+            d = np.eye(m) + rng.uniform(0.0, 0.1, size=(m, m)) / m
+            standard.append(StandardWell(cells, bb, cc, np.linalg.inv(d)))
+        else:
+            size = depth * m
+            d = np.eye(size) + rng.uniform(0.0, 0.5, size=(size, size)) / size
+            seg = np.arange(depth, dtype=np.int64)
+            multisegment.append(MultisegmentWell(depth, seg, cells, bb, seg.copy(), cells.copy(),
+                                                 cc, d))
+    return WellSet(standard, multisegment)
 
 
 def _smooth_field(shape, sigma, rng):

@@ -1,0 +1,80 @@
+"""Wells against the reference-generated
+fixtures (tests/golden/make_wells.py): the generator's wells draw for draw,
+coupled folding on the host (CPU), separately applied well terms on the
+device and full solves in both well modes (GPU)."""
+
+import numpy as np
+import pytest
+from numpy.testing import assert_allclose, assert_array_equal
+
+import paper_2309_11488_b200 as P
+
+CASES = {
+    "wells_std_8x7x5": dict(nx=8, ny=7, nz=5, well_count=3, well_kind="standard", seed=4),
+    "wells_ms_8x7x5": dict(nx=8, ny=7, nz=5, well_count=2, well_kind="multisegment", seed=5),
+    "wells_std_b2_6x6x4": dict(nx=6, ny=6, nz=4, block_size=2, well_count=2,
+                               well_kind="standard", well_depth=4, seed=6),
+}
+
+
+def close(got, ref, rel):
+    scale = max(np.abs(ref).max(), 1e-300)
+    assert_allclose(got, ref, rtol=0, atol=rel * scale)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_generator_wells_draw_for_draw(golden, name):
+    g, ref = P.generate(P.GeneratorSpec(**CASES[name])), golden(name)
+    assert_array_equal(g.a.values, ref["vals"])
+    assert_array_equal(g.rhs.data, ref["rhs"])
+    for k, w in enumerate(g.wells.standard):
+        assert_array_equal(w.perforated_cells, ref[f"std{k}_cells"])
+        assert_array_equal(w.b_blocks, ref[f"std{k}_b"])
+        assert_array_equal(w.c_blocks, ref[f"std{k}_c"])
+        assert_array_equal(w.d_inverse, ref[f"std{k}_dinv"])
+    for k, w in enumerate(g.wells.multisegment):
+        assert_array_equal(w.b_cells, ref[f"ms{k}_cells"])
+        assert_array_equal(w.b_blocks, ref[f"ms{k}_b"])
+        assert_array_equal(w.d_dense, ref[f"ms{k}_d"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fold_into_matrix(golden, name):
+    """Coupled mode folds C^T D^-1 B into A on the host (bs/wells.py:218-283)."""
+    g, ref = P.generate(P.GeneratorSpec(**CASES[name])), golden(name)
+    f = P.fold_into_matrix(g.a, g.wells)
+    assert_array_equal(f.pattern.row_pointers, ref["fold_rp"])
+    assert_array_equal(f.pattern.column_indices, ref["fold_ci"])
+    close(f.values, ref["fold_vals"], 1e-14)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_well_augmented_operator_on_device(golden, name):
+    g, ref = P.generate(P.GeneratorSpec(**CASES[name])), golden(name)
+    op = P.WellAugmentedOperator(g.a, g.wells)
+    close(op.apply_array(ref["x"]), ref["op_x"], 1e-13)
+    # the public per-well entry points agree with the set
+    y = P.spmv(g.a, P.BlockVector(ref["x"], g.a.block_size))
+    for w in g.wells.standard:
+        P.apply_standard(w, P.BlockVector(ref["x"], g.a.block_size), y)
+    for w in g.wells.multisegment:
+        P.apply_multisegment(w, P.BlockVector(ref["x"], g.a.block_size), y)
+    close(y.data, ref["op_x"], 1e-13)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("mode", ["separate", "coupled"])
+@pytest.mark.parametrize("backend", ["level", "color"])
+def test_solve_with_wells(golden, name, mode, backend):
+    g, ref = P.generate(P.GeneratorSpec(**CASES[name])), golden(name)
+    cfg = P.SolverConfig(backend=P.Backend.from_name(backend), well_mode=P.WellMode(mode),
+                         stop=P.StoppingCriteria(1e-8, 200))
+    x, rep = P.solve_with_fallback(cfg, g.a, g.rhs, g.wells)
+    conv, its, n0, fin, fb = ref[f"{mode}_{backend}_report"]
+    assert rep.converged and not rep.fallback_used
+    assert abs(rep.iterations - its) <= 1.0, (rep.iterations, its)
+    assert_allclose(rep.initial_norm, n0, rtol=1e-12)
+    xr = ref[f"{mode}_{backend}_x"]
+    assert np.linalg.norm(x.data - xr) <= 1e-7 * np.linalg.norm(xr)
