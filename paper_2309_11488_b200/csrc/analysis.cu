@@ -222,7 +222,7 @@ __device__ int color_walk(int i, const int32_t* __restrict__ rp, const int32_t* 
     if (cj < 0) return -1;
     if (cj < 64) used |= 1ull << cj; else big = true;
   }
-  for (int q = ut_ptr[i]; q < ut_ptr[i + 1]; ++q) {
+  for (int q = ut_ptr ? ut_ptr[i] : 0; ut_ptr && q < ut_ptr[i + 1]; ++q) {
     const int cj = ld_relaxed_i(color + ut_idx[q]);
     if (cj < 0) return -1;
     if (cj < 64) used |= 1ull << cj; else big = true;
@@ -235,7 +235,7 @@ __device__ int color_walk(int i, const int32_t* __restrict__ rp, const int32_t* 
         const int j = ci[q];
         if (j < i && ld_relaxed_i(color + j) == c) hit = true;
       }
-      for (int q = ut_ptr[i]; q < ut_ptr[i + 1] && !hit; ++q)
+      for (int q = ut_ptr ? ut_ptr[i] : 0; ut_ptr && q < ut_ptr[i + 1] && !hit; ++q)
         if (ld_relaxed_i(color + ut_idx[q]) == c) hit = true;
       if (hit) ++c;
     }
@@ -243,14 +243,43 @@ __device__ int color_walk(int i, const int32_t* __restrict__ rp, const int32_t* 
   return c;
 }
 
-// (same R-slice units as k_level_sync_free)
+// *asym = 1 unless every row's transposed-upper list (rows j < i storing
+// (j, i)) is exactly its own strict-lower column set
+__global__ void k_symmetric(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const int32_t* __restrict__ ut_ptr,
+                            const int32_t* __restrict__ ut_idx, int* asym) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int k0 = rp[i], k1 = rp[i + 1];
+    int nlow = 0;
+    while (k0 + nlow < k1 && ci[k0 + nlow] < i) ++nlow;
+    bool bad = nlow != ut_ptr[i + 1] - ut_ptr[i];
+    for (int q = ut_ptr[i]; !bad && q < ut_ptr[i + 1]; ++q) {
+      const int j = ut_idx[q];
+      int lo = k0, hi = k0 + nlow - 1;
+      bool found = false;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1, c = ci[mid];
+        if (c == j) { found = true; break; }
+        if (c < j) lo = mid + 1; else hi = mid - 1;
+      }
+      bad = !found;
+    }
+    if (bad) atomicExch(asym, 1);
+  }
+}
+
+// (same R-slice units as k_level_sync_free).  SYM: the pattern is
+// structurally symmetric (checked by k_symmetric), so the symmetrised lower
+// neighbours are the row's own lower entries and the transposed lists are
+// never read.
+template <bool SYM, int NB = (SYM ? kLNb : kCNb)>
 __global__ void __launch_bounds__(256, 5) k_color_sync_free(int n, const int32_t* __restrict__ rp,
                                   const int32_t* __restrict__ ci,
                                   const int32_t* __restrict__ ut_ptr,
                                   const int32_t* __restrict__ ut_idx, int32_t* color,
                                   unsigned int* ticket, unsigned long long* trace = nullptr) {
   const int lane = threadIdx.x & 31;
-  __shared__ int snb[8][kCR][kCNb][32];   // neighbour lists (see k_level_sync_free)
+  __shared__ int snb[8][kCR][NB][32];   // neighbour lists (see k_level_sync_free)
   for (;;) {
     unsigned int u = 0;
     if (lane == 0) u = atomicAdd(ticket, 1u);
@@ -258,11 +287,11 @@ __global__ void __launch_bounds__(256, 5) k_color_sync_free(int n, const int32_t
     const long long base = (long long)u * kCR * kSlice;
     if (base >= n) break;
     unsigned pend[kCR];
-    unsigned used[kCR];   // colours 0..31 seen: a short row's mex is <= kCNb
+    unsigned used[kCR];   // colours 0..31 seen: a short row's mex is <= NB
     bool longrow[kCR], live[kCR];
     // row setup in two rounds for all R rows at once (row and transposed
     // extents, then the first entries of both lists); rows whose neighbour
-    // set may exceed kCNb walk memory instead (color_walk)
+    // set may exceed NB walk memory instead (color_walk)
     int k0[kCR], k1[kCR], u0[kCR], u1[kCR];
 #pragma unroll
     for (int q = 0; q < kCR; ++q) {
@@ -271,41 +300,41 @@ __global__ void __launch_bounds__(256, 5) k_color_sync_free(int n, const int32_t
       pend[q] = 0; used[q] = 0u; longrow[q] = false;
       k0[q] = live[q] ? rp[i] : 0;
       k1[q] = live[q] ? rp[i + 1] : 0;
-      u0[q] = live[q] ? ut_ptr[i] : 0;
-      u1[q] = live[q] ? ut_ptr[i + 1] : 0;
+      u0[q] = (live[q] && !SYM) ? ut_ptr[i] : 0;
+      u1[q] = (live[q] && !SYM) ? ut_ptr[i + 1] : 0;
     }
 #pragma unroll
     for (int q = 0; q < kCR; ++q) {
       const long long i = base + q * kSlice + lane;
-      int c[kCNb + 1], t[kCNb + 1];
+      int c[NB + 1], t[NB + 1];
 #pragma unroll
-      for (int w = 0; w <= kCNb; ++w) {
+      for (int w = 0; w <= NB; ++w) {
         c[w] = k0[q] + w < k1[q] ? ci[k0[q] + w] : n;
-        t[w] = u0[q] + w < u1[q] ? ut_idx[u0[q] + w] : -1;
+        t[w] = (!SYM && u0[q] + w < u1[q]) ? ut_idx[u0[q] + w] : -1;
       }
       int cnt = 0;
-      int nbq[kCNb];
+      int nbq[NB];
 #pragma unroll
-      for (int w = 0; w <= kCNb; ++w)
+      for (int w = 0; w <= NB; ++w)
         if (c[w] < i) {
-          if (cnt < kCNb) nbq[cnt] = c[w];
+          if (cnt < NB) nbq[cnt] = c[w];
           ++cnt;
         }
       const int nrow = cnt;
-      bool overflow = nrow > kCNb || u1[q] - u0[q] > kCNb;
+      bool overflow = nrow > NB || u1[q] - u0[q] > NB;
 #pragma unroll
-      for (int w = 0; w < kCNb; ++w) {
+      for (int w = 0; w < NB; ++w) {
         if (t[w] < 0) continue;
         bool dup = false;   // (j,i) and (i,j) both stored: one neighbour
 #pragma unroll
-        for (int v = 0; v < kCNb; ++v) dup |= v < nrow && nbq[v] == t[w];
+        for (int v = 0; v < NB; ++v) dup |= v < nrow && nbq[v] == t[w];
         if (dup) continue;
-        if (cnt < kCNb) nbq[cnt] = t[w];
+        if (cnt < NB) nbq[cnt] = t[w];
         ++cnt;
       }
-      overflow |= cnt > kCNb;
+      overflow |= cnt > NB;
 #pragma unroll
-      for (int w = 0; w < kCNb; ++w) snb[threadIdx.x >> 5][q][w][lane] = nbq[w];
+      for (int w = 0; w < NB; ++w) snb[threadIdx.x >> 5][q][w][lane] = nbq[w];
       longrow[q] = overflow;
       pend[q] = (live[q] && !overflow) ? ((1u << cnt) - 1u) : 0u;
     }
@@ -317,20 +346,20 @@ __global__ void __launch_bounds__(256, 5) k_color_sync_free(int n, const int32_t
         const int i = (int)(base + q * kSlice + lane);
         int c = -1;
         if (!longrow[q]) {
-          int got[kCNb];
+          int got[NB];
 #pragma unroll
-          for (int w = 0; w < kCNb; ++w)
+          for (int w = 0; w < NB; ++w)
             got[w] = (pend[q] & (1u << w)) ? ld_relaxed_i(color + snb[threadIdx.x >> 5][q][w][lane])
                                            : -1;
 #pragma unroll
-          for (int w = 0; w < kCNb; ++w)
+          for (int w = 0; w < NB; ++w)
             if ((pend[q] & (1u << w)) && got[w] >= 0) {
               if (got[w] < 32) used[q] |= 1u << got[w];   // larger ones cannot be the mex
               pend[q] &= ~(1u << w);
             }
           if (!pend[q]) c = __ffs(~used[q]) - 1;
         } else {
-          c = color_walk(i, rp, ci, ut_ptr, ut_idx, color);
+          c = color_walk(i, rp, ci, SYM ? nullptr : ut_ptr, ut_idx, color);
         }
         if (c >= 0) {
           st_relaxed_i(color + i, c);
@@ -571,7 +600,19 @@ int b2s_graph_color(int n, const int32_t* rp, const int32_t* ci, int32_t* row_gr
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, ptr, n + 1, st);
   k_upper_fill<<<grid_for(n), 256, 0, st>>>(n, rp, ci, ptr, fill, idx);
   k_fill_int<<<grid_for(n), 256, 0, st>>>(n, row_group, -1);
-  k_color_sync_free<<<sync_free_grid(n, (const void*)k_color_sync_free), 256, 0, st>>>(n, rp, ci, ptr, idx, row_group, ticket);
+  // structurally symmetric patterns (every reservoir stencil): colour over
+  // the lower entries alone
+  B2S_CHECK(cudaMemsetAsync(cnt + n, 0, sizeof(int32_t), st));
+  k_symmetric<<<grid_for(n), 256, 0, st>>>(n, rp, ci, ptr, idx, cnt + n);
+  int asym = 1;
+  B2S_CHECK(cudaMemcpyAsync(&asym, cnt + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  if (asym)
+    k_color_sync_free<false><<<sync_free_grid(n, (const void*)k_color_sync_free<false>), 256, 0,
+                               st>>>(n, rp, ci, ptr, idx, row_group, ticket);
+  else
+    k_color_sync_free<true><<<sync_free_grid(n, (const void*)k_color_sync_free<true>), 256, 0,
+                              st>>>(n, rp, ci, ptr, idx, row_group, ticket);
   B2S_LAUNCH_CHECK();
   B2S_CHECK(cudaFreeAsync(tmp, st));
   B2S_CHECK(cudaFreeAsync(cnt, st));
@@ -610,8 +651,8 @@ int b2s_analysis_trace(int kind, int n, const int32_t* rp, const int32_t* ci, in
     B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
     cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, ptr, n + 1, st);
     k_upper_fill<<<grid_for(n), 256, 0, st>>>(n, rp, ci, ptr, fill, idx);
-    k_color_sync_free<<<sync_free_grid(n, (const void*)k_color_sync_free), 256, 0, st>>>(n, rp, ci, ptr, idx, row_group, ticket,
-                                                         trace);
+    k_color_sync_free<false><<<sync_free_grid(n, (const void*)k_color_sync_free<false>), 256, 0,
+                               st>>>(n, rp, ci, ptr, idx, row_group, ticket, trace);
     cudaFreeAsync(tmp, st); cudaFreeAsync(cnt, st); cudaFreeAsync(ptr, st);
     cudaFreeAsync(fill, st); cudaFreeAsync(idx, st);
   }
