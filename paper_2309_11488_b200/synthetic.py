@@ -75,6 +75,12 @@ class SystemBundle:
             from .wells import WellSet
             self.wells = WellSet()
 
+    @property
+    def meta(self):
+        """bs/io.py:27-31 BundleMeta view (name, block size, grid)."""
+        from .mmio import BundleMeta
+        return BundleMeta(self.name, self.a.block_size, self.grid_dims)
+
 
 def _faces(nx, ny, nz, active=None):
     """Face pairs (lo, hi) in the reference's order: all +x faces, then +y,
