@@ -387,6 +387,14 @@ class Sell:
                  if (fill and goff is not None and ns) else False)
         return cls(sp, cols, vals, ns, width, stale)
 
+    def fill_from(self, smap: SliceMap, m: DevBSR, sel: int, src: torch.Tensor | None = None):
+        """Fill a layout sized by ``build(..., fill=False)`` (values of ``m``,
+        through ``src`` when given) -- the value pass of a two-step build."""
+        check(lib().b2s_sell_fill_src(smap.nslices, m.b, ptr(smap.row0), ptr(smap.nrows),
+                                      ptr(m.pat.rp), ptr(m.pat.ci), ptr(m.vals), sel,
+                                      ptr(self.sp), None, 0, ptr(self.cols), ptr(self.vals),
+                                      ptr(src), stream()), "sell_fill")
+
 
 def spmv(smap: SliceMap, a: Sell, b: int, x: torch.Tensor, y: torch.Tensor, mode: int = 0,
          w: torch.Tensor | None = None, parts0=None, parts1=None):

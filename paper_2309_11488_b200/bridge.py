@@ -23,10 +23,11 @@ import numpy as np
 import torch
 
 from . import _device as D
+from . import trace
 from .analysis import (ParallelPlan, Strategy, _device_plan, sequential_plan)
 from .blockcore import BlockMatrix, BlockVector
 from .errors import SingularPivot, SolveFailed
-from .ilu0 import Ilu0Factorization, factor_device
+from .ilu0 import Ilu0Factorization, factor_device, prepare_two_colour
 from .krylov import (DEFAULT_MAX_ITERATIONS, DeviceKrylov, SolveReport, StoppingCriteria,
                      WellAugmentedOperator, _REASONS, bicgstab)
 from .wells import WellMode, WellSet, fold_into_matrix
@@ -98,10 +99,15 @@ class DeviceSolver:
 
     def setup(self, backend: Backend | None = None):
         backend = backend or self.cfg.backend
-        self.plan = plan_device(backend, self.pre_bsr.pat)
-        self.pre_bsr.wait_values()   # values may still be in flight (overlapped upload)
-        self.bsr.wait_values()
-        self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr)
+        with trace.phase("analysis"):
+            self.plan = plan_device(backend, self.pre_bsr.pat)
+            # the pattern-only part of the factorisation, also before the values
+            prep = prepare_two_colour(self.pre_matrix, self.plan, self.pre_bsr.pat)
+        with trace.phase("wait_values"):
+            self.pre_bsr.wait_values()   # values may still be in flight (overlapped upload)
+            self.bsr.wait_values()
+        with trace.phase("factor"):
+            self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr, prep)
         if self.pre_bsr is self.bsr and self.fact.a_sell is not None:
             # 2-colour factorisation: the operator's SELL layout already exists
             self.krylov = DeviceKrylov.build(self.a, self.fact)
@@ -164,14 +170,17 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         rep = SolveReport(True, 0.0, 0.0, 0.0, 0.0, 0)
         return BlockVector(np.zeros(0) if x0 is None else x0.data.copy(), bs), rep
     dev = D.require_cuda()
-    # the 72 B/block values (the bulk of the upload) travel while the device
-    # analyses the pattern; the solve waits for them only at factorisation
-    bsr = D.DevBSR.upload(a_sys, overlap=cfg.jacobi_partitions == 0)
-    # the vectors queue behind the values on the copy stream: the analysis
-    # (pattern only) must not wait for them
-    rhs = bsr.upload_after(b.data)
-    x0d = (torch.zeros(n * bs, dtype=torch.float64, device=dev) if x0 is None
-           else bsr.upload_after(x0.data))
+    trace.start()
+    with trace.phase("upload"):
+        # the 72 B/block values (the bulk of the upload) travel while the
+        # device analyses the pattern; the solve waits for them only at
+        # factorisation
+        bsr = D.DevBSR.upload(a_sys, overlap=cfg.jacobi_partitions == 0)
+        # the vectors queue behind the values on the copy stream: the
+        # analysis (pattern only) must not wait for them
+        rhs = bsr.upload_after(b.data)
+        x0d = (torch.zeros(n * bs, dtype=torch.float64, device=dev) if x0 is None
+               else bsr.upload_after(x0.data))
 
     pre_bsr, pre_mat = bsr, a_sys
     primary = None
@@ -188,7 +197,8 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         setup = time.perf_counter() - t0
         t1 = time.perf_counter()
         xd = x0d.clone()
-        res = solver.solve(rhs, xd, cfg.stop)
+        with trace.phase("krylov"):
+            res = solver.solve(rhs, xd, cfg.stop)
         _sync()
         primary = _report(res, time.perf_counter() - t1, solver.plan.group_count)
         primary.setup_elapsed = setup
@@ -198,7 +208,10 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         primary.setup_elapsed = time.perf_counter() - t0
 
     if primary.converged:
-        return BlockVector(D.to_host(x, n * bs), bs), primary
+        with trace.phase("download"):
+            out = BlockVector(D.to_host(x, n * bs), bs)
+        primary.phases = trace.finish()
+        return out, primary
 
     fb_t0 = time.perf_counter()
     fb_stop = StoppingCriteria(cfg.stop.relative_reduction,

@@ -205,24 +205,45 @@ class Ilu0Factorization:
             self.tiles = None
 
 
-def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR"):
+def prepare_two_colour(a: BlockMatrix, plan: ParallelPlan, pat: "D.DevPattern"):
+    """Pattern-only half of the 2-colour factorisation (permuted pattern and
+    source map, slice map, layout offsets, buffers): runs while the values
+    are still on their way to the device.  None when the plan is not a
+    2-group plan this path handles."""
+    n, b = a.num_block_rows, a.block_size
+    if not (plan.group_count == 2 and not plan.is_identity and b <= 4 and
+            os.environ.get("B2S_FACTOR_2C", "1") != "0"):
+        return None
+    D.find_diagonal(pat)                           # MissingDiagonal(first row)
+    bb = b * b
+    dev = pat.rp.device
+    ppat, src = D.permute_pattern(pat, plan.device("permutation"),
+                                  plan.device("inverse_permutation"))
+    smap = plan.slice_map()
+    if smap.gslice_host is None or len(smap.gslice_host) != 3:
+        return None
+    shell = D.DevBSR(ppat, b, D.empty_f64(1, dev))     # pattern only
+    return {"pattern": ppat, "src": src, "smap": smap,
+            "a_sell": D.Sell.build(smap, shell, 0, fill=False),
+            "lower": D.Sell.build(smap, shell, 1, fill=False),
+            "inv": D.empty_f64(n * bb, dev),
+            "udiag": D.empty_f64((n - int(smap.goff1)) * bb, dev),
+            "dtiles": D.empty_f64(smap.nslices * bb * 32, dev),
+            "s1": int(smap.gslice_host[1]), "goff1": int(smap.goff1)}
+
+
+def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", prep=None):
     """2-colour plans: operator layout + factors straight from the input
     values (csrc/factor2c.cu); None if the pattern is not a 2-colour
     structure (then the general path runs)."""
     n, b = a.num_block_rows, a.block_size
-    bb = b * b
-    dev = bsr.pat.rp.device
-    pat, src = D.permute_pattern(bsr.pat, plan.device("permutation"),
-                                 plan.device("inverse_permutation"))
-    smap = plan.slice_map()
-    if smap.gslice_host is None or len(smap.gslice_host) != 3:
+    prep = prep or prepare_two_colour(a, plan, bsr.pat)
+    if prep is None:
         return None
-    s1, goff1 = int(smap.gslice_host[1]), int(smap.goff1)
-    a_sell = D.Sell.build(smap, D.DevBSR(pat, b, bsr.vals), 0, src=src)
-    lower = D.Sell.build(smap, D.DevBSR(pat, b, bsr.vals), 1, fill=False)
-    inv = D.empty_f64(n * bb, dev)
-    udiag = D.empty_f64((n - goff1) * bb, dev)
-    dtiles = D.empty_f64(smap.nslices * bb * 32, dev)
+    smap, a_sell, lower = prep["smap"], prep["a_sell"], prep["lower"]
+    inv, udiag, dtiles = prep["inv"], prep["udiag"], prep["dtiles"]
+    s1, goff1 = prep["s1"], prep["goff1"]
+    a_sell.fill_from(smap, D.DevBSR(prep["pattern"], b, bsr.vals), 0, prep["src"])
     bad = C.c_int32(-1)
     rc = D.lib().b2s_factor_2colour(n, b, goff1, s1, smap.nslices, D.ptr(smap.row0),
                                     D.ptr(smap.nrows), D.ptr(a_sell.sp), D.ptr(a_sell.cols),
@@ -234,13 +255,15 @@ def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR"):
     if rc == SINGULAR_PIVOT:
         raise SingularPivot(int(plan.device("inverse_permutation")[int(bad.value)].item()))
     check(rc, "factor_2colour")
-    tc = {"pattern": pat, "a_sell": a_sell, "udiag": udiag, "goff1": goff1, "s1": s1}
+    tc = {"pattern": prep["pattern"], "a_sell": a_sell, "udiag": udiag, "goff1": goff1, "s1": s1}
     return Ilu0Factorization(plan, b, n, None, inv, smap, lower, None, dtiles, False, a, None,
                              two_colour=tc)
 
 
-def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) -> Ilu0Factorization:
-    """``decompose`` on an (optionally pre-uploaded) matrix."""
+def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
+                  prep=None) -> Ilu0Factorization:
+    """``decompose`` on an (optionally pre-uploaded) matrix; ``prep`` is
+    ``prepare_two_colour``'s pattern-only half when the caller ran it early."""
     a = a.as_block_row_major()
     n = a.num_block_rows
     if plan.num_rows != n:
@@ -248,13 +271,11 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None) ->
     b = a.block_size
     bsr = bsr or D.DevBSR.upload(a)
     dev = bsr.pat.rp.device
+    f = _factor_two_colour(a, plan, bsr, prep)
+    if f is not None:
+        return f
     D.find_diagonal(bsr.pat)                       # MissingDiagonal(first row)
     identity = plan.is_identity
-    if (plan.group_count == 2 and not identity and b <= 4 and
-            os.environ.get("B2S_FACTOR_2C", "1") != "0"):
-        f = _factor_two_colour(a, plan, bsr)
-        if f is not None:
-            return f
     a_perm = bsr if identity else permute_device(bsr, plan)
     lu = D.DevBSR(a_perm.pat, b, a_perm.vals.clone())
     diag = D.find_diagonal(lu.pat)

@@ -167,6 +167,8 @@ class SolveReport:
     setup_elapsed: float = 0.0
     # device-side accounting (not in the reference): graph replays and kernels
     gpu_launches: int = 0
+    # B2S_TRACE=1: {phase: (host_ms, gpu_ms)} (paper_2309_11488_b200/trace.py)
+    phases: dict | None = None
 
 
 # ---------------------------------------------------------------------------
