@@ -151,6 +151,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def count_step_kernels(fn):
+    """Kernels one step launches, counted by the CUDA profiler (CUPTI)."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"
+                 and not e.name.startswith("Memcpy") and not e.name.startswith("Memset")]
+    except Exception:
+        return None
+    ours = sum(1 for n in names if "b2s::" in n)
+    cub = sum(1 for n in names if "cub::" in n)
+    return {"per_step": ours + cub, "b2s": ours, "cub": cub, "other": len(names) - ours - cub}
+
+
 # ---------------------------------------------------------------------------
 
 def main():
@@ -325,6 +342,13 @@ def run_single(args):
 
     clk = main_run.pop("clocks", None)
     launches = main_run.pop("gpu_launches")
+    # measured kernel count of one step (CUPTI, outside the timed region):
+    # every device kernel of setup + solve, ours (b2s::) and CUB's
+    kinfo = count_step_kernels(lambda: DeviceSolver(a, bsr, P.SolverConfig(
+        backend=P.Backend.from_name(args.backend), stop=stop)).setup().solve(
+            rhs_d, torch.zeros_like(x_d), stop))
+    if kinfo:
+        launches = kinfo["per_step"] * args.steps
     line = {
         "metric": METRIC, "value": n / (main_run["solve_ms"] / 1e3) / 1e6, "unit": UNIT,
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -346,6 +370,7 @@ def run_single(args):
                     "ilu_apply_bytes": apply_bytes},
         "other_plan": other, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
         "gpu_launches": launches,
+        "gpu_launches_per_step": kinfo,
     }
     print(json.dumps(line), flush=True)
 
