@@ -95,7 +95,8 @@ __global__ void k_factor_pairs(int n, const int32_t* __restrict__ rp,
 __global__ void k_factor_simple(int n, const int32_t* __restrict__ rp,
                                 const int32_t* __restrict__ diag,
                                 const int32_t* __restrict__ pptr,
-                                const int2* __restrict__ pairs, int8_t* simple) {
+                                const int2* __restrict__ pairs, int8_t* simple,
+                                int* nonsimple) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int k0 = rp[i], d = diag[i];
     bool ok = d - k0 <= kFast;
@@ -104,6 +105,7 @@ __global__ void k_factor_simple(int n, const int32_t* __restrict__ rp,
       if (b1 - b0 > 1 || (b1 > b0 && pairs[b0].x != d)) ok = false;
     }
     simple[i] = ok ? 1 : 0;
+    if (!ok) atomicAdd(nonsimple, 1);
   }
 }
 
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(256) k_factor_numeric(
     SliceMap map, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
     const int32_t* __restrict__ diag, const int32_t* __restrict__ pptr,
     const int2* __restrict__ pairs, const int8_t* __restrict__ simple_row, double* w,
-    double* invd, int* flag, int* bad, Tickets2* tk, int sleep_ns) {
+    double* invd, int* flag, int* bad, Tickets2* tk, int sleep_ns, int all_simple) {
   constexpr int BB = B * B;
   const int lane = threadIdx.x & 31;
   for (;;) {
@@ -200,7 +202,9 @@ __global__ void __launch_bounds__(256) k_factor_numeric(
           if (!invert_block<B>(dblk, inv)) atomicMin(bad, i);
 #pragma unroll
           for (int e = 0; e < BB; ++e) st_relaxed_f64(invd + (long long)i * BB + e, canon(inv[e]));
-          st_flag_release(flag + i, 1);  // for general-path consumers
+          // for general-path consumers (none when every row is simple: the
+          // release fence is then skipped)
+          if (!all_simple) st_flag_release(flag + i, 1);
           done = true;
         }
       }
@@ -264,7 +268,7 @@ template <int B>
 int launch_numeric(SliceMap map, const int32_t* rp, const int32_t* ci, const int32_t* diag,
                    const int32_t* pptr, const int2* pairs, const int8_t* simple, double* w,
                    double* invd, int* flag,
-                   int* bad, Tickets2* tk, cudaStream_t st) {
+                   int* bad, Tickets2* tk, int all_simple, cudaStream_t st) {
   int per_sm = 0, dev = 0, sms = kSms;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_factor_numeric<B>, 256, 0);
   cudaGetDevice(&dev);
@@ -277,7 +281,7 @@ int launch_numeric(SliceMap map, const int32_t* rp, const int32_t* ci, const int
   if (const char* e = getenv("B2S_FACTOR_SLEEP")) sleep_ns = atoi(e);
   if (const char* e = getenv("B2S_FACTOR_WARPS")) threads = 32 * atoi(e);
   k_factor_numeric<B><<<g, threads, 0, st>>>(map, rp, ci, diag, pptr, pairs, simple, w, invd,
-                                             flag, bad, tk, sleep_ns);
+                                             flag, bad, tk, sleep_ns, all_simple);
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
@@ -339,17 +343,22 @@ int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_
   k_factor_pairs<<<grid_rows(n), 256, 0, st>>>(n, rp, ci, diag, nullptr, pptr, pairs);
   int8_t* simple = nullptr;
   B2S_CHECK(cudaMallocAsync(&simple, n, st));
-  k_factor_simple<<<grid_rows(n), 256, 0, st>>>(n, rp, diag, pptr, pairs, simple);
+  B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));   // (cnt is free again)
+  k_factor_simple<<<grid_rows(n), 256, 0, st>>>(n, rp, diag, pptr, pairs, simple, cnt);
+  int32_t nonsimple = 1;
+  B2S_CHECK(cudaMemcpyAsync(&nonsimple, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  const int all_simple = nonsimple == 0 ? 1 : 0;
   // the inverse diagonals double as the fast path's "ready" marks
   if (int rcf = fill_sentinel((long long)n * b * b, inv_diag, st)) return rcf;
   B2S_LAUNCH_CHECK();
   SliceMap map{nslices, row0, nrows};
   int rc;
   switch (b) {
-    case 1: rc = launch_numeric<1>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, st); break;
-    case 2: rc = launch_numeric<2>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, st); break;
-    case 3: rc = launch_numeric<3>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, st); break;
-    default: rc = launch_numeric<4>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, st); break;
+    case 1: rc = launch_numeric<1>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, all_simple, st); break;
+    case 2: rc = launch_numeric<2>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, all_simple, st); break;
+    case 3: rc = launch_numeric<3>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, all_simple, st); break;
+    default: rc = launch_numeric<4>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, all_simple, st); break;
   }
   if (rc != B2S_OK) return rc;
   int h = big;
