@@ -177,21 +177,22 @@ int b2s_ilu0_apply_phased(int n, int b, int kc, int ngroups, const int32_t* gsli
                           const double* dinv_tiles, const double* r, double* y, double* z,
                           cudaStream_t stream);
 
-/* Tiled level-scheduled sweeps (csrc/tiles.cu): px*py column patches of an
- * nx x ny natural-order grid (px > 0) or T contiguous input-row ranges; one
- * co-resident CTA per tile, tile values in shared memory.  kc = max entries
- * per row of L/U.  B2S_UNSUPPORTED when a tile does not fit on an SM. */
-long long b2s_tiles_smem_bytes(int b, int rmax);
+/* Tiled level-scheduled sweeps (csrc/tiles.cu): rows split into px*py column
+ * patches of an nx x ny natural-order grid (px > 0) or T contiguous input-row
+ * ranges; one co-resident CTA per tile walks the tile's rows one plan group
+ * ("step") at a time -- a producer warp streams each step's packed record
+ * into a shared-memory ring with TMA bulk copies, consumer warps resolve
+ * in-tile dependencies from shared memory and poll only cross-tile ones.
+ * rp/ci/diag/lu: combined L\U in plan order; inv: inverse diagonal blocks.
+ * B2S_UNSUPPORTED when T exceeds the SMs or the ring does not fit. */
 int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const int32_t* iperm,
                      const int32_t* rp, const int32_t* ci, const int32_t* diag, const double* lu,
-                     const double* inv, const int32_t* goff, int ngroups, int kc, int warps,
-                     void** handle_out, cudaStream_t stream);
+                     const double* inv, const int32_t* goff, int ngroups, void** handle_out,
+                     cudaStream_t stream);
 int b2s_tiles_destroy(void* handle);
-/* kind 0: polling warps per tile; 1 (default when it fits): the wave kernel,
- * one warp per tile consuming its slices in order with a cp.async ring */
-int b2s_tiles_set_kernel(void* handle, int kind);
-/* debug: per-slice start times of the wave kernel into buf[2][T][1024] */
-int b2s_tiles_trace(void* handle, unsigned long long* buf);
+/* debug: per-step event times of the step kernels into buf[2][T][1024][4];
+ * dbg != 0 only for timing experiments (results are then wrong) */
+int b2s_tiles_trace(void* handle, unsigned long long* buf, int dbg);
 int b2s_tiles_apply(int b, const void* handle, const double* r, double* y, double* z,
                     int reset_y, cudaStream_t stream);
 

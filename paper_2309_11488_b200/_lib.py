@@ -76,11 +76,9 @@ SIGNATURES = {
     "b2s_fuse_check": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _PI, _P]),
     "b2s_ilu0_apply_phased": (_I, [_I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                    _P, _P, _P, _P]),
-    "b2s_tiles_smem_bytes": (_LL, [_I, _I]),
-    "b2s_tiles_set_kernel": (_I, [_P, _I]),
-    "b2s_tiles_trace": (_I, [_P, _P]),
-    "b2s_tiles_create": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I,
-                              _I, C.POINTER(C.c_void_p), _P]),
+    "b2s_tiles_trace": (_I, [_P, _P, _I]),
+    "b2s_tiles_create": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I,
+                              C.POINTER(C.c_void_p), _P]),
     "b2s_tiles_destroy": (_I, [_P]),
     "b2s_tiles_apply": (_I, [_I, _P, _P, _P, _P, _I, _P]),
     "b2s_dot": (_I, [_LL, _P, _P, _I, _P, _P, _P]),

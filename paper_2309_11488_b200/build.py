@@ -36,28 +36,63 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+OBJ = ROOT / "build" / "obj"
+
+
+def _newer(target: Path, deps) -> bool:
+    if not target.exists():
         return True
-    t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
+    t = target.stat().st_mtime
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def _headers():
+    return list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
+
+
+def _stale() -> bool:
+    return _newer(LIB, [CSRC / s for s in SOURCES] + _headers())
+
+
 def build_library(force: bool = False, verbose: bool = False) -> Path:
+    """Compile each source to an object in parallel (only the stale ones),
+    then link the shared library."""
     if not force and not _stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}",
-           *[str(CSRC / s) for s in SOURCES], "-o", str(LIB) + ".tmp"]
-    proc = subprocess.run(cmd, capture_output=True, text=True)
+    OBJ.mkdir(parents=True, exist_ok=True)
+    hdr = _headers()
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    procs = []
+    for src in SOURCES:
+        obj = OBJ / (Path(src).stem + ".o")
+        if force or _newer(obj, [CSRC / src] + hdr):
+            cmd = [nvcc(), *compile_flags, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(CSRC / src),
+                   "-o", str(obj) + ".tmp"]
+            procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                                     stderr=subprocess.PIPE, text=True)))
+    logs, failed = [], []
+    for src, obj, p in procs:
+        out, err = p.communicate()
+        logs.append(f"== {src}\n{out}{err}")
+        if p.returncode != 0:
+            failed.append((src, err))
+        else:
+            os.replace(str(obj) + ".tmp", obj)
     log = CSRC / "ptxas.log"
-    log.write_text(proc.stdout + proc.stderr)
+    log.write_text("\n".join(logs))
+    if failed:
+        for src, err in failed:
+            sys.stderr.write(f"== {src}\n{err[-6000:]}")
+        raise RuntimeError(f"nvcc failed on {[f[0] for f in failed]}; see {log}")
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+           *[str(OBJ / (Path(s).stem + ".o")) for s in SOURCES], "-o", str(LIB) + ".tmp"]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stderr[-6000:])
-        raise RuntimeError(f"nvcc failed ({proc.returncode}); see {log}")
+        raise RuntimeError(f"link failed ({proc.returncode})")
     os.replace(str(LIB) + ".tmp", LIB)
     if verbose:
-        sys.stderr.write(proc.stderr)
+        sys.stderr.write("\n".join(logs))
     return LIB
 
 

@@ -338,11 +338,13 @@ def _patches(nx: int, ny: int, tiles: int):
 
 
 def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
-    """Deep level schedules are latency-bound in the sync-free sweeps; give
-    them the tiled kernels (csrc/tiles.cu) when a tile fits in an SM.
-    B2S_TILES=0 disables, B2S_TILES_T sets the tile count."""
-    # experimental (csrc/tiles.cu): correct but not yet faster than the
-    # sync-free sweeps on B200, so off unless B2S_TILES=1
+    """Opt-in (B2S_TILES=1): the tiled step kernels (csrc/tiles.cu), which
+    resolve in-tile dependencies of a level schedule on-chip.  Results are
+    bit-identical to the sync-free sweeps, but on B200 they are not faster yet
+    (C4: 0.87 ms vs 0.68 ms per application; profiles/r01/tile_steps_trace.json,
+    DESIGN.md section 3), so the sync-free sweeps stay the default.
+    B2S_TILES_T sets the tile count (default: the SMs, or the column patches
+    of a natural-order grid that fit on them)."""
     if os.environ.get("B2S_TILES", "0") == "0":
         return
     n = f.num_block_rows
@@ -361,15 +363,12 @@ def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
                                   D.ptr(plan.device("inverse_permutation")),
                                   D.ptr(f._lu.pat.rp), D.ptr(f._lu.pat.ci), D.ptr(diag),
                                   D.ptr(f._lu.vals), D.ptr(f._invd),
-                                  D.ptr(plan.device("group_offsets")), plan.group_count, f.kc,
-                                  int(os.environ.get("B2S_TILE_WARPS", 16)), C.byref(h),
-                                  D.stream())
-    if rc == 5:   # B2S_UNSUPPORTED: a tile does not fit, keep the sync-free sweeps
+                                  D.ptr(plan.device("group_offsets")), plan.group_count,
+                                  C.byref(h), D.stream())
+    if rc == 5:   # B2S_UNSUPPORTED: the ring does not fit, keep the sync-free sweeps
         return
     check(rc, "tiles_create")
     f.tiles = h.value
-    if os.environ.get("B2S_TILES_KERNEL", "wave") == "poll":
-        check(D.lib().b2s_tiles_set_kernel(f.tiles, 0), "tiles_set_kernel")
     f.tile_shape = (px, py) if px else (T,)
 
 

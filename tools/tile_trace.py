@@ -26,15 +26,15 @@ plan = plan_device(P.Backend.LEVEL_SCHEDULED, bsr.pat)
 f = factor_device(a, plan, bsr)
 assert f.tiles
 T = f.tile_shape[0] * f.tile_shape[1] if len(f.tile_shape) == 2 else f.tile_shape[0]
-buf = torch.zeros(2 * T * 1024, dtype=torch.int64, device="cuda")
-D.lib().b2s_tiles_trace(f.tiles, buf.data_ptr())
+buf = torch.zeros(2 * T * 1024 * 4, dtype=torch.int64, device="cuda")
+D.lib().b2s_tiles_trace(f.tiles, buf.data_ptr(), 0)
 m = a.num_block_rows * 3
 x = torch.rand(m, dtype=torch.float64, device="cuda")
 z = torch.empty(m, dtype=torch.float64, device="cuda")
 for _ in range(3):
     f.apply_device(x, z)
 torch.cuda.synchronize()
-tr = buf.view(2, T, 1024).cpu().numpy().astype(np.int64)
+tr = buf.view(2, T, 1024, 4)[..., 2].cpu().numpy().astype(np.int64)
 for d, name in ((0, "forward"), (1, "backward")):
     v = tr[d]
     t0 = v[v > 0].min()
