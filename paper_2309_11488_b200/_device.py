@@ -115,6 +115,15 @@ def pin_host(obj):
     return pinned_copy(obj)
 
 
+def to_host_vector(v: torch.Tensor, count: int, block_size: int):
+    """The solution as a host BlockVector: finiteness is checked on the device
+    (one reduction) instead of on the host, then one D2H into pinned memory."""
+    from .blockcore import BlockVector
+    if not all_finite(v, int(count)):
+        raise ValueError("block vector entries must be finite")
+    return BlockVector._checked_on_device(to_host(v, count), block_size)
+
+
 def to_host(v: torch.Tensor, count: int) -> np.ndarray:
     """D2H of the first ``count`` elements into page-locked memory (fast DMA;
     the returned array owns a pinned block of the caching host allocator)."""

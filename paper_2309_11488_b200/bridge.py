@@ -209,7 +209,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
 
     if primary.converged:
         with trace.phase("download"):
-            out = BlockVector(D.to_host(x, n * bs), bs)
+            out = D.to_host_vector(x, n * bs, bs)
         primary.phases = trace.finish()
         return out, primary
 
@@ -235,7 +235,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     report.elapsed += primary.elapsed
     if not report.converged:
         raise SolveFailed(primary, report)
-    return BlockVector(D.to_host(xd, n * bs), bs), report
+    return D.to_host_vector(xd, n * bs, bs), report
 
 
 def _solve_separate_wells(cfg: SolverConfig, a_sys: BlockMatrix, wells: WellSet,

@@ -18,6 +18,7 @@ struct State {
   double rho, rho_prev, alpha, omega, beta;
   double norm0, target, final_norm, its;
   int k, maxit, done, reason;
+  int init_exit;   // finished by k_ctl_init (no iteration): zero/non-finite r0, rho_0 breakdown
 };
 
 enum CtlStep { kCtlNone = 0, kCtlAlpha = 1, kCtlS = 2, kCtlOmega = 3, kCtlEndBegin = 4 };

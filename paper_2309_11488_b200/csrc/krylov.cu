@@ -57,7 +57,8 @@ __device__ double reduce_parts(const double* parts, int np, double* red) {
   return block_sum(v, red);  // valid in thread 0
 }
 
-__global__ void k_ctl_init(State* st, const double* prr, int np, double tol, int maxit) {
+__global__ void k_ctl_init(State* st, const double* prr, int np, double tol, int maxit,
+                           int* host_done) {
   __shared__ double red[8];
   const double s = reduce_parts(prr, np, red);
   if (threadIdx.x == 0) {
@@ -71,6 +72,9 @@ __global__ void k_ctl_init(State* st, const double* prr, int np, double tol, int
     // top of iteration 0 (maxit >= 1): rho_0 = rhat.r0 = the same partials
     else if (fabs(s) < kBreakdown) { st->done = 1; st->reason = kBreakdownR; }
     else st->rho = s;
+    // no iteration needed: let the host's replay loop stop at its first check
+    st->init_exit = st->done;
+    if (st->done && host_done) *reinterpret_cast<volatile int*>(host_done) = 1;
   }
 }
 
@@ -300,48 +304,58 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   cudaStream_t user = a->stream;
   const int grid_v = np;
 
-  // ---- setup on the caller's stream: r0 = b - A x0, |r0|, r^ = r0, rho_0 partials
-  B2S_CHECK(cudaMemsetAsync(tickets, 0, 64, user));
-  k_copy<<<grid_v, 256, 0, user>>>(m, a->x, x0);
-  int rc = launch_spmv(a->b, 3, np, map, A, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{}, user);
-  if (rc) return rc;
-  k_ctl_init<<<1, 256, 0, user>>>(state, prr, np, a->tol, a->maxit);
-  k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
-  k_copy<<<grid_v, 256, 0, user>>>(m, r, v);  // v is only read for k > 0
-  if (ilu && !phased) {
-    if ((rc = fill_sentinel(m, y, user))) return rc;
-    if ((rc = fill_sentinel(m, phat, user))) return rc;
-    if ((rc = fill_sentinel(m, shat, user))) return rc;
+  // mapped pinned word the exiting CTA (or the init kernel) sets; the host
+  // polls it `lag` replays behind the device
+  int* host_done = nullptr;
+  int* dev_done = nullptr;
+  if (cudaHostAlloc(&host_done, sizeof(int), cudaHostAllocMapped) != cudaSuccess)
+    return B2S_CUDA_ERROR;
+  *host_done = 0;
+  if (cudaHostGetDevicePointer(&dev_done, host_done, 0) != cudaSuccess) {
+    cudaFreeHost(host_done);
+    return B2S_CUDA_ERROR;
   }
-  B2S_LAUNCH_CHECK();
+
+  // ---- setup on the caller's stream: r0 = b - A x0, |r0|, r^ = r0, rho_0
+  // partials.  No host synchronisation here: the iteration graph is captured
+  // and instantiated while these kernels run, and the initial state is read
+  // back once, after the solve.
+  int rc = B2S_OK;
+  if (cudaMemsetAsync(tickets, 0, 64, user) != cudaSuccess) rc = B2S_CUDA_ERROR;
+  if (rc == B2S_OK) {
+    k_copy<<<grid_v, 256, 0, user>>>(m, a->x, x0);
+    rc = launch_spmv(a->b, 3, np, map, A, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{}, user);
+  }
+  if (rc == B2S_OK) {
+    k_ctl_init<<<1, 256, 0, user>>>(state, prr, np, a->tol, a->maxit, dev_done);
+    k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
+    k_copy<<<grid_v, 256, 0, user>>>(m, r, v);  // v is only read for k > 0
+    if (ilu && !phased) {
+      rc = fill_sentinel(m, y, user);
+      if (!rc) rc = fill_sentinel(m, phat, user);
+      if (!rc) rc = fill_sentinel(m, shat, user);
+    }
+  }
+  if (rc == B2S_OK && cudaGetLastError() != cudaSuccess) rc = B2S_CUDA_ERROR;
+  if (rc != B2S_OK) {
+    cudaStreamSynchronize(user);
+    cudaFreeHost(host_done);
+    return rc;
+  }
   State hs;
-  B2S_CHECK(cudaMemcpyAsync(&hs, state, sizeof(State), cudaMemcpyDeviceToHost, user));
-  B2S_CHECK(cudaStreamSynchronize(user));
-  res->initial_norm = hs.norm0;
-  if (hs.done) {  // non-finite or zero initial residual: no iteration
-    res->converged = hs.reason == kConverged;
-    res->reason = hs.reason;
-    res->final_norm = hs.norm0;
-    return B2S_OK;
-  }
 
   // ---- capture one iteration
   cudaStream_t cs;
-  B2S_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  int* host_done = nullptr;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaStreamSynchronize(user);
+    cudaFreeHost(host_done);
+    return B2S_CUDA_ERROR;
+  }
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int status = B2S_OK;
   int kernels = 0;
   do {
-    if (cudaHostAlloc(&host_done, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
-      status = B2S_CUDA_ERROR; break;
-    }
-    *host_done = 0;
-    int* dev_done = nullptr;
-    if (cudaHostGetDevicePointer(&dev_done, host_done, 0) != cudaSuccess) {
-      status = B2S_CUDA_ERROR; break;
-    }
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       status = B2S_CUDA_ERROR; break;
     }
@@ -454,6 +468,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
 
   B2S_CHECK(cudaMemcpyAsync(&hs, state, sizeof(State), cudaMemcpyDeviceToHost, user));
   B2S_CHECK(cudaStreamSynchronize(user));
+  res->initial_norm = hs.norm0;
+  if (hs.init_exit) {  // zero or non-finite initial residual, rho_0 breakdown: no iteration
+    res->converged = hs.reason == kConverged;
+    res->reason = hs.reason;
+    res->final_norm = hs.norm0;
+    return B2S_OK;
+  }
   res->iterations = hs.its;
   res->reason = hs.reason == kRunning ? kBudget : hs.reason;
   if (hs.reason == kConverged) {
