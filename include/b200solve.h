@@ -54,6 +54,19 @@ int b2s_level_schedule(int n, const int32_t* rp, const int32_t* ci, int32_t* row
 int b2s_graph_color(int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,
                     int32_t* ngroups_host, cudaStream_t stream);
 
+/* The same two plans with a grid hint (nx, ny of a natural-order stencil;
+ * nx <= 0: none): the closed-form plan (level = ix+iy+iz, colour = parity) is
+ * checked against every row's defining equation in one pass -- a plan that
+ * satisfies them all is, by induction over the rows, the reference's plan --
+ * and the sync-free wavefront runs only if some row violates it.
+ * *used_hint = 1 when the checked guess was taken. */
+int b2s_level_schedule_hint(int n, const int32_t* rp, const int32_t* ci, int nx, int ny,
+                            int32_t* row_group, int32_t* ngroups_host, int* used_hint,
+                            cudaStream_t stream);
+int b2s_graph_color_hint(int n, const int32_t* rp, const int32_t* ci, int nx, int ny,
+                         int32_t* row_group, int32_t* ngroups_host, int* used_hint,
+                         cudaStream_t stream);
+
 /* debug: rerun the level (kind 0) / colour (1) kernel recording each row's
  * publication time (%globaltimer, ns) in trace[n] */
 int b2s_analysis_trace(int kind, int n, const int32_t* rp, const int32_t* ci, int32_t* row_group,

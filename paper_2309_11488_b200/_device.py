@@ -15,6 +15,7 @@ Layout in HBM:
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -144,12 +145,32 @@ def empty_f64(n, dev):
 
 # ---------------------------------------------------------------------------
 
+def grid_hint(n: int, rp: np.ndarray, ci: np.ndarray):
+    """(nx, ny) if the couplings of the middle row look like a natural-order
+    nx x ny x nz stencil (positive offsets {1, nx, nx*ny}, or a 2-D / 1-D
+    subset), else None.  A hint only: the plan kernels verify any guess built
+    from it against every row, so a wrong hint costs one pass, never a result."""
+    if n < 8:
+        return None
+    r = n // 2
+    off = np.asarray(ci[int(rp[r]):int(rp[r + 1])], dtype=np.int64) - r
+    u = [int(v) for v in np.unique(off[off > 0])]
+    if u == [1]:
+        return n, 1
+    if len(u) == 2 and u[0] == 1 and n % u[1] == 0:
+        return u[1], n // u[1]
+    if len(u) == 3 and u[0] == 1 and u[2] % u[1] == 0 and n % u[2] == 0:
+        return u[1], u[2] // u[1]
+    return None
+
+
 @dataclass
 class DevPattern:
     n: int
     nnz: int
     rp: torch.Tensor
     ci: torch.Tensor
+    grid: tuple | None = None    # grid_hint of the host pattern
 
     @classmethod
     def upload(cls, pattern) -> "DevPattern":
@@ -158,7 +179,7 @@ class DevPattern:
         rp = np.asarray(pattern.row_pointers)
         ci = np.asarray(pattern.column_indices)
         return cls(n, int(rp[-1]) if n else 0, i32(rp, dev), i32(ci, dev) if ci.size
-                   else empty_i32(1, dev))
+                   else empty_i32(1, dev), grid_hint(n, rp, ci))
 
     def host(self):
         rp = self.rp[: self.n + 1].cpu().numpy().astype(np.int64)
@@ -250,10 +271,15 @@ def groups(p: DevPattern, kind: str):
     """Device level schedule / colouring; returns (row_group int32, ngroups)."""
     g = empty_i32(p.n, p.rp.device)
     ng = C.c_int32(0)
-    fn = lib().b2s_level_schedule if kind == "level" else lib().b2s_graph_color
+    used = C.c_int(0)
+    fn = lib().b2s_level_schedule_hint if kind == "level" else lib().b2s_graph_color_hint
     # MissingDiagonal first, exactly like bs/analysis.py:79-82
     find_diagonal(p)
-    check(fn(p.n, ptr(p.rp), ptr(p.ci), ptr(g), C.byref(ng), stream()), kind)
+    nx, ny = (p.grid if p.grid is not None and os.environ.get("B2S_PLAN_HINT", "1") != "0"
+              else (0, 0))
+    check(fn(p.n, ptr(p.rp), ptr(p.ci), nx, ny, ptr(g), C.byref(ng), C.byref(used), stream()),
+          kind)
+    p.hint_used = bool(used.value)
     return g, int(ng.value)
 
 

@@ -49,6 +49,8 @@ SIGNATURES = {
     "b2s_find_diagonal": (_I, [_I, _P, _P, _P, _PI, _P]),
     "b2s_level_schedule": (_I, [_I, _P, _P, _P, _PI, _P]),
     "b2s_graph_color": (_I, [_I, _P, _P, _P, _PI, _P]),
+    "b2s_level_schedule_hint": (_I, [_I, _P, _P, _I, _I, _P, _P, _P, _P]),
+    "b2s_graph_color_hint": (_I, [_I, _P, _P, _I, _I, _P, _P, _P, _P]),
     "b2s_analysis_trace": (_I, [_I, _I, _P, _P, _P, _P, _P]),
     "b2s_plan_from_groups": (_I, [_I, _P, _I, _P, _P, _P, _P]),
     "b2s_permute_bsr": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),

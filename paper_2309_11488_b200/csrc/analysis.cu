@@ -523,6 +523,83 @@ inline int sync_free_grid(int n, const void* fn) {
 
 }  // namespace b2s
 
+namespace b2s {
+
+// ---------------------------------------------------------------------------
+// Speculate and verify.  Both plans are the unique solution of per-row
+// equations over earlier rows only:
+//   level(i)  = 1 + max{level(j) : j < i, (i,j) in pattern}   (0 if none)
+//   colour(i) = mex{colour(j) : j < i, (i,j) or (j,i) in pattern}
+// so, by induction on i, any assignment that satisfies every equation IS the
+// reference's plan (bit for bit).  For a natural-order nx x ny x nz stencil
+// the solutions are known in closed form (level = ix+iy+iz, colour = its
+// parity); one parallel pass checks a guess instead of ~(nx+ny+nz) dependent
+// L2 round trips of the wavefront.  Any violated equation -> the wavefront.
+__global__ void k_grid_guess(int n, int nx, int ny, int parity, int32_t* g) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int ix = i % nx, iy = (i / nx) % ny, iz = i / (nx * ny);
+    const int s = ix + iy + iz;
+    g[i] = parity ? (s & 1) : s;
+  }
+}
+// out[0]: violations; out[1]: max group
+__global__ void k_verify_levels(int n, const int32_t* __restrict__ rp,
+                                const int32_t* __restrict__ ci, const int32_t* __restrict__ g,
+                                int32_t* out) {
+  int bad = 0, mx = -1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int m = -1;
+    for (int q = rp[i]; q < rp[i + 1]; ++q) {
+      const int c = ci[q];
+      if (c >= i) break;   // sorted columns: the strict-lower entries come first
+      m = max(m, g[c]);
+    }
+    const int gi = g[i];
+    bad |= gi != m + 1;
+    mx = max(mx, gi);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAdd(out, 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out + 1, mx);
+}
+// colours over the strict-lower entries, which is the symmetrised lower
+// adjacency only if the pattern is structurally symmetric: every upper entry
+// (i,j) must have its mirror (j,i) (binary search in row j)
+__global__ void k_verify_colours(int n, const int32_t* __restrict__ rp,
+                                 const int32_t* __restrict__ ci, const int32_t* __restrict__ g,
+                                 int32_t* out) {
+  int bad = 0, mx = -1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    unsigned long long mask = 0ull;
+    for (int q = rp[i]; q < rp[i + 1]; ++q) {
+      const int c = ci[q];
+      if (c < i) {
+        const int gc = g[c];
+        if (gc < 0 || gc >= 64) bad = 1; else mask |= 1ull << gc;
+      } else if (c > i) {
+        int lo = rp[c], hi = rp[c + 1] - 1;
+        bool found = false;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1, v = ci[mid];
+          if (v == i) { found = true; break; }
+          if (v < i) lo = mid + 1; else hi = mid - 1;
+        }
+        bad |= !found;
+      }
+    }
+    const int gi = g[i];
+    bad |= gi != __ffsll((long long)~mask) - 1;
+    mx = max(mx, gi);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAdd(out, 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out + 1, mx);
+}
+
+}  // namespace b2s
+
 using namespace b2s;
 
 extern "C" {
@@ -621,6 +698,51 @@ int b2s_graph_color(int n, const int32_t* rp, const int32_t* ci, int32_t* row_gr
   B2S_CHECK(cudaFreeAsync(idx, st));
   B2S_CHECK(cudaFreeAsync(ticket, st));
   return finish_groups(n, row_group, ngroups_host, st);
+}
+
+// Level schedule / colouring with a grid hint (nx, ny of a natural-order
+// stencil; nx <= 0: none): the closed-form plan is checked against every
+// row's equation in one pass and used when it holds; otherwise (or without
+// a hint) the sync-free wavefront.  Either way the result is the reference's.
+static int groups_hint(int kind, int n, const int32_t* rp, const int32_t* ci, int nx, int ny,
+                       int32_t* row_group, int32_t* ngroups_host, int* used_hint,
+                       cudaStream_t st) {
+  *ngroups_host = 0;
+  if (used_hint) *used_hint = 0;
+  if (n <= 0) return n < 0 ? B2S_SHAPE : B2S_OK;
+  if (nx > 0 && ny > 0) {
+    int32_t* d = nullptr;
+    B2S_CHECK(cudaMallocAsync(&d, 2 * sizeof(int32_t), st));
+    B2S_CHECK(cudaMemsetAsync(d, 0, sizeof(int32_t), st));
+    B2S_CHECK(cudaMemsetAsync(d + 1, 0xff, sizeof(int32_t), st));
+    k_grid_guess<<<grid_for(n), 256, 0, st>>>(n, nx, ny, kind, row_group);
+    if (kind == 0) k_verify_levels<<<grid_for(n), 256, 0, st>>>(n, rp, ci, row_group, d);
+    else k_verify_colours<<<grid_for(n), 256, 0, st>>>(n, rp, ci, row_group, d);
+    B2S_LAUNCH_CHECK();
+    int32_t h[2] = {1, -1};
+    B2S_CHECK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    B2S_CHECK(cudaFreeAsync(d, st));
+    B2S_CHECK(cudaStreamSynchronize(st));
+    if (h[0] == 0) {
+      *ngroups_host = h[1] + 1;
+      if (used_hint) *used_hint = 1;
+      return B2S_OK;
+    }
+  }
+  return kind == 0 ? b2s_level_schedule(n, rp, ci, row_group, ngroups_host, st)
+                   : b2s_graph_color(n, rp, ci, row_group, ngroups_host, st);
+}
+
+int b2s_level_schedule_hint(int n, const int32_t* rp, const int32_t* ci, int nx, int ny,
+                            int32_t* row_group, int32_t* ngroups_host, int* used_hint,
+                            cudaStream_t st) {
+  return groups_hint(0, n, rp, ci, nx, ny, row_group, ngroups_host, used_hint, st);
+}
+
+int b2s_graph_color_hint(int n, const int32_t* rp, const int32_t* ci, int nx, int ny,
+                         int32_t* row_group, int32_t* ngroups_host, int* used_hint,
+                         cudaStream_t st) {
+  return groups_hint(1, n, rp, ci, nx, ny, row_group, ngroups_host, used_hint, st);
 }
 
 // debug (tools/analysis_trace.py): publication time of every row

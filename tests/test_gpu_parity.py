@@ -495,3 +495,40 @@ def test_two_colour_factor_bit_equal_to_general(monkeypatch, golden, name):
     x1, r1 = P.bicgstab(P.MatrixOperator(a), f1, rhs, stop=stop)
     assert r0.iterations == r1.iterations and r0.final_norm == r1.final_norm
     assert_array_equal(x0.data, x1.data)
+
+
+@pytest.mark.parametrize("name", SYSTEMS + ["random_patterns"])
+def test_plan_hint_is_verified(monkeypatch, golden, name):
+    """The closed-form grid plans (csrc/analysis.cu k_grid_guess) are taken
+    only when every row's defining equation holds, so plans with and without
+    the hint are identical; masked / random patterns fall back to the
+    wavefront, also for deliberately wrong hints."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2309_11488_b200 import _device as D
+    g = golden(name)
+    mats = ([matrix({k[len(f"r{t}_"):]: v for k, v in g.items() if k.startswith(f"r{t}_")})
+             for t in range(12)] if name == "random_patterns" else [matrix(g)])
+    for a in mats:
+        p = D.DevPattern.upload(a.pattern)
+        for kind in ("level", "color"):
+            monkeypatch.setenv("B2S_PLAN_HINT", "0")
+            g0, n0 = D.groups(p, kind)
+            monkeypatch.setenv("B2S_PLAN_HINT", "1")
+            g1, n1 = D.groups(p, kind)
+            assert n0 == n1 and torch.equal(g0[: p.n], g1[: p.n])
+            if name in ("c1_20x20x10", "gen_6x5x4_b2", "hetero_10x12x6"):
+                assert p.hint_used, (name, kind)
+            if name.startswith("masked"):
+                assert not p.hint_used
+            # wrong hints: every (nx, ny) is checked, never trusted
+            fn = (D.lib().b2s_level_schedule_hint if kind == "level"
+                  else D.lib().b2s_graph_color_hint)
+            for nx, ny in ((2, 3), (p.n, 1), (1, p.n)):
+                gw = D.empty_i32(p.n, p.rp.device)
+                ng, used = C.c_int32(0), C.c_int(0)
+                D.check(fn(p.n, D.ptr(p.rp), D.ptr(p.ci), nx, ny, D.ptr(gw), C.byref(ng),
+                           C.byref(used), D.stream()), kind)
+                assert ng.value == n0 and torch.equal(gw[: p.n], g0[: p.n]), (nx, ny)
