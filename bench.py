@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--no-other-plan", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--ref-slab", type=int, default=2, help="z-planes of the CPU sample")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="take the multi-GPU code path even with one rank (smoke test)")
+    ap.add_argument("--dist-comm", default="mesh", choices=["mesh", "nccl"],
+                    help="N>1: peer-memory device loop (default) or NCCL host loop")
     return ap.parse_args()
 
 
@@ -181,7 +185,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.force_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from bench_dist import run_distributed
         return run_distributed(args, world, rank, local, METRIC, UNIT, Clocks, peaks,

@@ -1,11 +1,17 @@
-"""Multi-GPU leg of bench.py (torchrun, one rank per GPU, NCCL over NVLink).
+"""Multi-GPU leg of bench.py (torchrun, one rank per GPU, NVLink peer memory).
 
 Weak scaling: the global system is GeneratorSpec(nx, ny, nz * N, seed=0);
 rank g owns z-planes [g*nz, (g+1)*nz) (1M cells at the default grid),
 generated draw-for-draw as the rows of the global system.  One step = one
 complete partitioned solve: per-slab level/colour plan + block-Jacobi ILU0
-+ BiCGStab with halo SpMV and all-reduced dots.  Times are CUDA events on
-each rank, max over ranks.
++ BiCGStab.  Default communication ("mesh"): every rank runs the
+device-resident BiCGStab loop (one CUDA graph per iteration) and the kernels
+talk to the peers through NVLink peer memory opened with CUDA IPC -- the
+SpMV's ghost rows are read straight from the owners' vectors and the dot
+products are all-reduced through per-rank mailboxes by the last CTA of each
+reducing kernel (csrc/krylov.cu, b2s_mesh).  "--dist-comm nccl" runs the
+host-driven loop with NCCL send/recv halos and all-reduces instead.  Times
+are CUDA events on each rank, max over ranks.
 """
 
 from __future__ import annotations
@@ -19,7 +25,8 @@ import torch.distributed as dist
 def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_port_sample):
     import paper_2309_11488_b200 as P
     from paper_2309_11488_b200.distributed import (NcclComm, Shard, exchange_requests,
-                                                   generate_slab, slab_bounds, solve_shards)
+                                                   generate_slab, slab_bounds,
+                                                   solve_shard_mesh_dist, solve_shards)
     import numpy as np
 
     nx, ny, nz = (int(v) for v in args.grid.split(","))
@@ -36,12 +43,15 @@ def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_p
         return out
 
     st = torch.cuda.current_stream()
-    shard = Shard(slab, owners, None)          # matrix uploaded once (resident)
+    mesh = getattr(args, "dist_comm", "mesh") == "mesh"
+    shard = Shard(slab, owners, backend)       # matrix uploaded once (resident)
     exchange_requests([shard], world, gather)
-    comm = NcclComm(shard)
+    comm = None if mesh else NcclComm(shard)
 
     def step():
         shard.setup(backend)                   # plan + permute + ILU0 + layouts
+        if mesh:
+            return solve_shard_mesh_dist(shard, stop, cache_key=args.backend)[0]
         return solve_shards([shard], comm, stop)[0]
 
     def timed(fn, steps, warmup):
@@ -69,6 +79,11 @@ def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_p
     def e2e_step():                            # host slab in, host x out
         sh = Shard(slab, owners, backend)
         exchange_requests([sh], world, gather)
+        if mesh:
+            sh.mesh = shard.mesh                   # the IPC-shared buffers stay mapped
+            rep, x = solve_shard_mesh_dist(sh, stop, cache_key=args.backend)
+            x.cpu()
+            return rep
         rep, xs = solve_shards([sh], NcclComm(sh), stop)
         xs[0].cpu()
         return rep
@@ -84,7 +99,9 @@ def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_p
                                    f"{slab.rows} cells/GPU z-slabs, block-Jacobi ILU0, halo "
                                    f"SpMV, all-reduced dots, tol {args.tol:g}",
                        "backend": args.backend, "cells_total": n_total,
-                       "parallelism": f"slab x{world} (NCCL)"},
+                       "parallelism": f"slab x{world} ("
+                                      + ("NVLink peer memory, device loop" if mesh else
+                                         "NCCL, host loop") + ")"},
             "iterations": iters, "solve_ms": ms, "clocks": clk,
             "e2e": None if e2e_ms is None else {
                 "value": n_total / (e2e_ms / 1e3) / 1e6, "unit": unit, "ms_per_step": e2e_ms,

@@ -239,6 +239,52 @@ int b2s_fuse_check(int s1, int b, const int32_t* row0, const int32_t* nrows, con
                    const int32_t* u_cols, const double* u_vals, int* ok_host,
                    cudaStream_t stream);
 
+/* Sharded solves (one shard per rank): peer-memory communication.  Every
+ * pointer is device memory valid in this process -- another process's
+ * buffers opened with b2s_ipc_open (NVLink P2P), or another shard's buffers
+ * on the same GPU.  Ghost rows (the columns of owned rows that other ranks
+ * own) are appended after the n owned rows of x, phat and shat; before each
+ * SpMV they are pulled straight from the owners' vectors.  Dot products are
+ * all-reduced through per-rank mailboxes (kMboxSlots x nranks x 4 doubles):
+ * the last CTA of each reducing kernel posts its local sums into every
+ * rank's mailbox and sums all ranks' posts in rank order (deterministic). */
+typedef struct {
+  int rank, nranks;
+  int nghost;                      /* ghost rows after the n owned rows */
+  const int32_t* ghost_owner;      /* [nghost] owning rank */
+  const int32_t* ghost_row;        /* [nghost] plan-order row on the owner */
+  int nnbr;
+  const int32_t* nbr;              /* [nnbr] ranks this one pulls ghosts from */
+  double* const* peer_x;           /* [nranks] every rank's x / phat / shat */
+  double* const* peer_phat;
+  double* const* peer_shat;
+  long long* flags;                /* [nranks] readiness flags peers post here */
+  long long* const* peer_flags;    /* [nranks] every rank's flags */
+  double* mbox;                    /* this rank's mailbox */
+  double* const* peer_mbox;        /* [nranks] every rank's mailbox */
+  long long seq_base;              /* strictly increasing per solve, equal on all ranks */
+  int shared_device;               /* shards share one GPU: no programmatic launch overlap */
+  /* optional: called (by every shard's host thread) once all host-side
+   * preparation is done and again after the device loop -- shards on one GPU
+   * rendezvous there, so no implicitly synchronising host call (host/device
+   * allocation, graph instantiation) runs while a peer's kernel waits */
+  void (*host_barrier)(void*);
+  void* host_barrier_ctx;
+} b2s_mesh;
+
+#define B2S_MBOX_SLOTS 8
+/* bytes of one rank's mailbox */
+long long b2s_mesh_mbox_bytes(int nranks);
+/* double offsets of phat and shat inside the b2s_bicgstab workspace */
+int b2s_bicgstab_workspace_layout(int n, int nghost, int b, long long* phat_off,
+                                  long long* shat_off);
+long long b2s_bicgstab_workspace_bytes_mesh(int n, int nghost, int b, int nparts);
+/* CUDA IPC of a device buffer (any pointer inside a cudaMalloc allocation):
+ * 64-byte handle + offset from the allocation base; open maps it here. */
+int b2s_ipc_handle(const void* ptr, unsigned char* handle64, long long* offset);
+int b2s_ipc_open(const unsigned char* handle64, long long offset, void** ptr_out);
+int b2s_ipc_close(void* base);
+
 typedef struct {
   int n, b, nparts, precond /* 0 none, 1 ilu0 */, kc, maxit, check_lag;
   int refill_y; /* 1: U has same-group entries, refill the sweep scratch each apply */
@@ -263,6 +309,10 @@ typedef struct {
   const int32_t* gslice_host;
   /* 2 colours and b2s_fuse_check() passed: fused colour-0 backward + SpMV */
   int fuse;
+  /* sharded solve over peer memory (NULL: single system); x is then
+   * (n + mesh->nghost) * b long and the workspace sized by
+   * b2s_bicgstab_workspace_bytes_mesh */
+  const b2s_mesh* mesh;
 } b2s_bicg_args;
 
 typedef struct {

@@ -35,7 +35,19 @@ class BicgArgs(C.Structure):
                 ("u_sp", _P), ("u_cols", _P), ("u_vals", _P),
                 ("dinv_tiles", _P), ("tiles", _P), ("rhs", _P), ("x", _P), ("work", _P),
                 ("stream", _P), ("ngroups", _I), ("goff1", _I), ("gslice_host", _P),
-                ("fuse", _I)]
+                ("fuse", _I), ("mesh", _P)]
+
+
+class Mesh(C.Structure):
+    """b2s_mesh (include/b200solve.h): peer-memory communication of a shard."""
+    _fields_ = [("rank", _I), ("nranks", _I), ("nghost", _I), ("ghost_owner", _P),
+                ("ghost_row", _P), ("nnbr", _I), ("nbr", _P), ("peer_x", _P),
+                ("peer_phat", _P), ("peer_shat", _P), ("flags", _P), ("peer_flags", _P),
+                ("mbox", _P), ("peer_mbox", _P), ("seq_base", C.c_longlong),
+                ("shared_device", _I), ("host_barrier", _P), ("host_barrier_ctx", _P)]
+
+
+BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
 
 
 class BicgResult(C.Structure):
@@ -84,6 +96,12 @@ SIGNATURES = {
     "b2s_tiles_destroy": (_I, [_P]),
     "b2s_tiles_apply": (_I, [_I, _P, _P, _P, _P, _I, _P]),
     "b2s_dot": (_I, [_LL, _P, _P, _I, _P, _P, _P]),
+    "b2s_mesh_mbox_bytes": (_LL, [_I]),
+    "b2s_bicgstab_workspace_layout": (_I, [_I, _I, _I, _PLL, _PLL]),
+    "b2s_bicgstab_workspace_bytes_mesh": (_LL, [_I, _I, _I, _I]),
+    "b2s_ipc_handle": (_I, [_P, _P, _PLL]),
+    "b2s_ipc_open": (_I, [_P, _LL, C.POINTER(C.c_void_p)]),
+    "b2s_ipc_close": (_I, [_P]),
     "b2s_all_finite": (_I, [_LL, _P, _P, _P]),
     "b2s_reduce": (_I, [_P, _I, _P, _P]),
     "b2s_vec_p": (_I, [_LL, _I, C.c_double, C.c_double, _P, _P, _P, _P, _P]),

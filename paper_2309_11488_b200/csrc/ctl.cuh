@@ -19,7 +19,66 @@ struct State {
   double norm0, target, final_norm, its;
   int k, maxit, done, reason;
   int init_exit;   // finished by k_ctl_init (no iteration): zero/non-finite r0, rho_0 breakdown
+  long long cseq;  // mesh: control points passed (mailbox sequence)
+  long long pub;   // mesh: vectors published (readiness-flag sequence)
 };
+
+// Sharded solves: the all-reduce mailbox of this rank and every rank's
+// (b2s_mesh in b200solve.h).  mbox == nullptr: single system.
+constexpr int kMboxSlots = B2S_MBOX_SLOTS;
+enum MboxSlot { kSlotInit = 0, kSlotFinal = 5, kSlotFinite = 6 };
+struct MeshDev {
+  int rank, nranks;
+  double* mbox;
+  double* const* peer_mbox;
+  long long seq_base;
+};
+
+__device__ __forceinline__ void st_relaxed_sys(double* p, double v) {
+  asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(long long* p, long long v) {
+  asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// All-reduce of (a, b) over the mesh, one thread: post the local sums into
+// slot `slot` of every rank's mailbox, wait for every rank's post of this
+// sequence number, sum them in rank order.  Every rank computes the same
+// bits.  A slot is reused only after every rank has read it: a rank posts
+// into slot s again only after passing the control points in between, which
+// need every other rank's later posts.
+__device__ __forceinline__ void mesh_sum(const MeshDev& m, long long seq, int slot, double& a,
+                                         double& b) {
+  const int N = m.nranks;
+  for (int h = 0; h < N; ++h) {
+    double* e = m.peer_mbox[h] + ((long long)slot * N + m.rank) * 4;
+    st_relaxed_sys(e, a);
+    st_relaxed_sys(e + 1, b);
+  }
+  __threadfence_system();
+  for (int h = 0; h < N; ++h)
+    st_release_sys(reinterpret_cast<long long*>(m.peer_mbox[h] + ((long long)slot * N + m.rank) * 4 + 2),
+                   seq);
+  double sa = 0.0, sb = 0.0;
+  for (int h = 0; h < N; ++h) {
+    const double* e = m.mbox + ((long long)slot * N + h) * 4;
+    while (ld_acquire_sys(reinterpret_cast<const long long*>(e + 2)) < seq) __nanosleep(32);
+    sa += ld_relaxed_sys(e);
+    sb += ld_relaxed_sys(e + 1);
+  }
+  a = sa;
+  b = sb;
+}
 
 enum CtlStep { kCtlNone = 0, kCtlAlpha = 1, kCtlS = 2, kCtlOmega = 3, kCtlEndBegin = 4 };
 
@@ -28,6 +87,7 @@ struct Ctl {
   unsigned* counter;    // arrival ticket of this call site (self-resetting)
   int* host_done;       // mapped pinned word the host polls (may be nullptr)
   int step;             // CtlStep
+  MeshDev mesh;         // sharded solve: all-reduce the sums first
 };
 
 // deterministic sum of np partials by one CTA (L2 loads: written by other SMs)
@@ -63,10 +123,12 @@ __device__ __forceinline__ void ctl_finish(State* st, int* host_done, int reason
 __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const double* p1, int np,
                                         double* red) {
   State* st = c.st;
-  const double a = reduce_parts_cg(p0, np, red);
+  const double a0 = reduce_parts_cg(p0, np, red);
   double b = 0.0;
   if (c.step == kCtlOmega || c.step == kCtlEndBegin) b = reduce_parts_cg(p1, np, red);
   if (threadIdx.x != 0) return;
+  double a = a0;
+  if (c.mesh.mbox) mesh_sum(c.mesh, c.mesh.seq_base + (++st->cseq), c.step, a, b);
   switch (c.step) {
     case kCtlAlpha: {  // gamma = rhat.v  (bs/krylov.py:206-210)
       if (fabs(a) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }

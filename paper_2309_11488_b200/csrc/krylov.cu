@@ -25,6 +25,9 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cstring>
+#include <cuda.h>
+
 #include "ctl.cuh"
 #include "sell.cuh"
 
@@ -58,10 +61,15 @@ __device__ double reduce_parts(const double* parts, int np, double* red) {
 }
 
 __global__ void k_ctl_init(State* st, const double* prr, int np, double tol, int maxit,
-                           int* host_done) {
+                           int* host_done, MeshDev mesh) {
   __shared__ double red[8];
-  const double s = reduce_parts(prr, np, red);
+  double s = reduce_parts(prr, np, red);
   if (threadIdx.x == 0) {
+    if (!mesh.mbox) { st->cseq = 0; st->pub = 0; }
+    if (mesh.mbox) {   // sharded: |r0|^2 over every rank
+      double unused = 0.0;
+      mesh_sum(mesh, mesh.seq_base + (++st->cseq), kSlotInit, s, unused);
+    }
     const double n0 = sqrt(s);
     st->rho = 0.0; st->rho_prev = 1.0; st->alpha = 1.0; st->omega = 1.0; st->beta = 0.0;
     st->norm0 = n0; st->target = tol * n0; st->final_norm = n0; st->its = 0.0;
@@ -75,6 +83,72 @@ __global__ void k_ctl_init(State* st, const double* prr, int np, double tol, int
     // no iteration needed: let the host's replay loop stop at its first check
     st->init_exit = st->done;
     if (st->done && host_done) *reinterpret_cast<volatile int*>(host_done) = 1;
+  }
+}
+
+// ---- sharded solves: ghost rows straight from the owners' vectors
+struct MeshHalo {
+  int rank, nranks, nghost, nnbr;
+  const int32_t* nbr;
+  const int32_t* ghost_owner;
+  const int32_t* ghost_row;
+  double* const* peer_vec[3];   // x, phat, shat of every rank
+  long long* flags;             // posted by peers: "vector #seq is ready"
+  long long* const* peer_flags;
+  long long seq_base;
+};
+
+__global__ void k_zero_words(unsigned* p, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0u;
+}
+
+__global__ void k_mesh_reset(State* st) {
+  st->done = 0;
+  st->pub = 0;
+  st->cseq = 0;
+}
+
+// one thread: this rank's vector (the kernels before it in the stream) is
+// complete -- post the sequence number into every rank's flags
+__global__ void k_mesh_publish(State* st, MeshHalo h, const int* done) {
+  if (done && *done) return;
+  const long long seq = h.seq_base + (++st->pub);
+  __threadfence_system();
+  for (int q = 0; q < h.nranks; ++q) st_release_sys(h.peer_flags[q] + h.rank, seq);
+}
+// one CTA: wait until every neighbour posted the same vector (a separate
+// kernel, so waiting never holds more than one SM)
+__global__ void k_mesh_wait(const State* st, MeshHalo h, const int* done) {
+  if (done && *done) return;
+  const long long seq = h.seq_base + st->pub;
+  for (int k = threadIdx.x; k < h.nnbr; k += blockDim.x) {
+    const long long* f = h.flags + h.nbr[k];
+    while (ld_acquire_sys(f) < seq) __nanosleep(64);
+  }
+}
+// ghost rows of vector `which` (0 x, 1 phat, 2 shat) -> dst (after the owned rows)
+__global__ void k_mesh_pull(MeshHalo h, int which, int b, double* dst, const int* done) {
+  if (done && *done) return;
+  const long long total = (long long)h.nghost * b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long g = t / b;
+    const int c = (int)(t - g * b);
+    const double* src = h.peer_vec[which][h.ghost_owner[g]];
+    dst[t] = __ldcg(src + (long long)h.ghost_row[g] * b + c);
+  }
+}
+// all-reduce of a local partial array (or of a flag) into out[0]
+__global__ void k_mesh_scalar(State* st, MeshDev mesh, int slot, const double* parts, int np,
+                              const int* flag, double* out) {
+  __shared__ double red[8];
+  double v = 0.0;
+  if (parts) v = reduce_parts(parts, np, red);
+  if (threadIdx.x == 0) {
+    if (flag) v = *flag ? 1.0 : 0.0;
+    double unused = 0.0;
+    if (mesh.mbox) mesh_sum(mesh, mesh.seq_base + (++st->cseq), slot, v, unused);
+    out[0] = v;
   }
 }
 
@@ -256,13 +330,18 @@ using namespace b2s;
 
 extern "C" {
 
-static long long vec_doubles(int n, int b) {
-  long long m = (long long)n * b;
+static long long vec_doubles_g(int n, int nghost, int b) {
+  long long m = (long long)(n + nghost) * b;
   return (m + 31) / 32 * 32;  // 256-byte aligned sub-buffers
 }
 
+
 long long b2s_bicgstab_workspace_bytes(int n, int b, int nparts) {
-  const long long m = vec_doubles(n, b);
+  return b2s_bicgstab_workspace_bytes_mesh(n, 0, b, nparts);
+}
+
+long long b2s_bicgstab_workspace_bytes_mesh(int n, int nghost, int b, int nparts) {
+  const long long m = vec_doubles_g(n, nghost, b);
   // r rhat p v phat s shat t y x0  + 6 partial arrays (2 x nparts: the fused
   // 2-colour passes split a dot product over two kernels) + state + tickets
   return (10 * m + 6 * 2 * (long long)((nparts + 31) / 32 * 32)) * 8 + 256 + 64;
@@ -278,7 +357,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
        reinterpret_cast<uintptr_t>(a->work)) & 15)
     return B2S_SHAPE;
   const long long m = (long long)a->n * a->b;
-  const long long mv = vec_doubles(a->n, a->b);
+  const b2s_mesh* mesh = a->mesh;
+  const int nghost = mesh ? mesh->nghost : 0;
+  const long long mv = vec_doubles_g(a->n, nghost, a->b);
   const long long npv = 2 * ((a->nparts + 31) / 32 * 32);
   double* w = a->work;
   double *r = w, *rhat = w + mv, *p = w + 2 * mv, *v = w + 3 * mv, *phat = w + 4 * mv,
@@ -294,8 +375,34 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   const bool phased = ilu && !a->tiles && a->ngroups >= 2 && a->gslice_host;
   // 2 colours + colour-0 rows of A == [diag, U row] (b2s_fuse_check): the
   // backward pass of colour 0 and the SpMV rows of colour 0 share one read
-  const bool fused = phased && a->ngroups == 2 && a->fuse;
+  // (sharded: the SpMV needs the owners' ghost rows of p^ between the two)
+  const bool fused = phased && a->ngroups == 2 && a->fuse && !mesh;
   const int reset = (ilu && !phased) ? 1 : 0;  // sync-free sweeps need sentinel-filled outputs
+  MeshDev md{};
+  MeshHalo mh{};
+  if (mesh && !ilu) return B2S_UNSUPPORTED;   // sharded solves are block-Jacobi ILU0
+  if (mesh) {
+    if (mesh->nranks < 1 || mesh->rank < 0 || mesh->rank >= mesh->nranks || !mesh->mbox ||
+        !mesh->peer_mbox || !mesh->flags || !mesh->peer_flags)
+      return B2S_SHAPE;
+    md = MeshDev{mesh->rank, mesh->nranks, mesh->mbox, mesh->peer_mbox, mesh->seq_base};
+    mh.rank = mesh->rank; mh.nranks = mesh->nranks; mh.nghost = mesh->nghost;
+    mh.nnbr = mesh->nnbr; mh.nbr = mesh->nbr;
+    mh.ghost_owner = mesh->ghost_owner; mh.ghost_row = mesh->ghost_row;
+    mh.peer_vec[0] = mesh->peer_x; mh.peer_vec[1] = mesh->peer_phat;
+    mh.peer_vec[2] = mesh->peer_shat;
+    mh.flags = mesh->flags; mh.peer_flags = mesh->peer_flags; mh.seq_base = mesh->seq_base;
+  }
+  // publish this rank's vector, wait for the neighbours', pull the ghosts
+  auto halo = [&](cudaStream_t q, int which, double* vec, const int* dn) {
+    k_mesh_publish<<<1, 1, 0, q>>>(state, mh, dn);
+    k_mesh_wait<<<1, 32, 0, q>>>(state, mh, dn);
+    if (mh.nghost > 0) {
+      long long g = ((long long)mh.nghost * a->b + 255) / 256;
+      if (g > kSms * 2) g = kSms * 2;
+      k_mesh_pull<<<(int)g, 256, 0, q>>>(mh, which, a->b, vec + m, dn);
+    }
+  };
   const int np = a->nparts;
   SliceMap map{a->nslices, a->row0, a->nrows};
   Sell A{a->a_sp, a->a_cols, a->a_vals};
@@ -317,37 +424,42 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   }
 
   // ---- setup on the caller's stream: r0 = b - A x0, |r0|, r^ = r0, rho_0
-  // partials.  No host synchronisation here: the iteration graph is captured
-  // and instantiated while these kernels run, and the initial state is read
-  // back once, after the solve.
-  int rc = B2S_OK;
-  if (cudaMemsetAsync(tickets, 0, 64, user) != cudaSuccess) rc = B2S_CUDA_ERROR;
-  if (rc == B2S_OK) {
+  // partials.  Launched after the iteration graph is captured and
+  // instantiated (host work that may synchronise the device implicitly --
+  // sharded solves on one GPU must not do that while another shard's kernel
+  // waits for this one); the initial state is read back once, after the solve.
+  auto setup = [&]() -> int {
+    int rc = B2S_OK;
+    k_zero_words<<<1, 32, 0, user>>>(reinterpret_cast<unsigned*>(tickets), 16);
     k_copy<<<grid_v, 256, 0, user>>>(m, a->x, x0);
-    rc = launch_spmv(a->b, 3, np, map, A, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{}, user);
-  }
-  if (rc == B2S_OK) {
-    k_ctl_init<<<1, 256, 0, user>>>(state, prr, np, a->tol, a->maxit, dev_done);
-    k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
-    k_copy<<<grid_v, 256, 0, user>>>(m, r, v);  // v is only read for k > 0
-    if (ilu && !phased) {
-      rc = fill_sentinel(m, y, user);
-      if (!rc) rc = fill_sentinel(m, phat, user);
-      if (!rc) rc = fill_sentinel(m, shat, user);
+    if (mesh) {
+      // the readiness/mailbox sequences restart from seq_base: clear `done`
+      // and the counters the halo kernels read before k_ctl_init runs
+      k_mesh_reset<<<1, 1, 0, user>>>(state);
+      halo(user, 0, a->x, &state->done);
     }
-  }
-  if (rc == B2S_OK && cudaGetLastError() != cudaSuccess) rc = B2S_CUDA_ERROR;
-  if (rc != B2S_OK) {
-    cudaStreamSynchronize(user);
-    cudaFreeHost(host_done);
+    rc = launch_spmv(a->b, 3, np, map, A, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{}, user);
+    if (rc == B2S_OK) {
+      k_ctl_init<<<1, 256, 0, user>>>(state, prr, np, a->tol, a->maxit, dev_done, md);
+      k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
+      k_copy<<<grid_v, 256, 0, user>>>(m, r, v);  // v is only read for k > 0
+      if (ilu && !phased) {
+        rc = fill_sentinel(m, y, user);
+        if (!rc) rc = fill_sentinel(m, phat, user);
+        if (!rc) rc = fill_sentinel(m, shat, user);
+      }
+    }
+    if (rc == B2S_OK && cudaGetLastError() != cudaSuccess) rc = B2S_CUDA_ERROR;
     return rc;
-  }
+  };
+  auto peer_barrier = [&]() {
+    if (mesh && mesh->host_barrier) mesh->host_barrier(mesh->host_barrier_ctx);
+  };
   State hs;
 
   // ---- capture one iteration
   cudaStream_t cs;
   if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
-    cudaStreamSynchronize(user);
     cudaFreeHost(host_done);
     return B2S_CUDA_ERROR;
   }
@@ -362,7 +474,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     // programmatic dependent launch between the iteration's kernels
     // (B2S_PDL=0 turns it off)
     const char* pdl_env = getenv("B2S_PDL");
-    const bool pdl = !(pdl_env && pdl_env[0] == '0');
+    // (shards sharing one GPU: a programmatically launched kernel would hold
+    // SMs while its predecessor's last CTA waits for another shard)
+    const bool pdl = !(pdl_env && pdl_env[0] == '0') && !(mesh && mesh->shared_device);
     double* ph = ilu ? phat : p;
     double* sh = ilu ? shat : s;
     launch_k(k_p_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
@@ -377,7 +491,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
                       done, &g0, cs, pdl);
       launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
-                        done, Ctl{state, counters + 0, dev_done, kCtlAlpha}, cs, pdl);
+                        done, Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl);
       kernels += 3;
     } else if (phased) {
       launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
@@ -390,13 +504,14 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                          tickets, done, cs);
       kernels += 2;
     }
+    if (mesh) { halo(cs, 1, ph, done); kernels += mh.nghost > 0 ? 3 : 2; }
     if (!fused) {
       launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done,
-                  Ctl{state, counters + 0, dev_done, kCtlAlpha}, cs, pdl); ++kernels;
+                  Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl); ++kernels;
     }
     launch_k(k_s_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
              (const double*)r, (const double*)v, ph, a->x, s, pss, reset,
-             Ctl{state, counters + 1, dev_done, kCtlS});
+             Ctl{state, counters + 1, dev_done, kCtlS, md});
     ++kernels;
     if (fused) {
       launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, s, y,
@@ -405,7 +520,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, s, shat, t, s, ptt, pts, done,
                       &g0, cs, pdl);
       launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
-                        Ctl{state, counters + 2, dev_done, kCtlOmega}, cs, pdl);
+                        Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl);
       kernels += 3;
     } else if (phased) {
       launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
@@ -418,16 +533,19 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                          tickets, done, cs);
       kernels += 2;
     }
+    if (mesh) { halo(cs, 2, sh, done); kernels += mh.nghost > 0 ? 3 : 2; }
     if (!fused) {
       launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done,
-                  Ctl{state, counters + 2, dev_done, kCtlOmega}, cs, pdl); ++kernels;
+                  Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl); ++kernels;
     }
     launch_k(k_r_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state, sh,
              (const double*)t, (const double*)s, (const double*)rhat, a->x, r, prr, prho, reset,
-             Ctl{state, counters + 3, dev_done, kCtlEndBegin});
+             Ctl{state, counters + 3, dev_done, kCtlEndBegin, md});
     ++kernels;
     if (cudaStreamEndCapture(cs, &graph) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
     if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
+    peer_barrier();   // every shard is past its host-side preparation
+    if ((status = setup()) != B2S_OK) { cudaStreamSynchronize(user); break; }
     // order the graph after the setup work on the caller's stream
     cudaEvent_t ev;
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
@@ -458,6 +576,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     cudaEventDestroy(fin);
     if (cudaStreamSynchronize(cs) != cudaSuccess) status = B2S_CUDA_ERROR;
     for (int q = 0; q < 8; ++q) cudaEventDestroy(ring[q]);
+    peer_barrier();   // no shard tears down while another still runs
   } while (0);
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
@@ -484,23 +603,78 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   }
   // not converged: true residual of the current x, then x0 if x is not finite
   // (bs/krylov.py:242-244)
-  rc = launch_spmv(a->b, 3, np, map, A, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user);
+  // (sharded: x's ghost rows first, and both results all-reduced, so every
+  // rank reports the global norm and restores x0 together)
+  if (mesh) halo(user, 0, a->x, nullptr);
+  int rc = launch_spmv(a->b, 3, np, map, A, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user);
   if (rc) return rc;
-  k_reduce_parts<<<1, 256, 0, user>>>(pg, np, pss);
+  if (mesh) k_mesh_scalar<<<1, 256, 0, user>>>(state, md, kSlotFinal, pg, np, nullptr, pss);
+  else k_reduce_parts<<<1, 256, 0, user>>>(pg, np, pss);
   int* bad = reinterpret_cast<int*>(ptt);
-  B2S_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), user));
+  k_zero_words<<<1, 32, 0, user>>>(reinterpret_cast<unsigned*>(bad), 1);
   k_all_finite<<<grid_v, 256, 0, user>>>(m, a->x, bad);
+  if (mesh) k_mesh_scalar<<<1, 256, 0, user>>>(state, md, kSlotFinite, nullptr, 0, bad, pts);
   B2S_LAUNCH_CHECK();
-  double fin2 = 0.0;
+  double fin2 = 0.0, gbad = 0.0;
   int hbad = 0;
   B2S_CHECK(cudaMemcpyAsync(&fin2, pss, sizeof(double), cudaMemcpyDeviceToHost, user));
   B2S_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, user));
+  if (mesh) B2S_CHECK(cudaMemcpyAsync(&gbad, pts, sizeof(double), cudaMemcpyDeviceToHost, user));
   B2S_CHECK(cudaStreamSynchronize(user));
   res->final_norm = sqrt(fin2);
+  if (mesh) hbad = gbad != 0.0;
   if (hbad) {
     k_copy<<<grid_v, 256, 0, user>>>(m, x0, a->x);
     B2S_LAUNCH_CHECK();
   }
+  return B2S_OK;
+}
+
+long long b2s_mesh_mbox_bytes(int nranks) {
+  return nranks < 1 ? 0 : (long long)kMboxSlots * nranks * 4 * 8;
+}
+
+int b2s_bicgstab_workspace_layout(int n, int nghost, int b, long long* phat_off,
+                                  long long* shat_off) {
+  if (n < 0 || nghost < 0 || b < 1) return B2S_SHAPE;
+  const long long mv = vec_doubles_g(n, nghost, b);
+  *phat_off = 4 * mv;
+  *shat_off = 6 * mv;
+  return B2S_OK;
+}
+
+int b2s_ipc_handle(const void* ptr, unsigned char* handle64, long long* offset) {
+  // the allocation's base through the driver entry point (no libcuda link
+  // dependency: the library must load on hosts without a driver)
+  using range_fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fp)
+    return B2S_CUDA_ERROR;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<range_fn>(fp)(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) !=
+      CUDA_SUCCESS)
+    return B2S_CUDA_ERROR;
+  cudaIpcMemHandle_t h;
+  B2S_CHECK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(handle64, &h, sizeof(h));
+  *offset = (long long)(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return B2S_OK;
+}
+
+int b2s_ipc_open(const unsigned char* handle64, long long offset, void** ptr_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  B2S_CHECK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr_out = static_cast<char*>(base) + offset;
+  return B2S_OK;
+}
+
+int b2s_ipc_close(void* base) {
+  B2S_CHECK(cudaIpcCloseMemHandle(base));
   return B2S_OK;
 }
 

@@ -22,6 +22,7 @@ partitioned solver be checked against the oracle on a single GPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass
 
@@ -478,3 +479,216 @@ def nccl_solver(spec: GeneratorSpec, backend=Backend.LEVEL_SCHEDULED):
         return out
     exchange_requests([shard], world, gather)
     return [shard], NcclComm(shard)
+
+
+# ---------------------------------------------------------------------------
+# peer-memory solver: the device-resident BiCGStab loop of the single-GPU
+# path (b2s_bicgstab, one CUDA graph per iteration) on every shard, with the
+# communication done by the kernels themselves (csrc/krylov.cu, b2s_mesh):
+# ghost rows are read straight out of the owning shard's vector, and the
+# partial dot products are all-reduced through per-rank mailboxes in the
+# last CTA of each reducing kernel.  No host round trip per iteration.  The
+# peers are other processes' buffers opened through CUDA IPC (NVLink P2P on
+# one node), or other shards on the same GPU (tests) -- the kernels are the
+# same either way.
+
+class MeshState:
+    """Device buffers of one shard for ``b2s_bicgstab`` with a ``b2s_mesh``."""
+
+    def __init__(self, shard: "Shard", nranks: int):
+        lib = D.lib()
+        R, G, b, dev = shard.R, shard.G, shard.b, shard.dev
+        nbytes = int(lib.b2s_bicgstab_workspace_bytes_mesh(R, G, b, D.NPARTS))
+        self.work = torch.zeros(nbytes // 8 + 1, dtype=torch.float64, device=dev)
+        self.x = torch.zeros((R + G) * b + 2, dtype=torch.float64, device=dev)
+        self.flags = torch.zeros(max(nranks, 1), dtype=torch.int64, device=dev)
+        self.mbox = torch.zeros(int(lib.b2s_mesh_mbox_bytes(nranks)) // 8, dtype=torch.float64,
+                                device=dev)
+        po, so = C.c_longlong(0), C.c_longlong(0)
+        check(lib.b2s_bicgstab_workspace_layout(R, G, b, C.byref(po), C.byref(so)), "layout")
+        self.phat = self.work.data_ptr() + 8 * po.value
+        self.shat = self.work.data_ptr() + 8 * so.value
+        self.nranks = nranks
+        self.solves = 0
+        self.peers = None         # per rank: [x, phat, shat, flags, mbox] addresses here
+        self.opened = []          # IPC bases to close
+
+    def local_ptrs(self):
+        return [self.x.data_ptr(), self.phat, self.shat, self.flags.data_ptr(),
+                self.mbox.data_ptr()]
+
+    def close(self):
+        for base in self.opened:
+            D.lib().b2s_ipc_close(C.c_void_p(base))
+        self.opened = []
+
+
+def _mesh_struct(shard: "Shard", ms: MeshState, owner_rows: dict, shared_device: bool):
+    """The ``_lib.Mesh`` of one shard (and the device arrays it points to)."""
+    from ._lib import Mesh
+    dev = shard.dev
+    G = shard.G
+    owner = np.zeros(max(G, 1), dtype=np.int32)
+    row = np.zeros(max(G, 1), dtype=np.int32)
+    for h, idx in shard.recv.items():
+        owner[idx] = h
+        row[idx] = np.asarray(owner_rows[h], dtype=np.int32)
+    nbr = np.array(sorted(shard.recv) or [0], dtype=np.int32)
+    keep = {"owner": torch.from_numpy(owner).to(dev), "row": torch.from_numpy(row).to(dev),
+            "nbr": torch.from_numpy(nbr).to(dev)}
+    for k, name in enumerate(("x", "phat", "shat", "flags", "mbox")):
+        keep[name] = torch.tensor([p[k] for p in ms.peers], dtype=torch.int64, device=dev)
+    m = Mesh()
+    m.rank, m.nranks, m.nghost = shard.slab.rank, ms.nranks, G
+    m.ghost_owner, m.ghost_row = D.ptr(keep["owner"]), D.ptr(keep["row"])
+    m.nnbr, m.nbr = len(shard.recv), D.ptr(keep["nbr"])
+    m.peer_x, m.peer_phat, m.peer_shat = (D.ptr(keep["x"]), D.ptr(keep["phat"]),
+                                          D.ptr(keep["shat"]))
+    m.flags, m.peer_flags = ms.flags.data_ptr(), D.ptr(keep["flags"])
+    m.mbox, m.peer_mbox = ms.mbox.data_ptr(), D.ptr(keep["mbox"])
+    ms.solves += 1
+    m.seq_base = ms.solves << 32          # equal on every rank: one per global solve
+    m.shared_device = 1 if shared_device else 0
+    return m, keep
+
+
+def _mesh_prepare(shard: "Shard", nranks: int, x0=None):
+    """Plan-order rhs and x0 of a shard (x0 into the mesh x buffer)."""
+    if getattr(shard, "mesh", None) is None or shard.mesh.nranks != nranks or \
+            shard.mesh.x.numel() != (shard.R + shard.G) * shard.b + 2:
+        shard.mesh = MeshState(shard, nranks)
+    ms = shard.mesh
+    iperm = shard.plan.device("inverse_permutation")
+    # the right-hand side is resident like the matrix (uploaded once per shard)
+    rhs = getattr(shard, "rhs_d", None)
+    if rhs is None:
+        rhs = shard.rhs_d = D.f64(shard.slab.rhs, shard.dev)
+    shard.rhs_p = D.gather_rows(rhs, iperm, shard.R, shard.b)
+    x = D.f64(x0, shard.dev) if x0 is not None else torch.zeros_like(rhs)
+    ms.x.zero_()
+    ms.x[: shard.R * shard.b] = D.gather_rows(x, iperm, shard.R, shard.b)
+    return ms
+
+
+def _mesh_report(res, t0, groups) -> SolveReport:
+    from .bridge import _report
+    return _report(res, time.perf_counter() - t0, groups)
+
+
+def _mesh_outputs(shards):
+    return [D.gather_rows(s.mesh.x[: s.R * s.b], s.plan.device("permutation"), s.R, s.b)
+            for s in shards]
+
+
+def solve_shards_mesh(shards, stop: StoppingCriteria, x0=None):
+    """All shards of this process on one GPU, each running the device loop on
+    its own stream and host thread, communicating through peer memory.
+    Returns (report, per-shard x in input order) like ``solve_shards``."""
+    import threading
+
+    from .krylov import DeviceKrylov
+    N = len(shards)
+    by_rank = {s.slab.rank: s for s in shards}
+    mss = [_mesh_prepare(s, N, None if x0 is None else x0[i]) for i, s in enumerate(shards)]
+    ptrs = [by_rank[r].mesh.local_ptrs() for r in range(N)]
+    # the shards' host threads rendezvous around the device loop (b2s_mesh
+    # host_barrier): on one GPU, no shard may make an implicitly
+    # synchronising call while another shard's kernel waits for it
+    from ._lib import BARRIER_FN
+    rendezvous = threading.Barrier(N)
+    barrier_cb = BARRIER_FN(lambda _ctx: rendezvous.wait())
+    jobs = []
+    for s, ms in zip(shards, mss):
+        ms.peers = ptrs
+        me = s.slab.rank
+        owner_rows = {h: by_rank[h].send[me].cpu().numpy() for h in s.recv}
+        mesh, keep = _mesh_struct(s, ms, owner_rows, shared_device=True)
+        mesh.host_barrier = C.cast(barrier_cb, C.c_void_p)
+        keep["barrier"] = barrier_cb
+        kr = DeviceKrylov(s.R, s.b, s.smap, s.sell, s.fact, ms.work, False)
+        jobs.append((s, ms, kr, mesh, keep))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    results, errors = [None] * N, []
+
+    def run(i):
+        s, ms, kr, mesh, _ = jobs[i]
+        try:
+            st = torch.cuda.Stream(device=s.dev)
+            with torch.cuda.stream(st):
+                results[i] = kr.solve(s.rhs_p, ms.x, stop, mesh=mesh)
+                st.synchronize()
+        except Exception as exc:   # surfaced below, after every thread is back
+            errors.append(exc)
+            rendezvous.abort()
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(N)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+    rep = _mesh_report(results[0], t0, shards[0].plan.group_count)
+    for r in results[1:]:
+        assert r.iterations == results[0].iterations and r.converged == results[0].converged
+    return rep, _mesh_outputs(shards)
+
+
+def solve_shard_mesh_dist(shard: "Shard", stop: StoppingCriteria, x0=None, cache_key=None):
+    """This process's shard of a torch.distributed job (one GPU per rank):
+    peers' buffers are opened once through CUDA IPC (NVLink P2P)."""
+    import torch.distributed as dist
+
+    from .krylov import DeviceKrylov
+    rank, world = dist.get_rank(), dist.get_world_size()
+    tm = [time.perf_counter()]
+    dist.barrier()       # every peer is done reading this rank's x of the last solve
+    tm.append(time.perf_counter())
+    ms = _mesh_prepare(shard, world, x0)
+
+    def gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+    lib = D.lib()
+    if ms.peers is None:
+        mine = []
+        for p in ms.local_ptrs():
+            h = (C.c_ubyte * 64)()
+            off = C.c_longlong(0)
+            check(lib.b2s_ipc_handle(C.c_void_p(p), h, C.byref(off)), "ipc_handle")
+            mine.append((bytes(h), off.value))
+        peers = [None] * world
+        for r, hs in gather((rank, mine)):
+            if r == rank:
+                peers[r] = ms.local_ptrs()
+                continue
+            opened = []
+            for hb, off in hs:
+                out = C.c_void_p(None)
+                buf = (C.c_ubyte * 64).from_buffer_copy(hb)
+                check(lib.b2s_ipc_open(buf, off, C.byref(out)), "ipc_open")
+                opened.append(out.value)
+                ms.opened.append(out.value - off)
+            peers[r] = opened
+        ms.peers = peers
+    key = ("owner_rows", cache_key)
+    if getattr(shard, "_owner_rows_key", None) != key:
+        sends = {h: rows.cpu().numpy() for h, rows in shard.send.items()}
+        everyone = gather((rank, sends))
+        shard._owner_rows = {r: d[rank] for r, d in everyone if rank in d}
+        shard._owner_rows_key = key
+    mesh, keep = _mesh_struct(shard, ms, shard._owner_rows, shared_device=False)
+    kr = DeviceKrylov(shard.R, shard.b, shard.smap, shard.sell, shard.fact, ms.work, False)
+    t0 = time.perf_counter()
+    tm.append(t0)
+    res = kr.solve(shard.rhs_p, ms.x, stop, mesh=mesh)
+    tm.append(time.perf_counter())
+    rep = _mesh_report(res, t0, shard.plan.group_count)
+    out = _mesh_outputs([shard])[0]
+    if os.environ.get("B2S_MESH_TIMING") == "1":
+        torch.cuda.synchronize()
+        tm.append(time.perf_counter())
+        print("mesh timing ms (barrier, prepare, solve, outputs):",
+              [round((b - a) * 1e3, 3) for a, b in zip(tm, tm[1:])], flush=True)
+    return rep, out

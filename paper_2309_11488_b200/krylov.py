@@ -224,8 +224,10 @@ class DeviceKrylov:
         return cls(n, b, smap, sell, fact, work, fuse)
 
     def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
-              check_lag: int = 2) -> BicgResult:
-        """Solve in place on plan-order device vectors (x: x0 in, x out)."""
+              check_lag: int = 2, mesh=None) -> BicgResult:
+        """Solve in place on plan-order device vectors (x: x0 in, x out).
+        ``mesh``: a ``_lib.Mesh`` for one shard of a partitioned solve (x then
+        carries the ghost rows after the owned ones; distributed.py)."""
         f = self.fact
         args = BicgArgs()
         args.n, args.b, args.nparts = self.n, self.b, D.NPARTS
@@ -254,6 +256,8 @@ class DeviceKrylov:
                 args.fuse = 1 if self.fuse else 0
         args.rhs, args.x, args.work = D.ptr(rhs), D.ptr(x), D.ptr(self.work)
         args.stream = D.stream()
+        if mesh is not None:
+            args.mesh = C.addressof(mesh)
         res = BicgResult()
         check(D.lib().b2s_bicgstab(C.byref(args), C.byref(res)), "bicgstab")
         return res

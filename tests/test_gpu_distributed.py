@@ -52,3 +52,76 @@ def test_one_shard_equals_single_gpu_solver():
                                    b.a, b.rhs)
     assert rep.iterations == r1.iterations
     assert np.linalg.norm(xs[0].cpu().numpy() - x1.data) <= 1e-10 * np.linalg.norm(x1.data)
+
+
+@pytest.mark.parametrize("dims,world,backend",
+                         [((8, 7, 12), 2, "level"), ((6, 6, 9), 3, "color"),
+                          ((10, 8, 8), 4, "level"), ((12, 10, 16), 4, "color")])
+def test_mesh_solve_matches_partitioned_oracle(dims, world, backend):
+    """The peer-memory device loop (csrc/krylov.cu b2s_mesh: ghost rows read
+    from the owners' vectors, mailbox all-reduce in the control CTA), all
+    shards on one GPU, each on its own stream and host thread."""
+    from paper_2309_11488_b200.distributed import solve_shards_mesh
+    spec = P.GeneratorSpec(*dims, seed=5, diagonal_boost=1e-2)
+    tol = 1e-8
+    be = P.Backend.from_name(backend)
+    shards, comm = local_solver(spec, world, be)
+    rep_h, xs_h = solve_shards(shards, comm, P.StoppingCriteria(tol, 200))
+    rep, xs = solve_shards_mesh(shards, P.StoppingCriteria(tol, 200))
+    x = np.concatenate([v.cpu().numpy() for v in xs])
+    xh = np.concatenate([v.cpu().numpy() for v in xs_h])
+    assert rep.converged and rep_h.converged
+    assert abs(rep.iterations - rep_h.iterations) <= 1.0, (rep.iterations, rep_h.iterations)
+    np.testing.assert_allclose(rep.initial_norm, rep_h.initial_norm, rtol=1e-12)
+    assert np.linalg.norm(x - xh) <= 1e-6 * np.linalg.norm(xh)
+    if backend == "level":
+        xo, ro = oracle_partitioned(spec, world, tol)
+        assert abs(rep.iterations - ro.iterations) <= 1.0, (rep.iterations, ro.iterations)
+        assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
+    # a second solve on the same buffers (sequence numbers move on)
+    rep2, xs2 = solve_shards_mesh(shards, P.StoppingCriteria(tol, 200))
+    assert rep2.iterations == rep.iterations
+    assert np.array_equal(np.concatenate([v.cpu().numpy() for v in xs2]), x)
+
+
+def test_mesh_one_shard_equals_single_gpu_solver():
+    from paper_2309_11488_b200.distributed import solve_shards_mesh
+    spec = P.GeneratorSpec(9, 8, 7, seed=2)
+    shards, _ = local_solver(spec, 1)
+    rep, xs = solve_shards_mesh(shards, P.StoppingCriteria(1e-8, 200))
+    b = P.generate(spec)
+    x1, r1 = P.solve_with_fallback(P.SolverConfig(stop=P.StoppingCriteria(1e-8, 200)),
+                                   b.a, b.rhs)
+    assert rep.iterations == r1.iterations
+    assert np.linalg.norm(xs[0].cpu().numpy() - x1.data) <= 1e-10 * np.linalg.norm(x1.data)
+
+
+def test_mesh_two_processes_over_ipc(tmp_path):
+    """Two processes, one shard each, peer buffers opened through CUDA IPC
+    (the multi-GPU path of bench.py; both ranks on cuda:0 here)."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    from paper_2309_11488_b200.distributed import solve_shards_mesh
+    dims, world = (8, 7, 12), 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(root / "tests" / "workers" / "mesh_worker.py"), "8,7,12", "level", "--same-gpu"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1]
+    got = json.loads(line)
+    spec = P.GeneratorSpec(*dims, seed=5, diagonal_boost=1e-2)
+    shards, _ = local_solver(spec, world, P.Backend.LEVEL_SCHEDULED)
+    rep, xs = solve_shards_mesh(shards, P.StoppingCriteria(1e-8, 200))
+    x = np.concatenate([v.cpu().numpy() for v in xs])
+    assert all(got["converged"]) and got["rerun_bit_equal"]
+    assert got["iterations"][0] == rep.iterations
+    assert np.array_equal(np.asarray(got["x"]), x)   # same kernels, same sums: same bits
