@@ -162,6 +162,8 @@ __global__ void k_mesh_scalar(State* st, MeshDev mesh, int slot, const double* p
 // vectors (workspace sub-buffers are 256-byte aligned; torch allocations
 // 512-byte).  The per-thread accumulation order is fixed by (m, grid), so
 // the partial sums are deterministic.
+constexpr int kU = 2;   // element pairs in flight per thread in the vector passes
+
 __device__ __forceinline__ double2 ld2(const double* p, long long j) {
   return __ldcs(reinterpret_cast<const double2*>(p) + j);
 }
@@ -169,7 +171,7 @@ __device__ __forceinline__ void st2(double* p, long long j, double a, double b) 
   reinterpret_cast<double2*>(p)[j] = make_double2(a, b);
 }
 
-__global__ void __launch_bounds__(256) k_p_update(long long m, const State* st,
+__global__ void __launch_bounds__(256, 4) k_p_update(long long m, const State* st,
                                                   const double* __restrict__ r,
                                                   const double* __restrict__ v, double* p) {
   griddep_wait();
@@ -187,16 +189,20 @@ __global__ void __launch_bounds__(256) k_p_update(long long m, const State* st,
     if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[m - 1] = r[m - 1];
     return;
   }
-  for (; j + T < m2; j += 2 * T) {
-    const double2 r0 = ld2(r, j), r1 = ld2(r, j + T);
-    const double2 p0 = ld2(p, j), p1 = ld2(p, j + T);
-    const double2 v0 = ld2(v, j), v1 = ld2(v, j + T);
-    st2(p, j, r0.x + beta * (p0.x - omega * v0.x), r0.y + beta * (p0.y - omega * v0.y));
-    st2(p, j + T, r1.x + beta * (p1.x - omega * v1.x), r1.y + beta * (p1.y - omega * v1.y));
-  }
-  if (j < m2) {
-    const double2 r0 = ld2(r, j), p0 = ld2(p, j), v0 = ld2(v, j);
-    st2(p, j, r0.x + beta * (p0.x - omega * v0.x), r0.y + beta * (p0.y - omega * v0.y));
+  for (; j < m2; j += kU * T) {
+    double2 rr[kU], pp[kU], vv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long q = j + u * T;
+      if (q < m2) { rr[u] = ld2(r, q); pp[u] = ld2(p, q); vv[u] = ld2(v, q); }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long q = j + u * T;
+      if (q < m2)
+        st2(p, q, rr[u].x + beta * (pp[u].x - omega * vv[u].x),
+            rr[u].y + beta * (pp[u].y - omega * vv[u].y));
+    }
   }
   if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0)
     p[m - 1] = r[m - 1] + beta * (p[m - 1] - omega * v[m - 1]);
@@ -210,7 +216,7 @@ __device__ __forceinline__ void s_elem(double rv, double vv, double ph, double& 
   acc = fma(so, so, acc);
 }
 
-__global__ void __launch_bounds__(256) k_s_update(long long m, const State* st,
+__global__ void __launch_bounds__(256, 4) k_s_update(long long m, const State* st,
                                                   const double* __restrict__ r,
                                                   const double* __restrict__ v, double* phat,
                                                   double* __restrict__ x,
@@ -224,15 +230,30 @@ __global__ void __launch_bounds__(256) k_s_update(long long m, const State* st,
   double acc = 0.0;
   const long long m2 = m >> 1, T = (long long)gridDim.x * blockDim.x;
   long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; j < m2; j += T) {
-    const double2 rv = ld2(r, j), vv = ld2(v, j), ph = ld2(phat, j);
-    double2 xv = reinterpret_cast<const double2*>(x)[j];
-    double s0, s1;
-    s_elem(rv.x, vv.x, ph.x, xv.x, s0, alpha, acc);
-    s_elem(rv.y, vv.y, ph.y, xv.y, s1, alpha, acc);
-    st2(s, j, s0, s1);
-    st2(x, j, xv.x, xv.y);
-    if (reset) st2(phat, j, sentinel(), sentinel());
+  // kU pairs per thread in flight (every load issued before any store), in
+  // the same per-thread order j, j+T, j+2T, ... as a plain grid-stride loop
+  for (; j < m2; j += kU * T) {
+    double2 rv[kU], vv[kU], ph[kU], xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long q = j + u * T;
+      if (q < m2) {
+        rv[u] = ld2(r, q); vv[u] = ld2(v, q); ph[u] = ld2(phat, q);
+        xv[u] = reinterpret_cast<const double2*>(x)[q];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long q = j + u * T;
+      if (q < m2) {
+        double s0, s1;
+        s_elem(rv[u].x, vv[u].x, ph[u].x, xv[u].x, s0, alpha, acc);
+        s_elem(rv[u].y, vv[u].y, ph[u].y, xv[u].y, s1, alpha, acc);
+        st2(s, q, s0, s1);
+        st2(x, q, xv[u].x, xv[u].y);
+        if (reset) st2(phat, q, sentinel(), sentinel());
+      }
+    }
   }
   if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     double s0;
@@ -254,7 +275,7 @@ __device__ __forceinline__ void r_elem(double sh, double tv, double sv, double r
   a1 = fma(rh, ro, a1);
 }
 
-__global__ void __launch_bounds__(256) k_r_update(long long m, const State* st, double* shat,
+__global__ void __launch_bounds__(256, 4) k_r_update(long long m, const State* st, double* shat,
                                                   const double* __restrict__ tv,
                                                   const double* __restrict__ s,
                                                   const double* __restrict__ rhat,
@@ -269,15 +290,28 @@ __global__ void __launch_bounds__(256) k_r_update(long long m, const State* st, 
   double a0 = 0.0, a1 = 0.0;
   const long long m2 = m >> 1, T = (long long)gridDim.x * blockDim.x;
   long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; j < m2; j += T) {
-    const double2 sh = ld2(shat, j), t2 = ld2(tv, j), sv = ld2(s, j), rh = ld2(rhat, j);
-    double2 xv = reinterpret_cast<const double2*>(x)[j];
-    double r0, r1;
-    r_elem(sh.x, t2.x, sv.x, rh.x, xv.x, r0, omega, a0, a1);
-    r_elem(sh.y, t2.y, sv.y, rh.y, xv.y, r1, omega, a0, a1);
-    st2(x, j, xv.x, xv.y);
-    st2(r, j, r0, r1);
-    if (reset) st2(shat, j, sentinel(), sentinel());
+  for (; j < m2; j += kU * T) {
+    double2 sh[kU], t2[kU], sv[kU], rh[kU], xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long q = j + u * T;
+      if (q < m2) {
+        sh[u] = ld2(shat, q); t2[u] = ld2(tv, q); sv[u] = ld2(s, q); rh[u] = ld2(rhat, q);
+        xv[u] = reinterpret_cast<const double2*>(x)[q];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long q = j + u * T;
+      if (q < m2) {
+        double r0, r1;
+        r_elem(sh[u].x, t2[u].x, sv[u].x, rh[u].x, xv[u].x, r0, omega, a0, a1);
+        r_elem(sh[u].y, t2[u].y, sv[u].y, rh[u].y, xv[u].y, r1, omega, a0, a1);
+        st2(x, q, xv[u].x, xv[u].y);
+        st2(r, q, r0, r1);
+        if (reset) st2(shat, q, sentinel(), sentinel());
+      }
+    }
   }
   if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     double r0;
@@ -544,13 +578,17 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     ++kernels;
     if (cudaStreamEndCapture(cs, &graph) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
     if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
+    // shards sharing one GPU replay on their own (caller's) stream: every
+    // extra stream risks sharing a hardware work queue with a peer's stream,
+    // i.e. a false dependency behind a kernel that waits for that very peer
+    cudaStream_t rs = (mesh && mesh->shared_device) ? user : cs;
     peer_barrier();   // every shard is past its host-side preparation
     if ((status = setup()) != B2S_OK) { cudaStreamSynchronize(user); break; }
     // order the graph after the setup work on the caller's stream
     cudaEvent_t ev;
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
     cudaEventRecord(ev, user);
-    cudaStreamWaitEvent(cs, ev, 0);
+    cudaStreamWaitEvent(rs, ev, 0);
     cudaEventDestroy(ev);
     // ---- replay: the host stays `lag` iterations behind the device
     const int lag = a->check_lag > 0 ? a->check_lag : 2;
@@ -559,8 +597,8 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     for (int q = 0; q < 8; ++q) cudaEventCreateWithFlags(&ring[q], cudaEventDisableTiming);
     int launched = 0;
     for (int it = 0; it < total; ++it) {
-      if (cudaGraphLaunch(exec, cs) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
-      cudaEventRecord(ring[it & 7], cs);
+      if (cudaGraphLaunch(exec, rs) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
+      cudaEventRecord(ring[it & 7], rs);
       ++launched;
       if (it >= lag) {
         cudaEventSynchronize(ring[(it - lag) & 7]);
@@ -571,10 +609,10 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     // leave the caller's stream ordered after the solve
     cudaEvent_t fin;
     cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
-    cudaEventRecord(fin, cs);
+    cudaEventRecord(fin, rs);
     cudaStreamWaitEvent(user, fin, 0);
     cudaEventDestroy(fin);
-    if (cudaStreamSynchronize(cs) != cudaSuccess) status = B2S_CUDA_ERROR;
+    if (cudaStreamSynchronize(rs) != cudaSuccess) status = B2S_CUDA_ERROR;
     for (int q = 0; q < 8; ++q) cudaEventDestroy(ring[q]);
     peer_barrier();   // no shard tears down while another still runs
   } while (0);

@@ -583,7 +583,10 @@ def _mesh_outputs(shards):
 def solve_shards_mesh(shards, stop: StoppingCriteria, x0=None):
     """All shards of this process on one GPU, each running the device loop on
     its own stream and host thread, communicating through peer memory.
-    Returns (report, per-shard x in input order) like ``solve_shards``."""
+    Returns (report, per-shard x in input order) like ``solve_shards``.
+    The shards' kernels wait for each other, so every shard's stream needs its
+    own hardware work queue: run with CUDA_DEVICE_MAX_CONNECTIONS >= shards + a
+    few (tests/conftest.py sets 32)."""
     import threading
 
     from .krylov import DeviceKrylov
@@ -614,7 +617,9 @@ def solve_shards_mesh(shards, stop: StoppingCriteria, x0=None):
     def run(i):
         s, ms, kr, mesh, _ = jobs[i]
         try:
-            st = torch.cuda.Stream(device=s.dev)
+            st = getattr(s, "_mesh_stream", None)
+            if st is None:   # one persistent stream per shard (see b2s_mesh shared_device)
+                st = s._mesh_stream = torch.cuda.Stream(device=s.dev)
             with torch.cuda.stream(st):
                 results[i] = kr.solve(s.rhs_p, ms.x, stop, mesh=mesh)
                 st.synchronize()

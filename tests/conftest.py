@@ -1,5 +1,11 @@
+import os
 import sys
 from pathlib import Path
+
+# Sharded solves on one GPU (tests/test_gpu_distributed.py) run one stream per
+# shard whose kernels wait on each other; every stream needs its own hardware
+# work queue (default 8 per process), so ask for the maximum before CUDA starts.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import numpy as np
 import pytest

@@ -6,7 +6,9 @@ partition -> decompose(level plan) -> bicgstab(full operator)."""
 import numpy as np
 import pytest
 
-pytestmark = pytest.mark.gpu
+# (a hard per-test limit: a cross-shard wait that never resolves must fail the
+# test, not hang the suite)
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300, method="thread")]
 
 import paper_2309_11488_b200 as P  # noqa: E402
 from oracle import port as O  # noqa: E402

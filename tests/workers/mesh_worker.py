@@ -8,6 +8,8 @@ path on a one-GPU box.  Rank 0 prints one JSON line.
 import json
 import os
 import sys
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[2]
