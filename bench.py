@@ -189,7 +189,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from bench_dist import run_distributed
         return run_distributed(args, world, rank, local, METRIC, UNIT, Clocks, peaks,
-                               cpu_port_sample)
+                               cpu_port_sample, count_step_kernels)
     run_single(args)
 
 

@@ -22,7 +22,48 @@ import torch
 import torch.distributed as dist
 
 
-def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_port_sample):
+def kernel_roofline(shard, peaks):
+    """Dominant kernels of the shard's iteration (SpMV over the owned rows with
+    ghost columns, ILU0 application), CUDA-event timed on this rank, against
+    SURVEY §8(d)'s algorithmic bytes for the shard (bench.py's formulas)."""
+    from paper_2309_11488_b200 import _device as D
+    n, b = shard.R, shard.b
+    nnz = int(shard.slab.rp[-1])
+    nloc = int(shard.pmat.pattern.num_blocks)
+    m = n * b
+    st = torch.cuda.current_stream()
+    x = torch.rand((n + shard.G) * b, dtype=torch.float64, device=shard.dev)
+    y = torch.empty(m, dtype=torch.float64, device=shard.dev)
+    z = torch.empty(m, dtype=torch.float64, device=shard.dev)
+    parts = torch.empty(D.NPARTS, dtype=torch.float64, device=shard.dev)
+
+    def timed(fn, reps=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e3
+    t_spmv = timed(lambda: D.spmv(shard.smap, shard.sell, b, x, y, 1, x, parts))
+    t_apply = timed(lambda: shard.fact.apply_device(x[:m], z))
+    spmv_bytes = nnz * 76 + (n + 1) * 4 + 48 * n
+    apply_bytes = (nloc - n) * 76 + 72 * n + 8 * (n + 1) + \
+        (48 if shard.plan.group_count == 2 else 96) * n
+    hbm, kind = peaks()
+    dom = (("ilu0_apply (fwd+bwd sweeps)", apply_bytes, t_apply) if t_apply >= t_spmv
+           else ("bsr_spmv (halo columns)", spmv_bytes, t_spmv))
+    gbs = dom[1] / (dom[2] * 1e-6) / 1e9
+    return {"bound": "hbm", "kernel": dom[0], "achieved": gbs, "peak": hbm, "peak_kind": kind,
+            "unit": "GB/s", "frac": gbs / hbm, "traffic": None, "algorithmic_bytes": dom[1],
+            "us": dom[2], "spmv_us": t_spmv, "ilu_apply_us": t_apply}
+
+
+def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_port_sample,
+                    count_step_kernels=None):
     import paper_2309_11488_b200 as P
     from paper_2309_11488_b200.distributed import (NcclComm, Shard, exchange_requests,
                                                    generate_slab, slab_bounds,
@@ -76,19 +117,30 @@ def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_p
     ms, iters = timed(step, args.steps, args.warmup)
     clk = clocks.stop()
 
-    def e2e_step():                            # host slab in, host x out
-        sh = Shard(slab, owners, backend)
-        exchange_requests([sh], world, gather)
+    # e2e: every step is a new system with the shard's pattern (a simulator's
+    # next Newton step): its block values and rhs go H2D from page-locked host
+    # buffers, the solution comes back D2H into page-locked memory; the
+    # pattern-dependent host work (halo plan, ghost maps) is done once
+    from paper_2309_11488_b200._device import pinned_copy
+    vals_h, rhs_h = pinned_copy(slab.vals3.reshape(-1)), pinned_copy(slab.rhs)
+    x_h = torch.empty(slab.rows * slab.b, dtype=torch.float64, pin_memory=True)
+
+    def e2e_step():
+        shard.refresh_values(vals_h, rhs_h)
+        shard.setup(backend)
         if mesh:
-            sh.mesh = shard.mesh                   # the IPC-shared buffers stay mapped
-            rep, x = solve_shard_mesh_dist(sh, stop, cache_key=args.backend)
-            x.cpu()
-            return rep
-        rep, xs = solve_shards([sh], NcclComm(sh), stop)
-        xs[0].cpu()
+            rep, x = solve_shard_mesh_dist(shard, stop, cache_key=args.backend)
+        else:
+            rep, xs = solve_shards([shard], comm, stop)
+            x = xs[0]
+        x_h.copy_(x, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
         return rep
     e2e_ms, _ = (None, None) if args.no_e2e else timed(e2e_step, max(1, args.steps // 3), 1)
     n_total = spec.nx * spec.ny * spec.nz
+    roof = kernel_roofline(shard, peaks)
+    # kernels of one step on this rank (CUPTI), outside the timed region
+    kinfo = count_step_kernels(step) if count_step_kernels else None
     if rank == 0:
         line = {
             "metric": metric, "value": n_total / (ms / 1e3) / 1e6, "unit": unit,
@@ -105,9 +157,12 @@ def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_p
             "iterations": iters, "solve_ms": ms, "clocks": clk,
             "e2e": None if e2e_ms is None else {
                 "value": n_total / (e2e_ms / 1e3) / 1e6, "unit": unit, "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": world * (slab.rp.size * 4 + slab.ci.size * 4
-                                               + slab.vals3.size * 8 + slab.rhs.size * 8),
+                "h2d_bytes_per_step": world * (slab.vals3.size * 8 + slab.rhs.size * 8),
+                "host_memory": "pinned",
                 "d2h_bytes_per_step": n_total * 24},
+            "roofline": roof,
+            "gpu_launches": (kinfo["per_step"] * args.steps * world) if kinfo else None,
+            "gpu_launches_per_step": kinfo,
             "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)

@@ -211,6 +211,25 @@ class Shard:
             self.set_send(self._requests)
         return self
 
+    def refresh_values(self, vals: np.ndarray, rhs: np.ndarray):
+        """A new system with this shard's sparsity pattern (the next Newton
+        step): H2D of the slab's block values and right-hand side only (async
+        from page-locked buffers); the preconditioner's blocks (the owned
+        columns) are gathered on the device -- the host-side halo and pattern
+        work of the constructor is not repeated."""
+        dev, b = self.dev, self.b
+        src = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64).reshape(-1))
+        self.obsr.vals.copy_(src, non_blocking=D.is_pinned(src))
+        if getattr(self, "_own_idx", None) is None:
+            self._own_idx = D.i32(np.flatnonzero(self.halo_plan.own), dev)
+        nk = self._own_idx.numel()
+        check(D.lib().b2s_gather_blocks(nk, b, D.ptr(self._own_idx), D.ptr(self.obsr.vals),
+                                        D.ptr(self.pbsr.vals), D.stream()), "gather_blocks")
+        r = torch.from_numpy(np.ascontiguousarray(rhs, dtype=np.float64))
+        if getattr(self, "rhs_d", None) is None:
+            self.rhs_d = torch.empty(r.numel(), dtype=torch.float64, device=dev)
+        self.rhs_d.copy_(r, non_blocking=D.is_pinned(r))
+
     # rows this shard must send to rank h (plan-order local ids), given the
     # ghost ids rank h requested from us
     def set_send(self, requests: dict[int, np.ndarray]):
@@ -444,7 +463,9 @@ def solve_shards(shards, comm, stop: StoppingCriteria, x0=None):
     ``shard.slab.rhs``; returns (report, list of per-shard x in input order)."""
     for i, s in enumerate(shards):
         iperm = s.plan.device("inverse_permutation")
-        rhs = D.f64(s.slab.rhs, s.dev)
+        rhs = getattr(s, "rhs_d", None)      # resident (refresh_values / an earlier solve)
+        if rhs is None:
+            rhs = s.rhs_d = D.f64(s.slab.rhs, s.dev)
         s.rhs_p = D.gather_rows(rhs, iperm, s.R, s.b)
         x = D.f64(x0[i], s.dev) if x0 is not None else torch.zeros_like(rhs)
         s.x_p = D.gather_rows(x, iperm, s.R, s.b)
