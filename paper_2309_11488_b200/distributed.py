@@ -203,10 +203,11 @@ class Shard:
         perm = self.plan.device("permutation")
         iperm = self.plan.device("inverse_permutation")
         cmap = torch.cat([perm, torch.arange(R, R + self.G, dtype=torch.int32, device=dev)])
-        self.op = D.permute(self.obsr, cmap, iperm)
+        # (plan-order pattern + source map; the SELL layout is filled straight
+        # from the unpermuted values: no permuted value copy)
+        opat, src = D.permute_pattern(self.obsr.pat, cmap, iperm)
         self.smap = self.fact.smap
-        self.sell = D.Sell.build(self.smap, self.op, 0)
-        self.perm_h = self.plan.permutation          # local old -> new
+        self.sell = D.Sell.build(self.smap, D.DevBSR(opat, self.b, self.obsr.vals), 0, src=src)
         if getattr(self, "_requests", None) is not None:
             self.set_send(self._requests)
         return self
@@ -231,11 +232,18 @@ class Shard:
         self.rhs_d.copy_(r, non_blocking=D.is_pinned(r))
 
     # rows this shard must send to rank h (plan-order local ids), given the
-    # ghost ids rank h requested from us
+    # ghost ids rank h requested from us (gathered through the device
+    # permutation: the plan never comes back to the host)
     def set_send(self, requests: dict[int, np.ndarray]):
         self._requests = requests
-        self.send = {h: D.i32(self.perm_h[g - self.slab.r0], self.dev)
-                     for h, g in requests.items()}
+        if getattr(self, "_req_idx", None) is None:
+            self._req_idx = {h: torch.as_tensor(np.asarray(g, dtype=np.int64) - self.slab.r0,
+                                                device=self.dev)
+                             for h, g in requests.items()}
+        if getattr(self, "plan", None) is None:
+            return               # no plan yet: setup() fills the lists
+        perm = self.plan.device("permutation")
+        self.send = {h: perm.index_select(0, idx) for h, idx in self._req_idx.items()}
 
     def vec(self, with_ghosts=False):
         return torch.zeros((self.R + (self.G if with_ghosts else 0)) * self.b,
