@@ -270,6 +270,20 @@ typedef struct {
    * allocation, graph instantiation) runs while a peer's kernel waits */
   void (*host_barrier)(void*);
   void* host_barrier_ctx;
+  /* Optional, 2-colour plans: run the fused colour passes on the local block
+   * (b2s_bicg_args' operator = the owned columns only) and add the ghost
+   * couplings afterwards -- they are the last entries of their rows, so the
+   * row sums continue in column order.  bnd_*: the rows with ghost couplings
+   * (plan order) as CSR over ghost indices; full_*: the whole operator (ghost
+   * columns included) on the same slice map, for the r0 / final residuals. */
+  int nbnd;
+  const int32_t* bnd_row;
+  const int32_t* bnd_ptr;
+  const int32_t* bnd_col;
+  const double* bnd_val;
+  const int32_t* full_sp;
+  const int32_t* full_cols;
+  const double* full_vals;
 } b2s_mesh;
 
 #define B2S_MBOX_SLOTS 8

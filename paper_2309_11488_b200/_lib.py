@@ -44,7 +44,9 @@ class Mesh(C.Structure):
                 ("ghost_row", _P), ("nnbr", _I), ("nbr", _P), ("peer_x", _P),
                 ("peer_phat", _P), ("peer_shat", _P), ("flags", _P), ("peer_flags", _P),
                 ("mbox", _P), ("peer_mbox", _P), ("seq_base", C.c_longlong),
-                ("shared_device", _I), ("host_barrier", _P), ("host_barrier_ctx", _P)]
+                ("shared_device", _I), ("host_barrier", _P), ("host_barrier_ctx", _P),
+                ("nbnd", _I), ("bnd_row", _P), ("bnd_ptr", _P), ("bnd_col", _P), ("bnd_val", _P),
+                ("full_sp", _P), ("full_cols", _P), ("full_vals", _P)]
 
 
 BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)

@@ -152,6 +152,74 @@ __global__ void k_mesh_scalar(State* st, MeshDev mesh, int slot, const double* p
   }
 }
 
+// Sharded 2-colour solves: the fused passes ran on the local block; add the
+// ghost couplings of the boundary rows (pulled just before) and their share
+// of the fused dot products, then run the control step over every partial
+// (the local kernels' at [0, poff), these at [poff, poff + grid)).  The
+// ghost entries are the last ones of their rows, so the row sum simply
+// continues in column order.
+template <int B, int MODE>
+__global__ void __launch_bounds__(256) k_ghost_correct(int nb, const int32_t* __restrict__ brow,
+                                                       const int32_t* __restrict__ bptr,
+                                                       const int32_t* __restrict__ bcol,
+                                                       const double* __restrict__ bval,
+                                                       const double* __restrict__ xg, double* y,
+                                                       const double* __restrict__ w,
+                                                       double* part0, double* part1, int poff,
+                                                       const int* done, Ctl ctl) {
+  constexpr int BB = B * B;
+  __shared__ double red[8];
+  if (done && *done) return;
+  double p0 = 0.0, p1 = 0.0;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nb; q += gridDim.x * blockDim.x) {
+    const long long row = brow[q];
+    double yl[B], acc[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] = yl[c] = y[row * B + c];
+    for (int e = bptr[q]; e < bptr[q + 1]; ++e) {
+      const long long g = bcol[e];
+      double blk[BB], xv[B], pr[B];
+#pragma unroll
+      for (int k = 0; k < BB; ++k) blk[k] = bval[(long long)e * BB + k];
+#pragma unroll
+      for (int c = 0; c < B; ++c) xv[c] = __ldcg(xg + g * B + c);
+      matvec<B>(blk, xv, pr);
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] += pr[c];
+    }
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      y[row * B + c] = acc[c];
+      const double d = acc[c] - yl[c];
+      if (MODE == kDotW) p0 = fma(w[row * B + c], d, p0);
+      if (MODE == kSelfAndW) {
+        p0 = fma(d, acc[c] + yl[c], p0);   // t.t: new^2 - old^2
+        p1 = fma(w[row * B + c], d, p1);
+      }
+    }
+  }
+  const double t0 = block_sum(p0, red);
+  if (threadIdx.x == 0) part0[poff + blockIdx.x] = t0;
+  if (MODE == kSelfAndW) {
+    const double t1 = block_sum(p1, red);
+    if (threadIdx.x == 0) part1[poff + blockIdx.x] = t1;
+  }
+  if (ctl.st && last_cta(ctl.counter)) ctl_run(ctl, part0, part1, poff + gridDim.x, red);
+}
+constexpr int kCorrCtas = 32;
+
+template <int MODE>
+void launch_ghost_correct(int b, const b2s_mesh* m, const double* xg, double* y, const double* w,
+                          double* p0, double* p1, int poff, const int* done, Ctl ctl,
+                          cudaStream_t st) {
+  switch (b) {
+    case 1: k_ghost_correct<1, MODE><<<kCorrCtas, 256, 0, st>>>(m->nbnd, m->bnd_row, m->bnd_ptr, m->bnd_col, m->bnd_val, xg, y, w, p0, p1, poff, done, ctl); break;
+    case 2: k_ghost_correct<2, MODE><<<kCorrCtas, 256, 0, st>>>(m->nbnd, m->bnd_row, m->bnd_ptr, m->bnd_col, m->bnd_val, xg, y, w, p0, p1, poff, done, ctl); break;
+    case 3: k_ghost_correct<3, MODE><<<kCorrCtas, 256, 0, st>>>(m->nbnd, m->bnd_row, m->bnd_ptr, m->bnd_col, m->bnd_val, xg, y, w, p0, p1, poff, done, ctl); break;
+    default: k_ghost_correct<4, MODE><<<kCorrCtas, 256, 0, st>>>(m->nbnd, m->bnd_row, m->bnd_ptr, m->bnd_col, m->bnd_val, xg, y, w, p0, p1, poff, done, ctl); break;
+  }
+}
+
 #define GRID_STRIDE(t, m) \
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (m); \
        t += (long long)gridDim.x * blockDim.x)
@@ -410,7 +478,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // 2 colours + colour-0 rows of A == [diag, U row] (b2s_fuse_check): the
   // backward pass of colour 0 and the SpMV rows of colour 0 share one read
   // (sharded: the SpMV needs the owners' ghost rows of p^ between the two)
-  const bool fused = phased && a->ngroups == 2 && a->fuse && !mesh;
+  const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh->full_vals);
   const int reset = (ilu && !phased) ? 1 : 0;  // sync-free sweeps need sentinel-filled outputs
   MeshDev md{};
   MeshHalo mh{};
@@ -440,6 +508,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   const int np = a->nparts;
   SliceMap map{a->nslices, a->row0, a->nrows};
   Sell A{a->a_sp, a->a_cols, a->a_vals};
+  // sharded + fused: A is the local block; the residuals need every column
+  const Sell Afull = (mesh && mesh->full_vals)
+                         ? Sell{mesh->full_sp, mesh->full_cols, mesh->full_vals} : A;
   Sell L{a->l_sp, a->l_cols, a->l_vals}, U{a->u_sp, a->u_cols, a->u_vals};
   const int* done = &state->done;
   cudaStream_t user = a->stream;
@@ -472,7 +543,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       k_mesh_reset<<<1, 1, 0, user>>>(state);
       halo(user, 0, a->x, &state->done);
     }
-    rc = launch_spmv(a->b, 3, np, map, A, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{}, user);
+    rc = launch_spmv(a->b, 3, np, map, Afull, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{}, user);
     if (rc == B2S_OK) {
       k_ctl_init<<<1, 256, 0, user>>>(state, prr, np, a->tol, a->maxit, dev_done, md);
       k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
@@ -524,9 +595,16 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       int g0 = np;
       launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
                       done, &g0, cs, pdl);
+      const Ctl ca{state, counters + 0, dev_done, kCtlAlpha, md};
       launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
-                        done, Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl);
+                        done, mesh ? Ctl{} : ca, cs, pdl);
       kernels += 3;
+      if (mesh) {   // ghost rows of p^, then the boundary rows' ghost couplings + alpha
+        halo(cs, 1, phat, done);
+        launch_ghost_correct<kDotW>(a->b, mesh, phat + m, v, rhat, pg, nullptr, g0 + np, done, ca,
+                                    cs);
+        kernels += mh.nghost > 0 ? 4 : 3;
+      }
     } else if (phased) {
       launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
                     p, y, phat, done, cs, false, pdl);
@@ -538,7 +616,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                          tickets, done, cs);
       kernels += 2;
     }
-    if (mesh) { halo(cs, 1, ph, done); kernels += mh.nghost > 0 ? 3 : 2; }
+    if (mesh && !fused) { halo(cs, 1, ph, done); kernels += mh.nghost > 0 ? 3 : 2; }
     if (!fused) {
       launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done,
                   Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl); ++kernels;
@@ -553,9 +631,16 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       int g0 = np;
       launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, s, shat, t, s, ptt, pts, done,
                       &g0, cs, pdl);
+      const Ctl co{state, counters + 2, dev_done, kCtlOmega, md};
       launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
-                        Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl);
+                        mesh ? Ctl{} : co, cs, pdl);
       kernels += 3;
+      if (mesh) {
+        halo(cs, 2, shat, done);
+        launch_ghost_correct<kSelfAndW>(a->b, mesh, shat + m, t, s, ptt, pts, g0 + np, done, co,
+                                        cs);
+        kernels += mh.nghost > 0 ? 4 : 3;
+      }
     } else if (phased) {
       launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
                     s, y, shat, done, cs, false, pdl);
@@ -567,7 +652,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                          tickets, done, cs);
       kernels += 2;
     }
-    if (mesh) { halo(cs, 2, sh, done); kernels += mh.nghost > 0 ? 3 : 2; }
+    if (mesh && !fused) { halo(cs, 2, sh, done); kernels += mh.nghost > 0 ? 3 : 2; }
     if (!fused) {
       launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done,
                   Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl); ++kernels;
@@ -644,7 +729,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // (sharded: x's ghost rows first, and both results all-reduced, so every
   // rank reports the global norm and restores x0 together)
   if (mesh) halo(user, 0, a->x, nullptr);
-  int rc = launch_spmv(a->b, 3, np, map, A, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user);
+  int rc = launch_spmv(a->b, 3, np, map, Afull, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user);
   if (rc) return rc;
   if (mesh) k_mesh_scalar<<<1, 256, 0, user>>>(state, md, kSlotFinal, pg, np, nullptr, pss);
   else k_reduce_parts<<<1, 256, 0, user>>>(pg, np, pss);

@@ -191,6 +191,17 @@ class Shard:
         self.pbsr = D.DevBSR.upload(self.pmat)
         opat = D.DevPattern(R, len(ci), D.i32(slab.rp, dev), D.i32(lcol, dev))
         self.obsr = D.DevBSR(opat, b, D.f64(slab.vals3.reshape(-1), dev))
+        # ghost couplings of the boundary rows as CSR over ghost indices (the
+        # fused 2-colour loop adds them after the halo pull; b2s_mesh bnd_*)
+        gh = ~own
+        erow = rows[gh]
+        ub, cnt = np.unique(erow, return_counts=True)
+        self._bnd_in = torch.as_tensor(ub.astype(np.int64), device=dev)
+        self._bnd_ptr = D.i32(np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64), dev)
+        self._bnd_col = D.i32((lcol[gh] - R).astype(np.int64), dev)
+        self._gh_idx = D.i32(np.flatnonzero(gh).astype(np.int64), dev)
+        self._bnd_val = torch.empty(max(int(gh.sum()), 1) * b * b, dtype=torch.float64, device=dev)
+        self._gather_ghost_blocks()
         self.dev = dev
         if backend is not None:
             self.setup(backend)
@@ -208,9 +219,16 @@ class Shard:
         opat, src = D.permute_pattern(self.obsr.pat, cmap, iperm)
         self.smap = self.fact.smap
         self.sell = D.Sell.build(self.smap, D.DevBSR(opat, self.b, self.obsr.vals), 0, src=src)
+        self._bnd_row = perm.index_select(0, self._bnd_in)
         if getattr(self, "_requests", None) is not None:
             self.set_send(self._requests)
         return self
+
+    def _gather_ghost_blocks(self):
+        nk = int(self._gh_idx.numel())
+        if nk:
+            check(D.lib().b2s_gather_blocks(nk, self.b, D.ptr(self._gh_idx), D.ptr(self.obsr.vals),
+                                            D.ptr(self._bnd_val), D.stream()), "gather_blocks")
 
     def refresh_values(self, vals: np.ndarray, rhs: np.ndarray):
         """A new system with this shard's sparsity pattern (the next Newton
@@ -226,6 +244,7 @@ class Shard:
         nk = self._own_idx.numel()
         check(D.lib().b2s_gather_blocks(nk, b, D.ptr(self._own_idx), D.ptr(self.obsr.vals),
                                         D.ptr(self.pbsr.vals), D.stream()), "gather_blocks")
+        self._gather_ghost_blocks()
         r = torch.from_numpy(np.ascontiguousarray(rhs, dtype=np.float64))
         if getattr(self, "rhs_d", None) is None:
             self.rhs_d = torch.empty(r.numel(), dtype=torch.float64, device=dev)
@@ -578,7 +597,29 @@ def _mesh_struct(shard: "Shard", ms: MeshState, owner_rows: dict, shared_device:
     ms.solves += 1
     m.seq_base = ms.solves << 32          # equal on every rank: one per global solve
     m.shared_device = 1 if shared_device else 0
+    if _mesh_fused(shard):
+        m.nbnd = int(shard._bnd_in.numel())
+        m.bnd_row, m.bnd_ptr = D.ptr(shard._bnd_row), D.ptr(shard._bnd_ptr)
+        m.bnd_col, m.bnd_val = D.ptr(shard._bnd_col), D.ptr(shard._bnd_val)
+        m.full_sp, m.full_cols, m.full_vals = (D.ptr(shard.sell.sp), D.ptr(shard.sell.cols),
+                                               D.ptr(shard.sell.vals))
     return m, keep
+
+
+def _mesh_fused(shard) -> bool:
+    """2-colour shard: the fused colour passes run on the local block (the
+    factorisation's own operator layout) plus the ghost correction."""
+    f = shard.fact
+    return (f.a_sell is not None and f.phased and not f.tiles and
+            os.environ.get("B2S_FUSE", "1") != "0")
+
+
+def _mesh_krylov(shard, ms):
+    from .krylov import DeviceKrylov
+    if _mesh_fused(shard):
+        return DeviceKrylov(shard.R, shard.b, shard.smap, shard.fact.a_sell, shard.fact, ms.work,
+                            True)
+    return DeviceKrylov(shard.R, shard.b, shard.smap, shard.sell, shard.fact, ms.work, False)
 
 
 def _mesh_prepare(shard: "Shard", nranks: int, x0=None):
@@ -637,7 +678,7 @@ def solve_shards_mesh(shards, stop: StoppingCriteria, x0=None):
         mesh, keep = _mesh_struct(s, ms, owner_rows, shared_device=True)
         mesh.host_barrier = C.cast(barrier_cb, C.c_void_p)
         keep["barrier"] = barrier_cb
-        kr = DeviceKrylov(s.R, s.b, s.smap, s.sell, s.fact, ms.work, False)
+        kr = _mesh_krylov(s, ms)
         jobs.append((s, ms, kr, mesh, keep))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -713,7 +754,7 @@ def solve_shard_mesh_dist(shard: "Shard", stop: StoppingCriteria, x0=None, cache
         shard._owner_rows = {r: d[rank] for r, d in everyone if rank in d}
         shard._owner_rows_key = key
     mesh, keep = _mesh_struct(shard, ms, shard._owner_rows, shared_device=False)
-    kr = DeviceKrylov(shard.R, shard.b, shard.smap, shard.sell, shard.fact, ms.work, False)
+    kr = _mesh_krylov(shard, ms)
     t0 = time.perf_counter()
     tm.append(t0)
     res = kr.solve(shard.rhs_p, ms.x, stop, mesh=mesh)

@@ -155,3 +155,20 @@ def test_refresh_values_equals_fresh_shard():
     assert rep1.iterations == rep2.iterations
     for a, b in zip(xs1, xs2):
         assert torch.equal(a, b)
+
+
+def test_mesh_fused_colour_passes_match_unfused(monkeypatch):
+    """2-colour shards: fused colour passes on the local block + ghost
+    correction (b2s_mesh bnd_*) against the unfused mesh loop."""
+    from paper_2309_11488_b200.distributed import _mesh_fused, solve_shards_mesh
+    spec = P.GeneratorSpec(12, 10, 16, seed=5, diagonal_boost=1e-2)
+    shards, _ = local_solver(spec, 4, P.Backend.GRAPH_COLORED)
+    assert all(_mesh_fused(s) for s in shards)
+    rep_f, xs_f = solve_shards_mesh(shards, P.StoppingCriteria(1e-8, 200))
+    monkeypatch.setenv("B2S_FUSE", "0")
+    rep_u, xs_u = solve_shards_mesh(shards, P.StoppingCriteria(1e-8, 200))
+    xf = np.concatenate([v.cpu().numpy() for v in xs_f])
+    xu = np.concatenate([v.cpu().numpy() for v in xs_u])
+    assert rep_f.converged and rep_u.converged
+    assert abs(rep_f.iterations - rep_u.iterations) <= 1.0
+    assert np.linalg.norm(xf - xu) <= 1e-7 * np.linalg.norm(xu)
