@@ -111,6 +111,10 @@ int b2s_slices_grouped_fill(int ngroups, int nslices, const int32_t* offsets,
 int b2s_sell_offsets(int nslices, const int32_t* row0, const int32_t* nrows, const int32_t* rp,
                      const int32_t* ci, int sel, int32_t* sp, long long* slots_host,
                      cudaStream_t stream);
+/* the same, plus the widest slice in entries per row (one readback) */
+int b2s_sell_offsets_ex(int nslices, const int32_t* row0, const int32_t* nrows, const int32_t* rp,
+                        const int32_t* ci, int sel, int32_t* sp, long long* slots_host,
+                        int* width_host, cudaStream_t stream);
 /* goff/ngroups (optional, plan group offsets): entries of a triangular
  * selection whose column lies in the row's own group are encoded -(c+2),
  * "read the value from before the sweep" -- the reference updates a whole

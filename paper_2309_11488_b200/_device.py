@@ -260,10 +260,16 @@ class DevBSR:
 
 
 def find_diagonal(p: DevPattern) -> torch.Tensor:
+    """Diagonal slot of every row (MissingDiagonal otherwise); kept on the
+    pattern, which never changes, so a later caller costs no device round trip."""
+    diag = getattr(p, "_diag", None)
+    if diag is not None:
+        return diag
     diag = empty_i32(p.n, p.rp.device)
     bad = C.c_int32(-1)
     rc = lib().b2s_find_diagonal(p.n, ptr(p.rp), ptr(p.ci), ptr(diag), C.byref(bad), stream())
     check(rc, "find_diagonal", bad.value)
+    p._diag = diag
     return diag
 
 
@@ -402,9 +408,10 @@ class Sell:
         dev = m.pat.rp.device
         sp = empty_i32(smap.nslices + 1, dev)
         slots = C.c_longlong(0)
-        check(lib().b2s_sell_offsets(smap.nslices, ptr(smap.row0), ptr(smap.nrows),
-                                     ptr(m.pat.rp), ptr(m.pat.ci), sel, ptr(sp),
-                                     C.byref(slots), stream()), "sell_offsets")
+        wmax = C.c_int(0)
+        check(lib().b2s_sell_offsets_ex(smap.nslices, ptr(smap.row0), ptr(smap.nrows),
+                                        ptr(m.pat.rp), ptr(m.pat.ci), sel, ptr(sp),
+                                        C.byref(slots), C.byref(wmax), stream()), "sell_offsets")
         ns = int(slots.value)
         if ns * m.b * m.b > _I32_MAX * 8:
             raise ValueError("matrix too large for one device layout")
@@ -415,9 +422,7 @@ class Sell:
                                           ptr(m.pat.rp), ptr(m.pat.ci), ptr(m.vals), sel,
                                           ptr(sp), ptr(goff), int(ngroups), ptr(cols),
                                           ptr(vals), ptr(src), stream()), "sell_fill")
-        width = 0
-        if smap.nslices:
-            width = int(((sp[1:smap.nslices + 1] - sp[:smap.nslices]).max().item()) // 32)
+        width = int(wmax.value)
         stale = (bool((cols[:ns] <= -2).any().item())
                  if (fill and goff is not None and ns) else False)
         return cls(sp, cols, vals, ns, width, stale)

@@ -75,6 +75,8 @@ SIGNATURES = {
     "b2s_slices_grouped_count": (_I, [_I, _P, _P, _PI, _P]),
     "b2s_slices_grouped_fill": (_I, [_I, _I, _P, _P, _P, _P, _P]),
     "b2s_sell_offsets": (_I, [_I, _P, _P, _P, _P, _I, _P, _PLL, _P]),
+    "b2s_sell_offsets_ex": (_I, [_I, _P, _P, _P, _P, _I, _P, C.POINTER(C.c_longlong),
+                                 C.POINTER(C.c_int), _P]),
     "b2s_sell_fill": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P]),
     "b2s_diag_tiles": (_I, [_I, _I, _P, _P, _P, _P, _P]),
     "b2s_sell_fill_src": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P]),

@@ -310,35 +310,48 @@ int b2s_slices_grouped_fill(int ngroups, int nslices, const int32_t* off, const 
   return B2S_OK;
 }
 
-// Slot offsets of a SELL-32 layout: sp[0..nslices], total slots to host.
-// sel: 0 = every block, 1 = strict lower, 2 = strict upper.
-int b2s_sell_offsets(int nslices, const int32_t* row0, const int32_t* nrows, const int32_t* rp,
-                     const int32_t* ci, int sel, int32_t* sp, long long* slots_host,
-                     cudaStream_t st) {
+// Slot offsets of a SELL-32 layout and the widest slice (entries per row),
+// both read back with one synchronisation.
+int b2s_sell_offsets_ex(int nslices, const int32_t* row0, const int32_t* nrows, const int32_t* rp,
+                        const int32_t* ci, int sel, int32_t* sp, long long* slots_host,
+                        int* width_host, cudaStream_t st) {
   if (nslices < 0 || sel < 0 || sel > 2) return B2S_SHAPE;
   *slots_host = 0;
+  if (width_host) *width_host = 0;
   if (nslices == 0) {
     B2S_CHECK(cudaMemsetAsync(sp, 0, sizeof(int32_t), st));
     return B2S_OK;
   }
   int32_t* cnt = nullptr;
-  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (nslices + 1), st));
+  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (nslices + 2), st));
   B2S_CHECK(cudaMemsetAsync(cnt + nslices, 0, sizeof(int32_t), st));
   k_sell_width<<<grid_for((long long)nslices * 32), 256, 0, st>>>(nslices, row0, nrows, rp, ci,
                                                                    sel, cnt);
-  size_t tb = 0;
+  size_t tb = 0, tm = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, sp, nslices + 1, st);
+  cub::DeviceReduce::Max(nullptr, tm, cnt, cnt + nslices + 1, nslices, st);
   void* tmp = nullptr;
-  B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
+  B2S_CHECK(cudaMallocAsync(&tmp, tb > tm ? tb : tm, st));
+  cub::DeviceReduce::Max(tmp, tm, cnt, cnt + nslices + 1, nslices, st);
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, sp, nslices + 1, st);
   B2S_LAUNCH_CHECK();
-  int32_t h = 0;
-  B2S_CHECK(cudaMemcpyAsync(&h, sp + nslices, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  int32_t h[2] = {0, 0};
+  B2S_CHECK(cudaMemcpyAsync(&h[0], sp + nslices, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaMemcpyAsync(&h[1], cnt + nslices + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   B2S_CHECK(cudaFreeAsync(tmp, st));
   B2S_CHECK(cudaFreeAsync(cnt, st));
   B2S_CHECK(cudaStreamSynchronize(st));
-  *slots_host = h;
+  *slots_host = h[0];
+  if (width_host) *width_host = h[1] / kSlice;
   return B2S_OK;
+}
+
+// Slot offsets of a SELL-32 layout: sp[0..nslices], total slots to host.
+// sel: 0 = every block, 1 = strict lower, 2 = strict upper.
+int b2s_sell_offsets(int nslices, const int32_t* row0, const int32_t* nrows, const int32_t* rp,
+                     const int32_t* ci, int sel, int32_t* sp, long long* slots_host,
+                     cudaStream_t st) {
+  return b2s_sell_offsets_ex(nslices, row0, nrows, rp, ci, sel, sp, slots_host, nullptr, st);
 }
 
 int b2s_sell_fill_src(int nslices, int b, const int32_t* row0, const int32_t* nrows,
