@@ -532,3 +532,20 @@ def test_plan_hint_is_verified(monkeypatch, golden, name):
                 D.check(fn(p.n, D.ptr(p.rp), D.ptr(p.ci), nx, ny, D.ptr(gw), C.byref(ng),
                            C.byref(used), D.stream()), kind)
                 assert ng.value == n0 and torch.equal(gw[: p.n], g0[: p.n]), (nx, ny)
+
+
+def test_tiled_sweeps_inside_device_krylov(monkeypatch, golden):
+    """The opt-in tile step kernels (csrc/tiles.cu) run inside the device
+    BiCGStab loop (launch_tiled in the iteration graph) with the same result
+    as the sync-free sweeps."""
+    g = golden("c1_20x20x10")
+    a = matrix(g)
+    rhs = P.BlockVector(g["rhs"], 3)
+    cfg = P.SolverConfig(backend=P.Backend.LEVEL_SCHEDULED, stop=P.StoppingCriteria(1e-8, 200))
+    monkeypatch.setenv("B2S_TILES", "0")
+    x0, r0 = P.solve_with_fallback(cfg, a, rhs)
+    monkeypatch.setenv("B2S_TILES", "1")
+    monkeypatch.setenv("B2S_TILES_T", "6")
+    x1, r1 = P.solve_with_fallback(cfg, a, rhs)
+    assert r0.converged and r1.converged and r0.iterations == r1.iterations
+    assert_array_equal(x1.data, x0.data)
