@@ -57,6 +57,8 @@ constexpr int kWin = 1024;        // tile results kept in shared memory (rows)
 constexpr int kCons = 384;        // consumer threads per CTA (12 warps, 4 lanes per row)
 constexpr int kMaxStages = 8;     // ring depth cap
 constexpr int kHdr = 32;          // stage header bytes (step meta)
+// window: kWin slots + one never-written slot, rounded up to 128 bytes
+__host__ __device__ constexpr int kWinBytes(int b) { return ((kWin + 1) * b * 8 + 127) & ~127; }
 
 struct StepSet {
   int T, nsteps;
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(32 + kCons, 1)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
   unsigned long long* empty = full + kMaxStages;
   double* win = reinterpret_cast<double*>(smem + 16 * kMaxStages);
-  char* ring = smem + 16 * kMaxStages + kWin * B * 8;
+  char* ring = smem + 16 * kMaxStages + kWinBytes(B);
   const int t = blockIdx.x;
   const int s_lo = ss.tstep[t], s_hi = ss.tstep[t + 1], nst = s_hi - s_lo;
   const int tbase = ss.toff[t];
@@ -309,7 +311,9 @@ __global__ void __launch_bounds__(32 + kCons, 1)
         for (int kk = 0; kk < 4; ++kk) cd[kk] = (ok && k0 + kk < w) ? codes[(k0 + kk) * np + r] : -1;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const double* p = win + (cd[kk] & (kWin - 1)) * B;
+          // padding / remote / same-group codes read slot kWin, which nobody
+          // writes (the value is replaced or masked below)
+          const double* p = win + (cd[kk] >= 0 ? (cd[kk] & (kWin - 1)) : kWin) * B;
 #pragma unroll
           for (int c = 0; c < B; ++c) dep[kk][c] = p[c];
           slow |= cd[kk] <= -2;
@@ -357,11 +361,13 @@ __global__ void __launch_bounds__(32 + kCons, 1)
         }
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {   // ascending column order, like the reference
-          const bool in = k0 + kk < w;
-          const double* vp = vals + ((k0 + kk) * BB + cb * B) * np + r;
+          // (a padding entry past the row's width reads entry 0 of this
+          // record -- never memory of another stage -- and is masked below)
+          const int ke = k0 + kk < w ? k0 + kk : 0;
+          const double* vp = vals + (ke * BB + cb * B) * np + r;
           double sum = 0.0;
 #pragma unroll
-          for (int e = 0; e < B; ++e) sum = fma(in ? vp[e * np] : 0.0, dep[kk][e], sum);
+          for (int e = 0; e < B; ++e) sum = fma(vp[e * np], dep[kk][e], sum);
           acc = cd[kk] != -1 ? acc + sum : acc;
         }
       }
@@ -744,7 +750,7 @@ int b2s_tiles_create(int n, int b, int T, int nx, int ny, int px, int py, const 
   B2S_CHECK(cudaMemcpyAsync(&stage, stage_max, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   B2S_CHECK(cudaStreamSynchronize(st));
   stage = (stage + 127) & ~127;
-  const long long fixed = 16ll * kMaxStages + (long long)kWin * b * 8;
+  const long long fixed = 16ll * kMaxStages + kWinBytes(b);
   const long long avail = (long long)smem_max - fixed;
   const int D = stage > 0 ? (int)std::min<long long>(kMaxStages, avail / stage) : 0;
   if (D < 2) status = B2S_UNSUPPORTED;
