@@ -115,7 +115,20 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU port: cpu_baseline and --impl reference
 
-def cpu_port_sample(args, nx, ny, slab):
+def host_info():
+    """Cores and CPU model of the host the CPU baseline runs on."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "cpu_model": model}
+
+
+def cpu_port_sample(args, nx, ny, slab, per_op=False):
     from oracle import port as O
     from paper_2309_11488_b200.synthetic import GeneratorSpec, generate
     g = generate(GeneratorSpec(nx, ny, slab, seed=0, diagonal_boost=args.boost))
@@ -125,11 +138,24 @@ def cpu_port_sample(args, nx, ny, slab):
     x, rep, groups, fb = O.solve(rp, ci, v3, g.rhs.data, args.backend, args.tol)
     dt = time.perf_counter() - t0
     cells = a.num_block_rows
-    return {"seconds": dt, "cells": cells, "iterations": rep.iterations,
-            "value": cells / dt / 1e6,
-            "sample": f"oracle port full solve ({args.backend} plan + ILU0 + BiCGStab to tol "
-                      f"{args.tol:g}) of GeneratorSpec({nx},{ny},{slab},seed=0): {cells} cells, "
-                      f"{rep.iterations} its, {dt:.2f} s"}
+    out = {"seconds": dt, "cells": cells, "iterations": rep.iterations,
+           "value": cells / dt / 1e6,
+           "sample": f"oracle port full solve ({args.backend} plan + ILU0 + BiCGStab to tol "
+                     f"{args.tol:g}) of GeneratorSpec({nx},{ny},{slab},seed=0): {cells} cells, "
+                     f"{rep.iterations} its, {dt:.2f} s"}
+    if per_op:   # the reference's per-op costs on the same sample (ms)
+        def t(fn):
+            t1 = time.perf_counter()
+            res = fn()
+            return res, (time.perf_counter() - t1) * 1e3
+        grp, t_plan = t(lambda: (O.level_groups if args.backend == "level" else O.color_groups)(rp, ci))
+        plan = O.plan_from_groups(grp)
+        f, t_fact = t(lambda: O.ilu0(rp, ci, v3, plan))
+        _, t_spmv = t(lambda: O.spmv(rp, ci, v3, g.rhs.data))
+        _, t_apply = t(lambda: O.ilu0_apply(f, g.rhs.data))
+        out["per_op_ms"] = {"plan": t_plan, "decompose": t_fact, "spmv": t_spmv,
+                            "ilu0_apply": t_apply}
+    return out
 
 
 def run_reference(args):
@@ -149,7 +175,7 @@ def run_reference(args):
                                    f"sample = {args.ref_slab}-plane slab of it",
                        "backend": args.backend, "tol": args.tol, "block_size": 3},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": samples[-1]["sample"]},
+                             "sample": samples[-1]["sample"], "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -340,9 +366,9 @@ def run_single(args):
 
     cpu = None
     if not args.no_cpu:
-        s = cpu_port_sample(args, nx, ny, args.ref_slab)
+        s = cpu_port_sample(args, nx, ny, args.ref_slab, per_op=True)
         cpu = {"value": s["value"], "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": s["sample"]}
+               "sample": s["sample"], "per_op_ms": s["per_op_ms"], "host": host_info()}
 
     clk = main_run.pop("clocks", None)
     launches = main_run.pop("gpu_launches")
