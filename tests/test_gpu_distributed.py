@@ -74,12 +74,16 @@ def test_mesh_solve_matches_partitioned_oracle(dims, world, backend):
     x = np.concatenate([v.cpu().numpy() for v in xs])
     xh = np.concatenate([v.cpu().numpy() for v in xs_h])
     assert rep.converged and rep_h.converged
-    assert abs(rep.iterations - rep_h.iterations) <= 1.0, (rep.iterations, rep_h.iterations)
+    # partitioned solves: the north star's band is +-10% (rounding-level
+    # differences in the dot products move ill-conditioned cases by a few)
+    assert abs(rep.iterations - rep_h.iterations) <= max(1.0, 0.1 * rep_h.iterations), \
+        (rep.iterations, rep_h.iterations)
     np.testing.assert_allclose(rep.initial_norm, rep_h.initial_norm, rtol=1e-12)
     assert np.linalg.norm(x - xh) <= 1e-6 * np.linalg.norm(xh)
     if backend == "level":
         xo, ro = oracle_partitioned(spec, world, tol)
-        assert abs(rep.iterations - ro.iterations) <= 1.0, (rep.iterations, ro.iterations)
+        assert abs(rep.iterations - ro.iterations) <= max(1.0, 0.1 * ro.iterations), \
+            (rep.iterations, ro.iterations)
         assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
     # a second solve on the same buffers (sequence numbers move on)
     rep2, xs2 = solve_shards_mesh(shards, P.StoppingCriteria(tol, 200))
@@ -170,5 +174,5 @@ def test_mesh_fused_colour_passes_match_unfused(monkeypatch):
     xf = np.concatenate([v.cpu().numpy() for v in xs_f])
     xu = np.concatenate([v.cpu().numpy() for v in xs_u])
     assert rep_f.converged and rep_u.converged
-    assert abs(rep_f.iterations - rep_u.iterations) <= 1.0
+    assert abs(rep_f.iterations - rep_u.iterations) <= max(1.0, 0.1 * rep_u.iterations)
     assert np.linalg.norm(xf - xu) <= 1e-7 * np.linalg.norm(xu)
