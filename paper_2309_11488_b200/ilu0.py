@@ -64,8 +64,9 @@ class Ilu0Factorization:
         # measured on B200 (tools/sweep_bench.py): few groups (colourings) are
         # bandwidth-bound -> static slice order, no ticket atomics (0.77 of
         # peak vs 0.68); deep level schedules are latency-bound -> dynamic
-        # tickets on one CTA per SM (1.10 vs 1.39 us per level)
-        self.sweep_flags = 0x4 if plan.group_count <= 16 else 0x10
+        # tickets on one CTA of 4 warps per SM (fewer pollers on L2: C4 level
+        # application 626 us vs 685 us with 8 warps, tools/scratch/sweep_scan.py)
+        self.sweep_flags = 0x4 if plan.group_count <= 16 else 0x410
         self.tiles = None        # b2s_tiles_create handle (tiled level sweeps), or None
         # few independent groups (colourings) and no same-group entries: the
         # phased sweeps, 2(G-1) plain passes, no polling (bit-identical)
