@@ -727,8 +727,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // not converged: true residual of the current x, then x0 if x is not finite
   // (bs/krylov.py:242-244)
   // (sharded: x's ghost rows first, and both results all-reduced, so every
-  // rank reports the global norm and restores x0 together)
-  if (mesh) halo(user, 0, a->x, nullptr);
+  // rank reports the global norm and restores x0 together; on one GPU the
+  // shards first rendezvous again -- a peer still tearing down its graph or
+  // freeing its host flag would otherwise wait for these waiting kernels)
+  if (mesh) {
+    peer_barrier();
+    halo(user, 0, a->x, nullptr);
+  }
   int rc = launch_spmv(a->b, 3, np, map, Afull, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user);
   if (rc) return rc;
   if (mesh) k_mesh_scalar<<<1, 256, 0, user>>>(state, md, kSlotFinal, pg, np, nullptr, pss);

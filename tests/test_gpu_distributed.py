@@ -176,3 +176,22 @@ def test_mesh_fused_colour_passes_match_unfused(monkeypatch):
     assert rep_f.converged and rep_u.converged
     assert abs(rep_f.iterations - rep_u.iterations) <= max(1.0, 0.1 * rep_u.iterations)
     assert np.linalg.norm(xf - xu) <= 1e-7 * np.linalg.norm(xu)
+
+
+@pytest.mark.parametrize("backend", ["level", "color"])
+def test_mesh_budget_exhaustion_reports_true_residual(backend):
+    """Non-converged sharded solve: the final true residual needs x's ghost
+    rows and an all-reduce (k_mesh_scalar) -- every shard reports the same
+    global norm, equal to the host loop's."""
+    from paper_2309_11488_b200.distributed import solve_shards_mesh
+    spec = P.GeneratorSpec(10, 8, 12, seed=5, diagonal_boost=1e-4)
+    shards, comm = local_solver(spec, 3, P.Backend.from_name(backend))
+    stop = P.StoppingCriteria(1e-12, 3)
+    rep, xs = solve_shards_mesh(shards, stop)
+    rep_h, xs_h = solve_shards(shards, comm, stop)
+    assert not rep.converged and rep.failure_reason == "budget" and rep.iterations == 3.0
+    assert rep_h.iterations == 3.0
+    np.testing.assert_allclose(rep.final_norm, rep_h.final_norm, rtol=1e-8)
+    x = np.concatenate([v.cpu().numpy() for v in xs])
+    xh = np.concatenate([v.cpu().numpy() for v in xs_h])
+    assert np.linalg.norm(x - xh) <= 1e-8 * np.linalg.norm(xh)
