@@ -572,6 +572,35 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   cudaGraphExec_t exec = nullptr;
   int status = B2S_OK;
   int kernels = 0;
+  // Sharded solves: overlapping the halo with the colour-1 SpMV (a side
+  // branch of the captured graph) hides the cross-GPU flag and pull latency,
+  // but the fork's event nodes break the programmatic-launch chain: on one
+  // GPU it measured slower (two shards 15.4 -> 16.5 ms), so it is on by
+  // default only for ranks with ghost rows on their own GPU.
+  // B2S_MESH_OVERLAP=1/0 forces it.
+  const char* ov_env = getenv("B2S_MESH_OVERLAP");
+  const bool overlap = mesh && (ov_env ? ov_env[0] == '1'
+                                       : (!mesh->shared_device && mesh->nghost > 0));
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (overlap && (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
+                  cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                  cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+    cudaFreeHost(host_done);
+    cudaStreamDestroy(cs);
+    return B2S_CUDA_ERROR;
+  }
+  auto fork_halo = [&](int which, double* vec) {
+    if (!overlap) return;
+    cudaEventRecord(ev_fork, cs);
+    cudaStreamWaitEvent(side, ev_fork, 0);
+    halo(side, which, vec, &state->done);
+    cudaEventRecord(ev_join, side);
+  };
+  auto join_halo = [&](int which, double* vec) {
+    if (overlap) cudaStreamWaitEvent(cs, ev_join, 0);
+    else halo(cs, which, vec, &state->done);
+  };
   do {
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       status = B2S_CUDA_ERROR; break;
@@ -596,11 +625,15 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
                       done, &g0, cs, pdl);
       const Ctl ca{state, counters + 0, dev_done, kCtlAlpha, md};
+      // sharded: p^ is complete here -- its halo (publish, wait, pull) runs on
+      // a side branch of the graph, overlapped with the colour-1 SpMV (which
+      // reads only local columns), and joins before the ghost correction
+      if (mesh) fork_halo(1, phat);
       launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
                         done, mesh ? Ctl{} : ca, cs, pdl);
       kernels += 3;
-      if (mesh) {   // ghost rows of p^, then the boundary rows' ghost couplings + alpha
-        halo(cs, 1, phat, done);
+      if (mesh) {   // the boundary rows' ghost couplings + alpha
+        join_halo(1, phat);
         launch_ghost_correct<kDotW>(a->b, mesh, phat + m, v, rhat, pg, nullptr, g0 + np, done, ca,
                                     cs);
         kernels += mh.nghost > 0 ? 4 : 3;
@@ -632,11 +665,12 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, s, shat, t, s, ptt, pts, done,
                       &g0, cs, pdl);
       const Ctl co{state, counters + 2, dev_done, kCtlOmega, md};
+      if (mesh) fork_halo(2, shat);
       launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
                         mesh ? Ctl{} : co, cs, pdl);
       kernels += 3;
       if (mesh) {
-        halo(cs, 2, shat, done);
+        join_halo(2, shat);
         launch_ghost_correct<kSelfAndW>(a->b, mesh, shat + m, t, s, ptt, pts, g0 + np, done, co,
                                         cs);
         kernels += mh.nghost > 0 ? 4 : 3;
@@ -704,6 +738,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
   cudaStreamDestroy(cs);
+  if (side) cudaStreamDestroy(side);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   if (host_done) cudaFreeHost(host_done);
   if (status != B2S_OK) return status;
   res->kernels_per_iteration = kernels;

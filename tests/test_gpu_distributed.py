@@ -195,3 +195,18 @@ def test_mesh_budget_exhaustion_reports_true_residual(backend):
     x = np.concatenate([v.cpu().numpy() for v in xs])
     xh = np.concatenate([v.cpu().numpy() for v in xs_h])
     assert np.linalg.norm(x - xh) <= 1e-8 * np.linalg.norm(xh)
+
+
+def test_mesh_halo_overlap_branch(monkeypatch):
+    """B2S_MESH_OVERLAP=1: the halo runs on a side branch of the iteration
+    graph, concurrent with the colour-1 SpMV -- same bits as in line."""
+    from paper_2309_11488_b200.distributed import solve_shards_mesh
+    spec = P.GeneratorSpec(12, 10, 16, seed=5, diagonal_boost=1e-2)
+    shards, _ = local_solver(spec, 4, P.Backend.GRAPH_COLORED)
+    monkeypatch.setenv("B2S_MESH_OVERLAP", "0")
+    rep0, xs0 = solve_shards_mesh(shards, P.StoppingCriteria(1e-8, 200))
+    monkeypatch.setenv("B2S_MESH_OVERLAP", "1")
+    rep1, xs1 = solve_shards_mesh(shards, P.StoppingCriteria(1e-8, 200))
+    assert rep0.iterations == rep1.iterations
+    for a, b in zip(xs0, xs1):
+        assert torch.equal(a, b)
