@@ -113,6 +113,9 @@ class DeviceSolver:
             self.krylov = DeviceKrylov.build(self.a, self.fact)
             return self
         a_perm = self.fact._a_perm if self.pre_bsr is self.bsr else None
+        if a_perm is None and self.pre_bsr is self.bsr and self.fact._a_src is not None:
+            self.krylov = DeviceKrylov.build(self.a, self.fact)   # layout from the input
+            return self
         if a_perm is None:
             from .analysis import permute_device
             a_perm = (self.bsr if self.fact._identity_perm

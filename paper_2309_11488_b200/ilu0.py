@@ -52,6 +52,7 @@ class Ilu0Factorization:
         self._identity_perm = identity
         self._source = source        # the (block-row-major) matrix that was factored
         self._a_perm = a_perm        # its unfactored plan-order copy (reused as operator)
+        self._a_src = None           # or (plan-order pattern, source map, input BSR)
         # 2-colour plans (csrc/factor2c.cu): the operator's SELL layout (U's
         # rows live there) and what is needed to rebuild the CSR factors
         self._two_colour = two_colour
@@ -277,8 +278,22 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
         return f
     D.find_diagonal(bsr.pat)                       # MissingDiagonal(first row)
     identity = plan.is_identity
-    a_perm = bsr if identity else permute_device(bsr, plan)
-    lu = D.DevBSR(a_perm.pat, b, a_perm.vals.clone())
+    a_src = None
+    if identity:
+        a_perm = bsr
+        lu = D.DevBSR(bsr.pat, b, bsr.vals.clone())
+    else:
+        # plan-order pattern + source map; the factor's values are gathered
+        # straight from the input (one pass), and the operator layout is
+        # later filled from the input the same way -- no permuted copy
+        ppat, src = D.permute_pattern(bsr.pat, plan.device("permutation"),
+                                      plan.device("inverse_permutation"))
+        vals = D.empty_f64(bsr.pat.nnz * b * b, dev)
+        if bsr.pat.nnz:
+            check(D.lib().b2s_gather_blocks(bsr.pat.nnz, b, D.ptr(src), D.ptr(bsr.vals),
+                                            D.ptr(vals), D.stream()), "gather_blocks")
+        lu = D.DevBSR(ppat, b, vals)
+        a_perm, a_src = None, (ppat, src, bsr)
     diag = D.find_diagonal(lu.pat)
     # group-aligned slices: a sweep never waits on a row of its own group
     # (same-group reads take the pre-sweep value, as the reference does)
@@ -301,6 +316,7 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
     check(D.lib().b2s_diag_tiles(smap.nslices, b, D.ptr(smap.row0), D.ptr(smap.nrows),
                                  D.ptr(inv), D.ptr(dtiles), D.stream()), "diag_tiles")
     f = Ilu0Factorization(plan, b, n, lu, inv, smap, lower, upper, dtiles, identity, a, a_perm)
+    f._a_src = a_src
     _maybe_tiles(f, plan, diag)
     return f
 

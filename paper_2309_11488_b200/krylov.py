@@ -196,6 +196,9 @@ class DeviceKrylov:
             smap = fact.smap
             if a_bsr is None and fact.a_sell is not None and fact._source is matrix:
                 sell = fact.a_sell   # 2-colour factorisation: the operator layout exists
+            elif a_bsr is None and fact._a_src is not None and fact._source is matrix:
+                ppat, src, inp = fact._a_src   # filled from the unpermuted input values
+                sell = D.Sell.build(smap, D.DevBSR(ppat, b, inp.vals), 0, src=src)
             elif a_bsr is None:
                 a_bsr = (fact._a_perm if fact._source is matrix
                          else _plan_order(D.DevBSR.upload(matrix), fact))
