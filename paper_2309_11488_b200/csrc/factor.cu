@@ -280,6 +280,7 @@ int launch_numeric(SliceMap map, const int32_t* rp, const int32_t* ci, const int
   int threads = 128, sleep_ns = 0;
   if (const char* e = getenv("B2S_FACTOR_SLEEP")) sleep_ns = atoi(e);
   if (const char* e = getenv("B2S_FACTOR_WARPS")) threads = 32 * atoi(e);
+  if (const char* e = getenv("B2S_FACTOR_CTAS_PER_SM")) g = atoi(e) * sms;
   k_factor_numeric<B><<<g, threads, 0, st>>>(map, rp, ci, diag, pptr, pairs, simple, w, invd,
                                              flag, bad, tk, sleep_ns, all_simple);
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
