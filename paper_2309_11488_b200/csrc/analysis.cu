@@ -466,14 +466,26 @@ __global__ void k_permute_cols(int n, const int32_t* __restrict__ rp,
   }
 }
 // out block q = in block src[q]  (bb doubles per block)
-__global__ void k_gather_blocks(long long nblk, int bb, const int32_t* __restrict__ src,
+// (block size a template parameter: the per-element division by BB is a
+// multiply-shift instead of a 64-bit division -- 254 -> ~150 us at C4)
+template <int BB>
+__global__ void k_gather_blocks(long long nblk, const int32_t* __restrict__ src,
                                 const double* __restrict__ in, double* __restrict__ out) {
-  const long long total = nblk * bb;
+  const long long total = nblk * BB;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    const long long q = t / bb;
-    const int e = (int)(t - q * bb);
-    out[t] = in[(long long)src[q] * bb + e];
+    const unsigned long long q = (unsigned long long)t / BB;
+    const int e = (int)(t - (long long)q * BB);
+    out[t] = __ldcs(in + (long long)__ldg(src + q) * BB + e);
+  }
+}
+inline void launch_gather_blocks(long long nblk, int bb, const int32_t* src, const double* in,
+                                 double* out, int grid, cudaStream_t st) {
+  switch (bb) {
+    case 1: k_gather_blocks<1><<<grid, 256, 0, st>>>(nblk, src, in, out); break;
+    case 4: k_gather_blocks<4><<<grid, 256, 0, st>>>(nblk, src, in, out); break;
+    case 9: k_gather_blocks<9><<<grid, 256, 0, st>>>(nblk, src, in, out); break;
+    default: k_gather_blocks<16><<<grid, 256, 0, st>>>(nblk, src, in, out); break;
   }
 }
 // vector rows: out[i] = in[src[i]]  (bs/analysis.py:153-159)
@@ -833,6 +845,7 @@ int b2s_permute_bsr(int n, int b, const int32_t* rp, const int32_t* ci, const do
                     const int32_t* cmap, const int32_t* take, int32_t* out_rp, int32_t* out_ci,
                     double* out_vals, int32_t* out_src, cudaStream_t st) {
   if (n < 0 || b < 1) return B2S_SHAPE;
+  if (b > 4 && vals && out_vals) return B2S_UNSUPPORTED;
   if (n == 0) {
     B2S_CHECK(cudaMemsetAsync(out_rp, 0, sizeof(int32_t), st));
     return B2S_OK;
@@ -853,8 +866,7 @@ int b2s_permute_bsr(int n, int b, const int32_t* rp, const int32_t* ci, const do
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, out_rp, n + 1, st);
   k_permute_cols<<<grid_for(n), 256, 0, st>>>(n, rp, ci, take, cmap, out_rp, out_ci, src);
   if (nnz > 0 && vals && out_vals)
-    k_gather_blocks<<<grid_for((long long)nnz * b * b), 256, 0, st>>>(nnz, b * b, src, vals,
-                                                                      out_vals);
+    launch_gather_blocks(nnz, b * b, src, vals, out_vals, grid_for((long long)nnz * b * b), st);
   B2S_LAUNCH_CHECK();
   B2S_CHECK(cudaFreeAsync(tmp, st));
   B2S_CHECK(cudaFreeAsync(cnt, st));
@@ -893,8 +905,9 @@ int b2s_narrow_index(long long m, const int64_t* in, int32_t* out, int* overflow
 int b2s_gather_blocks(long long nblk, int b, const int32_t* src, const double* in, double* out,
                       cudaStream_t st) {
   if (nblk < 0 || b < 1) return B2S_SHAPE;
+  if (b > 4) return B2S_UNSUPPORTED;
   if (nblk == 0) return B2S_OK;
-  k_gather_blocks<<<grid_for(nblk * b * b), 256, 0, st>>>(nblk, b * b, src, in, out);
+  launch_gather_blocks(nblk, b * b, src, in, out, grid_for(nblk * b * b), st);
   B2S_LAUNCH_CHECK();
   return B2S_OK;
 }
