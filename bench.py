@@ -279,7 +279,7 @@ def run_single(args):
             solver = DeviceSolver(a, bsr, cfg).setup()
             e1.record(st)
             x_d.zero_()
-            res = solver.solve(rhs_d, x_d, stop)
+            res = solver.solve(rhs_d, x_d, stop, x0_zero=True)   # x_d was zeroed
             e2.record(st)
             return solver, res, (e0, e1, e2)
         for _ in range(warmup):

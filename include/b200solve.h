@@ -331,6 +331,10 @@ typedef struct {
    * (n + mesh->nghost) * b long and the workspace sized by
    * b2s_bicgstab_workspace_bytes_mesh */
   const b2s_mesh* mesh;
+  /* 1: x0 is all zeros (the caller passed no initial guess): r0 = b - A 0 is
+   * b itself (bs/krylov.py:171 up to the sign of zero), so the initial
+   * residual SpMV (and, sharded, its ghost pull) is skipped */
+  int x0_zero;
 } b2s_bicg_args;
 
 typedef struct {

@@ -35,7 +35,7 @@ class BicgArgs(C.Structure):
                 ("u_sp", _P), ("u_cols", _P), ("u_vals", _P),
                 ("dinv_tiles", _P), ("tiles", _P), ("rhs", _P), ("x", _P), ("work", _P),
                 ("stream", _P), ("ngroups", _I), ("goff1", _I), ("gslice_host", _P),
-                ("fuse", _I), ("mesh", _P)]
+                ("fuse", _I), ("mesh", _P), ("x0_zero", _I)]
 
 
 class Mesh(C.Structure):

@@ -123,16 +123,18 @@ class DeviceSolver:
         self.krylov = DeviceKrylov.build(self.a, self.fact, a_perm)
         return self
 
-    def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria):
-        """x (input order) holds x0 on entry and the solution on exit."""
+    def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
+              x0_zero: bool = False):
+        """x (input order) holds x0 on entry and the solution on exit;
+        ``x0_zero``: the caller guarantees x == 0 (no initial guess)."""
         n, b = self.krylov.n, self.krylov.b
         f = self.fact
         if f._identity_perm:
-            return self.krylov.solve(rhs, x, stop)
+            return self.krylov.solve(rhs, x, stop, x0_zero=x0_zero)
         iperm = f.plan.device("inverse_permutation")
         bp = D.gather_rows(rhs, iperm, n, b)
         xp = D.gather_rows(x, iperm, n, b)
-        res = self.krylov.solve(bp, xp, stop)
+        res = self.krylov.solve(bp, xp, stop, x0_zero=x0_zero)
         x.copy_(D.gather_rows(xp, f.plan.device("permutation"), n, b)[: n * b])
         return res
 
@@ -201,7 +203,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         t1 = time.perf_counter()
         xd = x0d.clone()
         with trace.phase("krylov"):
-            res = solver.solve(rhs, xd, cfg.stop)
+            res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None)
         _sync()
         primary = _report(res, time.perf_counter() - t1, solver.plan.group_count)
         primary.setup_elapsed = setup
@@ -230,7 +232,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     fb_setup = time.perf_counter() - fb_t0
     t2 = time.perf_counter()
     xd = x0d.clone()
-    res = fb.solve(rhs, xd, fb_stop)
+    res = fb.solve(rhs, xd, fb_stop, x0_zero=x0 is None)
     _sync()
     report = _report(res, time.perf_counter() - t2, n)
     report.fallback_used = True

@@ -537,13 +537,17 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     int rc = B2S_OK;
     k_zero_words<<<1, 32, 0, user>>>(reinterpret_cast<unsigned*>(tickets), 16);
     k_copy<<<grid_v, 256, 0, user>>>(m, a->x, x0);
-    if (mesh) {
-      // the readiness/mailbox sequences restart from seq_base: clear `done`
-      // and the counters the halo kernels read before k_ctl_init runs
-      k_mesh_reset<<<1, 1, 0, user>>>(state);
-      halo(user, 0, a->x, &state->done);
+    // the readiness/mailbox sequences restart from seq_base: clear `done`
+    // and the counters the halo kernels read before k_ctl_init runs
+    if (mesh) k_mesh_reset<<<1, 1, 0, user>>>(state);
+    if (a->x0_zero) {   // r0 = b - A 0 = b: a copy and the |r0|^2 partials
+      k_copy<<<grid_v, 256, 0, user>>>(m, a->rhs, r);
+      k_dot_parts<<<np, 256, 0, user>>>(m, r, r, prr);
+    } else {
+      if (mesh) halo(user, 0, a->x, &state->done);
+      rc = launch_spmv(a->b, 3, np, map, Afull, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{},
+                       user);
     }
-    rc = launch_spmv(a->b, 3, np, map, Afull, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{}, user);
     if (rc == B2S_OK) {
       k_ctl_init<<<1, 256, 0, user>>>(state, prr, np, a->tol, a->maxit, dev_done, md);
       k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);

@@ -691,7 +691,7 @@ def solve_shards_mesh(shards, stop: StoppingCriteria, x0=None):
             if st is None:   # one persistent stream per shard (see b2s_mesh shared_device)
                 st = s._mesh_stream = torch.cuda.Stream(device=s.dev)
             with torch.cuda.stream(st):
-                results[i] = kr.solve(s.rhs_p, ms.x, stop, mesh=mesh)
+                results[i] = kr.solve(s.rhs_p, ms.x, stop, mesh=mesh, x0_zero=x0 is None)
                 st.synchronize()
         except Exception as exc:   # surfaced below, after every thread is back
             errors.append(exc)
@@ -757,7 +757,7 @@ def solve_shard_mesh_dist(shard: "Shard", stop: StoppingCriteria, x0=None, cache
     kr = _mesh_krylov(shard, ms)
     t0 = time.perf_counter()
     tm.append(t0)
-    res = kr.solve(shard.rhs_p, ms.x, stop, mesh=mesh)
+    res = kr.solve(shard.rhs_p, ms.x, stop, mesh=mesh, x0_zero=x0 is None)
     tm.append(time.perf_counter())
     rep = _mesh_report(res, t0, shard.plan.group_count)
     out = _mesh_outputs([shard])[0]

@@ -227,7 +227,7 @@ class DeviceKrylov:
         return cls(n, b, smap, sell, fact, work, fuse)
 
     def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
-              check_lag: int = 2, mesh=None) -> BicgResult:
+              check_lag: int = 2, mesh=None, x0_zero: bool = False) -> BicgResult:
         """Solve in place on plan-order device vectors (x: x0 in, x out).
         ``mesh``: a ``_lib.Mesh`` for one shard of a partitioned solve (x then
         carries the ghost rows after the owned ones; distributed.py)."""
@@ -261,6 +261,7 @@ class DeviceKrylov:
         args.stream = D.stream()
         if mesh is not None:
             args.mesh = C.addressof(mesh)
+        args.x0_zero = 1 if x0_zero else 0   # caller guarantees x == 0 on entry
         res = BicgResult()
         check(D.lib().b2s_bicgstab(C.byref(args), C.byref(res)), "bicgstab")
         return res
