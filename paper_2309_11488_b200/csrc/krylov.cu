@@ -157,7 +157,8 @@ __global__ void k_mesh_scalar(State* st, MeshDev mesh, int slot, const double* p
 // of the fused dot products, then run the control step over every partial
 // (the local kernels' at [0, poff), these at [poff, poff + grid)).  The
 // ghost entries are the last ones of their rows, so the row sum simply
-// continues in column order.
+// continues in column order.  kResidual: y = w - A_loc x already, subtract
+// the ghost products (the r0 / final true residuals).
 template <int B, int MODE>
 __global__ void __launch_bounds__(256) k_ghost_correct(int nb, const int32_t* __restrict__ brow,
                                                        const int32_t* __restrict__ bptr,
@@ -185,12 +186,13 @@ __global__ void __launch_bounds__(256) k_ghost_correct(int nb, const int32_t* __
       for (int c = 0; c < B; ++c) xv[c] = __ldcg(xg + g * B + c);
       matvec<B>(blk, xv, pr);
 #pragma unroll
-      for (int c = 0; c < B; ++c) acc[c] += pr[c];
+      for (int c = 0; c < B; ++c) acc[c] = MODE == kResidual ? acc[c] - pr[c] : acc[c] + pr[c];
     }
 #pragma unroll
     for (int c = 0; c < B; ++c) {
       y[row * B + c] = acc[c];
       const double d = acc[c] - yl[c];
+      if (MODE == kResidual) p0 = fma(d, acc[c] + yl[c], p0);   // r.r: new^2 - old^2
       if (MODE == kDotW) p0 = fma(w[row * B + c], d, p0);
       if (MODE == kSelfAndW) {
         p0 = fma(d, acc[c] + yl[c], p0);   // t.t: new^2 - old^2
@@ -478,7 +480,10 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // 2 colours + colour-0 rows of A == [diag, U row] (b2s_fuse_check): the
   // backward pass of colour 0 and the SpMV rows of colour 0 share one read
   // (sharded: the SpMV needs the owners' ghost rows of p^ between the two)
-  const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh->full_vals);
+  // sharded + fused: the operator passed is the local block, the boundary
+  // rows' ghost couplings come separately (b2s_mesh bnd_*)
+  const bool mesh_local = mesh && mesh->bnd_ptr != nullptr;
+  const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh_local);
   const int reset = (ilu && !phased) ? 1 : 0;  // sync-free sweeps need sentinel-filled outputs
   MeshDev md{};
   MeshHalo mh{};
@@ -508,9 +513,12 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   const int np = a->nparts;
   SliceMap map{a->nslices, a->row0, a->nrows};
   Sell A{a->a_sp, a->a_cols, a->a_vals};
-  // sharded + fused: A is the local block; the residuals need every column
+  // residuals: the whole operator when given, else the local block + the
+  // residual-mode ghost correction (np + kCorrCtas partials)
+  const bool res_corr = mesh_local && !mesh->full_vals;
   const Sell Afull = (mesh && mesh->full_vals)
                          ? Sell{mesh->full_sp, mesh->full_cols, mesh->full_vals} : A;
+  const int np_res = res_corr ? np + kCorrCtas : np;
   Sell L{a->l_sp, a->l_cols, a->l_vals}, U{a->u_sp, a->u_cols, a->u_vals};
   const int* done = &state->done;
   cudaStream_t user = a->stream;
@@ -547,9 +555,14 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       if (mesh) halo(user, 0, a->x, &state->done);
       rc = launch_spmv(a->b, 3, np, map, Afull, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{},
                        user);
+      if (res_corr)
+        launch_ghost_correct<kResidual>(a->b, mesh, a->x + m, r, nullptr, prr, nullptr, np,
+                                        nullptr, Ctl{}, user);
     }
+    if (a->x0_zero && res_corr)   // the correction's partial slots stay zero
+      k_zero_words<<<1, 32, 0, user>>>(reinterpret_cast<unsigned*>(prr + np), 2 * kCorrCtas);
     if (rc == B2S_OK) {
-      k_ctl_init<<<1, 256, 0, user>>>(state, prr, np, a->tol, a->maxit, dev_done, md);
+      k_ctl_init<<<1, 256, 0, user>>>(state, prr, np_res, a->tol, a->maxit, dev_done, md);
       k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
       k_copy<<<grid_v, 256, 0, user>>>(m, r, v);  // v is only read for k > 0
       if (ilu && !phased) {
@@ -777,7 +790,10 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   }
   int rc = launch_spmv(a->b, 3, np, map, Afull, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user);
   if (rc) return rc;
-  if (mesh) k_mesh_scalar<<<1, 256, 0, user>>>(state, md, kSlotFinal, pg, np, nullptr, pss);
+  if (res_corr)
+    launch_ghost_correct<kResidual>(a->b, mesh, a->x + m, t, nullptr, pg, nullptr, np, nullptr,
+                                    Ctl{}, user);
+  if (mesh) k_mesh_scalar<<<1, 256, 0, user>>>(state, md, kSlotFinal, pg, np_res, nullptr, pss);
   else k_reduce_parts<<<1, 256, 0, user>>>(pg, np, pss);
   int* bad = reinterpret_cast<int*>(ptt);
   k_zero_words<<<1, 32, 0, user>>>(reinterpret_cast<unsigned*>(bad), 1);

@@ -214,15 +214,25 @@ class Shard:
         perm = self.plan.device("permutation")
         iperm = self.plan.device("inverse_permutation")
         cmap = torch.cat([perm, torch.arange(R, R + self.G, dtype=torch.int32, device=dev)])
-        # (plan-order pattern + source map; the SELL layout is filled straight
-        # from the unpermuted values: no permuted value copy)
-        opat, src = D.permute_pattern(self.obsr.pat, cmap, iperm)
+        self._cmap, self._iperm = cmap, iperm
+        self._sell = None     # whole operator (ghost columns): built on first use
         self.smap = self.fact.smap
-        self.sell = D.Sell.build(self.smap, D.DevBSR(opat, self.b, self.obsr.vals), 0, src=src)
         self._bnd_row = perm.index_select(0, self._bnd_in)
         if getattr(self, "_requests", None) is not None:
             self.set_send(self._requests)
         return self
+
+    @property
+    def sell(self) -> "D.Sell":
+        """The whole operator in plan order with the ghost columns appended, as
+        a SELL layout filled straight from the unpermuted values through the
+        permutation's source map.  Built on first use: the fused 2-colour
+        device loop never needs it (local block + ghost correction)."""
+        if self._sell is None:
+            opat, src = D.permute_pattern(self.obsr.pat, self._cmap, self._iperm)
+            self._sell = D.Sell.build(self.smap, D.DevBSR(opat, self.b, self.obsr.vals), 0,
+                                      src=src)
+        return self._sell
 
     def _gather_ghost_blocks(self):
         nk = int(self._gh_idx.numel())
@@ -601,8 +611,7 @@ def _mesh_struct(shard: "Shard", ms: MeshState, owner_rows: dict, shared_device:
         m.nbnd = int(shard._bnd_in.numel())
         m.bnd_row, m.bnd_ptr = D.ptr(shard._bnd_row), D.ptr(shard._bnd_ptr)
         m.bnd_col, m.bnd_val = D.ptr(shard._bnd_col), D.ptr(shard._bnd_val)
-        m.full_sp, m.full_cols, m.full_vals = (D.ptr(shard.sell.sp), D.ptr(shard.sell.cols),
-                                               D.ptr(shard.sell.vals))
+        # (full_*: left null -- residuals use the local block + ghost correction)
     return m, keep
 
 

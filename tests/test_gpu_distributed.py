@@ -210,3 +210,23 @@ def test_mesh_halo_overlap_branch(monkeypatch):
     assert rep0.iterations == rep1.iterations
     for a, b in zip(xs0, xs1):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("backend", ["level", "color"])
+def test_mesh_nonzero_initial_guess(backend):
+    """x0 != 0: the initial residual takes x0's ghost rows (and, for fused
+    2-colour shards, the local block plus the residual-mode ghost correction)."""
+    from paper_2309_11488_b200.distributed import solve_shards_mesh
+    spec = P.GeneratorSpec(10, 8, 12, seed=5, diagonal_boost=1e-2)
+    shards, comm = local_solver(spec, 3, P.Backend.from_name(backend))
+    rng = np.random.default_rng(11)
+    x0 = [rng.uniform(-1, 1, s.R * s.b) for s in shards]
+    stop = P.StoppingCriteria(1e-8, 200)
+    rep, xs = solve_shards_mesh(shards, stop, x0=x0)
+    rep_h, xs_h = solve_shards(shards, comm, stop, x0=x0)
+    assert rep.converged and rep_h.converged
+    np.testing.assert_allclose(rep.initial_norm, rep_h.initial_norm, rtol=1e-12)
+    assert abs(rep.iterations - rep_h.iterations) <= max(1.0, 0.1 * rep_h.iterations)
+    x = np.concatenate([v.cpu().numpy() for v in xs])
+    xh = np.concatenate([v.cpu().numpy() for v in xs_h])
+    assert np.linalg.norm(x - xh) <= 1e-6 * np.linalg.norm(xh)
