@@ -9,13 +9,14 @@ fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import MissingDiagonal, ShapeError, SingularPivot
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libb200solve.so"
+LIB_PATH = Path(os.environ.get("B2S_LIB", _PKG / "libb200solve.so"))
 
 OK, SHAPE, MISSING_DIAGONAL, SINGULAR_PIVOT, CUDA_ERROR, UNSUPPORTED = range(6)
 
