@@ -1,6 +1,8 @@
 """Device-resident solve times of every BASELINE single-GPU configuration
 (C1 4k, C2 NORNE-scale masked, C3 350k heterogeneous, C4 1M), level and
-colour plans, tol 1e-8: setup, Krylov, iterations, Mcells/s.
+colour plans, tol 1e-8, plus SURVEY 8(d)'s variants: C1 and C4 at the
+reference default tol 0.01, and C4 with diagonal boost 1e-2 (harder) at
+tol 1e-8: setup, Krylov, iterations, Mcells/s.
 
 python tools/configs_bench.py    (one JSON line per config and plan)
 """
@@ -17,22 +19,26 @@ from paper_2309_11488_b200 import _device as D  # noqa: E402
 from paper_2309_11488_b200 import synthetic as S  # noqa: E402
 from paper_2309_11488_b200.bridge import DeviceSolver  # noqa: E402
 
-CONFIGS = {
-    "C1 20x20x10": lambda: P.generate(P.GeneratorSpec(20, 20, 10, seed=0)),
-    "C2 46x112x22 masked": lambda: S.generate_masked(46, 112, 22, seed=2309),
-    "C3 92x224x17 heterogeneous": lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=1.0,
-                                                                   diagonal_boost=1e-2),
-    "C4 100x100x100": lambda: P.generate(P.GeneratorSpec(100, 100, 100, seed=0)),
-}
+CONFIGS = [   # (name, generator, tol)
+    ("C1 20x20x10", lambda: P.generate(P.GeneratorSpec(20, 20, 10, seed=0)), 1e-8),
+    ("C1 20x20x10", lambda: P.generate(P.GeneratorSpec(20, 20, 10, seed=0)), 1e-2),
+    ("C2 46x112x22 masked", lambda: S.generate_masked(46, 112, 22, seed=2309), 1e-8),
+    ("C3 92x224x17 heterogeneous", lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=1.0,
+                                                                    diagonal_boost=1e-2), 1e-8),
+    ("C4 100x100x100", lambda: P.generate(P.GeneratorSpec(100, 100, 100, seed=0)), 1e-8),
+    ("C4 100x100x100", lambda: P.generate(P.GeneratorSpec(100, 100, 100, seed=0)), 1e-2),
+    ("C4 100x100x100 boost 1e-2",
+     lambda: P.generate(P.GeneratorSpec(100, 100, 100, diagonal_boost=1e-2, seed=0)), 1e-8),
+]
 st = torch.cuda.current_stream()
-for name, make in CONFIGS.items():
+for name, make, tol in CONFIGS:
     bnd = make()
     a = bnd.a
     bsr = D.DevBSR.upload(a)
     rhs = D.f64(bnd.rhs.data, bsr.vals.device)
     for backend in ("level", "color"):
         cfg = P.SolverConfig(backend=P.Backend.from_name(backend),
-                             stop=P.StoppingCriteria(1e-8, 200))
+                             stop=P.StoppingCriteria(tol, 200))
         x = torch.zeros_like(rhs)
         times = []
         solver = None
@@ -52,7 +58,7 @@ for name, make in CONFIGS.items():
         kr = sum(t[1] for t in times) / len(times)
         solver_groups = solver.plan.group_count
         solver = None
-        print(json.dumps({"config": name, "cells": a.num_block_rows, "backend": backend,
+        print(json.dumps({"config": name, "tol": tol, "cells": a.num_block_rows, "backend": backend,
                           "groups": solver_groups, "iterations": float(res.iterations),
                           "converged": bool(res.converged), "setup_ms": round(su, 3),
                           "krylov_ms": round(kr, 3), "solve_ms": round(su + kr, 3),
