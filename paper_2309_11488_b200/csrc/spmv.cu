@@ -163,12 +163,16 @@ __global__ void __launch_bounds__(256) k_spmv(SliceMap map, int s0, int s1, int 
     double acc[B];
 #pragma unroll
     for (int c = 0; c < B; ++c) acc[c] = 0.0;
-    // two entries per step, all loads of the pair issued before any math
+    // two entries per step, all loads of the pair issued before any math;
+    // the next pair's column indices load one step ahead, so a step's x
+    // gathers do not wait behind its own index loads
+    int cn0 = width > 0 ? __ldcs(a.cols + slot0 + lane) : -1;
+    int cn1 = width > 1 ? __ldcs(a.cols + slot0 + 32 + lane) : -1;
     for (int k = 0; k < width; k += 2) {
       const bool two = k + 1 < width;
-      int col[2];
-      col[0] = __ldcs(a.cols + slot0 + 32 * k + lane);
-      col[1] = two ? __ldcs(a.cols + slot0 + 32 * (k + 1) + lane) : -1;
+      int col[2] = {cn0, cn1};
+      cn0 = k + 2 < width ? __ldcs(a.cols + slot0 + 32 * (k + 2) + lane) : -1;
+      cn1 = k + 3 < width ? __ldcs(a.cols + slot0 + 32 * (k + 3) + lane) : -1;
       double blk[2][BB], xv[2][B];
 #pragma unroll
       for (int e = 0; e < BB; ++e) {
