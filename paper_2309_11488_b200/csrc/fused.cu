@@ -63,11 +63,14 @@ __global__ void __launch_bounds__(256) k_bwd_spmv(SliceMap map, int s0, int s1, 
     // two entries per step, every load of the pair issued before any math
     // (the compiler's own schedule of a one-entry loop left one L2 round
     // trip per entry exposed in one of the two instantiations)
+    // (the next pair's column indices load one step ahead, as in k_spmv)
+    int cn0 = width > 1 ? __ldcs(a.cols + slot0 + 32 + lane) : -1;
+    int cn1 = width > 2 ? __ldcs(a.cols + slot0 + 64 + lane) : -1;
     for (int k = 1; k < width; k += 2) {
       const bool two = k + 1 < width;
-      int col[2];
-      col[0] = __ldcs(a.cols + slot0 + 32 * k + lane);
-      col[1] = two ? __ldcs(a.cols + slot0 + 32 * (k + 1) + lane) : -1;
+      int col[2] = {cn0, cn1};
+      cn0 = k + 2 < width ? __ldcs(a.cols + slot0 + 32 * (k + 2) + lane) : -1;
+      cn1 = k + 3 < width ? __ldcs(a.cols + slot0 + 32 * (k + 3) + lane) : -1;
       double blk[2][BB], dep[2][B];
 #pragma unroll
       for (int e = 0; e < BB; ++e) {
