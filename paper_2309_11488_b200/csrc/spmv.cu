@@ -139,7 +139,7 @@ __global__ void k_diag_tiles(int nslices, int bb, const int32_t* __restrict__ ro
 
 
 template <int B, int MODE>
-__global__ void __launch_bounds__(256) k_spmv(SliceMap map, int s0, int s1, int poff, Sell a,
+__global__ void __launch_bounds__(256, B <= 3 ? 4 : 1) k_spmv(SliceMap map, int s0, int s1, int poff, Sell a,
                                               const double* __restrict__ x,
                                               double* __restrict__ y,
                                               const double* __restrict__ w,
@@ -155,24 +155,44 @@ __global__ void __launch_bounds__(256) k_spmv(SliceMap map, int s0, int s1, int 
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   double p0 = 0.0, p1 = 0.0;
+  // the column indices of the next entry pair load one step ahead -- across
+  // slice boundaries too: a slice's last step fetches the next slice's first
+  // pair -- so a step's x gathers never wait behind their own index loads
+  int nslot0 = 0, nwidth = 0, cn0 = -1, cn1 = -1;
+  if (s0 + gw < s1) {
+    nslot0 = a.sp[s0 + gw];
+    nwidth = (a.sp[s0 + gw + 1] - nslot0) >> 5;
+    cn0 = nwidth > 0 ? __ldcs(a.cols + nslot0 + lane) : -1;
+    cn1 = nwidth > 1 ? __ldcs(a.cols + nslot0 + 32 + lane) : -1;
+  }
   for (int s = s0 + gw; s < s1; s += nw) {
-    const int slot0 = a.sp[s];
-    const int width = (a.sp[s + 1] - slot0) >> 5;
+    const int slot0 = nslot0;
+    const int width = nwidth;
+    const bool more = s + nw < s1;
+    if (more) {
+      nslot0 = a.sp[s + nw];
+      nwidth = (a.sp[s + nw + 1] - nslot0) >> 5;
+    }
     const bool ok = lane < map.nrows[s];
     const long long row = (long long)map.row0[s] + lane;
     double acc[B];
 #pragma unroll
     for (int c = 0; c < B; ++c) acc[c] = 0.0;
-    // two entries per step, all loads of the pair issued before any math;
-    // the next pair's column indices load one step ahead, so a step's x
-    // gathers do not wait behind its own index loads
-    int cn0 = width > 0 ? __ldcs(a.cols + slot0 + lane) : -1;
-    int cn1 = width > 1 ? __ldcs(a.cols + slot0 + 32 + lane) : -1;
+    // two entries per step, all loads of the pair issued before any math
+    if (width == 0) {   // no step to fetch the next slice's first pair in
+      cn0 = more && nwidth > 0 ? __ldcs(a.cols + nslot0 + lane) : -1;
+      cn1 = more && nwidth > 1 ? __ldcs(a.cols + nslot0 + 32 + lane) : -1;
+    }
     for (int k = 0; k < width; k += 2) {
       const bool two = k + 1 < width;
       int col[2] = {cn0, cn1};
-      cn0 = k + 2 < width ? __ldcs(a.cols + slot0 + 32 * (k + 2) + lane) : -1;
-      cn1 = k + 3 < width ? __ldcs(a.cols + slot0 + 32 * (k + 3) + lane) : -1;
+      if (k + 2 < width) {
+        cn0 = __ldcs(a.cols + slot0 + 32 * (k + 2) + lane);
+        cn1 = k + 3 < width ? __ldcs(a.cols + slot0 + 32 * (k + 3) + lane) : -1;
+      } else {
+        cn0 = more && nwidth > 0 ? __ldcs(a.cols + nslot0 + lane) : -1;
+        cn1 = more && nwidth > 1 ? __ldcs(a.cols + nslot0 + 32 + lane) : -1;
+      }
       double blk[2][BB], xv[2][B];
 #pragma unroll
       for (int e = 0; e < BB; ++e) {
