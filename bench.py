@@ -72,17 +72,53 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling (every 100 ms) across the timed region."""
+    """SM clock and clock-event reasons sampled across the timed region: NVML
+    every 10 ms from a thread (at least one sample however short the region),
+    else ``nvidia-smi -lms 100`` (whose first sample can come after a short
+    region has ended)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+    BITS = (0x8, 0x40, 0x20, 0x4)   # nvmlClocksEventReason{Hw,HwThermal,SwThermal}Slowdown, SwPowerCap
 
     def __init__(self, index=0):
         self.index, self.proc, self.out = index, None, None
+        self.nvml = self.handle = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            try:   # the CUDA ordinal's PCI address (CUDA_VISIBLE_DEVICES may renumber)
+                import torch
+                pr = torch.cuda.get_device_properties(index)
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                self.handle = N.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.handle = N.nvmlDeviceGetHandleByIndex(index)
+            self.nvml = N
+        except Exception:
+            self.nvml = None
+
+    def _loop(self):
+        N = self.nvml
+        while True:
+            try:
+                self.samples.append((N.nvmlDeviceGetClockInfo(self.handle, N.NVML_CLOCK_SM),
+                                     N.nvmlDeviceGetMaxClockInfo(self.handle, N.NVML_CLOCK_SM),
+                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.handle)))
+            except Exception:
+                pass
+            if self.done.wait(0.01):
+                break
 
     def start(self):
+        if self.nvml is not None:
+            import threading
+            self.samples, self.done = [], threading.Event()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
+            self.thread.start()
+            return
         self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.proc = subprocess.Popen(
@@ -93,6 +129,15 @@ class Clocks:
             self.proc = None
 
     def stop(self):
+        if self.nvml is not None:
+            self.done.set()
+            self.thread.join(timeout=5)
+            sm = sorted(float(r[0]) for r in self.samples)
+            reasons = sorted({n for r in self.samples for n, b in zip(self.NAMES, self.BITS)
+                              if r[2] & b})
+            return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                    "sm_max_mhz": max(float(r[1]) for r in self.samples) if sm else None,
+                    "reasons": reasons, "samples": len(sm), "sampler": "nvml 10 ms"}
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -112,7 +157,8 @@ class Clocks:
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm),
+                "sampler": "nvidia-smi 100 ms"}
 
 
 # ---------------------------------------------------------------------------
