@@ -289,6 +289,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1 or args.force_dist:
+        if "RANK" not in os.environ:   # --force-dist without a launcher: a world of one
+            os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0",
+                               "MASTER_ADDR": "127.0.0.1",
+                               "MASTER_PORT": os.environ.get("MASTER_PORT", "29517")})
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from bench_dist import run_distributed
         return run_distributed(args, world, rank, local, METRIC, UNIT, Clocks, peaks,
