@@ -218,6 +218,14 @@ int b2s_tiles_apply(int b, const void* handle, const double* r, double* y, doubl
 int b2s_dot(long long m, const double* a, const double* b, int nparts, double* parts,
             double* out, cudaStream_t stream);
 int b2s_all_finite(long long m, const double* a, int* bad, cudaStream_t stream);
+/* Inner product in the reference's exact summation order (bs/krylov.py:30-47,
+ * REDUCTION_CHUNK = 64): parts[c] = numpy's np.add.reduceat of a*b over the
+ * c-th 64-element chunk (ceil(m/64) doubles), *total = np.cumsum(parts)[-1]
+ * (skipped when total is NULL).  Bit-identical to the reference
+ * (csrc/refdot.cu); used by the public dot/norm/dot_partials and the
+ * reported initial residual norm, not by the Krylov loop. */
+int b2s_dot_chunked(long long m, const double* a, const double* b, double* parts,
+                    double* total, cudaStream_t stream);
 int b2s_reduce(const double* parts, int np, double* out, cudaStream_t stream);
 
 /* BiCGStab vector steps with host scalars (multi-GPU loop; bs/krylov.py:201-233):

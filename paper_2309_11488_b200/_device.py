@@ -451,6 +451,19 @@ def dot(a: torch.Tensor, b: torch.Tensor, m: int) -> float:
     return float(out.item())
 
 
+def dot_chunked(a: torch.Tensor, b: torch.Tensor, m: int, partials: bool = False):
+    """The reference's chunk-64 inner product (bs/krylov.py:30-47), bit for bit
+    (csrc/refdot.cu).  Returns the device total (1 double) or, with
+    ``partials``, the per-chunk partial sums."""
+    dev = a.device
+    np_ = (int(m) + 63) // 64
+    parts = torch.empty(max(np_, 1), dtype=torch.float64, device=dev)
+    out = None if partials else torch.empty(1, dtype=torch.float64, device=dev)
+    check(lib().b2s_dot_chunked(int(m), ptr(a), ptr(b), ptr(parts), ptr(out), stream()),
+          "dot_chunked")
+    return parts[:np_] if partials else out
+
+
 def fill_sentinel(v: torch.Tensor, m: int):
     check(lib().b2s_fill_sentinel(m, ptr(v), stream()), "fill_sentinel")
 

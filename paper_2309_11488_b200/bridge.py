@@ -28,8 +28,8 @@ from .analysis import (ParallelPlan, Strategy, _device_plan, sequential_plan)
 from .blockcore import BlockMatrix, BlockVector
 from .errors import SingularPivot, SolveFailed
 from .ilu0 import Ilu0Factorization, factor_device, prepare_two_colour
-from .krylov import (DEFAULT_MAX_ITERATIONS, DeviceKrylov, SolveReport, StoppingCriteria,
-                     WellAugmentedOperator, _REASONS, bicgstab)
+from .krylov import (DEFAULT_MAX_ITERATIONS, DeviceKrylov, RefNorm, SolveReport,
+                     StoppingCriteria, WellAugmentedOperator, _REASONS, bicgstab)
 from .wells import WellMode, WellSet, fold_into_matrix
 
 
@@ -110,11 +110,11 @@ class DeviceSolver:
             self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr, prep)
         if self.pre_bsr is self.bsr and self.fact.a_sell is not None:
             # 2-colour factorisation: the operator's SELL layout already exists
-            self.krylov = DeviceKrylov.build(self.a, self.fact)
+            self.krylov = DeviceKrylov.build(self.a, self.fact, same_values=True)
             return self
         a_perm = self.fact._a_perm if self.pre_bsr is self.bsr else None
         if a_perm is None and self.pre_bsr is self.bsr and self.fact._a_src is not None:
-            self.krylov = DeviceKrylov.build(self.a, self.fact)   # layout from the input
+            self.krylov = DeviceKrylov.build(self.a, self.fact, same_values=True)   # from the input
             return self
         if a_perm is None:
             from .analysis import permute_device
@@ -139,8 +139,9 @@ class DeviceSolver:
         return res
 
 
-def _report(res, elapsed, groups) -> SolveReport:
-    return SolveReport(bool(res.converged), float(res.iterations), float(res.initial_norm),
+def _report(res, elapsed, groups, norm0: float | None = None) -> SolveReport:
+    n0 = float(res.initial_norm) if norm0 is None else norm0
+    return SolveReport(bool(res.converged), float(res.iterations), n0,
                        float(res.final_norm), elapsed, groups,
                        failure_reason=None if res.converged else _REASONS.get(res.reason, "budget"),
                        gpu_launches=int(res.graph_launches) * int(res.kernels_per_iteration))
@@ -148,6 +149,18 @@ def _report(res, elapsed, groups) -> SolveReport:
 
 def _sync():
     torch.cuda.current_stream().synchronize()
+
+
+def _initial_residual(bsr: "D.DevBSR", rhs: torch.Tensor, x0d: torch.Tensor | None):
+    """b - A x0 in input order (bs/krylov.py:175) for the reported initial
+    norm; b itself when there is no initial guess."""
+    if x0d is None:
+        return rhs
+    n, b = bsr.pat.n, bsr.b
+    smap = D.SliceMap.plain(n, rhs.device)
+    y = D.empty_f64(n * b, rhs.device)
+    D.spmv(smap, D.Sell.build(smap, bsr, 0), b, x0d, y)
+    return rhs - y[: n * b]
 
 
 def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells=None,
@@ -189,6 +202,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
 
     pre_bsr, pre_mat = bsr, a_sys
     primary = None
+    norm0 = None
     x = None
     try:
         if cfg.jacobi_partitions > 0:
@@ -198,6 +212,8 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
             pre_mat, _ = drop_cross_blocks(a_sys, parts)
             pre_bsr = D.DevBSR.upload(pre_mat)
         solver = DeviceSolver(a_sys, bsr, cfg, pre_bsr, pre_mat).setup()
+        # the reported ||r0|| in the reference's order, beside the loop
+        norm0 = RefNorm(_initial_residual(bsr, rhs, None if x0 is None else x0d), n * bs)
         _sync()
         setup = time.perf_counter() - t0
         t1 = time.perf_counter()
@@ -205,7 +221,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         with trace.phase("krylov"):
             res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None)
         _sync()
-        primary = _report(res, time.perf_counter() - t1, solver.plan.group_count)
+        primary = _report(res, time.perf_counter() - t1, solver.plan.group_count, norm0.value())
         primary.setup_elapsed = setup
         x = xd
     except SingularPivot as exc:
@@ -228,13 +244,16 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         fb_report = _failed_report(f"singular pivot in row {exc.row}")
         fb_report.fallback_used = True
         raise SolveFailed(primary, fb_report)
+    if norm0 is None:   # the primary failed before its loop: ||r0|| from here
+        norm0 = RefNorm(_initial_residual(bsr, rhs, None if x0 is None else x0d), n * bs)
     _sync()
     fb_setup = time.perf_counter() - fb_t0
     t2 = time.perf_counter()
     xd = x0d.clone()
     res = fb.solve(rhs, xd, fb_stop, x0_zero=x0 is None)
     _sync()
-    report = _report(res, time.perf_counter() - t2, n)
+    report = _report(res, time.perf_counter() - t2, n,
+                     norm0.value() if norm0 is not None else None)
     report.fallback_used = True
     report.setup_elapsed = primary.setup_elapsed + fb_setup
     report.elapsed += primary.elapsed

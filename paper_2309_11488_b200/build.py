@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libb200solve.so"
 SOURCES = ["analysis.cu", "spmv.cu", "factor.cu", "ilu0.cu", "fused.cu", "factor2c.cu", "tiles.cu", "krylov.cu",
-           "jacobi.cu", "wells.cu"]
+           "jacobi.cu", "wells.cu", "refdot.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

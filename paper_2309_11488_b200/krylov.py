@@ -42,35 +42,64 @@ _REASONS = {2: "breakdown", 3: "numerical", 4: "budget"}
 
 def dot_partials(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """Per-chunk partial sums of a*b over consecutive 64-element chunks
-    (bs/krylov.py:30-36), computed on the device."""
+    (bs/krylov.py:30-36), computed on the device in numpy's exact order."""
     a = np.asarray(a, dtype=np.float64).reshape(-1)
     b = np.asarray(b, dtype=np.float64).reshape(-1)
     if a.size == 0:
         return np.zeros(0)
     dev = D.require_cuda()
-    prod = D.f64(a, dev) * D.f64(b, dev)
-    pad = (-prod.numel()) % REDUCTION_CHUNK
-    if pad:
-        prod = torch.cat([prod, prod.new_zeros(pad)])
-    return prod.view(-1, REDUCTION_CHUNK).sum(dim=1).cpu().numpy()
+    return D.dot_chunked(D.f64(a, dev), D.f64(b, dev), a.size, partials=True).cpu().numpy()
 
 
 def dot_arrays(a: np.ndarray, b: np.ndarray) -> float:
+    """Chunk partials accumulated strictly left to right (bs/krylov.py:39-44):
+    bit-identical to the reference (csrc/refdot.cu)."""
     a = np.asarray(a, dtype=np.float64).reshape(-1)
     b = np.asarray(b, dtype=np.float64).reshape(-1)
     if a.size == 0:
         return 0.0
     dev = D.require_cuda()
-    return D.dot(D.f64(a, dev), D.f64(b, dev), a.size)
+    return float(D.dot_chunked(D.f64(a, dev), D.f64(b, dev), a.size).item())
 
 
 def norm_array(a: np.ndarray) -> float:
     return float(np.sqrt(dot_arrays(a, a)))
 
 
+_SIDE: dict = {}
+
+
+def _side_stream(dev: torch.device) -> torch.cuda.Stream:
+    s = _SIDE.get(dev.index)
+    if s is None:
+        s = _SIDE[dev.index] = torch.cuda.Stream(device=dev)
+    return s
+
+
+class RefNorm:
+    """``||r0||`` in the reference's summation order (bs/krylov.py:176,
+    norm_array), computed on a side stream while the Krylov loop runs: the
+    reported ``initial_norm`` is then bit-identical to
+    ``norm_array(b - A x0)``; the loop's own stopping target uses its
+    fixed-order device reduction (within an ulp of it)."""
+
+    def __init__(self, r0: torch.Tensor, m: int):
+        side = _side_stream(r0.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._sq = D.dot_chunked(r0, r0, m) if m else None
+            self._ev = torch.cuda.Event()
+            self._ev.record(side)
+        r0.record_stream(side)
+
+    def value(self) -> float:
+        self._ev.synchronize()
+        return 0.0 if self._sq is None else float(np.sqrt(float(self._sq.item())))
+
+
 def dot(a: BlockVector, b: BlockVector) -> float:
-    """Deterministic inner product of two block vectors (fixed-order device
-    reduction: identical results on every run)."""
+    """Deterministic chunked inner product of two block vectors (the
+    reference's order, bit for bit)."""
     if a.data.size != b.data.size:
         raise ShapeError("vectors have different lengths")
     return dot_arrays(a.data, b.data)
@@ -84,7 +113,12 @@ def norm(a: BlockVector) -> float:
 # operators and reports
 
 class MatrixOperator:
-    """Plain blocked SpMV operator (bs/krylov.py:63-81)."""
+    """Plain blocked SpMV operator (bs/krylov.py:63-81).
+
+    The reference reads ``matrix.values`` at every apply.  Here the device copy
+    is taken at the start of every public call (``apply_array``/``apply``,
+    ``bicgstab``), so in-place changes to the host arrays between calls are
+    always seen; inside one call the host arrays are read once."""
 
     def __init__(self, a: BlockMatrix):
         self.matrix = a.as_block_row_major()
@@ -98,19 +132,24 @@ class MatrixOperator:
     def num_blocks(self) -> int:
         return self.matrix.num_block_rows
 
-    def device(self) -> DeviceOperator:
-        if self._dev is None:
+    def device(self, refresh: bool = False) -> DeviceOperator:
+        if self._dev is None or refresh:
             self._dev = DeviceOperator(self.matrix)
         return self._dev
+
+    def prepare(self):
+        """Device copies of the current host arrays (start of a public call)."""
+        self.device(refresh=True)
 
     def apply_device(self, x: torch.Tensor, y: torch.Tensor):
         self.device().apply(x, y)
 
     def apply_array(self, x: np.ndarray) -> np.ndarray:
+        self.prepare()
         op = self.device()
         dev = op.bsr.pat.rp.device
         y = D.empty_f64(op.n * op.b, dev)
-        op.apply(D.f64(x, dev), y)
+        self.apply_device(D.f64(x, dev), y)
         return y[: op.n * op.b].cpu().numpy()
 
     def apply(self, x: BlockVector) -> BlockVector:
@@ -119,23 +158,22 @@ class MatrixOperator:
 
 class WellAugmentedOperator(MatrixOperator):
     """SpMV followed by every well's -C^T D^-1 B x (bs/krylov.py:84-94), both on
-    the device (csrc/spmv.cu, csrc/wells.cu)."""
+    the device (csrc/spmv.cu, csrc/wells.cu).  Like the reference
+    (wells.apply_contributions_array), a COUPLED or empty set adds nothing:
+    its wells are already folded into the matrix."""
 
     def __init__(self, a: BlockMatrix, wells):
         super().__init__(a)
         self.wells = wells
 
+    def _separate(self) -> bool:
+        from .wells import WellMode
+        return self.wells.mode is not WellMode.COUPLED and not self.wells.is_empty
+
     def apply_device(self, x: torch.Tensor, y: torch.Tensor):
         self.device().apply(x, y)
-        self.wells.device(self.block_size, self.num_blocks).apply(x, y)
-
-    def apply_array(self, x: np.ndarray) -> np.ndarray:
-        op = self.device()
-        dev = op.bsr.pat.rp.device
-        xd = D.f64(x, dev)
-        y = D.empty_f64(op.n * op.b, dev)
-        self.apply_device(xd, y)
-        return y[: op.n * op.b].cpu().numpy()
+        if self._separate():
+            self.wells.device(self.block_size, self.num_blocks).apply(x, y)
 
 
 @dataclass(frozen=True)
@@ -188,19 +226,24 @@ class DeviceKrylov:
 
     @classmethod
     def build(cls, matrix: BlockMatrix, fact: Ilu0Factorization | None,
-              a_bsr: "D.DevBSR" = None) -> "DeviceKrylov":
+              a_bsr: "D.DevBSR" = None, same_values: bool = False) -> "DeviceKrylov":
+        """``same_values``: the caller guarantees ``matrix``'s host values are
+        the ones ``fact`` was computed from (one solve_with_fallback call), so
+        the factorisation's device copy of them can serve as the operator.
+        Otherwise (public bicgstab) the operator is uploaded afresh."""
         n, b = matrix.num_block_rows, matrix.block_size
         fuse_env = os.environ.get("B2S_FUSE", "1") != "0"
         sell = None
         if fact is not None:
             smap = fact.smap
-            if a_bsr is None and fact.a_sell is not None and fact._source is matrix:
+            reuse = same_values and fact._source is matrix
+            if a_bsr is None and fact.a_sell is not None and reuse:
                 sell = fact.a_sell   # 2-colour factorisation: the operator layout exists
-            elif a_bsr is None and fact._a_src is not None and fact._source is matrix:
+            elif a_bsr is None and fact._a_src is not None and reuse:
                 ppat, src, inp = fact._a_src   # filled from the unpermuted input values
                 sell = D.Sell.build(smap, D.DevBSR(ppat, b, inp.vals), 0, src=src)
             elif a_bsr is None:
-                a_bsr = (fact._a_perm if fact._source is matrix
+                a_bsr = (fact._a_perm if reuse and fact._a_perm is not None
                          else _plan_order(D.DevBSR.upload(matrix), fact))
             dev = fact.dtiles.device
         else:
@@ -287,6 +330,7 @@ def bicgstab(op, precond, b: BlockVector, x0: BlockVector | None = None,
         stop = StoppingCriteria()
     if b.block_size != op.block_size or b.num_blocks != op.num_blocks:
         raise ShapeError("right-hand side does not match the operator")
+    x0_given = x0 is not None
     if x0 is None:
         x0 = BlockVector.zeros(op.num_blocks, op.block_size)
     elif x0.block_size != b.block_size or x0.num_blocks != b.num_blocks:
@@ -297,27 +341,35 @@ def bicgstab(op, precond, b: BlockVector, x0: BlockVector | None = None,
     # WellAugmentedOperator and other operators/preconditioners: host-driven
     # loop over device vectors (device operators stay on the device)
     if native:
-        return _bicgstab_native(op, precond, b, x0, stop)
+        return _bicgstab_native(op, precond, b, x0, stop, x0_zero=x0_given is False)
     return _bicgstab_generic(op, precond, b, x0, stop)
 
 
 def _bicgstab_native(op: MatrixOperator, fact, b: BlockVector, x0: BlockVector,
-                     stop: StoppingCriteria, krylov: DeviceKrylov | None = None):
+                     stop: StoppingCriteria, krylov: DeviceKrylov | None = None,
+                     x0_zero: bool = False):
     t0 = time.perf_counter()
     kr = krylov or DeviceKrylov.build(op.matrix, fact)
     n, bs = kr.n, kr.b
     dev = kr.work.device
     bd, xd = D.f64(b.data, dev), D.f64(x0.data, dev)
+    if x0_zero:
+        r0 = bd
+    else:   # input-order residual through the public operator (bs/krylov.py:175)
+        y = D.empty_f64(n * bs, dev)
+        op.apply_device(xd, y)
+        r0 = bd - y[: n * bs]
+    norm0 = RefNorm(r0, n * bs)
     perm = fact is not None and not fact._identity_perm
     if perm:
         iperm = fact.plan.device("inverse_permutation")
         bd, xd = D.gather_rows(bd, iperm, n, bs), D.gather_rows(xd, iperm, n, bs)
-    res = kr.solve(bd, xd, stop)
+    res = kr.solve(bd, xd, stop, x0_zero=x0_zero)
     if perm:
         xd = D.gather_rows(xd, fact.plan.device("permutation"), n, bs)
     x = D.to_host(xd, n * bs)
     groups = fact.plan.group_count if fact is not None else 0
-    rep = SolveReport(bool(res.converged), float(res.iterations), float(res.initial_norm),
+    rep = SolveReport(bool(res.converged), float(res.iterations), norm0.value(),
                       float(res.final_norm), time.perf_counter() - t0, groups,
                       failure_reason=None if res.converged else _REASONS.get(res.reason, "budget"),
                       gpu_launches=int(res.graph_launches) * int(res.kernels_per_iteration))
@@ -336,6 +388,8 @@ def _bicgstab_generic(op, precond, b: BlockVector, x0: BlockVector, stop: Stoppi
     dev = D.require_cuda()
     m = b.data.size
 
+    if hasattr(op, "prepare"):
+        op.prepare()
     if hasattr(op, "apply_device"):
         def A(v):   # device operator (SpMV [+ wells]): no host round trip
             y = torch.empty_like(v)
@@ -360,8 +414,11 @@ def _bicgstab_generic(op, precond, b: BlockVector, x0: BlockVector, stop: Stoppi
         def M(v):
             return D.f64(apply_m(v.cpu().numpy()), dev)
 
+    def dt(u, v):   # the reference's chunk-64 order, bit for bit (csrc/refdot.cu)
+        return float(D.dot_chunked(u, v, m).item()) if m else 0.0
+
     def nrm(v):
-        return float(np.sqrt(D.dot(v, v, m))) if m else 0.0
+        return float(np.sqrt(dt(v, v)))
 
     x = D.f64(x0.data, dev) if m else torch.zeros(0, dtype=torch.float64, device=dev)
     bd = D.f64(b.data, dev) if m else x.clone()
@@ -384,14 +441,14 @@ def _bicgstab_generic(op, precond, b: BlockVector, x0: BlockVector, stop: Stoppi
     its = 0.0
     reason = "budget"
     for k in range(stop.max_iterations):
-        rho = D.dot(rhat, r, m)
+        rho = dt(rhat, r)
         if abs(rho) < _BREAKDOWN_FLOOR:
             reason = "breakdown"
             break
         p = r.clone() if k == 0 else r + ((rho / rho_prev) * (alpha / omega)) * (p - omega * v)
         phat = M(p)
         v = A(phat)
-        gamma = D.dot(rhat, v, m)
+        gamma = dt(rhat, v)
         if abs(gamma) < _BREAKDOWN_FLOOR:
             reason = "breakdown"
             break
@@ -407,11 +464,11 @@ def _bicgstab_generic(op, precond, b: BlockVector, x0: BlockVector, stop: Stoppi
             return BlockVector(x.cpu().numpy(), b.block_size), report(True, its, ns)
         shat = M(s)
         t = A(shat)
-        tt = D.dot(t, t, m)
+        tt = dt(t, t)
         if tt < _BREAKDOWN_FLOOR:
             reason = "breakdown"
             break
-        omega = D.dot(t, s, m) / tt
+        omega = dt(t, s) / tt
         if abs(omega) < _BREAKDOWN_FLOOR:
             reason = "breakdown"
             break

@@ -12,26 +12,17 @@ page-locked host memory, ready for the solver's DMA upload.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
 
 from .blockcore import BlockMatrix, BlockVector, Layout, SparsityPattern
 from .errors import BlockingError, DuplicateEntry, IndexOutOfRange, ParseError, ShapeError
+from .synthetic import BundleMeta, SystemBundle
 from .wells import MultisegmentWell, StandardWell, WellMode, WellSet
 
 _MATRIX_HEADER = ("matrixmarket", "matrix", "coordinate", "real", "general")
 _ARRAY_HEADER = ("matrixmarket", "matrix", "array", "real", "general")
-
-
-@dataclass
-class BundleMeta:
-    """bs/io.py:27-31."""
-
-    name: str
-    block_size: int
-    grid_dims: tuple | None = None
 
 
 def rhs_path(path) -> Path:
@@ -323,7 +314,6 @@ def _parse_wells(lines) -> WellSet:
 def read_system(path, pinned: bool = False):
     """Read a system written by :func:`write_system` (bs/io.py:175-190):
     a missing rhs file yields zeros, missing wells an empty set."""
-    from .synthetic import SystemBundle
     p = Path(path)
     a = _read_matrix(p, pinned)
     rp = rhs_path(p)
@@ -333,7 +323,7 @@ def read_system(path, pinned: bool = False):
         rhs = BlockVector.zeros(a.num_block_rows, a.block_size)
     wp = wells_path(p)
     wells = _read_wells(wp) if wp.exists() else WellSet()
-    return SystemBundle(a, rhs, p.stem, None, wells)
+    return SystemBundle(a, rhs, wells, BundleMeta(name=p.stem, block_size=a.block_size))
 
 
 __all__ = ["BundleMeta", "read_system", "write_system", "rhs_path", "wells_path"]

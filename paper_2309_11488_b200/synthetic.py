@@ -30,6 +30,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .blockcore import BlockMatrix, BlockVector, Layout, SparsityPattern
+from .errors import ShapeError
 
 
 @dataclass(frozen=True)
@@ -63,23 +64,28 @@ class GeneratorSpec:
 
 
 @dataclass
+class BundleMeta:
+    """bs/io.py:27-31."""
+
+    name: str
+    block_size: int
+    grid_dims: tuple | None = None
+
+
+@dataclass
 class SystemBundle:
+    """bs/io.py:33-44: same fields, order and shape checks."""
+
     a: BlockMatrix
     rhs: BlockVector
-    name: str
-    grid_dims: tuple | None = None
-    wells: object = None     # WellSet (empty when the spec has no wells)
+    wells: object          # WellSet
+    meta: BundleMeta
 
     def __post_init__(self):
-        if self.wells is None:
-            from .wells import WellSet
-            self.wells = WellSet()
-
-    @property
-    def meta(self):
-        """bs/io.py:27-31 BundleMeta view (name, block size, grid)."""
-        from .mmio import BundleMeta
-        return BundleMeta(self.name, self.a.block_size, self.grid_dims)
+        if self.rhs.block_size != self.a.block_size:
+            raise ShapeError("rhs block size differs from the matrix")
+        if self.rhs.num_blocks != self.a.num_block_rows:
+            raise ShapeError("rhs length differs from the matrix")
 
 
 def _faces(nx, ny, nz, active=None):
@@ -128,11 +134,13 @@ def _assemble(n, lo, hi, tvals, b, boost, rng):
     return rp, dst, blk
 
 
-def _bundle(rp, ci, blk, rhs, b, name, dims):
+def _bundle(rp, ci, blk, rhs, b, name, dims, wells=None):
+    from .wells import WellSet
     n = rp.size - 1
     pat = SparsityPattern(n, rp, ci)
     a = BlockMatrix(pat, b, blk.reshape(-1), Layout.BLOCK_ROW_MAJOR)
-    return SystemBundle(a, BlockVector(rhs, b), name, dims)
+    return SystemBundle(a, BlockVector(rhs, b), WellSet() if wells is None else wells,
+                        BundleMeta(name, b, dims))
 
 
 def generate(spec: GeneratorSpec) -> SystemBundle:
@@ -147,9 +155,8 @@ def generate(spec: GeneratorSpec) -> SystemBundle:
                         zip(faces, (spec.tx, spec.ty, spec.tz))])
     rp, ci, blk = _assemble(n, lo, hi, t, b, spec.diagonal_boost, rng)
     rhs = rng.uniform(-1.0, 1.0, size=n * b)
-    out = _bundle(rp, ci, blk, rhs, b, f"synthetic-{nx}x{ny}x{nz}", (nx, ny, nz))
-    out.wells = _generate_wells(spec, rng)
-    return out
+    wells = _generate_wells(spec, rng)
+    return _bundle(rp, ci, blk, rhs, b, f"synthetic-{nx}x{ny}x{nz}", (nx, ny, nz), wells)
 
 
 def _generate_wells(spec: GeneratorSpec, rng):

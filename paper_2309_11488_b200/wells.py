@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import hashlib
 import warnings
 from dataclasses import dataclass, field
 
@@ -233,12 +234,31 @@ class WellSet:
     def is_empty(self) -> bool:
         return not self.standard and not self.multisegment
 
+    def _fingerprint(self) -> bytes:
+        """Digest of every host array of every well (the reference reads them
+        at each apply, bs/wells.py:125-162): a device copy is reused only
+        while the wells are unchanged -- values updated in place (e.g.
+        d_dense plus _refactor), wells appended or removed."""
+        h = hashlib.blake2b(digest_size=16)
+        for w in (*self.standard, None, *self.multisegment):
+            if w is None:
+                h.update(b"|")
+                continue
+            for k, v in sorted(vars(w).items()):
+                for j, arr in enumerate(v if isinstance(v, tuple) else (v,)):
+                    if isinstance(arr, np.ndarray):
+                        h.update(f"{k}{j}{arr.dtype.str}{arr.shape}".encode())
+                        h.update(np.ascontiguousarray(arr).tobytes())
+        return h.digest()
+
     def device(self, nb: int, num_cells: int) -> DeviceWells:
         key = (nb, num_cells)
         cache = self.__dict__.setdefault("_dev", {})
-        if key not in cache:
-            cache[key] = DeviceWells(self, nb, num_cells)
-        return cache[key]
+        fp = self._fingerprint()
+        hit = cache.get(key)
+        if hit is None or hit[0] != fp:
+            hit = cache[key] = (fp, DeviceWells(self, nb, num_cells))
+        return hit[1]
 
     def apply_contributions(self, x: BlockVector, y: BlockVector) -> BlockVector:
         if self.mode is WellMode.COUPLED:

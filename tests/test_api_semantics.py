@@ -1,0 +1,85 @@
+"""API semantics the reference has and a device port could lose: bundle
+signature and shape checks (bs/io.py:33-44), COUPLED well sets add nothing
+in the operator (bs/krylov.py:84-94 via bs/wells.py:187-202), and in-place
+changes of host arrays between calls are seen (the reference reads the host
+arrays at every apply)."""
+
+import numpy as np
+import pytest
+from numpy.testing import assert_allclose, assert_array_equal
+
+import paper_2309_11488_b200 as P
+
+
+def test_system_bundle_reference_signature():
+    g = P.generate(P.GeneratorSpec(3, 3, 2, well_count=1, well_depth=2, seed=1))
+    b = P.SystemBundle(g.a, g.rhs, g.wells, P.BundleMeta("x", 3, (3, 3, 2)))
+    assert b.wells is g.wells and b.meta.name == "x"
+    assert g.meta == P.BundleMeta("synthetic-3x3x2", 3, (3, 3, 2))
+    with pytest.raises(P.ShapeError):
+        P.SystemBundle(g.a, P.BlockVector(np.zeros(9), 3), g.wells, g.meta)
+    with pytest.raises(P.ShapeError):
+        P.SystemBundle(g.a, P.BlockVector(np.zeros(g.rhs.data.size), 1), g.wells, g.meta)
+
+
+def test_bundle_round_trip_keeps_wells(tmp_path):
+    g = P.generate(P.GeneratorSpec(4, 3, 3, well_count=2, well_depth=2, seed=2))
+    P.write_system(g, tmp_path / "case.mtx")
+    back = P.read_system(tmp_path / "case.mtx")
+    assert back.meta.name == "case" and len(back.wells.standard) == 2
+    assert_array_equal(back.a.values, g.a.values)
+
+
+@pytest.mark.gpu
+def test_coupled_set_adds_nothing_in_the_operator():
+    g = P.generate(P.GeneratorSpec(5, 4, 4, well_count=2, well_depth=3, seed=3))
+    coupled = P.WellSet(g.wells.standard, g.wells.multisegment, P.WellMode.COUPLED)
+    x = np.random.default_rng(0).uniform(-1, 1, g.rhs.data.size)
+    plain = P.MatrixOperator(g.a).apply_array(x)
+    assert_array_equal(P.WellAugmentedOperator(g.a, coupled).apply_array(x), plain)
+    assert_array_equal(P.WellAugmentedOperator(g.a, P.WellSet()).apply_array(x), plain)
+    sep = P.WellAugmentedOperator(g.a, g.wells).apply_array(x)
+    assert not np.array_equal(sep, plain)
+
+
+@pytest.mark.gpu
+def test_in_place_changes_are_seen_between_calls():
+    g = P.generate(P.GeneratorSpec(5, 4, 4, well_count=1, well_depth=3,
+                                   well_kind="multisegment", seed=4))
+    x = np.random.default_rng(1).uniform(-1, 1, g.rhs.data.size)
+    op = P.WellAugmentedOperator(g.a, g.wells)
+    y0 = op.apply_array(x)
+    # matrix values changed in place
+    g.a.values *= 2.0
+    y1 = op.apply_array(x)
+    assert not np.array_equal(y0, y1)
+    # a well's D changed in place and refactored (bs/wells.py:106-114)
+    w = g.wells.multisegment[0]
+    w.d_dense *= 3.0
+    w._refactor()
+    y2 = op.apply_array(x)
+    want = P.spmv(g.a, P.BlockVector(x, 3)).data.copy()
+    g.wells.apply_contributions_array(x, want, 3)
+    assert not np.array_equal(y1, y2)
+    assert_allclose(y2, want, rtol=0, atol=1e-13 * np.abs(want).max())
+    # a well appended
+    extra = P.generate(P.GeneratorSpec(5, 4, 4, well_count=1, well_depth=2, seed=9)).wells
+    g.wells.standard.extend(extra.standard)
+    y3 = op.apply_array(x)
+    assert not np.array_equal(y2, y3)
+
+
+@pytest.mark.gpu
+def test_bicgstab_operator_reads_current_values():
+    """decompose(A) then A.values changed: the operator uses the new values,
+    the preconditioner the old ones -- as in the reference."""
+    g = P.generate(P.GeneratorSpec(6, 5, 4, seed=5))
+    for plan in (P.graph_color, P.level_schedule):
+        a = P.BlockMatrix(g.a.pattern, 3, g.a.values.copy())
+        fact = P.decompose(a, plan(a.pattern))
+        a.values *= 1.5
+        x, rep = P.bicgstab(P.MatrixOperator(a), fact, g.rhs,
+                            stop=P.StoppingCriteria(1e-10, 200))
+        assert rep.converged
+        r = g.rhs.data - P.spmv(a, x).data
+        assert np.linalg.norm(r) <= 1e-10 * np.linalg.norm(g.rhs.data) * 1.01
