@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--boost", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-full", action="store_true",
+                    help="skip the single-core full-workload port solve in cpu_baseline")
     ap.add_argument("--no-other-plan", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--ref-slab", type=int, default=2, help="z-planes of the CPU sample")
@@ -178,6 +180,40 @@ def host_info():
 
 
 def cpu_port_sample(args, nx, ny, slab, per_op=False):
+    """Single-core CPU solve of a bounded slab of the workload: the unmodified
+    reference (baseline/_ref) when installed, else the oracle port; with
+    ``per_op`` also SURVEY 8(d)'s per-op times on the same sample."""
+    bs = reference_module()
+    if bs is None:
+        return _port_sample(args, nx, ny, slab, per_op)
+    g = bs.generate(bs.GeneratorSpec(nx, ny, slab, seed=0, diagonal_boost=args.boost))
+    a, rhs = g.a, g.rhs
+    cfg = bs.SolverConfig(backend=bs.Backend(args.backend), stop=bs.StoppingCriteria(args.tol, 200))
+    t0 = time.perf_counter()
+    _, rep = bs.solve_with_fallback(cfg, a, rhs)
+    dt = time.perf_counter() - t0
+    cells = a.num_block_rows
+    out = {"seconds": dt, "cells": cells, "iterations": rep.iterations, "kind": "reference",
+           "value": cells / dt / 1e6,
+           "sample": f"unmodified reference solve_with_fallback ({args.backend} plan + ILU0 + "
+                     f"BiCGStab to tol {args.tol:g}) of GeneratorSpec({nx},{ny},{slab},seed=0): "
+                     f"{cells} cells, {rep.iterations} its, {dt:.2f} s, 1 core"}
+    if per_op:
+        def t(fn):
+            t1 = time.perf_counter()
+            res = fn()
+            return res, (time.perf_counter() - t1) * 1e3
+        plan, t_plan = t(lambda: (bs.level_schedule if args.backend == "level"
+                                  else bs.graph_color)(a.pattern))
+        f, t_fact = t(lambda: bs.decompose(a, plan))
+        _, t_spmv = t(lambda: bs.spmv(a, rhs))
+        _, t_apply = t(lambda: f.apply_array(rhs.data))
+        out["per_op_ms"] = {"plan": t_plan, "decompose": t_fact, "spmv": t_spmv,
+                            "ilu0_apply": t_apply}
+    return out
+
+
+def _port_sample(args, nx, ny, slab, per_op=False):
     from oracle import port as O
     from paper_2309_11488_b200.synthetic import GeneratorSpec, generate
     g = generate(GeneratorSpec(nx, ny, slab, seed=0, diagonal_boost=args.boost))
@@ -187,11 +223,11 @@ def cpu_port_sample(args, nx, ny, slab, per_op=False):
     x, rep, groups, fb = O.solve(rp, ci, v3, g.rhs.data, args.backend, args.tol)
     dt = time.perf_counter() - t0
     cells = a.num_block_rows
-    out = {"seconds": dt, "cells": cells, "iterations": rep.iterations,
+    out = {"seconds": dt, "cells": cells, "iterations": rep.iterations, "kind": "port",
            "value": cells / dt / 1e6,
            "sample": f"oracle port full solve ({args.backend} plan + ILU0 + BiCGStab to tol "
                      f"{args.tol:g}) of GeneratorSpec({nx},{ny},{slab},seed=0): {cells} cells, "
-                     f"{rep.iterations} its, {dt:.2f} s"}
+                     f"{rep.iterations} its, {dt:.2f} s, 1 core"}
     if per_op:   # the reference's per-op costs on the same sample (ms)
         def t(fn):
             t1 = time.perf_counter()
@@ -207,55 +243,144 @@ def cpu_port_sample(args, nx, ny, slab, per_op=False):
     return out
 
 
-def _ref_worker(payload):
-    """One independent CPU-port solve (a process of the reference arm's pool)."""
-    import argparse
-    opts, nx, ny, slab = payload
-    return cpu_port_sample(argparse.Namespace(**opts), nx, ny, slab)
+def full_port_solve(args, nx, ny, nz):
+    """One single-core oracle-port solve of the whole workload (pins the
+    per-cell extrapolation of the slab samples; ~45 s at C4)."""
+    s = _port_sample(args, nx, ny, nz)
+    return {"value": s["value"], "unit": UNIT, "seconds": s["seconds"],
+            "iterations": s["iterations"], "cores": 1, "kind": "port", "sample": s["sample"]}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the UNMODIFIED reference (baseline/_ref) on the host cores
+
+REF_DIR = ROOT / "baseline" / "_ref"
+_SLABS: list = []          # per-worker slab systems, set before the pool forks
+
+
+def reference_module():
+    """``blocksolve`` from baseline/_ref (pip --target install of the
+    unmodified /root/reference/pkg), or None when absent."""
+    if not (REF_DIR / "blocksolve").is_dir():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import blocksolve
+    return blocksolve
+
+
+def c4_slabs(nx, ny, nz, boost, parts, bs=None):
+    """Generate the C4 system (the reference's own generator when available;
+    ours is draw-for-draw identical) and cut it into ``parts`` contiguous
+    z-slabs: each slab's diagonal block (couplings to other slabs dropped,
+    the paper's MPI block-Jacobi decomposition) and its rhs rows."""
+    import numpy as np
+    if bs is not None:
+        g = bs.generate(bs.GeneratorSpec(nx, ny, nz, seed=0, diagonal_boost=boost))
+    else:
+        from paper_2309_11488_b200.synthetic import GeneratorSpec, generate
+        g = generate(GeneratorSpec(nx, ny, nz, seed=0, diagonal_boost=boost))
+    rp, ci = g.a.pattern.row_pointers, g.a.pattern.column_indices
+    v3 = g.a.as_block_row_major().values.reshape(-1, 3, 3)
+    rhs = g.rhs.data
+    plane = nx * ny
+    bounds = np.linspace(0, nz, parts + 1).round().astype(int)
+    slabs = []
+    for z0, z1 in zip(bounds[:-1], bounds[1:]):
+        r0, r1 = z0 * plane, z1 * plane
+        lo, hi = int(rp[r0]), int(rp[r1])
+        cols = ci[lo:hi]
+        keep = (cols >= r0) & (cols < r1)
+        rows = np.repeat(np.arange(r1 - r0), np.diff(rp[r0:r1 + 1]))
+        srp = np.zeros(r1 - r0 + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows[keep], minlength=r1 - r0), out=srp[1:])
+        slabs.append((srp, (cols[keep] - r0).astype(np.int64),
+                      np.ascontiguousarray(v3[lo:hi][keep]).reshape(-1),
+                      rhs[3 * r0:3 * r1].copy()))
+    return slabs, rp.size - 1
+
+
+def _ref_slab_solve(task):
+    """One slab solve by the unmodified reference's solve_with_fallback (or
+    the oracle port when the reference is not installed)."""
+    k, backend, tol = task
+    rp, ci, vals, rhs = _SLABS[k]
+    bs = reference_module()
+    t0 = time.perf_counter()
+    if bs is not None:
+        a = bs.BlockMatrix(bs.SparsityPattern(rp.size - 1, rp, ci), 3, vals)
+        b = bs.BlockVector(rhs, 3)
+        t0 = time.perf_counter()
+        cfg = bs.SolverConfig(backend=bs.Backend(backend), stop=bs.StoppingCriteria(tol, 200))
+        _, rep = bs.solve_with_fallback(cfg, a, b)
+        its, conv = rep.iterations, rep.converged
+    else:
+        from oracle import port as O
+        _, rep, _, _ = O.solve(rp, ci, vals.reshape(-1, 3, 3), rhs, backend, tol)
+        its, conv = rep.iterations, rep.converged
+    return {"cells": rp.size - 1, "seconds": time.perf_counter() - t0, "iterations": its,
+            "converged": bool(conv)}
 
 
 def run_reference(args):
-    """The reference's CPU path on the host, with every core it can use: the
-    reference solves one system single-threaded (numpy), and runs independent
-    systems concurrently (its CLI's thread pool), so each step is
-    one round of independent solves, one per core (a process each, one BLAS
-    thread each); value = cells solved / the round's longest solve."""
+    """The reference's own CPU path on the host, every core: each step solves
+    the full C4 workload (1,000,000 cells) as ``W`` contiguous z-slab systems
+    (C4's diagonal blocks, one per core, the paper's MPI-style block-Jacobi
+    decomposition), each by the UNMODIFIED reference ``solve_with_fallback``
+    single-threaded (baseline/_ref); value = cells / the step's wall time.
+    Rank 0 only (the other ranks exit without work)."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
     import multiprocessing
-    nx, ny, nz = (int(v) for v in args.grid.split(","))
-    workers = max(1, min(os.cpu_count() or 1, int(os.environ.get("B2S_REF_WORKERS", "64"))))
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"
-    opts = {"boost": args.boost, "backend": args.backend, "tol": args.tol}
-    payload = [(opts, nx, ny, args.ref_slab)] * workers
+    nx, ny, nz = (int(v) for v in args.grid.split(","))
+    workers = max(1, min(os.cpu_count() or 1, int(os.environ.get("B2S_REF_WORKERS", "64")), nz))
+    bs = reference_module()
+    kind = "reference" if bs is not None else "port"
+    slabs, cells = c4_slabs(nx, ny, nz, args.boost, workers, bs)
+    _SLABS[:] = slabs
+    tasks = [(k, args.backend, args.tol) for k in range(len(slabs))]
     rounds = []
-    with multiprocessing.get_context("spawn").Pool(workers) as pool:
+    with multiprocessing.get_context("fork").Pool(workers) as pool:
         for _ in range(args.warmup):
-            pool.map(_ref_worker, payload)
+            pool.map(_ref_slab_solve, tasks, chunksize=1)
         for _ in range(args.steps):
-            res = pool.map(_ref_worker, payload)
-            rounds.append((sum(r["cells"] for r in res), max(r["seconds"] for r in res), res))
-    cells = sum(r[0] for r in rounds)
-    secs = sum(r[1] for r in rounds)
-    value = cells / secs / 1e6
-    sample = rounds[-1][2][0]["sample"]
+            t0 = time.perf_counter()
+            res = pool.map(_ref_slab_solve, tasks, chunksize=1)
+            rounds.append((time.perf_counter() - t0, res))
+    secs = sum(r[0] for r in rounds)
+    value = cells * len(rounds) / secs / 1e6
+    last = rounds[-1][1]
+    its = sorted({r["iterations"] for r in last})
+    per_slab = sum(r["seconds"] for r in last) / len(last)
+    sample = (f"{'unmodified reference (baseline/_ref) solve_with_fallback' if bs else 'oracle port'}"
+              f" ({args.backend} plan + ILU0 + BiCGStab to tol {args.tol:g}) of each of "
+              f"{len(slabs)} z-slab diagonal blocks of C4 GeneratorSpec({nx},{ny},{nz},seed=0), "
+              f"{cells} cells per step, one process per core; slab iterations {its}, "
+              f"{per_slab:.1f} s per slab solve")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / len(rounds),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator, seed 0)",
-            "config": {"workload": f"C4 GeneratorSpec({nx},{ny},{nz},seed=0) per GPU; CPU "
-                                   f"step = {workers} independent {args.ref_slab}-plane slabs "
-                                   f"of it solved concurrently, one per core",
-                       "backend": args.backend, "tol": args.tol, "block_size": 3},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                             "sample": f"{workers} x [{sample}] concurrently per step",
-                             "single_core_value": sum(r[2][0]["value"] for r in rounds) / len(rounds),
+            "config": bench_config(args, nx, ny, nz, cells),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
+                             "sample": sample,
+                             "single_core_value": cells / per_slab / len(slabs) / 1e6,
+                             "all_converged": all(r["converged"] for _, rr in rounds for r in rr),
                              "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def bench_config(args, nx, ny, nz, cells):
+    """The workload both arms run (identical dict: same_config)."""
+    return {"workload": f"C4 GeneratorSpec({nx},{ny},{nz},seed=0): {cells} cells, 3x3 blocks, "
+                        f"full solve (plan+permute+ILU0+BiCGStab) to tol {args.tol:g}",
+            "backend": args.backend, "tol": args.tol, "cells_per_gpu": cells,
+            "block_size": 3, "boost": args.boost}
 
 
 def count_step_kernels(fn):
@@ -448,8 +573,10 @@ def run_single(args):
     cpu = None
     if not args.no_cpu:
         s = cpu_port_sample(args, nx, ny, args.ref_slab, per_op=True)
-        cpu = {"value": s["value"], "unit": UNIT, "cores": 1, "kind": "port",
+        cpu = {"value": s["value"], "unit": UNIT, "cores": 1, "kind": s["kind"],
                "sample": s["sample"], "per_op_ms": s["per_op_ms"], "host": host_info()}
+        if not args.no_cpu_full:
+            cpu["full_workload_single_core"] = full_port_solve(args, nx, ny, nz)
 
     clk = main_run.pop("clocks", None)
     launches = main_run.pop("gpu_launches")
@@ -465,12 +592,9 @@ def run_single(args):
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": main_run["solve_ms"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
-        "config": {"workload": f"C4 GeneratorSpec({nx},{ny},{nz},seed=0): {n} cells, 3x3 "
-                               f"blocks, full solve (plan+permute+ILU0+BiCGStab) to tol "
-                               f"{args.tol:g}",
-                   "backend": args.backend, "tol": args.tol, "cells_per_gpu": n,
-                   "nnzb_per_gpu": nnz, "parallelism": "single GPU",
-                   "l2": "inputs larger than L2 (579 MB matrix vs 126 MB)"},
+        "config": bench_config(args, nx, ny, nz, n),
+        "nnzb_per_gpu": nnz, "parallelism": "single GPU",
+        "l2": "inputs larger than L2 (579 MB matrix vs 126 MB)",
         **main_run,
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": dom[1], "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom[1] / hbm,

@@ -1,0 +1,154 @@
+"""Full-size elementwise fixtures, computed by the UNMODIFIED reference.
+
+For the BASELINE configs at their full sizes (C2 46x112x22 masked, C3
+92x224x17 heterogeneous in two variants, C4 100^3) and both parallel plans,
+this records what the reference computes, sampled at fixed seeded positions
+(the full arrays would be hundreds of MB):
+
+* plan: sha256 of the int32 row_group and int64 permutation (bit-exact pin);
+* decompose: 2,048 sampled blocks of the plan-order combined L\\U values and
+  2,048 sampled inverse diagonal blocks, plus the Frobenius norms;
+* spmv and Ilu0Factorization.apply of a seeded vector: 4,096 sampled
+  entries plus norms;
+* one BiCGStab iteration (budget 1: p-hat, v, s, s-hat, t, x): the returned
+  x sampled -- this is what the device's fused passes compute;
+* with ``--solve``: the full tol-1e-8 solve's report and an x sample, and
+  with ``--band K`` the reference's own iteration spread under 1e-14 factor
+  noise (K perturbed solves).
+
+Run in the build container only (the reference is absent on the GPU box):
+    python tests/golden/make_fullsize.py c2 c3 c4 [c3s --solve --band 3]
+Writes tests/golden/full_<case>.npz.  Test infrastructure.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.dont_write_bytecode = True
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parents[1]))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+
+import blocksolve as bs  # noqa: E402
+
+from paper_2309_11488_b200 import synthetic as S  # noqa: E402
+
+# C3s: the SURVEY.md §8(d) specification (sigma 2-3, boost 1e-4..1e-6)
+CASES = {
+    "c2": lambda: S.generate_masked(46, 112, 22, seed=2309),
+    "c3": lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=1.0, diagonal_boost=1e-2),
+    "c3s": lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=2.5, diagonal_boost=1e-5),
+    "c4": lambda: bs.generate(bs.GeneratorSpec(100, 100, 100, seed=0)),
+}
+NSAMP_BLOCKS = 2048
+NSAMP_VEC = 4096
+VEC_SEED = 99      # tests regenerate the input vector from this seed
+SAMPLE_SEED = 7
+
+
+def sha(a, dtype) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=dtype).tobytes()).hexdigest()
+
+
+def input_vector(n_scalars: int) -> np.ndarray:
+    return np.random.default_rng(VEC_SEED).uniform(-1.0, 1.0, n_scalars)
+
+
+def samples(n_blocks: int, n_scalars: int):
+    rng = np.random.default_rng(SAMPLE_SEED)
+    blk = np.sort(rng.choice(n_blocks, min(NSAMP_BLOCKS, n_blocks), replace=False))
+    vec = np.sort(rng.choice(n_scalars, min(NSAMP_VEC, n_scalars), replace=False))
+    return blk, vec
+
+
+def ref_matrix(bundle):
+    a = bundle.a
+    p = bs.SparsityPattern(a.num_block_rows, a.pattern.row_pointers, a.pattern.column_indices)
+    return (bs.BlockMatrix(p, a.block_size, a.values.copy()),
+            bs.BlockVector(bundle.rhs.data.copy(), a.block_size))
+
+
+def band_iterations(a, f, rhs, tol, k, seed=1234):
+    rng = np.random.default_rng(seed)
+    its = []
+    for _ in range(k):
+        for ph in (f._forward, f._backward):
+            ph.blocks[:] *= 1.0 + 1e-14 * rng.standard_normal(ph.blocks.shape)
+        f._diag_bwd[:] *= 1.0 + 1e-14 * rng.standard_normal(f._diag_bwd.shape)
+        _, r2 = bs.bicgstab(bs.MatrixOperator(a), f, rhs, stop=bs.StoppingCriteria(tol, 200))
+        its.append(r2.iterations)
+    return its
+
+
+def run(case: str, solve: bool, band: int, tol: float = 1e-8):
+    a, rhs = ref_matrix(CASES[case]())
+    n, b, nnzb = a.num_block_rows, a.block_size, a.pattern.num_blocks
+    blk, vec = samples(nnzb, n * b)
+    rows = np.sort(np.random.default_rng(SAMPLE_SEED + 1).choice(n, min(NSAMP_BLOCKS, n),
+                                                                 replace=False))
+    x = input_vector(n * b)
+    out = {"n": np.array(n), "nnzb": np.array(nnzb), "blk_idx": blk, "vec_idx": vec,
+           "row_idx": rows}
+    meta = {"case": case, "n": n, "nnzb": nnzb}
+    y = bs.spmv(a, bs.BlockVector(x, b)).data
+    out["spmv_sample"], out["spmv_norm"] = y[vec], np.array(np.linalg.norm(y))
+    for s in ("level", "color"):
+        t0 = time.time()
+        plan = bs.level_schedule(a.pattern) if s == "level" else bs.graph_color(a.pattern)
+        out[f"{s}_groups"] = np.array(plan.group_count)
+        out[f"{s}_row_group_sha"] = np.array(sha(plan.row_group, np.int32))
+        out[f"{s}_perm_sha"] = np.array(sha(plan.permutation, np.int64))
+        f = bs.decompose(a, plan)
+        lu = f.combined.values.reshape(-1, b, b)
+        out[f"{s}_lu_sample"] = lu[blk]
+        out[f"{s}_lu_norm"] = np.array(np.linalg.norm(lu))
+        out[f"{s}_lu_absmax"] = np.array(np.abs(lu).max())
+        invd = f.inverted_diagonals.reshape(-1, b, b)
+        out[f"{s}_invd_sample"] = invd[rows]
+        out[f"{s}_invd_norm"] = np.array(np.linalg.norm(invd))
+        out[f"{s}_invd_absmax"] = np.array(np.abs(invd).max())
+        z = f.apply(bs.BlockVector(x, b)).data
+        out[f"{s}_apply_sample"], out[f"{s}_apply_norm"] = z[vec], np.array(np.linalg.norm(z))
+        out[f"{s}_apply_absmax"] = np.array(np.abs(z).max())
+        x1, r1 = bs.bicgstab(bs.MatrixOperator(a), f, rhs, stop=bs.StoppingCriteria(tol, 1))
+        out[f"{s}_it1_x_sample"] = x1.data[vec]
+        out[f"{s}_it1_x_norm"] = np.array(np.linalg.norm(x1.data))
+        out[f"{s}_it1_x_absmax"] = np.array(np.abs(x1.data).max())
+        out[f"{s}_it1_report"] = np.array([r1.converged, r1.iterations, r1.initial_norm,
+                                           r1.final_norm])
+        m = {"groups": plan.group_count, "setup_s": round(time.time() - t0, 1)}
+        if solve:
+            t1 = time.time()
+            xs, rep = bs.bicgstab(bs.MatrixOperator(a), f, rhs, stop=bs.StoppingCriteria(tol, 200))
+            out[f"{s}_report"] = np.array([rep.converged, rep.iterations, rep.initial_norm,
+                                           rep.final_norm])
+            out[f"{s}_x_sample"] = xs.data[vec]
+            out[f"{s}_x_norm"] = np.array(np.linalg.norm(xs.data))
+            m.update(iterations=rep.iterations, converged=bool(rep.converged),
+                     solve_s=round(time.time() - t1, 1))
+            if band:
+                its = [rep.iterations] + band_iterations(a, f, rhs, tol, band)
+                out[f"{s}_band"] = np.array([min(its), max(its)])
+                m["band"] = [min(its), max(its)]
+        meta[s] = m
+    np.savez_compressed(HERE / f"full_{case}.npz", **out)
+    print(json.dumps(meta), flush=True)
+
+
+def main(argv):
+    solve = "--solve" in argv
+    band = int(argv[argv.index("--band") + 1]) if "--band" in argv else 0
+    cases = [c for c in argv if c in CASES]
+    for c in cases:
+        run(c, solve, band)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
