@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--boost", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--wells", type=int, default=20,
+                    help="standard wells of the extra wells run (0: skip it)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cpu-full", action="store_true",
                     help="skip the single-core full-workload port solve in cpu_baseline")
@@ -426,6 +428,7 @@ def main():
 
 
 def run_single(args):
+    import numpy as np
     import torch
 
     import paper_2309_11488_b200 as P
@@ -444,14 +447,14 @@ def run_single(args):
     x_d = torch.zeros(n * b, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream()
 
-    def measure(backend_name, steps, warmup, clocks=None):
+    def measure(backend_name, steps, warmup, clocks=None, wells=None):
         cfg = P.SolverConfig(backend=P.Backend.from_name(backend_name), stop=stop)
         out = {}
 
         def step():
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record(st)
-            solver = DeviceSolver(a, bsr, cfg).setup()
+            solver = DeviceSolver(a, bsr, cfg, wells=wells).setup()
             e1.record(st)
             x_d.zero_()
             res = solver.solve(rhs_d, x_d, stop, x0_zero=True)   # x_d was zeroed
@@ -495,6 +498,18 @@ def run_single(args):
         other = measure(oname, max(3, args.steps // 2), 2)
         other.pop("solver")
         other["backend"] = oname
+
+    # ---- the same system with separately applied standard wells (SURVEY
+    # 8(f) row 1): the well terms run inside the device loop
+    wells_run = None
+    if args.wells > 0:
+        wg = P.generate(P.GeneratorSpec(nx, ny, nz, seed=0, diagonal_boost=args.boost,
+                                        well_count=args.wells, well_depth=min(nz, 10)))
+        assert np.array_equal(wg.a.values, a.values)   # the wells are drawn after A and b
+        wells_run = measure(args.backend, max(3, args.steps // 2), 2, wells=wg.wells)
+        wells_run.pop("solver")
+        wells_run.update({"wells": args.wells, "kind": "standard", "perforations_per_well":
+                          min(nz, 10)})
 
     # ---- per-kernel CUDA-event timing on the headline solver's data
     solver = main_run.pop("solver")
@@ -603,7 +618,7 @@ def run_single(args):
                     "spmv_bytes": spmv_bytes, "ilu_apply_us": t_sweeps,
                     "ilu_apply_gbs": apply_gbs, "ilu_apply_frac": apply_gbs / hbm,
                     "ilu_apply_bytes": apply_bytes},
-        "other_plan": other, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+        "other_plan": other, "wells_run": wells_run, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
         "gpu_launches": launches,
         "gpu_launches_per_step": kinfo,
     }

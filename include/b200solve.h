@@ -36,6 +36,8 @@ extern "C" {
 #define B2S_SINGULAR_PIVOT 3   /* -> SingularPivot(row)    (bs/errors.py:28-33) */
 #define B2S_CUDA_ERROR 4       /* -> RuntimeError                              */
 #define B2S_UNSUPPORTED 5      /* block size outside 1..4                      */
+#define B2S_PEER_TIMEOUT 6     /* sharded solve: a peer did not answer within
+                                  b2s_mesh.timeout_ns (or aborted) -> PeerTimeout */
 
 /* ---- analysis (bs/analysis.py) ------------------------------------------ */
 
@@ -280,7 +282,7 @@ typedef struct {
    * preparation is done and again after the device loop -- shards on one GPU
    * rendezvous there, so no implicitly synchronising host call (host/device
    * allocation, graph instantiation) runs while a peer's kernel waits */
-  void (*host_barrier)(void*);
+  int (*host_barrier)(void*);   /* returns 0; nonzero: this host thread failed */
   void* host_barrier_ctx;
   /* Optional, 2-colour plans: run the fused colour passes on the local block
    * (b2s_bicg_args' operator = the owned columns only) and add the ghost
@@ -296,6 +298,11 @@ typedef struct {
   const int32_t* full_sp;
   const int32_t* full_cols;
   const double* full_vals;
+  /* bound on every device-side wait for a peer (0: $B2S_MESH_TIMEOUT_MS, else
+   * 60 s); a wait that expires raises the abort word in every rank's mailbox
+   * (the last 64 bytes of b2s_mesh_mbox_bytes), every rank leaves its loop
+   * and b2s_bicgstab returns B2S_PEER_TIMEOUT */
+  long long timeout_ns;
 } b2s_mesh;
 
 #define B2S_MBOX_SLOTS 8
@@ -310,6 +317,26 @@ long long b2s_bicgstab_workspace_bytes_mesh(int n, int nghost, int b, int nparts
 int b2s_ipc_handle(const void* ptr, unsigned char* handle64, long long* offset);
 int b2s_ipc_open(const unsigned char* handle64, long long offset, void** ptr_out);
 int b2s_ipc_close(void* base);
+
+/* Device description of a WellSet (standard wells first, then multi-segment
+ * ones, in list order); every pointer is device memory, offsets in doubles.
+ * Built by paper_2309_11488_b200/wells.py (DeviceWells). */
+typedef struct {
+  int nwells, nb;
+  const int32_t *kind, *M, *nseg, *bptr, *bcell, *bseg;
+  const int64_t* boff;
+  const double* bvals;
+  const int64_t* doff;
+  const double* dvals;
+  const int64_t* pivoff;
+  const int32_t* piv;
+  const int64_t* toff;
+  int ncells;
+  const int32_t *cells, *cptr;
+  const int64_t *ccoff, *ct2;
+  const int32_t* cM;
+  const double* cvals;
+} b2s_wells;
 
 typedef struct {
   int n, b, nparts, precond /* 0 none, 1 ilu0 */, kc, maxit, check_lag;
@@ -343,6 +370,19 @@ typedef struct {
    * b itself (bs/krylov.py:171 up to the sign of zero), so the initial
    * residual SpMV (and, sharded, its ghost pull) is skipped */
   int x0_zero;
+  /* Optional separately applied wells (bs/krylov.py:84-94, NULL: none): the
+   * operator is A - sum_w C_w^T D_w^-1 B_w.  Before each operator
+   * application the well terms of its input go into well_corr (compact
+   * perforated cells, b doubles each; well_scratch: sum over wells of nseg*M
+   * doubles) and the SpMV subtracts them before its dot-product epilogue.
+   * well_slice[s]: base of slice s's 32 entries in well_lane, or -1;
+   * well_lane[base + l]: compact cell of row row0[s] + l, or -1.  The wells'
+   * cells are in the operator's (plan) row order.  Not with fuse or mesh. */
+  const b2s_wells* wells;
+  const int32_t* well_slice;
+  const int32_t* well_lane;
+  double* well_corr;
+  double* well_scratch;
 } b2s_bicg_args;
 
 typedef struct {
@@ -356,25 +396,7 @@ int b2s_bicgstab(const b2s_bicg_args* args, b2s_bicg_result* result);
 
 /* ---- wells applied separately (bs/wells.py:125-162, bs/krylov.py:84-94) --- */
 
-/* Device description of a WellSet (standard wells first, then multi-segment
- * ones, in list order); every pointer is device memory, offsets in doubles.
- * Built by paper_2309_11488_b200/wells.py (DeviceWells). */
-typedef struct {
-  int nwells, nb;
-  const int32_t *kind, *M, *nseg, *bptr, *bcell, *bseg;
-  const int64_t* boff;
-  const double* bvals;
-  const int64_t* doff;
-  const double* dvals;
-  const int64_t* pivoff;
-  const int32_t* piv;
-  const int64_t* toff;
-  int ncells;
-  const int32_t *cells, *cptr;
-  const int64_t *ccoff, *ct2;
-  const int32_t* cM;
-  const double* cvals;
-} b2s_wells;
+
 
 /* y -= sum_w C_w^T D_w^-1 B_w x; scratch: sum over wells of nseg*M doubles.
  * Replaces WellSet.apply_contributions_array (bs/wells.py:196-202). */

@@ -18,7 +18,7 @@ from .errors import MissingDiagonal, ShapeError, SingularPivot
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("B2S_LIB", _PKG / "libb200solve.so"))
 
-OK, SHAPE, MISSING_DIAGONAL, SINGULAR_PIVOT, CUDA_ERROR, UNSUPPORTED = range(6)
+OK, SHAPE, MISSING_DIAGONAL, SINGULAR_PIVOT, CUDA_ERROR, UNSUPPORTED, PEER_TIMEOUT = range(7)
 
 _P = C.c_void_p
 _I = C.c_int
@@ -36,7 +36,9 @@ class BicgArgs(C.Structure):
                 ("u_sp", _P), ("u_cols", _P), ("u_vals", _P),
                 ("dinv_tiles", _P), ("tiles", _P), ("rhs", _P), ("x", _P), ("work", _P),
                 ("stream", _P), ("ngroups", _I), ("goff1", _I), ("gslice_host", _P),
-                ("fuse", _I), ("mesh", _P), ("x0_zero", _I)]
+                ("fuse", _I), ("mesh", _P), ("x0_zero", _I),
+                ("wells", _P), ("well_slice", _P), ("well_lane", _P), ("well_corr", _P),
+                ("well_scratch", _P)]
 
 
 class Mesh(C.Structure):
@@ -47,10 +49,11 @@ class Mesh(C.Structure):
                 ("mbox", _P), ("peer_mbox", _P), ("seq_base", C.c_longlong),
                 ("shared_device", _I), ("host_barrier", _P), ("host_barrier_ctx", _P),
                 ("nbnd", _I), ("bnd_row", _P), ("bnd_ptr", _P), ("bnd_col", _P), ("bnd_val", _P),
-                ("full_sp", _P), ("full_cols", _P), ("full_vals", _P)]
+                ("full_sp", _P), ("full_cols", _P), ("full_vals", _P),
+                ("timeout_ns", C.c_longlong)]
 
 
-BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
+BARRIER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)   # 0 = ok; nonzero: this host thread failed
 
 
 class BicgResult(C.Structure):
@@ -146,6 +149,11 @@ def load(path: Path | str | None = None):
         return lib
 
 
+class PeerTimeout(RuntimeError):
+    """A sharded solve's peer did not post within the mesh timeout (dead,
+    hung or misconfigured peer), or some rank aborted: B2S_PEER_TIMEOUT."""
+
+
 def check(rc: int, what: str, row: int | None = None):
     """Map a C status onto the reference's exceptions (bs/errors.py)."""
     if rc == OK:
@@ -158,4 +166,7 @@ def check(rc: int, what: str, row: int | None = None):
         raise SingularPivot(int(row if row is not None else -1))
     if rc == UNSUPPORTED:
         raise ShapeError(f"{what}: block size outside 1..4 is not supported on the device")
+    if rc == PEER_TIMEOUT:
+        raise PeerTimeout(f"{what}: a peer shard did not answer in time (or aborted); "
+                          "the mesh left its loop on every rank")
     raise RuntimeError(f"{what}: CUDA error (status {rc})")

@@ -29,7 +29,7 @@ from .blockcore import BlockMatrix, BlockVector
 from .errors import SingularPivot, SolveFailed
 from .ilu0 import Ilu0Factorization, factor_device, prepare_two_colour
 from .krylov import (DEFAULT_MAX_ITERATIONS, DeviceKrylov, RefNorm, SolveReport,
-                     StoppingCriteria, WellAugmentedOperator, _REASONS, bicgstab)
+                     StoppingCriteria, _REASONS)
 from .wells import WellMode, WellSet, fold_into_matrix
 
 
@@ -87,8 +87,10 @@ class DeviceSolver:
     """
 
     def __init__(self, a: BlockMatrix, bsr: "D.DevBSR", cfg: SolverConfig,
-                 precond_bsr: "D.DevBSR" = None, precond_matrix: BlockMatrix = None):
+                 precond_bsr: "D.DevBSR" = None, precond_matrix: BlockMatrix = None,
+                 wells: WellSet | None = None):
         self.a = a
+        self.wells = wells if wells is not None and not wells.is_empty else None
         self.bsr = bsr
         self.cfg = cfg
         self.pre_bsr = precond_bsr or bsr
@@ -108,19 +110,21 @@ class DeviceSolver:
             self.bsr.wait_values()
         with trace.phase("factor"):
             self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr, prep)
+        w = self.wells
         if self.pre_bsr is self.bsr and self.fact.a_sell is not None:
             # 2-colour factorisation: the operator's SELL layout already exists
-            self.krylov = DeviceKrylov.build(self.a, self.fact, same_values=True)
+            self.krylov = DeviceKrylov.build(self.a, self.fact, same_values=True, wells=w)
             return self
         a_perm = self.fact._a_perm if self.pre_bsr is self.bsr else None
         if a_perm is None and self.pre_bsr is self.bsr and self.fact._a_src is not None:
-            self.krylov = DeviceKrylov.build(self.a, self.fact, same_values=True)   # from the input
+            self.krylov = DeviceKrylov.build(self.a, self.fact, same_values=True,
+                                             wells=w)   # from the input
             return self
         if a_perm is None:
             from .analysis import permute_device
             a_perm = (self.bsr if self.fact._identity_perm
                       else permute_device(self.bsr, self.plan))
-        self.krylov = DeviceKrylov.build(self.a, self.fact, a_perm)
+        self.krylov = DeviceKrylov.build(self.a, self.fact, a_perm, wells=w)
         return self
 
     def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
@@ -151,15 +155,19 @@ def _sync():
     torch.cuda.current_stream().synchronize()
 
 
-def _initial_residual(bsr: "D.DevBSR", rhs: torch.Tensor, x0d: torch.Tensor | None):
-    """b - A x0 in input order (bs/krylov.py:175) for the reported initial
-    norm; b itself when there is no initial guess."""
+def _initial_residual(bsr: "D.DevBSR", rhs: torch.Tensor, x0d: torch.Tensor | None,
+                      wells: WellSet | None = None):
+    """b - op(x0) in input order (bs/krylov.py:175; op = A, or A minus the
+    separately applied wells, as WellAugmentedOperator.apply_array computes
+    it) for the reported initial norm; b itself when there is no initial guess."""
     if x0d is None:
         return rhs
     n, b = bsr.pat.n, bsr.b
     smap = D.SliceMap.plain(n, rhs.device)
     y = D.empty_f64(n * b, rhs.device)
     D.spmv(smap, D.Sell.build(smap, bsr, 0), b, x0d, y)
+    if wells is not None and not wells.is_empty:
+        wells.device(b, n).apply(x0d, y)
     return rhs - y[: n * b]
 
 
@@ -171,14 +179,15 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     if wells is None:
         wells = WellSet()
     t0 = time.perf_counter()
+    sep = None
     if cfg.well_mode is WellMode.COUPLED and not wells.is_empty:
         a_sys = fold_into_matrix(a, wells)          # host assembly, as the reference
     else:
         a_sys = a.as_block_row_major()
         if not wells.is_empty:
-            # the config governs the treatment, whatever the set was marked as
+            # the config governs the treatment, whatever the set was marked as;
+            # the well terms run inside the device loop (WellAugmentedOperator)
             sep = WellSet(wells.standard, wells.multisegment, WellMode.SEPARATE)
-            return _solve_separate_wells(cfg, a_sys, sep, b, x0, t0)
     n, bs = a_sys.num_block_rows, a_sys.block_size
     if b.block_size != bs or b.num_blocks != n:
         raise ShapeError("right-hand side does not match the operator")
@@ -211,9 +220,9 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
                               cfg.jacobi_partitions)
             pre_mat, _ = drop_cross_blocks(a_sys, parts)
             pre_bsr = D.DevBSR.upload(pre_mat)
-        solver = DeviceSolver(a_sys, bsr, cfg, pre_bsr, pre_mat).setup()
+        solver = DeviceSolver(a_sys, bsr, cfg, pre_bsr, pre_mat, wells=sep).setup()
         # the reported ||r0|| in the reference's order, beside the loop
-        norm0 = RefNorm(_initial_residual(bsr, rhs, None if x0 is None else x0d), n * bs)
+        norm0 = RefNorm(_initial_residual(bsr, rhs, None if x0 is None else x0d, sep), n * bs)
         _sync()
         setup = time.perf_counter() - t0
         t1 = time.perf_counter()
@@ -239,13 +248,13 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
                                max(cfg.stop.max_iterations, DEFAULT_MAX_ITERATIONS))
     fcfg = SolverConfig(Backend.REFERENCE_SEQUENTIAL, 0, cfg.well_mode, fb_stop)
     try:
-        fb = DeviceSolver(a_sys, bsr, fcfg).setup()
+        fb = DeviceSolver(a_sys, bsr, fcfg, wells=sep).setup()
     except SingularPivot as exc:
         fb_report = _failed_report(f"singular pivot in row {exc.row}")
         fb_report.fallback_used = True
         raise SolveFailed(primary, fb_report)
     if norm0 is None:   # the primary failed before its loop: ||r0|| from here
-        norm0 = RefNorm(_initial_residual(bsr, rhs, None if x0 is None else x0d), n * bs)
+        norm0 = RefNorm(_initial_residual(bsr, rhs, None if x0 is None else x0d, sep), n * bs)
     _sync()
     fb_setup = time.perf_counter() - fb_t0
     t2 = time.perf_counter()
@@ -260,52 +269,3 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     if not report.converged:
         raise SolveFailed(primary, report)
     return D.to_host_vector(xd, n * bs, bs), report
-
-
-def _solve_separate_wells(cfg: SolverConfig, a_sys: BlockMatrix, wells: WellSet,
-                          b: BlockVector, x0: BlockVector | None, t0: float):
-    """Wells applied after every SpMV (WellAugmentedOperator): device SpMV,
-    device well terms and device ILU0 inside the host-driven BiCGStab loop
-    (bs/bridge.py:92-98,108-136)."""
-    from .errors import ShapeError
-    from .ilu0 import decompose
-    n, bs = a_sys.num_block_rows, a_sys.block_size
-    if b.block_size != bs or b.num_blocks != n:
-        raise ShapeError("right-hand side does not match the operator")
-    op = WellAugmentedOperator(a_sys, wells)
-    primary = None
-    x = None
-    try:
-        pre = a_sys
-        if cfg.jacobi_partitions > 0:
-            from .jacobi import drop_cross_blocks, partition, transmissibility_weights
-            parts = partition(a_sys.pattern, transmissibility_weights(a_sys),
-                              cfg.jacobi_partitions)
-            pre, _ = drop_cross_blocks(a_sys, parts)
-        dev_pat = D.DevPattern.upload(pre.pattern)
-        fact = decompose(pre, plan_device(cfg.backend, dev_pat))
-        setup = time.perf_counter() - t0
-        x, primary = bicgstab(op, fact, b, x0=x0, stop=cfg.stop)
-        primary.setup_elapsed = setup
-    except SingularPivot as exc:
-        primary = _failed_report(f"singular pivot in row {exc.row}")
-        primary.setup_elapsed = time.perf_counter() - t0
-    if primary.converged:
-        return x, primary
-    fb_t0 = time.perf_counter()
-    fb_stop = StoppingCriteria(cfg.stop.relative_reduction,
-                               max(cfg.stop.max_iterations, DEFAULT_MAX_ITERATIONS))
-    try:
-        fb_fact = decompose(a_sys, sequential_plan(n))
-    except SingularPivot as exc:
-        fb_report = _failed_report(f"singular pivot in row {exc.row}")
-        fb_report.fallback_used = True
-        raise SolveFailed(primary, fb_report)
-    fb_setup = time.perf_counter() - fb_t0
-    x, report = bicgstab(op, fb_fact, b, x0=x0, stop=fb_stop)
-    report.fallback_used = True
-    report.setup_elapsed = primary.setup_elapsed + fb_setup
-    report.elapsed += primary.elapsed
-    if not report.converged:
-        raise SolveFailed(primary, report)
-    return x, report

@@ -12,7 +12,8 @@ namespace b2s {
 
 constexpr double kBreakdown = 1e-60;  // bs/krylov.py:27
 
-enum Reason { kRunning = 0, kConverged = 1, kBreakdownR = 2, kNumerical = 3, kBudget = 4 };
+enum Reason { kRunning = 0, kConverged = 1, kBreakdownR = 2, kNumerical = 3, kBudget = 4,
+              kAborted = 5 /* sharded: a peer did not answer in time, or aborted */ };
 
 struct State {
   double rho, rho_prev, alpha, omega, beta;
@@ -32,6 +33,7 @@ struct MeshDev {
   double* mbox;
   double* const* peer_mbox;
   long long seq_base;
+  long long timeout_ns;   // bound on every wait for a peer
 };
 
 __device__ __forceinline__ void st_relaxed_sys(double* p, double v) {
@@ -51,13 +53,46 @@ __device__ __forceinline__ double ld_relaxed_sys(const double* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Every rank's mailbox ends with an abort word (b2s_mesh_mbox_bytes): any
+// rank whose wait for a peer times out -- a dead, hung or misconfigured
+// peer -- raises it on every rank, so the whole mesh leaves its loop
+// (reason kAborted -> B2S_PEER_TIMEOUT) instead of spinning forever.
+__device__ __forceinline__ long long* abort_word(double* mbox, int nranks) {
+  return reinterpret_cast<long long*>(mbox + (long long)kMboxSlots * nranks * 4);
+}
+__device__ __forceinline__ void mesh_raise_abort(double* const* peer_mbox, int nranks) {
+  __threadfence_system();
+  for (int h = 0; h < nranks; ++h) st_release_sys(abort_word(peer_mbox[h], nranks), 1);
+}
+// spin until *f >= seq; false once the abort word is up or timeout_ns passed
+__device__ __forceinline__ bool wait_ge(const long long* f, long long seq, double* mbox,
+                                        int nranks, long long timeout_ns) {
+  const long long* ab = abort_word(mbox, nranks);
+  unsigned long long t0 = 0;
+  for (int it = 0;; ++it) {
+    if (ld_acquire_sys(f) >= seq) return true;
+    if (ld_acquire_sys(ab) != 0) return false;
+    const unsigned long long now = global_ns();
+    if (it == 0) t0 = now;
+    else if ((long long)(now - t0) > timeout_ns) return false;
+    __nanosleep(64);
+  }
+}
+
 // All-reduce of (a, b) over the mesh, one thread: post the local sums into
 // slot `slot` of every rank's mailbox, wait for every rank's post of this
 // sequence number, sum them in rank order.  Every rank computes the same
 // bits.  A slot is reused only after every rank has read it: a rank posts
 // into slot s again only after passing the control points in between, which
-// need every other rank's later posts.
-__device__ __forceinline__ void mesh_sum(const MeshDev& m, long long seq, int slot, double& a,
+// need every other rank's later posts.  Returns false (abort raised on every
+// rank) when some rank does not post in time.
+__device__ __forceinline__ bool mesh_sum(const MeshDev& m, long long seq, int slot, double& a,
                                          double& b) {
   const int N = m.nranks;
   for (int h = 0; h < N; ++h) {
@@ -72,12 +107,17 @@ __device__ __forceinline__ void mesh_sum(const MeshDev& m, long long seq, int sl
   double sa = 0.0, sb = 0.0;
   for (int h = 0; h < N; ++h) {
     const double* e = m.mbox + ((long long)slot * N + h) * 4;
-    while (ld_acquire_sys(reinterpret_cast<const long long*>(e + 2)) < seq) __nanosleep(32);
+    if (!wait_ge(reinterpret_cast<const long long*>(e + 2), seq, m.mbox, N, m.timeout_ns)) {
+      mesh_raise_abort(m.peer_mbox, N);
+      a = b = __longlong_as_double(0x7FF8000000000000ll);
+      return false;
+    }
     sa += ld_relaxed_sys(e);
     sb += ld_relaxed_sys(e + 1);
   }
   a = sa;
   b = sb;
+  return true;
 }
 
 enum CtlStep { kCtlNone = 0, kCtlAlpha = 1, kCtlS = 2, kCtlOmega = 3, kCtlEndBegin = 4 };
@@ -128,7 +168,10 @@ __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const do
   if (c.step == kCtlOmega || c.step == kCtlEndBegin) b = reduce_parts_cg(p1, np, red);
   if (threadIdx.x != 0) return;
   double a = a0;
-  if (c.mesh.mbox) mesh_sum(c.mesh, c.mesh.seq_base + (++st->cseq), c.step, a, b);
+  if (c.mesh.mbox && !mesh_sum(c.mesh, c.mesh.seq_base + (++st->cseq), c.step, a, b)) {
+    ctl_finish(st, c.host_done, kAborted);
+    return;
+  }
   switch (c.step) {
     case kCtlAlpha: {  // gamma = rhat.v  (bs/krylov.py:206-210)
       if (fabs(a) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }

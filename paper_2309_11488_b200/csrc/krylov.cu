@@ -35,7 +35,7 @@ namespace b2s {
 
 int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
                 const double* w, double* p0, double* p1, const int* done, Ctl ctl,
-                cudaStream_t st, bool pdl = false);
+                cudaStream_t st, bool pdl = false, WellFix wf = WellFix{});
 int launch_sweeps(int b, int kc, SliceMap map, Sell lo, Sell up, const double* dt,
                   const double* r, double* y, double* z, int reset_y, int flags, void* tickets,
                   const int* done, cudaStream_t st);
@@ -45,7 +45,10 @@ int launch_phased(int b, int kc, int ngroups, const int32_t* gslice_host, int go
                   const int* done, cudaStream_t st, bool skip_g0, bool pdl = false);
 int launch_spmv_range(int b, int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
                       const double* x, double* y, const double* w, double* p0, double* p1,
-                      const int* done, Ctl ctl, cudaStream_t st, bool pdl = false);
+                      const int* done, Ctl ctl, cudaStream_t st, bool pdl = false,
+                      WellFix wf = WellFix{});
+int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, double* corr,
+                      const int* done, cudaStream_t st);
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
                     double* p1, const int* done, int* grid_out, cudaStream_t st,
@@ -66,16 +69,18 @@ __global__ void k_ctl_init(State* st, const double* prr, int np, double tol, int
   double s = reduce_parts(prr, np, red);
   if (threadIdx.x == 0) {
     if (!mesh.mbox) { st->cseq = 0; st->pub = 0; }
+    bool ok = true;
     if (mesh.mbox) {   // sharded: |r0|^2 over every rank
       double unused = 0.0;
-      mesh_sum(mesh, mesh.seq_base + (++st->cseq), kSlotInit, s, unused);
+      ok = mesh_sum(mesh, mesh.seq_base + (++st->cseq), kSlotInit, s, unused);
     }
     const double n0 = sqrt(s);
     st->rho = 0.0; st->rho_prev = 1.0; st->alpha = 1.0; st->omega = 1.0; st->beta = 0.0;
     st->norm0 = n0; st->target = tol * n0; st->final_norm = n0; st->its = 0.0;
     st->k = 0; st->maxit = maxit; st->reason = kRunning;
     st->done = 0;
-    if (!isfinite(n0)) { st->done = 1; st->reason = kNumerical; }
+    if (!ok) { st->done = 1; st->reason = kAborted; }
+    else if (!isfinite(n0)) { st->done = 1; st->reason = kNumerical; }
     else if (n0 <= st->target || n0 == 0.0) { st->done = 1; st->reason = kConverged; }
     // top of iteration 0 (maxit >= 1): rho_0 = rhat.r0 = the same partials
     else if (fabs(s) < kBreakdown) { st->done = 1; st->reason = kBreakdownR; }
@@ -96,11 +101,16 @@ struct MeshHalo {
   long long* flags;             // posted by peers: "vector #seq is ready"
   long long* const* peer_flags;
   long long seq_base;
+  double* mbox;                 // this rank's mailbox (its abort word) ...
+  double* const* peer_mbox;     // ... and every rank's
+  long long timeout_ns;
 };
 
 __global__ void k_zero_words(unsigned* p, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0u;
 }
+
+__global__ void k_mesh_raise_abort(MeshDev m) { mesh_raise_abort(m.peer_mbox, m.nranks); }
 
 __global__ void k_mesh_reset(State* st) {
   st->done = 0;
@@ -117,13 +127,23 @@ __global__ void k_mesh_publish(State* st, MeshHalo h, const int* done) {
   for (int q = 0; q < h.nranks; ++q) st_release_sys(h.peer_flags[q] + h.rank, seq);
 }
 // one CTA: wait until every neighbour posted the same vector (a separate
-// kernel, so waiting never holds more than one SM)
-__global__ void k_mesh_wait(const State* st, MeshHalo h, const int* done) {
+// kernel, so waiting never holds more than one SM); a neighbour that does
+// not post in time (or an abort raised anywhere) ends the solve on every
+// rank: the kernels after this one no-op, the host sees kAborted
+__global__ void k_mesh_wait(State* st, MeshHalo h, const int* done, int* host_done) {
   if (done && *done) return;
   const long long seq = h.seq_base + st->pub;
+  bool ok = true;
   for (int k = threadIdx.x; k < h.nnbr; k += blockDim.x) {
     const long long* f = h.flags + h.nbr[k];
-    while (ld_acquire_sys(f) < seq) __nanosleep(64);
+    ok &= wait_ge(f, seq, h.mbox, h.nranks, h.timeout_ns);
+  }
+  if (__syncthreads_or(!ok) && threadIdx.x == 0) {
+    mesh_raise_abort(h.peer_mbox, h.nranks);
+    st->reason = kAborted;
+    st->done = 1;
+    __threadfence();
+    if (host_done) *reinterpret_cast<volatile int*>(host_done) = 1;
   }
 }
 // ghost rows of vector `which` (0 x, 1 phat, 2 shat) -> dst (after the owned rows)
@@ -147,7 +167,8 @@ __global__ void k_mesh_scalar(State* st, MeshDev mesh, int slot, const double* p
   if (threadIdx.x == 0) {
     if (flag) v = *flag ? 1.0 : 0.0;
     double unused = 0.0;
-    if (mesh.mbox) mesh_sum(mesh, mesh.seq_base + (++st->cseq), slot, v, unused);
+    if (mesh.mbox && !mesh_sum(mesh, mesh.seq_base + (++st->cseq), slot, v, unused))
+      st->reason = kAborted;   // v is NaN; b2s_bicgstab reports B2S_PEER_TIMEOUT
     out[0] = v;
   }
 }
@@ -483,7 +504,17 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // sharded + fused: the operator passed is the local block, the boundary
   // rows' ghost couplings come separately (b2s_mesh bnd_*)
   const bool mesh_local = mesh && mesh->bnd_ptr != nullptr;
-  const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh_local);
+  // separately applied wells: the well terms of p^ (s^) are computed right
+  // before each SpMV and subtracted in its epilogue (not with the fused
+  // colour passes, which produce v's colour-0 rows before p^ is complete)
+  const bool wells = a->wells != nullptr && a->wells->nwells > 0;
+  if (wells && (mesh || !a->well_slice || !a->well_lane || !a->well_corr || !a->well_scratch))
+    return mesh ? B2S_UNSUPPORTED : B2S_SHAPE;
+  const WellFix wf = wells ? WellFix{a->well_slice, a->well_lane, a->well_corr} : WellFix{};
+  auto well_terms = [&](const double* xin, const int* dn, cudaStream_t q) {
+    return wells ? launch_wells_corr(a->wells, xin, a->well_scratch, a->well_corr, dn, q) : 0;
+  };
+  const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh_local) && !wells;
   const int reset = (ilu && !phased) ? 1 : 0;  // sync-free sweeps need sentinel-filled outputs
   MeshDev md{};
   MeshHalo mh{};
@@ -492,24 +523,18 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     if (mesh->nranks < 1 || mesh->rank < 0 || mesh->rank >= mesh->nranks || !mesh->mbox ||
         !mesh->peer_mbox || !mesh->flags || !mesh->peer_flags)
       return B2S_SHAPE;
-    md = MeshDev{mesh->rank, mesh->nranks, mesh->mbox, mesh->peer_mbox, mesh->seq_base};
+    const char* to_env = getenv("B2S_MESH_TIMEOUT_MS");
+    const long long timeout_ns = mesh->timeout_ns > 0 ? mesh->timeout_ns
+                                 : (to_env ? atoll(to_env) * 1000000ll : 60000000000ll);
+    md = MeshDev{mesh->rank, mesh->nranks, mesh->mbox, mesh->peer_mbox, mesh->seq_base, timeout_ns};
     mh.rank = mesh->rank; mh.nranks = mesh->nranks; mh.nghost = mesh->nghost;
     mh.nnbr = mesh->nnbr; mh.nbr = mesh->nbr;
     mh.ghost_owner = mesh->ghost_owner; mh.ghost_row = mesh->ghost_row;
     mh.peer_vec[0] = mesh->peer_x; mh.peer_vec[1] = mesh->peer_phat;
     mh.peer_vec[2] = mesh->peer_shat;
     mh.flags = mesh->flags; mh.peer_flags = mesh->peer_flags; mh.seq_base = mesh->seq_base;
+    mh.mbox = mesh->mbox; mh.peer_mbox = mesh->peer_mbox; mh.timeout_ns = md.timeout_ns;
   }
-  // publish this rank's vector, wait for the neighbours', pull the ghosts
-  auto halo = [&](cudaStream_t q, int which, double* vec, const int* dn) {
-    k_mesh_publish<<<1, 1, 0, q>>>(state, mh, dn);
-    k_mesh_wait<<<1, 32, 0, q>>>(state, mh, dn);
-    if (mh.nghost > 0) {
-      long long g = ((long long)mh.nghost * a->b + 255) / 256;
-      if (g > kSms * 2) g = kSms * 2;
-      k_mesh_pull<<<(int)g, 256, 0, q>>>(mh, which, a->b, vec + m, dn);
-    }
-  };
   const int np = a->nparts;
   SliceMap map{a->nslices, a->row0, a->nrows};
   Sell A{a->a_sp, a->a_cols, a->a_vals};
@@ -536,6 +561,17 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     return B2S_CUDA_ERROR;
   }
 
+  // publish this rank's vector, wait for the neighbours', pull the ghosts
+  auto halo = [&](cudaStream_t q, int which, double* vec, const int* dn) {
+    k_mesh_publish<<<1, 1, 0, q>>>(state, mh, dn);
+    k_mesh_wait<<<1, 32, 0, q>>>(state, mh, dn, dev_done);
+    if (mh.nghost > 0) {
+      long long g = ((long long)mh.nghost * a->b + 255) / 256;
+      if (g > kSms * 2) g = kSms * 2;
+      k_mesh_pull<<<(int)g, 256, 0, q>>>(mh, which, a->b, vec + m, dn);
+    }
+  };
+
   // ---- setup on the caller's stream: r0 = b - A x0, |r0|, r^ = r0, rho_0
   // partials.  Launched after the iteration graph is captured and
   // instantiated (host work that may synchronise the device implicitly --
@@ -553,8 +589,10 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       k_dot_parts<<<np, 256, 0, user>>>(m, r, r, prr);
     } else {
       if (mesh) halo(user, 0, a->x, &state->done);
-      rc = launch_spmv(a->b, 3, np, map, Afull, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{},
-                       user);
+      rc = well_terms(a->x, nullptr, user);
+      if (rc == B2S_OK)
+        rc = launch_spmv(a->b, 3, np, map, Afull, a->x, r, a->rhs, prr, nullptr, nullptr, Ctl{},
+                         user, false, wf);
       if (res_corr)
         launch_ghost_correct<kResidual>(a->b, mesh, a->x + m, r, nullptr, prr, nullptr, np,
                                         nullptr, Ctl{}, user);
@@ -574,8 +612,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     if (rc == B2S_OK && cudaGetLastError() != cudaSuccess) rc = B2S_CUDA_ERROR;
     return rc;
   };
+  // a peer's host thread that failed (its callback returns nonzero) must not
+  // leave this shard spinning: raise the mesh-wide abort and leave
+  bool barrier_failed = false;
   auto peer_barrier = [&]() {
-    if (mesh && mesh->host_barrier) mesh->host_barrier(mesh->host_barrier_ctx);
+    if (mesh && mesh->host_barrier && mesh->host_barrier(mesh->host_barrier_ctx) != 0)
+      barrier_failed = true;
+    return !barrier_failed;
   };
   State hs;
 
@@ -668,8 +711,10 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     }
     if (mesh && !fused) { halo(cs, 1, ph, done); kernels += mh.nghost > 0 ? 3 : 2; }
     if (!fused) {
+      if (wells) { well_terms(ph, done, cs); kernels += 2; }
       launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done,
-                  Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl); ++kernels;
+                  Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl && !wells, wf);
+      ++kernels;
     }
     launch_k(k_s_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
              (const double*)r, (const double*)v, ph, a->x, s, pss, reset,
@@ -705,8 +750,10 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     }
     if (mesh && !fused) { halo(cs, 2, sh, done); kernels += mh.nghost > 0 ? 3 : 2; }
     if (!fused) {
+      if (wells) { well_terms(sh, done, cs); kernels += 2; }
       launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done,
-                  Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl); ++kernels;
+                  Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl && !wells, wf);
+      ++kernels;
     }
     launch_k(k_r_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state, sh,
              (const double*)t, (const double*)s, (const double*)rhat, a->x, r, prr, prho, reset,
@@ -718,7 +765,12 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     // extra stream risks sharing a hardware work queue with a peer's stream,
     // i.e. a false dependency behind a kernel that waits for that very peer
     cudaStream_t rs = (mesh && mesh->shared_device) ? user : cs;
-    peer_barrier();   // every shard is past its host-side preparation
+    if (!peer_barrier()) {   // a peer's host side failed before its loop
+      k_mesh_raise_abort<<<1, 1, 0, user>>>(md);
+      status = B2S_PEER_TIMEOUT;
+      cudaStreamSynchronize(user);
+      break;
+    }
     if ((status = setup()) != B2S_OK) { cudaStreamSynchronize(user); break; }
     // order the graph after the setup work on the caller's stream
     cudaEvent_t ev;
@@ -764,6 +816,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
 
   B2S_CHECK(cudaMemcpyAsync(&hs, state, sizeof(State), cudaMemcpyDeviceToHost, user));
   B2S_CHECK(cudaStreamSynchronize(user));
+  if (hs.reason == kAborted || barrier_failed) return B2S_PEER_TIMEOUT;
   res->initial_norm = hs.norm0;
   if (hs.init_exit) {  // zero or non-finite initial residual, rho_0 breakdown: no iteration
     res->converged = hs.reason == kConverged;
@@ -785,10 +838,17 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // shards first rendezvous again -- a peer still tearing down its graph or
   // freeing its host flag would otherwise wait for these waiting kernels)
   if (mesh) {
-    peer_barrier();
+    if (!peer_barrier()) {
+      k_mesh_raise_abort<<<1, 1, 0, user>>>(md);
+      cudaStreamSynchronize(user);
+      return B2S_PEER_TIMEOUT;
+    }
     halo(user, 0, a->x, nullptr);
   }
-  int rc = launch_spmv(a->b, 3, np, map, Afull, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user);
+  int rc = well_terms(a->x, nullptr, user);
+  if (rc) return rc;
+  rc = launch_spmv(a->b, 3, np, map, Afull, a->x, t, a->rhs, pg, nullptr, nullptr, Ctl{}, user,
+                   false, wf);
   if (rc) return rc;
   if (res_corr)
     launch_ghost_correct<kResidual>(a->b, mesh, a->x + m, t, nullptr, pg, nullptr, np, nullptr,
@@ -806,6 +866,11 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   B2S_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, user));
   if (mesh) B2S_CHECK(cudaMemcpyAsync(&gbad, pts, sizeof(double), cudaMemcpyDeviceToHost, user));
   B2S_CHECK(cudaStreamSynchronize(user));
+  if (mesh) {   // an abort raised by a peer during these last all-reduces
+    State h2;
+    B2S_CHECK(cudaMemcpy(&h2, state, sizeof(State), cudaMemcpyDeviceToHost));
+    if (h2.reason == kAborted) return B2S_PEER_TIMEOUT;
+  }
   res->final_norm = sqrt(fin2);
   if (mesh) hbad = gbad != 0.0;
   if (hbad) {
@@ -816,7 +881,8 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
 }
 
 long long b2s_mesh_mbox_bytes(int nranks) {
-  return nranks < 1 ? 0 : (long long)kMboxSlots * nranks * 4 * 8;
+  // kMboxSlots x nranks x 4 doubles, then the abort word (ctl.cuh abort_word)
+  return nranks < 1 ? 0 : (long long)kMboxSlots * nranks * 4 * 8 + 64;
 }
 
 int b2s_bicgstab_workspace_layout(int n, int nghost, int b, long long* phat_off,

@@ -22,6 +22,18 @@ struct Sell {
   const double* vals;   // [slots*b*b]
 };
 
+// Separately applied wells inside the device loop (b2s_bicg_args.wells):
+// corr[q] = sum over the wells perforating compact cell q of C^T D^-1 B x
+// (csrc/wells.cu, computed right before the SpMV); the SpMV subtracts it
+// from the row sum before its dot-product epilogue.  slice[s] = base of
+// slice s's 32 lane entries in lane[] or -1 (no perforated row in the slice);
+// lane[base + l] = compact cell index of row row0[s] + l, or -1.
+struct WellFix {
+  const int32_t* slice;
+  const int32_t* lane;
+  const double* corr;
+};
+
 // SpMV epilogues: 0 y = A x; 1 + partials w.y; 2 + partials y.y and y.w;
 // 3 y = w - A x (residual) + partials y.y
 enum SpmvMode { kPlain = 0, kDotW = 1, kSelfAndW = 2, kResidual = 3 };

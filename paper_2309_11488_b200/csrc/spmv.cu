@@ -138,14 +138,14 @@ __global__ void k_diag_tiles(int nslices, int bb, const int32_t* __restrict__ ro
 }
 
 
-template <int B, int MODE>
+template <int B, int MODE, bool WELLS>
 __global__ void __launch_bounds__(256, B <= 3 ? 4 : 1) k_spmv(SliceMap map, int s0, int s1, int poff, Sell a,
                                               const double* __restrict__ x,
                                               double* __restrict__ y,
                                               const double* __restrict__ w,
                                               double* __restrict__ part0,
                                               double* __restrict__ part1, const int* done,
-                                              Ctl ctl) {
+                                              Ctl ctl, WellFix wf) {
   constexpr int BB = B * B;
   __shared__ double red[8];
   griddep_wait();
@@ -215,6 +215,16 @@ __global__ void __launch_bounds__(256, B <= 3 ? 4 : 1) k_spmv(SliceMap map, int 
         }
       }
     }
+    if (WELLS) {   // the operator's well terms (bs/krylov.py:84-94), before the epilogue
+      const int wb = wf.slice[s];
+      if (wb >= 0) {
+        const int q = wf.lane[wb + lane];
+        if (ok && q >= 0) {
+#pragma unroll
+          for (int c = 0; c < B; ++c) acc[c] -= wf.corr[(long long)q * B + c];
+        }
+      }
+    }
     if (ok) {
 #pragma unroll
       for (int c = 0; c < B; ++c) {
@@ -248,39 +258,50 @@ inline int grid_for(long long work, int threads = 256) {
   return (int)g;
 }
 
-template <int B>
-int launch_spmv_b(int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
-                  const double* x, double* y, const double* w, double* p0, double* p1,
-                  const int* done, Ctl ctl, cudaStream_t st, bool pdl) {
+template <int B, bool WELLS>
+int launch_spmv_bw(int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
+                   const double* x, double* y, const double* w, double* p0, double* p1,
+                   const int* done, Ctl ctl, cudaStream_t st, bool pdl, WellFix wf) {
   dim3 g(nparts), t(256);
   switch (mode) {
-    case kPlain: launch_k(k_spmv<B, kPlain>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
-    case kDotW: launch_k(k_spmv<B, kDotW>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
-    case kSelfAndW: launch_k(k_spmv<B, kSelfAndW>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
-    case kResidual: launch_k(k_spmv<B, kResidual>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl); break;
+    case kPlain: launch_k(k_spmv<B, kPlain, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf); break;
+    case kDotW: launch_k(k_spmv<B, kDotW, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf); break;
+    case kSelfAndW: launch_k(k_spmv<B, kSelfAndW, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf); break;
+    case kResidual: launch_k(k_spmv<B, kResidual, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf); break;
     default: return B2S_SHAPE;
   }
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
+template <int B>
+int launch_spmv_b(int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
+                  const double* x, double* y, const double* w, double* p0, double* p1,
+                  const int* done, Ctl ctl, cudaStream_t st, bool pdl, WellFix wf) {
+  if (wf.slice)
+    return launch_spmv_bw<B, true>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl,
+                                   st, pdl, wf);
+  return launch_spmv_bw<B, false>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl,
+                                  st, pdl, wf);
+}
+
 // SpMV over slices [s0, s1) of the map; partials land at [poff, poff + nparts)
 int launch_spmv_range(int b, int mode, int nparts, SliceMap map, int s0, int s1, int poff, Sell a,
                       const double* x, double* y, const double* w, double* p0, double* p1,
-                      const int* done, Ctl ctl, cudaStream_t st, bool pdl) {
+                      const int* done, Ctl ctl, cudaStream_t st, bool pdl, WellFix wf) {
   switch (b) {
-    case 1: return launch_spmv_b<1>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl);
-    case 2: return launch_spmv_b<2>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl);
-    case 3: return launch_spmv_b<3>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl);
-    case 4: return launch_spmv_b<4>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl);
+    case 1: return launch_spmv_b<1>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl, wf);
+    case 2: return launch_spmv_b<2>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl, wf);
+    case 3: return launch_spmv_b<3>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl, wf);
+    case 4: return launch_spmv_b<4>(mode, nparts, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, st, pdl, wf);
     default: return B2S_UNSUPPORTED;
   }
 }
 
 int launch_spmv(int b, int mode, int nparts, SliceMap map, Sell a, const double* x, double* y,
                 const double* w, double* p0, double* p1, const int* done, Ctl ctl,
-                cudaStream_t st, bool pdl) {
+                cudaStream_t st, bool pdl, WellFix wf) {
   return launch_spmv_range(b, mode, nparts, map, 0, map.nslices, 0, a, x, y, w, p0, p1, done, ctl,
-                           st, pdl);
+                           st, pdl, wf);
 }
 
 }  // namespace b2s
@@ -419,7 +440,8 @@ int b2s_spmv(int b, int mode, int nparts, int nslices, const int32_t* row0,
   if (nslices < 0 || nparts < 1) return B2S_SHAPE;
   SliceMap map{nslices, row0, nrows};
   Sell a{sp, cols, vals};
-  return launch_spmv(b, mode, nparts, map, a, x, y, w, part0, part1, done, Ctl{}, st, false);
+  return launch_spmv(b, mode, nparts, map, a, x, y, w, part0, part1, done, Ctl{}, st, false,
+                     WellFix{});
 }
 
 }  // extern "C"

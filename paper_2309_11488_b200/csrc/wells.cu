@@ -43,7 +43,9 @@ struct WellsDev {
 constexpr int kMaxS = 64;   // t1/t2 held per lane: nseg*M <= 32 * kMaxS
 
 // pass 1: t2 of well w (one warp)
-__global__ void k_wells_t2(WellsDev W, const double* __restrict__ x, double* __restrict__ t2) {
+__global__ void k_wells_t2(WellsDev W, const double* __restrict__ x, double* __restrict__ t2,
+                           const int* done) {
+  if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= W.nwells) return;
@@ -118,6 +120,46 @@ __global__ void k_wells_apply(WellsDev W, const double* __restrict__ t2, double*
   }
 }
 
+// inside the device Krylov loop: corr[q] = sum of the cell's C_e^T t2 in
+// well order; the SpMV epilogue subtracts it (sell.cuh WellFix)
+__global__ void k_wells_corr(WellsDev W, const double* __restrict__ t2, double* __restrict__ corr,
+                             const int* done) {
+  if (done && *done) return;
+  const int N = W.nb;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < W.ncells; q += gridDim.x * blockDim.x) {
+    double tot[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int e = W.cptr[q]; e < W.cptr[q + 1]; ++e) {
+      const double* blk = W.cvals + W.ccoff[e];
+      const double* tv = t2 + W.ct2[e];
+      const int M = W.cM[e];
+      for (int c = 0; c < N; ++c) {
+        double s = 0.0;
+        for (int m = 0; m < M; ++m) s = fma(blk[m * N + c], tv[m], s);
+        tot[c] += s;
+      }
+    }
+    for (int c = 0; c < N; ++c) corr[(long long)q * N + c] = tot[c];
+  }
+}
+
+static WellsDev wells_dev(const b2s_wells* w) {
+  return WellsDev{w->nwells, w->nb,  w->kind,   w->M,    w->nseg,  w->bptr,  w->bcell,
+                  w->bseg,   w->boff, w->bvals, w->doff, w->dvals, w->pivoff, w->piv,
+                  w->toff,   w->ncells, w->cells, w->cptr, w->ccoff, w->ct2,  w->cM,
+                  w->cvals};
+}
+
+int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, double* corr,
+                      const int* done, cudaStream_t st) {
+  if (!w || w->nwells < 0 || w->nb < 1 || w->nb > 4) return B2S_SHAPE;
+  if (w->nwells == 0) return B2S_OK;
+  const WellsDev W = wells_dev(w);
+  k_wells_t2<<<(w->nwells + 7) / 8, 256, 0, st>>>(W, x, scratch, done);
+  const int g = (w->ncells + 255) / 256;
+  k_wells_corr<<<g < 1 ? 1 : g, 256, 0, st>>>(W, scratch, corr, done);
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
 }  // namespace b2s
 
 using namespace b2s;
@@ -129,12 +171,9 @@ int b2s_wells_apply(const b2s_wells* w, const double* x, double* y, double* scra
                     cudaStream_t st) {
   if (!w || w->nwells < 0 || w->nb < 1) return B2S_SHAPE;
   if (w->nwells == 0) return B2S_OK;
-  WellsDev W{w->nwells, w->nb,  w->kind,   w->M,    w->nseg,  w->bptr,  w->bcell,
-             w->bseg,   w->boff, w->bvals, w->doff, w->dvals, w->pivoff, w->piv,
-             w->toff,   w->ncells, w->cells, w->cptr, w->ccoff, w->ct2,  w->cM,
-             w->cvals};
+  const WellsDev W = wells_dev(w);
   const int warps = w->nwells;
-  k_wells_t2<<<(warps + 7) / 8, 256, 0, st>>>(W, x, scratch);
+  k_wells_t2<<<(warps + 7) / 8, 256, 0, st>>>(W, x, scratch, nullptr);
   const int g = (w->ncells + 255) / 256;
   k_wells_apply<<<g < 1 ? 1 : g, 256, 0, st>>>(W, scratch, y);
   B2S_LAUNCH_CHECK();

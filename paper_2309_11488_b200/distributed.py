@@ -167,6 +167,28 @@ class HaloPlan:
         return {h: self.ghosts[idx] for h, idx in self.recv.items()}
 
 
+class _DeviceBlock:
+    """A shard's diagonal block as the factorisation sees it: the host pattern
+    and block size, with the values resident on the device only (gathered
+    there from the uploaded slab) -- no host copy of the slab's blocks."""
+
+    def __init__(self, pattern: SparsityPattern, block_size: int):
+        self.pattern = pattern
+        self.block_size = block_size
+        self.layout = Layout.BLOCK_ROW_MAJOR
+
+    @property
+    def num_block_rows(self) -> int:
+        return self.pattern.num_block_rows
+
+    def as_block_row_major(self):
+        return self
+
+    @property
+    def values(self):
+        raise RuntimeError("a shard's preconditioner blocks live on the device only")
+
+
 class Shard:
     """Local rows in plan order + ghost section, block-Jacobi ILU0, halo maps."""
 
@@ -181,16 +203,25 @@ class Shard:
         own, lcol = hp.own, hp.lcol
         self.ghosts, self.G, self.recv = hp.ghosts, hp.G, hp.recv
         rows = np.repeat(np.arange(R), np.diff(slab.rp))
-        # preconditioner source: the diagonal block (cross-slab blocks dropped)
+        # preconditioner source: the diagonal block (cross-slab blocks dropped);
+        # its pattern on the host, its values only on the device
         prp = np.zeros(R + 1, dtype=np.int64)
         np.cumsum(np.bincount(rows[own], minlength=R), out=prp[1:])
-        self.pmat = BlockMatrix(SparsityPattern(R, prp, lcol[own]), b,
-                                slab.vals3[own].reshape(-1), Layout.BLOCK_ROW_MAJOR)
-        # one upload: both matrices stay resident; setup() re-runs the device
-        # pipeline (plan, permutation, factorisation, layouts) from them
-        self.pbsr = D.DevBSR.upload(self.pmat)
+        self.pmat = _DeviceBlock(SparsityPattern(R, prp, lcol[own]), b)
+        # one upload of the slab (pattern + values): the diagonal block's
+        # values are gathered from it on the device; both stay resident and
+        # setup() re-runs the device pipeline (plan, permutation,
+        # factorisation, layouts) from them
         opat = D.DevPattern(R, len(ci), D.i32(slab.rp, dev), D.i32(lcol, dev))
         self.obsr = D.DevBSR(opat, b, D.f64(slab.vals3.reshape(-1), dev))
+        self._own_idx = D.i32(np.flatnonzero(own), dev)
+        ppat = D.DevPattern.upload(self.pmat.pattern)
+        self.pbsr = D.DevBSR(ppat, b, torch.empty(max(ppat.nnz, 1) * b * b, dtype=torch.float64,
+                                                  device=dev))
+        if ppat.nnz:
+            check(D.lib().b2s_gather_blocks(ppat.nnz, b, D.ptr(self._own_idx),
+                                            D.ptr(self.obsr.vals), D.ptr(self.pbsr.vals),
+                                            D.stream()), "gather_blocks")
         # ghost couplings of the boundary rows as CSR over ghost indices (the
         # fused 2-colour loop adds them after the halo pull; b2s_mesh bnd_*)
         gh = ~own
@@ -249,8 +280,6 @@ class Shard:
         dev, b = self.dev, self.b
         src = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64).reshape(-1))
         self.obsr.vals.copy_(src, non_blocking=D.is_pinned(src))
-        if getattr(self, "_own_idx", None) is None:
-            self._own_idx = D.i32(np.flatnonzero(self.halo_plan.own), dev)
         nk = self._own_idx.numel()
         check(D.lib().b2s_gather_blocks(nk, b, D.ptr(self._own_idx), D.ptr(self.obsr.vals),
                                         D.ptr(self.pbsr.vals), D.stream()), "gather_blocks")
@@ -307,35 +336,48 @@ class LocalComm:
 
 
 class NcclComm:
-    """One shard per process over torch.distributed (NCCL over NVLink)."""
+    """One shard per process over torch.distributed (NCCL over NVLink).  With
+    a non-NCCL group (gloo: tests run two ranks on one GPU, which NCCL
+    refuses) the buffers are staged through host memory."""
 
     def __init__(self, shard):
         import torch.distributed as dist
         self.dist = dist
         self.shards = [shard]
+        self.host = dist.get_backend() != "nccl"
         s = shard
         # contiguous receive ranges per neighbour (ghost ids are sorted and
         # every owner's ids are contiguous)
         self.recv_rng = {h: (int(idx[0]), int(idx[-1]) + 1) for h, idx in s.recv.items()}
 
     def allreduce(self, vals):
-        v = vals[0].clone()
+        v = vals[0].detach().clone()
+        if self.host:
+            v = v.cpu()
         self.dist.all_reduce(v)
         return [v.cpu().numpy()]
 
     def halo(self, bufs):
         s, x = self.shards[0], bufs[0]
-        ops, keep = [], []
+        ops, keep, back = [], [], []
         for h, rows in s.send.items():
             sb = D.gather_rows(x, rows, rows.numel(), s.b)
+            if self.host:
+                sb = sb.cpu()
             keep.append(sb)
             ops.append(self.dist.P2POp(self.dist.isend, sb, h))
         for h, (lo, hi) in self.recv_rng.items():
             rv = x[(s.R + lo) * s.b:(s.R + hi) * s.b]
+            if self.host:
+                staged = torch.empty(rv.numel(), dtype=rv.dtype)
+                back.append((rv, staged))
+                rv = staged
             ops.append(self.dist.P2POp(self.dist.irecv, rv, h))
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
+        for dst, staged in back:
+            dst.copy_(staged)
 
 
 def route_requests(mine, gather):
@@ -637,6 +679,7 @@ def _mesh_prepare(shard: "Shard", nranks: int, x0=None):
             shard.mesh.x.numel() != (shard.R + shard.G) * shard.b + 2:
         shard.mesh = MeshState(shard, nranks)
     ms = shard.mesh
+    ms.mbox[-8:].zero_()   # the abort word (csrc/ctl.cuh abort_word): a fresh solve
     iperm = shard.plan.device("inverse_permutation")
     # the right-hand side is resident like the matrix (uploaded once per shard)
     rhs = getattr(shard, "rhs_d", None)
@@ -668,8 +711,15 @@ def solve_shards_mesh(shards, stop: StoppingCriteria, x0=None):
     few (tests/conftest.py sets 32)."""
     import threading
 
-    from .krylov import DeviceKrylov
     N = len(shards)
+    need = N + 2
+    have = int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8"))
+    if N > 1 and have < need:
+        # shards' kernels wait for each other: a waiting kernel sharing a
+        # hardware queue with its peer's would block it (until the mesh timeout)
+        raise RuntimeError(f"solve_shards_mesh: {N} shards on one GPU need "
+                           f"CUDA_DEVICE_MAX_CONNECTIONS >= {need} set before CUDA starts "
+                           f"(it is {have})")
     by_rank = {s.slab.rank: s for s in shards}
     mss = [_mesh_prepare(s, N, None if x0 is None else x0[i]) for i, s in enumerate(shards)]
     ptrs = [by_rank[r].mesh.local_ptrs() for r in range(N)]
@@ -678,7 +728,14 @@ def solve_shards_mesh(shards, stop: StoppingCriteria, x0=None):
     # synchronising call while another shard's kernel waits for it
     from ._lib import BARRIER_FN
     rendezvous = threading.Barrier(N)
-    barrier_cb = BARRIER_FN(lambda _ctx: rendezvous.wait())
+
+    def _barrier(_ctx):   # ctypes swallows exceptions: report failure as a status
+        try:
+            rendezvous.wait()
+            return 0
+        except threading.BrokenBarrierError:
+            return 1
+    barrier_cb = BARRIER_FN(_barrier)
     jobs = []
     for s, ms in zip(shards, mss):
         ms.peers = ptrs

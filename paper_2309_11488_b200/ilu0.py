@@ -66,7 +66,7 @@ class Ilu0Factorization:
         # bandwidth-bound -> static slice order, no ticket atomics (0.77 of
         # peak vs 0.68); deep level schedules are latency-bound -> dynamic
         # tickets on one CTA of 4 warps per SM (fewer pollers on L2: C4 level
-        # application 626 us vs 685 us with 8 warps, tools/scratch/sweep_scan.py)
+        # application 626 us vs 685 us with 8 warps, a warps-per-CTA scan, round 1)
         self.sweep_flags = 0x4 if plan.group_count <= 16 else 0x410
         self.tiles = None        # b2s_tiles_create handle (tiled level sweeps), or None
         # few independent groups (colourings) and no same-group entries: the

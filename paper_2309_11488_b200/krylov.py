@@ -223,14 +223,19 @@ class DeviceKrylov:
     fact: Ilu0Factorization | None
     work: torch.Tensor
     fuse: bool = False   # 2-colour fused backward + SpMV passes (csrc/fused.cu)
+    wells: object = None   # DeviceWells in this solver's row order (separate wells)
+    wtabs: tuple = ()      # its WellFix tables (slice, lane, corr)
 
     @classmethod
     def build(cls, matrix: BlockMatrix, fact: Ilu0Factorization | None,
-              a_bsr: "D.DevBSR" = None, same_values: bool = False) -> "DeviceKrylov":
+              a_bsr: "D.DevBSR" = None, same_values: bool = False,
+              wells=None) -> "DeviceKrylov":
         """``same_values``: the caller guarantees ``matrix``'s host values are
         the ones ``fact`` was computed from (one solve_with_fallback call), so
         the factorisation's device copy of them can serve as the operator.
-        Otherwise (public bicgstab) the operator is uploaded afresh."""
+        Otherwise (public bicgstab) the operator is uploaded afresh.
+        ``wells``: a WellSet applied separately (WellAugmentedOperator): its
+        terms run inside the device loop, in the plan's row order."""
         n, b = matrix.num_block_rows, matrix.block_size
         fuse_env = os.environ.get("B2S_FUSE", "1") != "0"
         sell = None
@@ -255,6 +260,16 @@ class DeviceKrylov:
         nbytes = int(D.lib().b2s_bicgstab_workspace_bytes(n, b, D.NPARTS))
         work = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=dev)
         fuse = False
+        dw, wtabs = None, ()
+        if wells is not None and not wells.is_empty:
+            from .wells import DeviceWells
+            cmap = None
+            if fact is not None and not fact._identity_perm:
+                cmap = np.asarray(fact.plan.permutation)   # old row -> plan row
+            dw = DeviceWells(wells, b, n, cell_map=cmap)
+            wtabs = dw.loop_tables(smap.row0[: smap.nslices].cpu().numpy(),
+                                   smap.nrows[: smap.nslices].cpu().numpy())
+            fuse_env = False   # the fused colour passes produce v before p^ is complete
         if sell is not None and fact is not None and sell is fact.a_sell:
             # U's colour-0 rows are this very layout (factor2c.cu): fusable by construction
             fuse = fact.phased and fuse_env
@@ -267,7 +282,7 @@ class DeviceKrylov:
                                          D.ptr(sell.vals), D.ptr(up.sp), D.ptr(up.cols),
                                          D.ptr(up.vals), C.byref(ok), D.stream()), "fuse_check")
             fuse = bool(ok.value)
-        return cls(n, b, smap, sell, fact, work, fuse)
+        return cls(n, b, smap, sell, fact, work, fuse, dw, wtabs)
 
     def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
               check_lag: int = 2, mesh=None, x0_zero: bool = False) -> BicgResult:
@@ -305,6 +320,11 @@ class DeviceKrylov:
         if mesh is not None:
             args.mesh = C.addressof(mesh)
         args.x0_zero = 1 if x0_zero else 0   # caller guarantees x == 0 on entry
+        if self.wells is not None and self.wells.nwells:
+            args.wells = C.addressof(self.wells._args)
+            sl, ln, corr = self.wtabs
+            args.well_slice, args.well_lane, args.well_corr = D.ptr(sl), D.ptr(ln), D.ptr(corr)
+            args.well_scratch = D.ptr(self.wells.scratch)
         res = BicgResult()
         check(D.lib().b2s_bicgstab(C.byref(args), C.byref(res)), "bicgstab")
         return res
@@ -335,7 +355,7 @@ def bicgstab(op, precond, b: BlockVector, x0: BlockVector | None = None,
         x0 = BlockVector.zeros(op.num_blocks, op.block_size)
     elif x0.block_size != b.block_size or x0.num_blocks != b.num_blocks:
         raise ShapeError("initial guess does not match the right-hand side")
-    native = (type(op) is MatrixOperator and
+    native = (type(op) in (MatrixOperator, WellAugmentedOperator) and
               (precond is None or isinstance(precond, Ilu0Factorization)) and
               op.num_blocks > 0)
     # WellAugmentedOperator and other operators/preconditioners: host-driven
@@ -349,13 +369,15 @@ def _bicgstab_native(op: MatrixOperator, fact, b: BlockVector, x0: BlockVector,
                      stop: StoppingCriteria, krylov: DeviceKrylov | None = None,
                      x0_zero: bool = False):
     t0 = time.perf_counter()
-    kr = krylov or DeviceKrylov.build(op.matrix, fact)
+    wells = op.wells if isinstance(op, WellAugmentedOperator) and op._separate() else None
+    kr = krylov or DeviceKrylov.build(op.matrix, fact, wells=wells)
     n, bs = kr.n, kr.b
     dev = kr.work.device
     bd, xd = D.f64(b.data, dev), D.f64(x0.data, dev)
     if x0_zero:
         r0 = bd
     else:   # input-order residual through the public operator (bs/krylov.py:175)
+        op.prepare()
         y = D.empty_f64(n * bs, dev)
         op.apply_device(xd, y)
         r0 = bd - y[: n * bs]

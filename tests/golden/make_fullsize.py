@@ -76,8 +76,21 @@ def ref_matrix(bundle):
 
 
 def band_iterations(a, f, rhs, tol, k, seed=1234):
+    """The reference's own iteration spread: k solves with an operator whose
+    results carry 1e-15 relative noise (what another summation order does),
+    then k with factors scaled by 1 + 1e-14 N(0,1)."""
     rng = np.random.default_rng(seed)
     its = []
+    for _ in range(k):
+        op = bs.MatrixOperator(a)
+        base = op.apply_array
+
+        def noisy(v, base=base):
+            y = base(v)
+            return y * (1.0 + 1e-15 * rng.standard_normal(y.shape))
+        op.apply_array = noisy
+        _, r2 = bs.bicgstab(op, f, rhs, stop=bs.StoppingCriteria(tol, 200))
+        its.append(r2.iterations)
     for _ in range(k):
         for ph in (f._forward, f._backward):
             ph.blocks[:] *= 1.0 + 1e-14 * rng.standard_normal(ph.blocks.shape)
@@ -87,7 +100,7 @@ def band_iterations(a, f, rhs, tol, k, seed=1234):
     return its
 
 
-def run(case: str, solve: bool, band: int, tol: float = 1e-8):
+def run(case: str, solve: bool, band: int, tol: float = 1e-8, plans=("level", "color")):
     a, rhs = ref_matrix(CASES[case]())
     n, b, nnzb = a.num_block_rows, a.block_size, a.pattern.num_blocks
     blk, vec = samples(nnzb, n * b)
@@ -99,7 +112,7 @@ def run(case: str, solve: bool, band: int, tol: float = 1e-8):
     meta = {"case": case, "n": n, "nnzb": nnzb}
     y = bs.spmv(a, bs.BlockVector(x, b)).data
     out["spmv_sample"], out["spmv_norm"] = y[vec], np.array(np.linalg.norm(y))
-    for s in ("level", "color"):
+    for s in plans:
         t0 = time.time()
         plan = bs.level_schedule(a.pattern) if s == "level" else bs.graph_color(a.pattern)
         out[f"{s}_groups"] = np.array(plan.group_count)
@@ -138,16 +151,18 @@ def run(case: str, solve: bool, band: int, tol: float = 1e-8):
                 out[f"{s}_band"] = np.array([min(its), max(its)])
                 m["band"] = [min(its), max(its)]
         meta[s] = m
-    np.savez_compressed(HERE / f"full_{case}.npz", **out)
+    tag = "" if tuple(plans) == ("level", "color") else "_" + "_".join(plans)
+    np.savez_compressed(HERE / f"full_{case}{tag}.npz", **out)
     print(json.dumps(meta), flush=True)
 
 
 def main(argv):
     solve = "--solve" in argv
     band = int(argv[argv.index("--band") + 1]) if "--band" in argv else 0
+    plans = tuple(p for p in ("level", "color") if f"--{p}" in argv) or ("level", "color")
     cases = [c for c in argv if c in CASES]
     for c in cases:
-        run(c, solve, band)
+        run(c, solve, band, plans=plans)
 
 
 if __name__ == "__main__":

@@ -16,7 +16,9 @@ from oracle import port as O  # noqa: E402
 from paper_2309_11488_b200.distributed import local_solver, slab_bounds, solve_shards  # noqa: E402
 
 
-def oracle_partitioned(spec, world, tol):
+def oracle_partitioned(spec, world, tol, plan="level"):
+    """The reference's partitioned recipe with the given plan (level schedule
+    or graph colouring of the relaxed pattern)."""
     full = P.generate(spec)
     a = full.a
     rp, ci, v3 = a.pattern.row_pointers, a.pattern.column_indices, a.values3d
@@ -26,7 +28,8 @@ def oracle_partitioned(spec, world, tol):
         z0, z1 = slab_bounds(spec.nz, world, r)
         part[z0 * nxy:z1 * nxy] = r
     jrp, jci, jv, _ = O.drop_cross(rp, ci, v3, part)
-    f = O.ilu0(jrp, jci, jv, O.plan_from_groups(O.level_groups(jrp, jci)))
+    groups = (O.level_groups if plan == "level" else O.color_groups)(jrp, jci)
+    f = O.ilu0(jrp, jci, jv, O.plan_from_groups(groups))
     x, rep = O.bicgstab(lambda v: O.spmv(rp, ci, v3, v), lambda r: O.ilu0_apply(f, r),
                         full.rhs.data, tol=tol)
     return x, rep
@@ -80,11 +83,11 @@ def test_mesh_solve_matches_partitioned_oracle(dims, world, backend):
         (rep.iterations, rep_h.iterations)
     np.testing.assert_allclose(rep.initial_norm, rep_h.initial_norm, rtol=1e-12)
     assert np.linalg.norm(x - xh) <= 1e-6 * np.linalg.norm(xh)
-    if backend == "level":
-        xo, ro = oracle_partitioned(spec, world, tol)
-        assert abs(rep.iterations - ro.iterations) <= max(1.0, 0.1 * ro.iterations), \
-            (rep.iterations, ro.iterations)
-        assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
+    # against the reference's partitioned recipe with the same plan
+    xo, ro = oracle_partitioned(spec, world, tol, backend)
+    assert abs(rep.iterations - ro.iterations) <= max(1.0, 0.1 * ro.iterations), \
+        (rep.iterations, ro.iterations)
+    assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
     # a second solve on the same buffers (sequence numbers move on)
     rep2, xs2 = solve_shards_mesh(shards, P.StoppingCriteria(tol, 200))
     assert rep2.iterations == rep.iterations
@@ -230,3 +233,112 @@ def test_mesh_nonzero_initial_guess(backend):
     x = np.concatenate([v.cpu().numpy() for v in xs])
     xh = np.concatenate([v.cpu().numpy() for v in xs_h])
     assert np.linalg.norm(x - xh) <= 1e-6 * np.linalg.norm(xh)
+
+
+@pytest.mark.parametrize("backend", ["level", "color"])
+def test_sharded_host_loop_matches_partitioned_oracle_per_plan(backend):
+    """Colour shards too (not only level): the host-driven sharded loop
+    against the reference's partitioned recipe with the same plan."""
+    spec = P.GeneratorSpec(8, 7, 12, seed=5, diagonal_boost=1e-2)
+    tol = 1e-8
+    xo, ro = oracle_partitioned(spec, 2, tol, backend)
+    shards, comm = local_solver(spec, 2, P.Backend.from_name(backend))
+    rep, xs = solve_shards(shards, comm, P.StoppingCriteria(tol, 200))
+    x = np.concatenate([v.cpu().numpy() for v in xs])
+    assert rep.converged and ro.converged
+    assert abs(rep.iterations - ro.iterations) <= max(1.0, 0.1 * ro.iterations)
+    assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
+
+
+def test_mesh_dead_peer_times_out_instead_of_hanging(monkeypatch):
+    """A shard whose peer never runs: its bounded device waits expire, the
+    abort word goes up on every rank and the solve raises PeerTimeout
+    (B2S_PEER_TIMEOUT) within the configured timeout instead of spinning
+    forever (csrc/ctl.cuh wait_ge)."""
+    import time
+
+    from paper_2309_11488_b200._lib import PeerTimeout
+    from paper_2309_11488_b200.distributed import (_mesh_krylov, _mesh_prepare, _mesh_struct)
+    monkeypatch.setenv("B2S_MESH_TIMEOUT_MS", "300")
+    spec = P.GeneratorSpec(8, 7, 12, seed=5, diagonal_boost=1e-2)
+    shards, _ = local_solver(spec, 2, P.Backend.LEVEL_SCHEDULED)
+    mss = [_mesh_prepare(s, 2) for s in shards]
+    ptrs = [s.mesh.local_ptrs() for s in shards]
+    s = shards[0]
+    mss[0].peers = ptrs
+    owner_rows = {h: shards[h].send[0].cpu().numpy() for h in s.recv}
+    mesh, keep = _mesh_struct(s, mss[0], owner_rows, shared_device=True)
+    kr = _mesh_krylov(s, mss[0])
+    t0 = time.perf_counter()
+    with pytest.raises(PeerTimeout):
+        kr.solve(s.rhs_p, mss[0].x, P.StoppingCriteria(1e-8, 200), mesh=mesh, x0_zero=True)
+    assert time.perf_counter() - t0 < 60.0
+    # the abort word is up on the silent peer too
+    assert int(shards[1].mesh.mbox[-8:].view(torch.int64)[0].item()) == 1
+    torch.cuda.synchronize()
+    # after a PeerTimeout the mesh state is rebuilt (sequence numbers and
+    # abort words start afresh) and the shards solve normally
+    from paper_2309_11488_b200.distributed import solve_shards_mesh
+    monkeypatch.delenv("B2S_MESH_TIMEOUT_MS")
+    for sh in shards:
+        sh.mesh = None
+    rep, _ = solve_shards_mesh(shards, P.StoppingCriteria(1e-8, 200))
+    assert rep.converged
+
+
+def test_mesh_needs_enough_hardware_queues(monkeypatch):
+    from paper_2309_11488_b200.distributed import solve_shards_mesh
+    spec = P.GeneratorSpec(8, 7, 12, seed=5, diagonal_boost=1e-2)
+    shards, _ = local_solver(spec, 4, P.Backend.LEVEL_SCHEDULED)
+    monkeypatch.setenv("CUDA_DEVICE_MAX_CONNECTIONS", "4")
+    with pytest.raises(RuntimeError, match="CUDA_DEVICE_MAX_CONNECTIONS"):
+        solve_shards_mesh(shards, P.StoppingCriteria(1e-8, 200))
+
+
+def _torchrun(args, world, timeout=300):
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           *args]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=root)
+
+
+def test_nccl_comm_host_loop_two_processes():
+    """NcclComm (the host-driven sharded loop over torch.distributed) in two
+    processes on the one GPU: NCCL refuses two ranks on one device, so the
+    group is gloo here (halos and partial sums staged through the host);
+    the same code path runs over NCCL on one GPU per rank."""
+    import json
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = _torchrun([str(root / "tests" / "workers" / "mesh_worker.py"), "8,7,12", "color",
+                     "--same-gpu", "--comm-loop"], 2)
+    assert out.returncode == 0, out.stderr[-3000:]
+    got = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    spec = P.GeneratorSpec(8, 7, 12, seed=5, diagonal_boost=1e-2)
+    shards, comm = local_solver(spec, 2, P.Backend.GRAPH_COLORED)
+    rep, xs = solve_shards(shards, comm, P.StoppingCriteria(1e-8, 200))
+    x = np.concatenate([v.cpu().numpy() for v in xs])
+    assert all(got["converged"])
+    assert got["iterations"][0] == rep.iterations
+    assert np.linalg.norm(np.asarray(got["x"]) - x) <= 1e-12 * np.linalg.norm(x)
+
+
+def test_nccl_comm_world_of_one_over_nccl():
+    """The same host loop over a real NCCL communicator (one rank)."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = _torchrun([str(root / "bench.py"), "--gpus", "1", "--force-dist", "--dist-comm", "nccl",
+                     "--grid", "24,20,16", "--steps", "2", "--warmup", "1", "--no-e2e",
+                     "--no-cpu"], 1)
+    assert out.returncode == 0, out.stderr[-3000:]
+    import json
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["value"] > 0 and line.get("converged", True)

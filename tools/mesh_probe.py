@@ -4,9 +4,13 @@ peer-memory device loop vs the host-driven loop)
 python tools/mesh_probe.py [world] [backend]
 """
 import json
+import os
 import sys
 import time
 from pathlib import Path
+
+# one hardware queue per shard stream (solve_shards_mesh checks it)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
