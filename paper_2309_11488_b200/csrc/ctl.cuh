@@ -12,6 +12,21 @@ namespace b2s {
 
 constexpr double kBreakdown = 1e-60;  // bs/krylov.py:27
 
+// BiCGStab's vector updates with explicit roundings (no contraction choice
+// left to the compiler), so every kernel that forms one -- the plain vector
+// passes and the fused colour passes that form p and s on the fly -- gets
+// the same bits.
+__device__ __forceinline__ double bicg_p(double r, double p, double v, double beta,
+                                         double omega) {
+  return __fma_rn(beta, __fma_rn(-omega, v, p), r);   // r + beta (p - omega v)
+}
+__device__ __forceinline__ double bicg_axpy(double y, double a, double x) {
+  return __fma_rn(-a, x, y);                           // y - a x
+}
+__device__ __forceinline__ double bicg_xupd(double x, double a, double d) {
+  return __fma_rn(a, d, x);                            // x + a d
+}
+
 enum Reason { kRunning = 0, kConverged = 1, kBreakdownR = 2, kNumerical = 3, kBudget = 4,
               kAborted = 5 /* sharded: a peer did not answer in time, or aborted */ };
 
@@ -20,6 +35,8 @@ struct State {
   double norm0, target, final_norm, its;
   int k, maxit, done, reason;
   int init_exit;   // finished by k_ctl_init (no iteration): zero/non-finite r0, rho_0 breakdown
+  int xpend;       // fused vector passes: x still lacks alpha p^ (added with omega s^ in the
+                   // r-update, or by k_x_fixup when the solve ends in between)
   long long cseq;  // mesh: control points passed (mailbox sequence)
   long long pub;   // mesh: vectors published (readiness-flag sequence)
 };
@@ -92,35 +109,57 @@ __device__ __forceinline__ bool wait_ge(const long long* f, long long seq, doubl
 // into slot s again only after passing the control points in between, which
 // need every other rank's later posts.  Returns false (abort raised on every
 // rank) when some rank does not post in time.
-__device__ __forceinline__ bool mesh_sum(const MeshDev& m, long long seq, int slot, double& a,
-                                         double& b) {
+__device__ __forceinline__ bool mesh_sum3(const MeshDev& m, long long seq, int slot, double& a,
+                                          double& b, double& c) {
   const int N = m.nranks;
   for (int h = 0; h < N; ++h) {
     double* e = m.peer_mbox[h] + ((long long)slot * N + m.rank) * 4;
     st_relaxed_sys(e, a);
     st_relaxed_sys(e + 1, b);
+    st_relaxed_sys(e + 3, c);
   }
   __threadfence_system();
   for (int h = 0; h < N; ++h)
     st_release_sys(reinterpret_cast<long long*>(m.peer_mbox[h] + ((long long)slot * N + m.rank) * 4 + 2),
                    seq);
-  double sa = 0.0, sb = 0.0;
+  double sa = 0.0, sb = 0.0, sc = 0.0;
   for (int h = 0; h < N; ++h) {
     const double* e = m.mbox + ((long long)slot * N + h) * 4;
     if (!wait_ge(reinterpret_cast<const long long*>(e + 2), seq, m.mbox, N, m.timeout_ns)) {
       mesh_raise_abort(m.peer_mbox, N);
-      a = b = __longlong_as_double(0x7FF8000000000000ll);
+      a = b = c = __longlong_as_double(0x7FF8000000000000ll);
       return false;
     }
     sa += ld_relaxed_sys(e);
     sb += ld_relaxed_sys(e + 1);
+    sc += ld_relaxed_sys(e + 3);
   }
   a = sa;
   b = sb;
+  c = sc;
   return true;
 }
+__device__ __forceinline__ bool mesh_sum(const MeshDev& m, long long seq, int slot, double& a,
+                                         double& b) {
+  double c = 0.0;
+  return mesh_sum3(m, seq, slot, a, b, c);
+}
 
-enum CtlStep { kCtlNone = 0, kCtlAlpha = 1, kCtlS = 2, kCtlOmega = 3, kCtlEndBegin = 4 };
+enum Pre { kPreNone = 0, kPreP = 1, kPreS = 2 };
+
+struct PreIn {
+  const State* st;
+  const double* r;
+  const double* v;
+  double* io;      // kPreP: p (old in, new out); kPreS: s (out)
+  double* pss;     // kPreS: one |s|^2 partial per CTA
+};
+
+// kCtlOmegaS: the fused vector passes form s together with s^ and t, so the
+// half-step exit test on |s| runs here, before omega (same order of tests as
+// the reference: |s| finite, |s| <= target, then t.t and omega breakdowns)
+enum CtlStep { kCtlNone = 0, kCtlAlpha = 1, kCtlS = 2, kCtlOmega = 3, kCtlEndBegin = 4,
+               kCtlOmegaS = 5 };
 
 struct Ctl {
   State* st;            // solver state (nullptr: no control step)
@@ -128,6 +167,8 @@ struct Ctl {
   int* host_done;       // mapped pinned word the host polls (may be nullptr)
   int step;             // CtlStep
   MeshDev mesh;         // sharded solve: all-reduce the sums first
+  const double* p2;     // kCtlOmegaS: the |s|^2 partials ...
+  int np2;              // ... and their count
 };
 
 // deterministic sum of np partials by one CTA (L2 loads: written by other SMs)
@@ -164,11 +205,14 @@ __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const do
                                         double* red) {
   State* st = c.st;
   const double a0 = reduce_parts_cg(p0, np, red);
-  double b = 0.0;
-  if (c.step == kCtlOmega || c.step == kCtlEndBegin) b = reduce_parts_cg(p1, np, red);
+  double b = 0.0, c2 = 0.0;
+  if (c.step == kCtlOmega || c.step == kCtlEndBegin || c.step == kCtlOmegaS)
+    b = reduce_parts_cg(p1, np, red);
+  if (c.step == kCtlOmegaS) c2 = reduce_parts_cg(c.p2, c.np2, red);
   if (threadIdx.x != 0) return;
   double a = a0;
-  if (c.mesh.mbox && !mesh_sum(c.mesh, c.mesh.seq_base + (++st->cseq), c.step, a, b)) {
+  const int slot = c.step == kCtlOmegaS ? kCtlOmega : c.step;
+  if (c.mesh.mbox && !mesh_sum3(c.mesh, c.mesh.seq_base + (++st->cseq), slot, a, b, c2)) {
     ctl_finish(st, c.host_done, kAborted);
     return;
   }
@@ -192,7 +236,20 @@ __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const do
       st->omega = om;
       return;
     }
+    case kCtlOmegaS: {  // |s| (bs/krylov.py:211-220), then tt, ts (:223-229)
+      st->its += 0.5;
+      st->xpend = 1;   // x += alpha p^ is deferred to the r-update (or k_x_fixup)
+      const double ns = sqrt(c2);
+      if (!isfinite(ns)) { ctl_finish(st, c.host_done, kNumerical); return; }
+      if (ns <= st->target) { st->final_norm = ns; ctl_finish(st, c.host_done, kConverged); return; }
+      if (a < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
+      const double om = b / a;
+      if (fabs(om) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
+      st->omega = om;
+      return;
+    }
     case kCtlEndBegin: {  // end of iteration k, then the top of k+1 (bs/krylov.py:195-200,230-240)
+      st->xpend = 0;   // the r-update advanced x by alpha p^ + omega s^
       st->its += 0.5;
       const double nr = sqrt(a);
       if (!isfinite(nr)) { ctl_finish(st, c.host_done, kNumerical); return; }

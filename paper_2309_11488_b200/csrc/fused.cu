@@ -26,20 +26,126 @@
 
 namespace b2s {
 
-template <int B, int MODE>
-__global__ void __launch_bounds__(256) k_bwd_spmv(SliceMap map, int s0, int s1, Sell a,
-                                                  const double* __restrict__ dtiles,
-                                                  const double* __restrict__ yin,
-                                                  double* __restrict__ z,
-                                                  double* __restrict__ v,
-                                                  const double* __restrict__ w,
-                                                  double* __restrict__ part0,
-                                                  double* __restrict__ part1, const int* done) {
+template <int PRE>
+__device__ __forceinline__ double pre_form(double r, double p, double v, int k, double beta,
+                                           double omega, double alpha) {
+  if (PRE == kPreP) return k == 0 ? r : bicg_p(r, p, v, beta, omega);
+  return bicg_axpy(r, alpha, v);
+}
+
+// strict-lower row sum of the colour-1 forward pass with on-the-fly inputs
+// (phase_row_sum's order: entries in pairs, ascending columns)
+template <int B, int PRE>
+__device__ __forceinline__ void pre_row_sum(const Sell& m, int slot0, int width, int lane,
+                                            const PreIn& in, int k, double beta, double omega,
+                                            double alpha, double (&acc)[B]) {
+  constexpr int BB = B * B;
+  int cn0 = width > 0 ? __ldcs(m.cols + slot0 + lane) : -1;
+  int cn1 = width > 1 ? __ldcs(m.cols + slot0 + 32 + lane) : -1;
+  for (int kk = 0; kk < width; kk += 2) {
+    const int col[2] = {cn0, cn1};
+    cn0 = kk + 2 < width ? __ldcs(m.cols + slot0 + 32 * (kk + 2) + lane) : -1;
+    cn1 = kk + 3 < width ? __ldcs(m.cols + slot0 + 32 * (kk + 3) + lane) : -1;
+    double blk[2][BB], dr[2][B], dp[2][B], dv[2][B];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int e = 0; e < BB; ++e)
+        blk[q][e] = col[q] >= 0 ? __ldcs(m.vals + vidx(slot0, kk + q, e, lane, BB)) : 0.0;
+      const long long cq = col[q] < 0 ? 0 : col[q];
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        dr[q][c] = col[q] >= 0 ? __ldg(in.r + cq * B + c) : 0.0;
+        dv[q][c] = (col[q] >= 0 && (PRE == kPreS || k > 0)) ? __ldg(in.v + cq * B + c) : 0.0;
+        dp[q][c] = (PRE == kPreP && col[q] >= 0 && k > 0) ? __ldg(in.io + cq * B + c) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (col[q] < 0) continue;
+      double dep[B], pr[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c)
+        dep[c] = pre_form<PRE>(dr[q][c], dp[q][c], dv[q][c], k, beta, omega, alpha);
+      matvec<B>(blk[q], dep, pr);
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] += pr[c];
+    }
+  }
+}
+
+// colour 1 (the last group of a 2-colouring: no upper entries):
+// u = p or s formed on the fly (stored), z = inv(U_ii) (u - L u)
+template <int B, int PRE>
+__global__ void __launch_bounds__(256) k_fwd_pre(int s0, int s1, SliceMap map, Sell lo,
+                                                 const double* __restrict__ dtiles, PreIn in,
+                                                 double* __restrict__ z, const int* done) {
   constexpr int BB = B * B;
   __shared__ double red[8];
   griddep_wait();
   griddep_launch();
   if (done && *done) return;
+  const int k = in.st->k;
+  const double beta = in.st->beta, omega = in.st->omega, alpha = in.st->alpha;
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  double ss = 0.0;
+  for (long long s = s0 + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < s1;
+       s += nw) {
+    const bool ok = lane < map.nrows[s];
+    const long long i = (long long)map.row0[s] + lane;
+    const int slot0 = lo.sp[s];
+    const int width = (lo.sp[s + 1] - slot0) >> 5;
+    double own[B], acc[B], dinv[BB];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      const double rr = ok ? __ldcs(in.r + i * B + c) : 0.0;
+      const double vv = (ok && (PRE == kPreS || k > 0)) ? __ldcs(in.v + i * B + c) : 0.0;
+      const double pp = (ok && PRE == kPreP && k > 0) ? __ldcs(in.io + i * B + c) : 0.0;
+      own[c] = pre_form<PRE>(rr, pp, vv, k, beta, omega, alpha);
+      acc[c] = 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < BB; ++e) dinv[e] = __ldcs(dtiles + (s * BB + e) * 32 + lane);
+    pre_row_sum<B, PRE>(lo, slot0, width, lane, in, k, beta, omega, alpha, acc);
+    if (!ok) continue;
+    double tv[B], out[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      in.io[i * B + c] = own[c];
+      if (PRE == kPreS) ss = fma(own[c], own[c], ss);
+      tv[c] = canon(own[c] - acc[c]) - 0.0;   // backward row of the last group: acc = 0
+    }
+    matvec<B>(dinv, tv, out);
+#pragma unroll
+    for (int c = 0; c < B; ++c) z[i * B + c] = canon(out[c]);
+  }
+  if (PRE == kPreS) {
+    const double t = block_sum(ss, red);
+    if (threadIdx.x == 0) in.pss[blockIdx.x] = t;
+  }
+}
+
+template <int B, int MODE, int PRE>
+__global__ void __launch_bounds__(256) k_bwd_spmv(SliceMap map, int s0, int s1, Sell a,
+                                                  const double* __restrict__ dtiles,
+                                                  const double* __restrict__ yin,
+                                                  double* __restrict__ z,
+                                                  double* v,
+                                                  const double* __restrict__ w,
+                                                  double* __restrict__ part0,
+                                                  double* __restrict__ part1, const int* done,
+                                                  PreIn in) {
+  constexpr int BB = B * B;
+  __shared__ double red[8];
+  griddep_wait();
+  griddep_launch();
+  if (done && *done) return;
+  int k = 0;
+  double beta = 0.0, omega = 0.0, alpha = 0.0, ss = 0.0;
+  if (PRE != kPreNone) {
+    k = in.st->k; beta = in.st->beta; omega = in.st->omega; alpha = in.st->alpha;
+  }
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -52,7 +158,14 @@ __global__ void __launch_bounds__(256) k_bwd_spmv(SliceMap map, int s0, int s1, 
     double yv[B], acc[B], dinv[BB], dg[BB];
 #pragma unroll
     for (int c = 0; c < B; ++c) {
-      yv[c] = ok ? __ldcs(yin + i * B + c) : 0.0;
+      if (PRE == kPreNone) {
+        yv[c] = ok ? __ldcs(yin + i * B + c) : 0.0;
+      } else {   // this row's p or s, formed here (kPreP reads the old v before v_i is written)
+        const double rr = ok ? __ldcs(in.r + i * B + c) : 0.0;
+        const double vv = (ok && (PRE == kPreS || k > 0)) ? __ldcs(in.v + i * B + c) : 0.0;
+        const double pp = (ok && PRE == kPreP && k > 0) ? __ldcs(in.io + i * B + c) : 0.0;
+        yv[c] = pre_form<PRE>(rr, pp, vv, k, beta, omega, alpha);
+      }
       acc[c] = 0.0;
     }
 #pragma unroll
@@ -95,6 +208,13 @@ __global__ void __launch_bounds__(256) k_bwd_spmv(SliceMap map, int s0, int s1, 
     }
     if (!ok) continue;
     double tv[B], zi[B], di[B];
+    if (PRE != kPreNone) {
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        in.io[i * B + c] = yv[c];
+        if (PRE == kPreS) ss = fma(yv[c], yv[c], ss);
+      }
+    }
 #pragma unroll
     for (int c = 0; c < B; ++c) tv[c] = yv[c] - acc[c];
     matvec<B>(dinv, tv, zi);
@@ -109,8 +229,16 @@ __global__ void __launch_bounds__(256) k_bwd_spmv(SliceMap map, int s0, int s1, 
       const double vv = acc[c] + di[c];
       v[i * B + c] = vv;
       if (MODE == kDotW) p0 = fma(w[i * B + c], vv, p0);
-      if (MODE == kSelfAndW) { p0 = fma(vv, vv, p0); p1 = fma(vv, w[i * B + c], p1); }
+      if (MODE == kSelfAndW) {   // w = s: formed in this very pass under kPreS
+        const double wv = PRE == kPreS ? yv[c] : w[i * B + c];
+        p0 = fma(vv, vv, p0);
+        p1 = fma(vv, wv, p1);
+      }
     }
+  }
+  if (PRE == kPreS) {
+    const double t = block_sum(ss, red);
+    if (threadIdx.x == 0) in.pss[blockIdx.x] = t;
   }
   double t0 = block_sum(p0, red);
   if (threadIdx.x == 0) part0[blockIdx.x] = t0;
@@ -159,36 +287,89 @@ inline int one_wave(const void* fn, int cap) {
   return per_sm * sms < cap ? per_sm * sms : cap;
 }
 
-template <int B>
-int launch_bwd_spmv_b(int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
-                      const double* yin, double* z, double* v, const double* w, double* p0,
-                      double* p1, const int* done, int* grid_out, cudaStream_t st, bool pdl) {
+template <int B, int PRE>
+int launch_bwd_spmv_bp(int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
+                       const double* yin, double* z, double* v, const double* w, double* p0,
+                       double* p1, const int* done, int* grid_out, cudaStream_t st, bool pdl,
+                       PreIn in) {
   if (mode == kDotW) {
-    const int g = one_wave((const void*)k_bwd_spmv<B, kDotW>, nparts);
+    const int g = one_wave((const void*)k_bwd_spmv<B, kDotW, PRE>, nparts);
     *grid_out = g;
-    launch_k(k_bwd_spmv<B, kDotW>, dim3(g), dim3(256), 0, st, pdl, map, 0, s1, a, dt, yin, z, v,
-             w, p0, p1, done);
+    launch_k(k_bwd_spmv<B, kDotW, PRE>, dim3(g), dim3(256), 0, st, pdl, map, 0, s1, a, dt, yin, z,
+             v, w, p0, p1, done, in);
   } else if (mode == kSelfAndW) {
-    const int g = one_wave((const void*)k_bwd_spmv<B, kSelfAndW>, nparts);
+    const int g = one_wave((const void*)k_bwd_spmv<B, kSelfAndW, PRE>, nparts);
     *grid_out = g;
-    launch_k(k_bwd_spmv<B, kSelfAndW>, dim3(g), dim3(256), 0, st, pdl, map, 0, s1, a, dt, yin, z,
-             v, w, p0, p1, done);
+    launch_k(k_bwd_spmv<B, kSelfAndW, PRE>, dim3(g), dim3(256), 0, st, pdl, map, 0, s1, a, dt,
+             yin, z, v, w, p0, p1, done, in);
   } else {
     return B2S_SHAPE;
   }
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
+template <int B>
+int launch_bwd_spmv_b(int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
+                      const double* yin, double* z, double* v, const double* w, double* p0,
+                      double* p1, const int* done, int* grid_out, cudaStream_t st, bool pdl,
+                      int pre, PreIn in) {
+  if (pre == kPreP)
+    return launch_bwd_spmv_bp<B, kPreP>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done,
+                                        grid_out, st, pdl, in);
+  if (pre == kPreS)
+    return launch_bwd_spmv_bp<B, kPreS>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done,
+                                        grid_out, st, pdl, in);
+  return launch_bwd_spmv_bp<B, kPreNone>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done,
+                                         grid_out, st, pdl, in);
+}
+
 // pass 2 of the fused pair (colour 0 = slices [0, s1)); partials at
-// [0, *grid_out) -- at most nparts CTAs, one resident wave
+// [0, *grid_out) -- at most nparts CTAs, one resident wave.  pre/in: form
+// the input on the fly (kPreP / kPreS, PreIn) instead of reading yin.
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
-                    double* p1, const int* done, int* grid_out, cudaStream_t st, bool pdl) {
+                    double* p1, const int* done, int* grid_out, cudaStream_t st, bool pdl,
+                    int pre, const PreIn* pre_in) {
+  const PreIn in = pre_in ? *pre_in : PreIn{};
   switch (b) {
-    case 1: return launch_bwd_spmv_b<1>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl);
-    case 2: return launch_bwd_spmv_b<2>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl);
-    case 3: return launch_bwd_spmv_b<3>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl);
-    case 4: return launch_bwd_spmv_b<4>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl);
+    case 1: return launch_bwd_spmv_b<1>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl, pre, in);
+    case 2: return launch_bwd_spmv_b<2>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl, pre, in);
+    case 3: return launch_bwd_spmv_b<3>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl, pre, in);
+    case 4: return launch_bwd_spmv_b<4>(mode, nparts, map, s1, a, dt, yin, z, v, w, p0, p1, done, grid_out, st, pdl, pre, in);
+    default: return B2S_UNSUPPORTED;
+  }
+}
+
+// pass 1 with on-the-fly input (colour 1 = slices [s0, s1)); kPreS partials
+// of |s|^2 at in.pss[0, *grid_out)
+template <int B>
+int launch_fwd_pre_b(int nparts, SliceMap map, int s0, int s1, Sell lo, const double* dt,
+                     double* z, const int* done, int* grid_out, cudaStream_t st, bool pdl,
+                     int pre, const PreIn& in) {
+  const void* fn = pre == kPreP ? (const void*)k_fwd_pre<B, kPreP> : (const void*)k_fwd_pre<B, kPreS>;
+  long long g = ((long long)(s1 - s0) + 7) / 8;   // 8 warps per CTA, one slice each
+  const int cap = one_wave(fn, nparts);
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  *grid_out = (int)g;
+  if (pre == kPreP)
+    launch_k(k_fwd_pre<B, kPreP>, dim3((int)g), dim3(256), 0, st, pdl, s0, s1, map, lo, dt, in, z,
+             done);
+  else
+    launch_k(k_fwd_pre<B, kPreS>, dim3((int)g), dim3(256), 0, st, pdl, s0, s1, map, lo, dt, in, z,
+             done);
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
+int launch_fwd_pre(int b, int nparts, SliceMap map, int s0, int s1, Sell lo, const double* dt,
+                   double* z, const int* done, int* grid_out, cudaStream_t st, bool pdl, int pre,
+                   const PreIn* pre_in) {
+  const PreIn in = *pre_in;
+  switch (b) {
+    case 1: return launch_fwd_pre_b<1>(nparts, map, s0, s1, lo, dt, z, done, grid_out, st, pdl, pre, in);
+    case 2: return launch_fwd_pre_b<2>(nparts, map, s0, s1, lo, dt, z, done, grid_out, st, pdl, pre, in);
+    case 3: return launch_fwd_pre_b<3>(nparts, map, s0, s1, lo, dt, z, done, grid_out, st, pdl, pre, in);
+    case 4: return launch_fwd_pre_b<4>(nparts, map, s0, s1, lo, dt, z, done, grid_out, st, pdl, pre, in);
     default: return B2S_UNSUPPORTED;
   }
 }

@@ -52,7 +52,10 @@ int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, doub
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
                     double* p1, const int* done, int* grid_out, cudaStream_t st,
-                    bool pdl = false);
+                    bool pdl = false, int pre = kPreNone, const PreIn* pre_in = nullptr);
+int launch_fwd_pre(int b, int nparts, SliceMap map, int s0, int s1, Sell lo, const double* dt,
+                   double* z, const int* done, int* grid_out, cudaStream_t st, bool pdl, int pre,
+                   const PreIn* pre_in);
 int launch_tiled(int b, const void* handle, const double* r, double* y, double* z, int reset_y,
                  const int* done, cudaStream_t st);
 
@@ -76,6 +79,7 @@ __global__ void k_ctl_init(State* st, const double* prr, int np, double tol, int
     }
     const double n0 = sqrt(s);
     st->rho = 0.0; st->rho_prev = 1.0; st->alpha = 1.0; st->omega = 1.0; st->beta = 0.0;
+    st->xpend = 0;
     st->norm0 = n0; st->target = tol * n0; st->final_norm = n0; st->its = 0.0;
     st->k = 0; st->maxit = maxit; st->reason = kRunning;
     st->done = 0;
@@ -291,19 +295,19 @@ __global__ void __launch_bounds__(256, 4) k_p_update(long long m, const State* s
     for (int u = 0; u < kU; ++u) {
       const long long q = j + u * T;
       if (q < m2)
-        st2(p, q, rr[u].x + beta * (pp[u].x - omega * vv[u].x),
-            rr[u].y + beta * (pp[u].y - omega * vv[u].y));
+        st2(p, q, bicg_p(rr[u].x, pp[u].x, vv[u].x, beta, omega),
+            bicg_p(rr[u].y, pp[u].y, vv[u].y, beta, omega));
     }
   }
   if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0)
-    p[m - 1] = r[m - 1] + beta * (p[m - 1] - omega * v[m - 1]);
+    p[m - 1] = bicg_p(r[m - 1], p[m - 1], v[m - 1], beta, omega);
 }
 
 // s = r - alpha v ; x += alpha p^ ; |s|^2 partials ; optionally p^ <- sentinel
 __device__ __forceinline__ void s_elem(double rv, double vv, double ph, double& xo, double& so,
                                        double alpha, double& acc) {
-  so = rv - alpha * vv;
-  xo += alpha * ph;
+  so = bicg_axpy(rv, alpha, vv);
+  xo = bicg_xupd(xo, alpha, ph);
   acc = fma(so, so, acc);
 }
 
@@ -360,24 +364,28 @@ __global__ void __launch_bounds__(256, 4) k_s_update(long long m, const State* s
 // x += omega s^ ; r = s - omega t ; |r|^2 and r^.r partials ; s^ <- sentinel
 __device__ __forceinline__ void r_elem(double sh, double tv, double sv, double rh, double& xo,
                                        double& ro, double omega, double& a0, double& a1) {
-  xo += omega * sh;
-  ro = sv - omega * tv;
+  xo = bicg_xupd(xo, omega, sh);
+  ro = bicg_axpy(sv, omega, tv);
   a0 = fma(ro, ro, a0);
   a1 = fma(rh, ro, a1);
 }
 
+// XA (fused vector passes): x += alpha p^ happens here too, x = (x + alpha
+// p^) + omega s^ with the same roundings as the two separate updates
+template <bool XA>
 __global__ void __launch_bounds__(256, 4) k_r_update(long long m, const State* st, double* shat,
                                                   const double* __restrict__ tv,
                                                   const double* __restrict__ s,
                                                   const double* __restrict__ rhat,
                                                   double* __restrict__ x,
                                                   double* __restrict__ r, double* prr,
-                                                  double* prho, int reset, Ctl ctl) {
+                                                  double* prho, int reset, Ctl ctl,
+                                                  const double* __restrict__ phat) {
   __shared__ double red[8];
   griddep_wait();
   griddep_launch();
   if (st->done) return;
-  const double omega = st->omega;
+  const double omega = st->omega, alpha = st->alpha;
   double a0 = 0.0, a1 = 0.0;
   const long long m2 = m >> 1, T = (long long)gridDim.x * blockDim.x;
   long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -389,6 +397,11 @@ __global__ void __launch_bounds__(256, 4) k_r_update(long long m, const State* s
       if (q < m2) {
         sh[u] = ld2(shat, q); t2[u] = ld2(tv, q); sv[u] = ld2(s, q); rh[u] = ld2(rhat, q);
         xv[u] = reinterpret_cast<const double2*>(x)[q];
+        if (XA) {
+          const double2 ph = ld2(phat, q);
+          xv[u].x = bicg_xupd(xv[u].x, alpha, ph.x);
+          xv[u].y = bicg_xupd(xv[u].y, alpha, ph.y);
+        }
       }
     }
 #pragma unroll
@@ -406,6 +419,7 @@ __global__ void __launch_bounds__(256, 4) k_r_update(long long m, const State* s
   }
   if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     double r0;
+    if (XA) x[m - 1] = bicg_xupd(x[m - 1], alpha, phat[m - 1]);
     r_elem(shat[m - 1], tv[m - 1], s[m - 1], rhat[m - 1], x[m - 1], r0, omega, a0, a1);
     r[m - 1] = r0;
     if (reset) shat[m - 1] = sentinel();
@@ -415,6 +429,17 @@ __global__ void __launch_bounds__(256, 4) k_r_update(long long m, const State* s
   const double t1 = block_sum(a1, red);
   if (threadIdx.x == 0) prho[blockIdx.x] = t1;
   if (ctl.st && last_cta(ctl.counter)) ctl_run(ctl, prr, prho, gridDim.x, red);
+}
+
+// the fused vector passes end a solve between the s half-step and the
+// r-update without x += alpha p^ (State.xpend): add it once, after the loop
+__global__ void k_x_fixup(long long m, const State* st, const double* __restrict__ phat,
+                          double* __restrict__ x) {
+  if (!st->xpend) return;
+  const double alpha = st->alpha;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m;
+       t += (long long)gridDim.x * blockDim.x)
+    x[t] = bicg_xupd(x[t], alpha, phat[t]);
 }
 
 template <class... P>
@@ -515,6 +540,14 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     return wells ? launch_wells_corr(a->wells, xin, a->well_scratch, a->well_corr, dn, q) : 0;
   };
   const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh_local) && !wells;
+  // fused vector passes on top of the fused colour passes: 7 kernels per
+  // iteration instead of 9.  They move the same bytes (the separate p-update
+  // largely hits L2), so they pay where the iteration is launch-bound --
+  // measured 65.9 vs 71.0 us per iteration at 48k cells, 388.8 vs 384.7 us at
+  // 1M (profiles/r02/vec_fusion.txt): on up to 400k cells by default;
+  // B2S_FUSE_VEC=1/0 forces it
+  const char* fv_env = getenv("B2S_FUSE_VEC");
+  const bool vecf = fused && (fv_env ? fv_env[0] == '1' : a->n <= 400000);
   const int reset = (ilu && !phased) ? 1 : 0;  // sync-free sweeps need sentinel-filled outputs
   MeshDev md{};
   MeshHalo mh{};
@@ -673,60 +706,36 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     const bool pdl = !(pdl_env && pdl_env[0] == '0') && !(mesh && mesh->shared_device);
     double* ph = ilu ? phat : p;
     double* sh = ilu ? shat : s;
-    launch_k(k_p_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
-             (const double*)r, (const double*)v, p);
-    ++kernels;
     const int reset_y = a->refill_y ? 0 : 1;
     const int s1c = fused ? a->gslice_host[1] : 0;
-    if (fused) {
-      launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, p, y,
-                    phat, done, cs, true, pdl);
-      int g0 = np;
-      launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
-                      done, &g0, cs, pdl);
+    if (vecf) {
+      // fused vector passes (7 kernels): p and s are formed inside the colour
+      // passes, the half-step |s| test moves to the omega control step, and
+      // x += alpha p^ + omega s^ is one update in the r-pass
+      PreIn inP{state, r, v, p, nullptr};
+      int gF = np, g0 = np;
+      launch_fwd_pre(a->b, np, map, s1c, map.nslices, L, a->dinv_tiles, phat, done, &gF, cs, pdl,
+                     kPreP, &inP);
+      launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, nullptr, phat, v, rhat, pg,
+                      nullptr, done, &g0, cs, pdl, kPreP, &inP);
       const Ctl ca{state, counters + 0, dev_done, kCtlAlpha, md};
-      // sharded: p^ is complete here -- its halo (publish, wait, pull) runs on
-      // a side branch of the graph, overlapped with the colour-1 SpMV (which
-      // reads only local columns), and joins before the ghost correction
       if (mesh) fork_halo(1, phat);
       launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
                         done, mesh ? Ctl{} : ca, cs, pdl);
       kernels += 3;
-      if (mesh) {   // the boundary rows' ghost couplings + alpha
+      if (mesh) {
         join_halo(1, phat);
         launch_ghost_correct<kDotW>(a->b, mesh, phat + m, v, rhat, pg, nullptr, g0 + np, done, ca,
                                     cs);
         kernels += mh.nghost > 0 ? 4 : 3;
       }
-    } else if (phased) {
-      launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
-                    p, y, phat, done, cs, false, pdl);
-      kernels += 2 * (a->ngroups - 1);
-    } else if (ilu) {
-      if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
-      if (a->tiles) launch_tiled(a->b, a->tiles, p, y, phat, reset_y, done, cs);
-      else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, reset_y, a->sweep_flags,
-                         tickets, done, cs);
-      kernels += 2;
-    }
-    if (mesh && !fused) { halo(cs, 1, ph, done); kernels += mh.nghost > 0 ? 3 : 2; }
-    if (!fused) {
-      if (wells) { well_terms(ph, done, cs); kernels += 2; }
-      launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done,
-                  Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl && !wells, wf);
-      ++kernels;
-    }
-    launch_k(k_s_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
-             (const double*)r, (const double*)v, ph, a->x, s, pss, reset,
-             Ctl{state, counters + 1, dev_done, kCtlS, md});
-    ++kernels;
-    if (fused) {
-      launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, s, y,
-                    shat, done, cs, true, pdl);
-      int g0 = np;
-      launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, s, shat, t, s, ptt, pts, done,
-                      &g0, cs, pdl);
-      const Ctl co{state, counters + 2, dev_done, kCtlOmega, md};
+      PreIn inS{state, r, v, s, pss};
+      launch_fwd_pre(a->b, np, map, s1c, map.nslices, L, a->dinv_tiles, shat, done, &gF, cs, pdl,
+                     kPreS, &inS);
+      PreIn inS0{state, r, v, s, pss + gF};
+      launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, nullptr, shat, t, s, ptt, pts,
+                      done, &g0, cs, pdl, kPreS, &inS0);
+      const Ctl co{state, counters + 2, dev_done, kCtlOmegaS, md, pss, gF + g0};
       if (mesh) fork_halo(2, shat);
       launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
                         mesh ? Ctl{} : co, cs, pdl);
@@ -737,28 +746,97 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                                         cs);
         kernels += mh.nghost > 0 ? 4 : 3;
       }
-    } else if (phased) {
-      launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
-                    s, y, shat, done, cs, false, pdl);
-      kernels += 2 * (a->ngroups - 1);
-    } else if (ilu) {
-      if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
-      if (a->tiles) launch_tiled(a->b, a->tiles, s, y, shat, reset_y, done, cs);
-      else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, reset_y, a->sweep_flags,
-                         tickets, done, cs);
-      kernels += 2;
-    }
-    if (mesh && !fused) { halo(cs, 2, sh, done); kernels += mh.nghost > 0 ? 3 : 2; }
-    if (!fused) {
-      if (wells) { well_terms(sh, done, cs); kernels += 2; }
-      launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done,
-                  Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl && !wells, wf);
+      launch_k(k_r_update<true>, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
+               shat, (const double*)t, (const double*)s, (const double*)rhat, a->x, r, prr, prho,
+               reset, Ctl{state, counters + 3, dev_done, kCtlEndBegin, md},
+               (const double*)phat);
+      ++kernels;
+    } else {
+      launch_k(k_p_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
+               (const double*)r, (const double*)v, p);
+      ++kernels;
+      if (fused) {
+        launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, p, y,
+                      phat, done, cs, true, pdl);
+        int g0 = np;
+        launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
+                        done, &g0, cs, pdl);
+        const Ctl ca{state, counters + 0, dev_done, kCtlAlpha, md};
+        // sharded: p^ is complete here -- its halo (publish, wait, pull) runs on
+        // a side branch of the graph, overlapped with the colour-1 SpMV (which
+        // reads only local columns), and joins before the ghost correction
+        if (mesh) fork_halo(1, phat);
+        launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
+                          done, mesh ? Ctl{} : ca, cs, pdl);
+        kernels += 3;
+        if (mesh) {   // the boundary rows' ghost couplings + alpha
+          join_halo(1, phat);
+          launch_ghost_correct<kDotW>(a->b, mesh, phat + m, v, rhat, pg, nullptr, g0 + np, done, ca,
+                                      cs);
+          kernels += mh.nghost > 0 ? 4 : 3;
+        }
+      } else if (phased) {
+        launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
+                      p, y, phat, done, cs, false, pdl);
+        kernels += 2 * (a->ngroups - 1);
+      } else if (ilu) {
+        if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
+        if (a->tiles) launch_tiled(a->b, a->tiles, p, y, phat, reset_y, done, cs);
+        else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, reset_y, a->sweep_flags,
+                           tickets, done, cs);
+        kernels += 2;
+      }
+      if (mesh && !fused) { halo(cs, 1, ph, done); kernels += mh.nghost > 0 ? 3 : 2; }
+      if (!fused) {
+        if (wells) { well_terms(ph, done, cs); kernels += 2; }
+        launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done,
+                    Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl && !wells, wf);
+        ++kernels;
+      }
+      launch_k(k_s_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
+               (const double*)r, (const double*)v, ph, a->x, s, pss, reset,
+               Ctl{state, counters + 1, dev_done, kCtlS, md});
+      ++kernels;
+      if (fused) {
+        launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, s, y,
+                      shat, done, cs, true, pdl);
+        int g0 = np;
+        launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, s, shat, t, s, ptt, pts, done,
+                        &g0, cs, pdl);
+        const Ctl co{state, counters + 2, dev_done, kCtlOmega, md};
+        if (mesh) fork_halo(2, shat);
+        launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
+                          mesh ? Ctl{} : co, cs, pdl);
+        kernels += 3;
+        if (mesh) {
+          join_halo(2, shat);
+          launch_ghost_correct<kSelfAndW>(a->b, mesh, shat + m, t, s, ptt, pts, g0 + np, done, co,
+                                          cs);
+          kernels += mh.nghost > 0 ? 4 : 3;
+        }
+      } else if (phased) {
+        launch_phased(a->b, a->kc, a->ngroups, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles,
+                      s, y, shat, done, cs, false, pdl);
+        kernels += 2 * (a->ngroups - 1);
+      } else if (ilu) {
+        if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
+        if (a->tiles) launch_tiled(a->b, a->tiles, s, y, shat, reset_y, done, cs);
+        else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, reset_y, a->sweep_flags,
+                           tickets, done, cs);
+        kernels += 2;
+      }
+      if (mesh && !fused) { halo(cs, 2, sh, done); kernels += mh.nghost > 0 ? 3 : 2; }
+      if (!fused) {
+        if (wells) { well_terms(sh, done, cs); kernels += 2; }
+        launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done,
+                    Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl && !wells, wf);
+        ++kernels;
+      }
+      launch_k(k_r_update<false>, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state, sh,
+               (const double*)t, (const double*)s, (const double*)rhat, a->x, r, prr, prho, reset,
+               Ctl{state, counters + 3, dev_done, kCtlEndBegin, md}, (const double*)nullptr);
       ++kernels;
     }
-    launch_k(k_r_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state, sh,
-             (const double*)t, (const double*)s, (const double*)rhat, a->x, r, prr, prho, reset,
-             Ctl{state, counters + 3, dev_done, kCtlEndBegin, md});
-    ++kernels;
     if (cudaStreamEndCapture(cs, &graph) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
     if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
     // shards sharing one GPU replay on their own (caller's) stream: every
@@ -814,6 +892,8 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if (status != B2S_OK) return status;
   res->kernels_per_iteration = kernels;
 
+  if (vecf)   // an exit between the s half-step and the r-update: x += alpha p^
+    k_x_fixup<<<grid_v, 256, 0, user>>>(m, state, phat, a->x);
   B2S_CHECK(cudaMemcpyAsync(&hs, state, sizeof(State), cudaMemcpyDeviceToHost, user));
   B2S_CHECK(cudaStreamSynchronize(user));
   if (hs.reason == kAborted || barrier_failed) return B2S_PEER_TIMEOUT;
@@ -999,7 +1079,8 @@ int b2s_vec_r(long long m, double omega, double* shat, const double* t, const do
   int rc;
   State* d = stage_state(scratch, 0, 0.0, 0.0, omega, st, &rc);
   if (rc) return rc;
-  k_r_update<<<nparts, 256, 0, st>>>(m, d, shat, t, s, rhat, x, r, prr, prho, reset, Ctl{});
+  k_r_update<false><<<nparts, 256, 0, st>>>(m, d, shat, t, s, rhat, x, r, prr, prho, reset, Ctl{},
+                                            nullptr);
   B2S_LAUNCH_CHECK();
   return B2S_OK;
 }

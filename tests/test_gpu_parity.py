@@ -574,3 +574,28 @@ def test_jacobi_relaxed_solve_matches_oracle(backend):
     assert rep.converged and ro.converged and not rep.fallback_used
     assert abs(rep.iterations - ro.iterations) <= 1.0, (rep.iterations, ro.iterations)
     assert np.linalg.norm(x.data - xo) <= 1e-6 * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("dims", [(20, 20, 10), (12, 10, 16)])
+def test_fused_vector_passes_match_separate(monkeypatch, dims):
+    """2-colour loop with the fused vector passes (p and s formed inside the
+    colour passes, the |s| test at the omega step, x += alpha p^ deferred to
+    the r-update or k_x_fixup) against the 9-kernel loop: same iteration count
+    -- including exits at the s half-step, where the deferred update must be
+    applied -- and the same solution to rounding."""
+    bundle = P.generate(P.GeneratorSpec(*dims, seed=11))
+    a, rhs = bundle.a, bundle.rhs
+    f = P.decompose(a, P.graph_color(a.pattern))
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("B2S_FUSE_VEC", flag)
+        for tol, its in ((1e-8, 200), (1e-10, 3)):   # converged at a half step; budget exit
+            x, rep = P.bicgstab(P.MatrixOperator(a), f, rhs, stop=P.StoppingCriteria(tol, its))
+            out[(flag, tol)] = (x.data, rep)
+    for tol in (1e-8, 1e-10):
+        (x1, r1), (x0, r0) = out[("1", tol)], out[("0", tol)]
+        assert r1.iterations == r0.iterations and r1.converged == r0.converged
+        assert r1.failure_reason == r0.failure_reason
+        assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+        np.testing.assert_allclose(r1.final_norm, r0.final_norm, rtol=1e-8)
+    assert out[("1", 1e-8)][1].iterations % 1.0 == 0.5   # the half-step exit is exercised

@@ -1,6 +1,6 @@
 """Per-iteration cost of the device BiCGStab loop on C4 (setup excluded).
 
-python tools/krylov_bench.py [color|level] [iters]
+python tools/krylov_bench.py [color|level] [iters] [nx,ny,nz]
 Runs a fixed number of iterations (tol 1e-30 so the budget ends the solve)
 and prints ms per iteration (CUDA events on the solve stream).
 """
@@ -18,7 +18,8 @@ from paper_2309_11488_b200.bridge import DeviceSolver  # noqa: E402
 
 backend = sys.argv[1] if len(sys.argv) > 1 else "color"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 60
-bundle = P.generate(P.GeneratorSpec(100, 100, 100, seed=0))
+dims = tuple(int(v) for v in sys.argv[3].split(",")) if len(sys.argv) > 3 else (100, 100, 100)
+bundle = P.generate(P.GeneratorSpec(*dims, seed=0))
 a, rhs = bundle.a, bundle.rhs
 bsr = D.DevBSR.upload(a)
 solver = DeviceSolver(a, bsr, P.SolverConfig(backend=P.Backend.from_name(backend))).setup()
@@ -38,7 +39,7 @@ for rep in range(4):
     e1.record(st)
     torch.cuda.synchronize()
     out.append(e0.elapsed_time(e1))
-print(json.dumps({"backend": backend, "iterations": res.iterations, "reason": res.reason,
+print(json.dumps({"backend": backend, "dims": dims, "iterations": res.iterations, "reason": res.reason,
                   "ms": out, "us_per_iter": min(out) / max(res.iterations, 1) * 1e3,
                   "kernels_per_iteration": res.kernels_per_iteration,
                   "graph_launches": res.graph_launches}))
