@@ -405,6 +405,12 @@ int b2s_wells_apply(const b2s_wells* wells, const double* x, double* y, double* 
 
 /* ---- Block-Jacobi copy plan (bs/jacobi.py:111-147) ---------------------- */
 
+/* The greedy heaviest-edge region growing of bs/jacobi.py:61-108 on the host:
+ * undirected edges lo[e] < hi[e] with weights w[e]; part[n] receives the
+ * partition of every cell (k balanced parts, seeds = lowest unassigned
+ * cells, heap order (-w, cell) as heapq) -- the reference's assignment. */
+int b2s_partition_greedy(long long n, long long nedges, const long long* lo, const long long* hi,
+                         const double* w, long long k, long long* part);
 int b2s_jacobi_pattern(int n, const int32_t* rp, const int32_t* ci, const int32_t* part,
                        int32_t* new_rp, int32_t* kept_host, cudaStream_t stream);
 int b2s_jacobi_fill(int n, const int32_t* rp, const int32_t* ci, const int32_t* part,

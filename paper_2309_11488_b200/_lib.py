@@ -95,6 +95,7 @@ SIGNATURES = {
                             _I, _I, _P, _P]),
     "b2s_fill_sentinel": (_I, [_LL, _P, _P]),
     "b2s_dot_chunked": (_I, [_LL, _P, _P, _P, _P, _P]),
+    "b2s_partition_greedy": (_I, [_LL, _LL, _P, _P, _P, _LL, _P]),
     "b2s_wells_apply": (_I, [_P, _P, _P, _P, _P]),
     "b2s_fuse_check": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _PI, _P]),
     "b2s_ilu0_apply_phased": (_I, [_I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P,

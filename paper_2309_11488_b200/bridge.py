@@ -215,11 +215,10 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     x = None
     try:
         if cfg.jacobi_partitions > 0:
-            from .jacobi import drop_cross_blocks, partition, transmissibility_weights
-            parts = partition(a_sys.pattern, transmissibility_weights(a_sys),
-                              cfg.jacobi_partitions)
-            pre_mat, _ = drop_cross_blocks(a_sys, parts)
-            pre_bsr = D.DevBSR.upload(pre_mat)
+            from .jacobi import relax_on_device
+            bsr.wait_values()
+            pre_mat = relax_on_device(a_sys, bsr, cfg.jacobi_partitions)
+            pre_bsr = pre_mat.bsr
         solver = DeviceSolver(a_sys, bsr, cfg, pre_bsr, pre_mat, wells=sep).setup()
         # the reported ||r0|| in the reference's order, beside the loop
         norm0 = RefNorm(_initial_residual(bsr, rhs, None if x0 is None else x0d, sep), n * bs)

@@ -84,3 +84,58 @@ int b2s_jacobi_fill(int n, const int32_t* rp, const int32_t* ci, const int32_t* 
 }
 
 }  // extern "C"
+
+// ---- the greedy partitioner (bs/jacobi.py:61-108), host side ---------------
+//
+// Region growing along the heaviest frontier edge is a strictly sequential
+// priority-queue walk, so it stays on the host (as in the reference), but in
+// C++ instead of Python: the same min-heap on (-w, cell) -- pops are fully
+// determined by that key, so the assignment is the reference's exactly.
+#include <queue>
+#include <utility>
+#include <vector>
+
+extern "C" int b2s_partition_greedy(long long n, long long nedges, const long long* lo,
+                                    const long long* hi, const double* w, long long k,
+                                    long long* part) {
+  if (n < 0 || nedges < 0 || k < 1 || k > (n > 0 ? n : 1)) return B2S_SHAPE;
+  std::vector<long long> deg(n + 1, 0);
+  for (long long e = 0; e < nedges; ++e) {
+    if (lo[e] < 0 || hi[e] >= n || lo[e] >= hi[e]) return B2S_SHAPE;
+    ++deg[lo[e] + 1];
+    ++deg[hi[e] + 1];
+  }
+  for (long long i = 0; i < n; ++i) deg[i + 1] += deg[i];
+  std::vector<long long> pos(deg.begin(), deg.end() - 1), adj(2 * nedges);
+  std::vector<double> aw(2 * nedges);
+  for (long long e = 0; e < nedges; ++e) {
+    adj[pos[lo[e]]] = hi[e]; aw[pos[lo[e]]++] = w[e];
+    adj[pos[hi[e]]] = lo[e]; aw[pos[hi[e]]++] = w[e];
+  }
+  for (long long i = 0; i < n; ++i) part[i] = -1;
+  typedef std::pair<double, long long> Item;   // (-w, cell): heapq's order
+  std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+  const long long base = n / k, rem = n % k;
+  long long seed = 0;
+  for (long long q = 0; q < k; ++q) {
+    const long long want = base + (q < rem ? 1 : 0);
+    long long got = 0;
+    while (!heap.empty()) heap.pop();
+    while (got < want) {
+      long long cell;
+      if (!heap.empty()) {
+        cell = heap.top().second;
+        heap.pop();
+        if (part[cell] >= 0) continue;
+      } else {
+        while (part[seed] >= 0) ++seed;
+        cell = seed;
+      }
+      part[cell] = q;
+      ++got;
+      for (long long t = deg[cell]; t < deg[cell + 1]; ++t)
+        if (part[adj[t]] < 0) heap.push(Item(-aw[t], adj[t]));
+    }
+  }
+  return B2S_OK;
+}
