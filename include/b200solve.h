@@ -215,6 +215,25 @@ int b2s_tiles_trace(void* handle, unsigned long long* buf, int dbg);
 int b2s_tiles_apply(int b, const void* handle, const double* r, double* y, double* z,
                     int reset_y, cudaStream_t stream);
 
+/* ---- wavefront sweeps for natural-order 7-point grids (csrc/gridwave.cu) --
+ * Deep plans (level schedules, the sequential plan) of an nx*ny*nz grid: one
+ * warp per tile of wx*wy <= 32 columns walks the levels, in-tile
+ * dependencies through warp shuffles, tile edges through sentinel-checked
+ * edge buffers.  create packs the plan-order factor (rp/ci/lu combined L\U,
+ * inv = inverse diagonals; perm old->plan, iperm plan->old) and verifies
+ * every row is a stencil row of the plan; B2S_UNSUPPORTED otherwise (keep the
+ * sync-free sweeps).  apply: z = U^-1 L^-1 r in plan order, bit-identical to
+ * b2s_ilu0_apply.  Replaces Ilu0Factorization.apply (bs/ilu0.py:105-142). */
+int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const int32_t* perm,
+                  const int32_t* iperm, const int32_t* rp, const int32_t* ci, const double* lu,
+                  const double* inv, void** handle_out, cudaStream_t stream);
+int b2s_gw_destroy(void* handle);
+int b2s_gw_apply(int b, const void* handle, const double* r, double* z, cudaStream_t stream);
+/* debug (B2S_GW_TRACE set at create): the last apply's per-step end times,
+ * [2][T][S] ns; shape = {TX, TY, S, wx, wy} */
+int b2s_gw_trace(const void* handle, unsigned long long* host, long long cap, long long* count,
+                 int* shape);
+
 /* ---- reductions (bs/krylov.py:30-60) ------------------------------------ */
 
 int b2s_dot(long long m, const double* a, const double* b, int nparts, double* parts,
@@ -383,6 +402,9 @@ typedef struct {
   const int32_t* well_lane;
   double* well_corr;
   double* well_scratch;
+  /* optional b2s_gw_create() handle: the preconditioner applications use the
+   * wavefront sweeps of a natural-order grid (takes precedence over tiles) */
+  const void* gw;
 } b2s_bicg_args;
 
 typedef struct {

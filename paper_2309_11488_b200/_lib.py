@@ -38,7 +38,7 @@ class BicgArgs(C.Structure):
                 ("stream", _P), ("ngroups", _I), ("goff1", _I), ("gslice_host", _P),
                 ("fuse", _I), ("mesh", _P), ("x0_zero", _I),
                 ("wells", _P), ("well_slice", _P), ("well_lane", _P), ("well_corr", _P),
-                ("well_scratch", _P)]
+                ("well_scratch", _P), ("gw", _P)]
 
 
 class Mesh(C.Structure):
@@ -96,6 +96,11 @@ SIGNATURES = {
     "b2s_fill_sentinel": (_I, [_LL, _P, _P]),
     "b2s_dot_chunked": (_I, [_LL, _P, _P, _P, _P, _P]),
     "b2s_partition_greedy": (_I, [_LL, _LL, _P, _P, _P, _LL, _P]),
+    "b2s_gw_create": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
+                           C.POINTER(C.c_void_p), _P]),
+    "b2s_gw_destroy": (_I, [_P]),
+    "b2s_gw_apply": (_I, [_I, _P, _P, _P, _P]),
+    "b2s_gw_trace": (_I, [_P, _P, _LL, C.POINTER(C.c_longlong), _P]),
     "b2s_wells_apply": (_I, [_P, _P, _P, _P, _P]),
     "b2s_fuse_check": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _PI, _P]),
     "b2s_ilu0_apply_phased": (_I, [_I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P,

@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libb200solve.so"
 SOURCES = ["analysis.cu", "spmv.cu", "factor.cu", "ilu0.cu", "fused.cu", "factor2c.cu", "tiles.cu", "krylov.cu",
-           "jacobi.cu", "wells.cu", "refdot.cu"]
+           "jacobi.cu", "wells.cu", "refdot.cu", "gridwave.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -62,6 +62,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
     hdr = _headers()
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    compile_flags += os.environ.get("B2S_EXTRA_NVCC", "").split()   # e.g. -DB2S_GW_TRACE_BUILD
     procs = []
     for src in SOURCES:
         obj = OBJ / (Path(src).stem + ".o")

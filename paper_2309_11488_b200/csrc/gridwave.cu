@@ -1,0 +1,609 @@
+// Wavefront ILU0 sweeps for natural-order 7-point grids (the level-scheduled
+// apply, bs/ilu0.py:105-142 `_sweeps`, on the reference's default backend).
+//
+// Why: a level schedule of an nx x ny x nz stencil has nx+ny+nz-2 levels;
+// the sync-free sweeps (ilu0.cu) pay one cross-SM L2 round trip per level
+// (~1 us), the tile step kernels (tiles.cu) ~0.6 us of in-SM overhead per
+// step.  Here the (x, y) plane is cut into tiles of at most 32 columns, ONE
+// WARP per tile, one lane per column (all z).  The warp walks the levels
+// l = x+y+z of its tile in order; at step l lane (x, y) owns row
+// (x, y, z = l-x-y), and its three lower neighbours were produced at step
+// l-1 by: itself (z-1, a register), lane-1 (x-1) and lane-wx (y-1) --
+// warp shuffles, no shared memory, no barrier.  Only the tile's west and
+// south edge lanes read a neighbour tile's value: from that tile's edge
+// buffer, with the sentinel protocol of the sync-free sweeps (values are
+// self-validating, no fences).  The critical path is levels x (in-warp step)
+// + tile crossings x (one L2 hop), with the step a few dependent FMAs.
+//
+// Data: the factor is repacked once per factorisation into the warp's step
+// order, [tile][step][entry][e][lane] (coalesced 256-byte warp loads), with
+// a per-slot meta word (plan row | entry mask).  Per row the arithmetic is
+// exactly the sync-free sweeps' -- strict-lower entries in ascending plan
+// column order (z-1, y-1, x-1), acc then subtract, canon; backward (x+1,
+// y+1, z+1), then inv(U_ii) -- so results are bit-identical.  A plan
+// qualifies when every row's lower entries are its minus-neighbours and its
+// upper entries its plus-neighbours (level schedules and the sequential plan
+// of such grids); the packing kernel verifies this row by row.
+#include <cstdlib>
+
+#include "sell.cuh"
+
+namespace b2s {
+
+constexpr int kGwLanes = 32;
+
+struct GwDev {
+  int nx, ny, nz, wx, wy, TX, TY, S;   // grid, tile shape, tiles, steps per tile (max)
+  int rf, rb;            // bytes of one forward / backward step record
+  const char* recf;      // [T*S] forward records:  meta[32] int32 | L[3][BB][32] f64
+  const char* recb;      // [T*S] backward records: meta[32] int32 | U[3][BB][32] | D[BB][32]
+  double* rpk;           // [T*S][B][32]  the sweep's input in step order (k_gw_gather)
+  double* ypk;           // [T*S][B][32]  forward results, step order
+  double* zpk;           // [T*S][B][32]  backward results, step order (k_gw_scatter)
+  double* eE;            // [T*S][wy][B]      forward: east-edge lanes' results
+  double* eN;            // [T*S][wx][B]      forward: north-edge lanes' results
+  double* eW;            // [T*S][wy][B]      backward: west-edge lanes' results
+  double* eS;            // [T*S][wx][B]      backward: south-edge lanes' results
+  unsigned long long* trace;   // debug (B2S_GW_TRACE): [2][T][S] step end times, or null
+};
+
+// meta word: -1 inactive, else plan row (bits 0..24) | entry mask << 25
+enum GwMask { kZm = 1, kYm = 2, kXm = 4, kXp = 8, kYp = 16, kZp = 32 };
+constexpr int kGwMetaBytes = 128;
+constexpr int kGwRingF = 8;   // forward ring stages (step records in flight)
+constexpr int kGwRingB = 6;   // backward ring stages
+constexpr int kGwEdgeAhead = 1;   // steps of look-ahead for the neighbour tiles' edge values
+
+__device__ __forceinline__ double gw_ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void gw_st_relaxed(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns_gw() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned gw_smem(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void gw_mbar_init(unsigned long long* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gw_smem(b)) : "memory");
+}
+__device__ __forceinline__ void gw_mbar_expect(unsigned long long* b, unsigned tx) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(
+                   gw_smem(b)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void gw_mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(gw_smem(b)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void gw_bulk(void* dst, const void* src, unsigned bytes,
+                                        unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          gw_smem(dst)), "l"(src), "r"(bytes), "r"(gw_smem(b))
+      : "memory");
+}
+__device__ __forceinline__ void gw_fence_proxy() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int B>
+__device__ __forceinline__ bool gw_ready(const double (&v)[B]) {
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < B; ++c) ok &= !is_sentinel(v[c]);
+  return ok;
+}
+template <int B>
+__device__ __forceinline__ void gw_load(const double* p, double (&v)[B]) {
+#pragma unroll
+  for (int c = 0; c < B; ++c) v[c] = gw_ld_relaxed(p + c);
+}
+template <int B>
+__device__ __forceinline__ void gw_poll(const double* p, double (&v)[B]) {
+  while (!gw_ready<B>(v)) gw_load<B>(p, v);
+}
+
+struct GwTile {
+  int t, tx, ty, x0, y0, xw, yw, xl, yl, L0, St;
+  bool valid;
+};
+
+__device__ __forceinline__ GwTile gw_tile(const GwDev& g, int t, int lane) {
+  GwTile a;
+  a.t = t;
+  a.tx = t % g.TX;
+  a.ty = t / g.TX;
+  a.x0 = a.tx * g.wx;
+  a.y0 = a.ty * g.wy;
+  a.xw = min(g.wx, g.nx - a.x0);
+  a.yw = min(g.wy, g.ny - a.y0);
+  a.xl = lane % g.wx;
+  a.yl = lane / g.wx;
+  a.valid = lane < g.wx * g.wy && a.xl < a.xw && a.yl < a.yw;
+  a.L0 = a.x0 + a.y0;
+  a.St = (a.xw - 1) + (a.yw - 1) + g.nz;
+  return a;
+}
+
+__device__ __forceinline__ void gw_mbar_init_n(unsigned long long* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(gw_smem(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void gw_mbar_arrive(unsigned long long* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(gw_smem(b))
+               : "memory");
+}
+
+// One warp per tile.  The tile's step records and input slices stream into a
+// shared-memory ring with TMA bulk copies (an mbarrier per stage counts the
+// bytes; lane 0 refills a stage right after the warp consumed it).  Per step:
+// a stage wait, shared-memory reads, two shuffles per component, three 3x3
+// products and the stores; the neighbour tiles' edge values needed at the
+// next step are requested one step early (the neighbour runs about one L2 hop
+// ahead, so an earlier request would find them not yet produced; measured:
+// 4 steps early 1457 us per C4 application, 1 step 792 us).  A separate
+// producer warp measured slower (1636 us).
+//
+// forward: y = r - L y, levels upward; backward: z = inv(U_ii) (y - U z),
+// levels downward.  DIR 0 / 1.
+template <int B, int DIR>
+__global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
+  constexpr int BB = B * B;
+  constexpr int R = DIR == 0 ? kGwRingF : kGwRingB;
+  constexpr int VB = B * 32 * 8;   // bytes of one step's vector slice
+  extern __shared__ __align__(128) char smem[];
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const GwTile a = gw_tile(g, blockIdx.x, lane);
+  const long long base = (long long)a.t * g.S;
+  const int rb = DIR == 0 ? g.rf : g.rb;
+  const int stage = rb + VB;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
+  char* ring = smem + 128;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < R; ++q) gw_mbar_init_n(full + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // step j of this sweep (j = 0, 1, ...) is tile step s = j (forward) or St-1-j;
+  // lane 0 keeps the ring R steps ahead (refilling a stage right after the
+  // warp consumed it)
+  const char* rec = DIR == 0 ? g.recf : g.recb;
+  const char* vin = reinterpret_cast<const char*>(DIR == 0 ? g.rpk : g.ypk);
+  auto issue = [&](int j) {
+    const int q = j % R;
+    const long long s = DIR == 0 ? j : a.St - 1 - j;
+    char* dst = ring + q * stage;
+    gw_mbar_expect(full + q, (unsigned)stage);
+    gw_bulk(dst, rec + (base + s) * (long long)rb, (unsigned)rb, full + q);
+    gw_bulk(dst + rb, vin + (base + s) * VB, (unsigned)VB, full + q);
+  };
+  if (lane == 0)
+    for (int j = 0; j < R && j < a.St; ++j) issue(j);
+  {  // the other direction's edge buffers of this tile go back to "not produced"
+    double* o1 = DIR == 0 ? g.eW : g.eE;
+    double* o2 = DIR == 0 ? g.eS : g.eN;
+    for (long long q = lane; q < (long long)g.S * g.wy * B; q += 32) o1[base * g.wy * B + q] = sentinel();
+    for (long long q = lane; q < (long long)g.S * g.wx * B; q += 32) o2[base * g.wx * B + q] = sentinel();
+  }
+  const bool hasW = a.tx > 0, hasS = a.ty > 0;
+  const bool hasE = a.tx + 1 < g.TX, hasN = a.ty + 1 < g.TY;
+  // this lane's neighbour-tile inputs (x side / y side) and its own edge outputs
+  const bool xe = DIR == 0 ? (a.xl == 0 && hasW) : (a.xl == a.xw - 1 && hasE);
+  const bool ye = DIR == 0 ? (a.yl == 0 && hasS) : (a.yl == a.yw - 1 && hasN);
+  const bool px = DIR == 0 ? (a.xl == a.xw - 1 && hasE) : (a.xl == 0 && hasW);
+  const bool py = DIR == 0 ? (a.yl == a.yw - 1 && hasN) : (a.yl == 0 && hasS);
+  // per-step pointers (stride B doubles per step along the tile's steps)
+  const int dstep = DIR == 0 ? 1 : -1;
+  const int s0 = DIR == 0 ? 0 : a.St - 1;
+  const double* xin = (DIR == 0 ? g.eE : g.eW) +
+                      (((DIR == 0 ? base - g.S : base + g.S) + s0 + (DIR == 0 ? g.wx - 1 : 1 - g.wx)) *
+                       g.wy + a.yl) * B;
+  const double* yin = (DIR == 0 ? g.eN : g.eS) +
+                      (((DIR == 0 ? base - (long long)g.TX * g.S : base + (long long)g.TX * g.S) + s0 +
+                        (DIR == 0 ? g.wy - 1 : 1 - g.wy)) * g.wx + a.xl) * B;
+  const long long xstride = (long long)dstep * g.wy * B, ystride = (long long)dstep * g.wx * B;
+  double* xout = (DIR == 0 ? g.eE : g.eW) + ((base + s0) * g.wy + a.yl) * B;
+  double* yout = (DIR == 0 ? g.eN : g.eS) + ((base + s0) * g.wx + a.xl) * B;
+  double* vout = (DIR == 0 ? g.ypk : g.zpk) + (base + s0) * B * 32 + lane;
+  const long long vstride = (long long)dstep * B * 32;
+  // neighbour-tile step of the value needed at our step s: in range?
+  const int xoff = DIR == 0 ? g.wx - 1 : 1 - g.wx, yoff = DIR == 0 ? g.wy - 1 : 1 - g.wy;
+  auto xok = [&](int s) { const int t = s + xoff; return xe && t >= 0 && t < g.S; };
+  auto yok = [&](int s) { const int t = s + yoff; return ye && t >= 0 && t < g.S; };
+  double ex[B], ey[B];
+#pragma unroll
+  for (int c = 0; c < B; ++c) ex[c] = ey[c] = sentinel();
+  if (a.St > 0) {
+    if (xok(s0)) gw_load<B>(xin, ex);
+    if (yok(s0)) gw_load<B>(yin, ey);
+  }
+  const int sx = DIR == 0 ? (lane > 0 ? lane - 1 : 0) : (lane + 1 < 32 ? lane + 1 : 31);
+  const int sy = DIR == 0 ? (lane >= g.wx ? lane - g.wx : 0) : (lane + g.wx < 32 ? lane + g.wx : 31);
+  constexpr int mx = DIR == 0 ? kXm : kXp, my = DIR == 0 ? kYm : kYp, mz = DIR == 0 ? kZm : kZp;
+  double prev[B];
+#pragma unroll
+  for (int c = 0; c < B; ++c) prev[c] = 0.0;
+  const unsigned ring_s = gw_smem(ring);
+  for (int j = 0; j < a.St; ++j) {
+    const int s = s0 + dstep * j;
+    const int q = j % R;
+    gw_mbar_wait(full + q, (unsigned)((j / R) & 1));
+    const char* st_ = ring + q * stage;
+    const int mt = reinterpret_cast<const int*>(st_)[lane];
+    const double* blk = reinterpret_cast<const double*>(st_ + kGwMetaBytes) + lane;
+    const double* vv = reinterpret_cast<const double*>(st_ + rb) + lane;
+    const int mask = mt >= 0 ? (mt >> 25) : 0;
+    double nx_[B], ny_[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      nx_[c] = __shfl_sync(0xffffffffu, prev[c], sx);
+      ny_[c] = __shfl_sync(0xffffffffu, prev[c], sy);
+    }
+    if (xe && (mask & mx)) {
+      gw_poll<B>(xin, ex);
+#pragma unroll
+      for (int c = 0; c < B; ++c) nx_[c] = ex[c];
+    }
+    if (ye && (mask & my)) {
+      gw_poll<B>(yin, ey);
+#pragma unroll
+      for (int c = 0; c < B; ++c) ny_[c] = ey[c];
+    }
+    // the next step's edge inputs, one step early
+    xin += xstride;
+    yin += ystride;
+    if (j + 1 < a.St) {
+      if (xok(s + dstep)) gw_load<B>(xin, ex);
+      if (yok(s + dstep)) gw_load<B>(yin, ey);
+    }
+    double acc[B], pr[B], m[BB];
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] = 0.0;
+    // ascending plan columns: forward z-1, y-1, x-1; backward x+1, y+1, z+1
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int bit = DIR == 0 ? (k == 0 ? mz : (k == 1 ? my : mx)) : (k == 0 ? mx : (k == 1 ? my : mz));
+      if (mask & bit) {
+#pragma unroll
+        for (int e = 0; e < BB; ++e) m[e] = blk[(k * BB + e) * 32];
+        const double* dep = k == 0 ? (DIR == 0 ? prev : nx_) : (k == 1 ? ny_ : (DIR == 0 ? nx_ : prev));
+        matvec<B>(m, dep, pr);
+#pragma unroll
+        for (int c = 0; c < B; ++c) acc[c] += pr[c];
+      }
+    }
+    double outv[B];
+    if (DIR == 0) {
+#pragma unroll
+      for (int c = 0; c < B; ++c) outv[c] = canon(vv[c * 32] - acc[c]);
+    } else {
+      double tv[B], o[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) tv[c] = vv[c * 32] - acc[c];
+#pragma unroll
+      for (int e = 0; e < BB; ++e) m[e] = blk[(3 * BB + e) * 32];
+      matvec<B>(m, tv, o);
+#pragma unroll
+      for (int c = 0; c < B; ++c) outv[c] = canon(o[c]);
+    }
+    if (mt >= 0) {
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        prev[c] = outv[c];
+        vout[c * 32] = outv[c];
+      }
+      if (px) {
+#pragma unroll
+        for (int c = 0; c < B; ++c) gw_st_relaxed(xout + c, outv[c]);
+      }
+      if (py) {
+#pragma unroll
+        for (int c = 0; c < B; ++c) gw_st_relaxed(yout + c, outv[c]);
+      }
+    }
+    vout += vstride;
+    xout += xstride;
+    yout += ystride;
+#ifdef B2S_GW_TRACE_BUILD
+    if (g.trace && lane == 0)
+      g.trace[(long long)DIR * g.TX * g.TY * g.S + base + s] = global_ns_gw();
+#endif
+    // the stage is consumed: refill it with step j + R
+    __syncwarp();
+    if (lane == 0 && j + R < a.St) {
+      gw_fence_proxy();
+      issue(j + R);
+    }
+  }
+  (void)ring_s;
+}
+
+// the sweep's input in step order / its output back to plan order
+template <int B>
+__global__ void k_gw_gather(GwDev g, const double* __restrict__ r) {
+  const long long total = (long long)g.TX * g.TY * g.S * 32;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long slot = q >> 5;
+    const int lane = (int)(q & 31);
+    const int mt = reinterpret_cast<const int*>(g.recf + slot * g.rf)[lane];
+    const long long pr = mt & 0x1FFFFFF;
+#pragma unroll
+    for (int c = 0; c < B; ++c) g.rpk[(slot * B + c) * 32 + lane] = mt >= 0 ? r[pr * B + c] : 0.0;
+  }
+}
+
+template <int B>
+__global__ void k_gw_scatter(GwDev g, double* __restrict__ z) {
+  const long long total = (long long)g.TX * g.TY * g.S * 32;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long slot = q >> 5;
+    const int lane = (int)(q & 31);
+    const int mt = reinterpret_cast<const int*>(g.recf + slot * g.rf)[lane];
+    if (mt < 0) continue;
+    const long long pr = mt & 0x1FFFFFF;
+#pragma unroll
+    for (int c = 0; c < B; ++c) z[pr * B + c] = g.zpk[(slot * B + c) * 32 + lane];
+  }
+}
+
+// ---- packing (once per factorisation): one thread per (tile, step, lane)
+__global__ void k_gw_pack(GwDev g, int b, int n, const int32_t* __restrict__ perm,
+                          const int32_t* __restrict__ iperm, const int32_t* __restrict__ rp,
+                          const int32_t* __restrict__ ci, const double* __restrict__ lu,
+                          const double* __restrict__ inv, char* recf, char* recb, int* bad) {
+  const int bb = b * b;
+  const long long T = (long long)g.TX * g.TY;
+  const long long total = T * g.S * 32;
+  const long long nxy = (long long)g.nx * g.ny;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(q % 32);
+    const long long slot = q / 32;
+    const int s = (int)(slot % g.S);
+    const int t = (int)(slot / g.S);
+    const GwTile a = gw_tile(g, t, lane);
+    const int x = a.x0 + a.xl, y = a.y0 + a.yl, z = a.L0 + s - x - y;
+    int* mf = reinterpret_cast<int*>(recf + slot * g.rf);
+    int* mb = reinterpret_cast<int*>(recb + slot * g.rb);
+    double* Lv = reinterpret_cast<double*>(recf + slot * g.rf + kGwMetaBytes);
+    double* Uv = reinterpret_cast<double*>(recb + slot * g.rb + kGwMetaBytes);
+    for (int k = 0; k < 3; ++k)
+      for (int e = 0; e < bb; ++e) {
+        Lv[(k * bb + e) * 32 + lane] = 0.0;
+        Uv[(k * bb + e) * 32 + lane] = 0.0;
+      }
+    for (int e = 0; e < bb; ++e) Uv[(3 * bb + e) * 32 + lane] = 0.0;
+    if (!a.valid || s >= a.St || z < 0 || z >= g.nz) {
+      mf[lane] = mb[lane] = -1;
+      continue;
+    }
+    const long long i = x + (long long)g.nx * y + nxy * z;   // natural (input) row
+    const int pr = perm[i];
+    int mask = 0;
+    for (int p = rp[pr]; p < rp[pr + 1]; ++p) {
+      const int c = ci[p];
+      const long long d = (long long)iperm[c] - i;
+      int kind = -1;
+      if (d == 0) continue;
+      if (d == -nxy && z > 0) kind = 0;
+      else if (d == -g.nx && y > 0) kind = 1;
+      else if (d == -1 && x > 0) kind = 2;
+      else if (d == 1 && x + 1 < g.nx) kind = 3;
+      else if (d == g.nx && y + 1 < g.ny) kind = 4;
+      else if (d == nxy && z + 1 < g.nz) kind = 5;
+      // lower entries must be the minus-neighbours and precede the row in the plan
+      if (kind < 0 || (kind < 3) != (c < pr) || (mask & (1 << kind))) { atomicExch(bad, 1); continue; }
+      mask |= 1 << kind;
+      // record order = ascending plan columns: forward z-1, y-1, x-1 (kinds 0,1,2);
+      // backward x+1, y+1, z+1 (kinds 3,4,5)
+      double* dst = kind < 3 ? Lv : Uv;
+      const int kk = kind < 3 ? kind : kind - 3;
+      for (int e = 0; e < bb; ++e) dst[(kk * bb + e) * 32 + lane] = lu[(long long)p * bb + e];
+    }
+    for (int e = 0; e < bb; ++e) Uv[(3 * bb + e) * 32 + lane] = inv[(long long)pr * bb + e];
+    mf[lane] = mb[lane] = pr | (mask << 25);
+  }
+}
+
+__global__ void k_gw_fill(long long m, double* v) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m;
+       t += (long long)gridDim.x * blockDim.x)
+    v[t] = sentinel();
+}
+
+struct GwHandle {
+  GwDev g;
+  int b, n;
+  void* mem;   // one allocation for everything
+};
+
+inline int gw_smem_bytes(const GwDev& g, int b, int dir) {
+  return 128 + (dir == 0 ? kGwRingF : kGwRingB) * ((dir == 0 ? g.rf : g.rb) + b * 32 * 8);
+}
+static_assert(2 * 8 * (kGwRingF > kGwRingB ? kGwRingF : kGwRingB) <= 128, "mbarriers fit");
+
+template <int B>
+int launch_gw_b(const GwHandle* h, const double* r, double* z, const int* done, cudaStream_t st) {
+  const GwDev& g = h->g;
+  const long long total = (long long)g.TX * g.TY * g.S * 32;
+  long long grid = (total + 255) / 256;
+  if (grid > kSms * 16) grid = kSms * 16;
+  k_gw_gather<B><<<(int)grid, 256, 0, st>>>(g, r);
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeCooperative;   // tiles wait on each other: all resident
+  attr.val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.TX * g.TY);
+  cfg.blockDim = dim3(32);
+  cfg.stream = st;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  cfg.dynamicSmemBytes = gw_smem_bytes(g, B, 0);
+  if (cudaLaunchKernelEx(&cfg, k_gw_sweep<B, 0>, g, done) != cudaSuccess) return B2S_CUDA_ERROR;
+  cfg.dynamicSmemBytes = gw_smem_bytes(g, B, 1);
+  if (cudaLaunchKernelEx(&cfg, k_gw_sweep<B, 1>, g, done) != cudaSuccess) return B2S_CUDA_ERROR;
+  k_gw_scatter<B><<<(int)grid, 256, 0, st>>>(g, z);
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
+// z = U^-1 L^-1 r (plan order) with the wavefront kernels
+int launch_gw(int b, const void* handle, const double* r, double* z, const int* done,
+              cudaStream_t st) {
+  const GwHandle* h = reinterpret_cast<const GwHandle*>(handle);
+  switch (b) {
+    case 1: return launch_gw_b<1>(h, r, z, done, st);
+    case 2: return launch_gw_b<2>(h, r, z, done, st);
+    case 3: return launch_gw_b<3>(h, r, z, done, st);
+    case 4: return launch_gw_b<4>(h, r, z, done, st);
+    default: return B2S_UNSUPPORTED;
+  }
+}
+
+template <int B>
+int gw_configure(const GwDev& g, int* per_sm) {
+  const int s0 = gw_smem_bytes(g, B, 0), s1 = gw_smem_bytes(g, B, 1);
+  if (cudaFuncSetAttribute((const void*)k_gw_sweep<B, 0>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, s0) != cudaSuccess ||
+      cudaFuncSetAttribute((const void*)k_gw_sweep<B, 1>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, s1) != cudaSuccess)
+    return B2S_CUDA_ERROR;
+  int a = 0, c = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_gw_sweep<B, 0>, 32, s0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_gw_sweep<B, 1>, 32, s1);
+  *per_sm = a < c ? a : c;
+  return B2S_OK;
+}
+
+}  // namespace b2s
+
+using namespace b2s;
+
+extern "C" {
+
+// Pack the factor of a natural-order nx*ny*nz 7-point grid for the wavefront
+// sweeps.  perm/iperm: the plan (old row -> plan row / plan row -> old row);
+// rp/ci/lu: the combined L\U in plan order (int32 pattern, b*b blocks), inv:
+// the inverse diagonal blocks in plan order.  B2S_UNSUPPORTED when the grid
+// does not fit (more tiles than can be co-resident) or some row is not a
+// stencil row of that plan -- the caller keeps the sync-free sweeps.
+int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const int32_t* perm,
+                  const int32_t* iperm, const int32_t* rp, const int32_t* ci, const double* lu,
+                  const double* inv, void** handle_out, cudaStream_t st) {
+  *handle_out = nullptr;
+  if (b < 1 || b > 4 || nx < 1 || ny < 1 || nz < 1 || (long long)nx * ny * nz != n ||
+      wx < 1 || wy < 1 || wx * wy > kGwLanes || n >= (1 << 25))
+    return B2S_SHAPE;
+  GwHandle* h = new GwHandle();
+  GwDev& g = h->g;
+  g.nx = nx; g.ny = ny; g.nz = nz; g.wx = wx; g.wy = wy;
+  g.TX = (nx + wx - 1) / wx;
+  g.TY = (ny + wy - 1) / wy;
+  g.S = (wx - 1) + (wy - 1) + nz;
+  const int bb = b * b;
+  g.rf = kGwMetaBytes + 3 * bb * 32 * 8;
+  g.rb = kGwMetaBytes + 4 * bb * 32 * 8;
+  const long long T = (long long)g.TX * g.TY;
+  // every tile waits on its neighbours: all CTAs must be co-resident
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int rc = B2S_OK;
+  switch (b) {
+    case 1: rc = gw_configure<1>(g, &per_sm); break;
+    case 2: rc = gw_configure<2>(g, &per_sm); break;
+    case 3: rc = gw_configure<3>(g, &per_sm); break;
+    default: rc = gw_configure<4>(g, &per_sm); break;
+  }
+  if (rc != B2S_OK) { delete h; return rc; }
+  if (T > (long long)per_sm * sms) { delete h; return B2S_UNSUPPORTED; }
+  const long long slots = T * g.S;
+  const long long nV = slots * b * 32;
+  const long long nEx = slots * wy * b, nEy = slots * wx * b;
+  const long long bytes = slots * ((long long)g.rf + g.rb) + (3 * nV + 2 * nEx + 2 * nEy) * 8 + 256;
+  if (cudaMalloc(&h->mem, bytes) != cudaSuccess) { delete h; return B2S_CUDA_ERROR; }
+  char* p = reinterpret_cast<char*>(h->mem);
+  char* recf = p; p += slots * g.rf;
+  char* recb = p; p += slots * g.rb;
+  double* d = reinterpret_cast<double*>(p);
+  g.rpk = d; d += nV;
+  g.ypk = d; d += nV;
+  g.zpk = d; d += nV;
+  g.eE = d; d += nEx;
+  g.eW = d; d += nEx;
+  g.eN = d; d += nEy;
+  g.eS = d; d += nEy;
+  g.recf = recf; g.recb = recb;
+  g.trace = nullptr;
+  if (getenv("B2S_GW_TRACE") && cudaMalloc(&g.trace, 2 * slots * 8) != cudaSuccess) g.trace = nullptr;
+  h->b = b;
+  h->n = n;
+  int* bad = nullptr;
+  int hbad = 0;
+  bool ok = cudaMallocAsync(&bad, sizeof(int), st) == cudaSuccess &&
+            cudaMemsetAsync(bad, 0, sizeof(int), st) == cudaSuccess;
+  if (ok) {
+    long long thr = slots * 32;
+    long long grid = (thr + 255) / 256;
+    if (grid > kSms * 64) grid = kSms * 64;
+    k_gw_pack<<<(int)grid, 256, 0, st>>>(g, b, n, perm, iperm, rp, ci, lu, inv, recf, recb, bad);
+    // all four edge buffers start "not produced" (each sweep then re-arms the
+    // other direction's buffers of its own tile)
+    const long long ne = 2 * nEx + 2 * nEy;
+    long long eg = (ne + 255) / 256;
+    if (eg > kSms * 16) eg = kSms * 16;
+    k_gw_fill<<<(int)(eg < 1 ? 1 : eg), 256, 0, st>>>(ne, g.eE);
+    ok = cudaGetLastError() == cudaSuccess &&
+         cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+         cudaFreeAsync(bad, st) == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess;
+  }
+  if (!ok || hbad) {
+    cudaFree(h->mem);
+    if (g.trace) cudaFree(g.trace);
+    delete h;
+    return ok ? B2S_UNSUPPORTED : B2S_CUDA_ERROR;
+  }
+  *handle_out = h;
+  return B2S_OK;
+}
+
+// debug: copy the step end times [2][T][S] (ns, globaltimer) of the last
+// apply into host memory (B2S_GW_TRACE set at create); *count = 2*T*S
+int b2s_gw_trace(const void* handle, unsigned long long* host, long long cap, long long* count,
+                 int* shape) {
+  const GwHandle* h = reinterpret_cast<const GwHandle*>(handle);
+  const long long n = 2ll * h->g.TX * h->g.TY * h->g.S;
+  *count = n;
+  shape[0] = h->g.TX; shape[1] = h->g.TY; shape[2] = h->g.S; shape[3] = h->g.wx; shape[4] = h->g.wy;
+  if (!h->g.trace || cap < n) return B2S_SHAPE;
+  B2S_CHECK(cudaMemcpy(host, h->g.trace, n * 8, cudaMemcpyDeviceToHost));
+  return B2S_OK;
+}
+
+int b2s_gw_destroy(void* handle) {
+  GwHandle* h = reinterpret_cast<GwHandle*>(handle);
+  if (!h) return B2S_OK;
+  if (h->g.trace) cudaFree(h->g.trace);
+  cudaFree(h->mem);
+  delete h;
+  return B2S_OK;
+}
+
+int b2s_gw_apply(int b, const void* handle, const double* r, double* z, cudaStream_t st) {
+  if (!handle) return B2S_SHAPE;
+  if (reinterpret_cast<const GwHandle*>(handle)->b != b) return B2S_SHAPE;
+  return launch_gw(b, handle, r, z, nullptr, st);
+}
+
+}  // extern "C"

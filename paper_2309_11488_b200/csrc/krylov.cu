@@ -58,6 +58,8 @@ int launch_fwd_pre(int b, int nparts, SliceMap map, int s0, int s1, Sell lo, con
                    const PreIn* pre_in);
 int launch_tiled(int b, const void* handle, const double* r, double* y, double* z, int reset_y,
                  const int* done, cudaStream_t st);
+int launch_gw(int b, const void* handle, const double* r, double* z, const int* done,
+              cudaStream_t st);
 
 // deterministic sum of np partials by one CTA of 256 threads
 __device__ double reduce_parts(const double* parts, int np, double* red) {
@@ -548,7 +550,8 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // B2S_FUSE_VEC=1/0 forces it
   const char* fv_env = getenv("B2S_FUSE_VEC");
   const bool vecf = fused && (fv_env ? fv_env[0] == '1' : a->n <= 400000);
-  const int reset = (ilu && !phased) ? 1 : 0;  // sync-free sweeps need sentinel-filled outputs
+  // sync-free sweeps need sentinel-filled outputs (not the wavefront sweeps)
+  const int reset = (ilu && !phased && !a->gw) ? 1 : 0;
   MeshDev md{};
   MeshHalo mh{};
   if (mesh && !ilu) return B2S_UNSUPPORTED;   // sharded solves are block-Jacobi ILU0
@@ -636,7 +639,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       k_ctl_init<<<1, 256, 0, user>>>(state, prr, np_res, a->tol, a->maxit, dev_done, md);
       k_copy<<<grid_v, 256, 0, user>>>(m, r, rhat);
       k_copy<<<grid_v, 256, 0, user>>>(m, r, v);  // v is only read for k > 0
-      if (ilu && !phased) {
+      if (ilu && !phased && !a->gw) {
         rc = fill_sentinel(m, y, user);
         if (!rc) rc = fill_sentinel(m, phat, user);
         if (!rc) rc = fill_sentinel(m, shat, user);
@@ -780,8 +783,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                       p, y, phat, done, cs, false, pdl);
         kernels += 2 * (a->ngroups - 1);
       } else if (ilu) {
-        if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
-        if (a->tiles) launch_tiled(a->b, a->tiles, p, y, phat, reset_y, done, cs);
+        if (a->refill_y && !a->gw) { fill_sentinel(m, y, cs); ++kernels; }
+        if (a->gw) launch_gw(a->b, a->gw, p, phat, done, cs);
+        else if (a->tiles) launch_tiled(a->b, a->tiles, p, y, phat, reset_y, done, cs);
         else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, reset_y, a->sweep_flags,
                            tickets, done, cs);
         kernels += 2;
@@ -819,8 +823,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                       s, y, shat, done, cs, false, pdl);
         kernels += 2 * (a->ngroups - 1);
       } else if (ilu) {
-        if (a->refill_y) { fill_sentinel(m, y, cs); ++kernels; }
-        if (a->tiles) launch_tiled(a->b, a->tiles, s, y, shat, reset_y, done, cs);
+        if (a->refill_y && !a->gw) { fill_sentinel(m, y, cs); ++kernels; }
+        if (a->gw) launch_gw(a->b, a->gw, s, shat, done, cs);
+        else if (a->tiles) launch_tiled(a->b, a->tiles, s, y, shat, reset_y, done, cs);
         else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, reset_y, a->sweep_flags,
                            tickets, done, cs);
         kernels += 2;

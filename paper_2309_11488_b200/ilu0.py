@@ -69,6 +69,7 @@ class Ilu0Factorization:
         # application 626 us vs 685 us with 8 warps, a warps-per-CTA scan, round 1)
         self.sweep_flags = 0x4 if plan.group_count <= 16 else 0x410
         self.tiles = None        # b2s_tiles_create handle (tiled level sweeps), or None
+        self.gw = None           # b2s_gw_create handle (wavefront sweeps of grids), or None
         # few independent groups (colourings) and no same-group entries: the
         # phased sweeps, 2(G-1) plain passes, no polling (bit-identical)
         ustale = False if two_colour else upper.stale
@@ -151,6 +152,10 @@ class Ilu0Factorization:
                 D.ptr(up.vals), D.ptr(self.dtiles), D.ptr(r_perm), D.ptr(y), D.ptr(z),
                 D.stream()), "ilu0_apply_phased")
             return z
+        if self.gw:
+            check(D.lib().b2s_gw_apply(self._b, self.gw, D.ptr(r_perm), D.ptr(z), D.stream()),
+                  "gw_apply")
+            return z
         D.fill_sentinel(y, m)
         D.fill_sentinel(z, m)
         if self.tiles:
@@ -199,6 +204,12 @@ class Ilu0Factorization:
         return self.apply_array(r)
 
     def __del__(self):
+        if getattr(self, "gw", None):
+            try:
+                D.lib().b2s_gw_destroy(self.gw)
+            except Exception:
+                pass
+            self.gw = None
         if getattr(self, "tiles", None):
             try:
                 D.lib().b2s_tiles_destroy(self.tiles)
@@ -318,6 +329,7 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
     f = Ilu0Factorization(plan, b, n, lu, inv, smap, lower, upper, dtiles, identity, a, a_perm)
     f._a_src = a_src
     _maybe_tiles(f, plan, diag)
+    _maybe_gw(f, plan)
     return f
 
 
@@ -352,6 +364,46 @@ def _patches(nx: int, ny: int, tiles: int):
     ok = [c for c in cands if c[0] >= 0.9 * most]
     _, _, px, py = min(ok, key=lambda c: (c[1], -c[0]))
     return px, py
+
+
+def _gw_tile_shape(nx: int, ny: int) -> tuple[int, int]:
+    """Columns of one wavefront tile (one warp: wx * wy <= 32): 8 x 4 keeps
+    the tile crossings on the critical path (TX + TY) low at 1M cells."""
+    env = os.environ.get("B2S_GW_TILE")
+    if env:
+        wx, wy = (int(v) for v in env.split(","))
+        return min(wx, nx), min(wy, ny)
+    wx = min(nx, 8)
+    wy = max(1, min(ny, 32 // wx))
+    return wx, wy
+
+
+def _maybe_gw(f: Ilu0Factorization, plan: ParallelPlan):
+    """Deep plans of a natural-order 7-point grid: the wavefront sweeps
+    (csrc/gridwave.cu, one warp per tile of columns, dependencies through
+    warp shuffles; bit-identical to the sync-free sweeps).  The packing
+    kernel verifies every row; anything else keeps the sync-free sweeps.
+    B2S_GW=0 turns it off."""
+    if os.environ.get("B2S_GW", "1") == "0" or f.tiles or f.phased or f._lu is None:
+        return
+    if plan.group_count < 16 or f._b > 4:
+        return
+    g = grid_shape(f._source)
+    if g is None:
+        return
+    nx, ny, nz = g
+    wx, wy = _gw_tile_shape(nx, ny)
+    h = C.c_void_p(None)
+    rc = D.lib().b2s_gw_create(f._n, f._b, nx, ny, nz, wx, wy,
+                               D.ptr(plan.device("permutation")),
+                               D.ptr(plan.device("inverse_permutation")),
+                               D.ptr(f._lu.pat.rp), D.ptr(f._lu.pat.ci), D.ptr(f._lu.vals),
+                               D.ptr(f._invd), C.byref(h), D.stream())
+    if rc == 5:   # B2S_UNSUPPORTED: not a stencil row of this plan / too many tiles
+        return
+    check(rc, "gw_create")
+    f.gw = h.value
+    f.gw_shape = (nx, ny, nz, wx, wy)
 
 
 def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):

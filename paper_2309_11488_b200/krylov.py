@@ -310,6 +310,7 @@ class DeviceKrylov:
                                                        D.ptr(f.upper.vals))
             args.dinv_tiles = D.ptr(f.dtiles)
             args.tiles = f.tiles
+            args.gw = f.gw
             if f.phased and not f.tiles:
                 args.ngroups = len(s.gslice_host) - 1
                 args.goff1 = s.goff1

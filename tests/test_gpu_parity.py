@@ -599,3 +599,37 @@ def test_fused_vector_passes_match_separate(monkeypatch, dims):
         assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
         np.testing.assert_allclose(r1.final_norm, r0.final_norm, rtol=1e-8)
     assert out[("1", 1e-8)][1].iterations % 1.0 == 0.5   # the half-step exit is exercised
+
+
+@pytest.mark.parametrize("dims", [(20, 20, 10), (12, 10, 16), (8, 7, 5), (3, 40, 6), (33, 5, 4)])
+@pytest.mark.parametrize("plan_kind", ["level", "sequential"])
+def test_wavefront_sweeps_bit_identical(monkeypatch, dims, plan_kind):
+    """Natural-order grids: the wavefront sweeps (csrc/gridwave.cu, one warp
+    per tile of columns) equal the sync-free sweeps bit for bit -- the
+    application, and whole solves through the device loop."""
+    bundle = P.generate(P.GeneratorSpec(*dims, seed=4, diagonal_boost=1e-2))
+    a, rhs = bundle.a, bundle.rhs
+    plan = PLANS[plan_kind](a.pattern)
+    r = P.BlockVector(np.random.default_rng(1).uniform(-1, 1, rhs.data.size), 3)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("B2S_GW", flag)
+        f = P.decompose(a, plan)
+        # (few-level plans take the phased sweeps instead)
+        assert (f.gw is not None) == (flag == "1" and not f.phased)
+        z = f.apply(r).data
+        x, rep = P.bicgstab(P.MatrixOperator(a), f, rhs, stop=P.StoppingCriteria(1e-10, 200))
+        out[flag] = (z, x.data, rep)
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_array_equal(out["1"][1], out["0"][1])
+    assert out["1"][2].iterations == out["0"][2].iterations
+
+
+def test_wavefront_declines_non_stencil_rows(monkeypatch):
+    """A pattern that is not a 7-point stencil of its grid keeps the sync-free
+    sweeps (the packing kernel verifies every row)."""
+    monkeypatch.setenv("B2S_GW", "1")
+    from paper_2309_11488_b200 import synthetic as S
+    m = S.generate_masked(14, 16, 8, seed=11).a
+    f = P.decompose(m, P.level_schedule(m.pattern))
+    assert f.gw is None

@@ -1,4 +1,4 @@
-"""Level-plan ILU0 application on C4: sync-free sweeps vs the tiled kernels.
+"""Level-plan ILU0 application on C4: sync-free sweeps vs the wavefront kernels.
 
 python tools/level_apply_bench.py [nx ny nz]
 Each variant is checked bit for bit against the sync-free sweeps; prints
@@ -43,8 +43,10 @@ x = torch.rand(m, dtype=torch.float64, device="cuda")
 alg = (nnz - n) * 76 + 72 * n + 8 * (n + 1) + 96 * n
 out = {"dims": dims, "groups": plan.group_count}
 ref = None
-variants = [("syncfree", {"B2S_TILES": "0"}), ("tiles_grid", {"B2S_TILES": "1"}),
-            ("tiles_range", {"B2S_TILES": "1", "B2S_TILES_GRID": "0"})]
+variants = [("syncfree", {"B2S_TILES": "0", "B2S_GW": "0"}),
+            ("wavefront", {"B2S_TILES": "0", "B2S_GW": "1"})]
+if os.environ.get("B2S_BENCH_TILES") == "1":
+    variants += [("tiles_grid", {"B2S_TILES": "1", "B2S_GW": "0"})]
 for name, env in variants:
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
@@ -57,7 +59,8 @@ for name, env in variants:
             ref = zz
         out[name] = {"us": round(t, 1), "gbs_alg": round(alg / t / 1e3, 1),
                      "bit_equal": bool(torch.equal(zz, ref)),
-                     "tiles": getattr(f, "tile_shape", None) if f.tiles else None}
+                     "tiles": getattr(f, "tile_shape", None) if f.tiles else None,
+                     "gw": getattr(f, "gw_shape", None) if f.gw else None}
         del f
     finally:
         for k, v in old.items():
