@@ -219,14 +219,19 @@ int b2s_tiles_apply(int b, const void* handle, const double* r, double* y, doubl
  * Deep plans (level schedules, the sequential plan) of an nx*ny*nz grid: one
  * warp per tile of wx*wy <= 32 columns walks the levels, in-tile
  * dependencies through warp shuffles, tile edges through sentinel-checked
- * edge buffers.  create packs the plan-order factor (rp/ci/lu combined L\U,
- * inv = inverse diagonals; perm old->plan, iperm plan->old) and verifies
- * every row is a stencil row of the plan; B2S_UNSUPPORTED otherwise (keep the
- * sync-free sweeps).  apply: z = U^-1 L^-1 r in plan order, bit-identical to
- * b2s_ilu0_apply.  Replaces Ilu0Factorization.apply (bs/ilu0.py:105-142). */
+ * edge buffers.  create checks that every row of the plan-order pattern
+ * (perm old->plan, iperm plan->old) is a stencil row of the plan --
+ * B2S_UNSUPPORTED otherwise (keep the sync-free sweeps) -- and fill packs the
+ * factor's values into the warp's step records.  apply: z = U^-1 L^-1 r in
+ * plan order, bit-identical to b2s_ilu0_apply.  Replaces
+ * Ilu0Factorization.apply (bs/ilu0.py:105-142). */
+long long b2s_gw_workspace_bytes(int n, int b, int nx, int ny, int nz, int wx, int wy);
+/* pattern phase (rp/ci: the plan-order pattern; synchronises once) */
 int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const int32_t* perm,
-                  const int32_t* iperm, const int32_t* rp, const int32_t* ci, const double* lu,
-                  const double* inv, void** handle_out, cudaStream_t stream);
+                  const int32_t* iperm, const int32_t* rp, const int32_t* ci, void* workspace,
+                  long long ws_bytes, void** handle_out, cudaStream_t stream);
+/* value phase, stream-ordered: lu = combined L\U on that pattern, inv = inverse diagonals */
+int b2s_gw_fill(void* handle, const double* lu, const double* inv, cudaStream_t stream);
 int b2s_gw_destroy(void* handle);
 int b2s_gw_apply(int b, const void* handle, const double* r, double* z, cudaStream_t stream);
 /* debug (B2S_GW_TRACE set at create): the last apply's per-step end times,

@@ -96,8 +96,10 @@ SIGNATURES = {
     "b2s_fill_sentinel": (_I, [_LL, _P, _P]),
     "b2s_dot_chunked": (_I, [_LL, _P, _P, _P, _P, _P]),
     "b2s_partition_greedy": (_I, [_LL, _LL, _P, _P, _P, _LL, _P]),
-    "b2s_gw_create": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
+    "b2s_gw_workspace_bytes": (_LL, [_I, _I, _I, _I, _I, _I, _I]),
+    "b2s_gw_create": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _LL,
                            C.POINTER(C.c_void_p), _P]),
+    "b2s_gw_fill": (_I, [_P, _P, _P, _P]),
     "b2s_gw_destroy": (_I, [_P]),
     "b2s_gw_apply": (_I, [_I, _P, _P, _P, _P]),
     "b2s_gw_trace": (_I, [_P, _P, _LL, C.POINTER(C.c_longlong), _P]),

@@ -358,12 +358,13 @@ __global__ void k_gw_scatter(GwDev g, double* __restrict__ z) {
   }
 }
 
-// ---- packing (once per factorisation): one thread per (tile, step, lane)
-__global__ void k_gw_pack(GwDev g, int b, int n, const int32_t* __restrict__ perm,
+// ---- packing, one thread per (tile, step, lane).  Pattern phase (before
+// the numeric factorisation): meta words, the CSR slot of each of the six
+// stencil entries, and the row-by-row check that the plan is a stencil plan.
+// Value phase (after it, asynchronous): the blocks into the step records.
+__global__ void k_gw_meta(GwDev g, int32_t* __restrict__ src, const int32_t* __restrict__ perm,
                           const int32_t* __restrict__ iperm, const int32_t* __restrict__ rp,
-                          const int32_t* __restrict__ ci, const double* __restrict__ lu,
-                          const double* __restrict__ inv, char* recf, char* recb, int* bad) {
-  const int bb = b * b;
+                          const int32_t* __restrict__ ci, int* bad) {
   const long long T = (long long)g.TX * g.TY;
   const long long total = T * g.S * 32;
   const long long nxy = (long long)g.nx * g.ny;
@@ -375,16 +376,10 @@ __global__ void k_gw_pack(GwDev g, int b, int n, const int32_t* __restrict__ per
     const int t = (int)(slot / g.S);
     const GwTile a = gw_tile(g, t, lane);
     const int x = a.x0 + a.xl, y = a.y0 + a.yl, z = a.L0 + s - x - y;
-    int* mf = reinterpret_cast<int*>(recf + slot * g.rf);
-    int* mb = reinterpret_cast<int*>(recb + slot * g.rb);
-    double* Lv = reinterpret_cast<double*>(recf + slot * g.rf + kGwMetaBytes);
-    double* Uv = reinterpret_cast<double*>(recb + slot * g.rb + kGwMetaBytes);
-    for (int k = 0; k < 3; ++k)
-      for (int e = 0; e < bb; ++e) {
-        Lv[(k * bb + e) * 32 + lane] = 0.0;
-        Uv[(k * bb + e) * 32 + lane] = 0.0;
-      }
-    for (int e = 0; e < bb; ++e) Uv[(3 * bb + e) * 32 + lane] = 0.0;
+    int* mf = reinterpret_cast<int*>(const_cast<char*>(g.recf) + slot * g.rf);
+    int* mb = reinterpret_cast<int*>(const_cast<char*>(g.recb) + slot * g.rb);
+    int32_t* sp = src + slot * 6 * 32 + lane;
+    for (int k = 0; k < 6; ++k) sp[k * 32] = -1;
     if (!a.valid || s >= a.St || z < 0 || z >= g.nz) {
       mf[lane] = mb[lane] = -1;
       continue;
@@ -406,14 +401,32 @@ __global__ void k_gw_pack(GwDev g, int b, int n, const int32_t* __restrict__ per
       // lower entries must be the minus-neighbours and precede the row in the plan
       if (kind < 0 || (kind < 3) != (c < pr) || (mask & (1 << kind))) { atomicExch(bad, 1); continue; }
       mask |= 1 << kind;
-      // record order = ascending plan columns: forward z-1, y-1, x-1 (kinds 0,1,2);
-      // backward x+1, y+1, z+1 (kinds 3,4,5)
-      double* dst = kind < 3 ? Lv : Uv;
-      const int kk = kind < 3 ? kind : kind - 3;
-      for (int e = 0; e < bb; ++e) dst[(kk * bb + e) * 32 + lane] = lu[(long long)p * bb + e];
+      sp[kind * 32] = p;
     }
-    for (int e = 0; e < bb; ++e) Uv[(3 * bb + e) * 32 + lane] = inv[(long long)pr * bb + e];
     mf[lane] = mb[lane] = pr | (mask << 25);
+  }
+}
+
+// record order = ascending plan columns: forward z-1, y-1, x-1 (kinds 0..2),
+// backward x+1, y+1, z+1 (kinds 3..5), then inv(U_ii)
+__global__ void k_gw_vals(GwDev g, int bb, const int32_t* __restrict__ src,
+                          const double* __restrict__ lu, const double* __restrict__ inv) {
+  const long long total = (long long)g.TX * g.TY * g.S * 32;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(q % 32);
+    const long long slot = q / 32;
+    const int mt = reinterpret_cast<const int*>(g.recf + slot * g.rf)[lane];
+    double* Lv = reinterpret_cast<double*>(const_cast<char*>(g.recf) + slot * g.rf + kGwMetaBytes);
+    double* Uv = reinterpret_cast<double*>(const_cast<char*>(g.recb) + slot * g.rb + kGwMetaBytes);
+    const int32_t* sp = src + slot * 6 * 32 + lane;
+    for (int k = 0; k < 6; ++k) {
+      const int p = sp[k * 32];
+      double* dst = (k < 3 ? Lv : Uv) + ((k % 3) * bb) * 32 + lane;
+      for (int e = 0; e < bb; ++e) dst[e * 32] = p >= 0 ? lu[(long long)p * bb + e] : 0.0;
+    }
+    const long long pr = mt >= 0 ? (mt & 0x1FFFFFF) : -1;
+    for (int e = 0; e < bb; ++e) Uv[(3 * bb + e) * 32 + lane] = pr >= 0 ? inv[pr * bb + e] : 0.0;
   }
 }
 
@@ -426,7 +439,8 @@ __global__ void k_gw_fill(long long m, double* v) {
 struct GwHandle {
   GwDev g;
   int b, n;
-  void* mem;   // one allocation for everything
+  void* mem;       // own allocation (unused: the caller's workspace)
+  int32_t* src;    // [slots][6][32] CSR slot of each stencil entry (-1: none)
 };
 
 inline int gw_smem_bytes(const GwDev& g, int b, int dir) {
@@ -498,15 +512,7 @@ extern "C" {
 // the inverse diagonal blocks in plan order.  B2S_UNSUPPORTED when the grid
 // does not fit (more tiles than can be co-resident) or some row is not a
 // stencil row of that plan -- the caller keeps the sync-free sweeps.
-int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const int32_t* perm,
-                  const int32_t* iperm, const int32_t* rp, const int32_t* ci, const double* lu,
-                  const double* inv, void** handle_out, cudaStream_t st) {
-  *handle_out = nullptr;
-  if (b < 1 || b > 4 || nx < 1 || ny < 1 || nz < 1 || (long long)nx * ny * nz != n ||
-      wx < 1 || wy < 1 || wx * wy > kGwLanes || n >= (1 << 25))
-    return B2S_SHAPE;
-  GwHandle* h = new GwHandle();
-  GwDev& g = h->g;
+static void gw_shape(GwDev& g, int b, int nx, int ny, int nz, int wx, int wy) {
   g.nx = nx; g.ny = ny; g.nz = nz; g.wx = wx; g.wy = wy;
   g.TX = (nx + wx - 1) / wx;
   g.TY = (ny + wy - 1) / wy;
@@ -514,6 +520,38 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
   const int bb = b * b;
   g.rf = kGwMetaBytes + 3 * bb * 32 * 8;
   g.rb = kGwMetaBytes + 4 * bb * 32 * 8;
+}
+
+static long long gw_bytes(const GwDev& g, int b) {
+  const long long slots = (long long)g.TX * g.TY * g.S;
+  return slots * ((long long)g.rf + g.rb) +
+         (3 * slots * b * 32 + 2 * slots * g.wy * b + 2 * slots * g.wx * b) * 8 +
+         slots * 6 * 32 * 4 + 256;
+}
+
+// device bytes b2s_gw_create needs as its workspace (0: bad shape)
+long long b2s_gw_workspace_bytes(int n, int b, int nx, int ny, int nz, int wx, int wy) {
+  if (b < 1 || b > 4 || nx < 1 || ny < 1 || nz < 1 || (long long)nx * ny * nz != n || wx < 1 ||
+      wy < 1 || wx * wy > kGwLanes)
+    return 0;
+  GwDev g{};
+  gw_shape(g, b, nx, ny, nz, wx, wy);
+  return gw_bytes(g, b);
+}
+
+// Pattern phase: shapes, meta words and the stencil check of every row (one
+// synchronisation, before the numeric factorisation is queued).
+int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const int32_t* perm,
+                  const int32_t* iperm, const int32_t* rp, const int32_t* ci, void* workspace,
+                  long long ws_bytes, void** handle_out, cudaStream_t st) {
+  *handle_out = nullptr;
+  if (b < 1 || b > 4 || nx < 1 || ny < 1 || nz < 1 || (long long)nx * ny * nz != n ||
+      wx < 1 || wy < 1 || wx * wy > kGwLanes || n >= (1 << 25) || !workspace)
+    return B2S_SHAPE;
+  GwHandle* h = new GwHandle();
+  GwDev& g = h->g;
+  gw_shape(g, b, nx, ny, nz, wx, wy);
+  if (ws_bytes < gw_bytes(g, b)) { delete h; return B2S_SHAPE; }
   const long long T = (long long)g.TX * g.TY;
   // every tile waits on its neighbours: all CTAs must be co-resident
   int dev = 0, sms = 0, per_sm = 0;
@@ -531,11 +569,10 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
   const long long slots = T * g.S;
   const long long nV = slots * b * 32;
   const long long nEx = slots * wy * b, nEy = slots * wx * b;
-  const long long bytes = slots * ((long long)g.rf + g.rb) + (3 * nV + 2 * nEx + 2 * nEy) * 8 + 256;
-  if (cudaMalloc(&h->mem, bytes) != cudaSuccess) { delete h; return B2S_CUDA_ERROR; }
-  char* p = reinterpret_cast<char*>(h->mem);
-  char* recf = p; p += slots * g.rf;
-  char* recb = p; p += slots * g.rb;
+  h->mem = nullptr;   // the workspace belongs to the caller
+  char* p = reinterpret_cast<char*>(workspace);
+  g.recf = p; p += slots * g.rf;
+  g.recb = p; p += slots * g.rb;
   double* d = reinterpret_cast<double*>(p);
   g.rpk = d; d += nV;
   g.ypk = d; d += nV;
@@ -544,7 +581,7 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
   g.eW = d; d += nEx;
   g.eN = d; d += nEy;
   g.eS = d; d += nEy;
-  g.recf = recf; g.recb = recb;
+  h->src = reinterpret_cast<int32_t*>(d);
   g.trace = nullptr;
   if (getenv("B2S_GW_TRACE") && cudaMalloc(&g.trace, 2 * slots * 8) != cudaSuccess) g.trace = nullptr;
   h->b = b;
@@ -554,10 +591,9 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
   bool ok = cudaMallocAsync(&bad, sizeof(int), st) == cudaSuccess &&
             cudaMemsetAsync(bad, 0, sizeof(int), st) == cudaSuccess;
   if (ok) {
-    long long thr = slots * 32;
-    long long grid = (thr + 255) / 256;
+    long long grid = (slots * 32 + 255) / 256;
     if (grid > kSms * 64) grid = kSms * 64;
-    k_gw_pack<<<(int)grid, 256, 0, st>>>(g, b, n, perm, iperm, rp, ci, lu, inv, recf, recb, bad);
+    k_gw_meta<<<(int)grid, 256, 0, st>>>(g, h->src, perm, iperm, rp, ci, bad);
     // all four edge buffers start "not produced" (each sweep then re-arms the
     // other direction's buffers of its own tile)
     const long long ne = 2 * nEx + 2 * nEy;
@@ -569,12 +605,25 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
          cudaFreeAsync(bad, st) == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess;
   }
   if (!ok || hbad) {
-    cudaFree(h->mem);
     if (g.trace) cudaFree(g.trace);
     delete h;
     return ok ? B2S_UNSUPPORTED : B2S_CUDA_ERROR;
   }
   *handle_out = h;
+  return B2S_OK;
+}
+
+// Value phase: the factor's blocks into the step records (stream-ordered,
+// no synchronisation).  lu: combined L\U in plan order on the pattern given to
+// create; inv: inverse diagonal blocks in plan order.
+int b2s_gw_fill(void* handle, const double* lu, const double* inv, cudaStream_t st) {
+  GwHandle* h = reinterpret_cast<GwHandle*>(handle);
+  if (!h) return B2S_SHAPE;
+  const long long slots = (long long)h->g.TX * h->g.TY * h->g.S;
+  long long grid = (slots * 32 + 255) / 256;
+  if (grid > kSms * 64) grid = kSms * 64;
+  k_gw_vals<<<(int)grid, 256, 0, st>>>(h->g, h->b * h->b, h->src, lu, inv);
+  B2S_LAUNCH_CHECK();
   return B2S_OK;
 }
 
@@ -595,7 +644,7 @@ int b2s_gw_destroy(void* handle) {
   GwHandle* h = reinterpret_cast<GwHandle*>(handle);
   if (!h) return B2S_OK;
   if (h->g.trace) cudaFree(h->g.trace);
-  cudaFree(h->mem);
+  if (h->mem) cudaFree(h->mem);
   delete h;
   return B2S_OK;
 }

@@ -292,6 +292,7 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
     a_src = None
     if identity:
         a_perm = bsr
+        gw = _gw_plan(bsr.pat.grid, plan, bsr.pat, b)
         lu = D.DevBSR(bsr.pat, b, bsr.vals.clone())
     else:
         # plan-order pattern + source map; the factor's values are gathered
@@ -299,6 +300,7 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
         # later filled from the input the same way -- no permuted copy
         ppat, src = D.permute_pattern(bsr.pat, plan.device("permutation"),
                                       plan.device("inverse_permutation"))
+        gw = _gw_plan(bsr.pat.grid, plan, ppat, b)
         vals = D.empty_f64(bsr.pat.nnz * b * b, dev)
         if bsr.pat.nnz:
             check(D.lib().b2s_gather_blocks(bsr.pat.nnz, b, D.ptr(src), D.ptr(bsr.vals),
@@ -329,7 +331,7 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
     f = Ilu0Factorization(plan, b, n, lu, inv, smap, lower, upper, dtiles, identity, a, a_perm)
     f._a_src = a_src
     _maybe_tiles(f, plan, diag)
-    _maybe_gw(f, plan)
+    _gw_fill(f, gw)
     return f
 
 
@@ -378,32 +380,48 @@ def _gw_tile_shape(nx: int, ny: int) -> tuple[int, int]:
     return wx, wy
 
 
-def _maybe_gw(f: Ilu0Factorization, plan: ParallelPlan):
-    """Deep plans of a natural-order 7-point grid: the wavefront sweeps
-    (csrc/gridwave.cu, one warp per tile of columns, dependencies through
-    warp shuffles; bit-identical to the sync-free sweeps).  The packing
-    kernel verifies every row; anything else keeps the sync-free sweeps.
+def _gw_plan(hint, plan: ParallelPlan, ppat: "D.DevPattern", b: int):
+    """Pattern phase of the wavefront sweeps (csrc/gridwave.cu) for deep plans
+    of a natural-order 7-point grid: one warp per tile of columns, in-tile
+    dependencies through warp shuffles, bit-identical to the sync-free
+    sweeps.  Runs before the numeric factorisation is queued (its single
+    synchronisation waits for the pattern work only); the kernel checks every
+    row, anything else keeps the sync-free sweeps.  Returns (handle,
+    workspace, shape) or None.  ``hint``: the input pattern's grid_hint
+    (nx, ny) -- taken at upload from one row; the kernel verifies them all.
     B2S_GW=0 turns it off."""
-    if os.environ.get("B2S_GW", "1") == "0" or f.tiles or f.phased or f._lu is None:
-        return
-    if plan.group_count < 16 or f._b > 4:
-        return
-    g = grid_shape(f._source)
-    if g is None:
-        return
-    nx, ny, nz = g
+    if os.environ.get("B2S_GW", "1") == "0" or os.environ.get("B2S_TILES", "0") != "0":
+        return None
+    if plan.group_count <= D.PHASED_MAX_GROUPS or b > 4:
+        return None
+    n = ppat.n
+    if hint is None or n % (hint[0] * hint[1]):
+        return None
+    nx, ny = hint
+    nz = n // (nx * ny)
     wx, wy = _gw_tile_shape(nx, ny)
+    nbytes = int(D.lib().b2s_gw_workspace_bytes(n, b, nx, ny, nz, wx, wy))
+    if nbytes <= 0:
+        return None
+    # the packed factor lives in a caching-allocator block (no cudaMalloc per solve)
+    ws = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=ppat.rp.device)
     h = C.c_void_p(None)
-    rc = D.lib().b2s_gw_create(f._n, f._b, nx, ny, nz, wx, wy,
-                               D.ptr(plan.device("permutation")),
-                               D.ptr(plan.device("inverse_permutation")),
-                               D.ptr(f._lu.pat.rp), D.ptr(f._lu.pat.ci), D.ptr(f._lu.vals),
-                               D.ptr(f._invd), C.byref(h), D.stream())
+    rc = D.lib().b2s_gw_create(n, b, nx, ny, nz, wx, wy, D.ptr(plan.device("permutation")),
+                               D.ptr(plan.device("inverse_permutation")), D.ptr(ppat.rp),
+                               D.ptr(ppat.ci), D.ptr(ws), nbytes, C.byref(h), D.stream())
     if rc == 5:   # B2S_UNSUPPORTED: not a stencil row of this plan / too many tiles
-        return
+        return None
     check(rc, "gw_create")
-    f.gw = h.value
-    f.gw_shape = (nx, ny, nz, wx, wy)
+    return h.value, ws, (nx, ny, nz, wx, wy)
+
+
+def _gw_fill(f: Ilu0Factorization, gw):
+    """Value phase: the factor's blocks into the step records (async)."""
+    if gw is None:
+        return
+    h, ws, shape = gw
+    f.gw, f._gw_ws, f.gw_shape = h, ws, shape
+    check(D.lib().b2s_gw_fill(h, D.ptr(f._lu.vals), D.ptr(f._invd), D.stream()), "gw_fill")
 
 
 def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
