@@ -46,7 +46,7 @@ class Ilu0Factorization:
         self._lu = lu
         self._invd = invd
         self.smap = smap
-        self.lower = lower
+        self._lower = lower
         self._upper = upper
         self.dtiles = dtiles
         self._identity_perm = identity
@@ -57,8 +57,13 @@ class Ilu0Factorization:
         # rows live there) and what is needed to rebuild the CSR factors
         self._two_colour = two_colour
         self.a_sell = two_colour["a_sell"] if two_colour else None
-        uw = (self.a_sell.width - 1) if two_colour else upper.width
-        self.kc = _kc(max(lower.width, uw))
+        # (deep plans of grids take the wavefront sweeps, csrc/gridwave.cu: their
+        # SELL layouts are built only if something asks for them)
+        if lower is None:
+            self.kc = 2
+        else:
+            uw = (self.a_sell.width - 1) if two_colour else upper.width
+            self.kc = _kc(max(lower.width, uw))
         self._combined = None
         self._inv_host = None
         self._tickets = torch.zeros(8, dtype=torch.int32, device=invd.device)
@@ -72,8 +77,8 @@ class Ilu0Factorization:
         self.gw = None           # b2s_gw_create handle (wavefront sweeps of grids), or None
         # few independent groups (colourings) and no same-group entries: the
         # phased sweeps, 2(G-1) plain passes, no polling (bit-identical)
-        ustale = False if two_colour else upper.stale
-        self.phased = (smap.gslice_host is not None and not lower.stale and not ustale
+        self.phased = (smap.gslice_host is not None and lower is not None and not lower.stale
+                       and not (False if two_colour else upper.stale)
                        and os.environ.get("B2S_PHASED", "1") != "0")
 
     # -- lazily materialised pieces of a 2-colour factorisation ----------------
@@ -92,6 +97,13 @@ class Ilu0Factorization:
                 D.ptr(t["udiag"]), D.ptr(vals), D.stream()), "factor_2colour_combined")
             self._lu = D.DevBSR(pat, self._b, vals)
         return self._lu
+
+    @property
+    def lower(self) -> "D.Sell":
+        if self._lower is None:
+            self._lower = D.Sell.build(self.smap, self.lu_device, 1,
+                                       self.plan.device("group_offsets"), self.plan.group_count)
+        return self._lower
 
     @property
     def upper(self) -> "D.Sell":
@@ -323,8 +335,10 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
         raise SingularPivot(row)
     check(rc, "ilu0_factor")
     goff = plan.device("group_offsets")
-    lower = D.Sell.build(smap, lu, 1, goff, plan.group_count)
-    upper = D.Sell.build(smap, lu, 2, goff, plan.group_count)
+    lower = upper = None
+    if gw is None:   # (the wavefront sweeps read their own packed records)
+        lower = D.Sell.build(smap, lu, 1, goff, plan.group_count)
+        upper = D.Sell.build(smap, lu, 2, goff, plan.group_count)
     dtiles = D.empty_f64(smap.nslices * b * b * 32, dev)
     check(D.lib().b2s_diag_tiles(smap.nslices, b, D.ptr(smap.row0), D.ptr(smap.nrows),
                                  D.ptr(inv), D.ptr(dtiles), D.stream()), "diag_tiles")

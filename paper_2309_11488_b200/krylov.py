@@ -296,16 +296,18 @@ class DeviceKrylov:
         args.kc = f.kc if f is not None else 2
         args.maxit = stop.max_iterations
         args.check_lag = check_lag
-        args.refill_y = 1 if (f is not None and not self.fuse and f.upper.stale) else 0
+        args.refill_y = 1 if (f is not None and not self.fuse and not f.gw and
+                              f.upper.stale) else 0
         args.sweep_flags = f.sweep_flags if f is not None else 0
         args.tol = stop.relative_reduction
         s = self.smap
         args.nslices, args.row0, args.nrows = s.nslices, D.ptr(s.row0), D.ptr(s.nrows)
         args.a_sp, args.a_cols, args.a_vals = D.ptr(self.a.sp), D.ptr(self.a.cols), D.ptr(self.a.vals)
         if f is not None:
-            args.l_sp, args.l_cols, args.l_vals = (D.ptr(f.lower.sp), D.ptr(f.lower.cols),
-                                                   D.ptr(f.lower.vals))
-            if not self.fuse:   # (the fused passes read U's rows from the operator)
+            if not f.gw:   # (the wavefront sweeps read their own packed records)
+                args.l_sp, args.l_cols, args.l_vals = (D.ptr(f.lower.sp), D.ptr(f.lower.cols),
+                                                       D.ptr(f.lower.vals))
+            if not self.fuse and not f.gw:   # (the fused passes read U's rows from the operator)
                 args.u_sp, args.u_cols, args.u_vals = (D.ptr(f.upper.sp), D.ptr(f.upper.cols),
                                                        D.ptr(f.upper.vals))
             args.dinv_tiles = D.ptr(f.dtiles)
