@@ -168,18 +168,27 @@ class HaloPlan:
 
 
 class _DeviceBlock:
-    """A shard's diagonal block as the factorisation sees it: the host pattern
-    and block size, with the values resident on the device only (gathered
-    there from the uploaded slab) -- no host copy of the slab's blocks."""
+    """A shard's diagonal block as the factorisation sees it: block size and
+    pattern, with the values resident on the device only (gathered there from
+    the uploaded slab) and the host pattern downloaded only if something asks
+    for it -- no host copy of the slab's blocks, no host pattern pass."""
 
-    def __init__(self, pattern: SparsityPattern, block_size: int):
-        self.pattern = pattern
+    def __init__(self, pat: "D.DevPattern", block_size: int):
+        self._pat = pat
+        self._pattern = None
         self.block_size = block_size
         self.layout = Layout.BLOCK_ROW_MAJOR
 
     @property
     def num_block_rows(self) -> int:
-        return self.pattern.num_block_rows
+        return self._pat.n
+
+    @property
+    def pattern(self) -> SparsityPattern:
+        if self._pattern is None:
+            rp, ci = self._pat.host()
+            self._pattern = SparsityPattern(self._pat.n, rp, ci)
+        return self._pattern
 
     def as_block_row_major(self):
         return self
@@ -187,6 +196,39 @@ class _DeviceBlock:
     @property
     def values(self):
         raise RuntimeError("a shard's preconditioner blocks live on the device only")
+
+
+class _DeviceHalo:
+    """The shard's halo bookkeeping computed on the device from the uploaded
+    slab pattern (the host keeps only the ghost ids and their owners -- tens
+    of thousands of ints): HaloPlan's result without its host passes over
+    every coupling."""
+
+    def __init__(self, ghosts: np.ndarray, recv: dict):
+        self.ghosts, self.recv = ghosts, recv
+        self.G = len(ghosts)
+
+    def requests(self):
+        """{owner rank: global ids this slab needs from it}"""
+        return {h: self.ghosts[idx] for h, idx in self.recv.items()}
+
+
+def _slab_grid_hint(slab: Slab):
+    """grid_hint of the slab's diagonal block from its middle row (host, one row)."""
+    R = slab.rows
+    if R < 8:
+        return None
+    r = R // 2
+    cols = np.asarray(slab.ci[int(slab.rp[r]):int(slab.rp[r + 1])], dtype=np.int64) - slab.r0
+    cols = cols[(cols >= 0) & (cols < R)]
+    u = [int(v) for v in np.unique(cols[cols > r] - r)]
+    if u == [1]:
+        return R, 1
+    if len(u) == 2 and u[0] == 1 and R % u[1] == 0:
+        return u[1], R // u[1]
+    if len(u) == 3 and u[0] == 1 and u[2] % u[1] == 0 and R % u[2] == 0:
+        return u[1], u[2] // u[1]
+    return None
 
 
 class Shard:
@@ -197,41 +239,56 @@ class Shard:
         dev = D.require_cuda()
         R, b = slab.rows, slab.b
         self.R, self.b = R, b
-        ci = slab.ci
-        hp = HaloPlan(slab, owners)
-        self.halo_plan = hp
-        own, lcol = hp.own, hp.lcol
-        self.ghosts, self.G, self.recv = hp.ghosts, hp.G, hp.recv
-        rows = np.repeat(np.arange(R), np.diff(slab.rp))
-        # preconditioner source: the diagonal block (cross-slab blocks dropped);
-        # its pattern on the host, its values only on the device
-        prp = np.zeros(R + 1, dtype=np.int64)
-        np.cumsum(np.bincount(rows[own], minlength=R), out=prp[1:])
-        self.pmat = _DeviceBlock(SparsityPattern(R, prp, lcol[own]), b)
-        # one upload of the slab (pattern + values): the diagonal block's
-        # values are gathered from it on the device; both stay resident and
-        # setup() re-runs the device pipeline (plan, permutation,
-        # factorisation, layouts) from them
-        opat = D.DevPattern(R, len(ci), D.i32(slab.rp, dev), D.i32(lcol, dev))
+        nnz = len(slab.ci)
+        # one upload of the slab (pattern + values); the halo bookkeeping, the
+        # diagonal block's pattern and its values are derived on the device
+        # and stay resident -- setup() re-runs the device pipeline (plan,
+        # permutation, factorisation, layouts) from them
+        src = torch.from_numpy(np.ascontiguousarray(slab.ci, dtype=np.int64))
+        ci = src.to(dev, non_blocking=D.is_pinned(src))
+        rp32 = D.i32(slab.rp, dev)
+        own = (ci >= slab.r0) & (ci < slab.r1)
+        gh = ~own
+        ghosts_d = torch.unique(ci[gh])                      # global ids, ascending
+        lcol = torch.where(own, ci - slab.r0, R + torch.searchsorted(ghosts_d, ci))
+        counts = (rp32[1:R + 1] - rp32[:R]).long()
+        rows = torch.repeat_interleave(torch.arange(R, device=dev), counts, output_size=nnz)
+        ghosts = ghosts_d.cpu().numpy()
+        gowner = np.searchsorted(owners, ghosts, side="right") - 1
+        recv = {int(h): np.flatnonzero(gowner == h) for h in np.unique(gowner)}
+        self.halo_plan = _DeviceHalo(ghosts, recv)
+        self.ghosts, self.G, self.recv = ghosts, len(ghosts), recv
+        opat = D.DevPattern(R, nnz, rp32, lcol.to(torch.int32) if nnz else D.empty_i32(1, dev))
         self.obsr = D.DevBSR(opat, b, D.f64(slab.vals3.reshape(-1), dev))
-        self._own_idx = D.i32(np.flatnonzero(own), dev)
-        ppat = D.DevPattern.upload(self.pmat.pattern)
-        self.pbsr = D.DevBSR(ppat, b, torch.empty(max(ppat.nnz, 1) * b * b, dtype=torch.float64,
+        # preconditioner source: the diagonal block (cross-slab blocks dropped)
+        own_rows = rows[own]
+        prp = torch.zeros(R + 1, dtype=torch.int64, device=dev)
+        prp[1:] = torch.cumsum(torch.bincount(own_rows, minlength=R), 0)
+        self._own_idx = torch.nonzero(own).flatten().to(torch.int32)
+        pnnz = int(self._own_idx.numel())
+        ppat = D.DevPattern(R, pnnz, prp.to(torch.int32),
+                            lcol[own].to(torch.int32) if pnnz else D.empty_i32(1, dev),
+                            _slab_grid_hint(slab))
+        self.pmat = _DeviceBlock(ppat, b)
+        self.pbsr = D.DevBSR(ppat, b, torch.empty(max(pnnz, 1) * b * b, dtype=torch.float64,
                                                   device=dev))
-        if ppat.nnz:
-            check(D.lib().b2s_gather_blocks(ppat.nnz, b, D.ptr(self._own_idx),
+        if pnnz:
+            check(D.lib().b2s_gather_blocks(pnnz, b, D.ptr(self._own_idx),
                                             D.ptr(self.obsr.vals), D.ptr(self.pbsr.vals),
                                             D.stream()), "gather_blocks")
         # ghost couplings of the boundary rows as CSR over ghost indices (the
         # fused 2-colour loop adds them after the halo pull; b2s_mesh bnd_*)
-        gh = ~own
-        erow = rows[gh]
-        ub, cnt = np.unique(erow, return_counts=True)
-        self._bnd_in = torch.as_tensor(ub.astype(np.int64), device=dev)
-        self._bnd_ptr = D.i32(np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64), dev)
-        self._bnd_col = D.i32((lcol[gh] - R).astype(np.int64), dev)
-        self._gh_idx = D.i32(np.flatnonzero(gh).astype(np.int64), dev)
-        self._bnd_val = torch.empty(max(int(gh.sum()), 1) * b * b, dtype=torch.float64, device=dev)
+        ub, cnt = torch.unique(rows[gh], return_counts=True)
+        self._bnd_in = ub.to(torch.int64)
+        bp = torch.zeros(ub.numel() + 1, dtype=torch.int64, device=dev)
+        bp[1:] = torch.cumsum(cnt, 0)
+        self._bnd_ptr = bp.to(torch.int32)
+        ngh = int(nnz - pnnz)
+        self._bnd_col = ((lcol[gh] - R).to(torch.int32) if ngh else D.empty_i32(1, dev))
+        self._gh_idx = (torch.nonzero(gh).flatten().to(torch.int32) if ngh else
+                        D.empty_i32(1, dev))
+        self._bnd_val = torch.empty(max(ngh, 1) * b * b, dtype=torch.float64, device=dev)
+        self._ngh = ngh
         self._gather_ghost_blocks()
         self.dev = dev
         if backend is not None:
@@ -266,7 +323,7 @@ class Shard:
         return self._sell
 
     def _gather_ghost_blocks(self):
-        nk = int(self._gh_idx.numel())
+        nk = self._ngh
         if nk:
             check(D.lib().b2s_gather_blocks(nk, self.b, D.ptr(self._gh_idx), D.ptr(self.obsr.vals),
                                             D.ptr(self._bnd_val), D.stream()), "gather_blocks")

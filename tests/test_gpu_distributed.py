@@ -342,3 +342,29 @@ def test_nccl_comm_world_of_one_over_nccl():
     import json
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["value"] > 0 and line.get("converged", True)
+
+
+def test_device_halo_plan_equals_host_halo_plan():
+    """The shard derives its halo bookkeeping on the device from the uploaded
+    slab; it must equal the host HaloPlan (ghost ids, owners, local columns,
+    the diagonal block's pattern)."""
+    from paper_2309_11488_b200.distributed import HaloPlan, Shard, generate_slab
+    spec = P.GeneratorSpec(9, 7, 12, seed=5)
+    world = 3
+    owners = np.array([slab_bounds(spec.nz, world, r)[0] * spec.nx * spec.ny
+                       for r in range(world)], dtype=np.int64)
+    for r in range(world):
+        slab = generate_slab(spec, r, world)
+        hp = HaloPlan(slab, owners)
+        sh = Shard(slab, owners, None)
+        np.testing.assert_array_equal(sh.ghosts, hp.ghosts)
+        assert sorted(sh.recv) == sorted(hp.recv)
+        for h in hp.recv:
+            np.testing.assert_array_equal(sh.recv[h], hp.recv[h])
+        np.testing.assert_array_equal(sh.obsr.pat.ci[: sh.obsr.pat.nnz].cpu().numpy(), hp.lcol)
+        rows = np.repeat(np.arange(slab.rows), np.diff(slab.rp))
+        prp = np.zeros(slab.rows + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows[hp.own], minlength=slab.rows), out=prp[1:])
+        pat = sh.pmat.pattern
+        np.testing.assert_array_equal(pat.row_pointers, prp)
+        np.testing.assert_array_equal(pat.column_indices, hp.lcol[hp.own])
