@@ -233,15 +233,35 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
   double prev[B];
 #pragma unroll
   for (int c = 0; c < B; ++c) prev[c] = 0.0;
-  const unsigned ring_s = gw_smem(ring);
-  for (int j = 0; j < a.St; ++j) {
-    const int s = s0 + dstep * j;
+  // the step's record is moved from its ring stage into registers one step
+  // ahead, so the shared-memory latency overlaps the previous step's
+  // dependent FMAs, and the stage is refilled as soon as it is copied
+  constexpr int NB = DIR == 0 ? 3 * BB : 4 * BB;   // blocks per record (+ inv(U_ii))
+  int mt_c = -1, mt_n = -1;
+  double bk_c[NB], bk_n[NB], vv_c[B], vv_n[B];
+  auto load_step = [&](int j, int& mt, double (&bk)[NB], double (&vv)[B]) {
     const int q = j % R;
     gw_mbar_wait(full + q, (unsigned)((j / R) & 1));
     const char* st_ = ring + q * stage;
-    const int mt = reinterpret_cast<const int*>(st_)[lane];
+    mt = reinterpret_cast<const int*>(st_)[lane];
     const double* blk = reinterpret_cast<const double*>(st_ + kGwMetaBytes) + lane;
-    const double* vv = reinterpret_cast<const double*>(st_ + rb) + lane;
+    const double* v = reinterpret_cast<const double*>(st_ + rb) + lane;
+#pragma unroll
+    for (int e = 0; e < NB; ++e) bk[e] = blk[e * 32];
+#pragma unroll
+    for (int c = 0; c < B; ++c) vv[c] = v[c * 32];
+  };
+  if (a.St > 0) load_step(0, mt_c, bk_c, vv_c);
+  for (int j = 0; j < a.St; ++j) {
+    const int s = s0 + dstep * j;
+    if (j + 1 < a.St) load_step(j + 1, mt_n, bk_n, vv_n);
+    // step j's stage is in registers: refill it with step j + R
+    __syncwarp();
+    if (lane == 0 && j + R < a.St) {
+      gw_fence_proxy();
+      issue(j + R);
+    }
+    const int mt = mt_c;
     const int mask = mt >= 0 ? (mt >> 25) : 0;
     double nx_[B], ny_[B];
 #pragma unroll
@@ -266,7 +286,7 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
       if (xok(s + dstep)) gw_load<B>(xin, ex);
       if (yok(s + dstep)) gw_load<B>(yin, ey);
     }
-    double acc[B], pr[B], m[BB];
+    double acc[B], pr[B];
 #pragma unroll
     for (int c = 0; c < B; ++c) acc[c] = 0.0;
     // ascending plan columns: forward z-1, y-1, x-1; backward x+1, y+1, z+1
@@ -274,10 +294,8 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
     for (int k = 0; k < 3; ++k) {
       const int bit = DIR == 0 ? (k == 0 ? mz : (k == 1 ? my : mx)) : (k == 0 ? mx : (k == 1 ? my : mz));
       if (mask & bit) {
-#pragma unroll
-        for (int e = 0; e < BB; ++e) m[e] = blk[(k * BB + e) * 32];
         const double* dep = k == 0 ? (DIR == 0 ? prev : nx_) : (k == 1 ? ny_ : (DIR == 0 ? nx_ : prev));
-        matvec<B>(m, dep, pr);
+        matvec<B>(bk_c + k * BB, dep, pr);
 #pragma unroll
         for (int c = 0; c < B; ++c) acc[c] += pr[c];
       }
@@ -285,14 +303,12 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
     double outv[B];
     if (DIR == 0) {
 #pragma unroll
-      for (int c = 0; c < B; ++c) outv[c] = canon(vv[c * 32] - acc[c]);
+      for (int c = 0; c < B; ++c) outv[c] = canon(vv_c[c] - acc[c]);
     } else {
       double tv[B], o[B];
 #pragma unroll
-      for (int c = 0; c < B; ++c) tv[c] = vv[c * 32] - acc[c];
-#pragma unroll
-      for (int e = 0; e < BB; ++e) m[e] = blk[(3 * BB + e) * 32];
-      matvec<B>(m, tv, o);
+      for (int c = 0; c < B; ++c) tv[c] = vv_c[c] - acc[c];
+      matvec<B>(bk_c + (NB - BB), tv, o);
 #pragma unroll
       for (int c = 0; c < B; ++c) outv[c] = canon(o[c]);
     }
@@ -318,14 +334,12 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
     if (g.trace && lane == 0)
       g.trace[(long long)DIR * g.TX * g.TY * g.S + base + s] = global_ns_gw();
 #endif
-    // the stage is consumed: refill it with step j + R
-    __syncwarp();
-    if (lane == 0 && j + R < a.St) {
-      gw_fence_proxy();
-      issue(j + R);
-    }
+    mt_c = mt_n;
+#pragma unroll
+    for (int e = 0; e < NB; ++e) bk_c[e] = bk_n[e];
+#pragma unroll
+    for (int c = 0; c < B; ++c) vv_c[c] = vv_n[c];
   }
-  (void)ring_s;
 }
 
 // the sweep's input in step order / its output back to plan order
