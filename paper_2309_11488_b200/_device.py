@@ -60,7 +60,7 @@ def i32(a: np.ndarray, dev) -> torch.Tensor:
     a = np.asarray(a)
     if a.dtype == np.int64 and a.size >= (1 << 16):
         src = torch.from_numpy(np.ascontiguousarray(a))
-        raw = src.to(dev, non_blocking=is_pinned(src))
+        raw = to_device(src, dev)
         out = torch.empty(a.size, dtype=torch.int32, device=dev)
         bad = C.c_int(0)
         check(lib().b2s_narrow_index(a.size, ptr(raw), ptr(out), C.byref(bad), stream()),
@@ -75,7 +75,86 @@ def i32(a: np.ndarray, dev) -> torch.Tensor:
 
 def f64(a: np.ndarray, dev) -> torch.Tensor:
     src = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
-    return src.to(dev, non_blocking=is_pinned(src))
+    return to_device(src, dev)
+
+
+def to_device(src: torch.Tensor, dev, stream=None) -> torch.Tensor:
+    """Host tensor -> new device tensor: plain async DMA from page-locked
+    memory, the staged path (staged_copy) for large pageable arrays."""
+    if is_pinned(src) or src.numel() * src.element_size() < STAGE_MIN_BYTES:
+        if stream is None:
+            return src.to(dev, non_blocking=is_pinned(src))
+        with torch.cuda.stream(stream):
+            return src.to(dev, non_blocking=is_pinned(src))
+    out = torch.empty(src.shape, dtype=src.dtype, device=dev)
+    staged_copy(out, src, stream or torch.cuda.current_stream(dev))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# pageable host -> device at DMA speed.  A copy out of ordinary (pageable)
+# numpy memory goes through the driver's own staging at a fraction of the
+# PCIe rate; here chunks are memcpy'd by a few host threads into a ring of
+# page-locked buffers and DMA'd from there while the next chunks are copied.
+
+STAGE_CHUNK = int(os.environ.get("B2S_STAGE_CHUNK_MB", "8")) << 20
+STAGE_BUFS = int(os.environ.get("B2S_STAGE_BUFS", "8"))
+STAGE_MIN_BYTES = 4 << 20
+_STAGERS: dict = {}
+
+
+class _Stager:
+    def __init__(self, dev):
+        import concurrent.futures as cf
+        import threading
+        self.bufs = [torch.empty(STAGE_CHUNK, dtype=torch.uint8, pin_memory=True)
+                     for _ in range(STAGE_BUFS)]
+        self.views = [b.numpy() for b in self.bufs]
+        self.events = [None] * STAGE_BUFS     # last DMA out of each buffer
+        workers = int(os.environ.get("B2S_STAGE_THREADS", "0")) or \
+            min(STAGE_BUFS - 1, max(2, (os.cpu_count() or 4) // 2))
+        self.pool = cf.ThreadPoolExecutor(max_workers=workers)
+        self.lock = threading.Lock()
+
+
+def staged_copy(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
+    """dst (contiguous device tensor) <- src (contiguous pageable host tensor of
+    the same byte size), DMAs enqueued on ``stream``; returns once every
+    chunk is in flight (the ring's buffers are reused only after their DMA)."""
+    nbytes = src.numel() * src.element_size()
+    if nbytes == 0:
+        return
+    dev = dst.device
+    st = _STAGERS.get(dev.index)
+    if st is None:
+        st = _STAGERS[dev.index] = _Stager(dev)
+    s8 = src.reshape(-1).view(torch.uint8).numpy()
+    d8 = dst.reshape(-1).view(torch.uint8)
+    nch = (nbytes + STAGE_CHUNK - 1) // STAGE_CHUNK
+    with st.lock:
+        def fill(i):
+            b = i % STAGE_BUFS
+            ev = st.events[b]
+            if ev is not None:
+                ev.synchronize()
+            lo = i * STAGE_CHUNK
+            hi = min(nbytes, lo + STAGE_CHUNK)
+            np.copyto(st.views[b][: hi - lo], s8[lo:hi])
+        futs = {}
+        for i in range(min(STAGE_BUFS - 1, nch)):
+            futs[i] = st.pool.submit(fill, i)
+        for i in range(nch):
+            futs.pop(i).result()
+            b = i % STAGE_BUFS
+            lo = i * STAGE_CHUNK
+            hi = min(nbytes, lo + STAGE_CHUNK)
+            with torch.cuda.stream(stream):
+                d8[lo:hi].copy_(st.bufs[b][: hi - lo], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+            st.events[b] = ev
+            if i + STAGE_BUFS - 1 < nch:
+                futs[i + STAGE_BUFS - 1] = st.pool.submit(fill, i + STAGE_BUFS - 1)
 
 
 def is_pinned(t: torch.Tensor) -> bool:
@@ -209,7 +288,10 @@ class DevBSR:
         src = torch.from_numpy(m.values)
         pinned = is_pinned(src)
         if not overlap:
-            out.vals.copy_(src, non_blocking=pinned)
+            if pinned or src.numel() * 8 < STAGE_MIN_BYTES:
+                out.vals.copy_(src, non_blocking=pinned)
+            else:
+                staged_copy(out.vals, src, torch.cuda.current_stream(dev))
             return out
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
@@ -223,13 +305,14 @@ class DevBSR:
             return out
         import threading
 
-        def copy():
+        def copy():   # pageable: through the page-locked staging ring
+            staged_copy(out.vals, src, side)
             with torch.cuda.stream(side):
-                out.vals.copy_(src)
                 done.record(side)
         th = threading.Thread(target=copy, daemon=True)
         th.start()
         out._pending = (th, done)
+        out._side = side
         return out
 
     def upload_after(self, a: np.ndarray) -> torch.Tensor:
@@ -238,13 +321,26 @@ class DevBSR:
         it on the copy engine; ordered by wait_values()."""
         side = getattr(self, "_side", None)
         pending = getattr(self, "_pending", None)
-        if side is None or pending is None or pending[0] is not None:
-            return f64(a, self.vals.device)
         src = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
-        out = torch.empty(src.numel(), dtype=torch.float64, device=self.vals.device)
+        if side is None or pending is None:
+            return f64(a, self.vals.device)
+        th, _ = pending
+        done = torch.cuda.Event()
+        if th is not None:   # pageable values still being staged: queue behind them
+            import threading
+            out = torch.empty(src.numel(), dtype=torch.float64, device=self.vals.device)
+
+            def copy(prev=th):
+                prev.join()
+                staged_copy(out, src, side)
+                with torch.cuda.stream(side):
+                    done.record(side)
+            t2 = threading.Thread(target=copy, daemon=True)
+            t2.start()
+            self._pending = (t2, done)
+            return out
+        out = to_device(src, self.vals.device, side)
         with torch.cuda.stream(side):
-            out.copy_(src, non_blocking=is_pinned(src))
-            done = torch.cuda.Event()
             done.record(side)
         self._pending = (None, done)
         return out

@@ -83,3 +83,26 @@ def test_bicgstab_operator_reads_current_values():
         assert rep.converged
         r = g.rhs.data - P.spmv(a, x).data
         assert np.linalg.norm(r) <= 1e-10 * np.linalg.norm(g.rhs.data) * 1.01
+
+
+@pytest.mark.gpu
+def test_staged_pageable_upload_is_exact():
+    """Pageable host arrays reach the device through the page-locked staging
+    ring (paper_2309_11488_b200/_device.py staged_copy) byte for byte, for
+    sizes around the chunk size, and a pageable solve equals a pinned one."""
+    import torch
+
+    from paper_2309_11488_b200 import _device as D
+    rng = np.random.default_rng(4)
+    C = D.STAGE_CHUNK // 8
+    for n in (1, 1000, C - 1, C, C + 1, 3 * C + 17, 9 * C + 5):
+        a = rng.standard_normal(n)
+        d = D.to_device(torch.from_numpy(a), torch.device("cuda"))
+        torch.cuda.synchronize()
+        assert_array_equal(d.cpu().numpy(), a)
+    g = P.generate(P.GeneratorSpec(60, 50, 40, seed=2))
+    cfg = P.SolverConfig(backend=P.Backend.GRAPH_COLORED, stop=P.StoppingCriteria(1e-8, 200))
+    x1, r1 = P.solve_with_fallback(cfg, g.a, g.rhs)
+    x2, r2 = P.solve_with_fallback(cfg, P.pin_host(g.a), P.pin_host(g.rhs))
+    assert_array_equal(x1.data, x2.data)
+    assert r1.iterations == r2.iterations
