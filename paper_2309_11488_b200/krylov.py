@@ -262,13 +262,15 @@ class DeviceKrylov:
         fuse = False
         dw, wtabs = None, ()
         if wells is not None and not wells.is_empty:
-            from .wells import DeviceWells
-            cmap = None
+            # the input-order packing is cached on the WellSet (while its
+            # arrays are unchanged); the plan-order view is built on the device
+            dw0 = wells.device(b, n)
             if fact is not None and not fact._identity_perm:
-                cmap = np.asarray(fact.plan.permutation)   # old row -> plan row
-            dw = DeviceWells(wells, b, n, cell_map=cmap)
-            wtabs = dw.loop_tables(smap.row0[: smap.nslices].cpu().numpy(),
-                                   smap.nrows[: smap.nslices].cpu().numpy())
+                perm = fact.plan.device("permutation")   # old row -> plan row
+            else:
+                perm = torch.arange(n, dtype=torch.int32, device=dev)
+            dw = dw0.in_plan_order(perm, smap)
+            wtabs = dw.tables
             fuse_env = False   # the fused colour passes produce v before p^ is complete
         if sell is not None and fact is not None and sell is fact.a_sell:
             # U's colour-0 rows are this very layout (factor2c.cu): fusable by construction

@@ -139,12 +139,8 @@ class DeviceWells:
     """A WellSet packed for csrc/wells.cu (standard wells first, then
     multi-segment ones; C entries grouped by cell in that well order)."""
 
-    def __init__(self, wells: "WellSet", nb: int, num_cells: int, cell_map=None):
-        """``cell_map``: new row of each input cell (the plan's
-        ``permutation``, old row -> new row) when the device vectors are in
-        plan order."""
+    def __init__(self, wells: "WellSet", nb: int, num_cells: int):
         dev = D.require_cuda()
-        cmap = (lambda c: int(c)) if cell_map is None else (lambda c: int(cell_map[int(c)]))
         order = [(0, w) for w in wells.standard] + [(1, w) for w in wells.multisegment]
         kind, Ms, nseg, bptr, bcell, bseg, boff, bvals = [], [], [], [0], [], [], [], []
         doff, dvals, pivoff, piv, toff = [], [], [], [], []
@@ -173,14 +169,14 @@ class DeviceWells:
                 raise ShapeError("well too large for the device well kernels")
             kind.append(k); Ms.append(m); nseg.append(s)
             for e in range(len(cells_b)):
-                bcell.append(cmap(cells_b[e])); bseg.append(int(segs_b[e]))
+                bcell.append(int(cells_b[e])); bseg.append(int(segs_b[e]))
                 boff.append(bpos); bvals.append(blocks_b[e].reshape(-1)); bpos += m * n
             bptr.append(len(bcell))
             doff.append(dpos); dvals.append(d); dpos += d.size
             pivoff.append(ppos); ppos += (s * m if k == 1 else 0)
             toff.append(tpos)
             for e in range(len(cells_c)):
-                centries.append((cmap(cells_c[e]), wi, blocks_c[e].reshape(-1),
+                centries.append((int(cells_c[e]), wi, blocks_c[e].reshape(-1),
                                  tpos + int(segs_c[e]) * m, m))
             tpos += s * m
         centries.sort(key=lambda t: (t[0], t[1]))   # per cell, in well order
@@ -212,7 +208,6 @@ class DeviceWells:
                        cM=i32(cM), cvals=f64(cvals))
         self.nwells = len(order)
         self.nb = nb
-        self.cells_host = np.asarray(cells, dtype=np.int64)   # compact cell q -> row
         self.scratch = torch.empty(max(tpos, 1), dtype=torch.float64, device=dev)
         a = _WellsArgs()
         a.nwells, a.nb, a.ncells = self.nwells, nb, len(cells)
@@ -220,25 +215,41 @@ class DeviceWells:
             setattr(a, k, v.data_ptr())
         self._args = a
 
-    def loop_tables(self, row0: np.ndarray, nrows: np.ndarray):
-        """WellFix tables of the device Krylov loop (csrc/sell.cuh) for a
-        slice map (host row0/nrows): per slice the base of its 32 lane
-        entries or -1, per lane the compact cell index or -1; plus the
-        per-cell correction buffer."""
+    def in_plan_order(self, perm: torch.Tensor, smap) -> "DeviceWells":
+        """The same wells for device vectors in a plan's row order (perm: old
+        row -> plan row, device): the cell indices are remapped on the device
+        and the WellFix tables of the Krylov loop (csrc/sell.cuh) are built
+        there too -- no host round trip.  Compact cell q keeps its input-order
+        place; slice_tab[s] = 32 s when slice s holds a perforated row (else
+        -1), lane_tab[32 s + lane] = its compact cell (else -1)."""
+        out = DeviceWells.__new__(DeviceWells)
+        out.__dict__.update(self.__dict__)
         dev = self.scratch.device
-        ns = len(row0)
-        rows = self.cells_host
-        sl = np.searchsorted(row0, rows, side="right") - 1
-        lanes = rows - row0[sl]
-        if np.any(sl < 0) or np.any(lanes >= nrows[sl]):
-            raise ShapeError("well cell outside the slice map")
-        uniq, inv = np.unique(sl, return_inverse=True)
-        slice_tab = np.full(max(ns, 1), -1, dtype=np.int32)
-        slice_tab[uniq] = 32 * np.arange(uniq.size, dtype=np.int32)
-        lane_tab = np.full(max(32 * uniq.size, 1), -1, dtype=np.int32)
-        lane_tab[32 * inv + lanes] = np.arange(rows.size, dtype=np.int32)
-        corr = torch.empty(max(rows.size * self.nb, 1), dtype=torch.float64, device=dev)
-        return (torch.from_numpy(slice_tab).to(dev), torch.from_numpy(lane_tab).to(dev), corr)
+        perm = perm.to(torch.int64)
+        t = dict(self._t)
+        if self.nwells:
+            t["bcell"] = perm.index_select(0, self._t["bcell"].long()).to(torch.int32)
+            t["cells"] = perm.index_select(0, self._t["cells"].long()).to(torch.int32)
+        out._t = t
+        a = _WellsArgs()
+        a.nwells, a.nb, a.ncells = self.nwells, self.nb, self._args.ncells
+        for k, v in t.items():
+            setattr(a, k, v.data_ptr())
+        out._args = a
+        ns = smap.nslices
+        slice_tab = torch.full((max(ns, 1),), -1, dtype=torch.int32, device=dev)
+        lane_tab = torch.full((max(32 * ns, 1),), -1, dtype=torch.int32, device=dev)
+        nc = self._args.ncells
+        if self.nwells and nc:
+            rows = t["cells"][:nc].long()
+            row0 = smap.row0[:ns].long()
+            sl = torch.searchsorted(row0, rows, right=True) - 1
+            lane = rows - row0.index_select(0, sl)
+            slice_tab[sl] = (32 * sl).to(torch.int32)
+            lane_tab[32 * sl + lane] = torch.arange(nc, dtype=torch.int32, device=dev)
+        corr = torch.empty(max(nc * self.nb, 1), dtype=torch.float64, device=dev)
+        out.tables = (slice_tab, lane_tab, corr)
+        return out
 
     def apply(self, x: torch.Tensor, y: torch.Tensor):
         """y -= sum of the wells' C^T D^-1 B x (device vectors, input order)."""
