@@ -49,6 +49,9 @@ int launch_spmv_range(int b, int mode, int nparts, SliceMap map, int s0, int s1,
                       WellFix wf = WellFix{});
 int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, double* corr,
                       const int* done, cudaStream_t st);
+int launch_wells_patch(const b2s_wells* w, int goff1, const double* corr, double* v,
+                       const double* wv, int mode, double* p0, double* p1, const int* done,
+                       cudaStream_t st);
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
                     double* p1, const int* done, int* grid_out, cudaStream_t st,
@@ -532,8 +535,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // rows' ghost couplings come separately (b2s_mesh bnd_*)
   const bool mesh_local = mesh && mesh->bnd_ptr != nullptr;
   // separately applied wells: the well terms of p^ (s^) are computed right
-  // before each SpMV and subtracted in its epilogue (not with the fused
-  // colour passes, which produce v's colour-0 rows before p^ is complete)
+  // before each SpMV and subtracted in its epilogue; with the fused colour
+  // passes (which produce v's colour-0 rows before p^ is complete) the
+  // colour-0 rows are patched after the terms are known (k_wells_patch)
   const bool wells = a->wells != nullptr && a->wells->nwells > 0;
   if (wells && (mesh || !a->well_slice || !a->well_lane || !a->well_corr || !a->well_scratch))
     return mesh ? B2S_UNSUPPORTED : B2S_SHAPE;
@@ -541,7 +545,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   auto well_terms = [&](const double* xin, const int* dn, cudaStream_t q) {
     return wells ? launch_wells_corr(a->wells, xin, a->well_scratch, a->well_corr, dn, q) : 0;
   };
-  const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh_local) && !wells;
+  const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh_local);
   // fused vector passes on top of the fused colour passes: 7 kernels per
   // iteration instead of 9.  They move the same bytes (the separate p-update
   // largely hits L2), so they pay where the iteration is launch-bound --
@@ -723,8 +727,14 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                       nullptr, done, &g0, cs, pdl, kPreP, &inP);
       const Ctl ca{state, counters + 0, dev_done, kCtlAlpha, md};
       if (mesh) fork_halo(1, phat);
+      if (wells) {
+        well_terms(phat, done, cs);
+        launch_wells_patch(a->wells, a->goff1, a->well_corr, v, rhat, 1, pg + g0, nullptr, done, cs);
+        kernels += 3;
+        ++g0;
+      }
       launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
-                        done, mesh ? Ctl{} : ca, cs, pdl);
+                        done, mesh ? Ctl{} : ca, cs, pdl && !wells, wf);
       kernels += 3;
       if (mesh) {
         join_halo(1, phat);
@@ -740,8 +750,14 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                       done, &g0, cs, pdl, kPreS, &inS0);
       const Ctl co{state, counters + 2, dev_done, kCtlOmegaS, md, pss, gF + g0};
       if (mesh) fork_halo(2, shat);
+      if (wells) {
+        well_terms(shat, done, cs);
+        launch_wells_patch(a->wells, a->goff1, a->well_corr, t, s, 2, ptt + g0, pts + g0, done, cs);
+        kernels += 3;
+        ++g0;
+      }
       launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
-                        mesh ? Ctl{} : co, cs, pdl);
+                        mesh ? Ctl{} : co, cs, pdl && !wells, wf);
       kernels += 3;
       if (mesh) {
         join_halo(2, shat);
@@ -769,8 +785,15 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
         // a side branch of the graph, overlapped with the colour-1 SpMV (which
         // reads only local columns), and joins before the ghost correction
         if (mesh) fork_halo(1, phat);
+        if (wells) {   // p^ complete: the well terms, colour-0 rows patched
+          well_terms(phat, done, cs);
+          launch_wells_patch(a->wells, a->goff1, a->well_corr, v, rhat, 1, pg + g0, nullptr, done,
+                             cs);
+          kernels += 3;
+          ++g0;
+        }
         launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
-                          done, mesh ? Ctl{} : ca, cs, pdl);
+                          done, mesh ? Ctl{} : ca, cs, pdl && !wells, wf);
         kernels += 3;
         if (mesh) {   // the boundary rows' ghost couplings + alpha
           join_halo(1, phat);
@@ -809,8 +832,15 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                         &g0, cs, pdl);
         const Ctl co{state, counters + 2, dev_done, kCtlOmega, md};
         if (mesh) fork_halo(2, shat);
+        if (wells) {
+          well_terms(shat, done, cs);
+          launch_wells_patch(a->wells, a->goff1, a->well_corr, t, s, 2, ptt + g0, pts + g0, done,
+                             cs);
+          kernels += 3;
+          ++g0;
+        }
         launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
-                          mesh ? Ctl{} : co, cs, pdl);
+                          mesh ? Ctl{} : co, cs, pdl && !wells, wf);
         kernels += 3;
         if (mesh) {
           join_halo(2, shat);

@@ -160,6 +160,47 @@ int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, doub
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
+// Fused 2-colour passes with wells: the colour-0 rows of v (t) were written by
+// the fused backward+SpMV pass before p^ (s^) was complete, so their well
+// terms are subtracted here, after launch_wells_corr, together with the
+// change of that pass's dot-product partials (one CTA, one partial slot):
+// mode 1: gamma += r^.(v_new - v_old); mode 2: t.t += t_new^2 - t_old^2,
+// t.s += s.(t_new - t_old).  Colour-1 rows get theirs in the SpMV epilogue.
+__global__ void k_wells_patch(const int32_t* __restrict__ cells, int ncells, int nb, int goff1,
+                              const double* __restrict__ corr, double* v,
+                              const double* __restrict__ w, int mode, double* p0, double* p1,
+                              const int* done) {
+  __shared__ double red[8];
+  if (done && *done) return;
+  double a0 = 0.0, a1 = 0.0;
+  for (int q = threadIdx.x; q < ncells; q += blockDim.x) {
+    const long long row = cells[q];
+    if (row >= goff1) continue;
+    for (int c = 0; c < nb; ++c) {
+      const double vo = v[row * nb + c];
+      const double vn = vo - corr[(long long)q * nb + c];
+      v[row * nb + c] = vn;
+      const double wv = w[row * nb + c];
+      if (mode == 1) a0 += wv * vn - wv * vo;
+      else { a0 += vn * vn - vo * vo; a1 += wv * vn - wv * vo; }
+    }
+  }
+  const double t0 = block_sum(a0, red);
+  if (threadIdx.x == 0) *p0 = t0;
+  if (mode == 2) {
+    const double t1 = block_sum(a1, red);
+    if (threadIdx.x == 0) *p1 = t1;
+  }
+}
+
+int launch_wells_patch(const b2s_wells* w, int goff1, const double* corr, double* v,
+                       const double* wv, int mode, double* p0, double* p1, const int* done,
+                       cudaStream_t st) {
+  k_wells_patch<<<1, 256, 0, st>>>(w->cells, w->ncells, w->nb, goff1, corr, v, wv, mode, p0, p1,
+                                   done);
+  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+}
+
 }  // namespace b2s
 
 using namespace b2s;

@@ -271,7 +271,6 @@ class DeviceKrylov:
                 perm = torch.arange(n, dtype=torch.int32, device=dev)
             dw = dw0.in_plan_order(perm, smap)
             wtabs = dw.tables
-            fuse_env = False   # the fused colour passes produce v before p^ is complete
         if sell is not None and fact is not None and sell is fact.a_sell:
             # U's colour-0 rows are this very layout (factor2c.cu): fusable by construction
             fuse = fact.phased and fuse_env

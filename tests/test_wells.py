@@ -109,3 +109,27 @@ def test_wells_in_device_loop_match_host_loop(name, backend):
     from paper_2309_11488_b200.krylov import norm_array
     assert r_b.converged and r_b.gpu_launches > 0
     assert r_b.initial_norm == norm_array(g.rhs.data - op.apply_array(x0.data))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("vec", ["1", "0"])
+def test_wells_with_fused_colour_passes(monkeypatch, vec):
+    """2-colour plans keep the fused colour passes with separate wells: the
+    colour-0 rows of v / t get their well terms after p^ / s^ is complete
+    (k_wells_patch, partials corrected); same answer as the unfused loop."""
+    from paper_2309_11488_b200.krylov import DeviceKrylov
+    monkeypatch.setenv("B2S_FUSE_VEC", vec)
+    g = P.generate(P.GeneratorSpec(14, 12, 10, well_count=4, well_depth=6, seed=21))
+    fact = P.decompose(g.a, P.graph_color(g.a.pattern))
+    op = P.WellAugmentedOperator(g.a, g.wells)
+    stop = P.StoppingCriteria(1e-10, 200)
+    assert DeviceKrylov.build(g.a, fact, wells=g.wells).fuse
+    x_f, r_f = P.bicgstab(op, fact, g.rhs, stop=stop)
+    monkeypatch.setenv("B2S_FUSE", "0")
+    assert not DeviceKrylov.build(g.a, fact, wells=g.wells).fuse
+    x_u, r_u = P.bicgstab(op, fact, g.rhs, stop=stop)
+    assert r_f.converged and r_u.converged
+    assert abs(r_f.iterations - r_u.iterations) <= 0.5
+    assert np.linalg.norm(x_f.data - x_u.data) <= 1e-9 * np.linalg.norm(x_u.data)
+    y = op.apply_array(x_f.data)
+    assert np.linalg.norm(g.rhs.data - y) <= 1e-10 * np.linalg.norm(g.rhs.data) * 1.01
