@@ -50,6 +50,7 @@ struct GwDev {
 // meta word: -1 inactive, else plan row (bits 0..24) | entry mask << 25
 enum GwMask { kZm = 1, kYm = 2, kXm = 4, kXp = 8, kYp = 16, kZp = 32 };
 constexpr int kGwMetaBytes = 128;
+constexpr int kGwTl = 64;     // launches kept per tile by the debug timeline
 constexpr int kGwRingF = 8;   // forward ring stages (step records in flight)
 constexpr int kGwRingB = 6;   // backward ring stages
 constexpr int kGwEdgeAhead = 1;   // steps of look-ahead for the neighbour tiles' edge values
@@ -161,7 +162,30 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
   constexpr int R = DIR == 0 ? kGwRingF : kGwRingB;
   constexpr int VB = B * 32 * 8;   // bytes of one step's vector slice
   extern __shared__ __align__(128) char smem[];
-  if (done && *done) return;
+#ifdef B2S_GW_TRACE_BUILD
+  const unsigned long long t_in = global_ns_gw();
+#endif
+  // PDL: everything below reads the predecessors' results
+  griddep_wait();
+  griddep_launch();
+#ifdef B2S_GW_TRACE_BUILD
+  const unsigned long long t_w = global_ns_gw();
+  // per-launch timeline of this tile: [T] counters, then [T][kGwTl][4]
+  // (entry, after the grid-dependency wait, exit, direction)
+  auto tl_rec = [&](unsigned long long t_out) {
+    if (!g.trace || threadIdx.x != 0) return;
+    unsigned long long* tl = g.trace + 2LL * g.TX * g.TY * g.S;
+    const unsigned long long k = tl[blockIdx.x]++;
+    unsigned long long* r = tl + g.TX * g.TY + ((long long)blockIdx.x * kGwTl + k % kGwTl) * 4;
+    r[0] = t_in; r[1] = t_w; r[2] = t_out; r[3] = DIR;
+  };
+#endif
+  if (done && *done) {
+#ifdef B2S_GW_TRACE_BUILD
+    tl_rec(0);
+#endif
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const GwTile a = gw_tile(g, blockIdx.x, lane);
   const long long base = (long long)a.t * g.S;
@@ -340,11 +364,16 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
 #pragma unroll
     for (int c = 0; c < B; ++c) vv_c[c] = vv_n[c];
   }
+#ifdef B2S_GW_TRACE_BUILD
+  tl_rec(global_ns_gw());
+#endif
 }
 
 // the sweep's input in step order / its output back to plan order
 template <int B>
 __global__ void k_gw_gather(GwDev g, const double* __restrict__ r) {
+  griddep_wait();
+  griddep_launch();
   const long long total = (long long)g.TX * g.TY * g.S * 32;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
@@ -359,6 +388,8 @@ __global__ void k_gw_gather(GwDev g, const double* __restrict__ r) {
 
 template <int B>
 __global__ void k_gw_scatter(GwDev g, double* __restrict__ z) {
+  griddep_wait();
+  griddep_launch();
   const long long total = (long long)g.TX * g.TY * g.S * 32;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
@@ -463,38 +494,36 @@ inline int gw_smem_bytes(const GwDev& g, int b, int dir) {
 static_assert(2 * 8 * (kGwRingF > kGwRingB ? kGwRingF : kGwRingB) <= 128, "mbarriers fit");
 
 template <int B>
-int launch_gw_b(const GwHandle* h, const double* r, double* z, const int* done, cudaStream_t st) {
+int launch_gw_b(const GwHandle* h, const double* r, double* z, const int* done, cudaStream_t st,
+                bool pdl) {
   const GwDev& g = h->g;
   const long long total = (long long)g.TX * g.TY * g.S * 32;
   long long grid = (total + 255) / 256;
   if (grid > kSms * 16) grid = kSms * 16;
-  k_gw_gather<B><<<(int)grid, 256, 0, st>>>(g, r);
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeCooperative;   // tiles wait on each other: all resident
-  attr.val.cooperative = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g.TX * g.TY);
-  cfg.blockDim = dim3(32);
-  cfg.stream = st;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  cfg.dynamicSmemBytes = gw_smem_bytes(g, B, 0);
-  if (cudaLaunchKernelEx(&cfg, k_gw_sweep<B, 0>, g, done) != cudaSuccess) return B2S_CUDA_ERROR;
-  cfg.dynamicSmemBytes = gw_smem_bytes(g, B, 1);
-  if (cudaLaunchKernelEx(&cfg, k_gw_sweep<B, 1>, g, done) != cudaSuccess) return B2S_CUDA_ERROR;
-  k_gw_scatter<B><<<(int)grid, 256, 0, st>>>(g, z);
-  return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
+  // The tiles wait on each other, so the sweep grids must be co-resident:
+  // b2s_gw_create admits a grid only when it fits the occupancy bound, and
+  // a tile can only wait on tiles that are running or will get a slot once
+  // the (finite) predecessor grids drain.  Not a cooperative launch: those
+  // cannot overlap their predecessor (PDL) and add a drain in CUDA graphs.
+  if (launch_k(k_gw_gather<B>, dim3((int)grid), dim3(256), 0, st, pdl, g, r) != cudaSuccess ||
+      launch_k(k_gw_sweep<B, 0>, dim3(g.TX * g.TY), dim3(32), gw_smem_bytes(g, B, 0), st, pdl, g,
+               done) != cudaSuccess ||
+      launch_k(k_gw_sweep<B, 1>, dim3(g.TX * g.TY), dim3(32), gw_smem_bytes(g, B, 1), st, pdl, g,
+               done) != cudaSuccess ||
+      launch_k(k_gw_scatter<B>, dim3((int)grid), dim3(256), 0, st, pdl, g, z) != cudaSuccess)
+    return B2S_CUDA_ERROR;
+  return B2S_OK;
 }
 
 // z = U^-1 L^-1 r (plan order) with the wavefront kernels
 int launch_gw(int b, const void* handle, const double* r, double* z, const int* done,
-              cudaStream_t st) {
+              cudaStream_t st, bool pdl) {
   const GwHandle* h = reinterpret_cast<const GwHandle*>(handle);
   switch (b) {
-    case 1: return launch_gw_b<1>(h, r, z, done, st);
-    case 2: return launch_gw_b<2>(h, r, z, done, st);
-    case 3: return launch_gw_b<3>(h, r, z, done, st);
-    case 4: return launch_gw_b<4>(h, r, z, done, st);
+    case 1: return launch_gw_b<1>(h, r, z, done, st, pdl);
+    case 2: return launch_gw_b<2>(h, r, z, done, st, pdl);
+    case 3: return launch_gw_b<3>(h, r, z, done, st, pdl);
+    case 4: return launch_gw_b<4>(h, r, z, done, st, pdl);
     default: return B2S_UNSUPPORTED;
   }
 }
@@ -597,7 +626,10 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
   g.eS = d; d += nEy;
   h->src = reinterpret_cast<int32_t*>(d);
   g.trace = nullptr;
-  if (getenv("B2S_GW_TRACE") && cudaMalloc(&g.trace, 2 * slots * 8) != cudaSuccess) g.trace = nullptr;
+  const long long trace_words = 2 * slots + (long long)g.TX * g.TY * (1 + 4 * kGwTl);
+  if (getenv("B2S_GW_TRACE") && (cudaMalloc(&g.trace, trace_words * 8) != cudaSuccess ||
+                                 cudaMemset(g.trace, 0, trace_words * 8) != cudaSuccess))
+    g.trace = nullptr;
   h->b = b;
   h->n = n;
   int* bad = nullptr;
@@ -642,7 +674,9 @@ int b2s_gw_fill(void* handle, const double* lu, const double* inv, cudaStream_t 
 }
 
 // debug: copy the step end times [2][T][S] (ns, globaltimer) of the last
-// apply into host memory (B2S_GW_TRACE set at create); *count = 2*T*S
+// apply into host memory (B2S_GW_TRACE set at create); *count = 2*T*S.
+// cap >= 2*T*S + T*(1 + 4*64): also each tile's (entry, dependency wait
+// done, exit, direction) of its last 64 sweep launches (trace builds)
 int b2s_gw_trace(const void* handle, unsigned long long* host, long long cap, long long* count,
                  int* shape) {
   const GwHandle* h = reinterpret_cast<const GwHandle*>(handle);
@@ -650,7 +684,9 @@ int b2s_gw_trace(const void* handle, unsigned long long* host, long long cap, lo
   *count = n;
   shape[0] = h->g.TX; shape[1] = h->g.TY; shape[2] = h->g.S; shape[3] = h->g.wx; shape[4] = h->g.wy;
   if (!h->g.trace || cap < n) return B2S_SHAPE;
-  B2S_CHECK(cudaMemcpy(host, h->g.trace, n * 8, cudaMemcpyDeviceToHost));
+  // with room for it, also the per-launch timeline of a trace build
+  const long long tl = (long long)h->g.TX * h->g.TY * (1 + 4 * kGwTl);
+  B2S_CHECK(cudaMemcpy(host, h->g.trace, (cap >= n + tl ? n + tl : n) * 8, cudaMemcpyDeviceToHost));
   return B2S_OK;
 }
 
@@ -666,7 +702,7 @@ int b2s_gw_destroy(void* handle) {
 int b2s_gw_apply(int b, const void* handle, const double* r, double* z, cudaStream_t st) {
   if (!handle) return B2S_SHAPE;
   if (reinterpret_cast<const GwHandle*>(handle)->b != b) return B2S_SHAPE;
-  return launch_gw(b, handle, r, z, nullptr, st);
+  return launch_gw(b, handle, r, z, nullptr, st, false);
 }
 
 }  // extern "C"

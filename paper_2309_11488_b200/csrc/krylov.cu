@@ -22,10 +22,14 @@
 //   s^ = M^-1 s                                       (fwd + bwd sweep)
 //   t  = A s^,  (t.t, t.s) partials                   (SpMV epilogue)
 //   x += omega s^, r = s - omega t, |r|^2 and r^.r partials (1 kernel)
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include <cstring>
+#include <mutex>
+#include <vector>
 #include <cuda.h>
 
 #include "ctl.cuh"
@@ -62,7 +66,7 @@ int launch_fwd_pre(int b, int nparts, SliceMap map, int s0, int s1, Sell lo, con
 int launch_tiled(int b, const void* handle, const double* r, double* y, double* z, int reset_y,
                  const int* done, cudaStream_t st);
 int launch_gw(int b, const void* handle, const double* r, double* z, const int* done,
-              cudaStream_t st);
+              cudaStream_t st, bool pdl);
 
 // deterministic sum of np partials by one CTA of 256 threads
 __device__ double reduce_parts(const double* parts, int np, double* red) {
@@ -483,6 +487,33 @@ __global__ void k_all_finite(long long m, const double* __restrict__ a, int* bad
 
 using namespace b2s;
 
+namespace {
+// Mapped page-locked words the host polls (one 64-byte line each), kept for
+// the life of the process: a cudaHostAlloc + cudaFreeHost pair per solve
+// measured 1-36 ms of host time inside the solve once the process holds a
+// large device working set (the wavefront records), against 0.01 ms without.
+std::mutex g_done_mu;
+std::vector<int*> g_done_free;
+int* done_acquire() {
+  std::lock_guard<std::mutex> lk(g_done_mu);
+  if (g_done_free.empty()) {
+    char* blk = nullptr;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&blk), 4096,
+                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+      return nullptr;
+    for (int i = 4096 / 64 - 1; i >= 0; --i) g_done_free.push_back(reinterpret_cast<int*>(blk + 64 * i));
+  }
+  int* w = g_done_free.back();
+  g_done_free.pop_back();
+  return w;
+}
+void done_release(int* w) {
+  if (!w) return;
+  std::lock_guard<std::mutex> lk(g_done_mu);
+  g_done_free.push_back(w);
+}
+}  // namespace
+
 extern "C" {
 
 static long long vec_doubles_g(int n, int nghost, int b) {
@@ -511,6 +542,14 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if ((reinterpret_cast<uintptr_t>(a->x) | reinterpret_cast<uintptr_t>(a->rhs) |
        reinterpret_cast<uintptr_t>(a->work)) & 15)
     return B2S_SHAPE;
+  // B2S_SOLVE_TIMING=1: host-side phase times of each solve on stderr
+  static const bool tmg = getenv("B2S_SOLVE_TIMING") && getenv("B2S_SOLVE_TIMING")[0] == '1';
+  using clk = std::chrono::steady_clock;
+  clk::time_point tp[9];
+  int ntp = 0;
+  auto mark = [&]() { if (tmg && ntp < 9) tp[ntp++] = clk::now(); };
+  mark();
+  if (tmg) { cudaDeviceSynchronize(); mark(); }
   const long long m = (long long)a->n * a->b;
   const b2s_mesh* mesh = a->mesh;
   const int nghost = mesh ? mesh->nghost : 0;
@@ -593,11 +632,11 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // polls it `lag` replays behind the device
   int* host_done = nullptr;
   int* dev_done = nullptr;
-  if (cudaHostAlloc(&host_done, sizeof(int), cudaHostAllocMapped) != cudaSuccess)
-    return B2S_CUDA_ERROR;
+  if (!(host_done = done_acquire())) return B2S_CUDA_ERROR;
+  mark();
   *host_done = 0;
   if (cudaHostGetDevicePointer(&dev_done, host_done, 0) != cudaSuccess) {
-    cudaFreeHost(host_done);
+    done_release(host_done);
     return B2S_CUDA_ERROR;
   }
 
@@ -665,7 +704,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // ---- capture one iteration
   cudaStream_t cs;
   if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
-    cudaFreeHost(host_done);
+    done_release(host_done);
     return B2S_CUDA_ERROR;
   }
   cudaGraph_t graph = nullptr;
@@ -686,7 +725,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if (overlap && (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
                   cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
                   cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)) {
-    cudaFreeHost(host_done);
+    done_release(host_done);
     cudaStreamDestroy(cs);
     return B2S_CUDA_ERROR;
   }
@@ -702,6 +741,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     else halo(cs, which, vec, &state->done);
   };
   do {
+    mark();
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       status = B2S_CUDA_ERROR; break;
     }
@@ -807,7 +847,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
         kernels += 2 * (a->ngroups - 1);
       } else if (ilu) {
         if (a->refill_y && !a->gw) { fill_sentinel(m, y, cs); ++kernels; }
-        if (a->gw) launch_gw(a->b, a->gw, p, phat, done, cs);
+        if (a->gw) launch_gw(a->b, a->gw, p, phat, done, cs, pdl);
         else if (a->tiles) launch_tiled(a->b, a->tiles, p, y, phat, reset_y, done, cs);
         else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, p, y, phat, reset_y, a->sweep_flags,
                            tickets, done, cs);
@@ -854,7 +894,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
         kernels += 2 * (a->ngroups - 1);
       } else if (ilu) {
         if (a->refill_y && !a->gw) { fill_sentinel(m, y, cs); ++kernels; }
-        if (a->gw) launch_gw(a->b, a->gw, s, shat, done, cs);
+        if (a->gw) launch_gw(a->b, a->gw, s, shat, done, cs, pdl);
         else if (a->tiles) launch_tiled(a->b, a->tiles, s, y, shat, reset_y, done, cs);
         else launch_sweeps(a->b, a->kc, map, L, U, a->dinv_tiles, s, y, shat, reset_y, a->sweep_flags,
                            tickets, done, cs);
@@ -873,7 +913,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       ++kernels;
     }
     if (cudaStreamEndCapture(cs, &graph) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
+    mark();
     if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
+    mark();
     // shards sharing one GPU replay on their own (caller's) stream: every
     // extra stream risks sharing a hardware work queue with a peer's stream,
     // i.e. a false dependency behind a kernel that waits for that very peer
@@ -907,6 +949,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       }
     }
     res->graph_launches = launched;
+    mark();
     // leave the caller's stream ordered after the solve
     cudaEvent_t fin;
     cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
@@ -923,7 +966,17 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if (side) cudaStreamDestroy(side);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
-  if (host_done) cudaFreeHost(host_done);
+  mark();
+  done_release(host_done);
+  host_done = nullptr;
+  dev_done = nullptr;   // (read by reference in halo(): the late halo below must not set it)
+  mark();
+  if (tmg && ntp == 9) {
+    auto ms = [&](int i) { return std::chrono::duration<double, std::milli>(tp[i + 1] - tp[i]).count(); };
+    fprintf(stderr, "b2s_bicgstab host ms: device sync %.3f host alloc %.3f prologue %.3f capture %.3f "
+            "instantiate %.3f loop %.3f teardown %.3f free host %.3f (%d graphs)\n", ms(0), ms(1),
+            ms(2), ms(3), ms(4), ms(5), ms(6), ms(7), res->graph_launches);
+  }
   if (status != B2S_OK) return status;
   res->kernels_per_iteration = kernels;
 

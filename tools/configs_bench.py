@@ -25,20 +25,23 @@ CONFIGS = [   # (name, generator, tol)
     ("C2 46x112x22 masked", lambda: S.generate_masked(46, 112, 22, seed=2309), 1e-8),
     ("C3 92x224x17 heterogeneous", lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=1.0,
                                                                     diagonal_boost=1e-2), 1e-8),
+    ("C3s 92x224x17 heterogeneous sigma 2",
+     lambda: S.generate_heterogeneous(92, 224, 17, sigma_k=2.0, diagonal_boost=1e-2), 1e-8, 400),
     ("C4 100x100x100", lambda: P.generate(P.GeneratorSpec(100, 100, 100, seed=0)), 1e-8),
     ("C4 100x100x100", lambda: P.generate(P.GeneratorSpec(100, 100, 100, seed=0)), 1e-2),
     ("C4 100x100x100 boost 1e-2",
      lambda: P.generate(P.GeneratorSpec(100, 100, 100, diagonal_boost=1e-2, seed=0)), 1e-8),
 ]
 st = torch.cuda.current_stream()
-for name, make, tol in CONFIGS:
+for name, make, tol, *rest in CONFIGS:
+    maxit = rest[0] if rest else 200
     bnd = make()
     a = bnd.a
     bsr = D.DevBSR.upload(a)
     rhs = D.f64(bnd.rhs.data, bsr.vals.device)
     for backend in ("level", "color"):
         cfg = P.SolverConfig(backend=P.Backend.from_name(backend),
-                             stop=P.StoppingCriteria(tol, 200))
+                             stop=P.StoppingCriteria(tol, maxit))
         x = torch.zeros_like(rhs)
         times = []
         solver = None
@@ -58,7 +61,8 @@ for name, make, tol in CONFIGS:
         kr = sum(t[1] for t in times) / len(times)
         solver_groups = solver.plan.group_count
         solver = None
-        print(json.dumps({"config": name, "tol": tol, "cells": a.num_block_rows, "backend": backend,
+        print(json.dumps({"config": name, "tol": tol, "maxit": maxit, "cells": a.num_block_rows,
+                          "backend": backend,
                           "groups": solver_groups, "iterations": float(res.iterations),
                           "converged": bool(res.converged), "setup_ms": round(su, 3),
                           "krylov_ms": round(kr, 3), "solve_ms": round(su + kr, 3),
