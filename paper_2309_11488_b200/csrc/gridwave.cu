@@ -93,6 +93,21 @@ __device__ __forceinline__ void gw_bulk(void* dst, const void* src, unsigned byt
           gw_smem(dst)), "l"(src), "r"(bytes), "r"(gw_smem(b))
       : "memory");
 }
+// predicated stage refill (one lane issues, no branch around it): proxy
+// fence, expect_tx, and the record + vector bulk copies into the stage
+__device__ __forceinline__ void gw_refill(bool p, unsigned long long* bar, unsigned tx, void* d0,
+                                          const void* s0, unsigned n0, void* d1, const void* s1,
+                                          unsigned n1) {
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b64 st;\n setp.ne.b32 p, %0, 0;\n"
+      " @p fence.proxy.async.shared::cta;\n"
+      " @p mbarrier.arrive.expect_tx.shared::cta.b64 st, [%1], %2;\n"
+      " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%3], [%4], %5, [%1];\n"
+      " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%6], [%7], %8, [%1];\n"
+      "}" ::"r"((int)p), "r"(gw_smem(bar)), "r"(tx), "r"(gw_smem(d0)), "l"(s0), "r"(n0),
+      "r"(gw_smem(d1)), "l"(s1), "r"(n1)
+      : "memory");
+}
 __device__ __forceinline__ void gw_fence_proxy() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -281,9 +296,12 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
     if (j + 1 < a.St) load_step(j + 1, mt_n, bk_n, vv_n);
     // step j's stage is in registers: refill it with step j + R
     __syncwarp();
-    if (lane == 0 && j + R < a.St) {
-      gw_fence_proxy();
-      issue(j + R);
+    {
+      const int jj = j + R, q = jj % R;
+      const long long sr = DIR == 0 ? jj : a.St - 1 - jj;
+      char* dst = ring + q * stage;
+      gw_refill(lane == 0 && jj < a.St, full + q, (unsigned)stage, dst, rec + (base + sr) * (long long)rb,
+                (unsigned)rb, dst + rb, vin + (base + sr) * VB, (unsigned)VB);
     }
     const int mt = mt_c;
     const int mask = mt >= 0 ? (mt >> 25) : 0;
@@ -310,20 +328,25 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
       if (xok(s + dstep)) gw_load<B>(xin, ex);
       if (yok(s + dstep)) gw_load<B>(yin, ey);
     }
-    double acc[B], pr[B];
-#pragma unroll
-    for (int c = 0; c < B; ++c) acc[c] = 0.0;
-    // ascending plan columns: forward z-1, y-1, x-1; backward x+1, y+1, z+1
+    // ascending plan columns: forward z-1, y-1, x-1; backward x+1, y+1, z+1.
+    // Branch-free: an absent entry has a zero block (k_gw_vals) and its
+    // input is selected to zero, so its product is +0.0 and adding it leaves
+    // the sum unchanged (the sum starts at +0.0 and can never be -0.0) --
+    // the three products are independent chains the scheduler interleaves.
+    double pr[3][B];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const int bit = DIR == 0 ? (k == 0 ? mz : (k == 1 ? my : mx)) : (k == 0 ? mx : (k == 1 ? my : mz));
-      if (mask & bit) {
-        const double* dep = k == 0 ? (DIR == 0 ? prev : nx_) : (k == 1 ? ny_ : (DIR == 0 ? nx_ : prev));
-        matvec<B>(bk_c + k * BB, dep, pr);
+      const double* dep = k == 0 ? (DIR == 0 ? prev : nx_) : (k == 1 ? ny_ : (DIR == 0 ? nx_ : prev));
+      const bool on = (mask & bit) != 0;
+      double d[B];
 #pragma unroll
-        for (int c = 0; c < B; ++c) acc[c] += pr[c];
-      }
+      for (int c = 0; c < B; ++c) d[c] = on ? dep[c] : 0.0;
+      matvec<B>(bk_c + k * BB, d, pr[k]);
     }
+    double acc[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] = ((0.0 + pr[0][c]) + pr[1][c]) + pr[2][c];
     double outv[B];
     if (DIR == 0) {
 #pragma unroll

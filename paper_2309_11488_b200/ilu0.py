@@ -77,8 +77,14 @@ class Ilu0Factorization:
         self.gw = None           # b2s_gw_create handle (wavefront sweeps of grids), or None
         # few independent groups (colourings) and no same-group entries: the
         # phased sweeps, 2(G-1) plain passes, no polling (bit-identical)
+        # (2(G-1) kernels per application: they pay for colourings -- few wide
+        # groups -- while shallow level schedules of small systems are faster
+        # on the sync-free sweeps: 13x7x9 level 286 vs 141 us per BiCGStab
+        # iteration, 10x10x10 306 vs 141, profiles/r02/phased_small.txt)
+        ng = len(smap.gslice_host) - 1 if smap.gslice_host is not None else 0
         self.phased = (smap.gslice_host is not None and lower is not None and not lower.stale
                        and not (False if two_colour else upper.stale)
+                       and (ng <= 4 or self._n >= 4096 * ng)
                        and os.environ.get("B2S_PHASED", "1") != "0")
 
     # -- lazily materialised pieces of a 2-colour factorisation ----------------

@@ -615,8 +615,9 @@ def test_wavefront_sweeps_bit_identical(monkeypatch, dims, plan_kind):
     for flag in ("1", "0"):
         monkeypatch.setenv("B2S_GW", flag)
         f = P.decompose(a, plan)
-        # (few-level plans take the phased sweeps instead)
-        assert (f.gw is not None) == (flag == "1" and not f.phased)
+        # (plans of at most PHASED_MAX_GROUPS levels keep the other sweeps)
+        from paper_2309_11488_b200 import _device as D
+        assert (f.gw is not None) == (flag == "1" and plan.group_count > D.PHASED_MAX_GROUPS)
         z = f.apply(r).data
         x, rep = P.bicgstab(P.MatrixOperator(a), f, rhs, stop=P.StoppingCriteria(1e-10, 200))
         out[flag] = (z, x.data, rep)
