@@ -78,6 +78,22 @@ def f64(a: np.ndarray, dev) -> torch.Tensor:
     return to_device(src, dev)
 
 
+_UPLOAD: dict = {}
+
+
+def upload_stream(dev) -> torch.cuda.Stream:
+    """The device's copy stream for overlapped uploads, one per process.  (A
+    new stream per call leaked a caching-allocator segment per solve: blocks
+    allocated on a stream are only reused by that stream -- measured +23 MB
+    reserved and one cudaMalloc per C4 solve, tools/e2e_phases.py.)"""
+    dev = torch.device(dev)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    st = _UPLOAD.get(idx)
+    if st is None:
+        st = _UPLOAD[idx] = torch.cuda.Stream(device=dev)
+    return st
+
+
 def to_device(src: torch.Tensor, dev, stream=None) -> torch.Tensor:
     """Host tensor -> new device tensor: plain async DMA from page-locked
     memory, the staged path (staged_copy) for large pageable arrays."""
@@ -293,7 +309,7 @@ class DevBSR:
             else:
                 staged_copy(out.vals, src, torch.cuda.current_stream(dev))
             return out
-        side = torch.cuda.Stream(device=dev)
+        side = upload_stream(dev)
         side.wait_stream(torch.cuda.current_stream())
         done = torch.cuda.Event()
         if pinned:   # page-locked: the DMA is asynchronous, no helper thread needed
