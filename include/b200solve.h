@@ -91,7 +91,9 @@ int b2s_gather_rows(int n, int b, const int32_t* src, const double* in, double* 
                     cudaStream_t stream);
 
 /* int64 -> int32 index narrowing on the device; *overflow_host = 1 when a
- * value does not fit (the host raises). */
+ * value does not fit (the host raises; synchronises the stream).  A null
+ * overflow_host skips the check and the synchronisation: for indices already
+ * validated on the host (a SparsityPattern whose n and nnz fit int32). */
 int b2s_narrow_index(long long m, const int64_t* in, int32_t* out, int* overflow_host,
                      cudaStream_t stream);
 

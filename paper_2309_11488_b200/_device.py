@@ -129,6 +129,7 @@ class _Stager:
         self.events = [None] * STAGE_BUFS     # last DMA out of each buffer
         workers = int(os.environ.get("B2S_STAGE_THREADS", "0")) or \
             min(STAGE_BUFS - 1, max(2, (os.cpu_count() or 4) // 2))
+        self.workers = workers
         self.pool = cf.ThreadPoolExecutor(max_workers=workers)
         self.lock = threading.Lock()
 
@@ -146,15 +147,19 @@ def staged_copy(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
         st = _STAGERS[dev.index] = _Stager(dev)
     s8 = src.reshape(-1).view(torch.uint8).numpy()
     d8 = dst.reshape(-1).view(torch.uint8)
-    nch = (nbytes + STAGE_CHUNK - 1) // STAGE_CHUNK
+    # arrays of a few chunks are cut finer so every copy thread gets a share
+    # (an 8 MB array would otherwise be one thread's memcpy)
+    chunk = min(STAGE_CHUNK, max(1 << 20, -(-nbytes // st.workers)))
+    chunk = -(-chunk // 4096) * 4096
+    nch = (nbytes + chunk - 1) // chunk
     with st.lock:
         def fill(i):
             b = i % STAGE_BUFS
             ev = st.events[b]
             if ev is not None:
                 ev.synchronize()
-            lo = i * STAGE_CHUNK
-            hi = min(nbytes, lo + STAGE_CHUNK)
+            lo = i * chunk
+            hi = min(nbytes, lo + chunk)
             np.copyto(st.views[b][: hi - lo], s8[lo:hi])
         futs = {}
         for i in range(min(STAGE_BUFS - 1, nch)):
@@ -162,8 +167,8 @@ def staged_copy(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
         for i in range(nch):
             futs.pop(i).result()
             b = i % STAGE_BUFS
-            lo = i * STAGE_CHUNK
-            hi = min(nbytes, lo + STAGE_CHUNK)
+            lo = i * chunk
+            hi = min(nbytes, lo + chunk)
             with torch.cuda.stream(stream):
                 d8[lo:hi].copy_(st.bufs[b][: hi - lo], non_blocking=True)
                 ev = torch.cuda.Event()
@@ -290,45 +295,91 @@ class DevBSR:
 
     @classmethod
     def upload(cls, m, overlap: bool = False) -> "DevBSR":
-        """Pattern first, then the values.  With ``overlap`` the value copy
-        (the bulk of the bytes) runs on a side stream from a helper thread
-        while the caller goes on with pattern-only work (the analysis);
+        """Pattern first, then the values.  With ``overlap`` every host->device
+        copy runs back to back on the device's upload stream (page-locked
+        arrays: plain async DMA; pageable: the staging ring, from a helper
+        thread) and the caller goes on as soon as the pattern is queued: the
+        indices are narrowed on the current stream behind an event and the
+        pattern-only work (the analysis) overlaps the value copy;
         ``wait_values()`` orders the current stream after it."""
         m = m.as_block_row_major()
-        pat = DevPattern.upload(m.pattern)
-        dev = pat.rp.device
-        if not m.values.size:
-            return cls(pat, int(m.block_size), empty_f64(1, dev))
-        out = cls(pat, int(m.block_size), torch.empty(m.values.size, dtype=torch.float64,
-                                                       device=dev))
-        src = torch.from_numpy(m.values)
-        pinned = is_pinned(src)
-        if not overlap:
-            if pinned or src.numel() * 8 < STAGE_MIN_BYTES:
-                out.vals.copy_(src, non_blocking=pinned)
+        if not overlap or not m.values.size:
+            pat = DevPattern.upload(m.pattern)
+            dev = pat.rp.device
+            if not m.values.size:
+                return cls(pat, int(m.block_size), empty_f64(1, dev))
+            out = cls(pat, int(m.block_size), torch.empty(m.values.size, dtype=torch.float64,
+                                                           device=dev))
+            src = torch.from_numpy(m.values)
+            if is_pinned(src) or src.numel() * 8 < STAGE_MIN_BYTES:
+                out.vals.copy_(src, non_blocking=is_pinned(src))
             else:
                 staged_copy(out.vals, src, torch.cuda.current_stream(dev))
             return out
+        dev = require_cuda()
+        p = m.pattern
+        n = int(p.num_block_rows)
+        rp_h = np.ascontiguousarray(p.row_pointers, dtype=np.int64)
+        ci_h = np.ascontiguousarray(p.column_indices, dtype=np.int64)
+        nnz = int(rp_h[-1]) if n else 0
+        # a SparsityPattern checked 0 <= ci < n and 0 = rp[0] <= ... <= nnz at
+        # construction: with n and nnz inside int32 no index can overflow, so
+        # the narrowing needs no host read (DevPattern.upload keeps the check)
+        if n > _I32_MAX or nnz > _I32_MAX:
+            raise ValueError("index does not fit the device's int32 indices")
+        cur = torch.cuda.current_stream(dev)
         side = upload_stream(dev)
-        side.wait_stream(torch.cuda.current_stream())
-        done = torch.cuda.Event()
-        if pinned:   # page-locked: the DMA is asynchronous, no helper thread needed
-            with torch.cuda.stream(side):
-                out.vals.copy_(src, non_blocking=True)
-                done.record(side)
-            out._pending = (None, done)
-            out._side = side
-            return out
+        side.wait_stream(cur)
+        rp_raw = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        ci_raw = torch.empty(max(nnz, 1), dtype=torch.int64, device=dev)
+        vals = torch.empty(m.values.size, dtype=torch.float64, device=dev)
+        srcs = [(rp_raw, torch.from_numpy(rp_h)), (ci_raw[:nnz], torch.from_numpy(ci_h)),
+                (vals, torch.from_numpy(m.values))]
+        ev_pat, done = torch.cuda.Event(), torch.cuda.Event()
         import threading
+        queued = threading.Event()
 
-        def copy():   # pageable: through the page-locked staging ring
-            staged_copy(out.vals, src, side)
-            with torch.cuda.stream(side):
+        errors: list = []
+
+        def copy_all():
+            try:
+                for i, (dst, src) in enumerate(srcs):
+                    if src.numel() == 0:
+                        pass
+                    elif is_pinned(src) or src.numel() * src.element_size() < STAGE_MIN_BYTES:
+                        with torch.cuda.stream(side):
+                            dst.copy_(src, non_blocking=is_pinned(src))
+                    else:
+                        staged_copy(dst, src, side)
+                    if i == 1:
+                        ev_pat.record(side)
+                        queued.set()
                 done.record(side)
-        th = threading.Thread(target=copy, daemon=True)
-        th.start()
+            except BaseException as exc:   # re-raised by the caller / wait_values
+                errors.append(exc)
+            finally:
+                queued.set()
+        if all(is_pinned(src) for _, src in srcs if src.numel()):
+            copy_all()   # page-locked: every DMA is asynchronous, no helper thread
+            th = None
+        else:
+            th = threading.Thread(target=copy_all, daemon=True)
+            th.start()
+            queued.wait()
+        if errors:
+            if th is not None:
+                th.join()
+            raise errors[0]
+        cur.wait_event(ev_pat)
+        rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        check(lib().b2s_narrow_index(n + 1, ptr(rp_raw), ptr(rp), None, stream()), "narrow_index")
+        check(lib().b2s_narrow_index(nnz, ptr(ci_raw), ptr(ci), None, stream()), "narrow_index")
+        pat = DevPattern(n, nnz, rp, ci, grid_hint(n, rp_h, ci_h))
+        out = cls(pat, int(m.block_size), vals)
         out._pending = (th, done)
         out._side = side
+        out._errors = errors
         return out
 
     def upload_after(self, a: np.ndarray) -> torch.Tensor:
@@ -367,8 +418,11 @@ class DevBSR:
             th, ev = pending
             if th is not None:
                 th.join()
-            torch.cuda.current_stream().wait_event(ev)
             self._pending = None
+            errors = getattr(self, "_errors", None)
+            if errors:
+                raise errors[0]
+            torch.cuda.current_stream().wait_event(ev)
 
 
 def find_diagonal(p: DevPattern) -> torch.Tensor:

@@ -509,7 +509,7 @@ __global__ void k_narrow(long long m, const int64_t* __restrict__ in, int32_t* _
     bad |= (v > 0x7fffffffll || v < -0x7fffffffll);
     out[t] = (int32_t)v;
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(overflow, 1);
+  if (overflow && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(overflow, 1);
 }
 
 inline int grid_for(long long work, int threads = 256) {
@@ -888,9 +888,14 @@ int b2s_gather_rows(int n, int b, const int32_t* src, const double* in, double* 
 // fit.  Saves the host a conversion pass over the column indices.
 int b2s_narrow_index(long long m, const int64_t* in, int32_t* out, int* overflow_host,
                      cudaStream_t st) {
-  *overflow_host = 0;
+  if (overflow_host) *overflow_host = 0;
   if (m < 0) return B2S_SHAPE;
   if (m == 0) return B2S_OK;
+  if (!overflow_host) {   // validated indices: no flag, no synchronisation
+    k_narrow<<<grid_for(m), 256, 0, st>>>(m, in, out, nullptr);
+    B2S_LAUNCH_CHECK();
+    return B2S_OK;
+  }
   int* d = nullptr;
   B2S_CHECK(cudaMallocAsync(&d, sizeof(int), st));
   B2S_CHECK(cudaMemsetAsync(d, 0, sizeof(int), st));

@@ -95,7 +95,8 @@ def test_staged_pageable_upload_is_exact():
     from paper_2309_11488_b200 import _device as D
     rng = np.random.default_rng(4)
     C = D.STAGE_CHUNK // 8
-    for n in (1, 1000, C - 1, C, C + 1, 3 * C + 17, 9 * C + 5):
+    # (arrays of a few chunks are cut into >= 1 MB pieces: both regimes)
+    for n in (1, 1000, (1 << 17) - 1, (1 << 17) + 3, C - 1, C, C + 1, 3 * C + 17, 9 * C + 5):
         a = rng.standard_normal(n)
         d = D.to_device(torch.from_numpy(a), torch.device("cuda"))
         torch.cuda.synchronize()
