@@ -35,6 +35,7 @@ constexpr int kGwLanes = 32;
 struct GwDev {
   int nx, ny, nz, wx, wy, TX, TY, S;   // grid, tile shape, tiles, steps per tile (max)
   int rf, rb;            // bytes of one forward / backward step record
+  int shallow;           // 1: the shallow rings (more tiles co-resident), 0: the deep ones
   const char* recf;      // [T*S] forward records:  meta[32] int32 | L[3][BB][32] f64
   const char* recb;      // [T*S] backward records: meta[32] int32 | U[3][BB][32] | D[BB][32]
   double* rpk;           // [T*S][B][32]  the sweep's input in step order (k_gw_gather)
@@ -53,6 +54,10 @@ constexpr int kGwMetaBytes = 128;
 constexpr int kGwTl = 64;     // launches kept per tile by the debug timeline
 constexpr int kGwRingF = 8;   // forward ring stages (step records in flight)
 constexpr int kGwRingB = 6;   // backward ring stages
+// shallow rings for grids with more tiles than 3 per SM (the deep rings'
+// shared memory allows 3 CTAs per SM, these 7)
+constexpr int kGwRingFs = 4;
+constexpr int kGwRingBs = 3;
 constexpr int kGwEdgeAhead = 1;   // steps of look-ahead for the neighbour tiles' edge values
 
 __device__ __forceinline__ double gw_ld_relaxed(const double* p) {
@@ -171,10 +176,10 @@ __device__ __forceinline__ void gw_mbar_arrive(unsigned long long* b) {
 //
 // forward: y = r - L y, levels upward; backward: z = inv(U_ii) (y - U z),
 // levels downward.  DIR 0 / 1.
-template <int B, int DIR>
+template <int B, int DIR, int SH>
 __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
   constexpr int BB = B * B;
-  constexpr int R = DIR == 0 ? kGwRingF : kGwRingB;
+  constexpr int R = DIR == 0 ? (SH ? kGwRingFs : kGwRingF) : (SH ? kGwRingBs : kGwRingB);
   constexpr int VB = B * 32 * 8;   // bytes of one step's vector slice
   extern __shared__ __align__(128) char smem[];
 #ifdef B2S_GW_TRACE_BUILD
@@ -512,7 +517,8 @@ struct GwHandle {
 };
 
 inline int gw_smem_bytes(const GwDev& g, int b, int dir) {
-  return 128 + (dir == 0 ? kGwRingF : kGwRingB) * ((dir == 0 ? g.rf : g.rb) + b * 32 * 8);
+  const int r = dir == 0 ? (g.shallow ? kGwRingFs : kGwRingF) : (g.shallow ? kGwRingBs : kGwRingB);
+  return 128 + r * ((dir == 0 ? g.rf : g.rb) + b * 32 * 8);
 }
 static_assert(2 * 8 * (kGwRingF > kGwRingB ? kGwRingF : kGwRingB) <= 128, "mbarriers fit");
 
@@ -529,10 +535,10 @@ int launch_gw_b(const GwHandle* h, const double* r, double* z, const int* done, 
   // the (finite) predecessor grids drain.  Not a cooperative launch: those
   // cannot overlap their predecessor (PDL) and add a drain in CUDA graphs.
   if (launch_k(k_gw_gather<B>, dim3((int)grid), dim3(256), 0, st, pdl, g, r) != cudaSuccess ||
-      launch_k(k_gw_sweep<B, 0>, dim3(g.TX * g.TY), dim3(32), gw_smem_bytes(g, B, 0), st, pdl, g,
-               done) != cudaSuccess ||
-      launch_k(k_gw_sweep<B, 1>, dim3(g.TX * g.TY), dim3(32), gw_smem_bytes(g, B, 1), st, pdl, g,
-               done) != cudaSuccess ||
+      launch_k(g.shallow ? k_gw_sweep<B, 0, 1> : k_gw_sweep<B, 0, 0>, dim3(g.TX * g.TY), dim3(32),
+               gw_smem_bytes(g, B, 0), st, pdl, g, done) != cudaSuccess ||
+      launch_k(g.shallow ? k_gw_sweep<B, 1, 1> : k_gw_sweep<B, 1, 0>, dim3(g.TX * g.TY), dim3(32),
+               gw_smem_bytes(g, B, 1), st, pdl, g, done) != cudaSuccess ||
       launch_k(k_gw_scatter<B>, dim3((int)grid), dim3(256), 0, st, pdl, g, z) != cudaSuccess)
     return B2S_CUDA_ERROR;
   return B2S_OK;
@@ -551,19 +557,29 @@ int launch_gw(int b, const void* handle, const double* r, double* z, const int* 
   }
 }
 
-template <int B>
-int gw_configure(const GwDev& g, int* per_sm) {
+template <int B, int SH>
+int gw_configure_r(GwDev& g, int* per_sm) {
+  g.shallow = SH;
   const int s0 = gw_smem_bytes(g, B, 0), s1 = gw_smem_bytes(g, B, 1);
-  if (cudaFuncSetAttribute((const void*)k_gw_sweep<B, 0>,
+  if (cudaFuncSetAttribute((const void*)k_gw_sweep<B, 0, SH>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, s0) != cudaSuccess ||
-      cudaFuncSetAttribute((const void*)k_gw_sweep<B, 1>,
+      cudaFuncSetAttribute((const void*)k_gw_sweep<B, 1, SH>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, s1) != cudaSuccess)
     return B2S_CUDA_ERROR;
   int a = 0, c = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_gw_sweep<B, 0>, 32, s0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_gw_sweep<B, 1>, 32, s1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_gw_sweep<B, 0, SH>, 32, s0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_gw_sweep<B, 1, SH>, 32, s1);
   *per_sm = a < c ? a : c;
   return B2S_OK;
+}
+
+// the deep rings when the tiles fit them, else the shallow ones; per_sm is
+// the co-residency bound of the choice
+template <int B>
+int gw_configure(GwDev& g, long long tiles, int sms, int* per_sm) {
+  int rc = gw_configure_r<B, 0>(g, per_sm);
+  if (rc != B2S_OK || tiles <= (long long)*per_sm * sms) return rc;
+  return gw_configure_r<B, 1>(g, per_sm);
 }
 
 }  // namespace b2s
@@ -625,10 +641,10 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int rc = B2S_OK;
   switch (b) {
-    case 1: rc = gw_configure<1>(g, &per_sm); break;
-    case 2: rc = gw_configure<2>(g, &per_sm); break;
-    case 3: rc = gw_configure<3>(g, &per_sm); break;
-    default: rc = gw_configure<4>(g, &per_sm); break;
+    case 1: rc = gw_configure<1>(g, T, sms, &per_sm); break;
+    case 2: rc = gw_configure<2>(g, T, sms, &per_sm); break;
+    case 3: rc = gw_configure<3>(g, T, sms, &per_sm); break;
+    default: rc = gw_configure<4>(g, T, sms, &per_sm); break;
   }
   if (rc != B2S_OK) { delete h; return rc; }
   if (T > (long long)per_sm * sms) { delete h; return B2S_UNSUPPORTED; }

@@ -601,7 +601,8 @@ def test_fused_vector_passes_match_separate(monkeypatch, dims):
     assert out[("1", 1e-8)][1].iterations % 1.0 == 0.5   # the half-step exit is exercised
 
 
-@pytest.mark.parametrize("dims", [(20, 20, 10), (12, 10, 16), (8, 7, 5), (3, 40, 6), (33, 5, 4)])
+@pytest.mark.parametrize("dims", [(20, 20, 10), (12, 10, 16), (8, 7, 5), (3, 40, 6), (33, 5, 4),
+                                  (240, 64, 3)])   # (480 tiles: the shallow rings)
 @pytest.mark.parametrize("plan_kind", ["level", "sequential"])
 def test_wavefront_sweeps_bit_identical(monkeypatch, dims, plan_kind):
     """Natural-order grids: the wavefront sweeps (csrc/gridwave.cu, one warp
