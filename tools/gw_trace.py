@@ -21,7 +21,7 @@ from paper_2309_11488_b200 import ilu0 as I  # noqa: E402
 from paper_2309_11488_b200.bridge import plan_device  # noqa: E402
 
 dims = tuple(int(v) for v in sys.argv[1:4]) if len(sys.argv) >= 4 else (100, 100, 100)
-a = P.generate(P.GeneratorSpec(*dims, seed=0)).a
+a = P.generate(P.GeneratorSpec(*dims, block_size=int(os.environ.get("BS", "3")), seed=0)).a
 bsr = D.DevBSR.upload(a)
 plan = plan_device(P.Backend.LEVEL_SCHEDULED, bsr.pat)
 f = I.factor_device(a, plan, bsr)
@@ -37,7 +37,7 @@ if len(sys.argv) > 4 and sys.argv[4] == "krylov":
         x.zero_()
         solver.solve(D.f64(g.rhs.data, "cuda"), x, P.StoppingCriteria(1e-30, 12))
 else:
-    x = torch.rand(3 * a.num_block_rows, dtype=torch.float64, device="cuda")
+    x = torch.rand(a.block_size * a.num_block_rows, dtype=torch.float64, device="cuda")
     z = torch.empty_like(x)
     for _ in range(3):
         f.apply_device(x, z)

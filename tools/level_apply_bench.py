@@ -34,11 +34,11 @@ def ev_time(fn, reps=20, warm=3):
 
 
 dims = tuple(int(v) for v in sys.argv[1:4]) if len(sys.argv) >= 4 else (100, 100, 100)
-a = P.generate(P.GeneratorSpec(*dims, seed=0)).a
+a = P.generate(P.GeneratorSpec(*dims, block_size=int(os.environ.get("BS", "3")), seed=0)).a
 n, nnz = a.num_block_rows, a.pattern.num_blocks
 bsr = D.DevBSR.upload(a)
 plan = plan_device(P.Backend.LEVEL_SCHEDULED, bsr.pat)
-m = 3 * n
+m = a.block_size * n
 x = torch.rand(m, dtype=torch.float64, device="cuda")
 alg = (nnz - n) * 76 + 72 * n + 8 * (n + 1) + 96 * n
 out = {"dims": dims, "groups": plan.group_count}
