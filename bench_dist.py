@@ -65,8 +65,9 @@ def kernel_roofline(shard, peaks):
 def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_port_sample,
                     count_step_kernels=None):
     import paper_2309_11488_b200 as P
-    from paper_2309_11488_b200.distributed import (NcclComm, Shard, exchange_requests,
-                                                   generate_slab, slab_bounds,
+    from paper_2309_11488_b200._lib import PeerTimeout
+    from paper_2309_11488_b200.distributed import (MeshUnavailable, NcclComm, Shard,
+                                                   exchange_requests, generate_slab, slab_bounds,
                                                    solve_shard_mesh_dist, solve_shards)
     import numpy as np
 
@@ -94,6 +95,21 @@ def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_p
         if mesh:
             return solve_shard_mesh_dist(shard, stop, cache_key=args.backend)[0]
         return solve_shards([shard], comm, stop)[0]
+
+    # peer memory between these GPUs: if CUDA IPC / peer access is refused on
+    # any rank (agreed on by all ranks: MeshUnavailable) or a peer times out,
+    # the line is measured on the NCCL host loop and says so
+    mesh_fallback = None
+    if mesh:
+        try:
+            step()
+        except (MeshUnavailable, PeerTimeout) as exc:
+            mesh_fallback = f"{type(exc).__name__}: {exc}"[:300]
+            if getattr(shard, "mesh", None) is not None:
+                shard.mesh.close()
+                shard.mesh = None
+            mesh = False
+            comm = NcclComm(shard)
 
     def timed(fn, steps, warmup):
         for _ in range(warmup):
@@ -185,7 +201,7 @@ def run_distributed(args, world, rank, local, metric, unit, Clocks, peaks, cpu_p
                        "parallelism": f"slab x{world} ("
                                       + ("NVLink peer memory, device loop" if mesh else
                                          "NCCL, host loop") + ")"},
-            "iterations": iters, "solve_ms": ms, "clocks": clk,
+            "iterations": iters, "solve_ms": ms, "clocks": clk, "mesh_fallback": mesh_fallback,
             "e2e": None if e2e_ms is None else {
                 "value": n_total / (e2e_ms / 1e3) / 1e6, "unit": unit, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": world * ((slab.rows + 1) * 8 + slab.ci.size * 8

@@ -649,6 +649,11 @@ def nccl_solver(spec: GeneratorSpec, backend=Backend.LEVEL_SCHEDULED):
 # one node), or other shards on the same GPU (tests) -- the kernels are the
 # same either way.
 
+class MeshUnavailable(RuntimeError):
+    """CUDA IPC / peer access between the ranks' GPUs failed on some rank
+    (raised on every rank alike; the NCCL host loop still works)."""
+
+
 class MeshState:
     """Device buffers of one shard for ``b2s_bicgstab`` with a ``b2s_mesh``."""
 
@@ -850,25 +855,43 @@ def solve_shard_mesh_dist(shard: "Shard", stop: StoppingCriteria, x0=None, cache
         return out
     lib = D.lib()
     if ms.peers is None:
+        # every rank exports its buffers and opens every peer's; a failure on
+        # any rank (no IPC / peer access between these GPUs) is agreed on by
+        # all of them before anyone waits on a peer, and raised everywhere as
+        # MeshUnavailable -- the caller can fall back to the NCCL host loop
+        err = None
         mine = []
-        for p in ms.local_ptrs():
-            h = (C.c_ubyte * 64)()
-            off = C.c_longlong(0)
-            check(lib.b2s_ipc_handle(C.c_void_p(p), h, C.byref(off)), "ipc_handle")
-            mine.append((bytes(h), off.value))
+        try:
+            for p in ms.local_ptrs():
+                h = (C.c_ubyte * 64)()
+                off = C.c_longlong(0)
+                check(lib.b2s_ipc_handle(C.c_void_p(p), h, C.byref(off)), "ipc_handle")
+                mine.append((bytes(h), off.value))
+        except Exception as exc:
+            err = repr(exc)
         peers = [None] * world
-        for r, hs in gather((rank, mine)):
+        for r, hs in gather((rank, mine if err is None else None)):
             if r == rank:
                 peers[r] = ms.local_ptrs()
                 continue
             opened = []
-            for hb, off in hs:
-                out = C.c_void_p(None)
-                buf = (C.c_ubyte * 64).from_buffer_copy(hb)
-                check(lib.b2s_ipc_open(buf, off, C.byref(out)), "ipc_open")
-                opened.append(out.value)
-                ms.opened.append(out.value - off)
+            try:
+                if err is None and hs is not None:
+                    for hb, off in hs:
+                        out = C.c_void_p(None)
+                        buf = (C.c_ubyte * 64).from_buffer_copy(hb)
+                        check(lib.b2s_ipc_open(buf, off, C.byref(out)), "ipc_open")
+                        opened.append(out.value)
+                        ms.opened.append(out.value - off)
+            except Exception as exc:
+                err = repr(exc)
             peers[r] = opened
+        verdicts = gather((rank, err))
+        bad = [(r, e) for r, e in verdicts if e is not None]
+        if bad or any(h is None for h in peers):
+            ms.close()
+            raise MeshUnavailable("; ".join(f"rank {r}: {e}" for r, e in bad)
+                                  or "a peer could not export its buffers")
         ms.peers = peers
     key = ("owner_rows", cache_key)
     if getattr(shard, "_owner_rows_key", None) != key:

@@ -331,6 +331,21 @@ def test_nccl_comm_host_loop_two_processes():
     assert np.linalg.norm(np.asarray(got["x"]) - x) <= 1e-12 * np.linalg.norm(x)
 
 
+def test_mesh_unavailable_is_agreed_and_falls_back():
+    """One rank cannot open its peers' IPC buffers: every rank raises
+    MeshUnavailable at the same point (no rank is left waiting on a peer)
+    and the solve completes on the host-driven loop instead."""
+    import json
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = _torchrun([str(root / "tests" / "workers" / "mesh_worker.py"), "8,7,12", "color",
+                     "--same-gpu", "--fail-ipc-rank", "1"], 2)
+    assert out.returncode == 0, out.stderr[-3000:]
+    got = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert got["fallback"] and "rank 1" in got["fallback"]
+    assert all(got["converged"]) and got["rerun_bit_equal"]
+
+
 def test_nccl_comm_world_of_one_over_nccl():
     """The same host loop over a real NCCL communicator (one rank)."""
     from pathlib import Path

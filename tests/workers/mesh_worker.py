@@ -42,14 +42,23 @@ def main():
         return out
     exchange_requests([shard], world, gather)
     stop = P.StoppingCriteria(1e-8, 200)
-    reps, xs = [], []
+    if "--fail-ipc-rank" in sys.argv:   # this rank cannot open its peers' buffers
+        if rank == int(sys.argv[sys.argv.index("--fail-ipc-rank") + 1]):
+            from paper_2309_11488_b200 import _device as D
+            D.lib().b2s_ipc_open = lambda *args: 3
+    from paper_2309_11488_b200.distributed import MeshUnavailable, NcclComm, solve_shards
+    reps, xs, fallback = [], [], None
     for _ in range(2):
-        if "--comm-loop" in sys.argv:   # the host-driven loop over torch.distributed
-            from paper_2309_11488_b200.distributed import NcclComm, solve_shards
+        if "--comm-loop" in sys.argv or fallback:   # the host-driven loop
             rep, xv = solve_shards([shard], NcclComm(shard), stop)
             x = xv[0]
         else:
-            rep, x = solve_shard_mesh_dist(shard, stop, cache_key=backend)
+            try:
+                rep, x = solve_shard_mesh_dist(shard, stop, cache_key=backend)
+            except MeshUnavailable as exc:   # every rank lands here alike
+                fallback = str(exc)
+                rep, xv = solve_shards([shard], NcclComm(shard), stop)
+                x = xv[0]
         reps.append(rep)
         xs.append(x.cpu().numpy())
     allx = gather((rank, xs[0], xs[1]))
@@ -61,6 +70,7 @@ def main():
                           "converged": [bool(r.converged) for r in reps],
                           "initial_norm": reps[0].initial_norm,
                           "rerun_bit_equal": bool(np.array_equal(x0, x1)),
+                          "fallback": fallback,
                           "x": x0.tolist()}), flush=True)
     if getattr(shard, "mesh", None) is not None:
         shard.mesh.close()
