@@ -277,12 +277,14 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
   double prev[B];
 #pragma unroll
   for (int c = 0; c < B; ++c) prev[c] = 0.0;
-  // the step's record is moved from its ring stage into registers one step
-  // ahead, so the shared-memory latency overlaps the previous step's
-  // dependent FMAs, and the stage is refilled as soon as it is copied
+  // the step's record is read from its ring stage at the top of the step
+  // (independent loads, issued ahead of the dependent chain) and the stage
+  // refilled as soon as every lane has it.  (Copying it into registers one
+  // step ahead measured slower once the products were branch-free: 512 vs
+  // 497 us at C4 -- the register rotation costs ~60 moves per step.)
   constexpr int NB = DIR == 0 ? 3 * BB : 4 * BB;   // blocks per record (+ inv(U_ii))
-  int mt_c = -1, mt_n = -1;
-  double bk_c[NB], bk_n[NB], vv_c[B], vv_n[B];
+  int mt_c = -1;
+  double bk_c[NB], vv_c[B];
   auto load_step = [&](int j, int& mt, double (&bk)[NB], double (&vv)[B]) {
     const int q = j % R;
     gw_mbar_wait(full + q, (unsigned)((j / R) & 1));
@@ -295,10 +297,9 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
 #pragma unroll
     for (int c = 0; c < B; ++c) vv[c] = v[c * 32];
   };
-  if (a.St > 0) load_step(0, mt_c, bk_c, vv_c);
   for (int j = 0; j < a.St; ++j) {
     const int s = s0 + dstep * j;
-    if (j + 1 < a.St) load_step(j + 1, mt_n, bk_n, vv_n);
+    load_step(j, mt_c, bk_c, vv_c);
     // step j's stage is in registers: refill it with step j + R
     __syncwarp();
     {
@@ -386,11 +387,6 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
     if (g.trace && lane == 0)
       g.trace[(long long)DIR * g.TX * g.TY * g.S + base + s] = global_ns_gw();
 #endif
-    mt_c = mt_n;
-#pragma unroll
-    for (int e = 0; e < NB; ++e) bk_c[e] = bk_n[e];
-#pragma unroll
-    for (int c = 0; c < B; ++c) vv_c[c] = vv_n[c];
   }
 #ifdef B2S_GW_TRACE_BUILD
   tl_rec(global_ns_gw());
