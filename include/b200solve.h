@@ -171,6 +171,14 @@ int b2s_factor_2colour(int n, int b, int goff1, int s1, int nslices, const int32
                        const double* a_vals, const int32_t* l_sp, int32_t* l_cols,
                        double* l_vals, double* inv, double* udiag, double* dtiles,
                        int32_t* bad_row_host, cudaStream_t stream);
+/* The same, stream-ordered with no host read (the solve path checks later):
+ * flags_dev (device, 2 ints) holds {INT32_MAX, 0} on entry and receives
+ * {smallest singular plan row or INT32_MAX, 1 if not a 2-colour structure}. */
+int b2s_factor_2colour_async(int n, int b, int goff1, int s1, int nslices, const int32_t* row0,
+                             const int32_t* nrows, const int32_t* a_sp, const int32_t* a_cols,
+                             const double* a_vals, const int32_t* l_sp, int32_t* l_cols,
+                             double* l_vals, double* inv, double* udiag, double* dtiles,
+                             int* flags_dev, cudaStream_t stream);
 /* the plan-order CSR values of combined L\U from the layouts above (rp =
  * the plan-order row pointers); materialised only on request */
 int b2s_factor_2colour_combined(int n, int b, int goff1, int s1, const int32_t* rp,

@@ -86,6 +86,8 @@ SIGNATURES = {
     "b2s_sell_fill_src": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
     "b2s_factor_2colour": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                 _PI, _P]),
+    "b2s_factor_2colour_async": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                      _P, _P, _P, _P]),
     "b2s_factor_2colour_combined": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                          _P]),
     "b2s_slice_conflicts": (_I, [_I, _P, _P, _P, _P, _PI, _P]),

@@ -99,8 +99,9 @@ class DeviceSolver:
         self.krylov: DeviceKrylov | None = None
         self.plan: ParallelPlan | None = None
 
-    def setup(self, backend: Backend | None = None):
+    def setup(self, backend: Backend | None = None, two_colour: bool = True):
         backend = backend or self.cfg.backend
+        self._backend = backend
         with trace.phase("analysis"):
             self.plan = plan_device(backend, self.pre_bsr.pat)
             # the pattern-only part of the factorisation, also before the values
@@ -109,7 +110,12 @@ class DeviceSolver:
             self.pre_bsr.wait_values()   # values may still be in flight (overlapped upload)
             self.bsr.wait_values()
         with trace.phase("factor"):
-            self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr, prep)
+            # a 2-colour factorisation's pivot / structure check is read after
+            # the solve (solve() below): the host builds and launches the loop
+            # while the device factorises
+            self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr,
+                                      prep if two_colour else None, defer=True,
+                                      two_colour=two_colour)
         w = self.wells
         if self.pre_bsr is self.bsr and self.fact.a_sell is not None:
             # 2-colour factorisation: the operator's SELL layout already exists
@@ -130,7 +136,25 @@ class DeviceSolver:
     def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
               x0_zero: bool = False):
         """x (input order) holds x0 on entry and the solution on exit;
-        ``x0_zero``: the caller guarantees x == 0 (no initial guess)."""
+        ``x0_zero``: the caller guarantees x == 0 (no initial guess).
+        A deferred factorisation check runs after the loop: SingularPivot is
+        raised as decompose would have; a pattern that was not a 2-colour
+        structure after all is refactorised on the general path and solved
+        again from the same x0."""
+        pending = self.fact._deferred is not None
+        x_in = x.clone() if pending and not x0_zero else None
+        res = self._solve(rhs, x, stop, x0_zero)
+        if pending and self.fact.check_deferred():
+            self.setup(self._backend, two_colour=False)
+            if x_in is None:
+                x.zero_()
+            else:
+                x.copy_(x_in)
+            res = self._solve(rhs, x, stop, x0_zero)
+        return res
+
+    def _solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
+               x0_zero: bool = False):
         n, b = self.krylov.n, self.krylov.b
         f = self.fact
         if f._identity_perm:
@@ -222,15 +246,21 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         solver = DeviceSolver(a_sys, bsr, cfg, pre_bsr, pre_mat, wells=sep).setup()
         # the reported ||r0|| in the reference's order, beside the loop
         norm0 = RefNorm(_initial_residual(bsr, rhs, None if x0 is None else x0d, sep), n * bs)
-        _sync()
-        setup = time.perf_counter() - t0
-        t1 = time.perf_counter()
+        # no host synchronisation between setup and solve: the phases are
+        # timed on the device (the host queues the loop while the device is
+        # still factorising)
+        e_setup = torch.cuda.Event(enable_timing=True)
+        e_setup.record()
         xd = x0d.clone()
         with trace.phase("krylov"):
             res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None)
+        e_end = torch.cuda.Event(enable_timing=True)
+        e_end.record()
         _sync()
-        primary = _report(res, time.perf_counter() - t1, solver.plan.group_count, norm0.value())
-        primary.setup_elapsed = setup
+        setup = (time.perf_counter() - t0) - e_setup.elapsed_time(e_end) / 1e3
+        primary = _report(res, e_setup.elapsed_time(e_end) / 1e3, solver.plan.group_count,
+                          norm0.value())
+        primary.setup_elapsed = max(setup, 0.0)
         x = xd
     except SingularPivot as exc:
         primary = _failed_report(f"singular pivot in row {exc.row}")

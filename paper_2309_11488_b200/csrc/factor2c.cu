@@ -204,6 +204,22 @@ extern "C" {
 // B2S_SINGULAR_PIVOT with the smallest failing plan row in *bad_row_host;
 // B2S_UNSUPPORTED when the pattern is not a two-colour structure (caller
 // falls back to the general factorisation).
+static int f2c_launch(int n, int b, int goff1, int s1, int nslices, const int32_t* row0,
+                      const int32_t* nrows, const int32_t* a_sp, const int32_t* a_cols,
+                      const double* a_vals, const int32_t* l_sp, int32_t* l_cols, double* l_vals,
+                      double* inv, double* udiag, double* dtiles, int* flags, cudaStream_t st) {
+  SliceMap map{nslices, row0, nrows};
+  Sell a{a_sp, a_cols, a_vals};
+  Sell lo{l_sp, l_cols, l_vals};
+  switch (b) {
+    case 1: return f2c_factor_b<1>(n, goff1, s1, nslices, map, a, lo, inv, udiag, dtiles, flags, st);
+    case 2: return f2c_factor_b<2>(n, goff1, s1, nslices, map, a, lo, inv, udiag, dtiles, flags, st);
+    case 3: return f2c_factor_b<3>(n, goff1, s1, nslices, map, a, lo, inv, udiag, dtiles, flags, st);
+    case 4: return f2c_factor_b<4>(n, goff1, s1, nslices, map, a, lo, inv, udiag, dtiles, flags, st);
+  }
+  return B2S_UNSUPPORTED;
+}
+
 int b2s_factor_2colour(int n, int b, int goff1, int s1, int nslices, const int32_t* row0,
                        const int32_t* nrows, const int32_t* a_sp, const int32_t* a_cols,
                        const double* a_vals, const int32_t* l_sp, int32_t* l_cols,
@@ -216,16 +232,8 @@ int b2s_factor_2colour(int n, int b, int goff1, int s1, int nslices, const int32
   B2S_CHECK(cudaMallocAsync(&flags, 2 * sizeof(int), st));
   const int init[2] = {0x7fffffff, 0};
   B2S_CHECK(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, st));
-  SliceMap map{nslices, row0, nrows};
-  Sell a{a_sp, a_cols, a_vals};
-  Sell lo{l_sp, l_cols, l_vals};
-  int rc = B2S_OK;
-  switch (b) {
-    case 1: rc = f2c_factor_b<1>(n, goff1, s1, nslices, map, a, lo, inv, udiag, dtiles, flags, st); break;
-    case 2: rc = f2c_factor_b<2>(n, goff1, s1, nslices, map, a, lo, inv, udiag, dtiles, flags, st); break;
-    case 3: rc = f2c_factor_b<3>(n, goff1, s1, nslices, map, a, lo, inv, udiag, dtiles, flags, st); break;
-    case 4: rc = f2c_factor_b<4>(n, goff1, s1, nslices, map, a, lo, inv, udiag, dtiles, flags, st); break;
-  }
+  const int rc = f2c_launch(n, b, goff1, s1, nslices, row0, nrows, a_sp, a_cols, a_vals, l_sp,
+                            l_cols, l_vals, inv, udiag, dtiles, flags, st);
   if (rc) return rc;
   int h[2];
   B2S_CHECK(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -237,6 +245,21 @@ int b2s_factor_2colour(int n, int b, int goff1, int s1, int nslices, const int32
     return B2S_SINGULAR_PIVOT;
   }
   return B2S_OK;
+}
+
+// The same without the host read: flags_dev (2 ints, device) must hold
+// {INT32_MAX, 0} on entry and receives {smallest singular plan row or
+// INT32_MAX, 1 if the pattern is not a two-colour structure}; the caller
+// reads them at a later synchronisation (stream-ordered, no sync here).
+int b2s_factor_2colour_async(int n, int b, int goff1, int s1, int nslices, const int32_t* row0,
+                             const int32_t* nrows, const int32_t* a_sp, const int32_t* a_cols,
+                             const double* a_vals, const int32_t* l_sp, int32_t* l_cols,
+                             double* l_vals, double* inv, double* udiag, double* dtiles,
+                             int* flags_dev, cudaStream_t st) {
+  if (n <= 0 || b < 1 || b > 4 || goff1 < 0 || goff1 > n || s1 < 0 || s1 > nslices || !flags_dev)
+    return B2S_SHAPE;
+  return f2c_launch(n, b, goff1, s1, nslices, row0, nrows, a_sp, a_cols, a_vals, l_sp, l_cols,
+                    l_vals, inv, udiag, dtiles, flags_dev, st);
 }
 
 int b2s_factor_2colour_combined(int n, int b, int goff1, int s1, const int32_t* rp,

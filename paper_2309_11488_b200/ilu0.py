@@ -33,6 +33,9 @@ def _kc(width: int) -> int:
     return 2 if width <= 2 else 4
 
 
+_I32_MAX = 2 ** 31 - 1
+
+
 class Ilu0Factorization:
     """Combined L/U factors (plan order), inverse diagonals and the plan,
     resident on the GPU (bs/ilu0.py:59-142)."""
@@ -45,6 +48,7 @@ class Ilu0Factorization:
         self._n = n
         self._lu = lu
         self._invd = invd
+        self._deferred = None    # device flags of a not yet checked 2-colour factorisation
         self.smap = smap
         self._lower = lower
         self._upper = upper
@@ -86,6 +90,21 @@ class Ilu0Factorization:
                        and not (False if two_colour else upper.stale)
                        and (ng <= 4 or self._n >= 4096 * ng)
                        and os.environ.get("B2S_PHASED", "1") != "0")
+
+    def check_deferred(self) -> bool:
+        """Read the flags of a deferred 2-colour factorisation (synchronises):
+        raises SingularPivot (input numbering, as decompose would have); True
+        if the pattern was not a 2-colour structure after all (the caller
+        refactorises with the general path).  False when nothing is pending."""
+        fl, self._deferred = self._deferred, None
+        if fl is None:
+            return False
+        bad, unsupported = (int(v) for v in fl.cpu().tolist())
+        if unsupported:
+            return True
+        if bad != _I32_MAX:
+            raise SingularPivot(int(self.plan.device("inverse_permutation")[bad].item()))
+        return False
 
     # -- lazily materialised pieces of a 2-colour factorisation ----------------
     @property
@@ -263,10 +282,14 @@ def prepare_two_colour(a: BlockMatrix, plan: ParallelPlan, pat: "D.DevPattern"):
             "s1": int(smap.gslice_host[1]), "goff1": int(smap.goff1)}
 
 
-def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", prep=None):
+def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", prep=None,
+                       defer: bool = False):
     """2-colour plans: operator layout + factors straight from the input
     values (csrc/factor2c.cu); None if the pattern is not a 2-colour
-    structure (then the general path runs)."""
+    structure (then the general path runs).  ``defer``: no host read here --
+    the singular-pivot / structure flags stay on the device until
+    ``check_deferred()`` (the solve path reads them after its loop, so the
+    host prepares the Krylov loop while the device factorises)."""
     n, b = a.num_block_rows, a.block_size
     prep = prep or prepare_two_colour(a, plan, bsr.pat)
     if prep is None:
@@ -275,6 +298,19 @@ def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", prep
     inv, udiag, dtiles = prep["inv"], prep["udiag"], prep["dtiles"]
     s1, goff1 = prep["s1"], prep["goff1"]
     a_sell.fill_from(smap, D.DevBSR(prep["pattern"], b, bsr.vals), 0, prep["src"])
+    tc = {"pattern": prep["pattern"], "a_sell": a_sell, "udiag": udiag, "goff1": goff1, "s1": s1}
+    if defer:
+        flags = torch.full((2,), _I32_MAX, dtype=torch.int32, device=inv.device)
+        flags[1:].zero_()
+        check(D.lib().b2s_factor_2colour_async(
+            n, b, goff1, s1, smap.nslices, D.ptr(smap.row0), D.ptr(smap.nrows),
+            D.ptr(a_sell.sp), D.ptr(a_sell.cols), D.ptr(a_sell.vals), D.ptr(lower.sp),
+            D.ptr(lower.cols), D.ptr(lower.vals), D.ptr(inv), D.ptr(udiag), D.ptr(dtiles),
+            D.ptr(flags), D.stream()), "factor_2colour_async")
+        f = Ilu0Factorization(plan, b, n, None, inv, smap, lower, None, dtiles, False, a, None,
+                              two_colour=tc)
+        f._deferred = flags
+        return f
     bad = C.c_int32(-1)
     rc = D.lib().b2s_factor_2colour(n, b, goff1, s1, smap.nslices, D.ptr(smap.row0),
                                     D.ptr(smap.nrows), D.ptr(a_sell.sp), D.ptr(a_sell.cols),
@@ -286,15 +322,17 @@ def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", prep
     if rc == SINGULAR_PIVOT:
         raise SingularPivot(int(plan.device("inverse_permutation")[int(bad.value)].item()))
     check(rc, "factor_2colour")
-    tc = {"pattern": prep["pattern"], "a_sell": a_sell, "udiag": udiag, "goff1": goff1, "s1": s1}
     return Ilu0Factorization(plan, b, n, None, inv, smap, lower, None, dtiles, False, a, None,
                              two_colour=tc)
 
 
 def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
-                  prep=None) -> Ilu0Factorization:
+                  prep=None, defer: bool = False, two_colour: bool = True) -> Ilu0Factorization:
     """``decompose`` on an (optionally pre-uploaded) matrix; ``prep`` is
-    ``prepare_two_colour``'s pattern-only half when the caller ran it early."""
+    ``prepare_two_colour``'s pattern-only half when the caller ran it early.
+    ``defer``: see ``_factor_two_colour`` (the caller must call
+    ``check_deferred()`` before trusting any result); ``two_colour=False``
+    forces the general factorisation."""
     a = a.as_block_row_major()
     n = a.num_block_rows
     if plan.num_rows != n:
@@ -302,7 +340,7 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
     b = a.block_size
     bsr = bsr or D.DevBSR.upload(a)
     dev = bsr.pat.rp.device
-    f = _factor_two_colour(a, plan, bsr, prep)
+    f = _factor_two_colour(a, plan, bsr, prep, defer) if two_colour else None
     if f is not None:
         return f
     D.find_diagonal(bsr.pat)                       # MissingDiagonal(first row)
