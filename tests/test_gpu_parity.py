@@ -205,6 +205,34 @@ def test_starved_budget_triggers_sequential_fallback():
     assert rep.group_count == bundle.a.num_block_rows
 
 
+def test_two_colour_singular_pivot_through_the_deferred_check():
+    """A pivot that is exactly zero only under the 2-colour ordering: decompose
+    raises SingularPivot(input row) on the spot, and solve_with_fallback --
+    whose factorisation check runs after the loop (deferred) -- reports the
+    primary failure and converges on the sequential fallback."""
+    n = 6
+    rows = {i: [i] for i in range(n)}
+    for i in range(n - 1):
+        rows[i + 1].append(i)
+        rows[i].append(i + 1)
+    p = pattern_from_rows(rows, n)
+    vals = np.zeros(p.num_blocks)
+    for k, (i, j) in enumerate(p):
+        vals[k] = 4.0 if i == j else -1.0
+    vals[p.position(3, 3)] = 0.5     # 0.5 - (1/4 + 1/4) = 0 with rows 2, 4 eliminated first
+    a = P.BlockMatrix(p, 1, vals)
+    plan = P.graph_color(p)
+    assert plan.group_count == 2
+    with pytest.raises(P.SingularPivot) as err:
+        P.decompose(a, plan)
+    assert err.value.row == 3
+    b = P.BlockVector(np.arange(1.0, n + 1.0), 1)
+    x, rep = P.solve_with_fallback(P.SolverConfig(backend=P.Backend.GRAPH_COLORED), a, b)
+    assert rep.fallback_used and rep.converged
+    r = b.data - P.spmv(a, x).data
+    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b.data) * 1.01
+
+
 def test_singular_system_raises_solve_failed():
     m = P.BlockMatrix.from_blocks([(0, 0, np.zeros((2, 2))), (1, 1, np.eye(2))])
     with pytest.raises(P.SolveFailed) as err:
