@@ -156,6 +156,18 @@ int b2s_spmv(int b, int mode, int nparts, int nslices, const int32_t* row0,
 int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_t* nrows,
                     const int32_t* rp, const int32_t* ci, const int32_t* diag, double* vals,
                     double* inv_diag, int32_t* bad_row_host, cudaStream_t stream);
+/* The same in two halves.  Symbolic (pattern only; may synchronise): the
+ * update pairs of every lower entry behind an opaque handle, freed
+ * stream-ordered by b2s_ilu0_symbolic_free.  Numeric: values in place; with
+ * bad_dev (device int, INT32_MAX on entry) the smallest failing permuted row
+ * is left there with no host read, else as b2s_ilu0_factor. */
+int b2s_ilu0_symbolic(int n, int b, const int32_t* rp, const int32_t* ci, const int32_t* diag,
+                      void** handle, cudaStream_t stream);
+int b2s_ilu0_numeric(const void* handle, int b, int nslices, const int32_t* row0,
+                     const int32_t* nrows, const int32_t* rp, const int32_t* ci,
+                     const int32_t* diag, double* vals, double* inv_diag, int* bad_dev,
+                     int32_t* bad_row_host, cudaStream_t stream);
+int b2s_ilu0_symbolic_free(void* handle, cudaStream_t stream);
 
 /* decompose (bs/ilu0.py:145-201) for a plan of two independent groups
  * (a 2-colouring), straight into SELL layouts on the group-aligned slice map

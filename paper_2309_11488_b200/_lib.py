@@ -93,6 +93,9 @@ SIGNATURES = {
     "b2s_slice_conflicts": (_I, [_I, _P, _P, _P, _P, _PI, _P]),
     "b2s_spmv": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "b2s_ilu0_factor": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _PI, _P]),
+    "b2s_ilu0_symbolic": (_I, [_I, _I, _P, _P, _P, C.POINTER(C.c_void_p), _P]),
+    "b2s_ilu0_numeric": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _PI, _P]),
+    "b2s_ilu0_symbolic_free": (_I, [_P, _P]),
     "b2s_ilu0_apply": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                             _I, _I, _P, _P]),
     "b2s_fill_sentinel": (_I, [_LL, _P, _P]),

@@ -27,7 +27,7 @@ from . import trace
 from .analysis import (ParallelPlan, Strategy, _device_plan, sequential_plan)
 from .blockcore import BlockMatrix, BlockVector
 from .errors import SingularPivot, SolveFailed
-from .ilu0 import Ilu0Factorization, factor_device, prepare_two_colour
+from .ilu0 import Ilu0Factorization, factor_device, prepare_general, prepare_two_colour
 from .krylov import (DEFAULT_MAX_ITERATIONS, DeviceKrylov, RefNorm, SolveReport,
                      StoppingCriteria, _REASONS)
 from .wells import WellMode, WellSet, fold_into_matrix
@@ -99,13 +99,19 @@ class DeviceSolver:
         self.krylov: DeviceKrylov | None = None
         self.plan: ParallelPlan | None = None
 
-    def setup(self, backend: Backend | None = None, two_colour: bool = True):
+    def setup(self, backend: Backend | None = None, two_colour: bool = True,
+              defer: bool = True):
+        """``defer``: the factorisation's pivot check is read after the solve
+        (solve() raises SingularPivot then); False raises it here."""
         backend = backend or self.cfg.backend
         self._backend = backend
         with trace.phase("analysis"):
             self.plan = plan_device(backend, self.pre_bsr.pat)
             # the pattern-only part of the factorisation, also before the values
-            prep = prepare_two_colour(self.pre_matrix, self.plan, self.pre_bsr.pat)
+            prep = (prepare_two_colour(self.pre_matrix, self.plan, self.pre_bsr.pat)
+                    if two_colour else None)
+            prep_g = (prepare_general(self.pre_matrix, self.plan, self.pre_bsr.pat)
+                      if prep is None else None)
         with trace.phase("wait_values"):
             self.pre_bsr.wait_values()   # values may still be in flight (overlapped upload)
             self.bsr.wait_values()
@@ -113,9 +119,8 @@ class DeviceSolver:
             # a 2-colour factorisation's pivot / structure check is read after
             # the solve (solve() below): the host builds and launches the loop
             # while the device factorises
-            self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr,
-                                      prep if two_colour else None, defer=True,
-                                      two_colour=two_colour)
+            self.fact = factor_device(self.pre_matrix, self.plan, self.pre_bsr, prep, defer=defer,
+                                      two_colour=two_colour, prep_general=prep_g)
         w = self.wells
         if self.pre_bsr is self.bsr and self.fact.a_sell is not None:
             # 2-colour factorisation: the operator's SELL layout already exists
@@ -145,7 +150,7 @@ class DeviceSolver:
         x_in = x.clone() if pending and not x0_zero else None
         res = self._solve(rhs, x, stop, x0_zero)
         if pending and self.fact.check_deferred():
-            self.setup(self._backend, two_colour=False)
+            self.setup(self._backend, two_colour=False, defer=False)
             if x_in is None:
                 x.zero_()
             else:
@@ -277,7 +282,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
                                max(cfg.stop.max_iterations, DEFAULT_MAX_ITERATIONS))
     fcfg = SolverConfig(Backend.REFERENCE_SEQUENTIAL, 0, cfg.well_mode, fb_stop)
     try:
-        fb = DeviceSolver(a_sys, bsr, fcfg, wells=sep).setup()
+        fb = DeviceSolver(a_sys, bsr, fcfg, wells=sep).setup(defer=False)
     except SingularPivot as exc:
         fb_report = _failed_report(f"singular pivot in row {exc.row}")
         fb_report.fallback_used = True

@@ -301,9 +301,124 @@ using namespace b2s;
 
 extern "C" {
 
-// Factor the permuted block-CSR matrix in place (values become combined
+// Symbolic half of the factorisation (pattern only): the update pairs of
+// every lower entry and the rows whose pivots are all "simple".  Allocates
+// stream-ordered device buffers behind an opaque handle (freed by
+// b2s_ilu0_symbolic_free); synchronises for the pair count.
+struct IluSym {
+  int n = 0, nnz = 0, npairs = 0, all_simple = 0;
+  int32_t* pptr = nullptr;
+  int2* pairs = nullptr;
+  int8_t* simple = nullptr;
+};
+
+int b2s_ilu0_symbolic(int n, int b, const int32_t* rp, const int32_t* ci, const int32_t* diag,
+                      void** handle, cudaStream_t st) {
+  *handle = nullptr;
+  if (n < 0 || b < 1) return B2S_SHAPE;
+  if (b > 4) return B2S_UNSUPPORTED;
+  IluSym* h = new IluSym();
+  h->n = n;
+  if (n == 0) { *handle = h; return B2S_OK; }
+  int32_t nnz = 0;
+  B2S_CHECK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  h->nnz = nnz;
+  int32_t* cnt = nullptr;
+  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (nnz + 1), st));
+  B2S_CHECK(cudaMallocAsync(&h->pptr, sizeof(int32_t) * (nnz + 1), st));
+  B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nnz + 1), st));
+  k_factor_pairs<<<grid_rows(n), 256, 0, st>>>(n, rp, ci, diag, cnt, nullptr, nullptr);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, h->pptr, nnz + 1, st);
+  void* tmp = nullptr;
+  B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, h->pptr, nnz + 1, st);
+  int32_t npairs = 0;
+  B2S_CHECK(cudaMemcpyAsync(&npairs, h->pptr + nnz, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  h->npairs = npairs;
+  B2S_CHECK(cudaMallocAsync(&h->pairs, sizeof(int2) * (npairs > 0 ? npairs : 1), st));
+  k_factor_pairs<<<grid_rows(n), 256, 0, st>>>(n, rp, ci, diag, nullptr, h->pptr, h->pairs);
+  B2S_CHECK(cudaMallocAsync(&h->simple, n, st));
+  B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));   // (cnt is free again)
+  k_factor_simple<<<grid_rows(n), 256, 0, st>>>(n, rp, diag, h->pptr, h->pairs, h->simple, cnt);
+  int32_t nonsimple = 1;
+  B2S_CHECK(cudaMemcpyAsync(&nonsimple, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(tmp, st));
+  B2S_CHECK(cudaFreeAsync(cnt, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  h->all_simple = nonsimple == 0 ? 1 : 0;
+  B2S_LAUNCH_CHECK();
+  *handle = h;
+  return B2S_OK;
+}
+
+int b2s_ilu0_symbolic_free(void* handle, cudaStream_t st) {
+  IluSym* h = reinterpret_cast<IluSym*>(handle);
+  if (!h) return B2S_OK;
+  if (h->pptr) cudaFreeAsync(h->pptr, st);
+  if (h->pairs) cudaFreeAsync(h->pairs, st);
+  if (h->simple) cudaFreeAsync(h->simple, st);
+  delete h;
+  return B2S_OK;
+}
+
+// Numeric half: factor the permuted block-CSR values in place (combined
 // L\U) and write the inverse diagonal blocks (row-major, n*b*b).  The slice
-// map gives the claim order (plan order); on a singular pivot the smallest
+// map gives the claim order (plan order).  bad_dev null: synchronises and
+// reports the smallest failing *permuted* row in bad_row_host
+// (B2S_SINGULAR_PIVOT); bad_dev given (device int, INT32_MAX on entry): the
+// row lands there, stream-ordered, no host read.
+int b2s_ilu0_numeric(const void* handle, int b, int nslices, const int32_t* row0,
+                     const int32_t* nrows, const int32_t* rp, const int32_t* ci,
+                     const int32_t* diag, double* vals, double* inv_diag, int* bad_dev,
+                     int32_t* bad_row_host, cudaStream_t st) {
+  if (bad_row_host) *bad_row_host = -1;
+  const IluSym* h = reinterpret_cast<const IluSym*>(handle);
+  if (!h || b < 1) return B2S_SHAPE;
+  if (b > 4) return B2S_UNSUPPORTED;
+  const int n = h->n;
+  if (n == 0) return B2S_OK;
+  int* flag = nullptr;
+  int* bad = bad_dev;
+  Tickets2* tk = nullptr;
+  B2S_CHECK(cudaMallocAsync(&flag, sizeof(int) * n, st));
+  B2S_CHECK(cudaMallocAsync(&tk, sizeof(Tickets2), st));
+  B2S_CHECK(cudaMemsetAsync(flag, 0, sizeof(int) * n, st));
+  B2S_CHECK(cudaMemsetAsync(tk, 0, sizeof(Tickets2), st));
+  const int big = 0x7fffffff;
+  if (!bad) {
+    B2S_CHECK(cudaMallocAsync(&bad, sizeof(int), st));
+    B2S_CHECK(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  }
+  // the inverse diagonals double as the fast path's "ready" marks
+  if (int rcf = fill_sentinel((long long)n * b * b, inv_diag, st)) return rcf;
+  B2S_LAUNCH_CHECK();
+  SliceMap map{nslices, row0, nrows};
+  int rc;
+  switch (b) {
+    case 1: rc = launch_numeric<1>(map, rp, ci, diag, h->pptr, h->pairs, h->simple, vals, inv_diag, flag, bad, tk, h->all_simple, st); break;
+    case 2: rc = launch_numeric<2>(map, rp, ci, diag, h->pptr, h->pairs, h->simple, vals, inv_diag, flag, bad, tk, h->all_simple, st); break;
+    case 3: rc = launch_numeric<3>(map, rp, ci, diag, h->pptr, h->pairs, h->simple, vals, inv_diag, flag, bad, tk, h->all_simple, st); break;
+    default: rc = launch_numeric<4>(map, rp, ci, diag, h->pptr, h->pairs, h->simple, vals, inv_diag, flag, bad, tk, h->all_simple, st); break;
+  }
+  if (rc != B2S_OK) return rc;
+  B2S_CHECK(cudaFreeAsync(flag, st));
+  B2S_CHECK(cudaFreeAsync(tk, st));
+  if (bad_dev) return B2S_OK;
+  int hb = big;
+  B2S_CHECK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  B2S_CHECK(cudaFreeAsync(bad, st));
+  B2S_CHECK(cudaStreamSynchronize(st));
+  if (hb != big) {
+    if (bad_row_host) *bad_row_host = hb;
+    return B2S_SINGULAR_PIVOT;
+  }
+  return B2S_OK;
+}
+
+// Both halves (the original entry point): on a singular pivot the smallest
 // failing *permuted* row goes to bad_row_host (B2S_SINGULAR_PIVOT).
 int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_t* nrows,
                     const int32_t* rp, const int32_t* ci, const int32_t* diag, double* vals,
@@ -312,69 +427,13 @@ int b2s_ilu0_factor(int n, int b, int nslices, const int32_t* row0, const int32_
   if (n < 0 || b < 1) return B2S_SHAPE;
   if (n == 0) return B2S_OK;
   if (b > 4) return B2S_UNSUPPORTED;
-  int32_t nnz = 0;
-  B2S_CHECK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  B2S_CHECK(cudaStreamSynchronize(st));
-  int32_t *cnt = nullptr, *pptr = nullptr;
-  int* flag = nullptr;
-  int* bad = nullptr;
-  Tickets2* tk = nullptr;
-  B2S_CHECK(cudaMallocAsync(&cnt, sizeof(int32_t) * (nnz + 1), st));
-  B2S_CHECK(cudaMallocAsync(&pptr, sizeof(int32_t) * (nnz + 1), st));
-  B2S_CHECK(cudaMallocAsync(&flag, sizeof(int) * n, st));
-  B2S_CHECK(cudaMallocAsync(&bad, sizeof(int), st));
-  B2S_CHECK(cudaMallocAsync(&tk, sizeof(Tickets2), st));
-  B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nnz + 1), st));
-  B2S_CHECK(cudaMemsetAsync(flag, 0, sizeof(int) * n, st));
-  B2S_CHECK(cudaMemsetAsync(tk, 0, sizeof(Tickets2), st));
-  const int big = 0x7fffffff;
-  B2S_CHECK(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-  // symbolic: count, scan, fill
-  k_factor_pairs<<<grid_rows(n), 256, 0, st>>>(n, rp, ci, diag, cnt, nullptr, nullptr);
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, pptr, nnz + 1, st);
-  void* tmp = nullptr;
-  B2S_CHECK(cudaMallocAsync(&tmp, tb, st));
-  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pptr, nnz + 1, st);
-  int32_t npairs = 0;
-  B2S_CHECK(cudaMemcpyAsync(&npairs, pptr + nnz, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  B2S_CHECK(cudaStreamSynchronize(st));
-  int2* pairs = nullptr;
-  B2S_CHECK(cudaMallocAsync(&pairs, sizeof(int2) * (npairs > 0 ? npairs : 1), st));
-  k_factor_pairs<<<grid_rows(n), 256, 0, st>>>(n, rp, ci, diag, nullptr, pptr, pairs);
-  int8_t* simple = nullptr;
-  B2S_CHECK(cudaMallocAsync(&simple, n, st));
-  B2S_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));   // (cnt is free again)
-  k_factor_simple<<<grid_rows(n), 256, 0, st>>>(n, rp, diag, pptr, pairs, simple, cnt);
-  int32_t nonsimple = 1;
-  B2S_CHECK(cudaMemcpyAsync(&nonsimple, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  B2S_CHECK(cudaStreamSynchronize(st));
-  const int all_simple = nonsimple == 0 ? 1 : 0;
-  // the inverse diagonals double as the fast path's "ready" marks
-  if (int rcf = fill_sentinel((long long)n * b * b, inv_diag, st)) return rcf;
-  B2S_LAUNCH_CHECK();
-  SliceMap map{nslices, row0, nrows};
-  int rc;
-  switch (b) {
-    case 1: rc = launch_numeric<1>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, all_simple, st); break;
-    case 2: rc = launch_numeric<2>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, all_simple, st); break;
-    case 3: rc = launch_numeric<3>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, all_simple, st); break;
-    default: rc = launch_numeric<4>(map, rp, ci, diag, pptr, pairs, simple, vals, inv_diag, flag, bad, tk, all_simple, st); break;
-  }
-  if (rc != B2S_OK) return rc;
-  int h = big;
-  B2S_CHECK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-  B2S_CHECK(cudaFreeAsync(tmp, st));
-  B2S_CHECK(cudaFreeAsync(pairs, st));
-  B2S_CHECK(cudaFreeAsync(simple, st));
-  B2S_CHECK(cudaFreeAsync(cnt, st));
-  B2S_CHECK(cudaFreeAsync(pptr, st));
-  B2S_CHECK(cudaFreeAsync(flag, st));
-  B2S_CHECK(cudaFreeAsync(bad, st));
-  B2S_CHECK(cudaFreeAsync(tk, st));
-  B2S_CHECK(cudaStreamSynchronize(st));
-  if (h != big) { *bad_row_host = h; return B2S_SINGULAR_PIVOT; }
-  return B2S_OK;
+  void* h = nullptr;
+  int rc = b2s_ilu0_symbolic(n, b, rp, ci, diag, &h, st);
+  if (rc == B2S_OK)
+    rc = b2s_ilu0_numeric(h, b, nslices, row0, nrows, rp, ci, diag, vals, inv_diag, nullptr,
+                          bad_row_host, st);
+  b2s_ilu0_symbolic_free(h, st);
+  return rc;
 }
 
 }  // extern "C"

@@ -48,7 +48,8 @@ class Ilu0Factorization:
         self._n = n
         self._lu = lu
         self._invd = invd
-        self._deferred = None    # device flags of a not yet checked 2-colour factorisation
+        self._deferred = None    # device flags of a not yet checked factorisation
+        self._op_shell = None    # the operator's SELL layout, sized in the pattern phase
         self.smap = smap
         self._lower = lower
         self._upper = upper
@@ -92,9 +93,9 @@ class Ilu0Factorization:
                        and os.environ.get("B2S_PHASED", "1") != "0")
 
     def check_deferred(self) -> bool:
-        """Read the flags of a deferred 2-colour factorisation (synchronises):
-        raises SingularPivot (input numbering, as decompose would have); True
-        if the pattern was not a 2-colour structure after all (the caller
+        """Read the flags of a deferred factorisation (synchronises): raises
+        SingularPivot (input numbering, as decompose would have); True if a
+        2-colour pattern was not a 2-colour structure after all (the caller
         refactorises with the general path).  False when nothing is pending."""
         fl, self._deferred = self._deferred, None
         if fl is None:
@@ -326,13 +327,46 @@ def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", prep
                              two_colour=tc)
 
 
+def prepare_general(a: BlockMatrix, plan: ParallelPlan, pat: "D.DevPattern"):
+    """Pattern-only half of the general factorisation: plan-order pattern and
+    source map, diagonal positions, slice map, the symbolic factorisation
+    (update pairs), the wavefront packing's pattern phase and the operator's
+    SELL layout (sized, filled later).  Every host synchronisation of the
+    setup that depends on the pattern alone happens here -- before the values
+    are needed (the solve path runs it while they are still uploading)."""
+    n, b = a.num_block_rows, a.block_size
+    D.find_diagonal(pat)                           # MissingDiagonal(first row)
+    identity = plan.is_identity
+    if identity:
+        ppat, src = pat, None
+    else:
+        # plan-order pattern + source map; the factor's values are gathered
+        # straight from the input (one pass), and the operator layout is
+        # later filled from the input the same way -- no permuted copy
+        ppat, src = D.permute_pattern(pat, plan.device("permutation"),
+                                      plan.device("inverse_permutation"))
+    gw = _gw_plan(pat.grid, plan, ppat, b)
+    diag = D.find_diagonal(ppat)
+    # group-aligned slices: a sweep never waits on a row of its own group
+    # (same-group reads take the pre-sweep value, as the reference does)
+    smap = plan.slice_map()
+    sym = C.c_void_p(None)
+    check(D.lib().b2s_ilu0_symbolic(n, b, D.ptr(ppat.rp), D.ptr(ppat.ci), D.ptr(diag),
+                                    C.byref(sym), D.stream()), "ilu0_symbolic")
+    shell = D.DevBSR(ppat, b, D.empty_f64(1, ppat.rp.device))   # pattern only
+    return {"identity": identity, "pattern": ppat, "src": src, "gw": gw, "diag": diag,
+            "smap": smap, "sym": sym, "op_shell": D.Sell.build(smap, shell, 0, fill=False)}
+
+
 def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
-                  prep=None, defer: bool = False, two_colour: bool = True) -> Ilu0Factorization:
-    """``decompose`` on an (optionally pre-uploaded) matrix; ``prep`` is
-    ``prepare_two_colour``'s pattern-only half when the caller ran it early.
-    ``defer``: see ``_factor_two_colour`` (the caller must call
-    ``check_deferred()`` before trusting any result); ``two_colour=False``
-    forces the general factorisation."""
+                  prep=None, defer: bool = False, two_colour: bool = True,
+                  prep_general=None) -> Ilu0Factorization:
+    """``decompose`` on an (optionally pre-uploaded) matrix; ``prep`` /
+    ``prep_general``: ``prepare_two_colour`` / ``prepare_general``'s
+    pattern-only half when the caller ran it early.  ``defer``: no host read
+    of the pivot check (the caller must call ``check_deferred()`` before
+    trusting any result); ``two_colour=False`` forces the general
+    factorisation."""
     a = a.as_block_row_major()
     n = a.num_block_rows
     if plan.num_rows != n:
@@ -340,44 +374,49 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
     b = a.block_size
     bsr = bsr or D.DevBSR.upload(a)
     dev = bsr.pat.rp.device
-    f = _factor_two_colour(a, plan, bsr, prep, defer) if two_colour else None
+    f = (_factor_two_colour(a, plan, bsr, prep, defer)
+         if two_colour and prep_general is None else None)
     if f is not None:
         return f
-    D.find_diagonal(bsr.pat)                       # MissingDiagonal(first row)
-    identity = plan.is_identity
+    g = prep_general or prepare_general(a, plan, bsr.pat)
+    identity, ppat, src, gw = g["identity"], g["pattern"], g["src"], g["gw"]
+    diag, smap, sym = g["diag"], g["smap"], g["sym"]
     a_src = None
     if identity:
         a_perm = bsr
-        gw = _gw_plan(bsr.pat.grid, plan, bsr.pat, b)
         lu = D.DevBSR(bsr.pat, b, bsr.vals.clone())
     else:
-        # plan-order pattern + source map; the factor's values are gathered
-        # straight from the input (one pass), and the operator layout is
-        # later filled from the input the same way -- no permuted copy
-        ppat, src = D.permute_pattern(bsr.pat, plan.device("permutation"),
-                                      plan.device("inverse_permutation"))
-        gw = _gw_plan(bsr.pat.grid, plan, ppat, b)
         vals = D.empty_f64(bsr.pat.nnz * b * b, dev)
         if bsr.pat.nnz:
             check(D.lib().b2s_gather_blocks(bsr.pat.nnz, b, D.ptr(src), D.ptr(bsr.vals),
                                             D.ptr(vals), D.stream()), "gather_blocks")
         lu = D.DevBSR(ppat, b, vals)
         a_perm, a_src = None, (ppat, src, bsr)
-    diag = D.find_diagonal(lu.pat)
-    # group-aligned slices: a sweep never waits on a row of its own group
-    # (same-group reads take the pre-sweep value, as the reference does)
-    smap = plan.slice_map()
     inv = D.empty_f64(n * b * b, dev)
-    bad = C.c_int32(-1)
-    rc = D.lib().b2s_ilu0_factor(n, b, smap.nslices, D.ptr(smap.row0), D.ptr(smap.nrows),
-                                 D.ptr(lu.pat.rp), D.ptr(lu.pat.ci), D.ptr(diag),
-                                 D.ptr(lu.vals), D.ptr(inv), C.byref(bad), D.stream())
-    if rc == SINGULAR_PIVOT:
-        row = int(bad.value)
-        if not identity:
-            row = int(plan.device("inverse_permutation")[row].item())
-        raise SingularPivot(row)
-    check(rc, "ilu0_factor")
+    flags = None
+    try:
+        if defer:
+            flags = torch.full((2,), _I32_MAX, dtype=torch.int32, device=dev)
+            flags[1:].zero_()
+            rc = D.lib().b2s_ilu0_numeric(sym, b, smap.nslices, D.ptr(smap.row0),
+                                          D.ptr(smap.nrows), D.ptr(lu.pat.rp), D.ptr(lu.pat.ci),
+                                          D.ptr(diag), D.ptr(lu.vals), D.ptr(inv), D.ptr(flags),
+                                          None, D.stream())
+        else:
+            bad = C.c_int32(-1)
+            rc = D.lib().b2s_ilu0_numeric(sym, b, smap.nslices, D.ptr(smap.row0),
+                                          D.ptr(smap.nrows), D.ptr(lu.pat.rp), D.ptr(lu.pat.ci),
+                                          D.ptr(diag), D.ptr(lu.vals), D.ptr(inv), None,
+                                          C.byref(bad), D.stream())
+            if rc == SINGULAR_PIVOT:
+                row = int(bad.value)
+                if not identity:
+                    row = int(plan.device("inverse_permutation")[row].item())
+                raise SingularPivot(row)
+        check(rc, "ilu0_numeric")
+    finally:
+        D.lib().b2s_ilu0_symbolic_free(sym, D.stream())
+        g["sym"] = None
     goff = plan.device("group_offsets")
     lower = upper = None
     if gw is None:   # (the wavefront sweeps read their own packed records)
@@ -388,6 +427,8 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
                                  D.ptr(inv), D.ptr(dtiles), D.stream()), "diag_tiles")
     f = Ilu0Factorization(plan, b, n, lu, inv, smap, lower, upper, dtiles, identity, a, a_perm)
     f._a_src = a_src
+    f._op_shell = g["op_shell"]
+    f._deferred = flags
     _maybe_tiles(f, plan, diag)
     _gw_fill(f, gw)
     return f

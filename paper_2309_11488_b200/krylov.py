@@ -242,11 +242,19 @@ class DeviceKrylov:
         if fact is not None:
             smap = fact.smap
             reuse = same_values and fact._source is matrix
+            shell = fact._op_shell if reuse else None
             if a_bsr is None and fact.a_sell is not None and reuse:
                 sell = fact.a_sell   # 2-colour factorisation: the operator layout exists
             elif a_bsr is None and fact._a_src is not None and reuse:
                 ppat, src, inp = fact._a_src   # filled from the unpermuted input values
-                sell = D.Sell.build(smap, D.DevBSR(ppat, b, inp.vals), 0, src=src)
+                if shell is not None:   # sized in the pattern phase: values only now
+                    sell = shell
+                    sell.fill_from(smap, D.DevBSR(ppat, b, inp.vals), 0, src)
+                else:
+                    sell = D.Sell.build(smap, D.DevBSR(ppat, b, inp.vals), 0, src=src)
+            elif a_bsr is None and shell is not None and fact._a_perm is not None:
+                sell = shell        # identity plan: the input is the operator
+                sell.fill_from(smap, fact._a_perm, 0)
             elif a_bsr is None:
                 a_bsr = (fact._a_perm if reuse and fact._a_perm is not None
                          else _plan_order(D.DevBSR.upload(matrix), fact))
