@@ -40,7 +40,6 @@ struct GwDev {
   const char* recb;      // [T*S] backward records: meta[32] int32 | U[3][BB][32] | D[BB][32]
   double* rpk;           // [T*S][B][32]  the sweep's input in step order (k_gw_gather)
   double* ypk;           // [T*S][B][32]  forward results, step order
-  double* zpk;           // [T*S][B][32]  backward results, step order (k_gw_scatter)
   double* eE;            // [T*S][wy][B]      forward: east-edge lanes' results
   double* eN;            // [T*S][wx][B]      forward: north-edge lanes' results
   double* eW;            // [T*S][wy][B]      backward: west-edge lanes' results
@@ -177,7 +176,7 @@ __device__ __forceinline__ void gw_mbar_arrive(unsigned long long* b) {
 // forward: y = r - L y, levels upward; backward: z = inv(U_ii) (y - U z),
 // levels downward.  DIR 0 / 1.
 template <int B, int DIR, int SH>
-__global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
+__global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done, double* zout) {
   constexpr int BB = B * B;
   constexpr int R = DIR == 0 ? (SH ? kGwRingFs : kGwRingF) : (SH ? kGwRingBs : kGwRingB);
   constexpr int VB = B * 32 * 8;   // bytes of one step's vector slice
@@ -258,7 +257,9 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
   const long long xstride = (long long)dstep * g.wy * B, ystride = (long long)dstep * g.wx * B;
   double* xout = (DIR == 0 ? g.eE : g.eW) + ((base + s0) * g.wy + a.yl) * B;
   double* yout = (DIR == 0 ? g.eN : g.eS) + ((base + s0) * g.wx + a.xl) * B;
-  double* vout = (DIR == 0 ? g.ypk : g.zpk) + (base + s0) * B * 32 + lane;
+  // forward results in step order (the backward sweep's input); backward
+  // results straight to their plan rows (no scatter pass)
+  double* vout = g.ypk + (base + s0) * B * 32 + lane;
   const long long vstride = (long long)dstep * B * 32;
   // neighbour-tile step of the value needed at our step s: in range?
   const int xoff = DIR == 0 ? g.wx - 1 : 1 - g.wx, yoff = DIR == 0 ? g.wy - 1 : 1 - g.wy;
@@ -366,10 +367,12 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done) {
       for (int c = 0; c < B; ++c) outv[c] = canon(o[c]);
     }
     if (mt >= 0) {
+      double* zr = zout + (long long)(mt & 0x1FFFFFF) * B;
 #pragma unroll
       for (int c = 0; c < B; ++c) {
         prev[c] = outv[c];
-        vout[c * 32] = outv[c];
+        if (DIR == 0) vout[c * 32] = outv[c];
+        else zr[c] = outv[c];
       }
       if (px) {
 #pragma unroll
@@ -410,22 +413,6 @@ __global__ void k_gw_gather(GwDev g, const double* __restrict__ r) {
   }
 }
 
-template <int B>
-__global__ void k_gw_scatter(GwDev g, double* __restrict__ z) {
-  griddep_wait();
-  griddep_launch();
-  const long long total = (long long)g.TX * g.TY * g.S * 32;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
-       q += (long long)gridDim.x * blockDim.x) {
-    const long long slot = q >> 5;
-    const int lane = (int)(q & 31);
-    const int mt = reinterpret_cast<const int*>(g.recf + slot * g.rf)[lane];
-    if (mt < 0) continue;
-    const long long pr = mt & 0x1FFFFFF;
-#pragma unroll
-    for (int c = 0; c < B; ++c) z[pr * B + c] = g.zpk[(slot * B + c) * 32 + lane];
-  }
-}
 
 // ---- packing, one thread per (tile, step, lane).  Pattern phase (before
 // the numeric factorisation): meta words, the CSR slot of each of the six
@@ -532,10 +519,9 @@ int launch_gw_b(const GwHandle* h, const double* r, double* z, const int* done, 
   // cannot overlap their predecessor (PDL) and add a drain in CUDA graphs.
   if (launch_k(k_gw_gather<B>, dim3((int)grid), dim3(256), 0, st, pdl, g, r) != cudaSuccess ||
       launch_k(g.shallow ? k_gw_sweep<B, 0, 1> : k_gw_sweep<B, 0, 0>, dim3(g.TX * g.TY), dim3(32),
-               gw_smem_bytes(g, B, 0), st, pdl, g, done) != cudaSuccess ||
+               gw_smem_bytes(g, B, 0), st, pdl, g, done, z) != cudaSuccess ||
       launch_k(g.shallow ? k_gw_sweep<B, 1, 1> : k_gw_sweep<B, 1, 0>, dim3(g.TX * g.TY), dim3(32),
-               gw_smem_bytes(g, B, 1), st, pdl, g, done) != cudaSuccess ||
-      launch_k(k_gw_scatter<B>, dim3((int)grid), dim3(256), 0, st, pdl, g, z) != cudaSuccess)
+               gw_smem_bytes(g, B, 1), st, pdl, g, done, z) != cudaSuccess)
     return B2S_CUDA_ERROR;
   return B2S_OK;
 }
@@ -603,7 +589,7 @@ static void gw_shape(GwDev& g, int b, int nx, int ny, int nz, int wx, int wy) {
 static long long gw_bytes(const GwDev& g, int b) {
   const long long slots = (long long)g.TX * g.TY * g.S;
   return slots * ((long long)g.rf + g.rb) +
-         (3 * slots * b * 32 + 2 * slots * g.wy * b + 2 * slots * g.wx * b) * 8 +
+         (2 * slots * b * 32 + 2 * slots * g.wy * b + 2 * slots * g.wx * b) * 8 +
          slots * 6 * 32 * 4 + 256;
 }
 
@@ -654,7 +640,6 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
   double* d = reinterpret_cast<double*>(p);
   g.rpk = d; d += nV;
   g.ypk = d; d += nV;
-  g.zpk = d; d += nV;
   g.eE = d; d += nEx;
   g.eW = d; d += nEx;
   g.eN = d; d += nEy;
