@@ -133,6 +133,12 @@ __device__ __forceinline__ void gw_poll(const double* p, double (&v)[B]) {
   while (!gw_ready<B>(v)) gw_load<B>(p, v);
 }
 
+// element e of lane l in a step record's block area: pairs of elements
+// interleaved per lane, [e/2][32 lanes][2]
+__host__ __device__ __forceinline__ long long gw_eidx(int e, int lane) {
+  return (long long)(e >> 1) * 64 + lane * 2 + (e & 1);
+}
+
 struct GwTile {
   int t, tx, ty, x0, y0, xw, yw, xl, yl, L0, St;
   bool valid;
@@ -291,10 +297,14 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done, doubl
     gw_mbar_wait(full + q, (unsigned)((j / R) & 1));
     const char* st_ = ring + q * stage;
     mt = reinterpret_cast<const int*>(st_)[lane];
-    const double* blk = reinterpret_cast<const double*>(st_ + kGwMetaBytes) + lane;
+    const double2* blk = reinterpret_cast<const double2*>(st_ + kGwMetaBytes) + lane;
     const double* v = reinterpret_cast<const double*>(st_ + rb) + lane;
 #pragma unroll
-    for (int e = 0; e < NB; ++e) bk[e] = blk[e * 32];
+    for (int e = 0; e < NB; e += 2) {
+      const double2 q = blk[(e >> 1) * 32];
+      bk[e] = q.x;
+      if (e + 1 < NB) bk[e + 1] = q.y;
+    }
 #pragma unroll
     for (int c = 0; c < B; ++c) vv[c] = v[c * 32];
   };
@@ -478,11 +488,13 @@ __global__ void k_gw_vals(GwDev g, int bb, const int32_t* __restrict__ src,
     const int32_t* sp = src + slot * 6 * 32 + lane;
     for (int k = 0; k < 6; ++k) {
       const int p = sp[k * 32];
-      double* dst = (k < 3 ? Lv : Uv) + ((k % 3) * bb) * 32 + lane;
-      for (int e = 0; e < bb; ++e) dst[e * 32] = p >= 0 ? lu[(long long)p * bb + e] : 0.0;
+      double* dst = k < 3 ? Lv : Uv;
+      for (int e = 0; e < bb; ++e)
+        dst[gw_eidx((k % 3) * bb + e, lane)] = p >= 0 ? lu[(long long)p * bb + e] : 0.0;
     }
     const long long pr = mt >= 0 ? (mt & 0x1FFFFFF) : -1;
-    for (int e = 0; e < bb; ++e) Uv[(3 * bb + e) * 32 + lane] = pr >= 0 ? inv[pr * bb + e] : 0.0;
+    for (int e = 0; e < bb; ++e) Uv[gw_eidx(3 * bb + e, lane)] = pr >= 0 ? inv[pr * bb + e] : 0.0;
+    if ((3 * bb) & 1) Lv[gw_eidx(3 * bb, lane)] = 0.0;   // (the pad of an odd count)
   }
 }
 
@@ -582,8 +594,10 @@ static void gw_shape(GwDev& g, int b, int nx, int ny, int nz, int wx, int wy) {
   g.TY = (ny + wy - 1) / wy;
   g.S = (wx - 1) + (wy - 1) + nz;
   const int bb = b * b;
-  g.rf = kGwMetaBytes + 3 * bb * 32 * 8;
-  g.rb = kGwMetaBytes + 4 * bb * 32 * 8;
+  // block elements in lane-interleaved pairs (one 16-byte shared load per
+  // two elements): element counts rounded up to even
+  g.rf = kGwMetaBytes + ((3 * bb + 1) & ~1) * 32 * 8;
+  g.rb = kGwMetaBytes + ((4 * bb + 1) & ~1) * 32 * 8;
 }
 
 static long long gw_bytes(const GwDev& g, int b) {
