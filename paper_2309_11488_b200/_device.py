@@ -252,16 +252,19 @@ def grid_hint(n: int, rp: np.ndarray, ci: np.ndarray):
     from it against every row, so a wrong hint costs one pass, never a result."""
     if n < 8:
         return None
-    r = n // 2
-    off = np.asarray(ci[int(rp[r]):int(rp[r + 1])], dtype=np.int64) - r
-    u = [int(v) for v in np.unique(off[off > 0])]
-    if u == [1]:
-        return n, 1
-    if len(u) == 2 and u[0] == 1 and n % u[1] == 0:
-        return u[1], n // u[1]
-    if len(u) == 3 and u[0] == 1 and u[2] % u[1] == 0 and n % u[2] == 0:
-        return u[1], u[2] // u[1]
-    return None
+    best = None
+    # a row on the top plane has no z+1 coupling (nz = 2: the middle row is
+    # one), so a few rows are looked at and the richest reading kept
+    for r in (n // 2, n // 4, (3 * n) // 4):
+        off = np.asarray(ci[int(rp[r]):int(rp[r + 1])], dtype=np.int64) - r
+        u = [int(v) for v in np.unique(off[off > 0])]
+        if len(u) == 3 and u[0] == 1 and u[2] % u[1] == 0 and n % u[2] == 0:
+            return u[1], u[2] // u[1]
+        if best is None and u == [1]:
+            best = (n, 1)
+        elif len(u) == 2 and u[0] == 1 and n % u[1] == 0 and (best is None or best[1] == 1):
+            best = (u[1], n // u[1])
+    return best
 
 
 @dataclass

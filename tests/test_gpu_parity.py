@@ -655,6 +655,23 @@ def test_wavefront_sweeps_bit_identical(monkeypatch, dims, plan_kind):
     assert out["1"][2].iterations == out["0"][2].iterations
 
 
+@pytest.mark.parametrize("bs", [1, 2, 4])
+def test_wavefront_sweeps_other_block_sizes(monkeypatch, bs):
+    """The wavefront kernels for b = 1, 2, 4 (deep and shallow rings) equal
+    the sync-free sweeps bit for bit."""
+    for dims in ((16, 12, 9), (240, 64, 2)):   # (> 32 levels)
+        a = P.generate(P.GeneratorSpec(*dims, block_size=bs, seed=6, diagonal_boost=1e-2)).a
+        plan = P.level_schedule(a.pattern)
+        r = P.BlockVector(np.random.default_rng(2).uniform(-1, 1, a.num_block_rows * bs), bs)
+        out = {}
+        for flag in ("1", "0"):
+            monkeypatch.setenv("B2S_GW", flag)
+            f = P.decompose(a, plan)
+            assert (f.gw is not None) == (flag == "1")
+            out[flag] = f.apply(r).data
+        np.testing.assert_array_equal(out["1"], out["0"])
+
+
 def test_wavefront_declines_non_stencil_rows(monkeypatch):
     """A pattern that is not a 7-point stencil of its grid keeps the sync-free
     sweeps (the packing kernel verifies every row)."""
