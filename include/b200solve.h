@@ -255,6 +255,21 @@ int b2s_gw_create(int n, int b, int nx, int ny, int nz, int wx, int wy, const in
 /* value phase, stream-ordered: lu = combined L\U on that pattern, inv = inverse diagonals */
 int b2s_gw_fill(void* handle, const double* lu, const double* inv, cudaStream_t stream);
 int b2s_gw_destroy(void* handle);
+/* ILU0 of the handle's grid straight into its step records (wavefront
+ * factorisation, bit-identical to b2s_ilu0_factor on these patterns): rp/ci/
+ * diag = plan-order pattern, vsrc = plan slot -> input slot (null: identity
+ * plan), vals = input values; writes the plan-order inverse diagonals (invd)
+ * and U_ii (dvals); the smallest singular plan row goes to *bad_dev (device,
+ * INT32_MAX on entry).  Stream-ordered, no host read; B2S_UNSUPPORTED when
+ * the tiles cannot be co-resident (factorise the general way). */
+long long b2s_gw_factor_workspace_bytes(const void* handle);
+int b2s_gw_factor(void* handle, const int32_t* rp, const int32_t* ci, const int32_t* diag,
+                  const int32_t* vsrc, const double* vals, double* invd, double* dvals,
+                  int* bad_dev, void* workspace, long long workspace_bytes, cudaStream_t stream);
+/* the combined L\U CSR values from the records (lu holds the plan-order
+ * operator values on entry) -- materialised only on request */
+int b2s_gw_unpack_lu(const void* handle, const int32_t* diag, const double* dvals, double* lu,
+                     cudaStream_t stream);
 int b2s_gw_apply(int b, const void* handle, const double* r, double* z, cudaStream_t stream);
 /* debug (B2S_GW_TRACE set at create): the last apply's per-step end times,
  * [2][T][S] ns; shape = {TX, TY, S, wx, wy} */

@@ -106,6 +106,9 @@ SIGNATURES = {
                            C.POINTER(C.c_void_p), _P]),
     "b2s_gw_fill": (_I, [_P, _P, _P, _P]),
     "b2s_gw_destroy": (_I, [_P]),
+    "b2s_gw_factor_workspace_bytes": (_LL, [_P]),
+    "b2s_gw_factor": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _LL, _P]),
+    "b2s_gw_unpack_lu": (_I, [_P, _P, _P, _P, _P]),
     "b2s_gw_apply": (_I, [_I, _P, _P, _P, _P]),
     "b2s_gw_trace": (_I, [_P, _P, _LL, C.POINTER(C.c_longlong), _P]),
     "b2s_wells_apply": (_I, [_P, _P, _P, _P, _P]),

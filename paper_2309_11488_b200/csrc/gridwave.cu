@@ -406,6 +406,259 @@ __global__ void __launch_bounds__(32) k_gw_sweep(GwDev g, const int* done, doubl
 #endif
 }
 
+// ---- wavefront ILU0 factorisation of the same grids (bs/ilu0.py:145-201).
+// On a natural-order 7-point stencil the elimination of row i touches only
+// its diagonal: L_ik = A_ik inv(U_kk) for its lower neighbours k (ascending
+// plan columns: z-1, y-1, x-1), U_ii = A_ii - sum_k L_ik A_ki, U_ij = A_ij.
+// inv(U_kk) of the three lower neighbours was produced one step earlier by
+// this lane (z-1) or lane-1 / lane-wx, or by the west / south tile (edge
+// buffers, 9 doubles per edge lane) -- the forward sweep's dependency
+// structure.  Per row the arithmetic is the numeric factor kernel's fast
+// path (factor.cu: matmul, then subtract, ascending k; the Gauss-Jordan
+// inverse), so the factors are bit-identical to it.
+//
+// Factor record per (tile, step): meta[32] | A_i,z-1 A_i,y-1 A_i,x-1 |
+// A_z-1,i A_y-1,i A_x-1,i | A_ii, element-pair interleaved like the sweeps'.
+constexpr int kGwFacBlocks = 7;
+
+__host__ __device__ inline int gw_rec_fac(int b) {
+  return kGwMetaBytes + ((kGwFacBlocks * b * b + 1) & ~1) * 32 * 8;
+}
+
+// pack the factor records and the backward records' upper blocks straight
+// from the input values (vsrc: plan-order slot -> input slot, null: same)
+template <int B>
+__global__ void k_gw_apack(GwDev g, const int32_t* __restrict__ src,
+                           const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const int32_t* __restrict__ diag, const int32_t* __restrict__ vsrc,
+                           const double* __restrict__ vin, char* __restrict__ fac) {
+  constexpr int BB = B * B;
+  constexpr int NE = (kGwFacBlocks * BB + 1) & ~1;
+  const int rfa = gw_rec_fac(B);
+  const long long total = (long long)g.TX * g.TY * g.S * 32;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(q % 32);
+    const long long slot = q / 32;
+    const int s = (int)(slot % g.S);
+    const int t = (int)(slot / g.S);
+    const int mt = reinterpret_cast<const int*>(g.recf + slot * g.rf)[lane];
+    reinterpret_cast<int*>(fac + slot * rfa)[lane] = mt;
+    double2* fv = reinterpret_cast<double2*>(fac + slot * rfa + kGwMetaBytes) + lane;
+    double* Uv = reinterpret_cast<double*>(const_cast<char*>(g.recb) + slot * g.rb + kGwMetaBytes);
+    const int32_t* sp = src + slot * 6 * 32 + lane;
+    const int pr = mt >= 0 ? (mt & 0x1FFFFFF) : -1;
+    auto val = [&](long long p, int e) {
+      return p >= 0 ? vin[(vsrc ? (long long)vsrc[p] : p) * BB + e] : 0.0;
+    };
+    // CSR slots: A_ik (kinds 0..2), A_ki = the lower neighbour's plus-entry of
+    // the opposite kind, read from the neighbour's own slot of src, A_ii
+    long long pa[kGwFacBlocks];
+    const GwTile a = gw_tile(g, t, lane);
+    const int x = a.x0 + a.xl, y = a.y0 + a.yl, z = a.L0 + s - x - y;
+    for (int k = 0; k < 3; ++k) {
+      const int p = mt >= 0 ? sp[k * 32] : -1;
+      pa[k] = p;
+      pa[3 + k] = -1;
+      if (p < 0) continue;
+      const int nx_ = x - (k == 2), ny_ = y - (k == 1), nz_ = z - (k == 0);   // the neighbour
+      const int ntx = nx_ / g.wx, nty = ny_ / g.wy;
+      const int nxl = nx_ - ntx * g.wx, nyl = ny_ - nty * g.wy;
+      const long long nslot = (long long)(nty * g.TX + ntx) * g.S + nxl + nyl + nz_;
+      pa[3 + k] = src[nslot * 6 * 32 + (5 - k) * 32 + nxl + g.wx * nyl];   // kinds 5,4,3
+    }
+    pa[6] = pr >= 0 ? diag[pr] : -1;
+    double v[NE];
+#pragma unroll
+    for (int j = 0; j < kGwFacBlocks; ++j)
+#pragma unroll
+      for (int e = 0; e < BB; ++e) v[j * BB + e] = val(pa[j], e);
+    if (NE > kGwFacBlocks * BB) v[NE - 1] = 0.0;
+#pragma unroll
+    for (int e = 0; e < NE; e += 2) fv[(e >> 1) * 32] = make_double2(v[e], v[e + 1]);
+    for (int k = 3; k < 6; ++k) {
+      const int p = mt >= 0 ? sp[k * 32] : -1;
+      for (int e = 0; e < BB; ++e) Uv[gw_eidx((k - 3) * BB + e, lane)] = val(p, e);
+    }
+  }
+}
+
+template <int B> struct GwFacRing { static constexpr int deep = B <= 3 ? 4 : 2, shallow = B <= 3 ? 2 : 1; };
+
+template <int B, int SH>
+__global__ void __launch_bounds__(32) k_gw_factor(GwDev g, const char* __restrict__ fac,
+                                                  double* eFE, double* eFN,
+                                                  double* __restrict__ invd,
+                                                  double* __restrict__ dvals, int* bad) {
+  constexpr int BB = B * B;
+  constexpr int R = SH ? GwFacRing<B>::shallow : GwFacRing<B>::deep;
+  extern __shared__ __align__(128) char smem[];
+  griddep_wait();
+  griddep_launch();
+  const int lane = threadIdx.x & 31;
+  const GwTile a = gw_tile(g, blockIdx.x, lane);
+  const long long base = (long long)a.t * g.S;
+  const int rfa = gw_rec_fac(B);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
+  char* ring = smem + 128;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < R; ++q) gw_mbar_init_n(full + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int j) {
+    const int q = j % R;
+    gw_mbar_expect(full + q, (unsigned)rfa);
+    gw_bulk(ring + q * rfa, fac + (base + j) * (long long)rfa, (unsigned)rfa, full + q);
+  };
+  if (lane == 0)
+    for (int j = 0; j < R && j < a.St; ++j) issue(j);
+  const bool hasW = a.tx > 0, hasS = a.ty > 0;
+  const bool hasE = a.tx + 1 < g.TX, hasN = a.ty + 1 < g.TY;
+  const bool xe = a.xl == 0 && hasW, ye = a.yl == 0 && hasS;
+  const bool px = a.xl == a.xw - 1 && hasE, py = a.yl == a.yw - 1 && hasN;
+  // neighbour tiles' inverse blocks needed at our step s: their step s+wx-1 / s+wy-1
+  const double* xin = eFE + (((base - g.S) + (g.wx - 1)) * g.wy + a.yl) * BB;
+  const double* yin = eFN + (((base - (long long)g.TX * g.S) + (g.wy - 1)) * g.wx + a.xl) * BB;
+  double* xout = eFE + (base * g.wy + a.yl) * BB;
+  double* yout = eFN + (base * g.wx + a.xl) * BB;
+  const long long xstride = (long long)g.wy * BB, ystride = (long long)g.wx * BB;
+  auto xok = [&](int s) { const int t = s + g.wx - 1; return xe && t >= 0 && t < g.S; };
+  auto yok = [&](int s) { const int t = s + g.wy - 1; return ye && t >= 0 && t < g.S; };
+  const int sx = lane > 0 ? lane - 1 : 0;
+  const int sy = lane >= g.wx ? lane - g.wx : 0;
+  double prev[BB];
+#pragma unroll
+  for (int e = 0; e < BB; ++e) prev[e] = 0.0;
+  // the neighbour tiles' inverse blocks, requested one step early (all
+  // elements in flight at once; re-read together while any is unproduced)
+  double ex[BB], ey[BB];
+#pragma unroll
+  for (int e = 0; e < BB; ++e) ex[e] = ey[e] = sentinel();
+  if (a.St > 0) {
+    if (xok(0)) gw_load<BB>(xin, ex);
+    if (yok(0)) gw_load<BB>(yin, ey);
+  }
+  for (int j = 0; j < a.St; ++j) {
+    const int q = j % R;
+    gw_mbar_wait(full + q, (unsigned)((j / R) & 1));
+    const char* st_ = ring + q * rfa;
+    const int mt = reinterpret_cast<const int*>(st_)[lane];
+    const double2* blk = reinterpret_cast<const double2*>(st_ + kGwMetaBytes) + lane;
+    double A[kGwFacBlocks * BB + 1];
+#pragma unroll
+    for (int e = 0; e < kGwFacBlocks * BB; e += 2) {
+      const double2 v = blk[(e >> 1) * 32];
+      A[e] = v.x;
+      A[e + 1] = v.y;
+    }
+    __syncwarp();
+    if (lane == 0 && j + R < a.St) {
+      gw_fence_proxy();
+      issue(j + R);
+    }
+    const int mask = mt >= 0 ? (mt >> 25) : 0;
+    // the three lower neighbours' inverse blocks (z-1: own previous step)
+    double dz[BB], dy[BB], dx[BB];
+#pragma unroll
+    for (int e = 0; e < BB; ++e) {
+      dz[e] = prev[e];
+      dx[e] = __shfl_sync(0xffffffffu, prev[e], sx);
+      dy[e] = __shfl_sync(0xffffffffu, prev[e], sy);
+    }
+    if (xok(j) && (mask & kXm)) {
+      gw_poll<BB>(xin + (long long)j * xstride, ex);
+#pragma unroll
+      for (int e = 0; e < BB; ++e) dx[e] = ex[e];
+    }
+    if (yok(j) && (mask & kYm)) {
+      gw_poll<BB>(yin + (long long)j * ystride, ey);
+#pragma unroll
+      for (int e = 0; e < BB; ++e) dy[e] = ey[e];
+    }
+    if (j + 1 < a.St) {   // the next step's edge inputs, one step early
+      if (xok(j + 1)) gw_load<BB>(xin + (long long)(j + 1) * xstride, ex);
+      if (yok(j + 1)) gw_load<BB>(yin + (long long)(j + 1) * ystride, ey);
+    }
+    // ascending plan columns z-1, y-1, x-1; an absent neighbour has zero
+    // blocks and a zero-selected inverse: its product and update are +0.0
+    double dblk[BB], L[3][BB];
+#pragma unroll
+    for (int e = 0; e < BB; ++e) dblk[e] = A[6 * BB + e];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int bit = k == 0 ? kZm : (k == 1 ? kYm : kXm);
+      const double* dep = k == 0 ? dz : (k == 1 ? dy : dx);
+      const bool on = (mask & bit) != 0;
+      double d[BB], prod[BB];
+#pragma unroll
+      for (int e = 0; e < BB; ++e) d[e] = on ? dep[e] : 0.0;
+      matmul<B>(A + k * BB, d, L[k]);              // L_ik = A_ik inv(U_kk)
+      matmul<B>(L[k], A + (3 + k) * BB, prod);     // A_ii -= L_ik U_ki (= A_ki)
+#pragma unroll
+      for (int e = 0; e < BB; ++e) dblk[e] -= prod[e];
+    }
+    double inv[BB];
+    const bool ok = invert_block<B>(dblk, inv);
+    if (mt >= 0) {
+      const int pr = mt & 0x1FFFFFF;
+      if (!ok) atomicMin(bad, pr);
+      double* Lv = reinterpret_cast<double*>(const_cast<char*>(g.recf) + (base + j) * g.rf + kGwMetaBytes);
+      double* Iv = reinterpret_cast<double*>(const_cast<char*>(g.recb) + (base + j) * g.rb + kGwMetaBytes);
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int e = 0; e < BB; ++e) Lv[gw_eidx(k * BB + e, lane)] = L[k][e];
+#pragma unroll
+      for (int e = 0; e < BB; ++e) {
+        const double o = canon(inv[e]);
+        prev[e] = o;
+        Iv[gw_eidx(3 * BB + e, lane)] = o;
+        invd[(long long)pr * BB + e] = o;
+        dvals[(long long)pr * BB + e] = dblk[e];
+      }
+      if (px) {
+#pragma unroll
+        for (int e = 0; e < BB; ++e) gw_st_relaxed(xout + (long long)j * xstride + e, prev[e]);
+      }
+      if (py) {
+#pragma unroll
+        for (int e = 0; e < BB; ++e) gw_st_relaxed(yout + (long long)j * ystride + e, prev[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < BB; ++e) prev[e] = 0.0;
+    }
+  }
+}
+
+// the combined L\U (plan-order CSR) from the records: L blocks and U_ii
+// over the gathered operator values (materialised only on request)
+template <int B>
+__global__ void k_gw_unpack_lu(GwDev g, const int32_t* __restrict__ src,
+                               const int32_t* __restrict__ diag,
+                               const double* __restrict__ dvals, double* __restrict__ lu) {
+  constexpr int BB = B * B;
+  const long long total = (long long)g.TX * g.TY * g.S * 32;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(q % 32);
+    const long long slot = q / 32;
+    const int mt = reinterpret_cast<const int*>(g.recf + slot * g.rf)[lane];
+    if (mt < 0) continue;
+    const int pr = mt & 0x1FFFFFF;
+    const double* Lv = reinterpret_cast<const double*>(g.recf + slot * g.rf + kGwMetaBytes);
+    const int32_t* sp = src + slot * 6 * 32 + lane;
+    for (int k = 0; k < 3; ++k) {
+      const int p = sp[k * 32];
+      if (p >= 0)
+        for (int e = 0; e < BB; ++e) lu[(long long)p * BB + e] = Lv[gw_eidx(k * BB + e, lane)];
+    }
+    const long long pd = diag[pr];
+    for (int e = 0; e < BB; ++e) lu[pd * BB + e] = dvals[(long long)pr * BB + e];
+  }
+}
+
 // the sweep's input in step order / its output back to plan order
 template <int B>
 __global__ void k_gw_gather(GwDev g, const double* __restrict__ r) {
@@ -468,6 +721,17 @@ __global__ void k_gw_meta(GwDev g, int32_t* __restrict__ src, const int32_t* __r
       if (kind < 0 || (kind < 3) != (c < pr) || (mask & (1 << kind))) { atomicExch(bad, 1); continue; }
       mask |= 1 << kind;
       sp[kind * 32] = p;
+    }
+    // the kernels accumulate in kind order (z-1, y-1, x-1 / x+1, y+1, z+1):
+    // it must be the ascending plan-column (CSR slot) order of the row
+    for (int h = 0; h < 2; ++h) {
+      int last = -1;
+      for (int k = 3 * h; k < 3 * h + 3; ++k) {
+        const int p = sp[k * 32];
+        if (p < 0) continue;
+        if (p < last) atomicExch(bad, 1);
+        last = p;
+      }
     }
     mf[lane] = mb[lane] = pr | (mask << 25);
   }
@@ -549,6 +813,51 @@ int launch_gw(int b, const void* handle, const double* r, double* z, const int* 
     case 4: return launch_gw_b<4>(h, r, z, done, st, pdl);
     default: return B2S_UNSUPPORTED;
   }
+}
+
+inline int gw_fac_smem(int b, int shallow) {
+  const int r = b <= 3 ? (shallow ? GwFacRing<3>::shallow : GwFacRing<3>::deep)
+                       : (shallow ? GwFacRing<4>::shallow : GwFacRing<4>::deep);
+  return 128 + r * gw_rec_fac(b);
+}
+
+// pack + factor (stream-ordered); B2S_UNSUPPORTED when the tiles cannot all
+// be co-resident with either factor ring
+template <int B>
+int launch_gw_factor(const GwDev& g, const int32_t* src, const int32_t* rp, const int32_t* ci,
+                     const int32_t* diag, const int32_t* vsrc, const double* vals, char* fac,
+                     double* eFE, double* eFN, double* invd, double* dvals, int* bad,
+                     cudaStream_t st) {
+  const long long T = (long long)g.TX * g.TY;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int shallow = -1;
+  for (int sh = 0; sh < 2 && shallow < 0; ++sh) {
+    const int sm = gw_fac_smem(B, sh);
+    const void* fn = sh ? (const void*)k_gw_factor<B, 1> : (const void*)k_gw_factor<B, 0>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) != cudaSuccess)
+      return B2S_CUDA_ERROR;
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 32, sm);
+    if (T <= (long long)per * sms) shallow = sh;
+  }
+  if (shallow < 0) return B2S_UNSUPPORTED;
+  const long long slots = T * g.S;
+  const long long ne = slots * (g.wx + g.wy) * B * B;   // eFE and eFN are contiguous
+  long long gf = (ne + 255) / 256;
+  if (gf > kSms * 16) gf = kSms * 16;
+  k_gw_fill<<<(int)gf, 256, 0, st>>>(ne, eFE);
+  long long grid = (slots * 32 + 255) / 256;
+  if (grid > kSms * 64) grid = kSms * 64;
+  k_gw_apack<B><<<(int)grid, 256, 0, st>>>(g, src, rp, ci, diag, vsrc, vals, fac);
+  const int sm = gw_fac_smem(B, shallow);
+  const cudaError_t e =
+      shallow ? launch_k(k_gw_factor<B, 1>, dim3((unsigned)T), dim3(32), sm, st, false, g,
+                         (const char*)fac, eFE, eFN, invd, dvals, bad)
+              : launch_k(k_gw_factor<B, 0>, dim3((unsigned)T), dim3(32), sm, st, false, g,
+                         (const char*)fac, eFE, eFN, invd, dvals, bad);
+  return e == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
 template <int B, int SH>
@@ -721,6 +1030,64 @@ int b2s_gw_trace(const void* handle, unsigned long long* host, long long cap, lo
   // with room for it, also the per-launch timeline of a trace build
   const long long tl = (long long)h->g.TX * h->g.TY * (1 + 4 * kGwTl);
   B2S_CHECK(cudaMemcpy(host, h->g.trace, (cap >= n + tl ? n + tl : n) * 8, cudaMemcpyDeviceToHost));
+  return B2S_OK;
+}
+
+// Scratch bytes b2s_gw_factor needs (factor records + its edge buffers).
+long long b2s_gw_factor_workspace_bytes(const void* handle) {
+  const GwHandle* h = reinterpret_cast<const GwHandle*>(handle);
+  if (!h) return 0;
+  const long long slots = (long long)h->g.TX * h->g.TY * h->g.S;
+  return slots * gw_rec_fac(h->b) + slots * (h->g.wx + h->g.wy) * h->b * h->b * 8 + 256;
+}
+
+// ILU0 of the grid given to create, straight from the input values (vsrc:
+// plan-order CSR slot -> input slot, null when the plan is the identity;
+// rp/ci/diag: the plan-order pattern and its diagonal slots), into the step
+// records (no b2s_gw_fill needed), the plan-order inverse diagonals invd and
+// U_ii (dvals, n*b*b).  Bit-identical to b2s_ilu0_factor on these patterns.
+// bad_dev (device int, INT32_MAX on entry) receives the smallest singular
+// plan row.  Stream-ordered, no host read.  B2S_UNSUPPORTED when the tiles do
+// not fit co-resident (the caller factorises the general way).
+int b2s_gw_factor(void* handle, const int32_t* rp, const int32_t* ci, const int32_t* diag,
+                  const int32_t* vsrc, const double* vals, double* invd, double* dvals,
+                  int* bad_dev, void* work, long long work_bytes, cudaStream_t st) {
+  GwHandle* h = reinterpret_cast<GwHandle*>(handle);
+  if (!h || !rp || !ci || !diag || !vals || !invd || !dvals || !bad_dev || !work) return B2S_SHAPE;
+  if (work_bytes < b2s_gw_factor_workspace_bytes(handle)) return B2S_SHAPE;
+  const long long slots = (long long)h->g.TX * h->g.TY * h->g.S;
+  char* fac = reinterpret_cast<char*>(work);
+  double* eF = reinterpret_cast<double*>(fac + slots * gw_rec_fac(h->b));
+  double* eFN = eF + slots * h->g.wy * h->b * h->b;
+  int rc;
+  switch (h->b) {
+    case 1: rc = launch_gw_factor<1>(h->g, h->src, rp, ci, diag, vsrc, vals, fac, eF, eFN, invd, dvals, bad_dev, st); break;
+    case 2: rc = launch_gw_factor<2>(h->g, h->src, rp, ci, diag, vsrc, vals, fac, eF, eFN, invd, dvals, bad_dev, st); break;
+    case 3: rc = launch_gw_factor<3>(h->g, h->src, rp, ci, diag, vsrc, vals, fac, eF, eFN, invd, dvals, bad_dev, st); break;
+    case 4: rc = launch_gw_factor<4>(h->g, h->src, rp, ci, diag, vsrc, vals, fac, eF, eFN, invd, dvals, bad_dev, st); break;
+    default: rc = B2S_UNSUPPORTED;
+  }
+  if (rc == B2S_OK) B2S_LAUNCH_CHECK();
+  return rc;
+}
+
+// The combined L\U values (plan-order CSR) from a b2s_gw_factor: lu must
+// hold the plan-order operator values; the L blocks and U_ii are written over.
+int b2s_gw_unpack_lu(const void* handle, const int32_t* diag, const double* dvals, double* lu,
+                     cudaStream_t st) {
+  const GwHandle* h = reinterpret_cast<const GwHandle*>(handle);
+  if (!h || !diag || !dvals || !lu) return B2S_SHAPE;
+  const long long slots = (long long)h->g.TX * h->g.TY * h->g.S;
+  long long grid = (slots * 32 + 255) / 256;
+  if (grid > kSms * 64) grid = kSms * 64;
+  switch (h->b) {
+    case 1: k_gw_unpack_lu<1><<<(int)grid, 256, 0, st>>>(h->g, h->src, diag, dvals, lu); break;
+    case 2: k_gw_unpack_lu<2><<<(int)grid, 256, 0, st>>>(h->g, h->src, diag, dvals, lu); break;
+    case 3: k_gw_unpack_lu<3><<<(int)grid, 256, 0, st>>>(h->g, h->src, diag, dvals, lu); break;
+    case 4: k_gw_unpack_lu<4><<<(int)grid, 256, 0, st>>>(h->g, h->src, diag, dvals, lu); break;
+    default: return B2S_UNSUPPORTED;
+  }
+  B2S_LAUNCH_CHECK();
   return B2S_OK;
 }
 

@@ -50,6 +50,7 @@ class Ilu0Factorization:
         self._invd = invd
         self._deferred = None    # device flags of a not yet checked factorisation
         self._op_shell = None    # the operator's SELL layout, sized in the pattern phase
+        self._gw_lazy = None     # wavefront factorisation: what materialises L\U on request
         self.smap = smap
         self._lower = lower
         self._upper = upper
@@ -112,6 +113,20 @@ class Ilu0Factorization:
     def lu_device(self) -> "D.DevBSR":
         """Combined L\\U in plan order, block CSR (built on first use for 2-colour
         factorisations, which never need it on the solve path)."""
+        if self._lu is None and self._gw_lazy is not None:
+            # wavefront factorisation: operator values in plan order, then the
+            # L blocks and U_ii from the records written over them
+            ppat, src, vin, diag, dvals = self._gw_lazy
+            bb = self._b * self._b
+            vals = D.empty_f64(max(ppat.nnz, 1) * bb, ppat.rp.device)
+            if src is None:
+                vals[: ppat.nnz * bb].copy_(vin[: ppat.nnz * bb])
+            elif ppat.nnz:
+                check(D.lib().b2s_gather_blocks(ppat.nnz, self._b, D.ptr(src), D.ptr(vin),
+                                                D.ptr(vals), D.stream()), "gather_blocks")
+            check(D.lib().b2s_gw_unpack_lu(self.gw, D.ptr(diag), D.ptr(dvals), D.ptr(vals),
+                                           D.stream()), "gw_unpack_lu")
+            self._lu = D.DevBSR(ppat, self._b, vals)
         if self._lu is None:
             t = self._two_colour
             pat, a_s, lo = t["pattern"], t["a_sell"], self.lower
@@ -327,6 +342,57 @@ def _factor_two_colour(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", prep
                              two_colour=tc)
 
 
+def _gw_factor_on() -> bool:
+    return os.environ.get("B2S_GW_FACTOR", "1") != "0"
+
+
+def _symbolic(n: int, b: int, ppat: "D.DevPattern", diag: torch.Tensor):
+    sym = C.c_void_p(None)
+    check(D.lib().b2s_ilu0_symbolic(n, b, D.ptr(ppat.rp), D.ptr(ppat.ci), D.ptr(diag),
+                                    C.byref(sym), D.stream()), "ilu0_symbolic")
+    return sym
+
+
+def _factor_gw(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", g: dict, defer: bool):
+    """Wavefront factorisation of a natural-order grid (csrc/gridwave.cu
+    b2s_gw_factor): straight from the input values into the sweep records;
+    None when it declines (then the general numeric factorisation runs)."""
+    n, b = a.num_block_rows, a.block_size
+    bb = b * b
+    identity, ppat, src, gw, diag, smap = (g["identity"], g["pattern"], g["src"], g["gw"],
+                                           g["diag"], g["smap"])
+    h = gw[0]
+    dev = bsr.pat.rp.device
+    nbytes = int(D.lib().b2s_gw_factor_workspace_bytes(h))
+    ws = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=dev)
+    inv = D.empty_f64(n * bb, dev)
+    dvals = D.empty_f64(n * bb, dev)
+    flags = torch.full((2,), _I32_MAX, dtype=torch.int32, device=dev)
+    flags[1:].zero_()
+    rc = D.lib().b2s_gw_factor(h, D.ptr(ppat.rp), D.ptr(ppat.ci), D.ptr(diag),
+                               None if src is None else D.ptr(src), D.ptr(bsr.vals), D.ptr(inv),
+                               D.ptr(dvals), D.ptr(flags), D.ptr(ws), nbytes, D.stream())
+    if rc == UNSUPPORTED:
+        return None
+    check(rc, "gw_factor")
+    if not defer:
+        bad = int(flags[0].item())
+        if bad != _I32_MAX:
+            raise SingularPivot(bad if identity else
+                                int(plan.device("inverse_permutation")[bad].item()))
+    dtiles = D.empty_f64(smap.nslices * bb * 32, dev)
+    check(D.lib().b2s_diag_tiles(smap.nslices, b, D.ptr(smap.row0), D.ptr(smap.nrows),
+                                 D.ptr(inv), D.ptr(dtiles), D.stream()), "diag_tiles")
+    f = Ilu0Factorization(plan, b, n, None, inv, smap, None, None, dtiles, identity, a,
+                          bsr if identity else None)
+    f._a_src = None if identity else (ppat, src, bsr)
+    f._op_shell = g["op_shell"]
+    f._deferred = flags if defer else None
+    f._gw_lazy = (ppat, src, bsr.vals, diag, dvals)
+    f.gw, f._gw_ws, f.gw_shape = gw
+    return f
+
+
 def prepare_general(a: BlockMatrix, plan: ParallelPlan, pat: "D.DevPattern"):
     """Pattern-only half of the general factorisation: plan-order pattern and
     source map, diagonal positions, slice map, the symbolic factorisation
@@ -350,9 +416,9 @@ def prepare_general(a: BlockMatrix, plan: ParallelPlan, pat: "D.DevPattern"):
     # group-aligned slices: a sweep never waits on a row of its own group
     # (same-group reads take the pre-sweep value, as the reference does)
     smap = plan.slice_map()
-    sym = C.c_void_p(None)
-    check(D.lib().b2s_ilu0_symbolic(n, b, D.ptr(ppat.rp), D.ptr(ppat.ci), D.ptr(diag),
-                                    C.byref(sym), D.stream()), "ilu0_symbolic")
+    # (the wavefront factorisation needs no update pairs; they are computed
+    # later only if it declines)
+    sym = None if (gw is not None and _gw_factor_on()) else _symbolic(n, b, ppat, diag)
     shell = D.DevBSR(ppat, b, D.empty_f64(1, ppat.rp.device))   # pattern only
     return {"identity": identity, "pattern": ppat, "src": src, "gw": gw, "diag": diag,
             "smap": smap, "sym": sym, "op_shell": D.Sell.build(smap, shell, 0, fill=False)}
@@ -379,6 +445,12 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
     if f is not None:
         return f
     g = prep_general or prepare_general(a, plan, bsr.pat)
+    if g["gw"] is not None and _gw_factor_on():
+        f = _factor_gw(a, plan, bsr, g, defer)
+        if f is not None:
+            return f
+    if g["sym"] is None:
+        g["sym"] = _symbolic(n, b, g["pattern"], g["diag"])
     identity, ppat, src, gw = g["identity"], g["pattern"], g["src"], g["gw"]
     diag, smap, sym = g["diag"], g["smap"], g["sym"]
     a_src = None
@@ -547,8 +619,8 @@ def _maybe_tiles(f: Ilu0Factorization, plan: ParallelPlan, diag: torch.Tensor):
     h = C.c_void_p(None)
     rc = D.lib().b2s_tiles_create(n, f._b, T, nx, ny, px, py,
                                   D.ptr(plan.device("inverse_permutation")),
-                                  D.ptr(f._lu.pat.rp), D.ptr(f._lu.pat.ci), D.ptr(diag),
-                                  D.ptr(f._lu.vals), D.ptr(f._invd),
+                                  D.ptr(f.lu_device.pat.rp), D.ptr(f.lu_device.pat.ci), D.ptr(diag),
+                                  D.ptr(f.lu_device.vals), D.ptr(f._invd),
                                   D.ptr(plan.device("group_offsets")), plan.group_count,
                                   C.byref(h), D.stream())
     if rc == 5:   # B2S_UNSUPPORTED: the ring does not fit, keep the sync-free sweeps

@@ -672,6 +672,47 @@ def test_wavefront_sweeps_other_block_sizes(monkeypatch, bs):
         np.testing.assert_array_equal(out["1"], out["0"])
 
 
+@pytest.mark.parametrize("dims,bs", [((20, 20, 10), 3), ((240, 64, 3), 3), ((16, 12, 9), 1),
+                                     ((13, 9, 40), 2)])
+def test_wavefront_factorisation_bit_identical(monkeypatch, dims, bs):
+    """The wavefront ILU0 factorisation (b2s_gw_factor, straight into the
+    sweep records) equals the general numeric factorisation bit for bit:
+    combined L\\U, inverse diagonals, applications and whole solves."""
+    a = P.generate(P.GeneratorSpec(*dims, block_size=bs, seed=8, diagonal_boost=1e-2)).a
+    rhs = P.BlockVector(np.random.default_rng(3).uniform(-1, 1, a.num_block_rows * bs), bs)
+    plan = P.level_schedule(a.pattern)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("B2S_GW_FACTOR", flag)
+        f = P.decompose(a, plan)
+        assert f.gw is not None and (f._gw_lazy is not None) == (flag == "1")
+        lu = f.lu_device.vals[: f.lu_device.pat.nnz * bs * bs].cpu().numpy()
+        inv = f._invd[: a.num_block_rows * bs * bs].cpu().numpy()
+        z = f.apply(rhs).data
+        x, rep = P.bicgstab(P.MatrixOperator(a), f, rhs, stop=P.StoppingCriteria(1e-10, 200))
+        out[flag] = (lu, inv, z, x.data, rep.iterations)
+    for k in range(4):
+        np.testing.assert_array_equal(out["1"][k], out["0"][k])
+    assert out["1"][4] == out["0"][4]
+
+
+def test_wavefront_factorisation_singular_pivot(monkeypatch):
+    """A singular pivot found by the wavefront factorisation raises
+    SingularPivot(input row) as the general factorisation does."""
+    a = P.generate(P.GeneratorSpec(20, 18, 8, seed=2)).a
+    vals = a.values.copy()
+    vals.reshape(-1, 3, 3)[a.pattern.position(0, 0)] = 0.0   # corner row: U_00 = A_00
+    a = P.BlockMatrix(a.pattern, 3, vals)
+    plan = P.level_schedule(a.pattern)
+    rows = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("B2S_GW_FACTOR", flag)
+        with pytest.raises(P.SingularPivot) as err:
+            P.decompose(a, plan)
+        rows[flag] = err.value.row
+    assert rows["1"] == rows["0"] == 0
+
+
 def test_wavefront_declines_non_stencil_rows(monkeypatch):
     """A pattern that is not a 7-point stencil of its grid keeps the sync-free
     sweeps (the packing kernel verifies every row)."""
