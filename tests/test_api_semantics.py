@@ -107,3 +107,31 @@ def test_staged_pageable_upload_is_exact():
     x2, r2 = P.solve_with_fallback(cfg, P.pin_host(g.a), P.pin_host(g.rhs))
     assert_array_equal(x1.data, x2.data)
     assert r1.iterations == r2.iterations
+
+
+@pytest.mark.gpu
+def test_concurrent_solves_from_threads_match_sequential():
+    """Independent systems solved concurrently from several host threads (the
+    reference CLI's --parallel pool; SURVEY 8(b) "threading") give exactly
+    the results of one-at-a-time solves: no shared mutable state on the
+    solve path beyond thread-safe pools."""
+    import concurrent.futures as cf
+    cases = []
+    for k, (dims, backend) in enumerate([((14, 12, 9), P.Backend.GRAPH_COLORED),
+                                         ((20, 18, 12), P.Backend.LEVEL_SCHEDULED),
+                                         ((16, 16, 6), P.Backend.REFERENCE_SEQUENTIAL),
+                                         ((30, 10, 8), P.Backend.GRAPH_COLORED)]):
+        g = P.generate(P.GeneratorSpec(*dims, seed=20 + k, well_count=1, well_depth=2))
+        cases.append((P.SolverConfig(backend=backend, stop=P.StoppingCriteria(1e-9, 300)),
+                      g.a, g.rhs, g.wells))
+
+    def run(case):
+        cfg, a, b, w = case
+        x, rep = P.solve_with_fallback(cfg, a, b, w)
+        return x.data.copy(), rep.iterations
+    seq = [run(c) for c in cases]
+    with cf.ThreadPoolExecutor(max_workers=4) as ex:
+        par = list(ex.map(run, cases * 3))
+    for i, (x, its) in enumerate(par):
+        assert_array_equal(x, seq[i % len(cases)][0])
+        assert its == seq[i % len(cases)][1]
