@@ -1,7 +1,7 @@
 """Level-plan setup on C4 (plan, factor, layouts, wavefront packing): CUDA
 events per phase, previous solver freed first (as in bench.py).
 
-python tools/setup_level_probe.py
+python tools/setup_level_probe.py [level|color]
 """
 import json
 import os
@@ -18,10 +18,11 @@ from paper_2309_11488_b200.bridge import DeviceSolver  # noqa: E402
 
 a = P.generate(P.GeneratorSpec(100, 100, 100, seed=0)).a
 bsr = D.DevBSR.upload(a)
-cfg = P.SolverConfig(backend=P.Backend.LEVEL_SCHEDULED)
+backend = sys.argv[1] if len(sys.argv) > 1 else "level"
+cfg = P.SolverConfig(backend=P.Backend.from_name(backend))
 st = torch.cuda.current_stream()
 out = {}
-for gw in ("1", "0"):
+for gw in (("1", "0") if backend == "level" else ("1",)):
     os.environ["B2S_GW"] = gw
     ts = []
     solver = None
@@ -57,7 +58,7 @@ def timed_gw(*args):
 
 
 I._gw_plan = timed_gw
-for _ in range(4):
+for _ in range(4 if backend == "level" else 0):
     solver = None
     solver = DeviceSolver(a, bsr, cfg).setup()
 print(json.dumps({"gw_plan_ms": [round(t, 3) for t in rec]}))

@@ -92,3 +92,18 @@ for r in rows:
     print(json.dumps(r))
 gpu = sum(e.device_time_total for e in prof.key_averages() if e.device_time_total) / 1e3
 print(json.dumps({"gpu_kernel_ms_total": round(gpu, 3)}))
+# device timeline: idle gaps between consecutive GPU activities (what the
+# host synchronisations cost), with the activity that ended each gap
+dev = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
+             key=lambda e: e.time_range.start)
+if dev:
+    t0, last_end = dev[0].time_range.start, dev[0].time_range.end
+    idle = 0.0
+    for e in dev[1:]:
+        gap = e.time_range.start - last_end
+        if gap > 5:
+            idle += gap
+            print(json.dumps({"gap_us": round(gap, 1), "at_us": round(e.time_range.start - t0, 1),
+                              "next": e.name[:60]}))
+        last_end = max(last_end, e.time_range.end)
+    print(json.dumps({"span_us": round(last_end - t0, 1), "idle_us": round(idle, 1)}))
