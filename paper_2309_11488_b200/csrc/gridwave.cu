@@ -428,7 +428,7 @@ __host__ __device__ inline int gw_rec_fac(int b) {
 // pack the factor records and the backward records' upper blocks straight
 // from the input values (vsrc: plan-order slot -> input slot, null: same)
 template <int B>
-__global__ void k_gw_apack(GwDev g, const int32_t* __restrict__ src,
+__global__ void __launch_bounds__(256, 4) k_gw_apack(GwDev g, const int32_t* __restrict__ src,
                            const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                            const int32_t* __restrict__ diag, const int32_t* __restrict__ vsrc,
                            const double* __restrict__ vin, char* __restrict__ fac) {
@@ -468,14 +468,19 @@ __global__ void k_gw_apack(GwDev g, const int32_t* __restrict__ src,
       pa[3 + k] = src[nslot * 6 * 32 + (5 - k) * 32 + nxl + g.wx * nyl];   // kinds 5,4,3
     }
     pa[6] = pr >= 0 ? diag[pr] : -1;
-    double v[NE];
+    // input offsets of the seven blocks, then the elements streamed through
+    // in record order (a few in flight, not all 63: occupancy)
+    const double* bp[kGwFacBlocks];
 #pragma unroll
     for (int j = 0; j < kGwFacBlocks; ++j)
+      bp[j] = pa[j] >= 0 ? vin + (vsrc ? (long long)vsrc[pa[j]] : pa[j]) * BB : nullptr;
 #pragma unroll
-      for (int e = 0; e < BB; ++e) v[j * BB + e] = val(pa[j], e);
-    if (NE > kGwFacBlocks * BB) v[NE - 1] = 0.0;
-#pragma unroll
-    for (int e = 0; e < NE; e += 2) fv[(e >> 1) * 32] = make_double2(v[e], v[e + 1]);
+    for (int e = 0; e < NE; e += 2) {
+      const int j0 = e / BB, j1 = (e + 1) / BB;
+      const double v0 = bp[j0] ? bp[j0][e - j0 * BB] : 0.0;
+      const double v1 = (e + 1 < kGwFacBlocks * BB && bp[j1]) ? bp[j1][e + 1 - j1 * BB] : 0.0;
+      fv[(e >> 1) * 32] = make_double2(v0, v1);
+    }
     for (int k = 3; k < 6; ++k) {
       const int p = mt >= 0 ? sp[k * 32] : -1;
       for (int e = 0; e < BB; ++e) Uv[gw_eidx((k - 3) * BB + e, lane)] = val(p, e);

@@ -1,7 +1,7 @@
 """Phase times of the end-to-end C4 solve through solve_with_fallback
 (host arrays in, host x out), page-locked or pageable inputs.
 
-python tools/e2e_phases.py [pinned|pageable] [steps]
+python tools/e2e_phases.py [pinned|pageable] [steps] [color|level]
 Prints one JSON line per step: wall ms and {phase: (host_ms, gpu_ms)}
 (paper_2309_11488_b200/trace.py; B2S_TRACE is switched on here).
 """
@@ -24,7 +24,8 @@ g = P.generate(P.GeneratorSpec(100, 100, 100, seed=0))
 a, rhs = g.a, g.rhs
 if mode == "pinned":
     a, rhs = P.pin_host(a), P.pin_host(rhs)
-cfg = P.SolverConfig(backend=P.Backend.GRAPH_COLORED, stop=P.StoppingCriteria(1e-8, 200))
+backend = sys.argv[3] if len(sys.argv) > 3 else "color"
+cfg = P.SolverConfig(backend=P.Backend.from_name(backend), stop=P.StoppingCriteria(1e-8, 200))
 if os.environ.get("E2E_MEMHIST"):
     torch.cuda.memory._record_memory_history(max_entries=200000)
 for i in range(steps + 2):
@@ -40,7 +41,7 @@ for i in range(steps + 2):
     alloc["allocated_gb"] = round(m1.get("allocated_bytes.all.current", 0) / 2**30, 3)
     if i >= 2:
         ph = {k: [round(v[0], 3), round(v[1], 3)] for k, v in (rep.phases or {}).items()}
-        print(json.dumps({"mode": mode, "wall_ms": round(ms, 3), "iterations": rep.iterations,
+        print(json.dumps({"mode": mode, "backend": backend, "wall_ms": round(ms, 3), "iterations": rep.iterations,
                           "phases": ph, "allocator": alloc}))
 if os.environ.get("E2E_MEMHIST"):
     # the live blocks after the last step, largest first, with their stacks
