@@ -122,6 +122,48 @@ __global__ void k_sell_fill(int nslices, int bb, const int32_t* __restrict__ row
   }
 }
 
+// sel 0 (every block): the k-th slot of a row is its k-th CSR entry, so each
+// (slice, k, lane) is independent -- one thread per slot, all loads of the
+// pass in flight at once (the sequential per-row loop above waits on a
+// dependent index -> value chain per entry).  CTA = 32 lanes x 8 slots of a
+// slice; wider slices loop.
+template <int BB>
+__global__ void __launch_bounds__(256) k_sell_fill_all(int nslices, const int32_t* __restrict__ row0,
+                                                       const int32_t* __restrict__ nrows,
+                                                       const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci,
+                                                       const double* __restrict__ vals,
+                                                       const int32_t* __restrict__ sp,
+                                                       int32_t* __restrict__ ocols,
+                                                       double* __restrict__ ovals,
+                                                       const int32_t* __restrict__ src) {
+  const int lane = threadIdx.x & 31;
+  for (int s = blockIdx.x; s < nslices; s += gridDim.x) {
+    const long long slot0 = sp[s];
+    const int width = (sp[s + 1] - sp[s]) / kSlice;
+    const bool live = lane < nrows[s];
+    const int row = row0[s] + lane;
+    const int q0 = live ? rp[row] : 0, len = live ? rp[row + 1] - q0 : 0;
+    for (int k = threadIdx.x >> 5; k < width; k += blockDim.x >> 5) {
+      double v[BB];
+      int c = -1;
+      if (k < len) {
+        const int q = q0 + k;
+        c = ci[q];
+        const long long qv = src ? src[q] : q;
+#pragma unroll
+        for (int e = 0; e < BB; ++e) v[e] = vals[qv * BB + e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < BB; ++e) v[e] = 0.0;
+      }
+      ocols[slot0 + 32ll * k + lane] = c;
+#pragma unroll
+      for (int e = 0; e < BB; ++e) ovals[vidx(slot0, k, e, lane, BB)] = v[e];
+    }
+  }
+}
+
 // per-slice b*b x 32 tiles of the inverse diagonal (row order of the map)
 __global__ void k_diag_tiles(int nslices, int bb, const int32_t* __restrict__ row0,
                              const int32_t* __restrict__ nrows, const double* __restrict__ inv,
@@ -405,9 +447,19 @@ int b2s_sell_fill_src(int nslices, int b, const int32_t* row0, const int32_t* nr
                       double* svals, const int32_t* src, cudaStream_t st) {
   if (nslices < 0 || b < 1 || sel < 0 || sel > 2) return B2S_SHAPE;
   if (nslices == 0) return B2S_OK;
-  k_sell_fill<<<grid_for((long long)nslices * 32), 256, 0, st>>>(nslices, b * b, row0, nrows, rp,
-                                                                  ci, vals, sel, sp, goff, ngroups,
-                                                                  cols, svals, src);
+  if (sel == 0 && !goff && b <= 4) {   // every block: one thread per slot
+    const int g = nslices < kSms * 32 ? nslices : kSms * 32;
+    switch (b) {
+      case 1: k_sell_fill_all<1><<<g, 256, 0, st>>>(nslices, row0, nrows, rp, ci, vals, sp, cols, svals, src); break;
+      case 2: k_sell_fill_all<4><<<g, 256, 0, st>>>(nslices, row0, nrows, rp, ci, vals, sp, cols, svals, src); break;
+      case 3: k_sell_fill_all<9><<<g, 256, 0, st>>>(nslices, row0, nrows, rp, ci, vals, sp, cols, svals, src); break;
+      default: k_sell_fill_all<16><<<g, 256, 0, st>>>(nslices, row0, nrows, rp, ci, vals, sp, cols, svals, src); break;
+    }
+  } else {
+    k_sell_fill<<<grid_for((long long)nslices * 32), 256, 0, st>>>(nslices, b * b, row0, nrows, rp,
+                                                                    ci, vals, sel, sp, goff, ngroups,
+                                                                    cols, svals, src);
+  }
   B2S_LAUNCH_CHECK();
   return B2S_OK;
 }
