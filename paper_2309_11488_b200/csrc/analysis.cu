@@ -452,6 +452,30 @@ __global__ void k_permute_cols(int n, const int32_t* __restrict__ rp,
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int o = take[k];
     const int s = rp[o], len = rp[o + 1] - s, d = nrp[k];
+    if (len <= 8) {
+      // short rows (stencils): sort (column, source) pairs in registers with
+      // a fixed odd-even transposition network, one write per entry; padding
+      // keys sort last and the network is stable for equal keys -- columns
+      // of a row are distinct anyway
+      int key[8], val[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        key[t] = t < len ? cmap[ci[s + t]] : 0x7fffffff;
+        val[t] = s + t;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int t = r & 1; t + 1 < 8; t += 2)
+          if (key[t] > key[t + 1]) {
+            const int k2 = key[t]; key[t] = key[t + 1]; key[t + 1] = k2;
+            const int v2 = val[t]; val[t] = val[t + 1]; val[t + 1] = v2;
+          }
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t < len) { nci[d + t] = key[t]; src[d + t] = val[t]; }
+      continue;
+    }
     for (int t = 0; t < len; ++t) {
       const int c = cmap[ci[s + t]];
       int u = t;
