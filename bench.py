@@ -599,6 +599,27 @@ def run_single(args):
         dtp = (time.perf_counter() - t0) / reps
         e2e["pageable"] = {"value": n / dtp / 1e6, "ms_per_step": dtp * 1e3,
                            "converged": bool(rep.converged)}
+        # a simulator's Newton loop: same pattern, new values every solve --
+        # SolveSession analyses the pattern once (outside the timed region);
+        # every step uploads values + rhs (page-locked), factorises, solves
+        # and downloads x.  Reported beside e2e, not instead of it.
+        sess = P.SolveSession(cfg, a_h.pattern, b)
+        for _ in range(2):
+            xh, rep = sess.solve(a_h, rhs_h)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s_conv = True
+        for _ in range(reps):
+            xh = None
+            xh, rep = sess.solve(a_h, rhs_h)
+            s_conv &= rep.converged
+        torch.cuda.synchronize()
+        dts = (time.perf_counter() - t0) / reps
+        sess.close()
+        e2e["values_refresh"] = {"value": n / dts / 1e6, "ms_per_step": dts * 1e3,
+                                 "h2d_bytes_per_step": nnz * 72 + 24 * n,
+                                 "d2h_bytes_per_step": 24 * n, "converged": s_conv,
+                                 "api": "SolveSession.solve (pattern analysed once)"}
 
     cpu = None
     if not args.no_cpu:

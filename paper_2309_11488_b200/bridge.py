@@ -100,18 +100,23 @@ class DeviceSolver:
         self.plan: ParallelPlan | None = None
 
     def setup(self, backend: Backend | None = None, two_colour: bool = True,
-              defer: bool = True):
+              defer: bool = True, pattern_phase=None):
         """``defer``: the factorisation's pivot check is read after the solve
-        (solve() raises SingularPivot then); False raises it here."""
+        (solve() raises SingularPivot then); False raises it here.
+        ``pattern_phase``: (plan, prep, prep_general) kept by a SolveSession
+        from an earlier solve on the same pattern."""
         backend = backend or self.cfg.backend
         self._backend = backend
         with trace.phase("analysis"):
-            self.plan = plan_device(backend, self.pre_bsr.pat)
-            # the pattern-only part of the factorisation, also before the values
-            prep = (prepare_two_colour(self.pre_matrix, self.plan, self.pre_bsr.pat)
-                    if two_colour else None)
-            prep_g = (prepare_general(self.pre_matrix, self.plan, self.pre_bsr.pat)
-                      if prep is None else None)
+            if pattern_phase is not None:
+                self.plan, prep, prep_g = pattern_phase
+            else:
+                self.plan = plan_device(backend, self.pre_bsr.pat)
+                # the pattern-only part of the factorisation, also before the values
+                prep = (prepare_two_colour(self.pre_matrix, self.plan, self.pre_bsr.pat)
+                        if two_colour else None)
+                prep_g = (prepare_general(self.pre_matrix, self.plan, self.pre_bsr.pat)
+                          if prep is None else None)
         with trace.phase("wait_values"):
             self.pre_bsr.wait_values()   # values may still be in flight (overlapped upload)
             self.bsr.wait_values()
@@ -303,3 +308,132 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
     if not report.converged:
         raise SolveFailed(primary, report)
     return D.to_host_vector(xd, n * bs, bs), report
+
+
+class _PatternStandIn:
+    """What the pattern-only setup reads of a BlockMatrix (n, b, pattern)."""
+
+    def __init__(self, pattern, block_size: int):
+        self.pattern = pattern
+        self.num_block_rows = pattern.num_block_rows
+        self.block_size = block_size
+
+    def as_block_row_major(self):
+        return self
+
+
+class SolveSession:
+    """Repeated solves on one sparsity pattern -- a simulator's Newton loop,
+    where every linear system has the same structure and new values.
+
+    The pattern phase of ``solve_with_fallback`` (index upload, plan,
+    permutation, slice maps, layout sizes, symbolic factorisation, the
+    wavefront packing pattern) runs once, at construction; each ``solve``
+    uploads only the block values and the right-hand side and runs the value
+    phase (factorisation, layout fill) and the Krylov loop.  Results, reports
+    and exceptions are those of ``solve_with_fallback(cfg, a, b, wells, x0)``
+    bit for bit: a primary failure (singular pivot, no convergence) and
+    systems the session cannot serve (another pattern, COUPLED wells, which
+    fold into the matrix) go through ``solve_with_fallback`` itself.  (The
+    reference has no such object: it re-analyses every call; this is the
+    device-side analogue of its ``refresh_values`` reuse for partitions,
+    ``bs/jacobi.py:139-147``.)"""
+
+    def __init__(self, cfg: SolverConfig, pattern, block_size: int = 3):
+        from .blockcore import SparsityPattern
+        if not isinstance(pattern, SparsityPattern):
+            raise TypeError("SolveSession needs a SparsityPattern")
+        self.cfg, self.pattern, self.b = cfg, pattern, int(block_size)
+        D.require_cuda()
+        if cfg.jacobi_partitions > 0:
+            self._phase = None       # (the relaxed operator depends on values)
+            return
+        n, bb = pattern.num_block_rows, self.b * self.b
+        pat = D.DevPattern.upload(pattern)
+        self.bsr = D.DevBSR(pat, self.b, torch.empty(max(pattern.num_blocks, 1) * bb,
+                                                     dtype=torch.float64, device=pat.rp.device))
+        stand = _PatternStandIn(pattern, self.b)
+        plan = plan_device(cfg.backend, pat)
+        prep = prepare_two_colour(stand, plan, pat)
+        prep_g = prepare_general(stand, plan, pat) if prep is None else None
+        if prep_g is not None:
+            prep_g["persistent"] = True
+        self._phase = (plan, prep, prep_g)
+        self._n = n
+
+    def close(self):
+        phase, self._phase = getattr(self, "_phase", None), None
+        if phase is None:
+            return
+        g = phase[2]
+        if g is not None:
+            if g.get("sym") is not None:
+                D.lib().b2s_ilu0_symbolic_free(g["sym"], D.stream())
+                g["sym"] = None
+            if g.get("gw") is not None:
+                D.lib().b2s_gw_destroy(g["gw"][0])
+                g["gw"] = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _serves(self, a: BlockMatrix, wells) -> bool:
+        if self._phase is None or a.block_size != self.b:
+            return False
+        if wells is not None and not wells.is_empty and self.cfg.well_mode is WellMode.COUPLED:
+            return False
+        p = a.pattern
+        return p is self.pattern or (
+            p.num_block_rows == self.pattern.num_block_rows
+            and np.array_equal(p.row_pointers, self.pattern.row_pointers)
+            and np.array_equal(p.column_indices, self.pattern.column_indices))
+
+    def solve(self, a: BlockMatrix, b: BlockVector, wells=None,
+              x0: BlockVector | None = None) -> tuple[BlockVector, SolveReport]:
+        from .errors import ShapeError
+        if not self._serves(a, wells):
+            return solve_with_fallback(self.cfg, a, b, wells, x0)
+        cfg = self.cfg
+        a_sys = a.as_block_row_major()
+        n, bs = a_sys.num_block_rows, a_sys.block_size
+        if b.block_size != bs or b.num_blocks != n:
+            raise ShapeError("right-hand side does not match the operator")
+        if x0 is not None and (x0.block_size != bs or x0.num_blocks != n):
+            raise ShapeError("initial guess does not match the right-hand side")
+        sep = None
+        if wells is not None and not wells.is_empty:
+            sep = WellSet(wells.standard, wells.multisegment, WellMode.SEPARATE)
+        t0 = time.perf_counter()
+        dev = self.bsr.vals.device
+        src = torch.from_numpy(a_sys.values)
+        nv = src.numel()
+        if D.is_pinned(src) or nv * 8 < D.STAGE_MIN_BYTES:
+            self.bsr.vals[:nv].copy_(src, non_blocking=D.is_pinned(src))
+        else:
+            D.staged_copy(self.bsr.vals[:nv], src, torch.cuda.current_stream(dev))
+        rhs = D.to_device(torch.from_numpy(np.ascontiguousarray(b.data, dtype=np.float64)), dev)
+        x0d = (torch.zeros(n * bs, dtype=torch.float64, device=dev) if x0 is None
+               else D.to_device(torch.from_numpy(np.ascontiguousarray(x0.data)), dev))
+        try:
+            solver = DeviceSolver(a_sys, self.bsr, cfg, wells=sep).setup(
+                pattern_phase=self._phase)
+            norm0 = RefNorm(_initial_residual(self.bsr, rhs, None if x0 is None else x0d, sep),
+                            n * bs)
+            e_setup = torch.cuda.Event(enable_timing=True)
+            e_setup.record()
+            xd = x0d.clone()
+            res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None)
+            e_end = torch.cuda.Event(enable_timing=True)
+            e_end.record()
+            _sync()
+            rep = _report(res, e_setup.elapsed_time(e_end) / 1e3, solver.plan.group_count,
+                          norm0.value())
+            rep.setup_elapsed = max((time.perf_counter() - t0) - rep.elapsed, 0.0)
+        except SingularPivot:
+            return solve_with_fallback(cfg, a, b, wells, x0)
+        if not rep.converged:
+            return solve_with_fallback(cfg, a, b, wells, x0)
+        return D.to_host_vector(xd, n * bs, bs), rep

@@ -257,7 +257,7 @@ class Ilu0Factorization:
         return self.apply_array(r)
 
     def __del__(self):
-        if getattr(self, "gw", None):
+        if getattr(self, "gw", None) and getattr(self, "_gw_owner", True):
             try:
                 D.lib().b2s_gw_destroy(self.gw)
             except Exception:
@@ -390,6 +390,7 @@ def _factor_gw(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR", g: dict, def
     f._deferred = flags if defer else None
     f._gw_lazy = (ppat, src, bsr.vals, diag, dvals)
     f.gw, f._gw_ws, f.gw_shape = gw
+    f._gw_owner = not g.get("persistent")
     return f
 
 
@@ -487,8 +488,9 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
                 raise SingularPivot(row)
         check(rc, "ilu0_numeric")
     finally:
-        D.lib().b2s_ilu0_symbolic_free(sym, D.stream())
-        g["sym"] = None
+        if not g.get("persistent"):   # (a SolveSession keeps it for the next values)
+            D.lib().b2s_ilu0_symbolic_free(sym, D.stream())
+            g["sym"] = None
     goff = plan.device("group_offsets")
     lower = upper = None
     if gw is None:   # (the wavefront sweeps read their own packed records)
@@ -503,6 +505,7 @@ def factor_device(a: BlockMatrix, plan: ParallelPlan, bsr: "D.DevBSR" = None,
     f._deferred = flags
     _maybe_tiles(f, plan, diag)
     _gw_fill(f, gw)
+    f._gw_owner = not g.get("persistent")
     return f
 
 

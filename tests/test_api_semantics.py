@@ -135,3 +135,46 @@ def test_concurrent_solves_from_threads_match_sequential():
     for i, (x, its) in enumerate(par):
         assert_array_equal(x, seq[i % len(cases)][0])
         assert its == seq[i % len(cases)][1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("backend", [P.Backend.GRAPH_COLORED, P.Backend.LEVEL_SCHEDULED,
+                                     P.Backend.REFERENCE_SEQUENTIAL])
+def test_solve_session_equals_solve_with_fallback(backend):
+    """A SolveSession (pattern phase once, values per solve) returns exactly
+    what solve_with_fallback returns for each system: several value sets on
+    one pattern, with wells and an initial guess, a singular system (through
+    the fallback) and a system on another pattern (delegated)."""
+    g = P.generate(P.GeneratorSpec(20, 18, 12, seed=3, well_count=2, well_depth=3))
+    cfg = P.SolverConfig(backend=backend, stop=P.StoppingCriteria(1e-9, 300))
+    sess = P.SolveSession(cfg, g.a.pattern, 3)
+    rng = np.random.default_rng(5)
+    for k in range(3):
+        vals = g.a.values * (1.0 + 0.05 * rng.standard_normal(g.a.values.size))
+        a = P.BlockMatrix(g.a.pattern, 3, vals)
+        b = P.BlockVector(rng.uniform(-1, 1, g.rhs.data.size), 3)
+        x0 = None if k == 0 else P.BlockVector(rng.uniform(-1, 1, b.data.size) * 1e-3, 3)
+        w = g.wells if k == 2 else None
+        x1, r1 = sess.solve(a, b, w, x0)
+        x2, r2 = P.solve_with_fallback(cfg, a, b, w, x0)
+        assert_array_equal(x1.data, x2.data)
+        assert (r1.iterations, r1.converged, r1.fallback_used) == \
+            (r2.iterations, r2.converged, r2.fallback_used)
+        assert r1.initial_norm == r2.initial_norm and r1.final_norm == r2.final_norm
+    # a pivot that is exactly zero at the corner row: both take the fallback path
+    vals = g.a.values.copy()
+    vals.reshape(-1, 3, 3)[g.a.pattern.position(0, 0)] = 0.0
+    a = P.BlockMatrix(g.a.pattern, 3, vals)
+    try:
+        x2, r2 = P.solve_with_fallback(cfg, a, g.rhs)
+        x1, r1 = sess.solve(a, g.rhs)
+        assert_array_equal(x1.data, x2.data) and r1.fallback_used == r2.fallback_used
+    except P.SolveFailed:
+        with pytest.raises(P.SolveFailed):
+            sess.solve(a, g.rhs)
+    # another pattern: delegated
+    h = P.generate(P.GeneratorSpec(8, 7, 6, seed=4))
+    x1, r1 = sess.solve(h.a, h.rhs)
+    x2, r2 = P.solve_with_fallback(cfg, h.a, h.rhs)
+    assert_array_equal(x1.data, x2.data)
+    sess.close()
