@@ -45,12 +45,11 @@ __global__ void k_find_diag(int n, const int32_t* __restrict__ rp,
 }
 
 // ---------------------------------------------------------------------------
-// Neighbour lists of up to kNb entries are held in registers and all their
+// Neighbour lists of up to kLNb / kCNb entries are held in registers and all their
 // published values are polled in one round per pass (one L2 round trip per
 // dependency level instead of one per neighbour); longer lists fall back to
 // a one-at-a-time walk.  A warp keeps polling while any lane still waits, so
 // lanes of one slice may depend on each other (natural order).
-constexpr int kNb = 8;
 
 // level(i) = 1 + max level(j) over strict-lower j, 0 without lower
 // neighbours (bs/analysis.py:85-100).  level[] must be -1 on entry.

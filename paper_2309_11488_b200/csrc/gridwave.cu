@@ -57,7 +57,6 @@ constexpr int kGwRingB = 6;   // backward ring stages
 // shared memory allows 3 CTAs per SM, these 7)
 constexpr int kGwRingFs = 4;
 constexpr int kGwRingBs = 3;
-constexpr int kGwEdgeAhead = 1;   // steps of look-ahead for the neighbour tiles' edge values
 
 __device__ __forceinline__ double gw_ld_relaxed(const double* p) {
   double v;

@@ -40,7 +40,6 @@ struct WellsDev {
   const double* cvals;
 };
 
-constexpr int kMaxS = 64;   // t1/t2 held per lane: nseg*M <= 32 * kMaxS
 
 // pass 1: t2 of well w (one warp)
 __global__ void k_wells_t2(WellsDev W, const double* __restrict__ x, double* __restrict__ t2,
