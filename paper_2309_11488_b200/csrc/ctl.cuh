@@ -222,8 +222,10 @@ __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const do
       st->alpha = st->rho / a;
       return;
     }
-    case kCtlS: {  // x has been advanced by alpha p^; test |s|  (bs/krylov.py:211-220)
+    case kCtlS: {  // test |s|  (bs/krylov.py:211-220); x advanced by alpha p^ here or,
+                   // deferred, in the r-update (k_x_fixup after an exit in between)
       st->its += 0.5;
+      st->xpend = 1;
       const double ns = sqrt(a);
       if (!isfinite(ns)) { ctl_finish(st, c.host_done, kNumerical); return; }
       if (ns <= st->target) { st->final_norm = ns; ctl_finish(st, c.host_done, kConverged); }

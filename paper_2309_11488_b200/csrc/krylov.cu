@@ -320,6 +320,9 @@ __device__ __forceinline__ void s_elem(double rv, double vv, double ph, double& 
   acc = fma(so, so, acc);
 }
 
+// XU = false: x is left alone (x += alpha p^ deferred to the r-update,
+// State.xpend): two vectors fewer to stream
+template <bool XU>
 __global__ void __launch_bounds__(256, 4) k_s_update(long long m, const State* st,
                                                   const double* __restrict__ r,
                                                   const double* __restrict__ v, double* phat,
@@ -342,8 +345,11 @@ __global__ void __launch_bounds__(256, 4) k_s_update(long long m, const State* s
     for (int u = 0; u < kU; ++u) {
       const long long q = j + u * T;
       if (q < m2) {
-        rv[u] = ld2(r, q); vv[u] = ld2(v, q); ph[u] = ld2(phat, q);
-        xv[u] = reinterpret_cast<const double2*>(x)[q];
+        rv[u] = ld2(r, q); vv[u] = ld2(v, q);
+        if (XU) {
+          ph[u] = ld2(phat, q);
+          xv[u] = reinterpret_cast<const double2*>(x)[q];
+        }
       }
     }
 #pragma unroll
@@ -351,17 +357,29 @@ __global__ void __launch_bounds__(256, 4) k_s_update(long long m, const State* s
       const long long q = j + u * T;
       if (q < m2) {
         double s0, s1;
-        s_elem(rv[u].x, vv[u].x, ph[u].x, xv[u].x, s0, alpha, acc);
-        s_elem(rv[u].y, vv[u].y, ph[u].y, xv[u].y, s1, alpha, acc);
+        if (XU) {
+          s_elem(rv[u].x, vv[u].x, ph[u].x, xv[u].x, s0, alpha, acc);
+          s_elem(rv[u].y, vv[u].y, ph[u].y, xv[u].y, s1, alpha, acc);
+          st2(x, q, xv[u].x, xv[u].y);
+        } else {
+          s0 = bicg_axpy(rv[u].x, alpha, vv[u].x);
+          acc = fma(s0, s0, acc);
+          s1 = bicg_axpy(rv[u].y, alpha, vv[u].y);
+          acc = fma(s1, s1, acc);
+        }
         st2(s, q, s0, s1);
-        st2(x, q, xv[u].x, xv[u].y);
         if (reset) st2(phat, q, sentinel(), sentinel());
       }
     }
   }
   if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     double s0;
-    s_elem(r[m - 1], v[m - 1], phat[m - 1], x[m - 1], s0, alpha, acc);
+    if (XU) {
+      s_elem(r[m - 1], v[m - 1], phat[m - 1], x[m - 1], s0, alpha, acc);
+    } else {
+      s0 = bicg_axpy(r[m - 1], alpha, v[m - 1]);
+      acc = fma(s0, s0, acc);
+    }
     s[m - 1] = s0;
     if (reset) phat[m - 1] = sentinel();
   }
@@ -595,6 +613,11 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   const bool vecf = fused && (fv_env ? fv_env[0] == '1' : a->n <= 400000);
   // sync-free sweeps need sentinel-filled outputs (not the wavefront sweeps)
   const int reset = (ilu && !phased && !a->gw) ? 1 : 0;
+  // x += alpha p^ deferred from the s-update to the r-update (one x pass per
+  // iteration instead of two, the same two roundings; k_x_fixup after a
+  // half-step exit) -- not with sync-free sweeps (their s-update refills p^)
+  const char* xd_env = getenv("B2S_XDEFER");
+  const bool xdefer = ilu && !vecf && !reset && !(xd_env && xd_env[0] == '0');
   MeshDev md{};
   MeshHalo mh{};
   if (mesh && !ilu) return B2S_UNSUPPORTED;   // sharded solves are block-Jacobi ILU0
@@ -860,8 +883,8 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                     Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl && !wells, wf);
         ++kernels;
       }
-      launch_k(k_s_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
-               (const double*)r, (const double*)v, ph, a->x, s, pss, reset,
+      launch_k(xdefer ? k_s_update<false> : k_s_update<true>, dim3(grid_v), dim3(256), 0, cs, pdl,
+               m, (const State*)state, (const double*)r, (const double*)v, ph, a->x, s, pss, reset,
                Ctl{state, counters + 1, dev_done, kCtlS, md});
       ++kernels;
       if (fused) {
@@ -907,9 +930,11 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                     Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl && !wells, wf);
         ++kernels;
       }
-      launch_k(k_r_update<false>, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state, sh,
-               (const double*)t, (const double*)s, (const double*)rhat, a->x, r, prr, prho, reset,
-               Ctl{state, counters + 3, dev_done, kCtlEndBegin, md}, (const double*)nullptr);
+      launch_k(xdefer ? k_r_update<true> : k_r_update<false>, dim3(grid_v), dim3(256), 0, cs, pdl,
+               m, (const State*)state, sh, (const double*)t, (const double*)s,
+               (const double*)rhat, a->x, r, prr, prho, reset,
+               Ctl{state, counters + 3, dev_done, kCtlEndBegin, md},
+               xdefer ? (const double*)ph : (const double*)nullptr);
       ++kernels;
     }
     if (cudaStreamEndCapture(cs, &graph) != cudaSuccess) { status = B2S_CUDA_ERROR; break; }
@@ -980,7 +1005,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if (status != B2S_OK) return status;
   res->kernels_per_iteration = kernels;
 
-  if (vecf)   // an exit between the s half-step and the r-update: x += alpha p^
+  if (vecf || xdefer)   // an exit between the s half-step and the r-update: x += alpha p^
     k_x_fixup<<<grid_v, 256, 0, user>>>(m, state, phat, a->x);
   B2S_CHECK(cudaMemcpyAsync(&hs, state, sizeof(State), cudaMemcpyDeviceToHost, user));
   B2S_CHECK(cudaStreamSynchronize(user));
@@ -1154,7 +1179,7 @@ int b2s_vec_s(long long m, double alpha, const double* r, const double* v, doubl
   int rc;
   State* d = stage_state(scratch, 0, alpha, 0.0, 0.0, st, &rc);
   if (rc) return rc;
-  k_s_update<<<nparts, 256, 0, st>>>(m, d, r, v, phat, x, s, parts, reset, Ctl{});
+  k_s_update<true><<<nparts, 256, 0, st>>>(m, d, r, v, phat, x, s, parts, reset, Ctl{});
   B2S_LAUNCH_CHECK();
   return B2S_OK;
 }
