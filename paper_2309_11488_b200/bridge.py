@@ -337,7 +337,9 @@ class SolveSession:
     fold into the matrix) go through ``solve_with_fallback`` itself.  (The
     reference has no such object: it re-analyses every call; this is the
     device-side analogue of its ``refresh_values`` reuse for partitions,
-    ``bs/jacobi.py:139-147``.)"""
+    ``bs/jacobi.py:139-147``.)  A session holds device buffers for one
+    system at a time: use one session per thread (independent sessions and
+    ``solve_with_fallback`` calls may run concurrently)."""
 
     def __init__(self, cfg: SolverConfig, pattern, block_size: int = 3):
         from .blockcore import SparsityPattern
