@@ -721,3 +721,21 @@ def test_wavefront_declines_non_stencil_rows(monkeypatch):
     m = S.generate_masked(14, 16, 8, seed=11).a
     f = P.decompose(m, P.level_schedule(m.pattern))
     assert f.gw is None
+
+
+@pytest.mark.parametrize("bs", [1, 2, 4])
+@pytest.mark.parametrize("strategy,backend", [("color", P.Backend.GRAPH_COLORED),
+                                              ("level", P.Backend.LEVEL_SCHEDULED)])
+def test_solve_other_block_sizes_against_oracle(bs, strategy, backend):
+    """Whole solves through solve_with_fallback for b = 1, 2, 4 (every
+    device path is templated on b <= 4) against the oracle port: the same
+    iteration count and solution to 1e-9."""
+    g = P.generate(P.GeneratorSpec(18, 14, 9, block_size=bs, seed=40 + bs, diagonal_boost=0.5))
+    a, rhs = g.a, g.rhs
+    cfg = P.SolverConfig(backend=backend, stop=P.StoppingCriteria(1e-10, 200))
+    x, rep = P.solve_with_fallback(cfg, a, rhs)
+    xo, ro, groups, fb = O.solve(a.pattern.row_pointers, a.pattern.column_indices, a.values3d,
+                                 rhs.data, strategy, 1e-10, 200)
+    assert rep.converged and ro.converged and not fb and not rep.fallback_used
+    assert rep.iterations == ro.iterations
+    assert np.linalg.norm(x.data - xo) <= 1e-9 * np.linalg.norm(xo)
