@@ -136,20 +136,32 @@ class _Stager:
 
 def staged_copy(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
     """dst (contiguous device tensor) <- src (contiguous pageable host tensor of
-    the same byte size), DMAs enqueued on ``stream``; returns once every
-    chunk is in flight (the ring's buffers are reused only after their DMA)."""
-    nbytes = src.numel() * src.element_size()
+    the same byte size; or int64 -> int32, narrowed while staging -- the
+    caller guarantees the values fit), DMAs enqueued on ``stream``; returns
+    once every chunk is in flight (the ring's buffers are reused only after
+    their DMA)."""
+    narrow = src.dtype == torch.int64 and dst.dtype == torch.int32
+    if narrow:
+        nbytes = src.numel()            # (counted in destination elements)
+        esz = 4
+    else:
+        nbytes = src.numel() * src.element_size()
+        esz = 1
     if nbytes == 0:
         return
     dev = dst.device
     st = _STAGERS.get(dev.index)
     if st is None:
         st = _STAGERS[dev.index] = _Stager(dev)
-    s8 = src.reshape(-1).view(torch.uint8).numpy()
-    d8 = dst.reshape(-1).view(torch.uint8)
+    if narrow:
+        s8 = src.reshape(-1).numpy()
+        d8 = dst.reshape(-1)
+    else:
+        s8 = src.reshape(-1).view(torch.uint8).numpy()
+        d8 = dst.reshape(-1).view(torch.uint8)
     # arrays of a few chunks are cut finer so every copy thread gets a share
     # (an 8 MB array would otherwise be one thread's memcpy)
-    chunk = min(STAGE_CHUNK, max(1 << 20, -(-nbytes // st.workers)))
+    chunk = min(STAGE_CHUNK // esz, max((1 << 20) // esz, -(-nbytes // st.workers)))
     chunk = -(-chunk // 4096) * 4096
     nch = (nbytes + chunk - 1) // chunk
     with st.lock:
@@ -160,7 +172,10 @@ def staged_copy(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
                 ev.synchronize()
             lo = i * chunk
             hi = min(nbytes, lo + chunk)
-            np.copyto(st.views[b][: hi - lo], s8[lo:hi])
+            if narrow:
+                np.copyto(st.views[b].view(np.int32)[: hi - lo], s8[lo:hi], casting="unsafe")
+            else:
+                np.copyto(st.views[b][: hi - lo], s8[lo:hi])
         futs = {}
         for i in range(min(STAGE_BUFS - 1, nch)):
             futs[i] = st.pool.submit(fill, i)
@@ -170,7 +185,8 @@ def staged_copy(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
             lo = i * chunk
             hi = min(nbytes, lo + chunk)
             with torch.cuda.stream(stream):
-                d8[lo:hi].copy_(st.bufs[b][: hi - lo], non_blocking=True)
+                buf = st.bufs[b].view(torch.int32) if narrow else st.bufs[b]
+                d8[lo:hi].copy_(buf[: hi - lo], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(stream)
             st.events[b] = ev
@@ -333,11 +349,15 @@ class DevBSR:
         cur = torch.cuda.current_stream(dev)
         side = upload_stream(dev)
         side.wait_stream(cur)
-        rp_raw = torch.empty(n + 1, dtype=torch.int64, device=dev)
-        ci_raw = torch.empty(max(nnz, 1), dtype=torch.int64, device=dev)
+        rp_t, ci_t = torch.from_numpy(rp_h), torch.from_numpy(ci_h)
+        # page-locked indices travel as they are and are narrowed on the
+        # device; pageable ones are narrowed while staging (half the bytes)
+        direct = is_pinned(rp_t) and (nnz == 0 or is_pinned(ci_t))
+        it = torch.int64 if direct else torch.int32
+        rp_raw = torch.empty(n + 1, dtype=it, device=dev)
+        ci_raw = torch.empty(max(nnz, 1), dtype=it, device=dev)
         vals = torch.empty(m.values.size, dtype=torch.float64, device=dev)
-        srcs = [(rp_raw, torch.from_numpy(rp_h)), (ci_raw[:nnz], torch.from_numpy(ci_h)),
-                (vals, torch.from_numpy(m.values))]
+        srcs = [(rp_raw, rp_t), (ci_raw[:nnz], ci_t), (vals, torch.from_numpy(m.values))]
         ev_pat, done = torch.cuda.Event(), torch.cuda.Event()
         import threading
         queued = threading.Event()
@@ -349,7 +369,8 @@ class DevBSR:
                 for i, (dst, src) in enumerate(srcs):
                     if src.numel() == 0:
                         pass
-                    elif is_pinned(src) or src.numel() * src.element_size() < STAGE_MIN_BYTES:
+                    elif dst.dtype == src.dtype and (
+                            is_pinned(src) or src.numel() * src.element_size() < STAGE_MIN_BYTES):
                         with torch.cuda.stream(side):
                             dst.copy_(src, non_blocking=is_pinned(src))
                     else:
@@ -374,10 +395,15 @@ class DevBSR:
                 th.join()
             raise errors[0]
         cur.wait_event(ev_pat)
-        rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
-        ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
-        check(lib().b2s_narrow_index(n + 1, ptr(rp_raw), ptr(rp), None, stream()), "narrow_index")
-        check(lib().b2s_narrow_index(nnz, ptr(ci_raw), ptr(ci), None, stream()), "narrow_index")
+        if direct:
+            rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+            ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+            check(lib().b2s_narrow_index(n + 1, ptr(rp_raw), ptr(rp), None, stream()),
+                  "narrow_index")
+            check(lib().b2s_narrow_index(nnz, ptr(ci_raw), ptr(ci), None, stream()),
+                  "narrow_index")
+        else:
+            rp, ci = rp_raw, ci_raw
         pat = DevPattern(n, nnz, rp, ci, grid_hint(n, rp_h, ci_h))
         out = cls(pat, int(m.block_size), vals)
         out._pending = (th, done)

@@ -101,6 +101,13 @@ def test_staged_pageable_upload_is_exact():
         d = D.to_device(torch.from_numpy(a), torch.device("cuda"))
         torch.cuda.synchronize()
         assert_array_equal(d.cpu().numpy(), a)
+    # int64 indices narrowed to int32 while staging
+    for n in (1, 5000, (C * 2) + 7, 3 * C + 1):
+        a = rng.integers(0, 2**31 - 1, size=n, dtype=np.int64)
+        d = torch.empty(n, dtype=torch.int32, device="cuda")
+        D.staged_copy(d, torch.from_numpy(a), torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        assert_array_equal(d.cpu().numpy(), a.astype(np.int32))
     g = P.generate(P.GeneratorSpec(60, 50, 40, seed=2))
     cfg = P.SolverConfig(backend=P.Backend.GRAPH_COLORED, stop=P.StoppingCriteria(1e-8, 200))
     x1, r1 = P.solve_with_fallback(cfg, g.a, g.rhs)
