@@ -89,6 +89,7 @@ class Clocks:
 
     def __init__(self, index=0):
         self.index, self.proc, self.out = index, None, None
+        self.period = float(os.environ.get("B2S_CLOCK_MS", "10")) / 1e3
         self.nvml = self.handle = None
         try:
             import pynvml as N
@@ -113,7 +114,7 @@ class Clocks:
                                      N.nvmlDeviceGetCurrentClocksEventReasons(self.handle)))
             except Exception:
                 pass
-            if self.done.wait(0.01):
+            if self.done.wait(self.period):
                 break
 
     def start(self):

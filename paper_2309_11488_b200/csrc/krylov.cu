@@ -530,6 +530,30 @@ void done_release(int* w) {
   std::lock_guard<std::mutex> lk(g_done_mu);
   g_done_free.push_back(w);
 }
+
+// A finished solve's graph, streams and events are destroyed at the start of
+// the thread's next solve instead of at its end: the ~0.2 ms of host
+// teardown then overlaps the caller's next device work instead of leaving
+// the device idle between the loop and the caller's follow-up kernels.
+struct Leftovers {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaStream_t streams[2] = {nullptr, nullptr};
+  cudaEvent_t events[10] = {};
+  int nev = 0;
+  void destroy() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (cudaStream_t& s : streams)
+      if (s) { cudaStreamDestroy(s); s = nullptr; }
+    for (int i = 0; i < nev; ++i)
+      if (events[i]) cudaEventDestroy(events[i]);
+    exec = nullptr;
+    graph = nullptr;
+    nev = 0;
+  }
+};
+thread_local Leftovers t_left;
 }  // namespace
 
 extern "C" {
@@ -560,6 +584,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if ((reinterpret_cast<uintptr_t>(a->x) | reinterpret_cast<uintptr_t>(a->rhs) |
        reinterpret_cast<uintptr_t>(a->work)) & 15)
     return B2S_SHAPE;
+  t_left.destroy();   // the previous solve's graph and streams (this thread)
   // B2S_SOLVE_TIMING=1: host-side phase times of each solve on stderr
   static const bool tmg = getenv("B2S_SOLVE_TIMING") && getenv("B2S_SOLVE_TIMING")[0] == '1';
   using clk = std::chrono::steady_clock;
@@ -723,6 +748,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     return !barrier_failed;
   };
   State hs;
+  bool tail_queued = false;
 
   // ---- capture one iteration
   cudaStream_t cs;
@@ -981,16 +1007,27 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     cudaEventRecord(fin, rs);
     cudaStreamWaitEvent(user, fin, 0);
     cudaEventDestroy(fin);
+    if (status == B2S_OK) {
+      // the solve's tail goes on the device before the host tears the graph
+      // down (that host work overlapped nothing before: ~0.3 ms idle at C4)
+      if (vecf || xdefer)   // an exit between the s half-step and the r-update: x += alpha p^
+        k_x_fixup<<<grid_v, 256, 0, user>>>(m, state, phat, a->x);
+      tail_queued = cudaMemcpyAsync(&hs, state, sizeof(State), cudaMemcpyDeviceToHost, user) ==
+                    cudaSuccess;
+    }
     if (cudaStreamSynchronize(rs) != cudaSuccess) status = B2S_CUDA_ERROR;
-    for (int q = 0; q < 8; ++q) cudaEventDestroy(ring[q]);
+    for (int q = 0; q < 8; ++q) t_left.events[t_left.nev++] = ring[q];
     peer_barrier();   // no shard tears down while another still runs
   } while (0);
-  if (exec) cudaGraphExecDestroy(exec);
-  if (graph) cudaGraphDestroy(graph);
-  cudaStreamDestroy(cs);
-  if (side) cudaStreamDestroy(side);
-  if (ev_fork) cudaEventDestroy(ev_fork);
-  if (ev_join) cudaEventDestroy(ev_join);
+  t_left.exec = exec;
+  t_left.graph = graph;
+  t_left.streams[0] = cs;
+  t_left.streams[1] = side;
+  if (ev_fork) t_left.events[t_left.nev++] = ev_fork;
+  if (ev_join) t_left.events[t_left.nev++] = ev_join;
+  // (sharded solves tear down at once: their peers' kernels may be spinning
+  // on this device, and nothing of theirs should wait behind our teardown)
+  if (mesh) t_left.destroy();
   mark();
   done_release(host_done);
   host_done = nullptr;
@@ -1005,9 +1042,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if (status != B2S_OK) return status;
   res->kernels_per_iteration = kernels;
 
-  if (vecf || xdefer)   // an exit between the s half-step and the r-update: x += alpha p^
-    k_x_fixup<<<grid_v, 256, 0, user>>>(m, state, phat, a->x);
-  B2S_CHECK(cudaMemcpyAsync(&hs, state, sizeof(State), cudaMemcpyDeviceToHost, user));
+  if (!tail_queued) return B2S_CUDA_ERROR;
   B2S_CHECK(cudaStreamSynchronize(user));
   if (hs.reason == kAborted || barrier_failed) return B2S_PEER_TIMEOUT;
   res->initial_norm = hs.norm0;
