@@ -241,6 +241,45 @@ def to_host_vector(v: torch.Tensor, count: int, block_size: int):
     return BlockVector._checked_on_device(to_host(v, count), block_size)
 
 
+class HostResult:
+    """A solve's result on its way to the host: the finiteness check, the
+    D2H of x into page-locked memory and any further device scalars are all
+    queued first, then one synchronisation (no device idle between small
+    reads)."""
+
+    def __init__(self, v: torch.Tensor, count: int, block_size: int):
+        count = int(count)
+        self.count, self.block_size = count, block_size
+        self._bad = torch.zeros(1, dtype=torch.int32, device=v.device)
+        check(lib().b2s_all_finite(count, ptr(v), ptr(self._bad), stream()), "all_finite")
+        self._bad_h = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        self._bad_h.copy_(self._bad, non_blocking=True)
+        self._x = torch.empty(count, dtype=v.dtype, pin_memory=True)
+        if count:
+            self._x.copy_(v[:count], non_blocking=True)
+        self._extra = []
+
+    def fetch(self, t: torch.Tensor) -> int:
+        """Queue a small device tensor's D2H; its value is ``value(k)`` after wait()."""
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        self._extra.append(h)
+        return len(self._extra) - 1
+
+    def wait(self):
+        torch.cuda.current_stream().synchronize()
+        return self
+
+    def value(self, k: int) -> torch.Tensor:
+        return self._extra[k]
+
+    def vector(self):
+        from .blockcore import BlockVector
+        if int(self._bad_h.item()):
+            raise ValueError("block vector entries must be finite")
+        return BlockVector._checked_on_device(self._x.numpy(), self.block_size)
+
+
 def to_host(v: torch.Tensor, count: int) -> np.ndarray:
     """D2H of the first ``count`` elements into page-locked memory (fast DMA;
     the returned array owns a pinned block of the caching host allocator)."""
@@ -521,8 +560,10 @@ def permute_pattern(p: DevPattern, cmap: torch.Tensor, take: torch.Tensor):
     return DevPattern(p.n, p.nnz, rp, ci), src
 
 
-def gather_rows(v: torch.Tensor, src: torch.Tensor, n: int, b: int) -> torch.Tensor:
-    out = torch.empty(n * b, dtype=torch.float64, device=v.device)
+def gather_rows(v: torch.Tensor, src: torch.Tensor, n: int, b: int,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(n * b, dtype=torch.float64, device=v.device)
     check(lib().b2s_gather_rows(n, b, ptr(src), ptr(v), ptr(out), stream()), "gather_rows")
     return out
 

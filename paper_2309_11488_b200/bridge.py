@@ -173,7 +173,7 @@ class DeviceSolver:
         bp = D.gather_rows(rhs, iperm, n, b)
         xp = D.gather_rows(x, iperm, n, b)
         res = self.krylov.solve(bp, xp, stop, x0_zero=x0_zero)
-        x.copy_(D.gather_rows(xp, f.plan.device("permutation"), n, b)[: n * b])
+        D.gather_rows(xp, f.plan.device("permutation"), n, b, out=x)
         return res
 
 
@@ -266,10 +266,13 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
             res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None)
         e_end = torch.cuda.Event(enable_timing=True)
         e_end.record()
-        _sync()
+        # everything the host reads next, queued, then one synchronisation
+        tail = D.HostResult(xd, n * bs, bs)
+        norm0.fetch_into(tail)
+        tail.wait()
         setup = (time.perf_counter() - t0) - e_setup.elapsed_time(e_end) / 1e3
         primary = _report(res, e_setup.elapsed_time(e_end) / 1e3, solver.plan.group_count,
-                          norm0.value())
+                          norm0.from_tail(tail))
         primary.setup_elapsed = max(setup, 0.0)
         x = xd
     except SingularPivot as exc:
@@ -278,7 +281,7 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
 
     if primary.converged:
         with trace.phase("download"):
-            out = D.to_host_vector(x, n * bs, bs)
+            out = tail.vector()
         primary.phases = trace.finish()
         return out, primary
 
@@ -430,12 +433,14 @@ class SolveSession:
             res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None)
             e_end = torch.cuda.Event(enable_timing=True)
             e_end.record()
-            _sync()
+            tail = D.HostResult(xd, n * bs, bs)
+            norm0.fetch_into(tail)
+            tail.wait()
             rep = _report(res, e_setup.elapsed_time(e_end) / 1e3, solver.plan.group_count,
-                          norm0.value())
+                          norm0.from_tail(tail))
             rep.setup_elapsed = max((time.perf_counter() - t0) - rep.elapsed, 0.0)
         except SingularPivot:
             return solve_with_fallback(cfg, a, b, wells, x0)
         if not rep.converged:
             return solve_with_fallback(cfg, a, b, wells, x0)
-        return D.to_host_vector(xd, n * bs, bs), rep
+        return tail.vector(), rep

@@ -96,6 +96,20 @@ class RefNorm:
         self._ev.synchronize()
         return 0.0 if self._sq is None else float(np.sqrt(float(self._sq.item())))
 
+    def fetch_into(self, tail: "D.HostResult"):
+        """Queue the squared norm's D2H on the current stream (after the side
+        stream's event) into ``tail``; ``from_tail`` reads it after wait()."""
+        if self._sq is None:
+            self._k = None
+            return
+        torch.cuda.current_stream().wait_event(self._ev)
+        self._k = tail.fetch(self._sq.reshape(1))
+
+    def from_tail(self, tail: "D.HostResult") -> float:
+        if self._k is None:
+            return 0.0
+        return float(np.sqrt(float(tail.value(self._k)[0])))
+
 
 def dot(a: BlockVector, b: BlockVector) -> float:
     """Deterministic chunked inner product of two block vectors (the
