@@ -144,16 +144,20 @@ class DeviceSolver:
         return self
 
     def solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
-              x0_zero: bool = False):
+              x0_zero: bool = False, on_done=None):
         """x (input order) holds x0 on entry and the solution on exit;
         ``x0_zero``: the caller guarantees x == 0 (no initial guess).
         A deferred factorisation check runs after the loop: SingularPivot is
         raised as decompose would have; a pattern that was not a 2-colour
         structure after all is refactorised on the general path and solved
-        again from the same x0."""
+        again from the same x0.  ``on_done()`` runs after each solve is
+        queued and before the check reads the flags, so the caller's result
+        reads join that one synchronisation."""
         pending = self.fact._deferred is not None
         x_in = x.clone() if pending and not x0_zero else None
         res = self._solve(rhs, x, stop, x0_zero)
+        if on_done is not None:
+            on_done()
         if pending and self.fact.check_deferred():
             self.setup(self._backend, two_colour=False, defer=False)
             if x_in is None:
@@ -161,6 +165,8 @@ class DeviceSolver:
             else:
                 x.copy_(x_in)
             res = self._solve(rhs, x, stop, x0_zero)
+            if on_done is not None:
+                on_done()
         return res
 
     def _solve(self, rhs: torch.Tensor, x: torch.Tensor, stop: StoppingCriteria,
@@ -183,6 +189,25 @@ def _report(res, elapsed, groups, norm0: float | None = None) -> SolveReport:
                        float(res.final_norm), elapsed, groups,
                        failure_reason=None if res.converged else _REASONS.get(res.reason, "budget"),
                        gpu_launches=int(res.graph_launches) * int(res.kernels_per_iteration))
+
+
+class _Tail:
+    """The end-of-solve event and the queued host reads (D.HostResult) of
+    x and the reported initial norm."""
+
+    def __init__(self, x: torch.Tensor, count: int, block_size: int, norm0: "RefNorm"):
+        self.x, self.count, self.block_size, self.norm0 = x, count, block_size, norm0
+        self.end = self.host = None
+
+    def __call__(self):
+        self.end = torch.cuda.Event(enable_timing=True)
+        self.end.record()
+        self.host = D.HostResult(self.x, self.count, self.block_size)
+        self.norm0.fetch_into(self.host)
+
+    def wait(self):
+        self.host.wait()
+        return self.end, self.host
 
 
 def _sync():
@@ -263,13 +288,11 @@ def solve_with_fallback(cfg: SolverConfig, a: BlockMatrix, b: BlockVector, wells
         e_setup.record()
         xd = x0d.clone()
         with trace.phase("krylov"):
-            res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None)
-        e_end = torch.cuda.Event(enable_timing=True)
-        e_end.record()
-        # everything the host reads next, queued, then one synchronisation
-        tail = D.HostResult(xd, n * bs, bs)
-        norm0.fetch_into(tail)
-        tail.wait()
+            # everything the host reads next (deferred factor flags, x, the
+            # initial norm) queued, then one synchronisation
+            queue = _Tail(xd, n * bs, bs, norm0)
+            res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None, on_done=queue)
+        e_end, tail = queue.wait()
         setup = (time.perf_counter() - t0) - e_setup.elapsed_time(e_end) / 1e3
         primary = _report(res, e_setup.elapsed_time(e_end) / 1e3, solver.plan.group_count,
                           norm0.from_tail(tail))
@@ -430,12 +453,9 @@ class SolveSession:
             e_setup = torch.cuda.Event(enable_timing=True)
             e_setup.record()
             xd = x0d.clone()
-            res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None)
-            e_end = torch.cuda.Event(enable_timing=True)
-            e_end.record()
-            tail = D.HostResult(xd, n * bs, bs)
-            norm0.fetch_into(tail)
-            tail.wait()
+            queue = _Tail(xd, n * bs, bs, norm0)
+            res = solver.solve(rhs, xd, cfg.stop, x0_zero=x0 is None, on_done=queue)
+            e_end, tail = queue.wait()
             rep = _report(res, e_setup.elapsed_time(e_end) / 1e3, solver.plan.group_count,
                           norm0.from_tail(tail))
             rep.setup_elapsed = max((time.perf_counter() - t0) - rep.elapsed, 0.0)
