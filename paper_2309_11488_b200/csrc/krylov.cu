@@ -59,7 +59,13 @@ int launch_wells_patch(const b2s_wells* w, int goff1, const double* corr, double
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
                     double* p1, const int* done, int* grid_out, cudaStream_t st,
-                    bool pdl = false, int pre = kPreNone, const PreIn* pre_in = nullptr);
+                    bool pdl = false, int pre = kPreNone, const PreIn* pre_in = nullptr,
+                    double* uimg = nullptr);
+int launch_simg(int b, int stage, int nparts, SliceMap map, int s0, int s1, int poff, Sell m_,
+                const double* dt, const double* in0, const double* in1, double* out0,
+                double* out1, double* parts, const int* done, Ctl ctl, int goff1,
+                const double* u, double* fv, long long mlen, const State* st, cudaStream_t q,
+                bool pdl);
 int launch_fwd_pre(int b, int nparts, SliceMap map, int s0, int s1, Sell lo, const double* dt,
                    double* z, const int* done, int* grid_out, cudaStream_t st, bool pdl, int pre,
                    const PreIn* pre_in);
@@ -643,6 +649,12 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // half-step exit) -- not with sync-free sweeps (their s-update refills p^)
   const char* xd_env = getenv("B2S_XDEFER");
   const bool xdefer = ilu && !vecf && !reset && !(xd_env && xd_env[0] == '0');
+  // s-image (fused.cu): the s^ forward sweep of a 2-colour plan replaced by
+  // F(s) = F(r) - alpha F(v), both images computed in passes that stream the
+  // same blocks anyway (F(r) in y's colour-1 rows, u = inv(A_kk) v and F(v)
+  // in t, which is dead until the s-phase); B2S_SIMG=0 turns it off
+  const char* si_env = getenv("B2S_SIMG");
+  const bool simg = fused && !vecf && xdefer && !mesh && !wells && !(si_env && si_env[0] == '0');
   MeshDev md{};
   MeshHalo mh{};
   if (mesh && !ilu) return B2S_UNSUPPORTED;   // sharded solves are block-Jacobi ILU0
@@ -863,7 +875,18 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       launch_k(k_p_update, dim3(grid_v), dim3(256), 0, cs, pdl, m, (const State*)state,
                (const double*)r, (const double*)v, p);
       ++kernels;
-      if (fused) {
+      if (simg) {
+        // p^ colour 1 + F(r); colour 0 + v + u; colour-1 SpMV + F(v) + alpha
+        launch_simg(a->b, 0, np, map, s1c, map.nslices, 0, L, a->dinv_tiles, p, r, phat, y,
+                    nullptr, done, Ctl{}, a->goff1, nullptr, nullptr, m, state, cs, pdl);
+        int g0 = np;
+        launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
+                        done, &g0, cs, pdl, kPreNone, nullptr, t);
+        launch_simg(a->b, 1, np, map, s1c, map.nslices, g0, A, nullptr, phat, rhat, v, nullptr, pg,
+                    done, Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, a->goff1, t, t, m,
+                    state, cs, pdl);
+        kernels += 3;
+      } else if (fused) {
         launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, p, y,
                       phat, done, cs, true, pdl);
         int g0 = np;
@@ -909,13 +932,21 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
                     Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl && !wells, wf);
         ++kernels;
       }
-      launch_k(xdefer ? k_s_update<false> : k_s_update<true>, dim3(grid_v), dim3(256), 0, cs, pdl,
-               m, (const State*)state, (const double*)r, (const double*)v, ph, a->x, s, pss, reset,
-               Ctl{state, counters + 1, dev_done, kCtlS, md});
+      if (simg)   // s, |s|^2, the half-step test, and colour 1's s^ from the images
+        launch_simg(a->b, 2, grid_v, map, s1c, map.nslices, 0, Sell{}, a->dinv_tiles, r, v, s,
+                    shat, pss, done, Ctl{state, counters + 1, dev_done, kCtlS, md}, a->goff1, y, t,
+                    m, state, cs, pdl);
+      else
+        launch_k(xdefer ? k_s_update<false> : k_s_update<true>, dim3(grid_v), dim3(256), 0, cs,
+                 pdl, m, (const State*)state, (const double*)r, (const double*)v, ph, a->x, s, pss,
+                 reset, Ctl{state, counters + 1, dev_done, kCtlS, md});
       ++kernels;
       if (fused) {
-        launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, s, y,
-                      shat, done, cs, true, pdl);
+        if (simg)
+          --kernels;   // no forward pass: the pair below counts as three
+        else
+          launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, s, y,
+                        shat, done, cs, true, pdl);
         int g0 = np;
         launch_bwd_spmv(a->b, 2, np, map, s1c, A, a->dinv_tiles, s, shat, t, s, ptt, pts, done,
                         &g0, cs, pdl);

@@ -180,14 +180,17 @@ __global__ void k_diag_tiles(int nslices, int bb, const int32_t* __restrict__ ro
 }
 
 
+#ifndef B2S_SPMV_CTAS
+#define B2S_SPMV_CTAS 2
+#endif
 template <int B, int MODE, bool WELLS>
-__global__ void __launch_bounds__(256, B <= 3 ? 4 : 1) k_spmv(SliceMap map, int s0, int s1, int poff, Sell a,
+__global__ void __launch_bounds__(256, B <= 3 ? B2S_SPMV_CTAS : 1) k_spmv(SliceMap map, int s0, int s1, int poff, Sell a,
                                               const double* __restrict__ x,
                                               double* __restrict__ y,
                                               const double* __restrict__ w,
                                               double* __restrict__ part0,
                                               double* __restrict__ part1, const int* done,
-                                              Ctl ctl, WellFix wf) {
+                                              Ctl ctl, WellFix wf, int ptotal) {
   constexpr int BB = B * B;
   __shared__ double red[8];
   griddep_wait();
@@ -280,6 +283,14 @@ __global__ void __launch_bounds__(256, B <= 3 ? 4 : 1) k_spmv(SliceMap map, int 
     }
   }
   if (MODE != kPlain) {
+    // a grid capped at one resident wave leaves the caller's slots
+    // [gridDim.x, ptotal) unwritten: zeros, so every consumer's fixed-order
+    // reduction over ptotal slots stays valid
+    if (blockIdx.x == 0)
+      for (int q = gridDim.x + threadIdx.x; q < ptotal; q += blockDim.x) {
+        part0[poff + q] = 0.0;
+        if (MODE == kSelfAndW) part1[poff + q] = 0.0;
+      }
     double t0 = block_sum(p0, red);
     if (threadIdx.x == 0) part0[poff + blockIdx.x] = t0;
     if (MODE == kSelfAndW) {
@@ -305,11 +316,27 @@ int launch_spmv_bw(int mode, int nparts, SliceMap map, int s0, int s1, int poff,
                    const double* x, double* y, const double* w, double* p0, double* p1,
                    const int* done, Ctl ctl, cudaStream_t st, bool pdl, WellFix wf) {
   dim3 g(nparts), t(256);
+#if B2S_SPMV_CTAS < 4
+  // one resident wave: 2 CTAs per SM without the 64-register cap measured
+  // faster than 4 capped ones (C4 SpMV 90.4 -> 87.7 us, colour-1 SpMV in the
+  // loop 60.3 -> 57.3 us; profiles/r02/simg.txt)
+  {
+    static int cap = 0;
+    if (!cap) {
+      int per_sm = 1, dev = 0, sms = kSms;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv<B, kDotW, WELLS>, 256, 0);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cap = (per_sm < 1 ? 1 : per_sm) * sms;
+    }
+    if ((int)g.x > cap) g.x = cap;
+  }
+#endif
   switch (mode) {
-    case kPlain: launch_k(k_spmv<B, kPlain, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf); break;
-    case kDotW: launch_k(k_spmv<B, kDotW, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf); break;
-    case kSelfAndW: launch_k(k_spmv<B, kSelfAndW, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf); break;
-    case kResidual: launch_k(k_spmv<B, kResidual, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf); break;
+    case kPlain: launch_k(k_spmv<B, kPlain, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf, nparts); break;
+    case kDotW: launch_k(k_spmv<B, kDotW, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf, nparts); break;
+    case kSelfAndW: launch_k(k_spmv<B, kSelfAndW, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf, nparts); break;
+    case kResidual: launch_k(k_spmv<B, kResidual, WELLS>, g, t, 0, st, pdl, map, s0, s1, poff, a, x, y, w, p0, p1, done, ctl, wf, nparts); break;
     default: return B2S_SHAPE;
   }
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
