@@ -138,6 +138,10 @@ __global__ void __launch_bounds__(256) k_bwd_spmv(SliceMap map, int s0, int s1, 
                                                   PreIn in, double* __restrict__ uimg) {
   constexpr int BB = B * B;
   __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) {
+    const int s = s0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (s < s1) prefetch_slice<BB>(a, s, dtiles);
+  }
   griddep_wait();
   griddep_launch();
   if (done && *done) return;
@@ -415,6 +419,10 @@ __global__ void __launch_bounds__(256) k_fwd_rimg(int s0, int s1, SliceMap map, 
                                                   double* __restrict__ z,
                                                   double* __restrict__ fr, const int* done) {
   constexpr int BB = B * B;
+  if ((threadIdx.x & 31) == 0) {
+    const long long s = s0 + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s < s1) prefetch_slice<BB>(lo, (int)s, dtiles);
+  }
   griddep_wait();
   griddep_launch();
   if (done && *done) return;
@@ -499,12 +507,13 @@ __global__ void __launch_bounds__(256, B <= 3 ? B2S_IMG_CTAS : 1) k_spmv1_img(Sl
                                                    double* fv) {
   constexpr int BB = B * B;
   __shared__ double red[8];
-  griddep_wait();
-  griddep_launch();
-  if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
+  if (lane == 0 && s0 + gw < s1) prefetch_slice<BB>(a, s0 + gw);
+  griddep_wait();
+  griddep_launch();
+  if (done && *done) return;
   double p0 = 0.0;
   for (int s = s0 + gw; s < s1; s += nw) {
     const int slot0 = a.sp[s];

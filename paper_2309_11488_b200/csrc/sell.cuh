@@ -43,4 +43,26 @@ __device__ __forceinline__ long long vidx(long long slot0, int k, int e, int lan
   return (slot0 + 32ll * k) * bb + 32ll * e + lane;
 }
 
+// L2 prefetch of one slice's SELL entries (column indices + block values).
+// They are setup data, so a kernel may issue it BEFORE griddep_wait(): its
+// first slice then streams in while the predecessor's last CTAs drain (one
+// bulk prefetch per array, issued by one lane).  B2S_PREWAIT=0 at compile
+// time leaves it out (A/B builds).
+#ifndef B2S_PREWAIT
+#define B2S_PREWAIT 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+template <int BB>
+__device__ __forceinline__ void prefetch_slice(const Sell& a, int s, const double* tiles = nullptr) {
+  if (!B2S_PREWAIT) return;
+  const int slot0 = a.sp[s], n = a.sp[s + 1] - slot0;
+  if (n > 0) {
+    prefetch_l2(a.vals + (long long)slot0 * BB, (unsigned)n * BB * 8u);
+    prefetch_l2(a.cols + slot0, (unsigned)n * 4u);
+  }
+  if (tiles) prefetch_l2(tiles + (long long)s * BB * 32, BB * 32 * 8u);
+}
+
 }  // namespace b2s

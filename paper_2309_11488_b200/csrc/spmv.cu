@@ -193,12 +193,13 @@ __global__ void __launch_bounds__(256, B <= 3 ? B2S_SPMV_CTAS : 1) k_spmv(SliceM
                                               Ctl ctl, WellFix wf, int ptotal) {
   constexpr int BB = B * B;
   __shared__ double red[8];
-  griddep_wait();
-  griddep_launch();
-  if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
+  if (lane == 0 && s0 + gw < s1) prefetch_slice<BB>(a, s0 + gw);
+  griddep_wait();
+  griddep_launch();
+  if (done && *done) return;
   double p0 = 0.0, p1 = 0.0;
   // the column indices of the next entry pair load one step ahead -- across
   // slice boundaries too: a slice's last step fetches the next slice's first
