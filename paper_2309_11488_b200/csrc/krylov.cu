@@ -638,10 +638,12 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // iteration instead of 9.  They move the same bytes (the separate p-update
   // largely hits L2), so they pay where the iteration is launch-bound --
   // measured 65.9 vs 71.0 us per iteration at 48k cells, 388.8 vs 384.7 us at
-  // 1M (profiles/r02/vec_fusion.txt): on up to 400k cells by default;
-  // B2S_FUSE_VEC=1/0 forces it
+  // 1M (profiles/r02/vec_fusion.txt).  The unfused passes take the s-image
+  // below, which wins from ~100k cells on (350k: 152.8 vs 165.4 us, 113k
+  // even, 48k: 57.1 vs 56.4; profiles/r02/simg.txt): on up to 100k cells by
+  // default; B2S_FUSE_VEC=1/0 forces it
   const char* fv_env = getenv("B2S_FUSE_VEC");
-  const bool vecf = fused && (fv_env ? fv_env[0] == '1' : a->n <= 400000);
+  const bool vecf = fused && (fv_env ? fv_env[0] == '1' : a->n <= 100000);
   // sync-free sweeps need sentinel-filled outputs (not the wavefront sweeps)
   const int reset = (ilu && !phased && !a->gw) ? 1 : 0;
   // x += alpha p^ deferred from the s-update to the r-update (one x pass per
