@@ -201,16 +201,40 @@ __device__ __forceinline__ void ctl_finish(State* st, int* host_done, int reason
 }
 
 // The scalar logic after each reduction point; whole CTA calls, thread 0 writes.
+// The state fields a step reads are loaded before the reductions, and the
+// two or three partial arrays are summed in one pass with one shared-memory
+// round (per-thread order and tree exactly reduce_parts_cg's): the control
+// step is the serial tail of its kernel.
 __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const double* p1, int np,
                                         double* red) {
+  (void)red;
   State* st = c.st;
-  const double a0 = reduce_parts_cg(p0, np, red);
-  double b = 0.0, c2 = 0.0;
-  if (c.step == kCtlOmega || c.step == kCtlEndBegin || c.step == kCtlOmegaS)
-    b = reduce_parts_cg(p1, np, red);
-  if (c.step == kCtlOmegaS) c2 = reduce_parts_cg(c.p2, c.np2, red);
+  __shared__ double red3[3][32];
+  const bool two = c.step == kCtlOmega || c.step == kCtlEndBegin || c.step == kCtlOmegaS;
+  const bool three = c.step == kCtlOmegaS;
+  const double rho = st->rho, alpha = st->alpha, omega = st->omega;
+  const double target = st->target, its = st->its;
+  const int k = st->k, maxit = st->maxit;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    v0 += __ldcg(p0 + i);
+    if (two) v1 += __ldcg(p1 + i);
+  }
+  if (three)
+    for (int i = threadIdx.x; i < c.np2; i += blockDim.x) v2 += __ldcg(c.p2 + i);
+  v0 = warp_sum(v0);
+  if (two) v1 = warp_sum(v1);
+  if (three) v2 = warp_sum(v2);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) { red3[0][w] = v0; red3[1][w] = v1; red3[2][w] = v2; }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int nw = blockDim.x >> 5;
+  double a = warp_sum(l < nw ? red3[0][l] : 0.0);
+  double b = two ? warp_sum(l < nw ? red3[1][l] : 0.0) : 0.0;
+  double c2 = three ? warp_sum(l < nw ? red3[2][l] : 0.0) : 0.0;
   if (threadIdx.x != 0) return;
-  double a = a0;
   const int slot = c.step == kCtlOmegaS ? kCtlOmega : c.step;
   if (c.mesh.mbox && !mesh_sum3(c.mesh, c.mesh.seq_base + (++st->cseq), slot, a, b, c2)) {
     ctl_finish(st, c.host_done, kAborted);
@@ -219,16 +243,16 @@ __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const do
   switch (c.step) {
     case kCtlAlpha: {  // gamma = rhat.v  (bs/krylov.py:206-210)
       if (fabs(a) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
-      st->alpha = st->rho / a;
+      st->alpha = rho / a;
       return;
     }
     case kCtlS: {  // test |s|  (bs/krylov.py:211-220); x advanced by alpha p^ here or,
                    // deferred, in the r-update (k_x_fixup after an exit in between)
-      st->its += 0.5;
+      st->its = its + 0.5;
       st->xpend = 1;
       const double ns = sqrt(a);
       if (!isfinite(ns)) { ctl_finish(st, c.host_done, kNumerical); return; }
-      if (ns <= st->target) { st->final_norm = ns; ctl_finish(st, c.host_done, kConverged); }
+      if (ns <= target) { st->final_norm = ns; ctl_finish(st, c.host_done, kConverged); }
       return;
     }
     case kCtlOmega: {  // tt, ts  (bs/krylov.py:223-229)
@@ -239,11 +263,11 @@ __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const do
       return;
     }
     case kCtlOmegaS: {  // |s| (bs/krylov.py:211-220), then tt, ts (:223-229)
-      st->its += 0.5;
+      st->its = its + 0.5;
       st->xpend = 1;   // x += alpha p^ is deferred to the r-update (or k_x_fixup)
       const double ns = sqrt(c2);
       if (!isfinite(ns)) { ctl_finish(st, c.host_done, kNumerical); return; }
-      if (ns <= st->target) { st->final_norm = ns; ctl_finish(st, c.host_done, kConverged); return; }
+      if (ns <= target) { st->final_norm = ns; ctl_finish(st, c.host_done, kConverged); return; }
       if (a < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
       const double om = b / a;
       if (fabs(om) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
@@ -252,16 +276,16 @@ __device__ __forceinline__ void ctl_run(const Ctl& c, const double* p0, const do
     }
     case kCtlEndBegin: {  // end of iteration k, then the top of k+1 (bs/krylov.py:195-200,230-240)
       st->xpend = 0;   // the r-update advanced x by alpha p^ + omega s^
-      st->its += 0.5;
+      st->its = its + 0.5;
       const double nr = sqrt(a);
       if (!isfinite(nr)) { ctl_finish(st, c.host_done, kNumerical); return; }
-      if (nr <= st->target) { st->final_norm = nr; ctl_finish(st, c.host_done, kConverged); return; }
-      st->rho_prev = st->rho;
-      st->k += 1;
-      if (st->k >= st->maxit) { ctl_finish(st, c.host_done, kBudget); return; }
+      if (nr <= target) { st->final_norm = nr; ctl_finish(st, c.host_done, kConverged); return; }
+      st->rho_prev = rho;
+      st->k = k + 1;
+      if (k + 1 >= maxit) { ctl_finish(st, c.host_done, kBudget); return; }
       if (fabs(b) < kBreakdown) { ctl_finish(st, c.host_done, kBreakdownR); return; }
       st->rho = b;
-      st->beta = (b / st->rho_prev) * (st->alpha / st->omega);
+      st->beta = (b / rho) * (alpha / omega);
       return;
     }
     default:
