@@ -22,17 +22,27 @@ def launches(path):
     h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr = rows[h]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    agg = collections.defaultdict(lambda: [0, 0.0])
+    mi = hdr.index("Metric Name")
+    # launches, duration (us), DRAM bytes -- a launch list with several metrics
+    # has one row per (launch, metric): only the duration rows are times
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    bscale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for r in rows[h + 1:]:
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0].replace("void ", "").split("<")[0]
-        agg[name][0] += 1
-        agg[name][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        val = float(r[vi].replace(",", ""))
+        if r[mi] == "gpu__time_duration.sum":
+            agg[name][0] += 1
+            agg[name][1] += val * scale.get(r[ui], 1.0)
+        elif r[mi].startswith("dram__bytes"):
+            agg[name][2] += val * bscale.get(r[ui], 1.0)
     tot = sum(v[1] for v in agg.values())
     return [{"kernel": k, "launches": v[0], "total_us": round(v[1], 1),
-             "share": round(v[1] / tot, 4)} for k, v in sorted(agg.items(), key=lambda x: -x[1][1])]
+             "share": round(v[1] / tot, 4), "dram_mb": round(v[2] / 1e6, 1),
+             "dram_tbs": round(v[2] / (v[1] * 1e6), 2) if v[1] else None}
+            for k, v in sorted(agg.items(), key=lambda x: -x[1][1])]
 
 
 def full(rep):
