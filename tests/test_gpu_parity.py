@@ -739,3 +739,47 @@ def test_solve_other_block_sizes_against_oracle(bs, strategy, backend):
     assert rep.converged and ro.converged and not fb and not rep.fallback_used
     assert rep.iterations == ro.iterations
     assert np.linalg.norm(x.data - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("dims", [(20, 20, 10), (12, 10, 16)])
+def test_s_image_matches_sweep(monkeypatch, dims):
+    """2-colour loop with the s-image (colour 1's forward substitution of s
+    as F(r) - alpha F(v), fused.cu) against the same loop with the s forward
+    sweep: same iteration counts and exits -- a half-step convergence and a
+    budget exit included -- and the same solution to rounding (s^'s colour-1
+    rows are rounded differently, nothing else)."""
+    monkeypatch.setenv("B2S_FUSE_VEC", "0")   # the s-image runs on the unfused passes
+    bundle = P.generate(P.GeneratorSpec(*dims, seed=11))
+    a, rhs = bundle.a, bundle.rhs
+    f = P.decompose(a, P.graph_color(a.pattern))
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("B2S_SIMG", flag)
+        for tol, its in ((1e-8, 200), (1e-10, 3)):
+            x, rep = P.bicgstab(P.MatrixOperator(a), f, rhs, stop=P.StoppingCriteria(tol, its))
+            out[(flag, tol)] = (x.data, rep)
+    for tol in (1e-8, 1e-10):
+        (x1, r1), (x0, r0) = out[("1", tol)], out[("0", tol)]
+        assert r1.iterations == r0.iterations and r1.converged == r0.converged
+        assert r1.failure_reason == r0.failure_reason
+        assert np.linalg.norm(x1 - x0) <= 1e-9 * np.linalg.norm(x0)
+        np.testing.assert_allclose(r1.final_norm, r0.final_norm, rtol=1e-5)
+    assert out[("1", 1e-8)][1].iterations % 1.0 == 0.5   # the half-step exit is exercised
+    assert not np.array_equal(out[("1", 1e-8)][0], out[("0", 1e-8)][0])   # the switch took effect
+
+
+@pytest.mark.parametrize("bs", [1, 2, 3, 4])
+def test_s_image_other_block_sizes_against_oracle(monkeypatch, bs):
+    """The s-image loop (forced on small systems) for b = 1..4 against the
+    oracle port's solve: the same iteration count and the solution to 1e-9."""
+    monkeypatch.setenv("B2S_FUSE_VEC", "0")
+    monkeypatch.setenv("B2S_SIMG", "1")
+    g = P.generate(P.GeneratorSpec(18, 14, 9, block_size=bs, seed=40 + bs, diagonal_boost=0.5))
+    a, rhs = g.a, g.rhs
+    cfg = P.SolverConfig(backend=P.Backend.GRAPH_COLORED, stop=P.StoppingCriteria(1e-10, 200))
+    x, rep = P.solve_with_fallback(cfg, a, rhs)
+    xo, ro, groups, fb = O.solve(a.pattern.row_pointers, a.pattern.column_indices, a.values3d,
+                                 rhs.data, "color", 1e-10, 200)
+    assert rep.converged and ro.converged and not fb and not rep.fallback_used
+    assert rep.iterations == ro.iterations
+    assert np.linalg.norm(x.data - xo) <= 1e-9 * np.linalg.norm(xo)
