@@ -497,14 +497,14 @@ __global__ void __launch_bounds__(256) k_fwd_rimg(int s0, int s1, SliceMap map, 
 #ifndef B2S_IMG_CTAS
 #define B2S_IMG_CTAS 2
 #endif
-template <int B>
+template <int B, bool WELLS>
 __global__ void __launch_bounds__(256, B <= 3 ? B2S_IMG_CTAS : 1) k_spmv1_img(SliceMap map, int s0, int s1, int poff, Sell a,
                                                    const double* __restrict__ x,
                                                    double* __restrict__ y,
                                                    const double* __restrict__ w,
                                                    double* __restrict__ part0, const int* done,
                                                    Ctl ctl, int goff1, const double* u,
-                                                   double* fv) {
+                                                   double* fv, WellFix wf) {
   constexpr int BB = B * B;
   __shared__ double red[8];
   const int lane = threadIdx.x & 31;
@@ -559,6 +559,16 @@ __global__ void __launch_bounds__(256, B <= 3 ? B2S_IMG_CTAS : 1) k_spmv1_img(Sl
 #pragma unroll
             for (int c = 0; c < B; ++c) acu[c] += pu[c];
           }
+        }
+      }
+    }
+    if (WELLS) {   // the operator's well terms, as k_spmv's epilogue
+      const int wb = wf.slice[s];
+      if (wb >= 0) {
+        const int q = wf.lane[wb + lane];
+        if (ok && q >= 0) {
+#pragma unroll
+          for (int c = 0; c < B; ++c) acc[c] -= wf.corr[(long long)q * B + c];
         }
       }
     }
@@ -657,7 +667,7 @@ int launch_simg_b(int stage, int nparts, SliceMap map, int s0, int s1, int poff,
                   const double* dt, const double* in0, const double* in1, double* out0,
                   double* out1, double* parts, const int* done, Ctl ctl, int goff1,
                   const double* u, double* fv, long long mlen, const State* st, cudaStream_t q,
-                  bool pdl) {
+                  bool pdl, WellFix wf) {
   if (stage == 0) {   // colour-1 forward on p + F(r): in0 = p, in1 = r, out0 = p^, out1 = F(r)
     static int cap = 0;
     if (!cap) cap = one_wave((const void*)k_fwd_rimg<B>, 1 << 30);
@@ -670,9 +680,15 @@ int launch_simg_b(int stage, int nparts, SliceMap map, int s0, int s1, int poff,
     // one resident wave of 2 CTAs per SM (b <= 3): the second image needs
     // ~96 registers; capped at 80 (3 per SM) it spilled and measured 66.4 us
     // against 58.7 at C4 (profiles/r02/simg.txt)
-    const int g = one_wave((const void*)k_spmv1_img<B>, nparts);
-    launch_k(k_spmv1_img<B>, dim3(g), dim3(256), 0, q, pdl, map, s0, s1, poff, m_, in0,
-             out0, in1, parts, done, ctl, goff1, u, fv);
+    if (wf.slice) {
+      const int g = one_wave((const void*)k_spmv1_img<B, true>, nparts);
+      launch_k(k_spmv1_img<B, true>, dim3(g), dim3(256), 0, q, pdl, map, s0, s1, poff, m_, in0,
+               out0, in1, parts, done, ctl, goff1, u, fv, wf);
+    } else {
+      const int g = one_wave((const void*)k_spmv1_img<B, false>, nparts);
+      launch_k(k_spmv1_img<B, false>, dim3(g), dim3(256), 0, q, pdl, map, s0, s1, poff, m_, in0,
+               out0, in1, parts, done, ctl, goff1, u, fv, wf);
+    }
   } else {   // s-update + colour-1 s^: in0 = r, in1 = v, out0 = s, out1 = s^, u = F(r)
     launch_k(k_s_update_img<B>, dim3(nparts), dim3(256), 0, q, pdl, mlen, st, in0, in1, out0,
              parts, ctl, map, s0, s1, dt, u, (const double*)fv, out1);
@@ -685,12 +701,12 @@ int launch_simg(int b, int stage, int nparts, SliceMap map, int s0, int s1, int 
                 const double* dt, const double* in0, const double* in1, double* out0,
                 double* out1, double* parts, const int* done, Ctl ctl, int goff1,
                 const double* u, double* fv, long long mlen, const State* st, cudaStream_t q,
-                bool pdl) {
+                bool pdl, WellFix wf) {
   switch (b) {
-    case 1: return launch_simg_b<1>(stage, nparts, map, s0, s1, poff, m_, dt, in0, in1, out0, out1, parts, done, ctl, goff1, u, fv, mlen, st, q, pdl);
-    case 2: return launch_simg_b<2>(stage, nparts, map, s0, s1, poff, m_, dt, in0, in1, out0, out1, parts, done, ctl, goff1, u, fv, mlen, st, q, pdl);
-    case 3: return launch_simg_b<3>(stage, nparts, map, s0, s1, poff, m_, dt, in0, in1, out0, out1, parts, done, ctl, goff1, u, fv, mlen, st, q, pdl);
-    case 4: return launch_simg_b<4>(stage, nparts, map, s0, s1, poff, m_, dt, in0, in1, out0, out1, parts, done, ctl, goff1, u, fv, mlen, st, q, pdl);
+    case 1: return launch_simg_b<1>(stage, nparts, map, s0, s1, poff, m_, dt, in0, in1, out0, out1, parts, done, ctl, goff1, u, fv, mlen, st, q, pdl, wf);
+    case 2: return launch_simg_b<2>(stage, nparts, map, s0, s1, poff, m_, dt, in0, in1, out0, out1, parts, done, ctl, goff1, u, fv, mlen, st, q, pdl, wf);
+    case 3: return launch_simg_b<3>(stage, nparts, map, s0, s1, poff, m_, dt, in0, in1, out0, out1, parts, done, ctl, goff1, u, fv, mlen, st, q, pdl, wf);
+    case 4: return launch_simg_b<4>(stage, nparts, map, s0, s1, poff, m_, dt, in0, in1, out0, out1, parts, done, ctl, goff1, u, fv, mlen, st, q, pdl, wf);
     default: return B2S_UNSUPPORTED;
   }
 }

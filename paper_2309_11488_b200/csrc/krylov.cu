@@ -55,7 +55,7 @@ int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, doub
                       const int* done, cudaStream_t st);
 int launch_wells_patch(const b2s_wells* w, int goff1, const double* corr, double* v,
                        const double* wv, int mode, double* p0, double* p1, const int* done,
-                       cudaStream_t st);
+                       cudaStream_t st, SImgPatch sp = SImgPatch{});
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
                     double* p1, const int* done, int* grid_out, cudaStream_t st,
@@ -65,7 +65,7 @@ int launch_simg(int b, int stage, int nparts, SliceMap map, int s0, int s1, int 
                 const double* dt, const double* in0, const double* in1, double* out0,
                 double* out1, double* parts, const int* done, Ctl ctl, int goff1,
                 const double* u, double* fv, long long mlen, const State* st, cudaStream_t q,
-                bool pdl);
+                bool pdl, WellFix wf = WellFix{});
 int launch_fwd_pre(int b, int nparts, SliceMap map, int s0, int s1, Sell lo, const double* dt,
                    double* z, const int* done, int* grid_out, cudaStream_t st, bool pdl, int pre,
                    const PreIn* pre_in);
@@ -656,7 +656,7 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   // same blocks anyway (F(r) in y's colour-1 rows, u = inv(A_kk) v and F(v)
   // in t, which is dead until the s-phase); B2S_SIMG=0 turns it off
   const char* si_env = getenv("B2S_SIMG");
-  const bool simg = fused && !vecf && xdefer && !mesh && !wells && !(si_env && si_env[0] == '0');
+  const bool simg = fused && !vecf && xdefer && !mesh && !(si_env && si_env[0] == '0');
   MeshDev md{};
   MeshHalo mh{};
   if (mesh && !ilu) return B2S_UNSUPPORTED;   // sharded solves are block-Jacobi ILU0
@@ -884,9 +884,16 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
         int g0 = np;
         launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
                         done, &g0, cs, pdl, kPreNone, nullptr, t);
+        if (wells) {   // p^ complete: the well terms; colour-0 rows of v (and u) patched
+          well_terms(phat, done, cs);
+          launch_wells_patch(a->wells, a->goff1, a->well_corr, v, rhat, 1, pg + g0, nullptr, done,
+                             cs, SImgPatch{t, map.row0, map.nslices, a->dinv_tiles});
+          kernels += 3;
+          ++g0;
+        }
         launch_simg(a->b, 1, np, map, s1c, map.nslices, g0, A, nullptr, phat, rhat, v, nullptr, pg,
                     done, Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, a->goff1, t, t, m,
-                    state, cs, pdl);
+                    state, cs, pdl && !wells, wf);
         kernels += 3;
       } else if (fused) {
         launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, p, y,

@@ -34,6 +34,15 @@ struct WellFix {
   const double* corr;
 };
 
+// s-image with separately applied wells (fused.cu): the wells patch of
+// v's colour-0 rows recomputes u = inv(A_ii) v at the patched rows
+struct SImgPatch {
+  double* u;              // nullptr: no s-image
+  const int32_t* row0;    // slice map (group-aligned, row0 ascending)
+  int nslices;
+  const double* dtiles;   // inverse diagonal tiles by slice
+};
+
 // SpMV epilogues: 0 y = A x; 1 + partials w.y; 2 + partials y.y and y.w;
 // 3 y = w - A x (residual) + partials y.y
 enum SpmvMode { kPlain = 0, kDotW = 1, kSelfAndW = 2, kResidual = 3 };

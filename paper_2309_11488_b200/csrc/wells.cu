@@ -13,6 +13,7 @@
 //      multi-segment ones, as WellSet.apply_contributions does), so a cell
 //      shared by several wells sees the reference's subtraction order.
 #include "common.cuh"
+#include "sell.cuh"
 
 namespace b2s {
 
@@ -168,20 +169,37 @@ int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, doub
 __global__ void k_wells_patch(const int32_t* __restrict__ cells, int ncells, int nb, int goff1,
                               const double* __restrict__ corr, double* v,
                               const double* __restrict__ w, int mode, double* p0, double* p1,
-                              const int* done) {
+                              const int* done, SImgPatch sp) {
   __shared__ double red[8];
   if (done && *done) return;
   double a0 = 0.0, a1 = 0.0;
   for (int q = threadIdx.x; q < ncells; q += blockDim.x) {
     const long long row = cells[q];
     if (row >= goff1) continue;
+    double vr[4];
     for (int c = 0; c < nb; ++c) {
       const double vo = v[row * nb + c];
       const double vn = vo - corr[(long long)q * nb + c];
       v[row * nb + c] = vn;
+      vr[c] = vn;
       const double wv = w[row * nb + c];
       if (mode == 1) a0 += wv * vn - wv * vo;
       else { a0 += vn * vn - vo * vo; a1 += wv * vn - wv * vo; }
+    }
+    if (sp.u) {   // s-image: u_i = inv(A_ii) v_i again for the patched row
+      int lo = 0, hi = sp.nslices - 1;   // the slice holding the row (row0 ascending)
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sp.row0[mid] <= row) lo = mid; else hi = mid - 1;
+      }
+      const long long lane = row - sp.row0[lo];
+      const int bb = nb * nb;
+      for (int e = 0; e < nb; ++e) {
+        double acc = 0.0;
+        for (int c = 0; c < nb; ++c)
+          acc = fma(sp.dtiles[((long long)lo * bb + e * nb + c) * 32 + lane], vr[c], acc);
+        sp.u[row * nb + e] = acc;
+      }
     }
   }
   const double t0 = block_sum(a0, red);
@@ -194,9 +212,9 @@ __global__ void k_wells_patch(const int32_t* __restrict__ cells, int ncells, int
 
 int launch_wells_patch(const b2s_wells* w, int goff1, const double* corr, double* v,
                        const double* wv, int mode, double* p0, double* p1, const int* done,
-                       cudaStream_t st) {
+                       cudaStream_t st, SImgPatch sp) {
   k_wells_patch<<<1, 256, 0, st>>>(w->cells, w->ncells, w->nb, goff1, corr, v, wv, mode, p0, p1,
-                                   done);
+                                   done, sp);
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 

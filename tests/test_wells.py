@@ -112,13 +112,16 @@ def test_wells_in_device_loop_match_host_loop(name, backend):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("vec", ["1", "0"])
-def test_wells_with_fused_colour_passes(monkeypatch, vec):
+@pytest.mark.parametrize("vec,simg", [("1", "1"), ("0", "1"), ("0", "0")])
+def test_wells_with_fused_colour_passes(monkeypatch, vec, simg):
     """2-colour plans keep the fused colour passes with separate wells: the
     colour-0 rows of v / t get their well terms after p^ / s^ is complete
-    (k_wells_patch, partials corrected); same answer as the unfused loop."""
+    (k_wells_patch, partials corrected; under the s-image it also recomputes
+    u = inv(A_ii) v at the patched rows and the colour-1 SpMV subtracts the
+    terms before forming F(v)); same answer as the unfused loop."""
     from paper_2309_11488_b200.krylov import DeviceKrylov
     monkeypatch.setenv("B2S_FUSE_VEC", vec)
+    monkeypatch.setenv("B2S_SIMG", simg)
     g = P.generate(P.GeneratorSpec(14, 12, 10, well_count=4, well_depth=6, seed=21))
     fact = P.decompose(g.a, P.graph_color(g.a.pattern))
     op = P.WellAugmentedOperator(g.a, g.wells)
