@@ -52,10 +52,10 @@ int launch_spmv_range(int b, int mode, int nparts, SliceMap map, int s0, int s1,
                       const int* done, Ctl ctl, cudaStream_t st, bool pdl = false,
                       WellFix wf = WellFix{});
 int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, double* corr,
-                      const int* done, cudaStream_t st);
+                      const int* done, cudaStream_t st, bool pdl = false);
 int launch_wells_patch(const b2s_wells* w, int goff1, const double* corr, double* v,
                        const double* wv, int mode, double* p0, double* p1, const int* done,
-                       cudaStream_t st, SImgPatch sp = SImgPatch{});
+                       cudaStream_t st, SImgPatch sp = SImgPatch{}, bool pdl = false);
 int launch_bwd_spmv(int b, int mode, int nparts, SliceMap map, int s1, Sell a, const double* dt,
                     const double* yin, double* z, double* v, const double* w, double* p0,
                     double* p1, const int* done, int* grid_out, cudaStream_t st,
@@ -630,8 +630,8 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
   if (wells && (mesh || !a->well_slice || !a->well_lane || !a->well_corr || !a->well_scratch))
     return mesh ? B2S_UNSUPPORTED : B2S_SHAPE;
   const WellFix wf = wells ? WellFix{a->well_slice, a->well_lane, a->well_corr} : WellFix{};
-  auto well_terms = [&](const double* xin, const int* dn, cudaStream_t q) {
-    return wells ? launch_wells_corr(a->wells, xin, a->well_scratch, a->well_corr, dn, q) : 0;
+  auto well_terms = [&](const double* xin, const int* dn, cudaStream_t q, bool pd = false) {
+    return wells ? launch_wells_corr(a->wells, xin, a->well_scratch, a->well_corr, dn, q, pd) : 0;
   };
   const bool fused = phased && a->ngroups == 2 && a->fuse && (!mesh || mesh_local);
   // fused vector passes on top of the fused colour passes: 7 kernels per
@@ -831,13 +831,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       const Ctl ca{state, counters + 0, dev_done, kCtlAlpha, md};
       if (mesh) fork_halo(1, phat);
       if (wells) {
-        well_terms(phat, done, cs);
-        launch_wells_patch(a->wells, a->goff1, a->well_corr, v, rhat, 1, pg + g0, nullptr, done, cs);
+        well_terms(phat, done, cs, pdl);
+        launch_wells_patch(a->wells, a->goff1, a->well_corr, v, rhat, 1, pg + g0, nullptr, done, cs, SImgPatch{}, pdl);
         kernels += 3;
         ++g0;
       }
       launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
-                        done, mesh ? Ctl{} : ca, cs, pdl && !wells, wf);
+                        done, mesh ? Ctl{} : ca, cs, pdl, wf);
       kernels += 3;
       if (mesh) {
         join_halo(1, phat);
@@ -854,13 +854,13 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       const Ctl co{state, counters + 2, dev_done, kCtlOmegaS, md, pss, gF + g0};
       if (mesh) fork_halo(2, shat);
       if (wells) {
-        well_terms(shat, done, cs);
-        launch_wells_patch(a->wells, a->goff1, a->well_corr, t, s, 2, ptt + g0, pts + g0, done, cs);
+        well_terms(shat, done, cs, pdl);
+        launch_wells_patch(a->wells, a->goff1, a->well_corr, t, s, 2, ptt + g0, pts + g0, done, cs, SImgPatch{}, pdl);
         kernels += 3;
         ++g0;
       }
       launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
-                        mesh ? Ctl{} : co, cs, pdl && !wells, wf);
+                        mesh ? Ctl{} : co, cs, pdl, wf);
       kernels += 3;
       if (mesh) {
         join_halo(2, shat);
@@ -885,15 +885,15 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
         launch_bwd_spmv(a->b, 1, np, map, s1c, A, a->dinv_tiles, p, phat, v, rhat, pg, nullptr,
                         done, &g0, cs, pdl, kPreNone, nullptr, t);
         if (wells) {   // p^ complete: the well terms; colour-0 rows of v (and u) patched
-          well_terms(phat, done, cs);
+          well_terms(phat, done, cs, pdl);
           launch_wells_patch(a->wells, a->goff1, a->well_corr, v, rhat, 1, pg + g0, nullptr, done,
-                             cs, SImgPatch{t, map.row0, map.nslices, a->dinv_tiles});
+                             cs, SImgPatch{t, map.row0, map.nslices, a->dinv_tiles}, pdl);
           kernels += 3;
           ++g0;
         }
         launch_simg(a->b, 1, np, map, s1c, map.nslices, g0, A, nullptr, phat, rhat, v, nullptr, pg,
                     done, Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, a->goff1, t, t, m,
-                    state, cs, pdl && !wells, wf);
+                    state, cs, pdl, wf);
         kernels += 3;
       } else if (fused) {
         launch_phased(a->b, a->kc, 2, a->gslice_host, a->goff1, map, L, U, a->dinv_tiles, p, y,
@@ -907,14 +907,14 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
         // reads only local columns), and joins before the ghost correction
         if (mesh) fork_halo(1, phat);
         if (wells) {   // p^ complete: the well terms, colour-0 rows patched
-          well_terms(phat, done, cs);
+          well_terms(phat, done, cs, pdl);
           launch_wells_patch(a->wells, a->goff1, a->well_corr, v, rhat, 1, pg + g0, nullptr, done,
-                             cs);
+                             cs, SImgPatch{}, pdl);
           kernels += 3;
           ++g0;
         }
         launch_spmv_range(a->b, 1, np, map, s1c, map.nslices, g0, A, phat, v, rhat, pg, nullptr,
-                          done, mesh ? Ctl{} : ca, cs, pdl && !wells, wf);
+                          done, mesh ? Ctl{} : ca, cs, pdl, wf);
         kernels += 3;
         if (mesh) {   // the boundary rows' ghost couplings + alpha
           join_halo(1, phat);
@@ -936,9 +936,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       }
       if (mesh && !fused) { halo(cs, 1, ph, done); kernels += mh.nghost > 0 ? 3 : 2; }
       if (!fused) {
-        if (wells) { well_terms(ph, done, cs); kernels += 2; }
+        if (wells) { well_terms(ph, done, cs, pdl); kernels += 2; }
         launch_spmv(a->b, 1, np, map, A, ph, v, rhat, pg, nullptr, done,
-                    Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl && !wells, wf);
+                    Ctl{state, counters + 0, dev_done, kCtlAlpha, md}, cs, pdl, wf);
         ++kernels;
       }
       if (simg)   // s, |s|^2, the half-step test, and colour 1's s^ from the images
@@ -962,14 +962,14 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
         const Ctl co{state, counters + 2, dev_done, kCtlOmega, md};
         if (mesh) fork_halo(2, shat);
         if (wells) {
-          well_terms(shat, done, cs);
+          well_terms(shat, done, cs, pdl);
           launch_wells_patch(a->wells, a->goff1, a->well_corr, t, s, 2, ptt + g0, pts + g0, done,
-                             cs);
+                             cs, SImgPatch{}, pdl);
           kernels += 3;
           ++g0;
         }
         launch_spmv_range(a->b, 2, np, map, s1c, map.nslices, g0, A, shat, t, s, ptt, pts, done,
-                          mesh ? Ctl{} : co, cs, pdl && !wells, wf);
+                          mesh ? Ctl{} : co, cs, pdl, wf);
         kernels += 3;
         if (mesh) {
           join_halo(2, shat);
@@ -991,9 +991,9 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
       }
       if (mesh && !fused) { halo(cs, 2, sh, done); kernels += mh.nghost > 0 ? 3 : 2; }
       if (!fused) {
-        if (wells) { well_terms(sh, done, cs); kernels += 2; }
+        if (wells) { well_terms(sh, done, cs, pdl); kernels += 2; }
         launch_spmv(a->b, 2, np, map, A, sh, t, s, ptt, pts, done,
-                    Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl && !wells, wf);
+                    Ctl{state, counters + 2, dev_done, kCtlOmega, md}, cs, pdl, wf);
         ++kernels;
       }
       launch_k(xdefer ? k_r_update<true> : k_r_update<false>, dim3(grid_v), dim3(256), 0, cs, pdl,

@@ -45,6 +45,8 @@ struct WellsDev {
 // pass 1: t2 of well w (one warp)
 __global__ void k_wells_t2(WellsDev W, const double* __restrict__ x, double* __restrict__ t2,
                            const int* done) {
+  griddep_wait();   // programmatic launch inside the Krylov graph
+  griddep_launch();
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -124,6 +126,8 @@ __global__ void k_wells_apply(WellsDev W, const double* __restrict__ t2, double*
 // well order; the SpMV epilogue subtracts it (sell.cuh WellFix)
 __global__ void k_wells_corr(WellsDev W, const double* __restrict__ t2, double* __restrict__ corr,
                              const int* done) {
+  griddep_wait();   // programmatic launch inside the Krylov graph
+  griddep_launch();
   if (done && *done) return;
   const int N = W.nb;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < W.ncells; q += gridDim.x * blockDim.x) {
@@ -150,13 +154,14 @@ static WellsDev wells_dev(const b2s_wells* w) {
 }
 
 int launch_wells_corr(const b2s_wells* w, const double* x, double* scratch, double* corr,
-                      const int* done, cudaStream_t st) {
+                      const int* done, cudaStream_t st, bool pdl) {
   if (!w || w->nwells < 0 || w->nb < 1 || w->nb > 4) return B2S_SHAPE;
   if (w->nwells == 0) return B2S_OK;
   const WellsDev W = wells_dev(w);
-  k_wells_t2<<<(w->nwells + 7) / 8, 256, 0, st>>>(W, x, scratch, done);
+  launch_k(k_wells_t2, dim3((w->nwells + 7) / 8), dim3(256), 0, st, pdl, W, x, scratch, done);
   const int g = (w->ncells + 255) / 256;
-  k_wells_corr<<<g < 1 ? 1 : g, 256, 0, st>>>(W, scratch, corr, done);
+  launch_k(k_wells_corr, dim3(g < 1 ? 1 : g), dim3(256), 0, st, pdl, W, (const double*)scratch,
+           corr, done);
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
@@ -171,6 +176,8 @@ __global__ void k_wells_patch(const int32_t* __restrict__ cells, int ncells, int
                               const double* __restrict__ w, int mode, double* p0, double* p1,
                               const int* done, SImgPatch sp) {
   __shared__ double red[8];
+  griddep_wait();   // programmatic launch inside the Krylov graph
+  griddep_launch();
   if (done && *done) return;
   double a0 = 0.0, a1 = 0.0;
   for (int q = threadIdx.x; q < ncells; q += blockDim.x) {
@@ -212,9 +219,9 @@ __global__ void k_wells_patch(const int32_t* __restrict__ cells, int ncells, int
 
 int launch_wells_patch(const b2s_wells* w, int goff1, const double* corr, double* v,
                        const double* wv, int mode, double* p0, double* p1, const int* done,
-                       cudaStream_t st, SImgPatch sp) {
-  k_wells_patch<<<1, 256, 0, st>>>(w->cells, w->ncells, w->nb, goff1, corr, v, wv, mode, p0, p1,
-                                   done, sp);
+                       cudaStream_t st, SImgPatch sp, bool pdl) {
+  launch_k(k_wells_patch, dim3(1), dim3(256), 0, st, pdl, (const int32_t*)w->cells, w->ncells,
+           w->nb, goff1, corr, v, wv, mode, p0, p1, done, sp);
   return cudaGetLastError() == cudaSuccess ? B2S_OK : B2S_CUDA_ERROR;
 }
 
