@@ -53,6 +53,58 @@ __global__ void k_wells_t2(WellsDev W, const double* __restrict__ x, double* __r
   if (w >= W.nwells) return;
   const int M = W.M[w], S = W.nseg[w] * M, N = W.nb;
   double* t = t2 + W.toff[w];
+  if (W.kind[w] == 0 && M <= 8) {
+    // standard well: lane j computes B_e x_cell of entry e = e0 + j (the
+    // loads of all perforations in flight at once, not one dependent chain
+    // per entry), then every lane sums the entries' vectors in entry order
+    // through shuffles -- the same additions in the same order as the
+    // sequential loop below, so t1 is bit-identical
+    const int e0 = W.bptr[w], e1 = W.bptr[w + 1];
+    double acc[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) acc[m] = 0.0;
+    for (int eb = e0; eb < e1; eb += 32) {
+      const int e = eb + lane;
+      double sv[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) sv[m] = 0.0;
+      if (e < e1) {
+        const double* blk = W.bvals + W.boff[e];
+        const double* xc = x + (long long)W.bcell[e] * N;
+        double xv[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) xv[c] = c < N ? xc[c] : 0.0;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          if (m < M) {
+            double sm = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (c < N) sm = fma(blk[m * N + c], xv[c], sm);
+            sv[m] = sm;
+          }
+        }
+      }
+      const int cnt = e1 - eb < 32 ? e1 - eb : 32;
+      for (int j = 0; j < cnt; ++j) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const double v = __shfl_sync(0xffffffffu, sv[m], j);
+          if (m < M) acc[m] += v;
+        }
+      }
+    }
+    // t2 = D^-1 t1 (one lane per row)
+    double r = 0.0;
+    const double* dinv = W.dvals + W.doff[w];
+    if (lane < M) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < M) r = fma(dinv[lane * M + c], acc[c], r);
+      t[lane] = r;
+    }
+    return;
+  }
   // t1: lane q owns entries q, q+32, ... of the nseg*M vector; entries of B
   // are visited in order, each adds its M-vector B_e x_cell
   for (int q = lane; q < S; q += 32) t[q] = 0.0;
