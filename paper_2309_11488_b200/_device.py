@@ -603,9 +603,10 @@ class SliceMap:
         if 2 <= ngroups <= PHASED_MAX_GROUPS:
             # host copy of the group -> slice table: the phased sweeps launch
             # one pass per group (the table is baked into the captured graph)
-            out.gslice_host = np.ascontiguousarray(base[: ngroups + 1].cpu().numpy(),
-                                                   dtype=np.int32)
-            out.goff1 = int(offsets[1].item())
+            # (one readback for the table and the first group's size)
+            both = torch.cat([base[: ngroups + 1], offsets[1:2].to(torch.int32)]).cpu().numpy()
+            out.gslice_host = np.ascontiguousarray(both[: ngroups + 1], dtype=np.int32)
+            out.goff1 = int(both[ngroups + 1])
         return out
 
     @classmethod
