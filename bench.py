@@ -26,6 +26,7 @@ concurrently).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -467,6 +468,10 @@ def run_single(args):
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
+        # no cyclic-GC pass inside the timed region (a pass over the host
+        # heap stalls the thread that feeds the device loop for milliseconds)
+        gc.collect()
+        gc.disable()
         if clocks:
             clocks.start()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -481,9 +486,12 @@ def run_single(args):
             evs.append(ev)
         t1.record(st)
         torch.cuda.synchronize()
+        gc.enable()
         if clocks:
             out["clocks"] = clocks.stop()
         ms = t0.elapsed_time(t1) / steps
+        per = [e[0].elapsed_time(e[2]) for e in evs]
+        out["step_ms_min_max"] = [min(per), max(per)]
         out.update({
             "solve_ms": ms, "iterations": sum(its) / len(its),
             "setup_ms": sum(e[0].elapsed_time(e[1]) for e in evs) / steps,

@@ -813,7 +813,12 @@ int b2s_bicgstab(const b2s_bicg_args* a, b2s_bicg_result* res) {
     const char* pdl_env = getenv("B2S_PDL");
     // (shards sharing one GPU: a programmatically launched kernel would hold
     // SMs while its predecessor's last CTA waits for another shard)
-    const bool pdl = !(pdl_env && pdl_env[0] == '0') && !(mesh && mesh->shared_device);
+    // (wavefront loops: no programmatic launches at all.  Their sweep tiles
+    // spin on each other, and with any kernel of the loop launched
+    // programmatically some C4 level steps stalled to 20-40 ms against 14.0:
+    // bench means 15.3-16.1 ms vs 13.95-14.06 with PDL off; plain launches of
+    // the sweeps alone did not cure it; profiles/r02/level_pdl.txt)
+    const bool pdl = !(pdl_env && pdl_env[0] == '0') && !(mesh && mesh->shared_device) && !a->gw;
     double* ph = ilu ? phat : p;
     double* sh = ilu ? shat : s;
     const int reset_y = a->refill_y ? 0 : 1;
